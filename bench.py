@@ -1,0 +1,478 @@
+#!/usr/bin/env python
+"""bench.py — ModeT hot-path benchmark (B200, sm_100a).
+
+Workload (BASELINE.json north_star unit): the finest pyramid level L1 of the
+small preset at 160x192x224 — ModeT operator forward + backward (S=1 head,
+d=6) plus the trilinear feature warp forward + backward (C=8 channels).
+One "step" = modet_fwd + modet_bwd + warp_fwd + warp_bwd over one volume whose
+synthetic inputs (seeded, the reference bench's distributions) are already
+resident in HBM.  The step footprint (~1.4 GB) is far larger than L2
+(126 MB), so no explicit flush is needed between steps.
+
+Metric: Gvoxel/s of that step (voxels processed / second, whole job).  With
+N ranks (torchrun, one GPU each) every rank processes its own independent
+volume (pair-parallel, no data-path collective): weak scaling.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every key.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DIMS = (160, 192, 224)  # h, w, l  (x, y, z)
+S, HD, NB, CH = 1, 6, 3, 8
+METRIC = "ModeT op fwd+bwd + feature warp fwd+bwd throughput at 160x192x224 (L1, S=1, d=6, C=8)"
+UNIT = "Gvoxel/s"
+
+# SURVEY.md §8(d) algorithmic bytes per voxel (fp32, each tensor once per
+# direction, W never materialised)
+BYTES = {
+    "modet_fwd": 4 * (2 * S * HD + 3 * S),
+    "modet_bwd": 4 * (4 * S * HD + 3 * S),
+    "warp_fwd": 4 * (3 + 2 * CH),
+    "warp_bwd": 4 * (6 + 3 * CH),
+}
+KERNEL_NAMES = {  # op -> the dominant CUDA kernel it launches
+    "modet_fwd": "modet_fwd_k",
+    "modet_bwd": "modet_bwd_k",
+    "warp_fwd": "warp_fwd_k",
+    "warp_bwd": "warp_bwd_k",
+}
+
+
+def load_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_ncu_traffic():
+    """dram bytes per launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------ clock sampler
+class ClockSampler:
+    """Polls NVML while the timed region runs (SM clock, max clock, reasons)."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        reasons = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ our arm
+def make_inputs(rank: int):
+    """Seeded synthetic inputs (bench.cpp:28-35 distributions): Q, K ~ U(-1,1),
+    B ~ U(-0.5,0.5); upstream gSF ~ U(-1,1); features ~ N(0,1); a smooth-ish
+    displacement field of up to ~2 voxels; warp upstream gradient ~ N(0,1).
+    Rank r uses seeds offset by r (independent pairs)."""
+    import torch
+
+    from paper_2403_16526_b200 import ops
+
+    h, w, l = DIMS
+    n = h * w * l
+    base = 1000 * rank
+    r = ops.Rng(5 + base)
+    Q = r.uniform((n, S * HD), -1.0, 1.0)
+    K = r.uniform((n, S * HD), -1.0, 1.0)
+    B = r.uniform((S, 27), -0.5, 0.5)
+    gSF = ops.Rng(6 + base).uniform((3 * S, n), -1.0, 1.0)
+    feat = ops.Rng(7 + base).normal((CH, l, w, h))
+    # smooth displacement: low-frequency sinusoids, amplitude 2 voxels
+    zz, yy, xx = torch.meshgrid(torch.arange(l, dtype=torch.float32),
+                                torch.arange(w, dtype=torch.float32),
+                                torch.arange(h, dtype=torch.float32), indexing="ij")
+    ph = ops.Rng(8 + base).uniform((9,), 0.0, 6.28).tolist()
+    field = torch.stack([
+        2.0 * torch.sin(xx / 23.0 + ph[0]) * torch.cos(yy / 29.0 + ph[1]) * torch.sin(zz / 31.0 + ph[2]),
+        2.0 * torch.cos(xx / 27.0 + ph[3]) * torch.sin(yy / 19.0 + ph[4]) * torch.cos(zz / 25.0 + ph[5]),
+        2.0 * torch.sin(xx / 21.0 + ph[6]) * torch.sin(yy / 33.0 + ph[7]) * torch.cos(zz / 17.0 + ph[8]),
+    ]).contiguous()
+    gout = ops.Rng(9 + base).normal((CH, l, w, h))
+    return dict(Q=Q, K=K, B=B, gSF=gSF, feat=feat, field=field, gout=gout)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_16526_b200 import _capi, ops
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    L = _capi.lib()
+    assert L.mdg_device_ok() == 1, "libmdg needs an sm_100a device"
+
+    h, w, l = DIMS
+    n = h * w * l
+    cfg = ops.AttentionConfig(S, HD, NB)
+    host_in = make_inputs(rank)
+    d_in = {k: v.to(dev) for k, v in host_in.items()}
+    Q, K, B, gSF = d_in["Q"], d_in["K"], d_in["B"], d_in["gSF"]
+    feat, field, gout = d_in["feat"], d_in["field"], d_in["gout"]
+    SF = torch.empty(3 * S, n, device=dev)
+    LSE = torch.empty(S, n, device=dev)
+    gQ, gK, gB = torch.zeros_like(Q), torch.zeros_like(K), torch.zeros_like(B)
+    warped = torch.empty_like(feat)
+    gin, gfield = torch.zeros_like(feat), torch.zeros_like(field)
+    d3 = ops.dims3(DIMS)
+    st = torch.cuda.current_stream()
+    sp = st.cuda_stream
+
+    def chk(rc):
+        if rc != 0:
+            raise RuntimeError(L.mdg_last_error().decode())
+
+    ops_order = ["modet_fwd", "modet_bwd", "warp_fwd", "warp_bwd"]
+
+    def step(ev=None):
+        # forward outputs are overwritten; backward targets accumulate (the
+        # reference contract) — re-zeroing them is part of the real step
+        if ev: ev[0].record(st)
+        chk(L.mdg_modet_fwd(Q.data_ptr(), K.data_ptr(), B.data_ptr(), d3, S, HD, NB, 0,
+                            SF.data_ptr(), LSE.data_ptr(), None, sp))
+        if ev: ev[1].record(st)
+        chk(L.mdg_modet_bwd(Q.data_ptr(), K.data_ptr(), B.data_ptr(), SF.data_ptr(),
+                            LSE.data_ptr(), gSF.data_ptr(), d3, S, HD, NB, 0, gQ.data_ptr(),
+                            gK.data_ptr(), gB.data_ptr(), sp))
+        if ev: ev[2].record(st)
+        chk(L.mdg_warp_fwd(feat.data_ptr(), CH, d3, field.data_ptr(), warped.data_ptr(), sp))
+        if ev: ev[3].record(st)
+        chk(L.mdg_warp_bwd(feat.data_ptr(), CH, d3, field.data_ptr(), gout.data_ptr(),
+                           gin.data_ptr(), gfield.data_ptr(), sp))
+        if ev: ev[4].record(st)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    K_ = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K_)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.mdg_launch_count()
+    with ClockSampler(local) as clk:
+        t0.record(st)
+        for i in range(K_):
+            step(evs[i])
+        t1.record(st)
+        torch.cuda.synchronize()
+    launches = L.mdg_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / K_
+    per_op = {op: statistics.mean(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(K_))
+              for j, op in enumerate(ops_order)}
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * n / (ms_max * 1e-3) / 1e9
+
+    # ---------------- e2e: the reference-facing host-buffer C-ABI calls
+    e2e = None if args.no_e2e else run_e2e(args, L, host_in, world, dev)
+
+    peak, peak_kind = load_peak()
+    dom = max(per_op, key=lambda k: per_op[k])
+    achieved = BYTES[dom] * n / (per_op[dom] * 1e-3) / 1e9
+    traffic = load_ncu_traffic().get(KERNEL_NAMES[dom])
+    step_bytes = sum(BYTES.values()) * n
+    result = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+        "steps": K_, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Rng streams, bench.cpp distributions)",
+        "config": {"workload": "L1 160x192x224: ModeT fwd+bwd (S=1,d=6,nb=3) + warp fwd+bwd (C=8)",
+                   "dims": list(DIMS), "heads": S, "head_dim": HD, "channels": CH,
+                   "parallelism": f"pair-parallel x{world} (independent volume per GPU)",
+                   "l2": "inputs larger than L2 (step footprint ~1.4 GB), no flush"},
+        "per_op_ms": {k: round(v, 4) for k, v in per_op.items()},
+        "roofline": {"bound": "hbm", "kernel": KERNEL_NAMES[dom],
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_kind": peak_kind,
+                     "bytes_per_launch": BYTES[dom] * n},
+        "roofline_step": {"achieved": round(step_bytes / (ms_max * 1e-3) / 1e9, 1),
+                          "peak": peak, "unit": "GB/s",
+                          "frac": round(step_bytes / (ms_max * 1e-3) / 1e9 / peak, 4),
+                          "bytes_per_step": step_bytes},
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, L, host_in, world, dev):
+    """Same metric through the host-buffer drop-ins (mdg_*_host): pinned host
+    inputs in, host outputs back, copies inside the timed region."""
+    import torch
+
+    from paper_2403_16526_b200 import ops
+
+    h, w, l = DIMS
+    n = h * w * l
+    pin = {k: v.pin_memory() for k, v in host_in.items()}
+    outs = {
+        "SF": torch.empty(3 * S, n).pin_memory(), "LSE": torch.empty(S, n).pin_memory(),
+        "gQ": torch.zeros(n, S * HD).pin_memory(), "gK": torch.zeros(n, S * HD).pin_memory(),
+        "gB": torch.zeros(S, 27).pin_memory(), "warped": torch.empty(CH, l, w, h).pin_memory(),
+        "gin": torch.zeros(CH, l, w, h).pin_memory(), "gfield": torch.zeros(3, l, w, h).pin_memory(),
+    }
+    d3 = ops.dims3(DIMS)
+    p = lambda t: t.data_ptr()  # noqa: E731
+
+    def step():
+        rc = L.mdg_modet_fwd_host(p(pin["Q"]), p(pin["K"]), p(pin["B"]), d3, S, HD, NB, 0,
+                                  p(outs["SF"]), p(outs["LSE"]))
+        rc |= L.mdg_modet_bwd_host(p(pin["Q"]), p(pin["K"]), p(pin["B"]), p(outs["SF"]),
+                                   p(outs["LSE"]), p(pin["gSF"]), d3, S, HD, NB, 0,
+                                   p(outs["gQ"]), p(outs["gK"]), p(outs["gB"]))
+        rc |= L.mdg_warp_fwd_host(p(pin["feat"]), CH, d3, p(pin["field"]), p(outs["warped"]))
+        rc |= L.mdg_warp_bwd_host(p(pin["feat"]), CH, d3, p(pin["field"]), p(pin["gout"]),
+                                  p(outs["gin"]), p(outs["gfield"]))
+        if rc:
+            raise RuntimeError(L.mdg_last_error().decode())
+
+    step()
+    steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([dt], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    f4 = 4
+    h2d = (2 * n * S * HD + 27 * S) * f4 \
+        + (2 * n * S * HD + 27 * S + 4 * n * S + 3 * n * S + 2 * n * S * HD + 27 * S) * f4 \
+        + (CH * n + 3 * n) * f4 + (2 * CH * n + 3 * n + CH * n + 3 * n) * f4
+    d2h = (4 * n * S) * f4 + (2 * n * S * HD + 27 * S) * f4 + CH * n * f4 + (CH * n + 3 * n) * f4
+    return {"value": round(world * n / dt / 1e9, 5), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 3),
+            "api": "mdg_modet_fwd_host + mdg_modet_bwd_host + mdg_warp_fwd_host + "
+                   "mdg_warp_bwd_host (pinned host buffers)", "steps": steps}
+
+
+# ----------------------------------------------------- reference CPU arm
+REF_SLAB_Z = 8  # each worker's bounded sample: a 160x192x8 depth slab
+
+
+def _ref_worker_inputs(seed):
+    import pyoracle
+
+    h, w, _ = DIMS
+    dims = (h, w, REF_SLAB_Z)
+    n = h * w * REF_SLAB_Z
+    r = pyoracle.Rng(seed)
+    f = lambda a: np.ascontiguousarray(a, dtype=np.float32)  # noqa: E731
+    Q = f(r.uniform(n * S * HD, -1, 1).reshape(n, S * HD))
+    K = f(r.uniform(n * S * HD, -1, 1).reshape(n, S * HD))
+    B = f(r.uniform(S * 27, -0.5, 0.5).reshape(S, 27))
+    gSF = f(pyoracle.Rng(seed + 1).uniform(3 * S * n, -1, 1).reshape(3 * S, REF_SLAB_Z, w, h))
+    feat = f(pyoracle.Rng(seed + 2).normal(CH * n).reshape(CH, REF_SLAB_Z, w, h))
+    fld = f(pyoracle.Rng(seed + 3).uniform(3 * n, -2, 2).reshape(3, REF_SLAB_Z, w, h))
+    gout = f(pyoracle.Rng(seed + 4).normal(CH * n).reshape(CH, REF_SLAB_Z, w, h))
+    return dims, (Q, K, B, gSF, feat, fld, gout)
+
+
+def _ref_step(lib, dims, inp):
+    """The reference's own hot path (attention.hpp + sampling.hpp kernels as
+    op_na_fused / op_subfields / op_warp call them), one slab."""
+    Q, K, B, gSF, feat, fld, gout = inp
+    W, err = lib.na_fwd(Q, K, B, dims, S, HD, NB)
+    assert err is None
+    lib.subfields_fwd(W, dims, S, NB)
+    gW = lib.subfields_bwd(gSF, dims, S, NB)
+    lib.na_bwd(Q, K, W, gW, dims, S, HD, NB)
+    lib.warp_fwd(feat, fld)
+    lib.warp_bwd(feat, fld, gout)
+
+
+def _cpu_run(kind, threads, steps, warmup):
+    """Run `threads` workers in parallel (ctypes releases the GIL), each on
+    its own slab; returns (Gvoxel/s, seconds per step, voxels per step)."""
+    import pyoracle
+
+    if kind == "reference":
+        lib = pyoracle.ref()
+    else:
+        lib = pyoracle.mdo()
+    work = [_ref_worker_inputs(100 + 17 * i) for i in range(threads)]
+    nvox = sum(d[0] * d[1] * d[2] for d, _ in work)
+
+    def one_step():
+        ts = [threading.Thread(target=_ref_step, args=(lib, d, inp)) for d, inp in work]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+
+    for _ in range(warmup):
+        one_step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one_step()
+    dt = (time.perf_counter() - t0) / max(steps, 1)
+    return nvox / dt / 1e9, dt, nvox
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(seconds):
+    """Reference CPU path (oracle/_ref, compiled from the reference sources)
+    on the host cores, bounded to ~`seconds` of work."""
+    import pyoracle
+
+    kind = "reference" if pyoracle.ref_available() else "port"
+    threads = cpu_threads()
+    v, dt, nvox = _cpu_run(kind, threads, 1, 0)
+    steps = max(1, int(seconds / max(dt, 1e-3)) - 1)
+    if steps > 1:
+        v, dt, nvox = _cpu_run(kind, threads, steps, 0)
+    return {"value": round(v, 6), "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{threads} threads x one 160x192x{REF_SLAB_Z} slab each "
+                      f"({nvox} voxels/step), {steps} step(s) of {dt:.2f}s: "
+                      "na_fused_fwd+subfields_fwd+subfields_bwd+na_fused_bwd+warp_fwd+warp_bwd",
+            "ms_per_step": round(dt * 1e3, 1)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import pyoracle
+
+    kind = "reference" if pyoracle.ref_available() else "port"
+    threads = cpu_threads()
+    v, dt, nvox = _cpu_run(kind, threads, args.steps, args.warmup)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Rng streams)",
+        "config": {"workload": "L1 160x192x224: ModeT fwd+bwd (S=1,d=6,nb=3) + warp fwd+bwd (C=8)",
+                   "sample": f"per step: {threads} CPU threads, one 160x192x{REF_SLAB_Z} slab each"},
+        "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{threads} x 160x192x{REF_SLAB_Z} slabs ({nvox} voxels) per step"},
+        "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.impl == "reference":
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        run_reference(args)
+    else:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,203 @@
+/*
+ * mdg.h — C ABI of the B200-native ModeT hot path (sm_100a).
+ *
+ * Drop-in boundary for the mdreg reference (/root/reference/proj).  Two tiers:
+ *
+ *  1. Reference-shaped kernel tier ("mdg_na_*", "mdg_subfields_*", "mdg_warp_*",
+ *     "mdg_upsample2_*", "mdg_conv3_*", "mdg_compose_*"): one entry point per
+ *     `mdreg::kern::` function on the path, same argument meaning, same
+ *     layouts, same overwrite/accumulate rules.  Each cites the reference
+ *     function it replaces (paths relative to proj/include/mdreg/).
+ *  2. Fused tier ("mdg_modet_*"): the B200-native ModeT operator.  Q·K over
+ *     the nb^3 window -> softmax -> sum of offsets in one kernel; the nb^3
+ *     weight tensor W is never materialised (optional output for parity).
+ *     The backward recomputes W from (Q, K, B, LSE) and fuses dQ, dK (gather,
+ *     no atomics) and dB (deterministic two-stage reduction).
+ *
+ * Conventions (reference common.hpp:40-74, volume.hpp:26-94):
+ *  - dims {h, w, l} = extents along x, y, z; voxel p = (z*w + y)*h + x.
+ *  - Feature maps and fields are channel-major {C, n}; fields have C = 3
+ *    (x, y, z components, voxel units of their own grid).
+ *  - All values fp32; all sizes int32 (n = h*w*l < 2^31).
+ *  - Device-pointer entry points take a cudaStream_t as `void *stream`
+ *    (NULL = legacy default stream) and are stream-ordered: they return once
+ *    the work is enqueued.  `*_host` entry points take host pointers and are
+ *    synchronous, exactly like the reference's CPU functions.
+ *  - Forward entry points OVERWRITE their outputs.  Backward entry points
+ *    ACCUMULATE (+=) into their gradient outputs, as the reference does
+ *    (attention.hpp:153-161, sampling.hpp:153-164, ops.hpp:84-96); a NULL
+ *    gradient pointer skips that gradient.
+ *
+ * Errors: every entry point returns an mdg_status.  A C ABI cannot throw, so
+ * the reference's exceptions map to codes and a per-thread message:
+ *    invalid_input  -> MDG_EINVAL   (shape / config / range violations)
+ *    numeric_error  -> MDG_ENUMERIC (non-finite attention logit)
+ *    CUDA failures  -> MDG_ECUDA
+ * Non-finite logits are detected on the device; the first offending
+ * (x, y, z, head) in the reference's loop order (head-major, then z, y, x) is
+ * recorded.  The reference-shaped tier and the *_host calls check it before
+ * returning (they synchronise the stream), exactly reproducing the
+ * reference's throw; the fused tier defers the check to
+ * mdg_check_numeric(stream) so a pyramid step stays asynchronous.
+ */
+#ifndef MDG_H
+#define MDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MDG_OK = 0,
+    MDG_EINVAL = 1,
+    MDG_ENUMERIC = 2,
+    MDG_ECUDA = 3
+} mdg_status;
+
+/* Q/K layouts accepted by the fused tier. */
+typedef enum {
+    MDG_QK_POSMAJOR = 0, /* reference layout {n, S*d} (attention.hpp:77-78) */
+    MDG_QK_PLANAR = 1    /* native layout {S*d, n}: one coalesced plane per channel */
+} mdg_qk_layout;
+
+typedef struct {
+    int h, w, l;
+} mdg_dims3;
+
+/* ------------------------------------------------------------- diagnostics */
+const char *mdg_last_error(void);
+/* position of the last non-finite logit reported by MDG_ENUMERIC */
+void mdg_last_error_position(int *x, int *y, int *z, int *head);
+/* 1 if the library was built for and runs on an sm_100a device */
+int mdg_device_ok(void);
+const char *mdg_build_info(void);
+/* synchronise `stream` and return MDG_ENUMERIC if any fused-tier kernel on
+ * this device recorded a non-finite logit since the last check; the position
+ * is decoded against `d`, the dims of the attention call being checked */
+mdg_status mdg_check_numeric(mdg_dims3 d, void *stream);
+/* number of kernels this library launched since load (host-side counter) */
+int64_t mdg_launch_count(void);
+
+/* ---------------------------------------------------- index logic (exact) */
+/* attention.hpp:57-60 window_offset: slot o -> (dx, dy, dz), x fastest */
+mdg_status mdg_window_offset(int o, int nb, int off[3]);
+/* sampling.hpp:38-49 resolve_axis evaluated ON THE DEVICE for n coordinates
+ * (used to prove the integer corner logic is bit-exact) */
+mdg_status mdg_resolve_axis(const float *x, int n, int dim, int *i0, int *i1, float *f,
+                            int *live, void *stream);
+
+/* ====================== reference-shaped kernel tier ====================== */
+
+/* attention.hpp:83-123 kern::na_fused_fwd.  Q, K {n, S*hd} position-major;
+ * B {S, nb^3}; W {S, n, nb^3} (overwritten). */
+mdg_status mdg_na_fused_fwd(const float *Q, const float *K, const float *B, mdg_dims3 d,
+                            int S, int hd, int nb, float *W, void *stream);
+/* attention.hpp:127-166 kern::na_fused_bwd (accumulates gQ, gK, gB) */
+mdg_status mdg_na_fused_bwd(const float *Q, const float *K, const float *W, mdg_dims3 d,
+                            int S, int hd, int nb, const float *gW, float *gQ, float *gK,
+                            float *gB, void *stream);
+/* attention.hpp:282-298 kern::subfields_fwd: W {S,n,nb^3} -> out {3S, n} */
+mdg_status mdg_subfields_fwd(const float *W, mdg_dims3 d, int S, int nb, float *out,
+                             void *stream);
+/* attention.hpp:301-316 kern::subfields_bwd (accumulates gW) */
+mdg_status mdg_subfields_bwd(mdg_dims3 d, int S, int nb, const float *gout, float *gW,
+                             void *stream);
+/* attention.hpp:421-427 (op_subfields row check): MDG_EINVAL if some row of W
+ * does not sum to 1 within tol */
+mdg_status mdg_subfields_check_rows(const float *W, mdg_dims3 d, int S, int nb, float tol,
+                                    void *stream);
+
+/* sampling.hpp:123-135 kern::warp_fwd: out_c(x) = in_c(x + field(x)) */
+mdg_status mdg_warp_fwd(const float *in, int C, mdg_dims3 d, const float *field, float *out,
+                        void *stream);
+/* sampling.hpp:139-167 kern::warp_bwd (accumulates; gin/gfield nullable) */
+mdg_status mdg_warp_bwd(const float *in, int C, mdg_dims3 d, const float *field,
+                        const float *gout, float *gin, float *gfield, void *stream);
+/* sampling.hpp:225-242 kern::upsample2_fwd (target range checked as in
+ * sampling.hpp:266-271 -> MDG_EINVAL) */
+mdg_status mdg_upsample2_fwd(const float *in, int C, mdg_dims3 d, mdg_dims3 td, float scale,
+                             float *out, void *stream);
+/* sampling.hpp:245-262 kern::upsample2_bwd (accumulates gin) */
+mdg_status mdg_upsample2_bwd(int C, mdg_dims3 d, mdg_dims3 td, float scale, const float *gout,
+                             float *gin, void *stream);
+/* ops.hpp:58-74 kern::conv3_fwd (zero-padded 3x3x3 correlation, kernel
+ * [oc][ic][dz][dy][dx]; bias nullable).  RegHead fusion (reghead.hpp:42-47)
+ * is this with ic = 3S, oc = 3. */
+mdg_status mdg_conv3_fwd(const float *in, int ic, mdg_dims3 d, const float *k,
+                         const float *bias, int oc, float *out, void *stream);
+/* ops.hpp:77-99 kern::conv3_bwd (accumulates; gin/gk/gbias nullable) */
+mdg_status mdg_conv3_bwd(const float *in, int ic, mdg_dims3 d, const float *k, int oc,
+                         const float *gout, float *gin, float *gk, float *gbias, void *stream);
+/* field_ops.hpp:42-49 / ops.hpp:295-298: out = res + warp(prev, res) */
+mdg_status mdg_compose_fwd(const float *prev, const float *res, mdg_dims3 d, float *out,
+                           void *stream);
+/* backward of op_compose (accumulates gprev, gres; nullable) */
+mdg_status mdg_compose_bwd(const float *prev, const float *res, mdg_dims3 d,
+                           const float *gout, float *gprev, float *gres, void *stream);
+/* reghead.hpp:52-67 scaling and squaring: out = (v/2^T) composed T times.
+ * `saved` (nullable, (steps+1)*3n floats) receives the intermediate fields
+ * phi_0 .. phi_T that mdg_scaling_squaring_bwd needs. */
+mdg_status mdg_scaling_squaring_fwd(const float *vel, mdg_dims3 d, int steps, float *out,
+                                    float *saved, void *stream);
+/* backward of op_scaling_squaring given `saved` from the forward
+ * (accumulates gvel) */
+mdg_status mdg_scaling_squaring_bwd(const float *saved, mdg_dims3 d, int steps,
+                                    const float *gout, float *gvel, void *stream);
+
+/* ============================== fused tier ============================== */
+
+/* ModeT forward.  Q, K in `layout`; B {S, nb^3}.  Outputs:
+ *   SF  {3S, n} sub-flows (what kern::subfields_fwd(na_fused_fwd(..)) gives)
+ *   LSE {S, n}  per-row log-sum-exp, saved for the backward
+ *   W   {S, n, nb^3} nullable — materialised only for parity checks. */
+mdg_status mdg_modet_fwd(const float *Q, const float *K, const float *B, mdg_dims3 d, int S,
+                         int hd, int nb, int layout, float *SF, float *LSE, float *W,
+                         void *stream);
+/* ModeT backward.  Given the forward's SF and LSE and the upstream gradient
+ * gSF {3S, n}, accumulates gQ, gK (same layout as Q, K) and gB {S, nb^3}.
+ * Equivalent to subfields_bwd + na_fused_bwd of the reference. */
+mdg_status mdg_modet_bwd(const float *Q, const float *K, const float *B, const float *SF,
+                         const float *LSE, const float *gSF, mdg_dims3 d, int S, int hd, int nb,
+                         int layout, float *gQ, float *gK, float *gB, void *stream);
+
+/* layout adapters between the reference {n, C} and native {C, n} */
+mdg_status mdg_qk_posmajor_to_planar(const float *src, int64_t n, int C, float *dst,
+                                     void *stream);
+mdg_status mdg_qk_planar_to_posmajor(const float *src, int64_t n, int C, float *dst,
+                                     void *stream);
+
+/* ============================ host-buffer calls ============================
+ * Synchronous drop-ins for the reference CPU functions: host pointers in and
+ * out; device staging and the copies happen inside the call. */
+mdg_status mdg_na_fused_fwd_host(const float *Q, const float *K, const float *B, mdg_dims3 d,
+                                 int S, int hd, int nb, float *W);
+mdg_status mdg_modet_fwd_host(const float *Q, const float *K, const float *B, mdg_dims3 d,
+                              int S, int hd, int nb, int layout, float *SF, float *LSE);
+mdg_status mdg_modet_bwd_host(const float *Q, const float *K, const float *B, const float *SF,
+                              const float *LSE, const float *gSF, mdg_dims3 d, int S, int hd,
+                              int nb, int layout, float *gQ, float *gK, float *gB);
+mdg_status mdg_warp_fwd_host(const float *in, int C, mdg_dims3 d, const float *field,
+                             float *out);
+mdg_status mdg_warp_bwd_host(const float *in, int C, mdg_dims3 d, const float *field,
+                             const float *gout, float *gin, float *gfield);
+
+/* ========================= synthetic input streams =========================
+ * Bit-identical to the reference's splitmix64/Box-Muller Rng (rng.hpp:23-67),
+ * so the GPU and the CPU reference consume identical bytes. */
+typedef struct mdg_rng mdg_rng;
+mdg_rng *mdg_rng_new(uint64_t seed);
+void mdg_rng_free(mdg_rng *r);
+void mdg_rng_fill_uniform(mdg_rng *r, float *out, int64_t n, double lo, double hi);
+void mdg_rng_fill_normal(mdg_rng *r, float *out, int64_t n, double mean, double sd);
+
+/* pinned host memory for the host-buffer path */
+void *mdg_host_alloc(size_t bytes);
+void mdg_host_free(void *p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDG_H */

@@ -1,0 +1,291 @@
+"""pyoracle — numpy/ctypes face of the CPU ORACLE.  TEST INFRASTRUCTURE ONLY.
+
+Loads ``oracle/_build/libmdo.so`` (the C restatement, ``oracle/mdo.c``) and,
+when present, ``oracle/_ref/libmdreg_ref.so`` (the unmodified reference headers
+compiled by ``oracle/Makefile``).  Only ``tests/``, ``__graft_entry__.smoke()``
+and ``bench.py``'s CPU-baseline leg import this module; the product package
+never does.
+
+Every wrapper takes/returns numpy float32 arrays in the reference layouts
+(channel-major fields ``{C, l, w, h}`` in numpy index order, i.e. x fastest;
+attention Q/K position-major ``{n, S*d}``; W ``{S, n, nb^3}``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_MDO = os.path.join(HERE, "_build", "libmdo.so")
+LIB_REF = os.path.join(HERE, "_ref", "libmdreg_ref.so")
+
+_f = C.POINTER(C.c_float)
+_i = C.POINTER(C.c_int)
+
+
+def build(quiet: bool = True) -> None:
+    """Compile the restatement (and _ref when /root/reference is present)."""
+    cmd = ["make", "-C", HERE, "-s"] if quiet else ["make", "-C", HERE]
+    subprocess.run(cmd, check=True)
+
+
+def _fp(a):
+    if a is None:
+        return None
+    assert a.dtype == np.float32 and a.flags["C_CONTIGUOUS"], (a.dtype, a.flags)
+    return a.ctypes.data_as(_f)
+
+
+class _Lib:
+    """Common signatures for libmdo (prefix mdo_) and libmdreg_ref (mdr_)."""
+
+    def __init__(self, path: str, prefix: str):
+        self.path = path
+        self.prefix = prefix
+        self.lib = C.CDLL(path)
+        L = self.lib
+        p = prefix
+
+        def sig(name, res, *args):
+            fn = getattr(L, p + name)
+            fn.restype = res
+            fn.argtypes = list(args)
+            return fn
+
+        ii = C.c_int
+        self._window_offset = sig("window_offset", None, ii, ii, _i)
+        if prefix == "mdo_":
+            self._na_fwd = sig("na_fwd", ii, _f, _f, _f, ii, ii, ii, ii, ii, ii, _f, _i)
+        else:
+            self._na_fwd = sig("na_fwd", ii, _f, _f, _f, ii, ii, ii, ii, ii, ii, _f)
+            self._na_naive_fwd = sig("na_naive_fwd", ii, _f, _f, _f, ii, ii, ii, ii, ii, ii, _f)
+            self._last_error = sig("last_error", C.c_char_p)
+            self._smooth_vel = sig("make_smooth_velocity", None, ii, ii, ii, C.c_uint64,
+                                   C.c_float, C.c_float, _f)
+            self._attn_bench = sig("attention_bench_fused_ms", C.c_double, ii, ii, ii, ii, ii,
+                                   ii, C.c_uint64)
+        self._na_bwd = sig("na_bwd", None, _f, _f, _f, ii, ii, ii, ii, ii, ii, _f, _f, _f, _f)
+        self._sf_fwd = sig("subfields_fwd", None, _f, ii, ii, ii, ii, ii, _f)
+        self._sf_bwd = sig("subfields_bwd", None, ii, ii, ii, ii, ii, _f, _f)
+        self._resolve = sig("resolve_axis", None, C.c_float, ii, _i, _i, _f, _i)
+        self._warp_fwd = sig("warp_fwd", None, _f, ii, ii, ii, ii, _f, _f)
+        self._warp_bwd = sig("warp_bwd", None, _f, ii, ii, ii, ii, _f, _f, _f, _f)
+        self._up_fwd = sig("upsample2_fwd", None, _f, ii, ii, ii, ii, ii, ii, ii, C.c_float, _f)
+        self._up_bwd = sig("upsample2_bwd", None, ii, ii, ii, ii, ii, ii, ii, C.c_float, _f, _f)
+        self._up_ok = sig("upsample_target_ok", ii, ii, ii, ii, ii, ii, ii)
+        self._conv_fwd = sig("conv3_fwd", None, _f, ii, ii, ii, ii, _f, _f, ii, _f)
+        self._conv_bwd = sig("conv3_bwd", None, _f, ii, ii, ii, ii, _f, ii, _f, _f, _f, _f)
+        self._comp_fwd = sig("compose_fwd", None, _f, _f, ii, ii, ii, _f)
+        self._comp_bwd = sig("compose_bwd", None, _f, _f, ii, ii, ii, _f, _f, _f)
+        self._ss = sig("scaling_squaring", None, _f, ii, ii, ii, ii, _f)
+
+    # -- attention ---------------------------------------------------------
+    def window_offset(self, o, nb=3):
+        off = (C.c_int * 3)()
+        self._window_offset(o, nb, off)
+        return tuple(off)
+
+    def na_fwd(self, Q, K, B, dims, S, hd, nb=3):
+        """Returns (W, bad) — bad is None or (x,y,z,head) of the first
+        non-finite logit (the reference raises numeric_error there)."""
+        h, w, l = dims
+        n = h * w * l
+        W = np.zeros((S, n, nb ** 3), np.float32)
+        if self.prefix == "mdo_":
+            bad = (C.c_int * 4)()
+            rc = self._na_fwd(_fp(Q), _fp(K), _fp(B), h, w, l, S, hd, nb, _fp(W), bad)
+            return W, (tuple(bad) if rc == 1 else None)
+        rc = self._na_fwd(_fp(Q), _fp(K), _fp(B), h, w, l, S, hd, nb, _fp(W))
+        return W, (self._last_error().decode() if rc else None)
+
+    def na_naive_fwd(self, Q, K, B, dims, S, hd, nb=3):
+        h, w, l = dims
+        W = np.zeros((S, h * w * l, nb ** 3), np.float32)
+        rc = self._na_naive_fwd(_fp(Q), _fp(K), _fp(B), h, w, l, S, hd, nb, _fp(W))
+        return W, (self._last_error().decode() if rc else None)
+
+    def na_bwd(self, Q, K, W, gW, dims, S, hd, nb=3, gQ=None, gK=None, gB=None):
+        h, w, l = dims
+        gQ = np.zeros_like(Q) if gQ is None else gQ
+        gK = np.zeros_like(K) if gK is None else gK
+        gB = np.zeros((S, nb ** 3), np.float32) if gB is None else gB
+        self._na_bwd(_fp(Q), _fp(K), _fp(W), h, w, l, S, hd, nb, _fp(gW), _fp(gQ), _fp(gK),
+                     _fp(gB))
+        return gQ, gK, gB
+
+    def subfields_fwd(self, W, dims, S, nb=3):
+        h, w, l = dims
+        out = np.zeros((3 * S, l, w, h), np.float32)
+        self._sf_fwd(_fp(W), h, w, l, S, nb, _fp(out))
+        return out
+
+    def subfields_bwd(self, gout, dims, S, nb=3, gW=None):
+        h, w, l = dims
+        gW = np.zeros((S, h * w * l, nb ** 3), np.float32) if gW is None else gW
+        self._sf_bwd(h, w, l, S, nb, _fp(gout), _fp(gW))
+        return gW
+
+    # -- sampling ----------------------------------------------------------
+    def resolve_axis(self, x, dim):
+        i0, i1, live = C.c_int(), C.c_int(), C.c_int()
+        f = C.c_float()
+        self._resolve(C.c_float(x), dim, C.byref(i0), C.byref(i1), C.byref(f), C.byref(live))
+        return i0.value, i1.value, f.value, live.value
+
+    def warp_fwd(self, vol, field):
+        Cc = vol.shape[0]
+        l, w, h = vol.shape[1:]
+        out = np.zeros_like(vol)
+        self._warp_fwd(_fp(vol), Cc, h, w, l, _fp(field), _fp(out))
+        return out
+
+    def warp_bwd(self, vol, field, gout, want_gin=True, want_gfield=True, gin=None, gfield=None):
+        Cc = vol.shape[0]
+        l, w, h = vol.shape[1:]
+        if want_gin and gin is None:
+            gin = np.zeros_like(vol)
+        if want_gfield and gfield is None:
+            gfield = np.zeros_like(field)
+        self._warp_bwd(_fp(vol), Cc, h, w, l, _fp(field), _fp(gout),
+                       _fp(gin) if want_gin else None, _fp(gfield) if want_gfield else None)
+        return gin, gfield
+
+    def upsample_target_ok(self, dims, tdims):
+        return bool(self._up_ok(*dims, *tdims))
+
+    def upsample2_fwd(self, x, tdims, scale=2.0):
+        Cc = x.shape[0]
+        l, w, h = x.shape[1:]
+        th, tw, tl = tdims
+        out = np.zeros((Cc, tl, tw, th), np.float32)
+        self._up_fwd(_fp(x), Cc, h, w, l, th, tw, tl, scale, _fp(out))
+        return out
+
+    def upsample2_bwd(self, gout, dims, scale=2.0, gin=None):
+        Cc = gout.shape[0]
+        tl, tw, th = gout.shape[1:]
+        h, w, l = dims
+        gin = np.zeros((Cc, l, w, h), np.float32) if gin is None else gin
+        self._up_bwd(Cc, h, w, l, th, tw, tl, scale, _fp(gout), _fp(gin))
+        return gin
+
+    # -- conv / fields -----------------------------------------------------
+    def conv3_fwd(self, x, k, bias):
+        ic = x.shape[0]
+        l, w, h = x.shape[1:]
+        oc = k.shape[0]
+        out = np.zeros((oc, l, w, h), np.float32)
+        self._conv_fwd(_fp(x), ic, h, w, l, _fp(k), _fp(bias), oc, _fp(out))
+        return out
+
+    def conv3_bwd(self, x, k, gout, gin=None, gk=None, gbias=None):
+        ic = x.shape[0]
+        l, w, h = x.shape[1:]
+        oc = k.shape[0]
+        gin = np.zeros_like(x) if gin is None else gin
+        gk = np.zeros_like(k) if gk is None else gk
+        gbias = np.zeros((oc,), np.float32) if gbias is None else gbias
+        self._conv_bwd(_fp(x), ic, h, w, l, _fp(k), oc, _fp(gout), _fp(gin), _fp(gk), _fp(gbias))
+        return gin, gk, gbias
+
+    def compose_fwd(self, prev, res):
+        l, w, h = prev.shape[1:]
+        out = np.zeros_like(prev)
+        self._comp_fwd(_fp(prev), _fp(res), h, w, l, _fp(out))
+        return out
+
+    def compose_bwd(self, prev, res, gout, gprev=None, gres=None):
+        l, w, h = prev.shape[1:]
+        gprev = np.zeros_like(prev) if gprev is None else gprev
+        gres = np.zeros_like(res) if gres is None else gres
+        self._comp_bwd(_fp(prev), _fp(res), h, w, l, _fp(gout), _fp(gprev), _fp(gres))
+        return gprev, gres
+
+    def scaling_squaring(self, vel, steps):
+        l, w, h = vel.shape[1:]
+        out = np.zeros_like(vel)
+        self._ss(_fp(vel), h, w, l, steps, _fp(out))
+        return out
+
+    # -- reference-only helpers --------------------------------------------
+    def make_smooth_velocity(self, dims, seed, magnitude, sigma):
+        h, w, l = dims
+        out = np.zeros((3, l, w, h), np.float32)
+        self._smooth_vel(h, w, l, seed, magnitude, sigma, _fp(out))
+        return out
+
+
+class Rng:
+    """splitmix64 + Box-Muller stream, bit-identical to reference rng.hpp:23-67
+    (vectorised in numpy; ``normal`` honours the one-value cache)."""
+
+    _G = np.uint64(0x9E3779B97F4A7C15)
+
+    def __init__(self, seed: int):
+        self.state = np.uint64(seed)
+        self.spare = None
+
+    def next_u64(self, n: int) -> np.ndarray:
+        with np.errstate(over="ignore"):
+            k = np.arange(1, n + 1, dtype=np.uint64)
+            z = self.state + k * self._G
+            self.state = self.state + np.uint64(n) * self._G
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            return z ^ (z >> np.uint64(31))
+
+    def uniform01(self, n: int) -> np.ndarray:
+        return (self.next_u64(n) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+    def uniform(self, n: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+        return lo + (hi - lo) * self.uniform01(n)
+
+    def uniform_int(self, lo: int, hi: int) -> int:
+        return lo + int(int(self.next_u64(1)[0]) % (hi - lo + 1))
+
+    def normal(self, n: int, mean: float = 0.0, sd: float = 1.0) -> np.ndarray:
+        out = np.empty(n, np.float64)
+        i = 0
+        if self.spare is not None and n > 0:
+            out[0] = self.spare
+            self.spare = None
+            i = 1
+        rem = n - i
+        pairs = (rem + 1) // 2
+        if pairs:
+            u = self.uniform01(2 * pairs)
+            u1 = np.maximum(u[0::2], 1e-300)
+            u2 = u[1::2]
+            r = np.sqrt(-2.0 * np.log(u1))
+            a = 6.283185307179586476925286766559 * u2
+            vals = np.empty(2 * pairs)
+            vals[0::2] = r * np.cos(a)
+            vals[1::2] = r * np.sin(a)
+            out[i:] = vals[:rem]
+            if rem % 2 == 1:
+                self.spare = vals[-1]
+        return mean + sd * out
+
+
+_cache = {}
+
+
+def mdo() -> _Lib:
+    if "mdo" not in _cache:
+        if not os.path.exists(LIB_MDO):
+            build()
+        _cache["mdo"] = _Lib(LIB_MDO, "mdo_")
+    return _cache["mdo"]
+
+
+def ref_available() -> bool:
+    return os.path.exists(LIB_REF)
+
+
+def ref() -> _Lib:
+    if "ref" not in _cache:
+        _cache["ref"] = _Lib(LIB_REF, "mdr_")
+    return _cache["ref"]

@@ -1,0 +1,112 @@
+"""ctypes binding of ``include/mdg.h`` (libmdg.so, sm_100a).
+
+The library is built in-tree (``paper_2403_16526_b200/libmdg.so``) by
+``__graft_entry__.build()`` / ``make -C paper_2403_16526_b200/csrc``.  There is
+no fallback: if the library is missing, importing the bindings raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmdg.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "mdg.h")
+
+MDG_OK, MDG_EINVAL, MDG_ENUMERIC, MDG_ECUDA = 0, 1, 2, 3
+MDG_QK_POSMAJOR, MDG_QK_PLANAR = 0, 1
+
+
+class Dims3(C.Structure):
+    """{h, w, l} = extents along x, y, z (reference common.hpp:40-50)."""
+
+    _fields_ = [("h", C.c_int), ("w", C.c_int), ("l", C.c_int)]
+
+    def __iter__(self):
+        return iter((self.h, self.w, self.l))
+
+    def __repr__(self):
+        return f"Dims3({self.h}, {self.w}, {self.l})"
+
+
+_p = C.c_void_p  # device or host pointer
+_i = C.c_int
+_f = C.c_float
+_st = C.c_int  # mdg_status
+
+# name -> (restype, argtypes); mirrors include/mdg.h one to one
+SIGNATURES = {
+    "mdg_last_error": (C.c_char_p, []),
+    "mdg_last_error_position": (None, [C.POINTER(_i)] * 4),
+    "mdg_device_ok": (_i, []),
+    "mdg_build_info": (C.c_char_p, []),
+    "mdg_check_numeric": (_st, [Dims3, _p]),
+    "mdg_launch_count": (C.c_int64, []),
+    "mdg_window_offset": (_st, [_i, _i, C.POINTER(_i)]),
+    "mdg_resolve_axis": (_st, [_p, _i, _i, _p, _p, _p, _p, _p]),
+    "mdg_na_fused_fwd": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _p, _p]),
+    "mdg_na_fused_bwd": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _p, _p, _p, _p, _p]),
+    "mdg_subfields_fwd": (_st, [_p, Dims3, _i, _i, _p, _p]),
+    "mdg_subfields_bwd": (_st, [Dims3, _i, _i, _p, _p, _p]),
+    "mdg_subfields_check_rows": (_st, [_p, Dims3, _i, _i, _f, _p]),
+    "mdg_warp_fwd": (_st, [_p, _i, Dims3, _p, _p, _p]),
+    "mdg_warp_bwd": (_st, [_p, _i, Dims3, _p, _p, _p, _p, _p]),
+    "mdg_upsample2_fwd": (_st, [_p, _i, Dims3, Dims3, _f, _p, _p]),
+    "mdg_upsample2_bwd": (_st, [_i, Dims3, Dims3, _f, _p, _p, _p]),
+    "mdg_conv3_fwd": (_st, [_p, _i, Dims3, _p, _p, _i, _p, _p]),
+    "mdg_conv3_bwd": (_st, [_p, _i, Dims3, _p, _i, _p, _p, _p, _p, _p]),
+    "mdg_compose_fwd": (_st, [_p, _p, Dims3, _p, _p]),
+    "mdg_compose_bwd": (_st, [_p, _p, Dims3, _p, _p, _p, _p]),
+    "mdg_scaling_squaring_fwd": (_st, [_p, Dims3, _i, _p, _p, _p]),
+    "mdg_scaling_squaring_bwd": (_st, [_p, Dims3, _i, _p, _p, _p]),
+    "mdg_modet_fwd": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p, _p]),
+    "mdg_modet_bwd": (_st, [_p, _p, _p, _p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p, _p]),
+    "mdg_qk_posmajor_to_planar": (_st, [_p, C.c_int64, _i, _p, _p]),
+    "mdg_qk_planar_to_posmajor": (_st, [_p, C.c_int64, _i, _p, _p]),
+    "mdg_na_fused_fwd_host": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _p]),
+    "mdg_modet_fwd_host": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p]),
+    "mdg_modet_bwd_host": (_st, [_p, _p, _p, _p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p]),
+    "mdg_warp_fwd_host": (_st, [_p, _i, Dims3, _p, _p]),
+    "mdg_warp_bwd_host": (_st, [_p, _i, Dims3, _p, _p, _p, _p]),
+    "mdg_rng_new": (_p, [C.c_uint64]),
+    "mdg_rng_free": (None, [_p]),
+    "mdg_rng_fill_uniform": (None, [_p, _p, C.c_int64, C.c_double, C.c_double]),
+    "mdg_rng_fill_normal": (None, [_p, _p, C.c_int64, C.c_double, C.c_double]),
+    "mdg_host_alloc": (_p, [C.c_size_t]),
+    "mdg_host_free": (None, [_p]),
+}
+
+
+class _Lib:
+    def __init__(self, path: str = LIB_PATH):
+        if not os.path.exists(path):
+            raise ImportError(
+                f"libmdg.so not found at {path}: build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)")
+        self.path = path
+        self.lib = C.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(self.lib, name)
+            fn.restype = res
+            fn.argtypes = args
+            setattr(self, name, fn)
+
+
+_LIB = None
+
+
+def lib() -> _Lib:
+    global _LIB
+    if _LIB is None:
+        _LIB = _Lib()
+    return _LIB
+
+
+def header_symbols(path: str = HEADER):
+    """Function names declared in include/mdg.h (for the export test)."""
+    import re
+
+    txt = open(path).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(mdg_[a-z0-9_]+)\s*\(", txt)))

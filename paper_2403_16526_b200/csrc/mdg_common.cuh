@@ -1,0 +1,124 @@
+// mdg_common.cuh — shared internals of libmdg (B200 / sm_100a).
+//
+// Indexing follows the reference layout contract (common.hpp:56-59): voxel
+// p = (z*w + y)*h + x, channel-major planes.  All kernels are fp32.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/mdg.h"
+
+namespace mdg {
+
+// ------------------------------------------------------------------ status
+void set_error(mdg_status st, const std::string &msg);
+mdg_status status_from_cuda(cudaError_t e, const char *where);
+extern std::atomic<int64_t> g_launches;
+
+#define MDG_CUDA_TRY(expr)                                                        \
+    do {                                                                          \
+        cudaError_t _e = (expr);                                                  \
+        if (_e != cudaSuccess) return ::mdg::status_from_cuda(_e, #expr);         \
+    } while (0)
+
+// after a launch: count it and surface launch-config errors
+#define MDG_LAUNCHED()                                                            \
+    do {                                                                          \
+        ::mdg::g_launches.fetch_add(1, std::memory_order_relaxed);                \
+        cudaError_t _e = cudaPeekAtLastError();                                   \
+        if (_e != cudaSuccess) return ::mdg::status_from_cuda(_e, __func__);      \
+    } while (0)
+
+#define MDG_REQUIRE(cond, msg)                                                    \
+    do {                                                                          \
+        if (!(cond)) {                                                            \
+            ::mdg::set_error(MDG_EINVAL, (msg));                                  \
+            return MDG_EINVAL;                                                    \
+        }                                                                         \
+    } while (0)
+
+inline cudaStream_t S_(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int64_t nvox(mdg_dims3 d) { return (int64_t)d.h * d.w * d.l; }
+inline std::string dims_str(mdg_dims3 d) {
+    return std::to_string(d.h) + "x" + std::to_string(d.w) + "x" + std::to_string(d.l);
+}
+inline bool dims_ok(mdg_dims3 d) {
+    return d.h >= 0 && d.w >= 0 && d.l >= 0 && nvox(d) < (int64_t(1) << 31);
+}
+
+// ----------------------------------------------- device-side numeric flag
+// One word per device: the smallest (head*n + p) key whose attention row
+// produced a non-finite logit, or ~0ull.  Keys follow the reference's loop
+// order (attention.hpp:91-96: head outer, then z, y, x) so atomicMin yields
+// the position the reference would have thrown at.
+unsigned long long *numeric_flag_ptr();  // device pointer for the current device
+// read + reset; returns true if set, and the (x,y,z,head) decoded w.r.t. the
+// dims of the call that is checking
+mdg_status consume_numeric_flag(cudaStream_t st, mdg_dims3 d);
+
+// --------------------------------------------------- stream-ordered scratch
+// cudaMallocAsync/cudaFreeAsync from the device's default mempool.
+struct Scratch {
+    void *p = nullptr;
+    cudaStream_t st = nullptr;
+    Scratch() = default;
+    Scratch(const Scratch &) = delete;
+    Scratch &operator=(const Scratch &) = delete;
+    cudaError_t alloc(size_t bytes, cudaStream_t s) {
+        st = s;
+        return cudaMallocAsync(&p, bytes ? bytes : 16, s);
+    }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    template <typename T>
+    T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+inline unsigned grid1d(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
+
+// --------------------------------------------------------- device helpers
+// sampling.hpp:29-49 resolve_axis — identical integer logic on the device.
+struct Ax {
+    int i0, i1;
+    float f;
+    bool live;
+};
+
+__device__ __forceinline__ Ax resolve_axis(float x, int dim) {
+    Ax a;
+    if (dim <= 1) {
+        a.i0 = 0;
+        a.i1 = 0;
+        a.f = 0.0f;
+        a.live = false;
+        return a;
+    }
+    const float hi = (float)(dim - 1);
+    const float xc = x < 0.0f ? 0.0f : (x > hi ? hi : x);
+    int i0 = (int)floorf(xc);
+    if (i0 > dim - 2) i0 = dim - 2;
+    a.i0 = i0;
+    a.i1 = i0 + 1;
+    a.f = __fsub_rn(xc, (float)i0);
+    a.live = x > 0.0f && x < hi;
+    return a;
+}
+
+// IEEE-rounded helpers: keep the reference's evaluation order without FMA
+// contraction so sampling results are bit-identical to the CPU reference.
+__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_(float a, float b) { return __fsub_rn(a, b); }
+// a*(1-f) + b*f with both products rounded (sampling.hpp:61-67)
+__device__ __forceinline__ float lerp_(float a, float b, float f) {
+    return add_(mul_(a, sub_(1.0f, f)), mul_(b, f));
+}
+
+}  // namespace mdg

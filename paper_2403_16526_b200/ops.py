@@ -1,0 +1,416 @@
+"""Python face of the B200 ModeT hot path (torch tensors as device memory).
+
+Mirrors the reference's interfaces so code written against mdreg reads the
+same way:
+
+* ``kern`` functions have the names, argument meaning and overwrite /
+  accumulate rules of ``mdreg::kern::*`` (attention.hpp, sampling.hpp,
+  ops.hpp) and take CUDA fp32 tensors in the reference layouts;
+* errors raise :class:`InvalidInput` / :class:`NumericError`, the Python
+  counterparts of ``mdreg::invalid_input`` / ``mdreg::numeric_error``
+  (common.hpp:25-37);
+* the fused ModeT operator (``modet_fwd`` / ``modet_bwd``) is the B200-native
+  replacement of ``op_na_fused`` + ``op_subfields``.
+
+Everything runs on the current torch CUDA stream through ``libmdg.so``; there
+is no CPU path.  torch provides memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _capi
+from ._capi import MDG_QK_PLANAR, MDG_QK_POSMAJOR, Dims3
+
+
+class InvalidInput(ValueError):
+    """mdreg::invalid_input — bad arguments or inconsistent shapes."""
+
+
+class NumericError(RuntimeError):
+    """mdreg::numeric_error — non-finite values during computation."""
+
+    position = None  # (x, y, z, head) for attention errors
+
+
+class CudaError(RuntimeError):
+    """A CUDA runtime failure inside libmdg."""
+
+
+def _check(status: int):
+    if status == _capi.MDG_OK:
+        return
+    L = _capi.lib()
+    msg = L.mdg_last_error().decode()
+    if status == _capi.MDG_EINVAL:
+        raise InvalidInput(msg)
+    if status == _capi.MDG_ENUMERIC:
+        e = NumericError(msg)
+        pos = [C.c_int() for _ in range(4)]
+        L.mdg_last_error_position(*[C.byref(v) for v in pos])
+        e.position = tuple(v.value for v in pos)
+        raise e
+    raise CudaError(msg)
+
+
+def _ptr(t, name="tensor"):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise InvalidInput(f"{name}: expected a torch tensor")
+    if not t.is_cuda:
+        raise InvalidInput(f"{name}: must be a CUDA tensor (no CPU path)")
+    if t.dtype != torch.float32:
+        raise InvalidInput(f"{name}: must be float32")
+    if not t.is_contiguous():
+        raise InvalidInput(f"{name}: must be contiguous")
+    return t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dims3(d) -> Dims3:
+    h, w, l = (int(v) for v in d)
+    return Dims3(h, w, l)
+
+
+def voxel_count(d) -> int:
+    h, w, l = d
+    return int(h) * int(w) * int(l)
+
+
+def halved(d):
+    """common.hpp:70-74 (ceil)."""
+    return tuple((int(v) + 1) // 2 for v in d)
+
+
+@dataclass
+class AttentionConfig:
+    """attention.hpp:40-54."""
+
+    heads: int = 1
+    head_dim: int = 6
+    neighborhood: int = 3
+
+    def radius(self) -> int:
+        return (self.neighborhood - 1) // 2
+
+    def window(self) -> int:
+        return self.neighborhood ** 3
+
+    def validate(self):
+        if self.neighborhood < 3 or self.neighborhood % 2 == 0:
+            raise InvalidInput("attention: neighborhood must be odd and >= 3")
+        if self.heads < 1 or self.head_dim < 1:
+            raise InvalidInput("attention: heads and head_dim must be positive")
+
+
+def window_offset(o: int, nb: int = 3):
+    """attention.hpp:57-60 (evaluated by libmdg)."""
+    off = (C.c_int * 3)()
+    _check(_capi.lib().mdg_window_offset(o, nb, off))
+    return tuple(off)
+
+
+class kern:  # noqa: N801 — mirrors the reference namespace mdreg::kern
+    """Reference-shaped kernel tier: in-place on caller-owned CUDA tensors."""
+
+    @staticmethod
+    def resolve_axis(x: torch.Tensor, dim: int):
+        n = x.numel()
+        i0 = torch.empty(n, dtype=torch.int32, device=x.device)
+        i1 = torch.empty_like(i0)
+        live = torch.empty_like(i0)
+        f = torch.empty(n, dtype=torch.float32, device=x.device)
+        _check(_capi.lib().mdg_resolve_axis(_ptr(x, "x"), n, dim, i0.data_ptr(), i1.data_ptr(),
+                                            f.data_ptr(), live.data_ptr(), _stream()))
+        return i0, i1, f, live
+
+    @staticmethod
+    def na_fused_fwd(Q, K, B, d, S, hd, nb, W):
+        _check(_capi.lib().mdg_na_fused_fwd(_ptr(Q, "Q"), _ptr(K, "K"), _ptr(B, "B"), dims3(d),
+                                            S, hd, nb, _ptr(W, "W"), _stream()))
+
+    @staticmethod
+    def na_fused_bwd(Q, K, W, d, S, hd, nb, gW, gQ, gK, gB):
+        _check(_capi.lib().mdg_na_fused_bwd(_ptr(Q), _ptr(K), _ptr(W), dims3(d), S, hd, nb,
+                                            _ptr(gW), _ptr(gQ), _ptr(gK), _ptr(gB), _stream()))
+
+    @staticmethod
+    def subfields_fwd(W, d, S, nb, out):
+        _check(_capi.lib().mdg_subfields_fwd(_ptr(W), dims3(d), S, nb, _ptr(out), _stream()))
+
+    @staticmethod
+    def subfields_bwd(d, S, nb, gout, gW):
+        _check(_capi.lib().mdg_subfields_bwd(dims3(d), S, nb, _ptr(gout), _ptr(gW), _stream()))
+
+    @staticmethod
+    def warp_fwd(in_, channels, d, field, out):
+        _check(_capi.lib().mdg_warp_fwd(_ptr(in_), channels, dims3(d), _ptr(field), _ptr(out),
+                                        _stream()))
+
+    @staticmethod
+    def warp_bwd(in_, channels, d, field, gout, gin, gfield):
+        _check(_capi.lib().mdg_warp_bwd(_ptr(in_), channels, dims3(d), _ptr(field), _ptr(gout),
+                                        _ptr(gin), _ptr(gfield), _stream()))
+
+    @staticmethod
+    def upsample2_fwd(in_, channels, d, td, scale, out):
+        _check(_capi.lib().mdg_upsample2_fwd(_ptr(in_), channels, dims3(d), dims3(td),
+                                             float(scale), _ptr(out), _stream()))
+
+    @staticmethod
+    def upsample2_bwd(channels, d, td, scale, gout, gin):
+        _check(_capi.lib().mdg_upsample2_bwd(channels, dims3(d), dims3(td), float(scale),
+                                             _ptr(gout), _ptr(gin), _stream()))
+
+    @staticmethod
+    def conv3_fwd(in_, ic, d, k, bias, oc, out):
+        _check(_capi.lib().mdg_conv3_fwd(_ptr(in_), ic, dims3(d), _ptr(k), _ptr(bias), oc,
+                                         _ptr(out), _stream()))
+
+    @staticmethod
+    def conv3_bwd(in_, ic, d, k, oc, gout, gin, gk, gbias):
+        _check(_capi.lib().mdg_conv3_bwd(_ptr(in_), ic, dims3(d), _ptr(k), oc, _ptr(gout),
+                                         _ptr(gin), _ptr(gk), _ptr(gbias), _stream()))
+
+
+# ------------------------------------------------------------------ op tier
+def _empty(*shape, like):
+    return torch.empty(*shape, dtype=torch.float32, device=like.device)
+
+
+def _zeros(*shape, like):
+    return torch.zeros(*shape, dtype=torch.float32, device=like.device)
+
+
+def check_numeric(d):
+    """Raise NumericError if a fused-tier kernel saw a non-finite logit
+    (position decoded against dims d)."""
+    _check(_capi.lib().mdg_check_numeric(dims3(d), _stream()))
+
+
+def modet_fwd(Q, K, B, d, cfg: AttentionConfig, layout=MDG_QK_POSMAJOR, want_w=False,
+              check=True):
+    """Fused ModeT forward: (SF {3S,n}, LSE {S,n}[, W {S,n,27}]).
+
+    Equals subfields_fwd(na_fused_fwd(Q,K,B)) of the reference
+    (attention.hpp:83-123, 282-298)."""
+    cfg.validate()
+    n = voxel_count(d)
+    S, hd = cfg.heads, cfg.head_dim
+    if Q.numel() != n * S * hd or K.shape != Q.shape:
+        raise InvalidInput("neighborhood_attention: Q/K layout inconsistent with config")
+    if B.numel() != S * cfg.window():
+        raise InvalidInput("neighborhood_attention: bias must be {S, n^3}")
+    SF = _empty(3 * S, n, like=Q)
+    LSE = _empty(S, n, like=Q)
+    W = _empty(S, n, cfg.window(), like=Q) if want_w else None
+    _check(_capi.lib().mdg_modet_fwd(_ptr(Q), _ptr(K), _ptr(B), dims3(d), S, hd,
+                                     cfg.neighborhood, layout, _ptr(SF), _ptr(LSE), _ptr(W),
+                                     _stream()))
+    if check:
+        check_numeric(d)
+    return (SF, LSE, W) if want_w else (SF, LSE)
+
+
+def modet_bwd(Q, K, B, SF, LSE, gSF, d, cfg: AttentionConfig, layout=MDG_QK_POSMAJOR,
+              gQ=None, gK=None, gB=None):
+    """Fused ModeT backward; accumulates into (and returns) gQ, gK, gB."""
+    gQ = _zeros(*Q.shape, like=Q) if gQ is None else gQ
+    gK = _zeros(*K.shape, like=K) if gK is None else gK
+    gB = _zeros(*B.shape, like=B) if gB is None else gB
+    _check(_capi.lib().mdg_modet_bwd(_ptr(Q), _ptr(K), _ptr(B), _ptr(SF), _ptr(LSE), _ptr(gSF),
+                                     dims3(d), cfg.heads, cfg.head_dim, cfg.neighborhood, layout,
+                                     _ptr(gQ), _ptr(gK), _ptr(gB), _stream()))
+    return gQ, gK, gB
+
+
+def na_fused(Q, K, B, d, cfg: AttentionConfig):
+    """op_na_fused forward value (attention.hpp:373-390): W {S, n, nb^3}."""
+    cfg.validate()
+    n = voxel_count(d)
+    if Q.dim() != 2 or Q.shape[0] != n or Q.shape[1] != cfg.heads * cfg.head_dim or \
+            K.shape != Q.shape:
+        raise InvalidInput("neighborhood_attention: Q/K layout inconsistent with config")
+    if B.numel() != cfg.heads * cfg.window():
+        raise InvalidInput("neighborhood_attention: bias must be {S, n^3}")
+    W = _empty(cfg.heads, n, cfg.window(), like=Q)
+    kern.na_fused_fwd(Q, K, B, d, cfg.heads, cfg.head_dim, cfg.neighborhood, W)
+    return W
+
+
+def subfields(W, d, cfg: AttentionConfig, norm_tol=1e-5):
+    """op_subfields forward value (attention.hpp:414-436) incl. the row check."""
+    n = voxel_count(d)
+    if W.dim() != 3 or W.shape[0] != cfg.heads or W.shape[1] != n or W.shape[2] != cfg.window():
+        raise InvalidInput("subfields: weights must be {S, n, win}")
+    _check(_capi.lib().mdg_subfields_check_rows(_ptr(W), dims3(d), cfg.heads, cfg.neighborhood,
+                                                float(norm_tol), _stream()))
+    out = _empty(3 * cfg.heads, n, like=W)
+    kern.subfields_fwd(W, d, cfg.heads, cfg.neighborhood, out)
+    return out
+
+
+def warp(vol, field, d=None):
+    """op_warp / field_ops warp forward: vol {C, l, w, h}, field {3, l, w, h}."""
+    if d is None:
+        d = (vol.shape[-1], vol.shape[-2], vol.shape[-3])
+    Cc = vol.numel() // voxel_count(d)
+    if field.numel() != 3 * voxel_count(d):
+        raise InvalidInput(f"warp: field must be {{3,{d[0]}x{d[1]}x{d[2]}}}")
+    out = torch.empty_like(vol)
+    kern.warp_fwd(vol, Cc, d, field, out)
+    return out
+
+
+def warp_bwd(vol, field, gout, d=None, gin=None, gfield=None, want_gin=True, want_gfield=True):
+    if d is None:
+        d = (vol.shape[-1], vol.shape[-2], vol.shape[-3])
+    Cc = vol.numel() // voxel_count(d)
+    if want_gin and gin is None:
+        gin = torch.zeros_like(vol)
+    if want_gfield and gfield is None:
+        gfield = torch.zeros_like(field)
+    kern.warp_bwd(vol, Cc, d, field, gout, gin if want_gin else None,
+                  gfield if want_gfield else None)
+    return gin, gfield
+
+
+def compose(prev, res, d=None):
+    """compose(prev, res)(x) = res(x) + prev(x + res(x)) (field_ops.hpp:42-49)."""
+    if prev.shape != res.shape:
+        raise InvalidInput("compose: field dims mismatch")
+    if d is None:
+        d = (prev.shape[-1], prev.shape[-2], prev.shape[-3])
+    out = torch.empty_like(prev)
+    _check(_capi.lib().mdg_compose_fwd(_ptr(prev), _ptr(res), dims3(d), _ptr(out), _stream()))
+    return out
+
+
+def compose_bwd(prev, res, gout, d=None, gprev=None, gres=None):
+    if d is None:
+        d = (prev.shape[-1], prev.shape[-2], prev.shape[-3])
+    gprev = torch.zeros_like(prev) if gprev is None else gprev
+    gres = torch.zeros_like(res) if gres is None else gres
+    _check(_capi.lib().mdg_compose_bwd(_ptr(prev), _ptr(res), dims3(d), _ptr(gout), _ptr(gprev),
+                                       _ptr(gres), _stream()))
+    return gprev, gres
+
+
+def upsample_field_2x(field, target, d=None):
+    """op_upsample_field_2x forward (ops.hpp:258-271): values x2 on the finer grid."""
+    if d is None:
+        d = (field.shape[-1], field.shape[-2], field.shape[-3])
+    Cc = field.numel() // voxel_count(d)
+    th, tw, tl = target
+    out = _empty(Cc, tl, tw, th, like=field)
+    kern.upsample2_fwd(field, Cc, d, target, 2.0, out)
+    return out
+
+
+def upsample_field_2x_bwd(gout, d, target, gin=None):
+    Cc = gout.numel() // voxel_count(target)
+    h, w, l = d
+    gin = _zeros(Cc, l, w, h, like=gout) if gin is None else gin
+    kern.upsample2_bwd(Cc, d, target, 2.0, gout, gin)
+    return gin
+
+
+def conv3(x, k, bias, d=None):
+    """op_conv3 forward (ops.hpp:137-158); RegHead = conv3 with ic=3S, oc=3."""
+    if d is None:
+        d = (x.shape[-1], x.shape[-2], x.shape[-3])
+    ic = x.numel() // voxel_count(d)
+    if k.dim() != 5 or tuple(k.shape[2:]) != (3, 3, 3):
+        raise InvalidInput("conv3: kernel must be {oc,ic,3,3,3}")
+    if k.shape[1] != ic:
+        raise InvalidInput("conv3: input channels do not match kernel")
+    oc = k.shape[0]
+    if bias is not None and bias.numel() != oc:
+        raise InvalidInput("conv3: bias size mismatch")
+    h, w, l = d
+    out = _empty(oc, l, w, h, like=x)
+    kern.conv3_fwd(x, ic, d, k, bias, oc, out)
+    return out
+
+
+def conv3_bwd(x, k, gout, d=None, gin=None, gk=None, gbias=None):
+    if d is None:
+        d = (x.shape[-1], x.shape[-2], x.shape[-3])
+    ic = x.numel() // voxel_count(d)
+    oc = k.shape[0]
+    gin = torch.zeros_like(x) if gin is None else gin
+    gk = torch.zeros_like(k) if gk is None else gk
+    gbias = _zeros(oc, like=k) if gbias is None else gbias
+    kern.conv3_bwd(x, ic, d, k, oc, gout, gin, gk, gbias)
+    return gin, gk, gbias
+
+
+def scaling_squaring(vel, steps, d=None, keep=False):
+    """reghead.hpp:52-67.  keep=True also returns the saved intermediates."""
+    if steps < 1:
+        raise InvalidInput("scaling_squaring: steps must be >= 1")
+    if d is None:
+        d = (vel.shape[-1], vel.shape[-2], vel.shape[-3])
+    out = torch.empty_like(vel)
+    saved = _empty(steps + 1, *vel.shape, like=vel) if keep else None
+    _check(_capi.lib().mdg_scaling_squaring_fwd(_ptr(vel), dims3(d), steps, _ptr(out),
+                                                _ptr(saved), _stream()))
+    return (out, saved) if keep else out
+
+
+def scaling_squaring_bwd(saved, steps, gout, d=None, gvel=None):
+    if d is None:
+        d = (gout.shape[-1], gout.shape[-2], gout.shape[-3])
+    gvel = torch.zeros_like(gout) if gvel is None else gvel
+    _check(_capi.lib().mdg_scaling_squaring_bwd(_ptr(saved), dims3(d), steps, _ptr(gout),
+                                                _ptr(gvel), _stream()))
+    return gvel
+
+
+def qk_posmajor_to_planar(x):
+    n, Cc = x.shape
+    out = torch.empty(Cc, n, dtype=x.dtype, device=x.device)
+    _check(_capi.lib().mdg_qk_posmajor_to_planar(_ptr(x), n, Cc, _ptr(out), _stream()))
+    return out
+
+
+def qk_planar_to_posmajor(x):
+    Cc, n = x.shape
+    out = torch.empty(n, Cc, dtype=x.dtype, device=x.device)
+    _check(_capi.lib().mdg_qk_planar_to_posmajor(_ptr(x), n, Cc, _ptr(out), _stream()))
+    return out
+
+
+def launch_count() -> int:
+    return int(_capi.lib().mdg_launch_count())
+
+
+class Rng:
+    """Synthetic input stream bit-identical to mdreg::Rng (rng.hpp:23-67)."""
+
+    def __init__(self, seed: int):
+        self._L = _capi.lib()
+        self._h = self._L.mdg_rng_new(seed)
+
+    def __del__(self):
+        try:
+            self._L.mdg_rng_free(self._h)
+        except Exception:
+            pass
+
+    def uniform(self, shape, lo=0.0, hi=1.0, out=None):
+        out = torch.empty(shape, dtype=torch.float32) if out is None else out
+        self._L.mdg_rng_fill_uniform(self._h, out.data_ptr(), out.numel(), lo, hi)
+        return out
+
+    def normal(self, shape, mean=0.0, sd=1.0, out=None):
+        out = torch.empty(shape, dtype=torch.float32) if out is None else out
+        self._L.mdg_rng_fill_normal(self._h, out.data_ptr(), out.numel(), mean, sd)
+        return out
