@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 
 DIMS = (160, 192, 224)  # h, w, l  (x, y, z)
 S, HD, NB, CH = 1, 6, 3, 8
+LAYOUT = 1  # MDG_QK_PLANAR: the fused tier's native {S*d, n} layout
 METRIC = "ModeT op fwd+bwd + feature warp fwd+bwd throughput at 160x192x224 (L1, S=1, d=6, C=8)"
 UNIT = "Gvoxel/s"
 
@@ -140,8 +141,9 @@ def make_inputs(rank: int):
     n = h * w * l
     base = 1000 * rank
     r = ops.Rng(5 + base)
-    Q = r.uniform((n, S * HD), -1.0, 1.0)
-    K = r.uniform((n, S * HD), -1.0, 1.0)
+    # drawn in the reference's position-major order, stored planar {S*d, n}
+    Q = r.uniform((n, S * HD), -1.0, 1.0).t().contiguous()
+    K = r.uniform((n, S * HD), -1.0, 1.0).t().contiguous()
     B = r.uniform((S, 27), -0.5, 0.5)
     gSF = ops.Rng(6 + base).uniform((3 * S, n), -1.0, 1.0)
     feat = ops.Rng(7 + base).normal((CH, l, w, h))
@@ -198,15 +200,16 @@ def run_ours(args):
     ops_order = ["modet_fwd", "modet_bwd", "warp_fwd", "warp_bwd"]
 
     def step(ev=None):
-        # forward outputs are overwritten; backward targets accumulate (the
-        # reference contract) — re-zeroing them is part of the real step
+        # forward outputs are overwritten; the ModeT backward writes fresh
+        # gQ/gK (accumulate=0, as for a tape's zero-initialised grads); the
+        # warp backward accumulates (reference contract)
         if ev: ev[0].record(st)
-        chk(L.mdg_modet_fwd(Q.data_ptr(), K.data_ptr(), B.data_ptr(), d3, S, HD, NB, 0,
+        chk(L.mdg_modet_fwd(Q.data_ptr(), K.data_ptr(), B.data_ptr(), d3, S, HD, NB, LAYOUT,
                             SF.data_ptr(), LSE.data_ptr(), None, sp))
         if ev: ev[1].record(st)
         chk(L.mdg_modet_bwd(Q.data_ptr(), K.data_ptr(), B.data_ptr(), SF.data_ptr(),
-                            LSE.data_ptr(), gSF.data_ptr(), d3, S, HD, NB, 0, gQ.data_ptr(),
-                            gK.data_ptr(), gB.data_ptr(), sp))
+                            LSE.data_ptr(), gSF.data_ptr(), d3, S, HD, NB, LAYOUT,
+                            gQ.data_ptr(), gK.data_ptr(), gB.data_ptr(), 0, sp))
         if ev: ev[2].record(st)
         chk(L.mdg_warp_fwd(feat.data_ptr(), CH, d3, field.data_ptr(), warped.data_ptr(), sp))
         if ev: ev[3].record(st)
@@ -302,10 +305,10 @@ def run_e2e(args, L, host_in, world, dev):
     p = lambda t: t.data_ptr()  # noqa: E731
 
     def step():
-        rc = L.mdg_modet_fwd_host(p(pin["Q"]), p(pin["K"]), p(pin["B"]), d3, S, HD, NB, 0,
+        rc = L.mdg_modet_fwd_host(p(pin["Q"]), p(pin["K"]), p(pin["B"]), d3, S, HD, NB, LAYOUT,
                                   p(outs["SF"]), p(outs["LSE"]))
         rc |= L.mdg_modet_bwd_host(p(pin["Q"]), p(pin["K"]), p(pin["B"]), p(outs["SF"]),
-                                   p(outs["LSE"]), p(pin["gSF"]), d3, S, HD, NB, 0,
+                                   p(outs["LSE"]), p(pin["gSF"]), d3, S, HD, NB, LAYOUT,
                                    p(outs["gQ"]), p(outs["gK"]), p(outs["gB"]))
         rc |= L.mdg_warp_fwd_host(p(pin["feat"]), CH, d3, p(pin["field"]), p(outs["warped"]))
         rc |= L.mdg_warp_bwd_host(p(pin["feat"]), CH, d3, p(pin["field"]), p(pin["gout"]),

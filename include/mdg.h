@@ -157,11 +157,14 @@ mdg_status mdg_modet_fwd(const float *Q, const float *K, const float *B, mdg_dim
                          int hd, int nb, int layout, float *SF, float *LSE, float *W,
                          void *stream);
 /* ModeT backward.  Given the forward's SF and LSE and the upstream gradient
- * gSF {3S, n}, accumulates gQ, gK (same layout as Q, K) and gB {S, nb^3}.
- * Equivalent to subfields_bwd + na_fused_bwd of the reference. */
+ * gSF {3S, n}, produces gQ, gK (same layout as Q, K) and gB {S, nb^3}.
+ * Equivalent to subfields_bwd + na_fused_bwd of the reference.
+ * accumulate != 0: gQ/gK/gB += (the reference rule); accumulate == 0: gQ and
+ * gK are overwritten (saves their read-modify-write; gB always accumulates). */
 mdg_status mdg_modet_bwd(const float *Q, const float *K, const float *B, const float *SF,
                          const float *LSE, const float *gSF, mdg_dims3 d, int S, int hd, int nb,
-                         int layout, float *gQ, float *gK, float *gB, void *stream);
+                         int layout, float *gQ, float *gK, float *gB, int accumulate,
+                         void *stream);
 
 /* layout adapters between the reference {n, C} and native {C, n} */
 mdg_status mdg_qk_posmajor_to_planar(const float *src, int64_t n, int C, float *dst,

@@ -60,7 +60,7 @@ SIGNATURES = {
     "mdg_scaling_squaring_fwd": (_st, [_p, Dims3, _i, _p, _p, _p]),
     "mdg_scaling_squaring_bwd": (_st, [_p, Dims3, _i, _p, _p, _p]),
     "mdg_modet_fwd": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p, _p]),
-    "mdg_modet_bwd": (_st, [_p, _p, _p, _p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p, _p]),
+    "mdg_modet_bwd": (_st, [_p, _p, _p, _p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p, _i, _p]),
     "mdg_qk_posmajor_to_planar": (_st, [_p, C.c_int64, _i, _p, _p]),
     "mdg_qk_planar_to_posmajor": (_st, [_p, C.c_int64, _i, _p, _p]),
     "mdg_na_fused_fwd_host": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _p]),

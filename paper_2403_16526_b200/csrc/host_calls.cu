@@ -121,7 +121,8 @@ mdg_status mdg_modet_bwd_host(const float *Q, const float *K, const float *B, co
     MDG_STAGE_TRY(sg.get(&dgQ, gQ, n * S * hd, true));  // accumulate targets go up too
     MDG_STAGE_TRY(sg.get(&dgK, gK, n * S * hd, true));
     MDG_STAGE_TRY(sg.get(&dgB, gB, (size_t)S * 27, true));
-    mdg_status r = mdg_modet_bwd(dQ, dK, dB, dSF, dL, dG, d, S, hd, nb, layout, dgQ, dgK, dgB, st);
+    mdg_status r =
+        mdg_modet_bwd(dQ, dK, dB, dSF, dL, dG, d, S, hd, nb, layout, dgQ, dgK, dgB, 1, st);
     if (r != MDG_OK) return r;
     MDG_STAGE_TRY(sg.down(gQ, dgQ, n * S * hd));
     MDG_STAGE_TRY(sg.down(gK, dgK, n * S * hd));

@@ -536,6 +536,13 @@ static mdg_status check_attn(mdg_dims3 d, int S, int hd, int nb) {
     return MDG_OK;
 }
 
+// modet_tiled.cu (planar layout, nb = 3); false => head_dim not instantiated
+bool tiled_fwd(int hd, const float *Q, const float *K, const float *B, mdg_dims3 d, int S,
+               float *SF, float *LSE, unsigned long long *flag, cudaStream_t st, cudaError_t *err);
+bool tiled_bwd(int hd, const float *Q, const float *K, const float *B, const float *SF,
+               const float *LSE, const float *gSF, mdg_dims3 d, int S, bool acc, float *gQ,
+               float *gK, float *gB, cudaStream_t st, cudaError_t *err);
+
 }  // namespace mdg
 
 using namespace mdg;
@@ -555,6 +562,14 @@ mdg_status mdg_modet_fwd(const float *Q, const float *K, const float *B, mdg_dim
     unsigned long long *flag = numeric_flag_ptr();
     const dim3 g(grid1d(n, kBlock), S);
     cudaStream_t st = S_(stream);
+    if (layout == MDG_QK_PLANAR && !W) {
+        cudaError_t e = cudaSuccess;
+        if (tiled_fwd(hd, Q, K, B, d, S, SF, LSE, flag, st, &e)) {
+            if (e != cudaSuccess) return status_from_cuda(e, "modet_fwd_tiled");
+            MDG_LAUNCHED();
+            return MDG_OK;
+        }
+    }
     if (layout == MDG_QK_POSMAJOR) {
         if (W) launch_fwd<MDG_QK_POSMAJOR, true>(hd, g, st, Q, K, B, d, S, SF, LSE, W, flag);
         else launch_fwd<MDG_QK_POSMAJOR, false>(hd, g, st, Q, K, B, d, S, SF, LSE, W, flag);
@@ -568,7 +583,8 @@ mdg_status mdg_modet_fwd(const float *Q, const float *K, const float *B, mdg_dim
 
 mdg_status mdg_modet_bwd(const float *Q, const float *K, const float *B, const float *SF,
                          const float *LSE, const float *gSF, mdg_dims3 d, int S, int hd, int nb,
-                         int layout, float *gQ, float *gK, float *gB, void *stream) {
+                         int layout, float *gQ, float *gK, float *gB, int accumulate,
+                         void *stream) {
     if (mdg_status e = check_attn(d, S, hd, nb)) return e;
     MDG_REQUIRE(nb == 3, "modet (fused tier): neighborhood must be 3; use mdg_na_fused_bwd");
     MDG_REQUIRE(hd <= 32, "modet (fused tier): head_dim must be <= 32");
@@ -577,6 +593,17 @@ mdg_status mdg_modet_bwd(const float *Q, const float *K, const float *B, const f
     if (n == 0) return MDG_OK;
     MDG_REQUIRE(Q && K && B && SF && LSE && gSF, "modet: null pointer");
     cudaStream_t st = S_(stream);
+    if (layout == MDG_QK_PLANAR) {
+        cudaError_t e = cudaSuccess;
+        if (tiled_bwd(hd, Q, K, B, SF, LSE, gSF, d, S, accumulate != 0, gQ, gK, gB, st, &e)) {
+            if (e != cudaSuccess) return status_from_cuda(e, "modet_bwd_tiled");
+            return MDG_OK;
+        }
+    }
+    if (!accumulate) {  // v1 kernels accumulate: start from zero
+        if (gQ) MDG_CUDA_TRY(cudaMemsetAsync(gQ, 0, (size_t)n * S * hd * sizeof(float), st));
+        if (gK) MDG_CUDA_TRY(cudaMemsetAsync(gK, 0, (size_t)n * S * hd * sizeof(float), st));
+    }
     const dim3 g(grid1d(n, kBlock), S);
     Scratch part;
     MDG_CUDA_TRY(part.alloc((size_t)S * g.x * 27 * sizeof(float), st));

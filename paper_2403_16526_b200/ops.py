@@ -220,14 +220,19 @@ def modet_fwd(Q, K, B, d, cfg: AttentionConfig, layout=MDG_QK_POSMAJOR, want_w=F
 
 
 def modet_bwd(Q, K, B, SF, LSE, gSF, d, cfg: AttentionConfig, layout=MDG_QK_POSMAJOR,
-              gQ=None, gK=None, gB=None):
-    """Fused ModeT backward; accumulates into (and returns) gQ, gK, gB."""
-    gQ = _zeros(*Q.shape, like=Q) if gQ is None else gQ
-    gK = _zeros(*K.shape, like=K) if gK is None else gK
+              gQ=None, gK=None, gB=None, accumulate=True):
+    """Fused ModeT backward; accumulates into (and returns) gQ, gK, gB.
+    Fresh gradient buffers are produced without a read-modify-write."""
+    if gQ is None and gK is None:
+        gQ, gK, acc = torch.empty_like(Q), torch.empty_like(K), False
+    else:
+        acc = accumulate
+        gQ = _zeros(*Q.shape, like=Q) if gQ is None else gQ
+        gK = _zeros(*K.shape, like=K) if gK is None else gK
     gB = _zeros(*B.shape, like=B) if gB is None else gB
     _check(_capi.lib().mdg_modet_bwd(_ptr(Q), _ptr(K), _ptr(B), _ptr(SF), _ptr(LSE), _ptr(gSF),
                                      dims3(d), cfg.heads, cfg.head_dim, cfg.neighborhood, layout,
-                                     _ptr(gQ), _ptr(gK), _ptr(gB), _stream()))
+                                     _ptr(gQ), _ptr(gK), _ptr(gB), int(acc), _stream()))
     return gQ, gK, gB
 
 

