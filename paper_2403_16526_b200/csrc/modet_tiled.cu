@@ -3,26 +3,45 @@
 // Layout: Q, K planar {S*d, n}; head s owns channel planes s*d .. s*d+d-1.
 //
 // Every kernel is a z-marching CTA: it owns an x-y column tile and walks a
-// chunk of z.  Each step stages ONE zero-padded z-plane (tile + 1-voxel x/y
-// halo) into shared memory with cp.async (zero-fill outside the volume, which
-// is exactly the reference's "out-of-bounds key contributes nothing, logit =
-// bias" rule, attention.hpp:77-81), double-buffered so the next plane lands
-// while the current one is consumed.  A staged plane is used by the three
-// voxels of a thread's column that have it in their 3x3x3 window
-// (z = p-1, p, p+1: "in-flight" slots), so every staged element is read from
-// shared memory once per slot instead of once per logit.
+// chunk of z.  Step p consumes one shared-memory buffer holding
+//   * the HALO plane p of the arrays the thread GATHERS from (tile + 1-voxel
+//     x/y halo), and
+//   * the tile INTERIOR of the arrays the thread OWNS, at plane p+1 (the voxel
+//     that enters the in-flight window this step),
+// double-buffered so step p+1's buffer lands while step p computes.  Staging
+// is 4-D TMA box loads (cp.async.bulk.tensor, one elected thread, mbarrier
+// completion).  TMA's hardware out-of-bounds zero fill is exactly the
+// reference's "out-of-bounds key contributes nothing, logit = bias" rule
+// (attention.hpp:77-81).  The innermost TMA start coordinate must be 16-byte
+// aligned, so halo boxes start at x0-4 and are 40 wide (the logical halo
+// column rx lives at physical column rx+3).  Volumes whose row pitch is not a
+// multiple of 16 bytes (h % 4 != 0) use 4-byte cp.async into the same layout.
 //
-//   fwd  (modet_fwd_tiled_k): per voxel the 27 logits in log2 units
-//        (q pre-scaled by log2 e), an online softmax processed one 3-logit
-//        x-row at a time with lazy rescaling (rescale only when the running
-//        max grows by > 8 in log2 units, so exponents stay <= 2^8), and the
-//        offset-weighted sums; writes SF {3S,n} and LSE {S,n} (natural log).
+// A staged x-strip is read from shared memory ONCE per step and used by the
+// three voxels of the thread's column that have plane p in their 3x3x3 window
+// (z = p+1, p, p-1: the "in-flight" slots).
+//
+// Arithmetic runs on Blackwell's packed FP32 pipe (FFMA2 / FADD2 / FMUL2):
+// the forward and column kernels pair the thread's two x-adjacent voxels, the
+// row kernel pairs channels.  A 3-register FFMA issues every 2 cycles per
+// SMSP, so the packed form doubles the FP32 work per issue slot.
+//
+//   fwd  (modet_fwd_tiled_k): 27 logits per voxel in log2 units (q pre-scaled
+//        by log2 e), online softmax one 3-logit x-row at a time: the first row
+//        sets the reference max, later rows rescale (warp-uniform, rare) only
+//        when the running max grows by > 16 in log2 units; fused
+//        offset-weighted sums.  Writes SF {3S,n}, LSE {S,n} (natural log).
 //   bwd  row kernel (modet_bwd_row_k): p as query.  W = exp2(l - LSE*log2e)
-//        recomputed, dl = W*(gSF.off(o) - gSF.SF), dQ_p += dl*K_{p+o},
-//        dB_o partial per CTA.
-//   bwd  column kernel (modet_bwd_col_k): q as key, gathering from the
-//        staged sources r = q - off(o): dK_q += dl(r,o)*Q_r.  No atomics;
-//        fixed summation order => deterministic.
+//        recomputed, dl = W*(gSF.off(o) - gSF.SF) (since <W, gW> = gSF.SF),
+//        dQ_p += dl*K_{p+o}, per-CTA dB partials (deterministic reduce).
+//   bwd  column kernel (modet_bwd_col_k): q as key, gathering from staged
+//        sources r = q - off(o): dK_q += dl(r,o)*Q_r.  The reference's scatter
+//        (attention.hpp:159-162) as a gather: no atomics, fixed order.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <type_traits>
+
 #include "mdg_common.cuh"
 
 namespace mdg {
@@ -30,362 +49,542 @@ namespace tiled {
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
-constexpr float kRescale = 8.0f;  // lazy-rescale threshold (log2 units)
+constexpr float kRescale = 16.0f;  // lazy-rescale threshold (log2 units)
+constexpr int kXOff = 3;           // physical column of logical halo column 0
+constexpr int kBoxX = 40;          // halo box width (starts at x0 - 4)
 
+__host__ __device__ constexpr int up32(int v) { return (v + 31) / 32 * 32; }
+
+// ------------------------------------------------------------ packed fp32
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 dup2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+
+// ------------------------------------------------------- async copy helpers
+__device__ __forceinline__ unsigned su32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
 __device__ __forceinline__ void cp_async4(float *dst, const float *src, bool pred) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src),
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(su32(dst)), "l"(src),
                  "r"(pred ? 4 : 0));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned phase) {
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(su32(b)), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+// 4-D TMA box load (x, y, z, channel); OOB elements are zero-filled
+__device__ __forceinline__ void tma4(float *dst, const CUtensorMap *m, int x, int y, int z, int c,
+                                     uint64_t *b) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(su32(dst)),
+        "l"(m), "r"(x), "r"(y), "r"(z), "r"(c), "r"(su32(b))
+        : "memory");
+}
 
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float2 ex2x2(float2 d) { return f2(ex2(d.x), ex2(d.y)); }
 
 struct Vol {
     int h, w, l;
     int64_t n, hw;
 };
 
-// Stage plane z of NCH channel planes (channel c at base(c)) for the tile
-// with interior origin (x0, y0) into dst[c][PY][PX] (row length RL = tile+2).
-// Warp-per-row, lane-per-x: coalesced 4-byte cp.async, zero-fill outside.
-template <int NCH, int PY, int RL, int PX, class Base>
-__device__ __forceinline__ void stage_plane(float *dst, Base base, int z, int x0, int y0,
-                                            const Vol &v) {
+// The two array sets of the operator:  set K = {K (d ch)}, set A = {Q (d ch),
+// LSE (1), gSF (3), SF (3)}.  fwd gathers K / owns Q; the row kernel gathers K
+// / owns A; the column kernel gathers A / owns K.
+struct MapsA {
+    CUtensorMap q, lse, g, sf;
+};
+struct Maps {
+    CUtensorMap k;  // set K
+    MapsA a;        // set A
+};
+
+struct Ptrs {
+    const float *K, *Q, *LSE, *gSF, *SF;  // head-offset bases
+    __device__ __forceinline__ const float *a(int c, int D, int64_t n) const {
+        if (c < D) return Q + (int64_t)c * n;
+        if (c == D) return LSE;
+        if (c < D + 4) return gSF + (int64_t)(c - D - 1) * n;
+        return SF + (int64_t)(c - D - 4) * n;
+    }
+    __device__ __forceinline__ const float *k(int c, int64_t n) const { return K + (int64_t)c * n; }
+};
+
+// ---------------------------------------------------------------- staging
+// Buffer = [halo: channel slots of HCH floats][own: channel slots of TX*TY].
+template <int TX, int TY>
+struct Geo {
+    static constexpr int PY = TY + 2, RL = TX + 2, HCH = up32(PY * kBoxX), OCH = TX * TY;
+};
+
+// cp.async fallback, halo part: logical (ry, rx) -> physical ry*40 + rx + 3
+template <int NCH, int TX, int TY, class Base>
+__device__ __forceinline__ void cp_halo(float *dst, Base base, int z, int x0, int y0,
+                                        const Vol &v) {
+    using G = Geo<TX, TY>;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const bool zok = z >= 0 && z < v.l;
-    for (int r = wid; r < NCH * PY; r += nw) {
-        const int c = r / PY, ry = r - c * PY;
+    int c = 0, ry = wid;
+    for (int r = wid; r < NCH * G::PY; r += nw) {
+        while (ry >= G::PY) {
+            ry -= G::PY;
+            ++c;
+        }
         const int gy = y0 - 1 + ry;
         const bool rok = zok && gy >= 0 && gy < v.w;
         const float *row = base(c);
         const int64_t roff = (int64_t)z * v.hw + (int64_t)gy * v.h;
-        float *drow = dst + r * PX;
-#pragma unroll
-        for (int rx = lane; rx < RL; rx += 32) {
+        float *drow = dst + c * G::HCH + ry * kBoxX + kXOff;
+        for (int rx = lane; rx < G::RL; rx += 32) {
             const int gx = x0 - 1 + rx;
             const bool ok = rok && gx >= 0 && gx < v.h;
             cp_async4(drow + rx, ok ? row + roff + gx : row, ok);
         }
+        ry += nw;
     }
 }
 
-// online-softmax state of one (voxel, head) row
-struct Soft {
-    float m, s, ax, ay, az, mn;
+// cp.async fallback, own part: (ty, tx) -> physical ty*TX + tx
+template <int NCH, int TX, int TY, class Base>
+__device__ __forceinline__ void cp_own(float *dst, Base base, int z, int x0, int y0,
+                                       const Vol &v) {
+    const bool zok = z >= 0 && z < v.l;
+    for (int i = threadIdx.x; i < NCH * TX * TY; i += blockDim.x) {
+        const int c = i / (TX * TY), e = i - c * (TX * TY);
+        const int gy = y0 + e / TX, gx = x0 + e % TX;
+        const bool ok = zok && gy < v.w && gx < v.h;
+        const float *row = base(c);
+        cp_async4(dst + i, ok ? row + (int64_t)z * v.hw + (int64_t)gy * v.h + gx : row, ok);
+    }
+}
+
+// Strip of the 4 logical halo columns 2tx-1 .. 2tx+2 (relative to the tile:
+// physical 2tx+3 .. 2tx+6) of one row, as the three overlapping pairs the two
+// voxels x = 2tx, 2tx+1 need for dx = -1, 0, +1.
+struct Strip {
+    float2 p[3];  // {k0,k1}, {k1,k2}, {k2,k3}
 };
-
-__device__ __forceinline__ void soft_init(Soft &st) {
-    st.m = -INFINITY;
-    st.s = st.ax = st.ay = st.az = 0.0f;
-    st.mn = INFINITY;
+__device__ __forceinline__ Strip strip(const float *rowp, int tx) {
+    const float *e = rowp + 2 * tx + 2;
+    const float k0 = e[1];
+    const float2 m = *reinterpret_cast<const float2 *>(e + 2);
+    const float k3 = e[4];
+    Strip s;
+    s.p[0] = f2(k0, m.x);
+    s.p[1] = m;
+    s.p[2] = f2(m.y, k3);
+    return s;
 }
 
-// fold one x-row of three logits (dx = -1, 0, +1) at window row (dy, dz)
-template <int DY, int DZ>
-__device__ __forceinline__ void soft_row(Soft &st, float lm, float l0, float lp) {
-    const float mr = fmaxf(fmaxf(lm, l0), lp);
-    st.mn = fminf(st.mn, fminf(fminf(lm, l0), lp));
-    if (mr > st.m + kRescale) {
-        const float f = ex2(st.m - mr);
-        st.s *= f;
-        st.ax *= f;
-        st.ay *= f;
-        st.az *= f;
-        st.m = mr;
+template <int V>
+using IC = std::integral_constant<int, V>;
+
+// z-marching driver: f(p, NEW, MID, OLD) for p = zb-1 .. ze with the slot
+// roles rotating every step (voxel z lives in slot (z - zb) mod 3)
+template <class F>
+__device__ __forceinline__ void march(int zb, int ze, F &&f) {
+    for (int t = 0;; t += 3) {
+        const int p = zb - 1 + t;
+        if (p > ze) break;
+        f(p, IC<0>(), IC<2>(), IC<1>());
+        if (p + 1 > ze) break;
+        f(p + 1, IC<1>(), IC<0>(), IC<2>());
+        if (p + 2 > ze) break;
+        f(p + 2, IC<2>(), IC<1>(), IC<0>());
     }
-    const float em = ex2(lm - st.m), e0 = ex2(l0 - st.m), ep = ex2(lp - st.m);
-    const float rs = em + e0 + ep;
-    st.s += rs;
-    st.ax += ep - em;
-    if (DY > 0) st.ay += rs;
-    if (DY < 0) st.ay -= rs;
-    if (DZ > 0) st.az += rs;
-    if (DZ < 0) st.az -= rs;
+}
+
+__device__ __forceinline__ void init_bars(uint64_t *bar) {
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+}
+
+// bias pairs {B*log2e, B*log2e} for the 27 window slots of head s
+__device__ __forceinline__ void load_bias2(float2 *sB2, const float *B, int s) {
+    if (threadIdx.x < 27) sB2[threadIdx.x] = dup2(B[s * 27 + threadIdx.x] * kLog2e);
 }
 
 // ======================================================================= fwd
-constexpr int FTX = 32, FTY = 16;                 // tile: 16 threads x 2 voxels, 16 rows
-constexpr int FRL = FTX + 2, FPX = 36, FPY = FTY + 2;
+constexpr int FTX = 32, FTY = 16;  // tile: 16 threads x 2 voxels, 16 rows
+using FG = Geo<FTX, FTY>;
+
+// online-softmax state of the thread's voxel pair (x = .x voxel, y = .y voxel)
+struct Soft2 {
+    float2 m, s, ax, ay, az;
+    float2 mn;  // running min logit (a -inf logit is a numeric error)
+};
+
+// fold one x-row of three logits (dx = -1, 0, +1) at window row (dy, dz)
+template <int DY, int DZ, bool FIRST>
+__device__ __forceinline__ void soft_row2(Soft2 &st, float2 lm, float2 l0, float2 lp) {
+    const float2 mr = f2(fmaxf(fmaxf(lm.x, l0.x), lp.x), fmaxf(fmaxf(lm.y, l0.y), lp.y));
+    st.mn = f2(fminf(st.mn.x, fminf(fminf(lm.x, l0.x), lp.x)),
+               fminf(st.mn.y, fminf(fminf(lm.y, l0.y), lp.y)));
+    if (FIRST) {
+        st.m = mr;
+    } else {
+        const bool need = mr.x > st.m.x + kRescale || mr.y > st.m.y + kRescale;
+        if (__any_sync(0xffffffffu, need)) {
+            if (need) {
+                const float2 nm = f2(fmaxf(st.m.x, mr.x), fmaxf(st.m.y, mr.y));
+                const float2 f = ex2x2(sub2(st.m, nm));
+                st.s = mul2(st.s, f);
+                st.ax = mul2(st.ax, f);
+                st.ay = mul2(st.ay, f);
+                st.az = mul2(st.az, f);
+                st.m = nm;
+            }
+        }
+    }
+    const float2 em = ex2x2(sub2(lm, st.m)), e0 = ex2x2(sub2(l0, st.m)),
+                 ep = ex2x2(sub2(lp, st.m));
+    const float2 rs = add2(add2(em, e0), ep);
+    const float2 dx = sub2(ep, em);
+    if (FIRST) {
+        st.s = rs;
+        st.ax = dx;
+        st.ay = DY > 0 ? rs : (DY < 0 ? f2(-rs.x, -rs.y) : f2(0.f, 0.f));
+        st.az = DZ > 0 ? rs : (DZ < 0 ? f2(-rs.x, -rs.y) : f2(0.f, 0.f));
+    } else {
+        st.s = add2(st.s, rs);
+        st.ax = add2(st.ax, dx);
+        if (DY > 0) st.ay = add2(st.ay, rs);
+        if (DY < 0) st.ay = sub2(st.ay, rs);
+        if (DZ > 0) st.az = add2(st.az, rs);
+        if (DZ < 0) st.az = sub2(st.az, rs);
+    }
+}
 
 template <int D>
 struct FwdSlots {
-    float q[3][2][D];
-    Soft st[3][2];
+    float2 q[3][D];  // per channel {voxel x, voxel x+1} * log2e
+    Soft2 st[3];
 };
 
-template <int D, int DZ>
-__device__ __forceinline__ void fwd_slot_rows(float (&q)[2][D], Soft (&st)[2], const float *P,
-                                              const float *sB, int tx, int ty) {
+template <int D, int DYI, int DZ, bool FIRST>
+__device__ __forceinline__ void fwd_slot(const float2 (&q)[D], Soft2 &st, const Strip (&ks)[D],
+                                         const float2 *sB2) {
+    constexpr int ob = (DZ + 1) * 9 + DYI * 3;
+    float2 lm = sB2[ob], l0 = sB2[ob + 1], lp = sB2[ob + 2];
 #pragma unroll
-    for (int dyi = 0; dyi < 3; ++dyi) {
-        float kr[D][4];
-        const float *rowp = P + (ty + dyi) * FPX + 2 * tx;
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-            const float2 a = *reinterpret_cast<const float2 *>(rowp + c * FPY * FPX);
-            const float2 b = *reinterpret_cast<const float2 *>(rowp + c * FPY * FPX + 2);
-            kr[c][0] = a.x;
-            kr[c][1] = a.y;
-            kr[c][2] = b.x;
-            kr[c][3] = b.y;
-        }
-        const int ob = (DZ + 1) * 9 + dyi * 3;
-        const float b0 = sB[ob], b1 = sB[ob + 1], b2 = sB[ob + 2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            float lm = b0, l0 = b1, lp = b2;
+    for (int c = 0; c < D; ++c) {
+        lm = fma2(q[c], ks[c].p[0], lm);
+        l0 = fma2(q[c], ks[c].p[1], l0);
+        lp = fma2(q[c], ks[c].p[2], lp);
+    }
+    soft_row2<DYI - 1, DZ, FIRST>(st, lm, l0, lp);
+}
+
+template <int D, bool TMA>
+__device__ __forceinline__ void fwd_stage(float *buf, const Maps &m, uint64_t *bar, int p,
+                                          int x0, int y0, int s, const Ptrs &P, const Vol &v) {
+    float *own = buf + D * FG::HCH;
+    if (TMA) {
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(bar, D * (FG::PY * kBoxX + FG::OCH) * 4);
 #pragma unroll
             for (int c = 0; c < D; ++c) {
-                lm = fmaf(q[r][c], kr[c][r], lm);
-                l0 = fmaf(q[r][c], kr[c][r + 1], l0);
-                lp = fmaf(q[r][c], kr[c][r + 2], lp);
+                tma4(buf + c * FG::HCH, &m.k, x0 - 4, y0 - 1, p, s * D + c, bar);
+                tma4(own + c * FG::OCH, &m.a.q, x0, y0, p + 1, s * D + c, bar);
             }
-            if (dyi == 0) soft_row<-1, DZ>(st[r], lm, l0, lp);
-            if (dyi == 1) soft_row<0, DZ>(st[r], lm, l0, lp);
-            if (dyi == 2) soft_row<1, DZ>(st[r], lm, l0, lp);
         }
+    } else {
+        cp_halo<D, FTX, FTY>(buf, [&](int c) { return P.k(c, v.n); }, p, x0, y0, v);
+        cp_own<D, FTX, FTY>(own, [&](int c) { return P.a(c, D, v.n); }, p + 1, x0, y0, v);
+        cp_commit();
     }
 }
 
-template <int D, int NEW, int MID, int OLD>
-__device__ __forceinline__ void fwd_step(FwdSlots<D> &S_, int p, int zb, int ze, float *smem,
-                                         const float *sB, const float *Kh, const float *Qh,
-                                         const Vol &v, int x0, int y0, int tx, int ty, int x,
-                                         int y, bool v0, bool v1, int s, float *SF, float *LSE,
-                                         unsigned long long *flag) {
-    constexpr int PLANE = D * FPY * FPX;
-    const int buf = (p - zb + 1) & 1;
-    cp_wait_all();
-    __syncthreads();
-    if (p + 1 <= ze)
-        stage_plane<D, FPY, FRL, FPX>(smem + (buf ^ 1) * PLANE,
-                                      [&](int c) { return Kh + (int64_t)c * v.n; }, p + 1, x0, y0,
-                                      v);
-    cp_commit();
-    const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
-    if (has_new) {
-        const int64_t off = (int64_t)(p + 1) * v.hw + (int64_t)y * v.h + x;
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-            S_.q[NEW][0][c] = v0 ? __ldg(Qh + (int64_t)c * v.n + off) * kLog2e : 0.0f;
-            S_.q[NEW][1][c] = v1 ? __ldg(Qh + (int64_t)c * v.n + off + 1) * kLog2e : 0.0f;
-        }
-        soft_init(S_.st[NEW][0]);
-        soft_init(S_.st[NEW][1]);
-    }
-    const float *P = smem + buf * PLANE;
-    if (has_new) fwd_slot_rows<D, -1>(S_.q[NEW], S_.st[NEW], P, sB, tx, ty);
-    if (has_mid) fwd_slot_rows<D, 0>(S_.q[MID], S_.st[MID], P, sB, tx, ty);
-    if (has_old) {
-        fwd_slot_rows<D, 1>(S_.q[OLD], S_.st[OLD], P, sB, tx, ty);
-        const int64_t off = (int64_t)(p - 1) * v.hw + (int64_t)y * v.h + x;
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            if (r == 0 ? !v0 : !v1) continue;
-            const Soft &t = S_.st[OLD][r];
-            const float inv = 1.0f / t.s;
-            float *sf = SF + 3 * (int64_t)s * v.n + off + r;
-            sf[0] = t.ax * inv;
-            sf[v.n] = t.ay * inv;
-            sf[2 * v.n] = t.az * inv;
-            LSE[(int64_t)s * v.n + off + r] = (t.m + __log2f(t.s)) * kLn2;
-            if (!isfinite(t.s) || t.mn == -INFINITY)
-                atomicMin(flag, (unsigned long long)s * (unsigned long long)v.n +
-                                    (unsigned long long)(off + r));
-        }
-    }
-}
-
-template <int D>
+template <int D, bool TMA>
 __global__ void __launch_bounds__(256, (D <= 6 ? 2 : 1))
-modet_fwd_tiled_k(const float *__restrict__ Q, const float *__restrict__ K,
-                  const float *__restrict__ B, Vol v, int zc, float *__restrict__ SF,
-                  float *__restrict__ LSE, unsigned long long *__restrict__ flag) {
-    constexpr int PLANE = D * FPY * FPX;
-    extern __shared__ __align__(16) float smem[];
-    float *sB = smem + 2 * PLANE;
+modet_fwd_tiled_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
+                  const float *__restrict__ K, const float *__restrict__ B, Vol v, int zc,
+                  float *__restrict__ SF, float *__restrict__ LSE,
+                  unsigned long long *__restrict__ flag) {
+    constexpr int BUF = D * (FG::HCH + FG::OCH);
+    extern __shared__ __align__(128) float smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * BUF);
+    float2 *sB2 = reinterpret_cast<float2 *>(smem + 2 * BUF + 8);
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int x0 = blockIdx.x * FTX, y0 = blockIdx.y * FTY;
     const int nzc = (v.l + zc - 1) / zc;
     const int s = blockIdx.z / nzc;
     const int zb = (blockIdx.z - s * nzc) * zc, ze = min(zb + zc, v.l);
-    const float *Kh = K + (int64_t)s * D * v.n;
-    const float *Qh = Q + (int64_t)s * D * v.n;
+    const Ptrs P{K + (int64_t)s * D * v.n, Q + (int64_t)s * D * v.n, nullptr, nullptr, nullptr};
     const int x = x0 + 2 * tx, y = y0 + ty;
     const bool v0 = y < v.w && x < v.h, v1 = y < v.w && x + 1 < v.h;
-    if (threadIdx.x < 27) sB[threadIdx.x] = B[s * 27 + threadIdx.x] * kLog2e;
-    stage_plane<D, FPY, FRL, FPX>(smem, [&](int c) { return Kh + (int64_t)c * v.n; }, zb - 1,
-                                  x0, y0, v);
-    cp_commit();
+    load_bias2(sB2, B, s);
+    if (TMA) init_bars(bar);
+    __syncthreads();
+    fwd_stage<D, TMA>(smem, maps, &bar[0], zb - 1, x0, y0, s, P, v);
     FwdSlots<D> S_;
-    for (int t = 0;; t += 3) {
-        const int p = zb - 1 + t;
-        if (p > ze) break;
-        fwd_step<D, 0, 2, 1>(S_, p, zb, ze, smem, sB, Kh, Qh, v, x0, y0, tx, ty, x, y, v0, v1,
-                             s, SF, LSE, flag);
-        if (p + 1 > ze) break;
-        fwd_step<D, 1, 0, 2>(S_, p + 1, zb, ze, smem, sB, Kh, Qh, v, x0, y0, tx, ty, x, y, v0,
-                             v1, s, SF, LSE, flag);
-        if (p + 2 > ze) break;
-        fwd_step<D, 2, 1, 0>(S_, p + 2, zb, ze, smem, sB, Kh, Qh, v, x0, y0, tx, ty, x, y, v0,
-                             v1, s, SF, LSE, flag);
-    }
+    march(zb, ze, [&](int p, auto NEW_, auto MID_, auto OLD_) {
+        constexpr int NEW = decltype(NEW_)::value, MID = decltype(MID_)::value,
+                      OLD = decltype(OLD_)::value;
+        const int j = p - zb + 1, b = j & 1;
+        if (TMA) mbar_wait(&bar[b], (j >> 1) & 1);
+        else cp_wait_all();
+        __syncthreads();
+        if (p + 1 <= ze)
+            fwd_stage<D, TMA>(smem + (b ^ 1) * BUF, maps, &bar[b ^ 1], p + 1, x0, y0, s, P, v);
+        const float *buf = smem + b * BUF;
+        const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
+        if (has_new) {
+            const float *own = buf + D * FG::HCH + ty * FTX + 2 * tx;
+#pragma unroll
+            for (int c = 0; c < D; ++c)
+                S_.q[NEW][c] = mul2(*reinterpret_cast<const float2 *>(own + c * FG::OCH),
+                                    dup2(kLog2e));
+            S_.st[NEW].mn = dup2(INFINITY);
+        }
+#pragma unroll
+        for (int dyi = 0; dyi < 3; ++dyi) {
+            Strip ks[D];
+#pragma unroll
+            for (int c = 0; c < D; ++c) ks[c] = strip(buf + c * FG::HCH + (ty + dyi) * kBoxX, tx);
+            // slot z sees plane p at window offset dz = p - z; the new slot's
+            // very first row initialises its softmax state
+            if (dyi == 0) {
+                if (has_new) fwd_slot<D, 0, -1, true>(S_.q[NEW], S_.st[NEW], ks, sB2);
+                if (has_mid) fwd_slot<D, 0, 0, false>(S_.q[MID], S_.st[MID], ks, sB2);
+                if (has_old) fwd_slot<D, 0, 1, false>(S_.q[OLD], S_.st[OLD], ks, sB2);
+            } else if (dyi == 1) {
+                if (has_new) fwd_slot<D, 1, -1, false>(S_.q[NEW], S_.st[NEW], ks, sB2);
+                if (has_mid) fwd_slot<D, 1, 0, false>(S_.q[MID], S_.st[MID], ks, sB2);
+                if (has_old) fwd_slot<D, 1, 1, false>(S_.q[OLD], S_.st[OLD], ks, sB2);
+            } else {
+                if (has_new) fwd_slot<D, 2, -1, false>(S_.q[NEW], S_.st[NEW], ks, sB2);
+                if (has_mid) fwd_slot<D, 2, 0, false>(S_.q[MID], S_.st[MID], ks, sB2);
+                if (has_old) fwd_slot<D, 2, 1, false>(S_.q[OLD], S_.st[OLD], ks, sB2);
+            }
+        }
+        if (has_old) {
+            const int64_t off = (int64_t)(p - 1) * v.hw + (int64_t)y * v.h + x;
+            const Soft2 &t = S_.st[OLD];
+            const float2 inv = f2(1.0f / t.s.x, 1.0f / t.s.y);
+            const float2 sx = mul2(t.ax, inv), sy = mul2(t.ay, inv), sz = mul2(t.az, inv);
+            const float2 lse = f2((t.m.x + __log2f(t.s.x)) * kLn2, (t.m.y + __log2f(t.s.y)) * kLn2);
+            float *sf = SF + 3 * (int64_t)s * v.n + off;
+            float *ls = LSE + (int64_t)s * v.n + off;
+            if (v0) {
+                sf[0] = sx.x;
+                sf[v.n] = sy.x;
+                sf[2 * v.n] = sz.x;
+                ls[0] = lse.x;
+            }
+            if (v1) {
+                sf[1] = sx.y;
+                sf[v.n + 1] = sy.y;
+                sf[2 * v.n + 1] = sz.y;
+                ls[1] = lse.y;
+            }
+            const bool bad0 = v0 && (!isfinite(t.s.x) || t.mn.x == -INFINITY);
+            const bool bad1 = v1 && (!isfinite(t.s.y) || t.mn.y == -INFINITY);
+            if (bad0 || bad1)
+                atomicMin(flag, (unsigned long long)((int64_t)s * v.n + off + (bad0 ? 0 : 1)));
+        }
+    });
 }
 
 // ================================================================ bwd: rows
-// p as query.  Tile 32 x 8, one voxel per thread, 3 in-flight z slots.
+// p as query.  Tile 32 x 8, one voxel per thread, 3 in-flight z slots;
+// channels processed in packed pairs.
 constexpr int RTX = 32, RTY = 8;
-constexpr int RRL = RTX + 2, RPX = 36, RPY = RTY + 2;
+using RG = Geo<RTX, RTY>;
 
 template <int D>
 struct RowSlots {
-    float q[3][D];   // q * log2e
-    float dq[3][D];
-    float L[3];      // LSE * log2e
+    static constexpr int D2 = (D + 1) / 2;
+    float2 q[3][D2];  // channel pairs of q * log2e (odd D: last .y = 0)
+    float2 dq[3][D2];
+    float L[3];  // LSE * log2e
     float gx[3], gy[3], gz[3], dot[3];
 };
 
-template <int D, int DZ>
-__device__ __forceinline__ void row_slot_rows(RowSlots<D> &R, int j, float (&db)[27],
-                                              const float *P, const float *sB, int tx, int ty) {
+template <int D, int DYI, int DZ>
+__device__ __forceinline__ void row_slot(RowSlots<D> &R, int j, float (&db)[27],
+                                         const float2 (&kr)[(D + 1) / 2][3], const float2 *sB2) {
+    constexpr int D2 = (D + 1) / 2;
+    constexpr int ob = (DZ + 1) * 9 + DYI * 3;
+    // gSF.off(o) - gSF.SF without the x term
+    float cb = -R.dot[j];
+    if (DZ > 0) cb += R.gz[j];
+    if (DZ < 0) cb -= R.gz[j];
+    if (DYI == 0) cb -= R.gy[j];
+    if (DYI == 2) cb += R.gy[j];
 #pragma unroll
-    for (int dyi = 0; dyi < 3; ++dyi) {
-        constexpr int dummy = 0;
-        (void)dummy;
-        float kr[D][3];
-        const float *rowp = P + (ty + dyi) * RPX + tx;
+    for (int dxi = 0; dxi < 3; ++dxi) {
+        float2 acc = f2(sB2[ob + dxi].x, 0.0f);
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-            kr[c][0] = rowp[c * RPY * RPX];
-            kr[c][1] = rowp[c * RPY * RPX + 1];
-            kr[c][2] = rowp[c * RPY * RPX + 2];
-        }
-        const int ob = (DZ + 1) * 9 + dyi * 3;
-        // coefficient gSF.off(o) - gSF.SF without the x term
-        float cb = (DZ > 0 ? R.gz[j] : (DZ < 0 ? -R.gz[j] : 0.0f)) - R.dot[j];
-        if (dyi == 0) cb -= R.gy[j];
-        if (dyi == 2) cb += R.gy[j];
+        for (int c = 0; c < D2; ++c) acc = fma2(R.q[j][c], kr[c][dxi], acc);
+        const float W = ex2(acc.x + acc.y - R.L[j]);
+        const float cf = dxi == 0 ? cb - R.gx[j] : (dxi == 2 ? cb + R.gx[j] : cb);
+        const float dl = W * cf;
+        db[ob + dxi] += dl;
+        const float2 dl2 = dup2(dl);
 #pragma unroll
-        for (int dxi = 0; dxi < 3; ++dxi) {
-            float lg = sB[ob + dxi];
-#pragma unroll
-            for (int c = 0; c < D; ++c) lg = fmaf(R.q[j][c], kr[c][dxi], lg);
-            const float W = ex2(lg - R.L[j]);
-            const float cf = dxi == 0 ? cb - R.gx[j] : (dxi == 2 ? cb + R.gx[j] : cb);
-            const float dl = W * cf;
-            db[ob + dxi] += dl;
-#pragma unroll
-            for (int c = 0; c < D; ++c) R.dq[j][c] = fmaf(dl, kr[c][dxi], R.dq[j][c]);
-        }
+        for (int c = 0; c < D2; ++c) R.dq[j][c] = fma2(dl2, kr[c][dxi], R.dq[j][c]);
     }
 }
 
-template <int D, bool ACC, int NEW, int MID, int OLD>
-__device__ __forceinline__ void row_step(RowSlots<D> &R, float (&db)[27], int p, int zb, int ze,
-                                         float *smem, const float *sB, const float *Kh,
-                                         const float *Qh, const float *LSEh, const float *gSFh,
-                                         const float *SFh, const Vol &v, int x0, int y0, int tx,
-                                         int ty, int x, int y, bool vv, float *gQh) {
-    constexpr int PLANE = D * RPY * RPX;
-    const int buf = (p - zb + 1) & 1;
-    cp_wait_all();
-    __syncthreads();
-    if (p + 1 <= ze)
-        stage_plane<D, RPY, RRL, RPX>(smem + (buf ^ 1) * PLANE,
-                                      [&](int c) { return Kh + (int64_t)c * v.n; }, p + 1, x0, y0,
-                                      v);
-    cp_commit();
-    const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
-    if (has_new) {
-        const int64_t off = (int64_t)(p + 1) * v.hw + (int64_t)y * v.h + x;
-        if (vv) {
+template <int D, bool TMA>
+__device__ __forceinline__ void row_stage(float *buf, const Maps &m, uint64_t *bar, int p,
+                                          int x0, int y0, int s, const Ptrs &P, const Vol &v) {
+    float *own = buf + D * RG::HCH;
+    if (TMA) {
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(bar, (D * RG::PY * kBoxX + (D + 7) * RG::OCH) * 4);
 #pragma unroll
             for (int c = 0; c < D; ++c) {
-                R.q[NEW][c] = __ldg(Qh + (int64_t)c * v.n + off) * kLog2e;
-                R.dq[NEW][c] = 0.0f;
+                tma4(buf + c * RG::HCH, &m.k, x0 - 4, y0 - 1, p, s * D + c, bar);
+                tma4(own + c * RG::OCH, &m.a.q, x0, y0, p + 1, s * D + c, bar);
             }
-            R.L[NEW] = __ldg(LSEh + off) * kLog2e;
-            const float gx = __ldg(gSFh + off), gy = __ldg(gSFh + v.n + off),
-                        gz = __ldg(gSFh + 2 * v.n + off);
-            R.gx[NEW] = gx;
-            R.gy[NEW] = gy;
-            R.gz[NEW] = gz;
-            R.dot[NEW] = gx * __ldg(SFh + off) + gy * __ldg(SFh + v.n + off) +
-                         gz * __ldg(SFh + 2 * v.n + off);
-        } else {
+            tma4(own + D * RG::OCH, &m.a.lse, x0, y0, p + 1, s, bar);
 #pragma unroll
-            for (int c = 0; c < D; ++c) R.q[NEW][c] = R.dq[NEW][c] = 0.0f;
-            R.L[NEW] = 0.0f;
-            R.gx[NEW] = R.gy[NEW] = R.gz[NEW] = R.dot[NEW] = 0.0f;  // => dl == 0
-        }
-    }
-    const float *P = smem + buf * PLANE;
-    if (has_new) row_slot_rows<D, -1>(R, NEW, db, P, sB, tx, ty);
-    if (has_mid) row_slot_rows<D, 0>(R, MID, db, P, sB, tx, ty);
-    if (has_old) {
-        row_slot_rows<D, 1>(R, OLD, db, P, sB, tx, ty);
-        if (vv && gQh) {
-            const int64_t off = (int64_t)(p - 1) * v.hw + (int64_t)y * v.h + x;
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-                float *dst = gQh + (int64_t)c * v.n + off;
-                // dl was formed from log2-domain logits: d/dq = log2e-free since
-                // the exponent uses q*log2e*k = (q.k)*log2e; the derivative of
-                // exp(q.k) wrt q is exp(.)*k — no extra factor.
-                *dst = ACC ? *dst + R.dq[OLD][c] : R.dq[OLD][c];
+            for (int c = 0; c < 3; ++c) {
+                tma4(own + (D + 1 + c) * RG::OCH, &m.a.g, x0, y0, p + 1, 3 * s + c, bar);
+                tma4(own + (D + 4 + c) * RG::OCH, &m.a.sf, x0, y0, p + 1, 3 * s + c, bar);
             }
         }
+    } else {
+        cp_halo<D, RTX, RTY>(buf, [&](int c) { return P.k(c, v.n); }, p, x0, y0, v);
+        cp_own<D + 7, RTX, RTY>(own, [&](int c) { return P.a(c, D, v.n); }, p + 1, x0, y0, v);
+        cp_commit();
     }
 }
 
-template <int D, bool ACC>
+template <int D, bool TMA, bool ACC>
 __global__ void __launch_bounds__(256, (D <= 6 ? 2 : 1))
-modet_bwd_row_k(const float *__restrict__ Q, const float *__restrict__ K,
-                const float *__restrict__ B, const float *__restrict__ SF,
-                const float *__restrict__ LSE, const float *__restrict__ gSF, Vol v, int zc,
-                float *__restrict__ gQ, float *__restrict__ gBpart) {
-    constexpr int PLANE = D * RPY * RPX;
-    extern __shared__ __align__(16) float smem[];
-    float *sB = smem + 2 * PLANE;
+modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
+                const float *__restrict__ K, const float *__restrict__ B,
+                const float *__restrict__ SF, const float *__restrict__ LSE,
+                const float *__restrict__ gSF, Vol v, int zc, float *__restrict__ gQ,
+                float *__restrict__ gBpart) {
+    constexpr int D2 = (D + 1) / 2;
+    constexpr int BUF = D * RG::HCH + (D + 7) * RG::OCH;
+    extern __shared__ __align__(128) float smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * BUF);
+    float2 *sB2 = reinterpret_cast<float2 *>(smem + 2 * BUF + 8);
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int x0 = blockIdx.x * RTX, y0 = blockIdx.y * RTY;
     const int nzc = (v.l + zc - 1) / zc;
     const int s = blockIdx.z / nzc;
     const int zb = (blockIdx.z - s * nzc) * zc, ze = min(zb + zc, v.l);
     const int64_t so = (int64_t)s * v.n;
-    const float *Kh = K + so * D, *Qh = Q + so * D;
-    const float *LSEh = LSE + so, *gSFh = gSF + 3 * so, *SFh = SF + 3 * so;
+    const Ptrs P{K + so * D, Q + so * D, LSE + so, gSF + 3 * so, SF + 3 * so};
     float *gQh = gQ ? gQ + so * D : nullptr;
     const int x = x0 + tx, y = y0 + ty;
     const bool vv = x < v.h && y < v.w;
-    if (threadIdx.x < 27) sB[threadIdx.x] = B[s * 27 + threadIdx.x] * kLog2e;
-    stage_plane<D, RPY, RRL, RPX>(smem, [&](int c) { return Kh + (int64_t)c * v.n; }, zb - 1, x0,
-                                  y0, v);
-    cp_commit();
+    load_bias2(sB2, B, s);
+    if (TMA) init_bars(bar);
+    __syncthreads();
+    row_stage<D, TMA>(smem, maps, &bar[0], zb - 1, x0, y0, s, P, v);
     RowSlots<D> R;
     float db[27];
 #pragma unroll
     for (int o = 0; o < 27; ++o) db[o] = 0.0f;
-    for (int t = 0;; t += 3) {
-        const int p = zb - 1 + t;
-        if (p > ze) break;
-        row_step<D, ACC, 0, 2, 1>(R, db, p, zb, ze, smem, sB, Kh, Qh, LSEh, gSFh, SFh, v, x0, y0,
-                                  tx, ty, x, y, vv, gQh);
-        if (p + 1 > ze) break;
-        row_step<D, ACC, 1, 0, 2>(R, db, p + 1, zb, ze, smem, sB, Kh, Qh, LSEh, gSFh, SFh, v, x0,
-                                  y0, tx, ty, x, y, vv, gQh);
-        if (p + 2 > ze) break;
-        row_step<D, ACC, 2, 1, 0>(R, db, p + 2, zb, ze, smem, sB, Kh, Qh, LSEh, gSFh, SFh, v, x0,
-                                  y0, tx, ty, x, y, vv, gQh);
-    }
+    march(zb, ze, [&](int p, auto NEW_, auto MID_, auto OLD_) {
+        constexpr int NEW = decltype(NEW_)::value, MID = decltype(MID_)::value,
+                      OLD = decltype(OLD_)::value;
+        const int j = p - zb + 1, b = j & 1;
+        if (TMA) mbar_wait(&bar[b], (j >> 1) & 1);
+        else cp_wait_all();
+        __syncthreads();
+        if (p + 1 <= ze)
+            row_stage<D, TMA>(smem + (b ^ 1) * BUF, maps, &bar[b ^ 1], p + 1, x0, y0, s, P, v);
+        const float *buf = smem + b * BUF;
+        const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
+        if (has_new) {
+            // own data of the voxel entering the window; zero outside the
+            // volume (TMA / cp.async zero fill) => dl == 0 there
+            const float *own = buf + D * RG::HCH + ty * RTX + tx;
+#pragma unroll
+            for (int c = 0; c < D2; ++c) {
+                const float a = own[(2 * c) * RG::OCH];
+                const float bq = 2 * c + 1 < D ? own[(2 * c + 1) * RG::OCH] : 0.0f;
+                R.q[NEW][c] = mul2(f2(a, bq), dup2(kLog2e));
+                R.dq[NEW][c] = f2(0.0f, 0.0f);
+            }
+            R.L[NEW] = own[D * RG::OCH] * kLog2e;
+            const float gx = own[(D + 1) * RG::OCH], gy = own[(D + 2) * RG::OCH],
+                        gz = own[(D + 3) * RG::OCH];
+            R.gx[NEW] = gx;
+            R.gy[NEW] = gy;
+            R.gz[NEW] = gz;
+            R.dot[NEW] = gx * own[(D + 4) * RG::OCH] + gy * own[(D + 5) * RG::OCH] +
+                         gz * own[(D + 6) * RG::OCH];
+        }
+#pragma unroll
+        for (int dyi = 0; dyi < 3; ++dyi) {
+            float2 kr[D2][3];
+#pragma unroll
+            for (int c = 0; c < D2; ++c) {
+                const float *e0 = buf + (2 * c) * RG::HCH + (ty + dyi) * kBoxX + kXOff + tx;
+                const float *e1 = e0 + RG::HCH;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) kr[c][i] = f2(e0[i], 2 * c + 1 < D ? e1[i] : 0.0f);
+            }
+            if (dyi == 0) {
+                if (has_new) row_slot<D, 0, -1>(R, NEW, db, kr, sB2);
+                if (has_mid) row_slot<D, 0, 0>(R, MID, db, kr, sB2);
+                if (has_old) row_slot<D, 0, 1>(R, OLD, db, kr, sB2);
+            } else if (dyi == 1) {
+                if (has_new) row_slot<D, 1, -1>(R, NEW, db, kr, sB2);
+                if (has_mid) row_slot<D, 1, 0>(R, MID, db, kr, sB2);
+                if (has_old) row_slot<D, 1, 1>(R, OLD, db, kr, sB2);
+            } else {
+                if (has_new) row_slot<D, 2, -1>(R, NEW, db, kr, sB2);
+                if (has_mid) row_slot<D, 2, 0>(R, MID, db, kr, sB2);
+                if (has_old) row_slot<D, 2, 1>(R, OLD, db, kr, sB2);
+            }
+        }
+        if (has_old && vv && gQh) {
+            const int64_t off = (int64_t)(p - 1) * v.hw + (int64_t)y * v.h + x;
+#pragma unroll
+            for (int c = 0; c < D2; ++c) {
+                float *d0 = gQh + (int64_t)(2 * c) * v.n + off;
+                *d0 = ACC ? *d0 + R.dq[OLD][c].x : R.dq[OLD][c].x;
+                if (2 * c + 1 < D) {
+                    float *d1 = d0 + v.n;
+                    *d1 = ACC ? *d1 + R.dq[OLD][c].y : R.dq[OLD][c].y;
+                }
+            }
+        }
+    });
     // dB: warp shuffle reduce, then across warps; one partial per CTA
-    cp_wait_all();
+    if (!TMA) cp_wait_all();
     __syncthreads();
     float *red = smem;  // reuse: [8 warps][27]
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -409,183 +608,193 @@ modet_bwd_row_k(const float *__restrict__ Q, const float *__restrict__ K,
 }
 
 // ============================================================= bwd: columns
-// q as key.  Tile 32 x 16 (16 threads x 2 voxels), 3 in-flight z slots.
-// Staged source planes: Q (D channels), LSE, gSF (3), SF (3) -> after landing
-// the SF x-plane is overwritten with dot = gSF.SF (one transform pass).
-constexpr int CTX = 32, CTY = 16;
-constexpr int CRL = CTX + 2, CPX = 36, CPY = CTY + 2;
+// q as key.  Tile 32 x 8, one key voxel per thread (consecutive lanes read
+// consecutive smem columns: conflict-free), channels in packed pairs, 3
+// in-flight z slots.  Staged source records (set A halo): Q (D ch), LSE,
+// gSF (3), SF (3); one transform pass per plane turns LSE into LSE*log2e and
+// SF_x into dot = gSF.SF.
+constexpr int CTX = 32, CTY = 8;
+using CG = Geo<CTX, CTY>;
 
 template <int D>
 struct ColSlots {
-    float k[3][2][D];  // k * log2e
-    float dk[3][2][D];
+    static constexpr int D2 = (D + 1) / 2;
+    float2 k[3][D2];  // channel pairs of k * log2e (odd D: last .y = 0)
+    float2 dk[3][D2];
 };
 
-template <int D, int DZ>
-__device__ __forceinline__ void col_slot_rows(float (&k)[2][D], float (&dk)[2][D], const float *P,
-                                              const float *sB, int tx, int ty) {
-    constexpr int CH = CPY * CPX;
-    // window slot o = (dx,dy,dz) links source r = q - off(o) to key q
+template <int D>
+struct SrcStrip {
+    static constexpr int D2 = (D + 1) / 2;
+    float2 q[D2][3];  // channel pairs of the 3 sources x-1, x, x+1
+    float L[3], gx[3], gy[3], gz[3], dt[3];
+};
+
+template <int D, int DYI, int DZ>
+__device__ __forceinline__ void col_slot(ColSlots<D> &C_, int j, const SrcStrip<D> &S,
+                                         const float2 *sB2) {
+    constexpr int D2 = (D + 1) / 2;
+    constexpr int ob = (DZ + 1) * 9 + DYI * 3;
+    // window slot o = (dx,dy,dz) links source r = q - off(o) to key q: the
+    // source is strip element si = 1 - dx = 2 - dxi
 #pragma unroll
-    for (int dyi = 0; dyi < 3; ++dyi) {
-        // sources at row (ty+1) - (dyi-1) = ty + 2 - dyi, x = 2tx-1 .. 2tx+2
-        const float *rowp = P + (ty + 2 - dyi) * CPX + 2 * tx;
-        float qs[D][4];
+    for (int dxi = 0; dxi < 3; ++dxi) {
+        const int si = 2 - dxi;
+        float2 acc = f2(sB2[ob + dxi].x, 0.0f);
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-            const float2 a = *reinterpret_cast<const float2 *>(rowp + c * CH);
-            const float2 b = *reinterpret_cast<const float2 *>(rowp + c * CH + 2);
-            qs[c][0] = a.x;
-            qs[c][1] = a.y;
-            qs[c][2] = b.x;
-            qs[c][3] = b.y;
-        }
-        float L[4], gx[4], cb[4];
+        for (int c = 0; c < D2; ++c) acc = fma2(S.q[c][si], C_.k[j][c], acc);
+        const float W = ex2(acc.x + acc.y - S.L[si]);
+        // gSF_r.off(o) - gSF_r.SF_r
+        float cf = -S.dt[si];
+        if (DYI == 0) cf -= S.gy[si];
+        if (DYI == 2) cf += S.gy[si];
+        if (DZ < 0) cf -= S.gz[si];
+        if (DZ > 0) cf += S.gz[si];
+        if (dxi == 0) cf -= S.gx[si];
+        if (dxi == 2) cf += S.gx[si];
+        const float2 dl2 = dup2(W * cf);
 #pragma unroll
-        for (int i = 0; i < 4; i += 2) {
-            const float2 l2 = *reinterpret_cast<const float2 *>(rowp + D * CH + i);
-            const float2 gx2 = *reinterpret_cast<const float2 *>(rowp + (D + 1) * CH + i);
-            const float2 gy2 = *reinterpret_cast<const float2 *>(rowp + (D + 2) * CH + i);
-            const float2 gz2 = *reinterpret_cast<const float2 *>(rowp + (D + 3) * CH + i);
-            const float2 dt2 = *reinterpret_cast<const float2 *>(rowp + (D + 4) * CH + i);
-            L[i] = l2.x * kLog2e;
-            L[i + 1] = l2.y * kLog2e;
-            gx[i] = gx2.x;
-            gx[i + 1] = gx2.y;
-            // gSF.off(o) - dot without the x term, for this (dy, dz)
-            float c0 = -dt2.x, c1 = -dt2.y;
-            if (dyi == 0) { c0 -= gy2.x; c1 -= gy2.y; }
-            if (dyi == 2) { c0 += gy2.x; c1 += gy2.y; }
-            if (DZ < 0) { c0 -= gz2.x; c1 -= gz2.y; }
-            if (DZ > 0) { c0 += gz2.x; c1 += gz2.y; }
-            cb[i] = c0;
-            cb[i + 1] = c1;
-        }
-        const int ob = (DZ + 1) * 9 + dyi * 3;
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-#pragma unroll
-            for (int dxi = 0; dxi < 3; ++dxi) {
-                const int si = r + 2 - dxi;  // source x index in the strip
-                float lg = sB[ob + dxi];
-#pragma unroll
-                for (int c = 0; c < D; ++c) lg = fmaf(qs[c][si], k[r][c], lg);
-                const float W = ex2(lg - L[si]);
-                const float cf = dxi == 0 ? cb[si] - gx[si] : (dxi == 2 ? cb[si] + gx[si] : cb[si]);
-                const float dl = W * cf;
-#pragma unroll
-                for (int c = 0; c < D; ++c) dk[r][c] = fmaf(dl, qs[c][si], dk[r][c]);
-            }
-        }
+        for (int c = 0; c < D2; ++c) C_.dk[j][c] = fma2(dl2, S.q[c][si], C_.dk[j][c]);
     }
 }
 
-template <int D, bool ACC, int NEW, int MID, int OLD>
-__device__ __forceinline__ void col_step(ColSlots<D> &C_, int p, int zb, int ze, float *smem,
-                                         const float *sB, const float *Kh, const float *Qh,
-                                         const float *LSEh, const float *gSFh, const float *SFh,
-                                         const Vol &v, int x0, int y0, int tx, int ty, int x,
-                                         int y, bool v0, bool v1, float *gKh) {
-    constexpr int NCH = D + 7;
-    constexpr int CH = CPY * CPX;
-    constexpr int PLANE = NCH * CH;
-    const int buf = (p - zb + 1) & 1;
-    cp_wait_all();
-    __syncthreads();
-    // transform the landed plane: dot = gSF . SF into channel D+4
-    {
-        float *P = smem + buf * PLANE;
-        for (int i = threadIdx.x; i < CPY * CRL; i += blockDim.x) {
-            const int ry = i / CRL, rx = i - ry * CRL;
-            float *e = P + ry * CPX + rx;
-            e[(D + 4) * CH] = e[(D + 1) * CH] * e[(D + 4) * CH] + e[(D + 2) * CH] * e[(D + 5) * CH] +
-                              e[(D + 3) * CH] * e[(D + 6) * CH];
-        }
-    }
-    auto base = [&](int c) -> const float * {
-        if (c < D) return Qh + (int64_t)c * v.n;
-        if (c == D) return LSEh;
-        if (c < D + 4) return gSFh + (int64_t)(c - D - 1) * v.n;
-        return SFh + (int64_t)(c - D - 4) * v.n;
-    };
-    if (p + 1 <= ze)
-        stage_plane<NCH, CPY, CRL, CPX>(smem + (buf ^ 1) * PLANE, base, p + 1, x0, y0, v);
-    cp_commit();
-    __syncthreads();  // transform visible
-    const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
-    if (has_new) {
-        const int64_t off = (int64_t)(p + 1) * v.hw + (int64_t)y * v.h + x;
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-            C_.k[NEW][0][c] = v0 ? __ldg(Kh + (int64_t)c * v.n + off) * kLog2e : 0.0f;
-            C_.k[NEW][1][c] = v1 ? __ldg(Kh + (int64_t)c * v.n + off + 1) * kLog2e : 0.0f;
-            C_.dk[NEW][0][c] = C_.dk[NEW][1][c] = 0.0f;
-        }
-    }
-    const float *P = smem + buf * PLANE;
-    // key z = p+1 sees sources in plane p at dz = -1 ... wait: o = q - r, so a
-    // source plane p below the key (p = z-1) is window offset dz = +1
-    if (has_new) col_slot_rows<D, 1>(C_.k[NEW], C_.dk[NEW], P, sB, tx, ty);
-    if (has_mid) col_slot_rows<D, 0>(C_.k[MID], C_.dk[MID], P, sB, tx, ty);
-    if (has_old) {
-        col_slot_rows<D, -1>(C_.k[OLD], C_.dk[OLD], P, sB, tx, ty);
-        if (gKh) {
-            const int64_t off = (int64_t)(p - 1) * v.hw + (int64_t)y * v.h + x;
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                if (r == 0 ? !v0 : !v1) continue;
-#pragma unroll
-                for (int c = 0; c < D; ++c) {
-                    float *dst = gKh + (int64_t)c * v.n + off + r;
-                    *dst = ACC ? *dst + C_.dk[OLD][r][c] : C_.dk[OLD][r][c];
-                }
-            }
-        }
+template <int D>
+__device__ __forceinline__ void col_transform(float *buf) {
+    constexpr int CH = CG::HCH;
+    for (int i = threadIdx.x; i < CG::PY * CG::RL; i += blockDim.x) {
+        const int ry = i / CG::RL, rx = i - ry * CG::RL;
+        float *e = buf + ry * kBoxX + kXOff + rx;
+        e[D * CH] *= kLog2e;
+        e[(D + 4) * CH] = e[(D + 1) * CH] * e[(D + 4) * CH] + e[(D + 2) * CH] * e[(D + 5) * CH] +
+                          e[(D + 3) * CH] * e[(D + 6) * CH];
     }
 }
 
-template <int D, bool ACC>
+template <int D, bool TMA>
+__device__ __forceinline__ void col_stage(float *buf, const Maps &m, uint64_t *bar, int p,
+                                          int x0, int y0, int s, const Ptrs &P, const Vol &v) {
+    float *own = buf + (D + 7) * CG::HCH;
+    if (TMA) {
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(bar, ((D + 7) * CG::PY * kBoxX + D * CG::OCH) * 4);
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                tma4(buf + c * CG::HCH, &m.a.q, x0 - 4, y0 - 1, p, s * D + c, bar);
+                tma4(own + c * CG::OCH, &m.k, x0, y0, p + 1, s * D + c, bar);
+            }
+            tma4(buf + D * CG::HCH, &m.a.lse, x0 - 4, y0 - 1, p, s, bar);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                tma4(buf + (D + 1 + c) * CG::HCH, &m.a.g, x0 - 4, y0 - 1, p, 3 * s + c, bar);
+                tma4(buf + (D + 4 + c) * CG::HCH, &m.a.sf, x0 - 4, y0 - 1, p, 3 * s + c, bar);
+            }
+        }
+    } else {
+        cp_halo<D + 7, CTX, CTY>(buf, [&](int c) { return P.a(c, D, v.n); }, p, x0, y0, v);
+        cp_own<D, CTX, CTY>(own, [&](int c) { return P.k(c, v.n); }, p + 1, x0, y0, v);
+        cp_commit();
+    }
+}
+
+template <int D, bool TMA, bool ACC>
 __global__ void __launch_bounds__(256, (D <= 6 ? 2 : 1))
-modet_bwd_col_k(const float *__restrict__ Q, const float *__restrict__ K,
-                const float *__restrict__ B, const float *__restrict__ SF,
-                const float *__restrict__ LSE, const float *__restrict__ gSF, Vol v, int zc,
-                float *__restrict__ gK) {
-    constexpr int PLANE = (D + 7) * CPY * CPX;
-    extern __shared__ __align__(16) float smem[];
-    float *sB = smem + 2 * PLANE;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
+                const float *__restrict__ K, const float *__restrict__ B,
+                const float *__restrict__ SF, const float *__restrict__ LSE,
+                const float *__restrict__ gSF, Vol v, int zc, float *__restrict__ gK) {
+    constexpr int D2 = (D + 1) / 2;
+    constexpr int BUF = (D + 7) * CG::HCH + D * CG::OCH;
+    extern __shared__ __align__(128) float smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * BUF);
+    float2 *sB2 = reinterpret_cast<float2 *>(smem + 2 * BUF + 8);
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int x0 = blockIdx.x * CTX, y0 = blockIdx.y * CTY;
     const int nzc = (v.l + zc - 1) / zc;
     const int s = blockIdx.z / nzc;
     const int zb = (blockIdx.z - s * nzc) * zc, ze = min(zb + zc, v.l);
     const int64_t so = (int64_t)s * v.n;
-    const float *Kh = K + so * D, *Qh = Q + so * D;
-    const float *LSEh = LSE + so, *gSFh = gSF + 3 * so, *SFh = SF + 3 * so;
+    const Ptrs P{K + so * D, Q + so * D, LSE + so, gSF + 3 * so, SF + 3 * so};
     float *gKh = gK + so * D;
-    const int x = x0 + 2 * tx, y = y0 + ty;
-    const bool v0 = y < v.w && x < v.h, v1 = y < v.w && x + 1 < v.h;
-    if (threadIdx.x < 27) sB[threadIdx.x] = B[s * 27 + threadIdx.x] * kLog2e;
-    auto base = [&](int c) -> const float * {
-        if (c < D) return Qh + (int64_t)c * v.n;
-        if (c == D) return LSEh;
-        if (c < D + 4) return gSFh + (int64_t)(c - D - 1) * v.n;
-        return SFh + (int64_t)(c - D - 4) * v.n;
-    };
-    stage_plane<D + 7, CPY, CRL, CPX>(smem, base, zb - 1, x0, y0, v);
-    cp_commit();
+    const int x = x0 + tx, y = y0 + ty;
+    const bool vv = x < v.h && y < v.w;
+    load_bias2(sB2, B, s);
+    if (TMA) init_bars(bar);
+    __syncthreads();
+    col_stage<D, TMA>(smem, maps, &bar[0], zb - 1, x0, y0, s, P, v);
     ColSlots<D> C_;
-    for (int t = 0;; t += 3) {
-        const int p = zb - 1 + t;
-        if (p > ze) break;
-        col_step<D, ACC, 0, 2, 1>(C_, p, zb, ze, smem, sB, Kh, Qh, LSEh, gSFh, SFh, v, x0, y0, tx,
-                                  ty, x, y, v0, v1, gKh);
-        if (p + 1 > ze) break;
-        col_step<D, ACC, 1, 0, 2>(C_, p + 1, zb, ze, smem, sB, Kh, Qh, LSEh, gSFh, SFh, v, x0, y0,
-                                  tx, ty, x, y, v0, v1, gKh);
-        if (p + 2 > ze) break;
-        col_step<D, ACC, 2, 1, 0>(C_, p + 2, zb, ze, smem, sB, Kh, Qh, LSEh, gSFh, SFh, v, x0, y0,
-                                  tx, ty, x, y, v0, v1, gKh);
-    }
+    march(zb, ze, [&](int p, auto NEW_, auto MID_, auto OLD_) {
+        constexpr int NEW = decltype(NEW_)::value, MID = decltype(MID_)::value,
+                      OLD = decltype(OLD_)::value;
+        const int j = p - zb + 1, b = j & 1;
+        if (TMA) mbar_wait(&bar[b], (j >> 1) & 1);
+        else cp_wait_all();
+        __syncthreads();
+        float *buf = smem + b * BUF;
+        col_transform<D>(buf);
+        // generic-proxy writes to a buffer the TMA (async proxy) refills later
+        if (TMA) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        if (p + 1 <= ze)
+            col_stage<D, TMA>(smem + (b ^ 1) * BUF, maps, &bar[b ^ 1], p + 1, x0, y0, s, P, v);
+        const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
+        if (has_new) {
+            const float *own = buf + (D + 7) * CG::HCH + ty * CTX + tx;
+#pragma unroll
+            for (int c = 0; c < D2; ++c) {
+                const float a = own[(2 * c) * CG::OCH];
+                const float bk = 2 * c + 1 < D ? own[(2 * c + 1) * CG::OCH] : 0.0f;
+                C_.k[NEW][c] = mul2(f2(a, bk), dup2(kLog2e));
+                C_.dk[NEW][c] = f2(0.0f, 0.0f);
+            }
+        }
+        __syncthreads();  // transform visible
+#pragma unroll
+        for (int dyi = 0; dyi < 3; ++dyi) {
+            // window row dy = dyi-1 links key row y to source row y - dy
+            const float *rowp = buf + (ty + 2 - dyi) * kBoxX + kXOff + tx;
+            SrcStrip<D> S;
+#pragma unroll
+            for (int c = 0; c < D2; ++c) {
+                const float *e0 = rowp + (2 * c) * CG::HCH;
+                const float *e1 = e0 + CG::HCH;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) S.q[c][i] = f2(e0[i], 2 * c + 1 < D ? e1[i] : 0.0f);
+            }
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                S.L[i] = rowp[D * CG::HCH + i];
+                S.gx[i] = rowp[(D + 1) * CG::HCH + i];
+                S.gy[i] = rowp[(D + 2) * CG::HCH + i];
+                S.gz[i] = rowp[(D + 3) * CG::HCH + i];
+                S.dt[i] = rowp[(D + 4) * CG::HCH + i];
+            }
+            // key z sees sources in plane p at window offset dz = z - p
+            if (dyi == 0) {
+                if (has_new) col_slot<D, 0, 1>(C_, NEW, S, sB2);
+                if (has_mid) col_slot<D, 0, 0>(C_, MID, S, sB2);
+                if (has_old) col_slot<D, 0, -1>(C_, OLD, S, sB2);
+            } else if (dyi == 1) {
+                if (has_new) col_slot<D, 1, 1>(C_, NEW, S, sB2);
+                if (has_mid) col_slot<D, 1, 0>(C_, MID, S, sB2);
+                if (has_old) col_slot<D, 1, -1>(C_, OLD, S, sB2);
+            } else {
+                if (has_new) col_slot<D, 2, 1>(C_, NEW, S, sB2);
+                if (has_mid) col_slot<D, 2, 0>(C_, MID, S, sB2);
+                if (has_old) col_slot<D, 2, -1>(C_, OLD, S, sB2);
+            }
+        }
+        if (has_old && vv) {
+            const int64_t off = (int64_t)(p - 1) * v.hw + (int64_t)y * v.h + x;
+#pragma unroll
+            for (int c = 0; c < D2; ++c) {
+                float *d0 = gKh + (int64_t)(2 * c) * v.n + off;
+                *d0 = ACC ? *d0 + C_.dk[OLD][c].x : C_.dk[OLD][c].x;
+                if (2 * c + 1 < D) {
+                    float *d1 = d0 + v.n;
+                    *d1 = ACC ? *d1 + C_.dk[OLD][c].y : C_.dk[OLD][c].y;
+                }
+            }
+        }
+    });
 }
 
 // deterministic final reduction of per-CTA dB partials (fixed order tree)
@@ -604,27 +813,100 @@ reduce_db_k(const float *__restrict__ part, int nparts, float *__restrict__ gB) 
     if (threadIdx.x == 0) gB[s * 27 + o] += sm[0];
 }
 
-// ------------------------------------------------------------- launchers
-static int pick_zc(int tiles, int l) {
-    // enough CTAs for ~4 per SM on 148 SMs, chunks of >= 8 planes
-    const int want = 148 * 4;
+// ------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// TMA usable: row pitch a multiple of 16 B, bases 16-B aligned, encoder found
+static bool tma_ok(const Vol &v, std::initializer_list<const void *> ptrs) {
+    if (v.h % 4 != 0 || !encoder()) return false;
+    for (const void *p : ptrs)
+        if (p && reinterpret_cast<uintptr_t>(p) % 16 != 0) return false;
+    return true;
+}
+
+// 4-D map over planar {nch, l, w, h} with a single-channel box {bx, by, 1, 1}
+static bool make_map(CUtensorMap *m, const float *base, const Vol &v, int nch, int bx, int by) {
+    const cuuint64_t dims[4] = {(cuuint64_t)v.h, (cuuint64_t)v.w, (cuuint64_t)v.l, (cuuint64_t)nch};
+    const cuuint64_t strides[3] = {(cuuint64_t)v.h * 4, (cuuint64_t)v.hw * 4, (cuuint64_t)v.n * 4};
+    const cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, 1, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    return encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(base), dims,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// set-A maps with box (bx, by)
+static bool make_maps_a(MapsA *m, const float *Q, const float *LSE, const float *gSF,
+                        const float *SF, const Vol &v, int S, int D, int bx, int by) {
+    return make_map(&m->q, Q, v, S * D, bx, by) && make_map(&m->lse, LSE, v, S, bx, by) &&
+           make_map(&m->g, gSF, v, 3 * S, bx, by) && make_map(&m->sf, SF, v, 3 * S, bx, by);
+}
+
+static int pick_zc(int tiles, int l, int per_sm) {
+    // enough CTAs for `per_sm` resident per SM on 148 SMs (x2 for balance),
+    // chunks of >= 8 planes
+    const int want = 148 * per_sm * 2;
     int nzc = (want + tiles - 1) / max(tiles, 1);
     nzc = max(1, min(nzc, (l + 7) / 8));
     return (l + nzc - 1) / nzc;
 }
+
+template <class KFn>
+static void set_smem(KFn k, size_t sm) {
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+}
+
+// shared memory: two buffers + 2 mbarriers (8 floats) + 27 bias pairs
+constexpr size_t kTail = 8 + 64;
 
 template <int D>
 static cudaError_t fwd_launch(const float *Q, const float *K, const float *B, mdg_dims3 d, int S,
                               float *SF, float *LSE, unsigned long long *flag, cudaStream_t st) {
     const Vol v{d.h, d.w, d.l, (int64_t)d.h * d.w * d.l, (int64_t)d.h * d.w};
     const int gx = (d.h + FTX - 1) / FTX, gy = (d.w + FTY - 1) / FTY;
-    const int zc = pick_zc(gx * gy * S, d.l);
+    const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 2 : 1);
     const int nzc = (d.l + zc - 1) / zc;
-    const size_t sm = (2 * D * FPY * FPX + 32) * sizeof(float);
-    auto k = modet_fwd_tiled_k<D>;
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<dim3(gx, gy, S * nzc), 256, sm, st>>>(Q, K, B, v, zc, SF, LSE, flag);
+    const size_t sm = (2 * D * (FG::HCH + FG::OCH) + kTail) * sizeof(float);
+    Maps m{};
+    const bool tma = tma_ok(v, {Q, K}) && make_map(&m.k, K, v, S * D, kBoxX, FG::PY) &&
+                     make_map(&m.a.q, Q, v, S * D, FTX, FTY);
+    const dim3 grid(gx, gy, S * nzc);
+    if (tma) {
+        set_smem(modet_fwd_tiled_k<D, true>, sm);
+        modet_fwd_tiled_k<D, true><<<grid, 256, sm, st>>>(m, Q, K, B, v, zc, SF, LSE, flag);
+    } else {
+        set_smem(modet_fwd_tiled_k<D, false>, sm);
+        modet_fwd_tiled_k<D, false><<<grid, 256, sm, st>>>(m, Q, K, B, v, zc, SF, LSE, flag);
+    }
     return cudaPeekAtLastError();
+}
+
+template <int D, bool TMA, bool ACC>
+static void row_launch(dim3 g, size_t sm, cudaStream_t st, const Maps &m, const float *Q,
+                       const float *K, const float *B, const float *SF, const float *LSE,
+                       const float *gSF, const Vol &v, int zc, float *gQ, float *part) {
+    set_smem(modet_bwd_row_k<D, TMA, ACC>, sm);
+    modet_bwd_row_k<D, TMA, ACC><<<g, 256, sm, st>>>(m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part);
+}
+
+template <int D, bool TMA, bool ACC>
+static void col_launch(dim3 g, size_t sm, cudaStream_t st, const Maps &m, const float *Q,
+                       const float *K, const float *B, const float *SF, const float *LSE,
+                       const float *gSF, const Vol &v, int zc, float *gK) {
+    set_smem(modet_bwd_col_k<D, TMA, ACC>, sm);
+    modet_bwd_col_k<D, TMA, ACC><<<g, 256, sm, st>>>(m, Q, K, B, SF, LSE, gSF, v, zc, gK);
 }
 
 template <int D>
@@ -632,18 +914,27 @@ static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, co
                               const float *LSE, const float *gSF, mdg_dims3 d, int S, bool acc,
                               float *gQ, float *gK, float *gB, cudaStream_t st) {
     const Vol v{d.h, d.w, d.l, (int64_t)d.h * d.w * d.l, (int64_t)d.h * d.w};
+    const bool tma = tma_ok(v, {Q, K, SF, LSE, gSF});
     cudaError_t e = cudaSuccess;
     if (gQ || gB) {
         const int gx = (d.h + RTX - 1) / RTX, gy = (d.w + RTY - 1) / RTY;
-        const int zc = pick_zc(gx * gy * S, d.l);
+        const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 2 : 1);
         const int nzc = (d.l + zc - 1) / zc;
         const int ncta = gx * gy * nzc;
         float *part = nullptr;
         if ((e = cudaMallocAsync(&part, (size_t)S * ncta * 27 * sizeof(float), st))) return e;
-        const size_t sm = (2 * D * RPY * RPX + 32) * sizeof(float);
-        auto k = acc ? modet_bwd_row_k<D, true> : modet_bwd_row_k<D, false>;
-        if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k<<<dim3(gx, gy, S * nzc), 256, sm, st>>>(Q, K, B, SF, LSE, gSF, v, zc, gQ, part);
+        const size_t sm = (2 * (D * RG::HCH + (D + 7) * RG::OCH) + kTail) * sizeof(float);
+        Maps m{};
+        const bool t = tma && make_map(&m.k, K, v, S * D, kBoxX, RG::PY) &&
+                       make_maps_a(&m.a, Q, LSE, gSF, SF, v, S, D, RTX, RTY);
+        const dim3 g(gx, gy, S * nzc);
+        if (t) {
+            if (acc) row_launch<D, true, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part);
+            else row_launch<D, true, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part);
+        } else {
+            if (acc) row_launch<D, false, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part);
+            else row_launch<D, false, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part);
+        }
         g_launches.fetch_add(1);
         if (gB) {
             reduce_db_k<<<dim3(27, S), 256, 0, st>>>(part, ncta, gB);
@@ -654,12 +945,20 @@ static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, co
     }
     if (gK) {
         const int gx = (d.h + CTX - 1) / CTX, gy = (d.w + CTY - 1) / CTY;
-        const int zc = pick_zc(gx * gy * S, d.l);
+        const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 2 : 1);
         const int nzc = (d.l + zc - 1) / zc;
-        const size_t sm = (2 * (D + 7) * CPY * CPX + 32) * sizeof(float);
-        auto k = acc ? modet_bwd_col_k<D, true> : modet_bwd_col_k<D, false>;
-        if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k<<<dim3(gx, gy, S * nzc), 256, sm, st>>>(Q, K, B, SF, LSE, gSF, v, zc, gK);
+        const size_t sm = (2 * ((D + 7) * CG::HCH + D * CG::OCH) + kTail) * sizeof(float);
+        Maps m{};
+        const bool t = tma && make_map(&m.k, K, v, S * D, CTX, CTY) &&
+                       make_maps_a(&m.a, Q, LSE, gSF, SF, v, S, D, kBoxX, CG::PY);
+        const dim3 g(gx, gy, S * nzc);
+        if (t) {
+            if (acc) col_launch<D, true, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK);
+            else col_launch<D, true, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK);
+        } else {
+            if (acc) col_launch<D, false, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK);
+            else col_launch<D, false, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK);
+        }
         g_launches.fetch_add(1);
         if ((e = cudaPeekAtLastError())) return e;
     }

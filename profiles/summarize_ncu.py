@@ -35,8 +35,8 @@ SCALE = {"ms": 1e-3, "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e
 
 
 def short(name):
-    m = re.match(r"(?:void )?(?:mdg::)?([A-Za-z0-9_]+)", name)
-    return m.group(1) if m else name
+    base = re.sub(r"^void ", "", name).split("(")[0].split("<")[0]
+    return base.split("::")[-1]
 
 
 def main(rep, launches, tag):
