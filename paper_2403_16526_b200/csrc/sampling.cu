@@ -95,8 +95,44 @@ __device__ __forceinline__ void xyz_of(int64_t p, int h, int w, int &x, int &y, 
     z = (int)(t / w);
 }
 
+// the 8 corner values of one channel plane (sampling.hpp:79-86 naming)
+struct Oct {
+    float v000, v100, v010, v110, v001, v101, v011, v111;
+};
+__device__ __forceinline__ Oct load_oct(const float *__restrict__ pl, const Corners &c) {
+    const int x0 = c.ax.i0, x1 = c.ax.i1;
+    return Oct{__ldg(pl + c.o00 + x0), __ldg(pl + c.o00 + x1), __ldg(pl + c.o10 + x0),
+               __ldg(pl + c.o10 + x1), __ldg(pl + c.o01 + x0), __ldg(pl + c.o01 + x1),
+               __ldg(pl + c.o11 + x0), __ldg(pl + c.o11 + x1)};
+}
+// sampling.hpp:53-68 on loaded corners
+__device__ __forceinline__ float lerp_oct(const Oct &o, const Corners &c) {
+    const float fx = c.ax.f;
+    const float c00 = lerp_(o.v000, o.v100, fx), c10 = lerp_(o.v010, o.v110, fx);
+    const float c01 = lerp_(o.v001, o.v101, fx), c11 = lerp_(o.v011, o.v111, fx);
+    return lerp_(lerp_(c00, c10, c.ay.f), lerp_(c01, c11, c.ay.f), c.az.f);
+}
+// sampling.hpp:73-99 on loaded corners
+__device__ __forceinline__ void grad_oct(const Oct &o, const Corners &c, float g[3]) {
+    const float fx = c.ax.f, fy = c.ay.f, fz = c.az.f;
+    const float gx = sub_(1.0f, fx), gy = sub_(1.0f, fy), gz = sub_(1.0f, fz);
+    g[0] = g[1] = g[2] = 0.0f;
+    if (c.ax.live)
+        g[0] = add_(mul_(add_(mul_(sub_(o.v100, o.v000), gy), mul_(sub_(o.v110, o.v010), fy)), gz),
+                    mul_(add_(mul_(sub_(o.v101, o.v001), gy), mul_(sub_(o.v111, o.v011), fy)), fz));
+    if (c.ay.live)
+        g[1] = add_(mul_(add_(mul_(sub_(o.v010, o.v000), gx), mul_(sub_(o.v110, o.v100), fx)), gz),
+                    mul_(add_(mul_(sub_(o.v011, o.v001), gx), mul_(sub_(o.v111, o.v101), fx)), fz));
+    if (c.az.live)
+        g[2] = add_(mul_(add_(mul_(sub_(o.v001, o.v000), gx), mul_(sub_(o.v101, o.v100), fx)), gy),
+                    mul_(add_(mul_(sub_(o.v011, o.v010), gx), mul_(sub_(o.v111, o.v110), fx)), fy));
+}
+
 // --------------------------------------------------------------- warp fwd
-// sampling.hpp:123-135
+// sampling.hpp:123-135.  CT > 0: channel count known at compile time, all
+// 8*CT corner loads issued before any interpolation (memory-level
+// parallelism); CT == 0: runtime channel loop.
+template <int CT>
 __global__ void __launch_bounds__(kSB)
 warp_fwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, float *__restrict__ out) {
@@ -107,41 +143,214 @@ warp_fwd_k(const float *__restrict__ in, int C, int h, int w, int l,
     xyz_of(p, h, w, x, y, z);
     const Corners c = corners_at(add_((float)x, __ldg(field + p)), add_((float)y, __ldg(field + n + p)),
                                  add_((float)z, __ldg(field + 2 * n + p)), h, w, l);
-    for (int ch = 0; ch < C; ++ch) out[ch * n + p] = sample(in + ch * n, c);
+    if (CT > 0) {
+        // 32-bit element offsets of the 4 corner rows (x0 corner; x1 = +1)
+        const int r00 = (int)(c.o00 + c.ax.i0), r10 = (int)(c.o10 + c.ax.i0);
+        const int r01 = (int)(c.o01 + c.ax.i0), r11 = (int)(c.o11 + c.ax.i0);
+        const float fx = c.ax.f, fy = c.ay.f, fz = c.az.f;
+        const float2 FX = make_float2(fx, fx), GX = make_float2(sub_(1.0f, fx), sub_(1.0f, fx));
+        const float2 FY = make_float2(fy, fy), GY = make_float2(sub_(1.0f, fy), sub_(1.0f, fy));
+        const float2 FZ = make_float2(fz, fz), GZ = make_float2(sub_(1.0f, fz), sub_(1.0f, fz));
+        // lerp a*(1-f) + b*f on channel pairs, each lane rounded like the
+        // reference's scalar code (sampling.hpp:61-67)
+        // (scalar _rn per lane: ptxas fuses packed mul+add into FFMA2 even for
+        // mul.rn.f32x2 / add.rn.f32x2, which would break bit-exactness)
+        auto lerp2 = [](float2 a, float2 b, float2 g, float2 f) {
+            return make_float2(add_(mul_(a.x, g.x), mul_(b.x, f.x)),
+                               add_(mul_(a.y, g.y), mul_(b.y, f.y)));
+        };
+#pragma unroll
+        for (int ch = 0; ch + 1 < CT; ch += 2) {
+            const float *a = in + (int64_t)ch * n, *b = a + n;
+            const float2 v000 = make_float2(__ldg(a + r00), __ldg(b + r00));
+            const float2 v100 = make_float2(__ldg(a + r00 + 1), __ldg(b + r00 + 1));
+            const float2 v010 = make_float2(__ldg(a + r10), __ldg(b + r10));
+            const float2 v110 = make_float2(__ldg(a + r10 + 1), __ldg(b + r10 + 1));
+            const float2 v001 = make_float2(__ldg(a + r01), __ldg(b + r01));
+            const float2 v101 = make_float2(__ldg(a + r01 + 1), __ldg(b + r01 + 1));
+            const float2 v011 = make_float2(__ldg(a + r11), __ldg(b + r11));
+            const float2 v111 = make_float2(__ldg(a + r11 + 1), __ldg(b + r11 + 1));
+            const float2 c0 = lerp2(lerp2(v000, v100, GX, FX), lerp2(v010, v110, GX, FX), GY, FY);
+            const float2 c1 = lerp2(lerp2(v001, v101, GX, FX), lerp2(v011, v111, GX, FX), GY, FY);
+            const float2 r = lerp2(c0, c1, GZ, FZ);
+            out[(int64_t)ch * n + p] = r.x;
+            out[(int64_t)(ch + 1) * n + p] = r.y;
+        }
+        if (CT & 1) {
+            const int ch = CT - 1;
+            out[(int64_t)ch * n + p] = lerp_oct(load_oct(in + (int64_t)ch * n, c), c);
+        }
+    } else {
+        for (int ch = 0; ch < C; ++ch) out[ch * n + p] = sample(in + ch * n, c);
+    }
+}
+
+// Warp-level merge of x-adjacent scatter targets: lanes hold x-consecutive
+// voxels, so for a smooth field lane t's x1 corner is usually lane t+1's x0
+// corner.  `in` = this lane absorbs lane t-1's x1 term, `out` = lane t+1
+// absorbed this lane's x1 term (row offsets r are channel independent).
+struct XMerge {
+    bool in[4], out[4];
+};
+__device__ __forceinline__ void xmerge_row(int r, bool ok, bool &in, bool &out) {
+    const int lane = threadIdx.x & 31;
+    const int key = ok ? r : -2 - lane;  // invalid lanes never match
+    const int up = __shfl_up_sync(0xffffffffu, ok ? r + 1 : -1, 1);
+    in = lane > 0 && ok && up == key;
+    out = __shfl_down_sync(0xffffffffu, (int)in, 1) != 0 && lane < 31;
+}
+__device__ __forceinline__ void scatter_row2(float *ia, float *ib, bool two, bool ok, int r,
+                                             float2 t0, float2 t1, bool in, bool out) {
+    const float nx = __shfl_up_sync(0xffffffffu, t1.x, 1);
+    const float ny = __shfl_up_sync(0xffffffffu, t1.y, 1);
+    if (in) {
+        t0.x += nx;
+        t0.y += ny;
+    }
+    if (ok) {
+        atomicAdd(ia + r, t0.x);
+        if (!out) atomicAdd(ia + r + 1, t1.x);
+        if (two) {
+            atomicAdd(ib + r, t0.y);
+            if (!out) atomicAdd(ib + r + 1, t1.y);
+        }
+    }
 }
 
 // --------------------------------------------------------------- warp bwd
-// sampling.hpp:139-167
+// sampling.hpp:139-167 (gfield: same per-channel order => bit-exact)
+template <int CT>
 __global__ void __launch_bounds__(kSB)
 warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, const float *__restrict__ gout,
            float *__restrict__ gin, float *__restrict__ gfield) {
     const int64_t n = (int64_t)h * w * l;
-    const int64_t p = (int64_t)blockIdx.x * kSB + threadIdx.x;
-    if (p >= n) return;
+    const int64_t p0 = (int64_t)blockIdx.x * kSB + threadIdx.x;
+    // CT > 0 keeps every lane alive for the warp-level scatter merge
+    const bool ok = p0 < n;
+    if (CT == 0 && !ok) return;
+    const int64_t p = ok ? p0 : 0;
     int x, y, z;
     xyz_of(p, h, w, x, y, z);
     const Corners c = corners_at(add_((float)x, __ldg(field + p)), add_((float)y, __ldg(field + n + p)),
                                  add_((float)z, __ldg(field + 2 * n + p)), h, w, l);
     float gx = 0.0f, gy = 0.0f, gz = 0.0f;
-    for (int ch = 0; ch < C; ++ch) {
-        const float g = __ldg(gout + ch * n + p);
-        if (g == 0.0f) continue;
-        if (gin) scatter(gin + ch * n, c, g);
-        if (gfield) {
-            float cg[3];
-            sample_grad(in + ch * n, c, cg);
-            gx = add_(gx, mul_(g, cg[0]));
-            gy = add_(gy, mul_(g, cg[1]));
-            gz = add_(gz, mul_(g, cg[2]));
+    if (CT > 0) {
+        // channel pairs; corner rows as 32-bit element offsets (x1 = x0 + 1;
+        // the launcher routes h == 1, where x1 == x0, to the CT == 0 kernel)
+        const int r00 = (int)(c.o00 + c.ax.i0), r10 = (int)(c.o10 + c.ax.i0);
+        const int r01 = (int)(c.o01 + c.ax.i0), r11 = (int)(c.o11 + c.ax.i0);
+        XMerge mg;
+        if (gin) {
+            xmerge_row(r00, ok, mg.in[0], mg.out[0]);
+            xmerge_row(r10, ok, mg.in[1], mg.out[1]);
+            xmerge_row(r01, ok, mg.in[2], mg.out[2]);
+            xmerge_row(r11, ok, mg.in[3], mg.out[3]);
+        }
+        const float fx = c.ax.f, fy = c.ay.f, fz = c.az.f;
+        const float gxw = sub_(1.0f, fx), gyw = sub_(1.0f, fy), gzw = sub_(1.0f, fz);
+        const float2 FX = make_float2(fx, fx), GX = make_float2(gxw, gxw);
+        const float2 FY = make_float2(fy, fy), GY = make_float2(gyw, gyw);
+        const float2 FZ = make_float2(fz, fz), GZ = make_float2(gzw, gzw);
+        const bool lx = c.ax.live, ly = c.ay.live, lz = c.az.live;
+        // scalar _rn per lane (see warp_fwd_k: packed ops would be fused)
+        auto m2 = [](float2 a, float2 b) { return make_float2(mul_(a.x, b.x), mul_(a.y, b.y)); };
+        auto a2 = [](float2 a, float2 b) { return make_float2(add_(a.x, b.x), add_(a.y, b.y)); };
+        auto s2 = [](float2 a, float2 b) { return make_float2(sub_(a.x, b.x), sub_(a.y, b.y)); };
+#pragma unroll
+        for (int ch = 0; ch < CT; ch += 2) {
+            const bool two = ch + 1 < CT;
+            const float *a = in + (int64_t)ch * n, *b = two ? a + n : a;
+            const float ga = __ldg(gout + (int64_t)ch * n + p);
+            const float gb = two ? __ldg(gout + (int64_t)(ch + 1) * n + p) : 0.0f;
+            const float2 g2 = make_float2(ga, gb);
+            if (gin) {
+                // terms ((g*wx)*wy)*wz exactly as sampling.hpp:110-117, with the
+                // shared prefixes computed once
+                const float2 gx0 = m2(g2, GX), gx1 = m2(g2, FX);
+                const float2 g00 = m2(gx0, GY), g10 = m2(gx1, GY), g01 = m2(gx0, FY),
+                             g11 = m2(gx1, FY);
+                const float2 t000 = m2(g00, GZ), t100 = m2(g10, GZ), t010 = m2(g01, GZ),
+                             t110 = m2(g11, GZ), t001 = m2(g00, FZ), t101 = m2(g10, FZ),
+                             t011 = m2(g01, FZ), t111 = m2(g11, FZ);
+                // (a zero gradient gives exact zero terms: the reference's skip
+                // of g == 0 channels, sampling.hpp:152, changes nothing)
+                float *ia = gin + (int64_t)ch * n, *ib = ia + n;
+                scatter_row2(ia, ib, two, ok, r00, t000, t100, mg.in[0], mg.out[0]);
+                scatter_row2(ia, ib, two, ok, r10, t010, t110, mg.in[1], mg.out[1]);
+                scatter_row2(ia, ib, two, ok, r01, t001, t101, mg.in[2], mg.out[2]);
+                scatter_row2(ia, ib, two, ok, r11, t011, t111, mg.in[3], mg.out[3]);
+            }
+            if (gfield) {
+                const float2 v000 = make_float2(__ldg(a + r00), __ldg(b + r00));
+                const float2 v100 = make_float2(__ldg(a + r00 + 1), __ldg(b + r00 + 1));
+                const float2 v010 = make_float2(__ldg(a + r10), __ldg(b + r10));
+                const float2 v110 = make_float2(__ldg(a + r10 + 1), __ldg(b + r10 + 1));
+                const float2 v001 = make_float2(__ldg(a + r01), __ldg(b + r01));
+                const float2 v101 = make_float2(__ldg(a + r01 + 1), __ldg(b + r01 + 1));
+                const float2 v011 = make_float2(__ldg(a + r11), __ldg(b + r11));
+                const float2 v111 = make_float2(__ldg(a + r11 + 1), __ldg(b + r11 + 1));
+                // sampling.hpp:89-97 per lane
+                const float2 zero = make_float2(0.0f, 0.0f);
+                const float2 cgx =
+                    lx ? a2(m2(a2(m2(s2(v100, v000), GY), m2(s2(v110, v010), FY)), GZ),
+                            m2(a2(m2(s2(v101, v001), GY), m2(s2(v111, v011), FY)), FZ))
+                       : zero;
+                const float2 cgy =
+                    ly ? a2(m2(a2(m2(s2(v010, v000), GX), m2(s2(v110, v100), FX)), GZ),
+                            m2(a2(m2(s2(v011, v001), GX), m2(s2(v111, v101), FX)), FZ))
+                       : zero;
+                const float2 cgz =
+                    lz ? a2(m2(a2(m2(s2(v001, v000), GX), m2(s2(v101, v100), FX)), GY),
+                            m2(a2(m2(s2(v011, v010), GX), m2(s2(v111, v110), FX)), FY))
+                       : zero;
+                // channel order preserved: a, then b
+                if (ga != 0.0f) {
+                    gx = add_(gx, mul_(ga, cgx.x));
+                    gy = add_(gy, mul_(ga, cgy.x));
+                    gz = add_(gz, mul_(ga, cgz.x));
+                }
+                if (two && gb != 0.0f) {
+                    gx = add_(gx, mul_(gb, cgx.y));
+                    gy = add_(gy, mul_(gb, cgy.y));
+                    gz = add_(gz, mul_(gb, cgz.y));
+                }
+            }
+        }
+    } else {
+        for (int ch = 0; ch < C; ++ch) {
+            const float g = __ldg(gout + ch * n + p);
+            if (g == 0.0f) continue;
+            if (gin) scatter(gin + ch * n, c, g);
+            if (gfield) {
+                float cg[3];
+                sample_grad(in + ch * n, c, cg);
+                gx = add_(gx, mul_(g, cg[0]));
+                gy = add_(gy, mul_(g, cg[1]));
+                gz = add_(gz, mul_(g, cg[2]));
+            }
         }
     }
-    if (gfield) {
+    if (gfield && ok) {
         gfield[p] = add_(gfield[p], gx);
         gfield[n + p] = add_(gfield[n + p], gy);
         gfield[2 * n + p] = add_(gfield[2 * n + p], gz);
     }
 }
+
+// channel counts with an unrolled instantiation (the pyramid's C = 1, 3, 8,
+// 16, ...); others use the runtime loop
+#define MDG_UNPACK(...) __VA_ARGS__
+#define MDG_WARP_DISPATCH(KERNEL, C, CFG, ARGS)                  \
+    switch (C) {                                                 \
+        case 1: KERNEL<1><<<MDG_UNPACK CFG>>> ARGS; break;       \
+        case 2: KERNEL<2><<<MDG_UNPACK CFG>>> ARGS; break;       \
+        case 3: KERNEL<3><<<MDG_UNPACK CFG>>> ARGS; break;       \
+        case 4: KERNEL<4><<<MDG_UNPACK CFG>>> ARGS; break;       \
+        case 8: KERNEL<8><<<MDG_UNPACK CFG>>> ARGS; break;       \
+        case 16: KERNEL<16><<<MDG_UNPACK CFG>>> ARGS; break;     \
+        default: KERNEL<0><<<MDG_UNPACK CFG>>> ARGS; break;      \
+    }
 
 // ------------------------------------------------------------ compose fwd
 // field_ops.hpp:42-49 / ops.hpp:295-298: out = res + prev(x + res(x))
@@ -294,7 +503,9 @@ mdg_status mdg_warp_fwd(const float *in, int C, mdg_dims3 d, const float *field,
     const int64_t n = nvox(d);
     if (n == 0 || C == 0) return MDG_OK;
     MDG_REQUIRE(in && field && out, "warp: null pointer");
-    warp_fwd_k<<<grid1d(n, kSB), kSB, 0, S_(stream)>>>(in, C, d.h, d.w, d.l, field, out);
+    // the unrolled kernels assume x1 = x0 + 1, i.e. h >= 2
+    MDG_WARP_DISPATCH(warp_fwd_k, d.h >= 2 ? C : 0, (grid1d(n, kSB), kSB, 0, S_(stream)),
+                      (in, C, d.h, d.w, d.l, field, out));
     MDG_LAUNCHED();
     return MDG_OK;
 }
@@ -306,8 +517,8 @@ mdg_status mdg_warp_bwd(const float *in, int C, mdg_dims3 d, const float *field,
     const int64_t n = nvox(d);
     if (n == 0 || C == 0 || (!gin && !gfield)) return MDG_OK;
     MDG_REQUIRE(in && field && gout, "warp: null pointer");
-    warp_bwd_k<<<grid1d(n, kSB), kSB, 0, S_(stream)>>>(in, C, d.h, d.w, d.l, field, gout, gin,
-                                                       gfield);
+    MDG_WARP_DISPATCH(warp_bwd_k, d.h >= 2 ? C : 0, (grid1d(n, kSB), kSB, 0, S_(stream)),
+                      (in, C, d.h, d.w, d.l, field, gout, gin, gfield));
     MDG_LAUNCHED();
     return MDG_OK;
 }
