@@ -62,6 +62,13 @@ unsigned long long *numeric_flag_ptr();  // device pointer for the current devic
 // dims of the call that is checking
 mdg_status consume_numeric_flag(cudaStream_t st, mdg_dims3 d);
 
+// Per-device fixup queue for the fused ModeT forward: voxel-heads whose
+// branch-free online softmax overflowed (logit spread > 2^7 in log2 units
+// above the first row's max) or saw a non-finite logit are recomputed exactly
+// by a follow-up kernel.  Layout: [0] = count (uint32), then kFixupCap keys.
+constexpr int kFixupCap = 1 << 16;
+unsigned long long *fixup_queue_ptr();
+
 // --------------------------------------------------- stream-ordered scratch
 // cudaMallocAsync/cudaFreeAsync from the device's default mempool.
 struct Scratch {

@@ -236,6 +236,77 @@ __device__ __forceinline__ void load_bias2(float2 *sB2, const float *B, int s) {
     if (threadIdx.x < 27) sB2[threadIdx.x] = dup2(B[s * 27 + threadIdx.x] * kLog2e);
 }
 
+// ------------------------------------------------------------ fixup queue
+__device__ __forceinline__ void fixup_push(unsigned long long *q, unsigned long long key) {
+    const unsigned long long i = atomicAdd(q, 1ull);
+    if (i < (unsigned long long)kFixupCap) q[1 + i] = key;
+}
+
+// Exact per-voxel recomputation (attention.hpp:83-123 + 282-298 maths, true
+// row max) of the queued voxel-heads; a queue overflow (pathological inputs)
+// recomputes every voxel.  Non-finite logits raise the numeric flag with the
+// reference's (head, z, y, x) ordering key.
+template <int D>
+__global__ void __launch_bounds__(256)
+modet_fwd_fixup_k(const float *__restrict__ Q, const float *__restrict__ K,
+                  const float *__restrict__ B, Vol v, int S, float *__restrict__ SF,
+                  float *__restrict__ LSE, const unsigned long long *__restrict__ fixq,
+                  unsigned long long *__restrict__ flag) {
+    const unsigned long long cnt = fixq[0];
+    if (cnt == 0) return;
+    const bool all = cnt > (unsigned long long)kFixupCap;
+    const int64_t total = all ? (int64_t)S * v.n : (int64_t)cnt;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t key = all ? i : (int64_t)fixq[1 + i];
+        const int s = (int)(key / v.n);
+        const int64_t p = key - (int64_t)s * v.n;
+        const int x = (int)(p % v.h), y = (int)((p / v.h) % v.w), z = (int)(p / v.hw);
+        const float *qb = Q + (int64_t)s * D * v.n + p;
+        const float *kb = K + (int64_t)s * D * v.n;
+        float q[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) q[c] = qb[(int64_t)c * v.n];
+        float lg[27];
+        bool bad = false;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int o = 0; o < 27; ++o) {
+            const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
+            float a = B[s * 27 + o];
+            const int xx = x + dx, yy = y + dy, zz = z + dz;
+            if (xx >= 0 && xx < v.h && yy >= 0 && yy < v.w && zz >= 0 && zz < v.l) {
+                const int64_t pq = ((int64_t)zz * v.w + yy) * v.h + xx;
+                float dot = 0.0f;
+#pragma unroll
+                for (int c = 0; c < D; ++c) dot = fmaf(q[c], kb[(int64_t)c * v.n + pq], dot);
+                a += dot;
+            }
+            bad |= !isfinite(a);
+            mx = fmaxf(mx, a);
+            lg[o] = a;
+        }
+        if (bad) {
+            atomicMin(flag, (unsigned long long)key);
+            continue;
+        }
+        float sum = 0.0f, ax = 0.0f, ay = 0.0f, az = 0.0f;
+#pragma unroll
+        for (int o = 0; o < 27; ++o) {
+            const float e = __expf(lg[o] - mx);
+            sum += e;
+            ax += (o % 3 - 1) * e;
+            ay += ((o / 3) % 3 - 1) * e;
+            az += (o / 9 - 1) * e;
+        }
+        const float inv = 1.0f / sum;
+        SF[(3 * (int64_t)s + 0) * v.n + p] = ax * inv;
+        SF[(3 * (int64_t)s + 1) * v.n + p] = ay * inv;
+        SF[(3 * (int64_t)s + 2) * v.n + p] = az * inv;
+        LSE[(int64_t)s * v.n + p] = mx + logf(sum);
+    }
+}
+
 // ======================================================================= fwd
 constexpr int FTX = 32, FTY = 16;  // tile: 16 threads x 2 voxels, 16 rows
 using FG = Geo<FTX, FTY>;
@@ -249,25 +320,15 @@ struct Soft2 {
 // fold one x-row of three logits (dx = -1, 0, +1) at window row (dy, dz)
 template <int DY, int DZ, bool FIRST>
 __device__ __forceinline__ void soft_row2(Soft2 &st, float2 lm, float2 l0, float2 lp) {
-    const float2 mr = f2(fmaxf(fmaxf(lm.x, l0.x), lp.x), fmaxf(fmaxf(lm.y, l0.y), lp.y));
+    const float2 mr = FIRST ? f2(fmaxf(fmaxf(lm.x, l0.x), lp.x), fmaxf(fmaxf(lm.y, l0.y), lp.y))
+                            : st.m;
     st.mn = f2(fminf(st.mn.x, fminf(fminf(lm.x, l0.x), lp.x)),
                fminf(st.mn.y, fminf(fminf(lm.y, l0.y), lp.y)));
-    if (FIRST) {
-        st.m = mr;
-    } else {
-        const bool need = mr.x > st.m.x + kRescale || mr.y > st.m.y + kRescale;
-        if (__any_sync(0xffffffffu, need)) {
-            if (need) {
-                const float2 nm = f2(fmaxf(st.m.x, mr.x), fmaxf(st.m.y, mr.y));
-                const float2 f = ex2x2(sub2(st.m, nm));
-                st.s = mul2(st.s, f);
-                st.ax = mul2(st.ax, f);
-                st.ay = mul2(st.ay, f);
-                st.az = mul2(st.az, f);
-                st.m = nm;
-            }
-        }
-    }
+    // The first row fixes the reference max; later rows never rescale (no
+    // branch in the hot loop).  A later logit more than 128 (log2 units)
+    // above it overflows the sum to inf: such voxels are queued and redone
+    // exactly by modet_fwd_fixup_k.
+    if (FIRST) st.m = mr;
     const float2 em = ex2x2(sub2(lm, st.m)), e0 = ex2x2(sub2(l0, st.m)),
                  ep = ex2x2(sub2(lp, st.m));
     const float2 rs = add2(add2(em, e0), ep);
@@ -332,7 +393,7 @@ __global__ void __launch_bounds__(256, (D <= 6 ? 2 : 1))
 modet_fwd_tiled_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                   const float *__restrict__ K, const float *__restrict__ B, Vol v, int zc,
                   float *__restrict__ SF, float *__restrict__ LSE,
-                  unsigned long long *__restrict__ flag) {
+                  unsigned long long *__restrict__ fixq) {
     constexpr int BUF = D * (FG::HCH + FG::OCH);
     extern __shared__ __align__(128) float smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * BUF);
@@ -410,10 +471,11 @@ modet_fwd_tiled_k(const __grid_constant__ Maps maps, const float *__restrict__ Q
                 sf[2 * v.n + 1] = sz.y;
                 ls[1] = lse.y;
             }
+            // overflow (huge logit spread) or a non-finite logit: exact redo
             const bool bad0 = v0 && (!isfinite(t.s.x) || t.mn.x == -INFINITY);
             const bool bad1 = v1 && (!isfinite(t.s.y) || t.mn.y == -INFINITY);
-            if (bad0 || bad1)
-                atomicMin(flag, (unsigned long long)((int64_t)s * v.n + off + (bad0 ? 0 : 1)));
+            if (bad0) fixup_push(fixq, (unsigned long long)((int64_t)s * v.n + off));
+            if (bad1) fixup_push(fixq, (unsigned long long)((int64_t)s * v.n + off + 1));
         }
     });
 }
@@ -537,7 +599,8 @@ modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                 R.q[NEW][c] = mul2(f2(a, bq), dup2(kLog2e));
                 R.dq[NEW][c] = f2(0.0f, 0.0f);
             }
-            R.L[NEW] = own[D * RG::OCH] * kLog2e;
+            // lanes outside the volume: LSE = +inf => W = 0 (no NaN into dB)
+            R.L[NEW] = vv ? own[D * RG::OCH] * kLog2e : INFINITY;
             const float gx = own[(D + 1) * RG::OCH], gy = own[(D + 2) * RG::OCH],
                         gz = own[(D + 3) * RG::OCH];
             R.gx[NEW] = gx;
@@ -658,13 +721,18 @@ __device__ __forceinline__ void col_slot(ColSlots<D> &C_, int j, const SrcStrip<
     }
 }
 
+// out-of-volume sources get LSE = +inf, i.e. W = 0 exactly: the reference
+// only scatters from in-bounds sources (attention.hpp:155)
 template <int D>
-__device__ __forceinline__ void col_transform(float *buf) {
+__device__ __forceinline__ void col_transform(float *buf, int x0, int y0, int z, const Vol &v) {
     constexpr int CH = CG::HCH;
+    const bool zok = z >= 0 && z < v.l;
     for (int i = threadIdx.x; i < CG::PY * CG::RL; i += blockDim.x) {
         const int ry = i / CG::RL, rx = i - ry * CG::RL;
+        const int gx = x0 - 1 + rx, gy = y0 - 1 + ry;
+        const bool in = zok && gx >= 0 && gx < v.h && gy >= 0 && gy < v.w;
         float *e = buf + ry * kBoxX + kXOff + rx;
-        e[D * CH] *= kLog2e;
+        e[D * CH] = in ? e[D * CH] * kLog2e : INFINITY;
         e[(D + 4) * CH] = e[(D + 1) * CH] * e[(D + 4) * CH] + e[(D + 2) * CH] * e[(D + 5) * CH] +
                           e[(D + 3) * CH] * e[(D + 6) * CH];
     }
@@ -730,7 +798,7 @@ modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
         else cp_wait_all();
         __syncthreads();
         float *buf = smem + b * BUF;
-        col_transform<D>(buf);
+        col_transform<D>(buf, x0, y0, p, v);
         // generic-proxy writes to a buffer the TMA (async proxy) refills later
         if (TMA) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         if (p + 1 <= ze)
@@ -883,13 +951,19 @@ static cudaError_t fwd_launch(const float *Q, const float *K, const float *B, md
     const bool tma = tma_ok(v, {Q, K}) && make_map(&m.k, K, v, S * D, kBoxX, FG::PY) &&
                      make_map(&m.a.q, Q, v, S * D, FTX, FTY);
     const dim3 grid(gx, gy, S * nzc);
+    unsigned long long *fixq = fixup_queue_ptr();
+    if (!fixq) return cudaErrorMemoryAllocation;
+    cudaError_t e = cudaMemsetAsync(fixq, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
     if (tma) {
         set_smem(modet_fwd_tiled_k<D, true>, sm);
-        modet_fwd_tiled_k<D, true><<<grid, 256, sm, st>>>(m, Q, K, B, v, zc, SF, LSE, flag);
+        modet_fwd_tiled_k<D, true><<<grid, 256, sm, st>>>(m, Q, K, B, v, zc, SF, LSE, fixq);
     } else {
         set_smem(modet_fwd_tiled_k<D, false>, sm);
-        modet_fwd_tiled_k<D, false><<<grid, 256, sm, st>>>(m, Q, K, B, v, zc, SF, LSE, flag);
+        modet_fwd_tiled_k<D, false><<<grid, 256, sm, st>>>(m, Q, K, B, v, zc, SF, LSE, fixq);
     }
+    modet_fwd_fixup_k<D><<<148, 256, 0, st>>>(Q, K, B, v, S, SF, LSE, fixq, flag);
+    g_launches.fetch_add(1);
     return cudaPeekAtLastError();
 }
 

@@ -44,6 +44,23 @@ unsigned long long *numeric_flag_ptr() {
     return g_flags[dev];
 }
 
+unsigned long long *fixup_queue_ptr() {
+    static std::vector<unsigned long long *> queues;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_flag_mu);
+    if ((int)queues.size() <= dev) queues.resize(dev + 1, nullptr);
+    if (!queues[dev]) {
+        unsigned long long *p = nullptr;
+        if (cudaMalloc(&p, (kFixupCap + 1) * sizeof(unsigned long long)) != cudaSuccess)
+            return nullptr;
+        cudaMemset(p, 0, sizeof(unsigned long long));
+        cudaDeviceSynchronize();
+        queues[dev] = p;
+    }
+    return queues[dev];
+}
+
 mdg_status consume_numeric_flag(cudaStream_t st, mdg_dims3 d) {
     unsigned long long *f = numeric_flag_ptr();
     if (!f) return status_from_cuda(cudaErrorMemoryAllocation, "numeric flag");

@@ -159,6 +159,38 @@ def test_tiled_kernels_ragged_tiles(cuda, oracle, dims, S, hd, accumulate):
     assert grad_ok(gB, gB0, 1e-4 if not accumulate else 1e-3)
 
 
+@pytest.mark.parametrize("spread", [30.0, 95.0, 300.0])
+def test_fused_forward_large_logit_spread(cuda, oracle, spread):
+    """The tiled forward fixes each voxel's softmax reference max from its first
+    window row; logits far above it (here a huge bias on the last window rows)
+    must still give the exact softmax (overflowed voxels go to the exact fixup
+    kernel)."""
+    dims, S, hd = (20, 9, 7), 2, 6
+    n = 20 * 9 * 7
+    Q = random_qk(dims, S * hd, 3)
+    K = random_qk(dims, S * hd, 4)
+    B = f32(pyoracle.Rng(5).normal(S * 27).reshape(S, 27))
+    B[0, 18:] += spread
+    B[1, 26] += spread
+    gSF = f32(pyoracle.Rng(6).normal(3 * S * n).reshape(3 * S, 7, 9, 20))
+    W0, SF0, gQ0, gK0, gB0 = oracle_modet(oracle, Q, K, B, dims, S, hd, gSF)
+    W, SF, LSE, gQ, gK, gB = run_fused(Q, K, B, dims, S, hd, gSF, MDG_QK_PLANAR)
+    assert rel_close(SF, SF0.reshape(SF.shape), FLOW_ATOL, FLOW_RTOL)
+    assert grad_ok(gQ, gQ0) and grad_ok(gK, gK0) and grad_ok(gB, gB0)
+
+
+def test_fused_forward_negative_inf_bias_raises(cuda, oracle):
+    dims = (8, 4, 3)
+    Q, K = random_qk(dims, 6, 1), random_qk(dims, 6, 2)
+    B = np.zeros((1, 27), np.float32)
+    B[0, 20] = -np.inf
+    _, bad = oracle.na_fwd(Q, K, B, dims, 1, 6)
+    with pytest.raises(ops.NumericError) as ei:
+        ops.modet_fwd(dev(Q.T.copy()), dev(K.T.copy()), dev(B), dims, ops.AttentionConfig(1, 6, 3),
+                      layout=MDG_QK_PLANAR)
+    assert ei.value.position == bad
+
+
 def test_config1_32cubed_s8_d8(cuda, oracle):
     """BASELINE configs[0]: 32^3, 8 heads x 8 channels; inputs in the order of
     the reference bench (bench.cpp:28-35): Rng(5) Q, K ~ U(-1,1), B ~ U(-.5,.5);
