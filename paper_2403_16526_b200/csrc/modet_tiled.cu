@@ -308,64 +308,64 @@ modet_fwd_fixup_k(const float *__restrict__ Q, const float *__restrict__ K,
 }
 
 // ======================================================================= fwd
-constexpr int FTX = 32, FTY = 16;  // tile: 16 threads x 2 voxels, 16 rows
+constexpr int FTX = 32, FTY = 8;  // tile: one voxel per thread, a warp per x-row
 using FG = Geo<FTX, FTY>;
 
-// online-softmax state of the thread's voxel pair (x = .x voxel, y = .y voxel)
-struct Soft2 {
-    float2 m, s, ax, ay, az;
-    float2 mn;  // running min logit (a -inf logit is a numeric error)
+// online-softmax state of one (voxel, head) row
+struct Soft {
+    float m, s, ax, ay, az;
+    float mn;  // running min logit (a -inf logit is a numeric error)
 };
 
 // fold one x-row of three logits (dx = -1, 0, +1) at window row (dy, dz)
 template <int DY, int DZ, bool FIRST>
-__device__ __forceinline__ void soft_row2(Soft2 &st, float2 lm, float2 l0, float2 lp) {
-    const float2 mr = FIRST ? f2(fmaxf(fmaxf(lm.x, l0.x), lp.x), fmaxf(fmaxf(lm.y, l0.y), lp.y))
-                            : st.m;
-    st.mn = f2(fminf(st.mn.x, fminf(fminf(lm.x, l0.x), lp.x)),
-               fminf(st.mn.y, fminf(fminf(lm.y, l0.y), lp.y)));
+__device__ __forceinline__ void soft_row(Soft &st, float lm, float l0, float lp) {
+    st.mn = fminf(st.mn, fminf(fminf(lm, l0), lp));
     // The first row fixes the reference max; later rows never rescale (no
     // branch in the hot loop).  A later logit more than 128 (log2 units)
     // above it overflows the sum to inf: such voxels are queued and redone
     // exactly by modet_fwd_fixup_k.
-    if (FIRST) st.m = mr;
-    const float2 em = ex2x2(sub2(lm, st.m)), e0 = ex2x2(sub2(l0, st.m)),
-                 ep = ex2x2(sub2(lp, st.m));
-    const float2 rs = add2(add2(em, e0), ep);
-    const float2 dx = sub2(ep, em);
+    if (FIRST) st.m = fmaxf(fmaxf(lm, l0), lp);
+    const float em = ex2(lm - st.m), e0 = ex2(l0 - st.m), ep = ex2(lp - st.m);
+    const float rs = (em + e0) + ep;
+    const float dx = ep - em;
     if (FIRST) {
         st.s = rs;
         st.ax = dx;
-        st.ay = DY > 0 ? rs : (DY < 0 ? f2(-rs.x, -rs.y) : f2(0.f, 0.f));
-        st.az = DZ > 0 ? rs : (DZ < 0 ? f2(-rs.x, -rs.y) : f2(0.f, 0.f));
+        st.ay = DY > 0 ? rs : (DY < 0 ? -rs : 0.0f);
+        st.az = DZ > 0 ? rs : (DZ < 0 ? -rs : 0.0f);
     } else {
-        st.s = add2(st.s, rs);
-        st.ax = add2(st.ax, dx);
-        if (DY > 0) st.ay = add2(st.ay, rs);
-        if (DY < 0) st.ay = sub2(st.ay, rs);
-        if (DZ > 0) st.az = add2(st.az, rs);
-        if (DZ < 0) st.az = sub2(st.az, rs);
+        st.s += rs;
+        st.ax += dx;
+        if (DY > 0) st.ay += rs;
+        if (DY < 0) st.ay -= rs;
+        if (DZ > 0) st.az += rs;
+        if (DZ < 0) st.az -= rs;
     }
 }
 
 template <int D>
 struct FwdSlots {
-    float2 q[3][D];  // per channel {voxel x, voxel x+1} * log2e
-    Soft2 st[3];
+    static constexpr int D2 = (D + 1) / 2;
+    float2 q[3][D2];  // channel pairs of q * log2e (odd D: last .y = 0)
+    Soft st[3];
 };
 
+// logits of one window x-row on the packed pipe: channel pairs accumulate
+// {even, odd} partial dots, combined once per logit
 template <int D, int DYI, int DZ, bool FIRST>
-__device__ __forceinline__ void fwd_slot(const float2 (&q)[D], Soft2 &st, const Strip (&ks)[D],
-                                         const float2 *sB2) {
+__device__ __forceinline__ void fwd_slot(const float2 (&q)[(D + 1) / 2], Soft &st,
+                                         const float2 (&kr)[(D + 1) / 2][3], const float2 *sB2) {
+    constexpr int D2 = (D + 1) / 2;
     constexpr int ob = (DZ + 1) * 9 + DYI * 3;
-    float2 lm = sB2[ob], l0 = sB2[ob + 1], lp = sB2[ob + 2];
+    float2 am = f2(sB2[ob].x, 0.0f), a0 = f2(sB2[ob + 1].x, 0.0f), ap = f2(sB2[ob + 2].x, 0.0f);
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
-        lm = fma2(q[c], ks[c].p[0], lm);
-        l0 = fma2(q[c], ks[c].p[1], l0);
-        lp = fma2(q[c], ks[c].p[2], lp);
+    for (int c = 0; c < D2; ++c) {
+        am = fma2(q[c], kr[c][0], am);
+        a0 = fma2(q[c], kr[c][1], a0);
+        ap = fma2(q[c], kr[c][2], ap);
     }
-    soft_row2<DYI - 1, DZ, FIRST>(st, lm, l0, lp);
+    soft_row<DYI - 1, DZ, FIRST>(st, am.x + am.y, a0.x + a0.y, ap.x + ap.y);
 }
 
 template <int D, bool TMA>
@@ -389,23 +389,24 @@ __device__ __forceinline__ void fwd_stage(float *buf, const Maps &m, uint64_t *b
 }
 
 template <int D, bool TMA>
-__global__ void __launch_bounds__(256, (D <= 6 ? 2 : 1))
+__global__ void __launch_bounds__(256, (D <= 6 ? 3 : 2))
 modet_fwd_tiled_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                   const float *__restrict__ K, const float *__restrict__ B, Vol v, int zc,
                   float *__restrict__ SF, float *__restrict__ LSE,
                   unsigned long long *__restrict__ fixq) {
+    constexpr int D2 = (D + 1) / 2;
     constexpr int BUF = D * (FG::HCH + FG::OCH);
     extern __shared__ __align__(128) float smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * BUF);
     float2 *sB2 = reinterpret_cast<float2 *>(smem + 2 * BUF + 8);
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int x0 = blockIdx.x * FTX, y0 = blockIdx.y * FTY;
     const int nzc = (v.l + zc - 1) / zc;
     const int s = blockIdx.z / nzc;
     const int zb = (blockIdx.z - s * nzc) * zc, ze = min(zb + zc, v.l);
     const Ptrs P{K + (int64_t)s * D * v.n, Q + (int64_t)s * D * v.n, nullptr, nullptr, nullptr};
-    const int x = x0 + 2 * tx, y = y0 + ty;
-    const bool v0 = y < v.w && x < v.h, v1 = y < v.w && x + 1 < v.h;
+    const int x = x0 + tx, y = y0 + ty;
+    const bool vv = y < v.w && x < v.h;
     load_bias2(sB2, B, s);
     if (TMA) init_bars(bar);
     __syncthreads();
@@ -423,59 +424,54 @@ modet_fwd_tiled_k(const __grid_constant__ Maps maps, const float *__restrict__ Q
         const float *buf = smem + b * BUF;
         const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
         if (has_new) {
-            const float *own = buf + D * FG::HCH + ty * FTX + 2 * tx;
+            const float *own = buf + D * FG::HCH + ty * FTX + tx;
 #pragma unroll
-            for (int c = 0; c < D; ++c)
-                S_.q[NEW][c] = mul2(*reinterpret_cast<const float2 *>(own + c * FG::OCH),
-                                    dup2(kLog2e));
-            S_.st[NEW].mn = dup2(INFINITY);
+            for (int c = 0; c < D2; ++c) {
+                const float a = own[(2 * c) * FG::OCH];
+                const float bq = 2 * c + 1 < D ? own[(2 * c + 1) * FG::OCH] : 0.0f;
+                S_.q[NEW][c] = mul2(f2(a, bq), dup2(kLog2e));
+            }
+            S_.st[NEW].mn = INFINITY;
         }
 #pragma unroll
         for (int dyi = 0; dyi < 3; ++dyi) {
-            Strip ks[D];
+            // channel pairs of the 3 keys x-1, x, x+1 of window row dy = dyi-1
+            float2 ks[D2][3];
 #pragma unroll
-            for (int c = 0; c < D; ++c) ks[c] = strip(buf + c * FG::HCH + (ty + dyi) * kBoxX, tx);
+            for (int c = 0; c < D2; ++c) {
+                const float *e0 = buf + (2 * c) * FG::HCH + (ty + dyi) * kBoxX + kXOff + tx;
+                const float *e1 = e0 + FG::HCH;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) ks[c][i] = f2(e0[i], 2 * c + 1 < D ? e1[i] : 0.0f);
+            }
             // slot z sees plane p at window offset dz = p - z; the new slot's
             // very first row initialises its softmax state
             if (dyi == 0) {
-                if (has_new) fwd_slot<D, 0, -1, true>(S_.q[NEW], S_.st[NEW], ks, sB2);
-                if (has_mid) fwd_slot<D, 0, 0, false>(S_.q[MID], S_.st[MID], ks, sB2);
-                if (has_old) fwd_slot<D, 0, 1, false>(S_.q[OLD], S_.st[OLD], ks, sB2);
+                fwd_slot<D, 0, -1, true>(S_.q[NEW], S_.st[NEW], ks, sB2);
+                fwd_slot<D, 0, 0, false>(S_.q[MID], S_.st[MID], ks, sB2);
+                fwd_slot<D, 0, 1, false>(S_.q[OLD], S_.st[OLD], ks, sB2);
             } else if (dyi == 1) {
-                if (has_new) fwd_slot<D, 1, -1, false>(S_.q[NEW], S_.st[NEW], ks, sB2);
-                if (has_mid) fwd_slot<D, 1, 0, false>(S_.q[MID], S_.st[MID], ks, sB2);
-                if (has_old) fwd_slot<D, 1, 1, false>(S_.q[OLD], S_.st[OLD], ks, sB2);
+                fwd_slot<D, 1, -1, false>(S_.q[NEW], S_.st[NEW], ks, sB2);
+                fwd_slot<D, 1, 0, false>(S_.q[MID], S_.st[MID], ks, sB2);
+                fwd_slot<D, 1, 1, false>(S_.q[OLD], S_.st[OLD], ks, sB2);
             } else {
-                if (has_new) fwd_slot<D, 2, -1, false>(S_.q[NEW], S_.st[NEW], ks, sB2);
-                if (has_mid) fwd_slot<D, 2, 0, false>(S_.q[MID], S_.st[MID], ks, sB2);
-                if (has_old) fwd_slot<D, 2, 1, false>(S_.q[OLD], S_.st[OLD], ks, sB2);
+                fwd_slot<D, 2, -1, false>(S_.q[NEW], S_.st[NEW], ks, sB2);
+                fwd_slot<D, 2, 0, false>(S_.q[MID], S_.st[MID], ks, sB2);
+                fwd_slot<D, 2, 1, false>(S_.q[OLD], S_.st[OLD], ks, sB2);
             }
         }
-        if (has_old) {
+        if (has_old && vv) {
             const int64_t off = (int64_t)(p - 1) * v.hw + (int64_t)y * v.h + x;
-            const Soft2 &t = S_.st[OLD];
-            const float2 inv = f2(1.0f / t.s.x, 1.0f / t.s.y);
-            const float2 sx = mul2(t.ax, inv), sy = mul2(t.ay, inv), sz = mul2(t.az, inv);
-            const float2 lse = f2((t.m.x + __log2f(t.s.x)) * kLn2, (t.m.y + __log2f(t.s.y)) * kLn2);
+            const Soft &t = S_.st[OLD];
+            const float inv = 1.0f / t.s;
             float *sf = SF + 3 * (int64_t)s * v.n + off;
-            float *ls = LSE + (int64_t)s * v.n + off;
-            if (v0) {
-                sf[0] = sx.x;
-                sf[v.n] = sy.x;
-                sf[2 * v.n] = sz.x;
-                ls[0] = lse.x;
-            }
-            if (v1) {
-                sf[1] = sx.y;
-                sf[v.n + 1] = sy.y;
-                sf[2 * v.n + 1] = sz.y;
-                ls[1] = lse.y;
-            }
+            sf[0] = t.ax * inv;
+            sf[v.n] = t.ay * inv;
+            sf[2 * v.n] = t.az * inv;
+            LSE[(int64_t)s * v.n + off] = (t.m + __log2f(t.s)) * kLn2;
             // overflow (huge logit spread) or a non-finite logit: exact redo
-            const bool bad0 = v0 && (!isfinite(t.s.x) || t.mn.x == -INFINITY);
-            const bool bad1 = v1 && (!isfinite(t.s.y) || t.mn.y == -INFINITY);
-            if (bad0) fixup_push(fixq, (unsigned long long)((int64_t)s * v.n + off));
-            if (bad1) fixup_push(fixq, (unsigned long long)((int64_t)s * v.n + off + 1));
+            if (!isfinite(t.s) || t.mn == -INFINITY)
+                fixup_push(fixq, (unsigned long long)((int64_t)s * v.n + off));
         }
     });
 }
@@ -573,7 +569,17 @@ modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
     if (TMA) init_bars(bar);
     __syncthreads();
     row_stage<D, TMA>(smem, maps, &bar[0], zb - 1, x0, y0, s, P, v);
+    // Slots are computed unconditionally (no per-slot branches, so the three
+    // slots' dependency chains interleave); a slot that holds no voxel has
+    // LSE = +inf, q = g = 0, i.e. W = 0 and dl = 0 exactly: nothing reaches dB.
     RowSlots<D> R;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+#pragma unroll
+        for (int c = 0; c < (D + 1) / 2; ++c) R.q[j][c] = R.dq[j][c] = f2(0.0f, 0.0f);
+        R.L[j] = INFINITY;
+        R.gx[j] = R.gy[j] = R.gz[j] = R.dot[j] = 0.0f;
+    }
     float db[27];
 #pragma unroll
     for (int o = 0; o < 27; ++o) db[o] = 0.0f;
@@ -608,6 +614,8 @@ modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
             R.gz[NEW] = gz;
             R.dot[NEW] = gx * own[(D + 4) * RG::OCH] + gy * own[(D + 5) * RG::OCH] +
                          gz * own[(D + 6) * RG::OCH];
+        } else {
+            R.L[NEW] = INFINITY;  // past the chunk end: the slot goes idle
         }
 #pragma unroll
         for (int dyi = 0; dyi < 3; ++dyi) {
@@ -620,17 +628,17 @@ modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                 for (int i = 0; i < 3; ++i) kr[c][i] = f2(e0[i], 2 * c + 1 < D ? e1[i] : 0.0f);
             }
             if (dyi == 0) {
-                if (has_new) row_slot<D, 0, -1>(R, NEW, db, kr, sB2);
-                if (has_mid) row_slot<D, 0, 0>(R, MID, db, kr, sB2);
-                if (has_old) row_slot<D, 0, 1>(R, OLD, db, kr, sB2);
+                row_slot<D, 0, -1>(R, NEW, db, kr, sB2);
+                row_slot<D, 0, 0>(R, MID, db, kr, sB2);
+                row_slot<D, 0, 1>(R, OLD, db, kr, sB2);
             } else if (dyi == 1) {
-                if (has_new) row_slot<D, 1, -1>(R, NEW, db, kr, sB2);
-                if (has_mid) row_slot<D, 1, 0>(R, MID, db, kr, sB2);
-                if (has_old) row_slot<D, 1, 1>(R, OLD, db, kr, sB2);
+                row_slot<D, 1, -1>(R, NEW, db, kr, sB2);
+                row_slot<D, 1, 0>(R, MID, db, kr, sB2);
+                row_slot<D, 1, 1>(R, OLD, db, kr, sB2);
             } else {
-                if (has_new) row_slot<D, 2, -1>(R, NEW, db, kr, sB2);
-                if (has_mid) row_slot<D, 2, 0>(R, MID, db, kr, sB2);
-                if (has_old) row_slot<D, 2, 1>(R, OLD, db, kr, sB2);
+                row_slot<D, 2, -1>(R, NEW, db, kr, sB2);
+                row_slot<D, 2, 0>(R, MID, db, kr, sB2);
+                row_slot<D, 2, 1>(R, OLD, db, kr, sB2);
             }
         }
         if (has_old && vv && gQh) {
@@ -837,17 +845,17 @@ modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
             }
             // key z sees sources in plane p at window offset dz = z - p
             if (dyi == 0) {
-                if (has_new) col_slot<D, 0, 1>(C_, NEW, S, sB2);
-                if (has_mid) col_slot<D, 0, 0>(C_, MID, S, sB2);
-                if (has_old) col_slot<D, 0, -1>(C_, OLD, S, sB2);
+                col_slot<D, 0, 1>(C_, NEW, S, sB2);
+                col_slot<D, 0, 0>(C_, MID, S, sB2);
+                col_slot<D, 0, -1>(C_, OLD, S, sB2);
             } else if (dyi == 1) {
-                if (has_new) col_slot<D, 1, 1>(C_, NEW, S, sB2);
-                if (has_mid) col_slot<D, 1, 0>(C_, MID, S, sB2);
-                if (has_old) col_slot<D, 1, -1>(C_, OLD, S, sB2);
+                col_slot<D, 1, 1>(C_, NEW, S, sB2);
+                col_slot<D, 1, 0>(C_, MID, S, sB2);
+                col_slot<D, 1, -1>(C_, OLD, S, sB2);
             } else {
-                if (has_new) col_slot<D, 2, 1>(C_, NEW, S, sB2);
-                if (has_mid) col_slot<D, 2, 0>(C_, MID, S, sB2);
-                if (has_old) col_slot<D, 2, -1>(C_, OLD, S, sB2);
+                col_slot<D, 2, 1>(C_, NEW, S, sB2);
+                col_slot<D, 2, 0>(C_, MID, S, sB2);
+                col_slot<D, 2, -1>(C_, OLD, S, sB2);
             }
         }
         if (has_old && vv) {
@@ -944,7 +952,7 @@ static cudaError_t fwd_launch(const float *Q, const float *K, const float *B, md
                               float *SF, float *LSE, unsigned long long *flag, cudaStream_t st) {
     const Vol v{d.h, d.w, d.l, (int64_t)d.h * d.w * d.l, (int64_t)d.h * d.w};
     const int gx = (d.h + FTX - 1) / FTX, gy = (d.w + FTY - 1) / FTY;
-    const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 2 : 1);
+    const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 3 : 2);
     const int nzc = (d.l + zc - 1) / zc;
     const size_t sm = (2 * D * (FG::HCH + FG::OCH) + kTail) * sizeof(float);
     Maps m{};
