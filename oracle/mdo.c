@@ -542,3 +542,79 @@ void mdo_scaling_squaring(const float *vel, int h, int w, int l, int steps, floa
     }
     free(tmp);
 }
+
+/* ---------------------------------------------------------- Q/K projection */
+
+/* ops.hpp:387-413: out[p,k] = b[k] + sum_c W[k,c] * in[c,p], summed in channel
+ * order starting from the bias */
+void mdo_linear_proj_fwd(const float *in, int c, int64_t n, const float *weight,
+                         const float *bias, int K, float *out) {
+    for (int64_t p = 0; p < n; ++p)
+        for (int k = 0; k < K; ++k) {
+            float s = bias[k];
+            for (int ch = 0; ch < c; ++ch) s += weight[(int64_t)k * c + ch] * in[ch * n + p];
+            out[p * K + k] = s;
+        }
+}
+
+/* ops.hpp:414-433 (tape closure): per position, per output k with g != 0 */
+void mdo_linear_proj_bwd(const float *in, int c, int64_t n, const float *weight, int K,
+                         const float *gout, float *gin, float *gw, float *gb) {
+    for (int64_t p = 0; p < n; ++p)
+        for (int k = 0; k < K; ++k) {
+            const float g = gout[p * K + k];
+            if (g == 0.0f) continue;
+            if (gb) gb[k] += g;
+            for (int ch = 0; ch < c; ++ch) {
+                if (gw) gw[(int64_t)k * c + ch] += g * in[ch * n + p];
+                if (gin) gin[ch * n + p] += g * weight[(int64_t)k * c + ch];
+            }
+        }
+}
+
+/* ops.hpp:445-461: two-pass mean / biased variance, inv = 1/sqrt(var + eps) */
+static void ln_stats(const float *src, int K, float eps, float *mean_out, float *inv_out) {
+    float mean = 0.0f;
+    for (int k = 0; k < K; ++k) mean += src[k];
+    mean /= (float)K;
+    float var = 0.0f;
+    for (int k = 0; k < K; ++k) var += (src[k] - mean) * (src[k] - mean);
+    var /= (float)K;
+    *mean_out = mean;
+    *inv_out = 1.0f / sqrtf(var + eps);
+}
+
+void mdo_layer_norm_fwd(const float *in, int64_t n, int K, const float *gamma,
+                        const float *beta, float eps, float *out) {
+    for (int64_t p = 0; p < n; ++p) {
+        const float *src = in + p * K;
+        float mean, inv;
+        ln_stats(src, K, eps, &mean, &inv);
+        for (int k = 0; k < K; ++k) out[p * K + k] = gamma[k] * (src[k] - mean) * inv + beta[k];
+    }
+}
+
+/* ops.hpp:462-494 */
+void mdo_layer_norm_bwd(const float *in, int64_t n, int K, const float *gamma, float eps,
+                        const float *gout, float *gin, float *gg, float *gb) {
+    for (int64_t p = 0; p < n; ++p) {
+        const float *src = in + p * K;
+        const float *go = gout + p * K;
+        float mean, inv;
+        ln_stats(src, K, eps, &mean, &inv);
+        float sum_g = 0.0f, sum_gx = 0.0f;
+        for (int k = 0; k < K; ++k) {
+            const float xh = (src[k] - mean) * inv;
+            sum_g += go[k] * gamma[k];
+            sum_gx += go[k] * gamma[k] * xh;
+        }
+        const float mg = sum_g / (float)K;
+        const float mgx = sum_gx / (float)K;
+        for (int k = 0; k < K; ++k) {
+            const float xh = (src[k] - mean) * inv;
+            if (gg) gg[k] += go[k] * xh;
+            if (gb) gb[k] += go[k];
+            if (gin) gin[p * K + k] += inv * (go[k] * gamma[k] - mg - xh * mgx);
+        }
+    }
+}

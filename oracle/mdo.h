@@ -94,6 +94,20 @@ void mdo_compose_bwd(const float *prev, const float *res, int h, int w, int l,
 /* reghead.hpp:60-67 (plain scaling and squaring) */
 void mdo_scaling_squaring(const float *vel, int h, int w, int l, int steps, float *out);
 
+/* ops.hpp:387-413 op_linear_proj forward: in {c, n} channel-major, weight
+ * {K, c}, bias {K} -> out position-major {n, K} */
+void mdo_linear_proj_fwd(const float *in, int c, int64_t n, const float *weight,
+                         const float *bias, int K, float *out);
+/* ops.hpp:414-433 backward (accumulates; gin/gw/gb may be NULL; g == 0 skipped) */
+void mdo_linear_proj_bwd(const float *in, int c, int64_t n, const float *weight, int K,
+                         const float *gout, float *gin, float *gw, float *gb);
+/* ops.hpp:439-461 op_layer_norm forward over the trailing K axis of {n, K} */
+void mdo_layer_norm_fwd(const float *in, int64_t n, int K, const float *gamma,
+                        const float *beta, float eps, float *out);
+/* ops.hpp:462-494 backward (accumulates; gin/gg/gb may be NULL) */
+void mdo_layer_norm_bwd(const float *in, int64_t n, int K, const float *gamma, float eps,
+                        const float *gout, float *gin, float *gg, float *gb);
+
 #ifdef __cplusplus
 }
 #endif

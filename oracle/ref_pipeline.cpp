@@ -1,6 +1,171 @@
 // ref_pipeline.cpp — TEST INFRASTRUCTURE ONLY: extern "C" access to the
-// reference pyramid driver (engine.hpp) for pipeline-level parity.  Filled in
-// as the GPU pipeline grows; forwards to mdreg:: symbols only.
+// reference's decoding pyramid (engine.hpp:179-219) and Q/K projection
+// (attention.hpp:351-356, ops.hpp:387-497) for pipeline-level parity.  Every
+// value comes from mdreg:: operators on an mdreg::Tape; the bodies only marshal
+// buffers.
+//
+// Packed per-level parameter block (the order of ModelParams::all_tensors,
+// engine.hpp:127-131):  proj.w {K,C} | proj.b {K} | ln_g {K} | ln_b {K} |
+// bias_b {S,27} | reghead.w {3,3S,3,3,3} | reghead.b {3},  K = S*hd.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
 #include "mdreg/engine.hpp"
 
-extern "C" int mdr_pipeline_available() { return 1; }
+using namespace mdreg;
+
+namespace {
+thread_local std::string g_perr;
+
+Tensor<float> tensor_from(const float *src, std::vector<int> shape) {
+    Tensor<float> t(std::move(shape));
+    std::memcpy(t.data.data(), src, t.data.size() * sizeof(float));
+    return t;
+}
+
+void add_into(float *dst, const Tensor<float> &g) {
+    if (!dst) return;
+    for (std::size_t i = 0; i < g.data.size(); ++i) dst[i] += g.data[i];
+}
+
+int64_t level_param_count(int C, int S, int hd, int nb) {
+    const int64_t K = (int64_t)S * hd, win = (int64_t)nb * nb * nb;
+    return K * C + 3 * K + S * win + 3 * 3 * S * 27 + 3;
+}
+}  // namespace
+
+extern "C" {
+
+int mdr_pipeline_available() { return 1; }
+const char *mdr_pipeline_error() { return g_perr.c_str(); }
+
+int64_t mdr_level_param_count(int C, int S, int hd, int nb) {
+    return level_param_count(C, S, hd, nb);
+}
+
+// op_project_qk (attention.hpp:351-356) forward, then the tape backward of
+// loss = sum(Q*gQ) + sum(K*gK).  Q/K position-major {n, K}.  Grads accumulate;
+// any grad pointer may be NULL; gQ == NULL skips the backward entirely.
+int mdr_project_qk(const float *f, const float *m, int C, int h, int w, int l,
+                   const float *weight, const float *bias, const float *ln_g,
+                   const float *ln_b, int K, float *Q, float *Kout, const float *gQ,
+                   const float *gK, float *gf, float *gm, float *gweight, float *gbias,
+                   float *gln_g, float *gln_b) {
+    try {
+        const int n = h * w * l;
+        Tape<float> t;
+        Var fv = t.input(tensor_from(f, {C, h, w, l}));
+        Var mv = t.input(tensor_from(m, {C, h, w, l}));
+        ProjectionVars pv{t.input(tensor_from(weight, {K, C})), t.input(tensor_from(bias, {K})),
+                          t.input(tensor_from(ln_g, {K})), t.input(tensor_from(ln_b, {K}))};
+        auto [q, k] = op_project_qk(t, fv, mv, pv);
+        std::memcpy(Q, t.value(q).data.data(), (size_t)n * K * sizeof(float));
+        std::memcpy(Kout, t.value(k).data.data(), (size_t)n * K * sizeof(float));
+        if (!gQ) return 0;
+        Var lq = op_sum_all(t, op_mul(t, q, t.input(tensor_from(gQ, {n, K}))));
+        Var lk = op_sum_all(t, op_mul(t, k, t.input(tensor_from(gK, {n, K}))));
+        t.backward(op_add(t, lq, lk));
+        add_into(gf, t.grad(fv));
+        add_into(gm, t.grad(mv));
+        add_into(gweight, t.grad(pv.weight));
+        add_into(gbias, t.grad(pv.bias));
+        add_into(gln_g, t.grad(pv.ln_gamma));
+        add_into(gln_b, t.grad(pv.ln_beta));
+    } catch (const std::exception &e) {
+        g_perr = e.what();
+        return 1;
+    }
+    return 0;
+}
+
+// The decoding half of build_pipeline (engine.hpp:189-216) on given encoder
+// features, coarse -> fine (f_feats[k] {C_k, dims_k}).  Forward writes phi
+// {3, n_fine} and (optionally) each level's residual; if gphi is non-NULL the
+// tape backward of loss = sum(phi * gphi) accumulates into the packed level
+// parameter grads and the feature grads (each nullable).
+int mdr_decoder(int levels, const int *dims, const int *channels, const int *heads, int hd,
+                int nb, int diffeomorphic, int ss_steps, const float *const *f_feats,
+                const float *const *m_feats, const float *const *params, const float *gphi,
+                float *phi_out, float *const *res_out, float *const *gparams,
+                float *const *gf, float *const *gm) {
+    try {
+        Tape<float> t;
+        std::vector<Var> fv, mv;
+        struct LV {
+            Var w, b, g, be, bias, rw, rb;
+        };
+        std::vector<LV> lv;
+        for (int k = 0; k < levels; ++k) {
+            const int h = dims[3 * k], w = dims[3 * k + 1], l = dims[3 * k + 2];
+            const int C = channels[k], S = heads[k], K = S * hd, win = nb * nb * nb;
+            fv.push_back(t.input(tensor_from(f_feats[k], {C, h, w, l})));
+            mv.push_back(t.input(tensor_from(m_feats[k], {C, h, w, l})));
+            const float *p = params[k];
+            LV v;
+            v.w = t.input(tensor_from(p, {K, C})), p += (int64_t)K * C;
+            v.b = t.input(tensor_from(p, {K})), p += K;
+            v.g = t.input(tensor_from(p, {K})), p += K;
+            v.be = t.input(tensor_from(p, {K})), p += K;
+            v.bias = t.input(tensor_from(p, {S, win})), p += (int64_t)S * win;
+            v.rw = t.input(tensor_from(p, {3, 3 * S, 3, 3, 3})), p += 3 * 3 * S * 27;
+            v.rb = t.input(tensor_from(p, {3}));
+            lv.push_back(v);
+        }
+        // engine.hpp:191-216, level loop, with the encoder outputs supplied
+        Var phi;
+        std::vector<Var> res_v;
+        for (int k = 0; k < levels; ++k) {
+            const Dims3 d{dims[3 * k], dims[3 * k + 1], dims[3 * k + 2]};
+            Var phi_up, m_in = mv[k];
+            if (k > 0) {
+                phi_up = op_upsample_field_2x(t, phi, d);
+                m_in = op_warp(t, mv[k], phi_up);
+            }
+            ProjectionVars pv{lv[k].w, lv[k].b, lv[k].g, lv[k].be};
+            auto [q, key] = op_project_qk(t, fv[k], m_in, pv);
+            AttentionConfig acfg;
+            acfg.heads = heads[k];
+            acfg.head_dim = hd;
+            acfg.neighborhood = nb;
+            Var weights = op_na_fused(t, q, key, lv[k].bias, d, acfg);
+            Var stack = op_subfields(t, weights, d, acfg);
+            Var res = op_reghead_fuse(t, stack, lv[k].rw, lv[k].rb);
+            if (diffeomorphic) res = op_scaling_squaring(t, res, ss_steps);
+            phi = (k == 0) ? res : op_compose(t, phi_up, res);
+            res_v.push_back(res);
+        }
+        const Tensor<float> &pv = t.value(phi);
+        std::memcpy(phi_out, pv.data.data(), pv.data.size() * sizeof(float));
+        if (res_out)
+            for (int k = 0; k < levels; ++k)
+                if (res_out[k]) {
+                    const Tensor<float> &rv = t.value(res_v[k]);
+                    std::memcpy(res_out[k], rv.data.data(), rv.data.size() * sizeof(float));
+                }
+        if (!gphi) return 0;
+        Var loss = op_sum_all(t, op_mul(t, phi, t.input(tensor_from(gphi, pv.shape))));
+        t.backward(loss);
+        for (int k = 0; k < levels; ++k) {
+            if (gf && gf[k]) add_into(gf[k], t.grad(fv[k]));
+            if (gm && gm[k]) add_into(gm[k], t.grad(mv[k]));
+            if (gparams && gparams[k]) {
+                float *g = gparams[k];
+                for (Var v : {lv[k].w, lv[k].b, lv[k].g, lv[k].be, lv[k].bias, lv[k].rw,
+                              lv[k].rb}) {
+                    const Tensor<float> &gt = t.grad(v);
+                    add_into(g, gt);
+                    g += gt.data.size();
+                }
+            }
+        }
+    } catch (const std::exception &e) {
+        g_perr = e.what();
+        return 1;
+    }
+    return 0;
+}
+
+}  // extern "C"
