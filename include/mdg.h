@@ -166,6 +166,88 @@ mdg_status mdg_modet_bwd(const float *Q, const float *K, const float *B, const f
                          int layout, float *gQ, float *gK, float *gB, int accumulate,
                          void *stream);
 
+/* Q/K projection (attention.hpp:351-356 op_project_qk = op_layer_norm(
+ * op_linear_proj(.)) ops.hpp:387-497, shared weights, LN eps 1e-5 over all
+ * K = S*hd outputs of a voxel).  f, m {C, n} channel-major; weight {K, C};
+ * bias, ln_g, ln_b {K}.  Q, K written in `layout` (MDG_QK_POSMAJOR = the
+ * reference {n, K}; MDG_QK_PLANAR = {K, n}, what the fused tier reads).  m/K
+ * may both be NULL to project one input. */
+mdg_status mdg_project_qk_fwd(const float *f, const float *m, int C, int64_t n,
+                              const float *weight, const float *bias, const float *ln_g,
+                              const float *ln_b, int K, int layout, float *Q, float *Kout,
+                              void *stream);
+/* backward (ops.hpp:414-433, 462-494): accumulates gf, gm {C, n} and the
+ * parameter gradients; every output pointer nullable; K <= 64 */
+mdg_status mdg_project_qk_bwd(const float *f, const float *m, int C, int64_t n,
+                              const float *weight, const float *bias, const float *ln_g, int K,
+                              int layout, const float *gQ, const float *gK, float *gf,
+                              float *gm, float *gweight, float *gbias, float *gln_g,
+                              float *gln_b, void *stream);
+
+/* ======================== decoding pyramid driver ========================
+ * The decoder half of build_pipeline (engine.hpp:179-219) on device-resident
+ * encoder features: per level k (coarse -> fine)
+ *     phi_up = upsample_field_2x(phi)          (k > 0, ops.hpp:258)
+ *     m_in   = warp(m_k, phi_up)               (k > 0, ops.hpp:275)
+ *     Q, K   = project_qk(f_k, m_in)           (attention.hpp:351)
+ *     SF     = ModeT(Q, K, rel_bias)           (fused tier)
+ *     res    = reghead conv3(SF)               (reghead.hpp:42)
+ *     res    = scaling_squaring(res)           (if diffeomorphic, reghead.hpp:52)
+ *     phi    = k == 0 ? res : compose(phi_up, res)   (ops.hpp:295)
+ * The object owns the saved activations; backward replays the levels in
+ * reverse (the tape order of engine.hpp) and ACCUMULATES into the parameter
+ * and feature gradients. */
+#define MDG_MAX_LEVELS 8
+typedef struct {
+    int levels;                         /* EncoderConfig::levels (<= MDG_MAX_LEVELS) */
+    int heads[MDG_MAX_LEVELS];          /* ModelConfig::heads_per_level, coarse -> fine */
+    int channels[MDG_MAX_LEVELS];       /* feature channels per level, coarse -> fine */
+    mdg_dims3 dims[MDG_MAX_LEVELS];     /* level grids, coarse -> fine */
+    int head_dim;                       /* ModelConfig::head_dim */
+    int neighborhood;                   /* must be 3 on the fused tier */
+    int diffeomorphic;                  /* ModelConfig::diffeomorphic */
+    int ss_steps;                       /* ModelConfig::ss_steps */
+    int check_finite;                   /* !=0: forward syncs and raises the non-finite
+                                           logit error (attention.hpp:110-114); backward
+                                           raises on a non-finite gradient
+                                           (tape.hpp:116-120) */
+} mdg_pyramid_config;
+
+/* LevelParams (engine.hpp:108-112), device pointers */
+typedef struct {
+    const float *proj_w;   /* {S*hd, C} */
+    const float *proj_b;   /* {S*hd} */
+    const float *ln_g;     /* {S*hd} */
+    const float *ln_b;     /* {S*hd} */
+    const float *rel_bias; /* {S, nb^3} */
+    const float *rh_w;     /* {3, 3S, 3, 3, 3} */
+    const float *rh_b;     /* {3} */
+} mdg_level_params;
+
+/* gradients of LevelParams (accumulated; each pointer nullable) */
+typedef struct {
+    float *proj_w, *proj_b, *ln_g, *ln_b, *rel_bias, *rh_w, *rh_b;
+} mdg_level_grads;
+
+typedef struct mdg_pyramid mdg_pyramid;
+
+/* validates the config (ModelConfig::validate engine.hpp:64-78, level dims
+ * must chain by check_upsample_target) and allocates the saved activations */
+mdg_status mdg_pyramid_create(const mdg_pyramid_config *cfg, mdg_pyramid **out);
+void mdg_pyramid_destroy(mdg_pyramid *p);
+/* f_feats[k], m_feats[k]: {C_k, n_k}; params[k]; writes phi {3, n_fine} and,
+ * if `residuals` and residuals[k] are non-NULL, each level's residual. */
+mdg_status mdg_pyramid_forward(mdg_pyramid *p, const float *const *f_feats,
+                               const float *const *m_feats, const mdg_level_params *params,
+                               float *phi, float *const *residuals, void *stream);
+/* backward of the last forward with dloss/dphi = gphi {3, n_fine}.  grads
+ * (array of `levels`, nullable), gf / gm (arrays of `levels` feature-gradient
+ * pointers, nullable, entries nullable) accumulate. */
+mdg_status mdg_pyramid_backward(mdg_pyramid *p, const float *gphi, const mdg_level_grads *grads,
+                                float *const *gf, float *const *gm, void *stream);
+/* bytes of device memory the pyramid object holds */
+int64_t mdg_pyramid_bytes(const mdg_pyramid *p);
+
 /* layout adapters between the reference {n, C} and native {C, n} */
 mdg_status mdg_qk_posmajor_to_planar(const float *src, int64_t n, int C, float *dst,
                                      void *stream);

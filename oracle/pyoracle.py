@@ -81,6 +81,95 @@ class _Lib:
         self._comp_fwd = sig("compose_fwd", None, _f, _f, ii, ii, ii, _f)
         self._comp_bwd = sig("compose_bwd", None, _f, _f, ii, ii, ii, _f, _f, _f)
         self._ss = sig("scaling_squaring", None, _f, ii, ii, ii, ii, _f)
+        i64 = C.c_int64
+        if prefix == "mdo_":
+            self._lin_fwd = sig("linear_proj_fwd", None, _f, ii, i64, _f, _f, ii, _f)
+            self._lin_bwd = sig("linear_proj_bwd", None, _f, ii, i64, _f, ii, _f, _f, _f, _f)
+            self._ln_fwd = sig("layer_norm_fwd", None, _f, i64, ii, _f, _f, C.c_float, _f)
+            self._ln_bwd = sig("layer_norm_bwd", None, _f, i64, ii, _f, C.c_float, _f, _f, _f,
+                               _f)
+        else:
+            self._pqk = sig("project_qk", ii, _f, _f, ii, ii, ii, ii, _f, _f, _f, _f, ii, _f, _f,
+                            _f, _f, _f, _f, _f, _f, _f, _f)
+            pp = C.POINTER(_f)
+            self._decoder = sig("decoder", ii, ii, _i, _i, _i, ii, ii, ii, ii, pp, pp, pp, _f,
+                                _f, pp, pp, pp, pp)
+            self._perr = sig("pipeline_error", C.c_char_p)
+            self._lpc = sig("level_param_count", i64, ii, ii, ii, ii)
+
+    # -- Q/K projection (ops.hpp:387-497, attention.hpp:351-356) -----------
+    def project_qk(self, f, m, weight, bias, ln_g, ln_b, gQ=None, gK=None):
+        """Q, K position-major {n, K}; with gQ/gK also returns the gradients
+        (gf, gm, gweight, gbias, gln_g, gln_b) of sum(Q*gQ) + sum(K*gK)."""
+        Cc = f.shape[0]
+        n = f.size // Cc
+        Kd = weight.shape[0]
+        grads = None
+        if self.prefix == "mdo_":
+            eps = C.c_float(1e-5)
+            outs = []
+            raws = []
+            for x in (f, m):
+                raw = np.zeros((n, Kd), np.float32)
+                self._lin_fwd(_fp(x), Cc, n, _fp(weight), _fp(bias), Kd, _fp(raw))
+                out = np.zeros((n, Kd), np.float32)
+                self._ln_fwd(_fp(raw), n, Kd, _fp(ln_g), _fp(ln_b), eps, _fp(out))
+                raws.append(raw)
+                outs.append(out)
+            if gQ is not None:
+                grads = [np.zeros_like(f), np.zeros_like(m), np.zeros_like(weight),
+                         np.zeros_like(bias), np.zeros_like(ln_g), np.zeros_like(ln_b)]
+                # tape order: K's nodes were pushed last, so they replay first
+                for x, raw, g, gx in ((m, raws[1], gK, grads[1]), (f, raws[0], gQ, grads[0])):
+                    graw = np.zeros((n, Kd), np.float32)
+                    self._ln_bwd(_fp(raw), n, Kd, _fp(ln_g), eps, _fp(g), _fp(graw),
+                                 _fp(grads[4]), _fp(grads[5]))
+                    self._lin_bwd(_fp(x), Cc, n, _fp(weight), Kd, _fp(graw), _fp(gx),
+                                  _fp(grads[2]), _fp(grads[3]))
+            return (outs[0], outs[1], grads) if gQ is not None else (outs[0], outs[1])
+        l, w, h = f.shape[1:]
+        Q = np.zeros((n, Kd), np.float32)
+        K = np.zeros((n, Kd), np.float32)
+        if gQ is not None:
+            grads = [np.zeros_like(f), np.zeros_like(m), np.zeros_like(weight),
+                     np.zeros_like(bias), np.zeros_like(ln_g), np.zeros_like(ln_b)]
+        g = grads or [None] * 6
+        rc = self._pqk(_fp(f), _fp(m), Cc, h, w, l, _fp(weight), _fp(bias), _fp(ln_g),
+                       _fp(ln_b), Kd, _fp(Q), _fp(K), _fp(gQ), _fp(gK), *[_fp(x) for x in g])
+        if rc:
+            raise RuntimeError(self._perr().decode())
+        return (Q, K, grads) if gQ is not None else (Q, K)
+
+    def decoder(self, dims, channels, heads, hd, f_feats, m_feats, params, gphi=None,
+                diffeomorphic=False, ss_steps=7, nb=3):
+        """Reference decoding pyramid (engine.hpp:189-216) on given features,
+        coarse -> fine.  params[k]: packed level block (ModelParams order).
+        Returns phi, residuals and (with gphi) (gparams, gf, gm)."""
+        assert self.prefix == "mdr_"
+        L = len(dims)
+        dims_c = (C.c_int * (3 * L))(*[int(v) for d in dims for v in d])
+        ch_c = (C.c_int * L)(*channels)
+        hd_c = (C.c_int * L)(*heads)
+        P = C.POINTER(C.c_float)
+        arr = lambda xs: (P * L)(*[_fp(x) for x in xs])  # noqa: E731
+        fine = dims[-1]
+        phi = np.zeros((3, fine[2], fine[1], fine[0]), np.float32)
+        res = [np.zeros((3, d[2], d[1], d[0]), np.float32) for d in dims]
+        gparams = gf = gm = None
+        if gphi is not None:
+            gparams = [np.zeros_like(p) for p in params]
+            gf = [np.zeros_like(x) for x in f_feats]
+            gm = [np.zeros_like(x) for x in m_feats]
+        rc = self._decoder(L, dims_c, ch_c, hd_c, hd, nb, int(diffeomorphic), ss_steps,
+                           arr(f_feats), arr(m_feats), arr(params), _fp(gphi), _fp(phi),
+                           arr(res), arr(gparams) if gparams else None,
+                           arr(gf) if gf else None, arr(gm) if gm else None)
+        if rc:
+            raise RuntimeError(self._perr().decode())
+        return (phi, res, (gparams, gf, gm)) if gphi is not None else (phi, res)
+
+    def level_param_count(self, C_, S, hd, nb=3):
+        return int(self._lpc(C_, S, hd, nb))
 
     # -- attention ---------------------------------------------------------
     def window_offset(self, o, nb=3):

@@ -29,6 +29,31 @@ class Dims3(C.Structure):
         return f"Dims3({self.h}, {self.w}, {self.l})"
 
 
+MAX_LEVELS = 8
+
+
+class PyramidConfig(C.Structure):
+    """mdg_pyramid_config (ModelConfig + level geometry, engine.hpp:30-78)."""
+
+    _fields_ = [("levels", C.c_int), ("heads", C.c_int * MAX_LEVELS),
+                ("channels", C.c_int * MAX_LEVELS), ("dims", Dims3 * MAX_LEVELS),
+                ("head_dim", C.c_int), ("neighborhood", C.c_int),
+                ("diffeomorphic", C.c_int), ("ss_steps", C.c_int), ("check_finite", C.c_int)]
+
+
+LEVEL_FIELDS = ("proj_w", "proj_b", "ln_g", "ln_b", "rel_bias", "rh_w", "rh_b")
+
+
+class LevelParams(C.Structure):
+    """mdg_level_params (LevelParams, engine.hpp:108-112)."""
+
+    _fields_ = [(f, C.c_void_p) for f in LEVEL_FIELDS]
+
+
+class LevelGrads(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in LEVEL_FIELDS]
+
+
 _p = C.c_void_p  # device or host pointer
 _i = C.c_int
 _f = C.c_float
@@ -61,6 +86,16 @@ SIGNATURES = {
     "mdg_scaling_squaring_bwd": (_st, [_p, Dims3, _i, _p, _p, _p]),
     "mdg_modet_fwd": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p, _p]),
     "mdg_modet_bwd": (_st, [_p, _p, _p, _p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p, _i, _p]),
+    "mdg_project_qk_fwd": (_st, [_p, _p, _i, C.c_int64, _p, _p, _p, _p, _i, _i, _p, _p, _p]),
+    "mdg_project_qk_bwd": (_st, [_p, _p, _i, C.c_int64, _p, _p, _p, _i, _i, _p, _p, _p, _p,
+                                 _p, _p, _p, _p, _p]),
+    "mdg_pyramid_create": (_st, [C.POINTER(PyramidConfig), C.POINTER(_p)]),
+    "mdg_pyramid_destroy": (None, [_p]),
+    "mdg_pyramid_forward": (_st, [_p, C.POINTER(_p), C.POINTER(_p), C.POINTER(LevelParams), _p,
+                                  C.POINTER(_p), _p]),
+    "mdg_pyramid_backward": (_st, [_p, _p, C.POINTER(LevelGrads), C.POINTER(_p), C.POINTER(_p),
+                                   _p]),
+    "mdg_pyramid_bytes": (C.c_int64, [_p]),
     "mdg_qk_posmajor_to_planar": (_st, [_p, C.c_int64, _i, _p, _p]),
     "mdg_qk_planar_to_posmajor": (_st, [_p, C.c_int64, _i, _p, _p]),
     "mdg_na_fused_fwd_host": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _p]),

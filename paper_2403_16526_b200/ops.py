@@ -393,6 +393,181 @@ def qk_planar_to_posmajor(x):
     return out
 
 
+@dataclass
+class ProjectionParams:
+    """attention.hpp:323-328 (weight {K, C}, bias / ln_gamma / ln_beta {K})."""
+
+    weight: torch.Tensor
+    bias: torch.Tensor
+    ln_gamma: torch.Tensor
+    ln_beta: torch.Tensor
+
+
+def project_qk(f, m, p: ProjectionParams, layout=MDG_QK_POSMAJOR):
+    """op_project_qk forward (attention.hpp:351-356): Q = LN(W F + b),
+    K = LN(W M + b).  f, m {C, n...}; returns Q, K as {n, K} (posmajor) or
+    {K, n} (planar)."""
+    Cc = f.shape[0]
+    n = f.numel() // Cc
+    if m.shape != f.shape:
+        raise InvalidInput("project_qk: shape mismatch")
+    if p.weight.dim() != 2 or p.weight.shape[1] != Cc:
+        raise InvalidInput("linear_proj: weight shape must be {K,c} with matching channels")
+    Kd = p.weight.shape[0]
+    if p.bias.numel() != Kd:
+        raise InvalidInput("linear_proj: bias size mismatch")
+    if p.ln_gamma.numel() != Kd or p.ln_beta.numel() != Kd:
+        raise InvalidInput("layer_norm: affine size mismatch")
+    shape = (n, Kd) if layout == MDG_QK_POSMAJOR else (Kd, n)
+    Q, K = _empty(*shape, like=f), _empty(*shape, like=f)
+    _check(_capi.lib().mdg_project_qk_fwd(_ptr(f), _ptr(m), Cc, n, _ptr(p.weight), _ptr(p.bias),
+                                          _ptr(p.ln_gamma), _ptr(p.ln_beta), Kd, layout,
+                                          _ptr(Q), _ptr(K), _stream()))
+    return Q, K
+
+
+def project_qk_bwd(f, m, p: ProjectionParams, gQ, gK, layout=MDG_QK_POSMAJOR, gf=None, gm=None,
+                   grads: ProjectionParams | None = None):
+    """Backward of op_project_qk; accumulates into (and returns) gf, gm and the
+    parameter gradients (a ProjectionParams of gradient tensors)."""
+    Cc = f.shape[0]
+    n = f.numel() // Cc
+    Kd = p.weight.shape[0]
+    gf = torch.zeros_like(f) if gf is None else gf
+    gm = torch.zeros_like(m) if gm is None else gm
+    if grads is None:
+        grads = ProjectionParams(torch.zeros_like(p.weight), torch.zeros_like(p.bias),
+                                 torch.zeros_like(p.ln_gamma), torch.zeros_like(p.ln_beta))
+    _check(_capi.lib().mdg_project_qk_bwd(
+        _ptr(f), _ptr(m), Cc, n, _ptr(p.weight), _ptr(p.bias), _ptr(p.ln_gamma), Kd, layout,
+        _ptr(gQ), _ptr(gK), _ptr(gf), _ptr(gm), _ptr(grads.weight), _ptr(grads.bias),
+        _ptr(grads.ln_gamma), _ptr(grads.ln_beta), _stream()))
+    return gf, gm, grads
+
+
+@dataclass
+class LevelParams:
+    """engine.hpp:108-112 LevelParams (projection, rel_pos_bias {S, 27},
+    RegHead weight {3, 3S, 3, 3, 3} and bias {3})."""
+
+    proj: ProjectionParams
+    rel_pos_bias: torch.Tensor
+    rh_weight: torch.Tensor
+    rh_bias: torch.Tensor
+
+    def tensors(self):
+        """ModelParams::all_tensors order (engine.hpp:127-131)."""
+        return [self.proj.weight, self.proj.bias, self.proj.ln_gamma, self.proj.ln_beta,
+                self.rel_pos_bias, self.rh_weight, self.rh_bias]
+
+    @staticmethod
+    def from_tensors(ts):
+        return LevelParams(ProjectionParams(*ts[:4]), ts[4], ts[5], ts[6])
+
+    def zeros_like(self):
+        return LevelParams.from_tensors([torch.zeros_like(t) for t in self.tensors()])
+
+
+@dataclass
+class ModelConfig:
+    """engine.hpp:30-78 (decoder part): heads coarse -> fine, head_dim,
+    neighborhood, diffeomorphic + ss_steps."""
+
+    heads_per_level: tuple = (8, 4, 2, 1, 1)
+    head_dim: int = 6
+    neighborhood: int = 3
+    diffeomorphic: bool = False
+    ss_steps: int = 7
+
+
+class Pyramid:
+    """The decoding pyramid (build_pipeline engine.hpp:179-219 minus the encoder)
+    on device-resident features, driven by libmdg's native driver.
+
+    ``dims`` / ``channels``: level grids and feature channels, coarse -> fine."""
+
+    def __init__(self, cfg: ModelConfig, dims, channels, check_finite=True):
+        L = len(dims)
+        if len(cfg.heads_per_level) != L or len(channels) != L:
+            raise InvalidInput("model: heads_per_level must have one entry per level")
+        if L > _capi.MAX_LEVELS:
+            raise InvalidInput("pyramid: too many levels")
+        c = _capi.PyramidConfig()
+        c.levels = L
+        for k in range(L):
+            c.heads[k] = int(cfg.heads_per_level[k])
+            c.channels[k] = int(channels[k])
+            c.dims[k] = dims3(dims[k])
+        c.head_dim, c.neighborhood = cfg.head_dim, cfg.neighborhood
+        c.diffeomorphic, c.ss_steps = int(cfg.diffeomorphic), cfg.ss_steps
+        c.check_finite = int(check_finite)
+        self.cfg, self.dims, self.channels = cfg, [tuple(d) for d in dims], list(channels)
+        self._L = _capi.lib()
+        h = C.c_void_p()
+        _check(self._L.mdg_pyramid_create(C.byref(c), C.byref(h)))
+        self._h = h
+        self._keep = None
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._L.mdg_pyramid_destroy(self._h)
+        except Exception:
+            pass
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self._L.mdg_pyramid_bytes(self._h))
+
+    @staticmethod
+    def _ptrs(ts):
+        arr = (C.c_void_p * len(ts))()
+        for i, t in enumerate(ts):
+            arr[i] = _ptr(t) if t is not None else None
+        return arr
+
+    @staticmethod
+    def _level_structs(levels, cls):
+        arr = (cls * len(levels))()
+        for i, lp in enumerate(levels):
+            for f, t in zip(_capi.LEVEL_FIELDS, lp.tensors()):
+                setattr(arr[i], f, _ptr(t) if t is not None else None)
+        return arr
+
+    def forward(self, f_feats, m_feats, params, want_residuals=False):
+        """Returns phi {3, fine dims} (and the per-level residuals)."""
+        L = len(self.dims)
+        fine = self.dims[-1]
+        phi = torch.empty(3, fine[2], fine[1], fine[0], dtype=torch.float32,
+                          device=f_feats[-1].device)
+        res = [torch.empty(3, d[2], d[1], d[0], dtype=torch.float32, device=phi.device)
+               for d in self.dims] if want_residuals else None
+        for k in range(L):
+            n = voxel_count(self.dims[k])
+            if f_feats[k].numel() != self.channels[k] * n or m_feats[k].shape != f_feats[k].shape:
+                raise InvalidInput(f"pyramid: level {k} feature shape mismatch")
+        fp, mp = self._ptrs(f_feats), self._ptrs(m_feats)
+        ps = self._level_structs(params, _capi.LevelParams)
+        rp = self._ptrs(res) if res is not None else None
+        self._keep = (list(f_feats), list(m_feats), list(params))  # saved for backward
+        _check(self._L.mdg_pyramid_forward(self._h, fp, mp, ps, _ptr(phi), rp, _stream()))
+        return (phi, res) if want_residuals else phi
+
+    def backward(self, gphi, grads=None, gf=None, gm=None):
+        """Accumulates into grads (list of LevelParams of gradient tensors) and the
+        feature gradients gf / gm (lists); returns (grads, gf, gm)."""
+        if self._keep is None:
+            raise InvalidInput("pyramid: backward without a forward")
+        f_feats, m_feats, params = self._keep
+        grads = [p.zeros_like() for p in params] if grads is None else grads
+        gf = [torch.zeros_like(t) for t in f_feats] if gf is None else gf
+        gm = [torch.zeros_like(t) for t in m_feats] if gm is None else gm
+        gs = self._level_structs(grads, _capi.LevelGrads)
+        _check(self._L.mdg_pyramid_backward(self._h, _ptr(gphi), gs, self._ptrs(gf),
+                                            self._ptrs(gm), _stream()))
+        return grads, gf, gm
+
+
 def launch_count() -> int:
     return int(_capi.lib().mdg_launch_count())
 

@@ -1,0 +1,192 @@
+"""GPU parity of the Q/K projection and the decoding pyramid driver.
+
+* project_qk (attention.hpp:351-356 = LN(linear)) forward vs the oracle
+  restatement (bit-pinned to the reference in test_oracle.py): elementwise
+  |d| <= 1e-5 + 1e-4|ref| (FMA vs separate mul/add); backward per-tensor
+  ||d||/||g|| <= 1e-4 (full-volume reductions in a different order).
+* the pyramid (build_pipeline engine.hpp:179-219 on given encoder features) vs
+  the REFERENCE's own tape (oracle/_ref, ref_pipeline.cpp): phi and residuals
+  elementwise, every parameter / feature gradient by relative norm (1e-4;
+  1e-3 for the cancellation-dominated pre-LayerNorm projection bias).
+"""
+import numpy as np
+import pytest
+import torch
+
+from _util import decoder_case, f32, rel_close, rel_norm, split_level_params, worst
+from paper_2403_16526_b200 import ops
+from paper_2403_16526_b200._capi import MDG_QK_PLANAR, MDG_QK_POSMAJOR
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def proj_case(C, K, dims, seed):
+    r = np.random.default_rng(seed)
+    h, w, l = dims
+    f = f32(r.standard_normal((C, l, w, h)))
+    m = f32(r.standard_normal((C, l, w, h)))
+    p = [f32(r.standard_normal((K, C)) * 0.3), f32(r.standard_normal(K) * 0.1),
+         f32(r.uniform(0.5, 1.5, K)), f32(r.standard_normal(K) * 0.2)]
+    n = h * w * l
+    gQ = f32(r.standard_normal((n, K)))
+    gK = f32(r.standard_normal((n, K)))
+    return f, m, p, gQ, gK
+
+
+@pytest.mark.parametrize("C,K,dims", [(8, 6, (9, 7, 5)), (16, 6, (12, 10, 8)), (32, 12, (7, 6, 5)),
+                                      (64, 24, (5, 4, 3)), (128, 48, (3, 3, 2)), (4, 1, (6, 5, 4)),
+                                      (3, 64, (4, 4, 4)), (5, 70, (3, 3, 3))])
+@pytest.mark.parametrize("layout", [MDG_QK_POSMAJOR, MDG_QK_PLANAR])
+def test_project_qk_matches_oracle(cuda, oracle, C, K, dims, layout):
+    f, m, p, gQ, gK = proj_case(C, K, dims, seed=C * 100 + K)
+    Qr, Kr, gr = oracle.project_qk(f, m, *p, gQ, gK)
+    pp = ops.ProjectionParams(*[dev(x) for x in p])
+    Q, Kt = ops.project_qk(dev(f), dev(m), pp, layout=layout)
+    Q, Kt = host(Q), host(Kt)
+    if layout == MDG_QK_PLANAR:
+        Q, Kt = Q.T, Kt.T
+    assert rel_close(Q, Qr), worst(Q, Qr)
+    assert rel_close(Kt, Kr), worst(Kt, Kr)
+    if K > 64:
+        with pytest.raises(ops.InvalidInput):
+            ops.project_qk_bwd(dev(f), dev(m), pp, dev(gQ), dev(gK), layout=layout)
+        return
+    gq, gk = dev(gQ), dev(gK)
+    if layout == MDG_QK_PLANAR:
+        gq, gk = dev(f32(gQ.T)), dev(f32(gK.T))
+    # accumulate semantics: start from ones, subtract afterwards
+    gf0 = torch.ones_like(dev(f))
+    gf, gm, g = ops.project_qk_bwd(dev(f), dev(m), pp, gq, gk, layout=layout, gf=gf0)
+    got = [host(gf) - 1.0, host(gm), host(g.weight), host(g.bias), host(g.ln_gamma),
+           host(g.ln_beta)]
+    for name, a, b in zip(["gf", "gm", "gw", "gb", "gg", "gbeta"], got, gr):
+        assert rel_norm(a, b) <= 1e-4, (name, rel_norm(a, b))
+
+
+def test_project_qk_reference_kats(cuda):
+    """test_attention.cpp:35-74: identical inputs -> identical Q and K; zero
+    weights with an LN shift beta give exactly beta."""
+    r = np.random.default_rng(1)
+    f = f32(r.standard_normal((8, 4, 4, 4)))
+    p = ops.ProjectionParams(dev(f32(r.standard_normal((12, 8)) * 1e-5)), dev(np.zeros(12, np.float32)),
+                             dev(np.ones(12, np.float32)), dev(np.zeros(12, np.float32)))
+    Q, K = ops.project_qk(dev(f), dev(f), p)
+    assert np.array_equal(host(Q), host(K))
+    beta = f32(0.1 * np.arange(6) - 0.2)
+    p0 = ops.ProjectionParams(dev(np.zeros((6, 4), np.float32)), dev(np.zeros(6, np.float32)),
+                              dev(np.ones(6, np.float32)), dev(beta))
+    f4 = f32(r.standard_normal((4, 3, 3, 3)))
+    Q, _ = ops.project_qk(dev(f4), dev(f4), p0)
+    assert np.allclose(host(Q), np.broadcast_to(beta, (27, 6)), rtol=1e-6, atol=0)
+
+
+def _torch_levels(params, channels, heads, hd):
+    out = []
+    for k, pk in enumerate(params):
+        ts = [dev(f32(x)) for x in split_level_params(pk, channels[k], heads[k], hd)]
+        out.append(ops.LevelParams.from_tensors(ts))
+    return out
+
+
+def _pack(lp):
+    return np.concatenate([host(t).ravel() for t in lp.tensors()])
+
+
+CASES = [
+    # fine dims, levels, channels (coarse->fine), heads, hd, diffeomorphic
+    ((16, 14, 12), 3, (32, 16, 8), (2, 1, 1), 6, False),
+    ((32, 32, 32), 5, (128, 64, 32, 16, 8), (8, 4, 2, 1, 1), 6, False),
+    ((13, 11, 9), 4, (16, 16, 8, 8), (4, 2, 2, 1), 4, False),
+    ((12, 10, 8), 3, (8, 8, 8), (2, 2, 1), 6, True),
+    ((9, 8, 7), 1, (8,), (2,), 6, False),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-L{c[1]}-ss{int(c[5])}")
+def test_pyramid_matches_reference(cuda, ref, case):
+    fine, L, channels, heads, hd, diffeo = case
+    dims, f_feats, m_feats, params = decoder_case(fine, L, channels, heads, hd, seed=sum(fine) + L)
+    r = np.random.default_rng(7)
+    gphi = f32(r.standard_normal((3, fine[2], fine[1], fine[0])))
+    phi_r, res_r, (gp_r, gf_r, gm_r) = ref.decoder(dims, channels, heads, hd, f_feats, m_feats,
+                                                    params, gphi, diffeomorphic=diffeo, ss_steps=4)
+    cfg = ops.ModelConfig(heads_per_level=heads, head_dim=hd, diffeomorphic=diffeo, ss_steps=4)
+    pyr = ops.Pyramid(cfg, dims, channels)
+    lp = _torch_levels(params, channels, heads, hd)
+    ff, mf = [dev(x) for x in f_feats], [dev(x) for x in m_feats]
+    phi, res = pyr.forward(ff, mf, lp, want_residuals=True)
+    assert rel_close(host(phi), phi_r), worst(host(phi), phi_r)
+    for k in range(L):
+        assert rel_close(host(res[k]), res_r[k]), (k, worst(host(res[k]), res_r[k]))
+    grads, gf, gm = pyr.backward(dev(gphi))
+    for k in range(L):
+        names = ["proj.w", "proj.b", "ln_g", "ln_b", "rel_bias", "rh_w", "rh_b"]
+        ours = [host(t) for t in grads[k].tensors()]
+        theirs = split_level_params(gp_r[k], channels[k], heads[k], hd)
+        for nm, a, b in zip(names, ours, theirs):
+            # proj.b feeds the LayerNorm: its gradient sums to exactly 0 over k
+            # and is a cancellation-dominated sum over voxels, so (like the
+            # pre-norm conv biases in SURVEY §8c) it gets a looser bound
+            tol = 1e-3 if nm == "proj.b" else 1e-4
+            assert rel_norm(a, b) <= tol, (k, nm, rel_norm(a, b))
+        assert rel_norm(host(gf[k]), gf_r[k]) <= 1e-4, (k, "gf", rel_norm(host(gf[k]), gf_r[k]))
+        assert rel_norm(host(gm[k]), gm_r[k]) <= 1e-4, (k, "gm", rel_norm(host(gm[k]), gm_r[k]))
+
+
+def test_pyramid_backward_accumulates_and_repeats(cuda):
+    dims, f_feats, m_feats, params = decoder_case((12, 10, 8), 3, (8, 8, 8), (2, 1, 1), 6, seed=3)
+    cfg = ops.ModelConfig(heads_per_level=(2, 1, 1), head_dim=6)
+    pyr = ops.Pyramid(cfg, dims, (8, 8, 8))
+    lp = _torch_levels(params, (8, 8, 8), (2, 1, 1), 6)
+    ff, mf = [dev(x) for x in f_feats], [dev(x) for x in m_feats]
+    gphi = dev(f32(np.random.default_rng(0).standard_normal((3, 8, 10, 12))))
+    phi1 = host(pyr.forward(ff, mf, lp))
+    g1, gf1, gm1 = pyr.backward(gphi)
+    phi2 = host(pyr.forward(ff, mf, lp))
+    assert np.array_equal(phi1, phi2)  # deterministic, no state leaks between calls
+    once = [[host(t) for t in g.tensors()] for g in g1]
+    once_f = [host(t) for t in gf1]
+    g2, gf2, _ = pyr.backward(gphi, grads=g1, gf=gf1)  # accumulates on top
+    # the image-side warp/compose scatters use fp32 atomics, so repeated
+    # backwards agree to rounding, not bit for bit
+    for k in range(3):
+        for a, b in zip(g2[k].tensors(), once[k]):
+            assert rel_norm(host(a), 2 * b) <= 1e-5
+        assert rel_norm(host(gf2[k]), 2 * once_f[k]) <= 1e-5
+
+
+def test_pyramid_errors(cuda):
+    cfg = ops.ModelConfig(heads_per_level=(1, 2), head_dim=6)
+    with pytest.raises(ops.InvalidInput, match="non-increasing"):
+        ops.Pyramid(cfg, [(4, 4, 4), (8, 8, 8)], (8, 8))
+    cfg = ops.ModelConfig(heads_per_level=(1, 1), head_dim=6)
+    with pytest.raises(ops.InvalidInput, match="upsample"):
+        ops.Pyramid(cfg, [(4, 4, 4), (10, 8, 8)], (8, 8))
+    with pytest.raises(ops.InvalidInput):
+        ops.Pyramid(ops.ModelConfig(heads_per_level=(1,), neighborhood=4), [(4, 4, 4)], (8,))
+
+
+def test_pyramid_nonfinite_raises(cuda):
+    dims, f_feats, m_feats, params = decoder_case((10, 8, 6), 2, (8, 8), (1, 1), 6, seed=5)
+    cfg = ops.ModelConfig(heads_per_level=(1, 1), head_dim=6)
+    pyr = ops.Pyramid(cfg, dims, (8, 8))
+    lp = _torch_levels(params, (8, 8), (1, 1), 6)
+    ff, mf = [dev(x) for x in f_feats], [dev(x) for x in m_feats]
+    pyr.forward(ff, mf, lp)
+    gphi = np.zeros((3, 6, 8, 10), np.float32)
+    gphi[1, 2, 3, 4] = np.nan
+    with pytest.raises(ops.NumericError, match="non-finite gradient"):
+        pyr.backward(dev(gphi))
+    # a non-finite logit in the forward raises like attention.hpp:110-114
+    lp[0].rel_pos_bias.fill_(float("inf"))
+    with pytest.raises(ops.NumericError, match="non-finite logit"):
+        pyr.forward(ff, mf, lp)
