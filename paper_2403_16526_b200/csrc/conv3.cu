@@ -8,6 +8,8 @@
 // per-CTA partials over fixed voxel chunks, then a fixed-order tree — the
 // result is deterministic (run to run) and within fp32 reduction tolerance of
 // the reference's sequential sums.
+#include <algorithm>
+
 #include "mdg_common.cuh"
 
 namespace mdg {
@@ -16,10 +18,11 @@ constexpr int kCB = 256;
 constexpr int kChunkPerThread = 8;
 
 __device__ __forceinline__ void xyz3(int64_t p, int h, int w, int &x, int &y, int &z) {
-    x = (int)(p % h);
-    const int64_t t = p / h;
-    y = (int)(t % w);
-    z = (int)(t / w);
+    const int p32 = (int)p;  // n < 2^31 (dims_ok): 32-bit div/mod
+    const int t = p32 / h;
+    x = p32 - t * h;
+    z = t / w;
+    y = t - z * w;
 }
 
 // ops.hpp:58-74
@@ -152,6 +155,269 @@ conv3_bwd_w_final_k(const float *__restrict__ part, int nparts, int ic,
     }
 }
 
+// ------------------------------------------------------------ tiled (oc == 3)
+// The RegHead shape (3S -> 3).  A CTA of 32x8 threads covers a 32x8x4 block:
+// each thread owns one (x, y) column of kV = 4 consecutive z voxels, so every
+// weight read from shared memory feeds kV voxels and every staged tap value
+// feeds all three output channels.  Input planes z0-1 .. z0+kV of a chunk of
+// channels are staged with a one-voxel zero halo, so taps need no bounds
+// checks.  Each output keeps the reference's term order (bias, then
+// channel-major, taps dz/dy/dx) with products and sums rounded separately and
+// zero weights skipped (ops.hpp:69): fwd and gin are bit-identical to the CPU
+// reference (an out-of-range tap adds kv*0 = +-0, leaving the sum unchanged).
+constexpr int kTX = 32, kTY = 8, kV = 4;
+constexpr int kHX = kTX + 2, kHY = kTY + 2, kHZ = kV + 2;
+constexpr int kPlaneXY = kHY * kHX;
+constexpr int kSlab = kHZ * kPlaneXY;  // one channel: kV+2 z planes with halo
+constexpr int kChunk = 2;             // channels staged per pass
+
+// Staging of nch channel slabs: every element the thread copies is first
+// loaded into registers (all loads in flight together), then stored, so a
+// stage costs about one global-load latency instead of one per element.
+// Rows are kHX wide; lanes run along x, so the index decomposition and the
+// y/z bounds test are per row.  nch <= kMaxStageCh.
+constexpr int kStageRows = kHZ * kHY;  // per channel
+
+template <int MAXCH>
+__device__ __forceinline__ void stage_slab(float *dst, const float *__restrict__ src, int nch,
+                                           int h, int w, int l, int x0, int y0, int z0) {
+    constexpr int kRowIters = (MAXCH * kStageRows + 7) / 8;  // per warp (8 warps)
+    const int64_t n = (int64_t)h * w * l;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int rows = nch * kStageRows;
+    const int gx0 = x0 - 1 + lane, gx1 = x0 - 1 + lane + 32;
+    const bool okx0 = gx0 >= 0 && gx0 < h, okx1 = lane + 32 < kHX && gx1 < h;
+    float v0[kRowIters], v1[kRowIters];
+#pragma unroll
+    for (int it = 0; it < kRowIters; ++it) {
+        const int r = wid + 8 * it;
+        v0[it] = 0.0f;
+        v1[it] = 0.0f;
+        if (r < rows) {
+            const int c = r / kStageRows, rr = r - c * kStageRows;
+            const int dz = rr / kHY, yy = rr - dz * kHY;
+            const int gy = y0 - 1 + yy, gz = z0 - 1 + dz;
+            if (gy >= 0 && gy < w && gz >= 0 && gz < l) {
+                const float *srow = src + (int64_t)c * n + ((int64_t)gz * w + gy) * h;
+                if (okx0) v0[it] = __ldg(srow + gx0);
+                if (okx1) v1[it] = __ldg(srow + gx1);
+            }
+        }
+    }
+#pragma unroll
+    for (int it = 0; it < kRowIters; ++it) {
+        const int r = wid + 8 * it;
+        if (r < rows) {
+            dst[r * kHX + lane] = v0[it];
+            if (lane + 32 < kHX) dst[r * kHX + lane + 32] = v1[it];
+        }
+    }
+}
+
+template <int OC>
+__global__ void __launch_bounds__(kTX *kTY, 2)
+conv3_fwd_tiled_k(const float *__restrict__ in, int ic, int h, int w, int l,
+                  const float *__restrict__ k, const float *__restrict__ bias,
+                  float *__restrict__ out) {
+    extern __shared__ float sm[];
+    float *kw = sm;                   // [OC][ic][27]
+    float *slab = sm + OC * ic * 27;  // [kChunk][kHZ][kHY][kHX]
+    for (int i = threadIdx.x; i < OC * ic * 27; i += blockDim.x) kw[i] = k[i];
+    const int tx = threadIdx.x % kTX, ty = threadIdx.x / kTX;
+    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY, z0 = blockIdx.z * kV;
+    float acc[kV][OC];
+#pragma unroll
+    for (int co = 0; co < OC; ++co) {
+        const float b0 = bias ? __ldg(bias + co) : 0.0f;
+#pragma unroll
+        for (int v = 0; v < kV; ++v) acc[v][co] = b0;
+    }
+    for (int c0 = 0; c0 < ic; c0 += kChunk) {
+        const int nch = min(kChunk, ic - c0);
+        __syncthreads();
+        stage_slab<kChunk>(slab, in + (int64_t)c0 * h * w * l, nch, h, w, l, x0, y0, z0);
+        __syncthreads();
+        for (int cc = 0; cc < nch; ++cc) {
+            const float *tp = slab + cc * kSlab + ty * kHX + tx;
+            const float *kc = kw + (c0 + cc) * 27;
+#pragma unroll
+            for (int t = 0; t < 27; ++t) {
+                const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
+                float xv[kV];
+#pragma unroll
+                for (int v = 0; v < kV; ++v) xv[v] = tp[((v + dz) * kHY + dy) * kHX + dx];
+#pragma unroll
+                for (int co = 0; co < OC; ++co) {
+                    const float kv = kc[co * ic * 27 + t];
+                    if (kv == 0.0f) continue;  // ops.hpp:69 (uniform)
+#pragma unroll
+                    for (int v = 0; v < kV; ++v) acc[v][co] = add_(acc[v][co], mul_(kv, xv[v]));
+                }
+            }
+        }
+    }
+    const int x = x0 + tx, y = y0 + ty;
+    if (x >= h || y >= w) return;
+    const int64_t n = (int64_t)h * w * l;
+#pragma unroll
+    for (int v = 0; v < kV; ++v) {
+        if (z0 + v >= l) break;
+        const int64_t p = ((int64_t)(z0 + v) * w + y) * h + x;
+#pragma unroll
+        for (int co = 0; co < OC; ++co) out[co * n + p] = acc[v][co];
+    }
+}
+
+// gin[ci] += sum_co sum_t k[co,ci,t] gout[co](p - off(t)), order (co, t)
+// (ops.hpp:94-96).  gout planes are staged once; tap t of voxel v reads slab
+// position (v + 2 - dz, ty + 2 - dy, tx + 2 - dx).
+template <int OC>
+__global__ void __launch_bounds__(kTX *kTY)
+conv3_bwd_in_tiled_k(int ic, int h, int w, int l, const float *__restrict__ k,
+                     const float *__restrict__ gout, float *__restrict__ gin) {
+    extern __shared__ float sm[];
+    float *kw = sm;
+    float *slab = sm + OC * ic * 27;  // [OC][kHZ][kHY][kHX] of gout
+    for (int i = threadIdx.x; i < OC * ic * 27; i += blockDim.x) kw[i] = k[i];
+    const int tx = threadIdx.x % kTX, ty = threadIdx.x / kTX;
+    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY, z0 = blockIdx.z * kV;
+    stage_slab<OC>(slab, gout, OC, h, w, l, x0, y0, z0);
+    __syncthreads();
+    const int x = x0 + tx, y = y0 + ty;
+    if (x >= h || y >= w) return;
+    const int64_t n = (int64_t)h * w * l;
+    const int nv = min(kV, l - z0);
+    const int64_t p0 = ((int64_t)z0 * w + y) * h + x, hw = (int64_t)h * w;
+    const float *tp = slab + ty * kHX + tx;
+    for (int ci = 0; ci < ic; ++ci) {
+        float acc[kV];
+#pragma unroll
+        for (int v = 0; v < kV; ++v) acc[v] = v < nv ? gin[(int64_t)ci * n + p0 + v * hw] : 0.0f;
+#pragma unroll
+        for (int co = 0; co < OC; ++co) {
+            const float *kk = kw + (co * ic + ci) * 27;
+            const float *gp = tp + co * kSlab;
+#pragma unroll
+            for (int t = 0; t < 27; ++t) {
+                const float kv = kk[t];
+                if (kv == 0.0f) continue;
+                const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
+#pragma unroll
+                for (int v = 0; v < kV; ++v)
+                    acc[v] = add_(acc[v], mul_(kv, gp[((v + 2 - dz) * kHY + (2 - dy)) * kHX + (2 - dx)]));
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < kV; ++v)
+            if (v < nv) gin[(int64_t)ci * n + p0 + v * hw] = acc[v];
+    }
+}
+
+// kernel / bias gradients: blockIdx.y = input channel ci; a persistent grid
+// walks the 32x8x4 blocks, staging channel ci's slab (kV+2 planes with halo)
+// in shared memory; each thread holds gout of its kV voxels for all OC output
+// channels and accumulates acc[co][t] += gout[co](p) * in[ci](p + off(t)) in
+// registers (every staged tap value feeds OC accumulators), + the bias sums on
+// ci == 0; then a fixed-order block reduction -> per-CTA partials ->
+// fixed-order final sum (deterministic).
+template <int OC>
+__global__ void __launch_bounds__(kTX *kTY, 2)
+conv3_bwd_w_tiled_k(const float *__restrict__ in, int ic, int h, int w, int l,
+                    const float *__restrict__ gout, float *__restrict__ part) {
+    __shared__ float slab[kSlab];
+    __shared__ float red[kTX * kTY / 32];
+    const int ci = blockIdx.y;
+    const int tx = threadIdx.x % kTX, ty = threadIdx.x / kTX;
+    const int ntx = (h + kTX - 1) / kTX, nty = (w + kTY - 1) / kTY, ntz = (l + kV - 1) / kV;
+    const int ntiles = ntx * nty * ntz;
+    const int64_t n = (int64_t)h * w * l, hw = (int64_t)h * w;
+    float acc[OC][27], accb[OC];
+#pragma unroll
+    for (int co = 0; co < OC; ++co) {
+        accb[co] = 0.0f;
+#pragma unroll
+        for (int t = 0; t < 27; ++t) acc[co][t] = 0.0f;
+    }
+    const float *src = in + (int64_t)ci * n;
+    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        const int bx = ti % ntx, by = (ti / ntx) % nty, bz = ti / (ntx * nty);
+        const int x0 = bx * kTX, y0 = by * kTY, z0 = bz * kV;
+        __syncthreads();
+        stage_slab<1>(slab, src, 1, h, w, l, x0, y0, z0);
+        __syncthreads();
+        const int x = x0 + tx, y = y0 + ty;
+        const bool inxy = x < h && y < w;
+        const int64_t p0 = ((int64_t)z0 * w + y) * h + x;
+        float g[kV][OC];
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+            const bool ok = inxy && z0 + v < l;
+#pragma unroll
+            for (int co = 0; co < OC; ++co) {
+                g[v][co] = ok ? __ldg(gout + co * n + p0 + v * hw) : 0.0f;
+                accb[co] += g[v][co];
+            }
+        }
+        const float *tp = slab + ty * kHX + tx;
+#pragma unroll
+        for (int t = 0; t < 27; ++t) {
+            const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
+#pragma unroll
+            for (int v = 0; v < kV; ++v) {
+                const float xv = tp[((v + dz) * kHY + dy) * kHX + dx];
+#pragma unroll
+                for (int co = 0; co < OC; ++co) acc[co][t] = fmaf(g[v][co], xv, acc[co][t]);
+            }
+        }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float *dst = part + ((int64_t)ci * gridDim.x + blockIdx.x) * (OC * 28);
+    auto reduce = [&](float v, int slot) {
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+        if (lane == 0) red[wid] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float sum = 0.0f;
+#pragma unroll
+            for (int i = 0; i < kTX * kTY / 32; ++i) sum += red[i];
+            dst[slot] = sum;
+        }
+        __syncthreads();
+    };
+#pragma unroll
+    for (int co = 0; co < OC; ++co) {
+#pragma unroll
+        for (int t = 0; t < 27; ++t) reduce(acc[co][t], co * 28 + t);
+        reduce(accb[co], co * 28 + 27);
+    }
+}
+
+// gk[co,ci,t] += sum over CTAs; gbias[co] += (ci == 0 partials only)
+template <int OC>
+__global__ void __launch_bounds__(256)
+conv3_bwd_w_tiled_final_k(const float *__restrict__ part, int nparts, int ic,
+                          float *__restrict__ gk, float *__restrict__ gbias) {
+    const int ci = blockIdx.y, slot = blockIdx.x;  // slot = co*28 + t
+    const int co = slot / 28, t = slot % 28;
+    if (t == 27 && (ci != 0 || !gbias)) return;
+    if (t < 27 && !gk) return;
+    float v = 0.0f;
+    for (int i = threadIdx.x; i < nparts; i += 256)
+        v += part[((int64_t)ci * nparts + i) * (OC * 28) + slot];
+    __shared__ float s[256];
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int m = 128; m > 0; m >>= 1) {
+        if (threadIdx.x < m) s[threadIdx.x] += s[threadIdx.x + m];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (t < 27) gk[((int64_t)co * ic + ci) * 27 + t] += s[0];
+        else gbias[co] += s[0];
+    }
+}
+
 }  // namespace mdg
 
 using namespace mdg;
@@ -165,6 +431,14 @@ mdg_status mdg_conv3_fwd(const float *in, int ic, mdg_dims3 d, const float *k,
     const int64_t n = nvox(d);
     if (n == 0) return MDG_OK;
     MDG_REQUIRE(in && k && out, "conv3: null pointer");
+    if (oc == 3 && ic <= 64) {  // RegHead: tiled shared-memory path
+        const size_t smem = (size_t)(3 * ic * 27 + kChunk * kSlab) * sizeof(float);
+        const dim3 g((d.h + kTX - 1) / kTX, (d.w + kTY - 1) / kTY, (d.l + kV - 1) / kV);
+        conv3_fwd_tiled_k<3><<<g, kTX * kTY, smem, S_(stream)>>>(in, ic, d.h, d.w, d.l, k, bias,
+                                                                 out);
+        MDG_LAUNCHED();
+        return MDG_OK;
+    }
     conv3_fwd_k<<<grid1d(n, kCB), kCB, 0, S_(stream)>>>(in, ic, d.h, d.w, d.l, k, bias, oc, out);
     MDG_LAUNCHED();
     return MDG_OK;
@@ -178,6 +452,31 @@ mdg_status mdg_conv3_bwd(const float *in, int ic, mdg_dims3 d, const float *k, i
     if (n == 0) return MDG_OK;
     MDG_REQUIRE(in && k && gout, "conv3: null pointer");
     cudaStream_t st = S_(stream);
+    if (oc == 3 && ic <= 64) {  // RegHead: tiled shared-memory path
+        const dim3 g((d.h + kTX - 1) / kTX, (d.w + kTY - 1) / kTY, (d.l + kV - 1) / kV);
+        if (gin) {
+            const size_t smem = (size_t)(3 * ic * 27 + 3 * kSlab) * sizeof(float);
+            conv3_bwd_in_tiled_k<3><<<g, kTX * kTY, smem, st>>>(ic, d.h, d.w, d.l, k, gout, gin);
+            MDG_LAUNCHED();
+        }
+        if (gk || gbias) {
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int64_t ntiles = (int64_t)g.x * g.y * g.z;
+            const int gx = (int)std::max<int64_t>(
+                1, std::min<int64_t>(ntiles, ((int64_t)sms * 2 + ic - 1) / ic));
+            Scratch part;
+            MDG_CUDA_TRY(part.alloc((size_t)ic * gx * 3 * 28 * sizeof(float), st));
+            conv3_bwd_w_tiled_k<3><<<dim3(gx, ic), kTX * kTY, 0, st>>>(in, ic, d.h, d.w, d.l, gout,
+                                                                      part.as<float>());
+            MDG_LAUNCHED();
+            conv3_bwd_w_tiled_final_k<3><<<dim3(3 * 28, ic), 256, 0, st>>>(part.as<float>(), gx,
+                                                                           ic, gk, gbias);
+            MDG_LAUNCHED();
+        }
+        return MDG_OK;
+    }
     if (gin) {
         conv3_bwd_in_k<<<grid1d(n, kCB), kCB, 0, st>>>(ic, d.h, d.w, d.l, k, oc, gout, gin);
         MDG_LAUNCHED();

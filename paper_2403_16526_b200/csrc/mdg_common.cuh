@@ -70,7 +70,12 @@ constexpr int kFixupCap = 1 << 16;
 unsigned long long *fixup_queue_ptr();
 
 // --------------------------------------------------- stream-ordered scratch
-// cudaMallocAsync/cudaFreeAsync from the device's default mempool.
+// cudaMallocAsync/cudaFreeAsync from the device's default mempool.  The pool's
+// release threshold is raised once per device so freed scratch stays mapped:
+// with the default (0) every synchronisation hands the memory back and the
+// next call pays for a fresh mapping inside its stream.
+void keep_pool_mapped();
+
 struct Scratch {
     void *p = nullptr;
     cudaStream_t st = nullptr;
@@ -79,6 +84,7 @@ struct Scratch {
     Scratch &operator=(const Scratch &) = delete;
     cudaError_t alloc(size_t bytes, cudaStream_t s) {
         st = s;
+        keep_pool_mapped();
         return cudaMallocAsync(&p, bytes ? bytes : 16, s);
     }
     ~Scratch() {

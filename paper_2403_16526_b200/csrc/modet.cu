@@ -62,10 +62,10 @@ modet_fwd_k(const float *__restrict__ Q, const float *__restrict__ K,
     const int s = blockIdx.y;
     if (p >= n) return;
     const int SD = S * hd;
-    const int x = (int)(p % h);
-    const int64_t t = p / h;
-    const int y = (int)(t % w);
-    const int z = (int)(t / w);
+    const int p32_ = (int)p, t = p32_ / h;  // n < 2^31: 32-bit div/mod
+    const int x = p32_ - t * h;
+    const int z = t / w;
+    const int y = t - z * w;
     const int64_t hw = (int64_t)h * w;
     const int64_t cs = QK<LAYOUT>::cstride(n);
     const int64_t ps = QK<LAYOUT>::pstride(SD);
@@ -150,10 +150,10 @@ modet_bwd_k(const float *__restrict__ Q, const float *__restrict__ K,
     for (int o = 0; o < 27; ++o) db[o] = 0.0f;
 
     if (active) {
-        const int x = (int)(p % h);
-        const int64_t t = p / h;
-        const int y = (int)(t % w);
-        const int z = (int)(t / w);
+        const int p32_ = (int)p, t = p32_ / h;  // n < 2^31: 32-bit div/mod
+        const int x = p32_ - t * h;
+        const int z = t / w;
+        const int y = t - z * w;
         const bool xm = x > 0, xp = x < h - 1, ym = y > 0, yp = y < w - 1, zm = z > 0,
                    zp = z < l - 1;
         const int64_t qoff = QK<LAYOUT>::at(p, s * hd, n, SD);
@@ -296,10 +296,10 @@ na_fwd_ref_k(const float *__restrict__ Q, const float *__restrict__ K,
     const int s = blockIdx.y;
     if (p >= n) return;
     const int win = nb * nb * nb, r = (nb - 1) / 2, SD = S * hd;
-    const int x = (int)(p % h);
-    const int64_t t = p / h;
-    const int y = (int)(t % w);
-    const int z = (int)(t / w);
+    const int p32_ = (int)p, t = p32_ / h;  // n < 2^31: 32-bit div/mod
+    const int x = p32_ - t * h;
+    const int z = t / w;
+    const int y = t - z * w;
     const float *q = Q + p * SD + s * hd;
     float *wr = W + ((int64_t)s * n + p) * win;
     float mx = -INFINITY, mn = INFINITY;
@@ -345,10 +345,10 @@ na_bwd_ref_rows_k(const float *__restrict__ K, const float *__restrict__ W,
     const int s = blockIdx.y;
     if (p >= n) return;
     const int win = nb * nb * nb, r = (nb - 1) / 2, SD = S * hd;
-    const int x = (int)(p % h);
-    const int64_t t = p / h;
-    const int y = (int)(t % w);
-    const int z = (int)(t / w);
+    const int p32_ = (int)p, t = p32_ / h;  // n < 2^31: 32-bit div/mod
+    const int x = p32_ - t * h;
+    const int z = t / w;
+    const int y = t - z * w;
     const int64_t row = ((int64_t)s * n + p) * win;
     float dot = 0.0f;
     for (int i = 0; i < win; ++i) dot = fmaf(W[row + i], gW[row + i], dot);
@@ -375,10 +375,10 @@ na_bwd_ref_cols_k(const float *__restrict__ Q, const float *__restrict__ dl, int
     const int s = blockIdx.y;
     if (p >= n) return;
     const int win = nb * nb * nb, r = (nb - 1) / 2, SD = S * hd;
-    const int x = (int)(p % h);
-    const int64_t t = p / h;
-    const int y = (int)(t % w);
-    const int z = (int)(t / w);
+    const int p32_ = (int)p, t = p32_ / h;  // n < 2^31: 32-bit div/mod
+    const int x = p32_ - t * h;
+    const int z = t / w;
+    const int y = t - z * w;
     float *gk = gK + p * SD + s * hd;
     // the reference visits sources in ascending p, i.e. descending slot o
     int o = win - 1;

@@ -20,13 +20,13 @@
 namespace mdg {
 
 constexpr int kPB = 256;
-constexpr int kSmemW = 8192;  // weights staged in smem up to this many floats
 
 struct ProjArgs {
     const float *in[2];
     float *out[2];
     const float *gout[2];
     float *gin[2];
+    float *graw[2];  // two-phase backward: pre-norm gradients {K, n} written here
     int ninputs;
     int C, K;
     int64_t n;
@@ -34,95 +34,120 @@ struct ProjArgs {
     int planar;
 };
 
+// pick one of the two inputs without dynamically indexing the parameter struct
+// (a runtime index would copy ProjArgs into local memory in every thread)
+template <typename T>
+__device__ __forceinline__ T pick(int which, T a0, T a1) {
+    return which ? a1 : a0;
+}
+
 __device__ __forceinline__ int64_t qk_index(int planar, int64_t p, int k, int64_t n, int K) {
     return planar ? (int64_t)k * n + p : p * K + k;
 }
 
-// stage W {K,C}, b, gamma, beta into shared memory (or point at global)
-struct ProjParams {
-    const float *W, *b, *g, *be;
+// Shared-memory parameter block, rows padded to KP = KMAX rounded up to 4 and
+// zero-filled beyond K, so the per-channel inner loops need no guards:
+//   Wt[C][KP] (W transposed: one channel's K weights contiguous) | b | g | be
+template <int KMAX>
+struct Pad {
+    static constexpr int KP = (KMAX + 3) & ~3;
 };
 
-__device__ __forceinline__ ProjParams stage_params(float *sm, const float *W, const float *b,
-                                                   const float *g, const float *be, int K,
-                                                   int C) {
-    ProjParams pp;
-    const int kc = K * C;
-    if (kc + 3 * K <= kSmemW) {
-        for (int i = threadIdx.x; i < kc; i += blockDim.x) sm[i] = W[i];
-        for (int i = threadIdx.x; i < K; i += blockDim.x) {
-            sm[kc + i] = b[i];
-            sm[kc + K + i] = g ? g[i] : 1.0f;
-            sm[kc + 2 * K + i] = be ? be[i] : 0.0f;
-        }
-        __syncthreads();
-        pp.W = sm;
-        pp.b = sm + kc;
-        pp.g = sm + kc + K;
-        pp.be = sm + kc + 2 * K;
-    } else {
-        pp.W = W;
-        pp.b = b;
-        pp.g = g;
-        pp.be = be;
-    }
-    return pp;
+inline size_t proj_smem_bytes(int KMAX_, int C) {
+    const int KP = (KMAX_ + 3) & ~3;
+    return (size_t)(C + 3) * KP * sizeof(float);
 }
 
-// raw[k] = b[k] + sum_c W[k,c] in[c,p]  (channel order, as ops.hpp:403-406)
 template <int KMAX>
-__device__ __forceinline__ void project_raw(const float *__restrict__ in, int64_t p, int64_t n,
-                                            int C, int K, const ProjParams &pp,
-                                            float (&raw)[KMAX]) {
+__device__ __forceinline__ void stage_params(float *sm, const float *W, const float *b,
+                                             const float *g, const float *be, int K, int C) {
+    constexpr int KP = Pad<KMAX>::KP;
+    for (int i = threadIdx.x; i < C * KP; i += blockDim.x) {
+        const int c = i / KP, k = i % KP;
+        sm[i] = k < K ? W[(int64_t)k * C + c] : 0.0f;
+    }
+    float *tail = sm + C * KP;
+    for (int k = threadIdx.x; k < KP; k += blockDim.x) {
+        tail[k] = k < K ? b[k] : 0.0f;
+        tail[KP + k] = (k < K && g) ? g[k] : 0.0f;
+        tail[2 * KP + k] = (k < K && be) ? be[k] : 0.0f;
+    }
+    __syncthreads();
+}
+
+// raw[k] = b[k] + sum_c W[k,c] in[c,p]  (channel order, as ops.hpp:403-406);
+// rows k >= K come out exactly 0
+template <int KMAX>
+__device__ __forceinline__ void project_raw(const float *__restrict__ in, int64_t n, int C,
+                                            const float *sm, float (&raw)[KMAX]) {
+    constexpr int KP = Pad<KMAX>::KP;
+    const float *sb = sm + C * KP;
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k) raw[k] = k < K ? pp.b[k] : 0.0f;
-    for (int c = 0; c < C; ++c) {
-        const float x = __ldg(in + (int64_t)c * n + p);
-        const float *wc = pp.W + c;
+    for (int k = 0; k < KMAX; ++k) raw[k] = sb[k];
+    // channels in batches of 8: the 8 independent loads are in flight together
+    // (a plain runtime-C loop serialises one global-load latency per channel)
+    int c = 0;
+    for (; c + 8 <= C; c += 8) {
+        float x[8];
 #pragma unroll
-        for (int k = 0; k < KMAX; ++k)
-            if (k < K) raw[k] = fmaf(wc[(int64_t)k * C], x, raw[k]);
+        for (int j = 0; j < 8; ++j) x[j] = __ldg(in + (int64_t)(c + j) * n);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float *wc = sm + (c + j) * KP;
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k) raw[k] = fmaf(wc[k], x[j], raw[k]);
+        }
+    }
+    for (; c < C; ++c) {
+        const float x = __ldg(in + (int64_t)c * n);
+        const float *wc = sm + c * KP;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) raw[k] = fmaf(wc[k], x, raw[k]);
     }
 }
 
 // two-pass mean / biased variance (ops.hpp:447-454); raw -> xhat in place
+// (rows >= K set to 0); returns inv = 1/sqrt(var + eps)
 template <int KMAX>
 __device__ __forceinline__ float ln_normalize(float (&raw)[KMAX], int K, float eps) {
     float mean = 0.0f;
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k)
-        if (k < K) mean += raw[k];
+    for (int k = 0; k < KMAX; ++k) mean += raw[k];  // padded rows are 0
     mean /= (float)K;
     float var = 0.0f;
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k)
-        if (k < K) {
-            const float t = raw[k] - mean;
-            var = fmaf(t, t, var);
-        }
+    for (int k = 0; k < KMAX; ++k) {
+        const float t = k < K ? raw[k] - mean : 0.0f;
+        var = fmaf(t, t, var);
+    }
     var /= (float)K;
     const float inv = 1.0f / sqrtf(var + eps);
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k) raw[k] = (raw[k] - mean) * inv;
+    for (int k = 0; k < KMAX; ++k) raw[k] = k < K ? (raw[k] - mean) * inv : 0.0f;
     return inv;
 }
 
-template <int KMAX>
+// EXACT: K == KMAX known at compile time (the fine levels' K = 6)
+template <int KMAX, bool EXACT>
 __global__ void __launch_bounds__(kPB)
 project_fwd_k(ProjArgs a, const float *__restrict__ W, const float *__restrict__ b,
               const float *__restrict__ g, const float *__restrict__ be) {
-    extern __shared__ float sm[];
-    const ProjParams pp = stage_params(sm, W, b, g, be, a.K, a.C);
+    extern __shared__ __align__(16) float sm[];
+    constexpr int KP = Pad<KMAX>::KP;
+    const int K = EXACT ? KMAX : a.K, C = a.C;
+    const int64_t n = a.n;
+    stage_params<KMAX>(sm, W, b, g, be, K, C);
     const int which = blockIdx.y;
     const int64_t p = (int64_t)blockIdx.x * kPB + threadIdx.x;
-    if (p >= a.n) return;
-    float raw[KMAX];
-    project_raw<KMAX>(a.in[which], p, a.n, a.C, a.K, pp, raw);
-    ln_normalize<KMAX>(raw, a.K, a.eps);
-    float *out = a.out[which];
+    if (p >= n) return;
+    float v[KMAX];
+    project_raw<KMAX>(pick(which, a.in[0], a.in[1]) + p, n, C, sm, v);
+    ln_normalize<KMAX>(v, K, a.eps);
+    float *out = pick(which, a.out[0], a.out[1]);
+    const float *sg = sm + (C + 1) * KP, *sbe = sm + (C + 2) * KP;
 #pragma unroll
     for (int k = 0; k < KMAX; ++k)
-        if (k < a.K) out[qk_index(a.planar, p, k, a.n, a.K)] = fmaf(pp.g[k], raw[k], pp.be[k]);
+        if (k < K) out[qk_index(a.planar, p, k, n, K)] = fmaf(sg[k], v[k], sbe[k]);
 }
 
 // K > 64: raw values go through the output buffer (two extra passes over it)
@@ -132,13 +157,14 @@ project_fwd_wide_k(ProjArgs a, const float *__restrict__ W, const float *__restr
     const int which = blockIdx.y;
     const int64_t p = (int64_t)blockIdx.x * kPB + threadIdx.x;
     if (p >= a.n) return;
-    const float *in = a.in[which];
-    float *out = a.out[which];
+    const float *in = pick(which, a.in[0], a.in[1]);
+    float *out = pick(which, a.out[0], a.out[1]);
     const int K = a.K, C = a.C;
     float mean = 0.0f;
     for (int k = 0; k < K; ++k) {
         float s = b[k];
-        for (int c = 0; c < C; ++c) s = fmaf(__ldg(W + (int64_t)k * C + c), __ldg(in + (int64_t)c * a.n + p), s);
+        for (int c = 0; c < C; ++c)
+            s = fmaf(__ldg(W + (int64_t)k * C + c), __ldg(in + (int64_t)c * a.n + p), s);
         out[qk_index(a.planar, p, k, a.n, K)] = s;
         mean += s;
     }
@@ -163,59 +189,69 @@ project_fwd_wide_k(ProjArgs a, const float *__restrict__ W, const float *__restr
 //   gin_c += sum_k graw_k W[k,c];  gW[k,c] += graw_k in_c;  gb += graw;
 //   ggamma += gout xh;  gbeta += gout
 // blockIdx.y = c-tile t of width CT: accumulates gW[:, t*CT .. t*CT+CT) in
-// registers; tile 0 also writes gin and (EXTRA) the gb/ggamma/gbeta sums; when
-// the extras do not fit next to the tile (KMAX > 8) they get their own y index.
+// registers; tile 0 also writes gin and (inline, KMAX <= 8) the gb / ggamma /
+// gbeta sums; for wider K each extra gets its own y index (ntiles + e).
 template <int KMAX, int CT>
-__global__ void __launch_bounds__(kPB)
+struct BwdShape {
+    static constexpr bool kInline = KMAX <= 8;
+    static constexpr int NE = kInline ? 3 * KMAX : 1;
+    static constexpr int NSLOT = KMAX * CT + NE;
+};
+
+template <int KMAX, int CT, bool EXACT>
+__global__ void __launch_bounds__(kPB, KMAX <= 6 ? 2 : 1)
 project_bwd_k(ProjArgs a, const float *__restrict__ W, const float *__restrict__ b,
-              const float *__restrict__ g, int ntiles, int extras_inline,
-              float *__restrict__ part) {
-    extern __shared__ float sm[];
-    const ProjParams pp = stage_params(sm, W, b, g, nullptr, a.K, a.C);
-    const int K = a.K, C = a.C;
+              const float *__restrict__ g, int ntiles, float *__restrict__ part) {
+    extern __shared__ __align__(16) float sm[];
+    using Sh = BwdShape<KMAX, CT>;
+    constexpr int KP = Pad<KMAX>::KP;
+    const int K = EXACT ? KMAX : a.K, C = a.C;
+    const int64_t n = a.n;
+    stage_params<KMAX>(sm, W, b, g, nullptr, K, C);
+    const float *sg = sm + (C + 1) * KP;
     const int tile = blockIdx.y;
-    const bool do_w = tile < ntiles;
-    // inline: tile 0 carries all three extras; else y = ntiles + e carries extra e
-    const bool do_extra = extras_inline ? tile == 0 : tile >= ntiles;
+    float *const graw_out0 = a.graw[0];
+    const bool do_w = tile < ntiles && !graw_out0;
+    const bool do_extra = Sh::kInline ? tile == 0 : tile >= ntiles;
     const int extra_kind = tile - ntiles;
     const bool do_gin = tile == 0;
     const int c0 = tile * CT;
-    constexpr int NE = KMAX <= 8 ? 3 * KMAX : 1;  // registers for the extras
     float acc[KMAX][CT];
-    float ex[NE];
+    float ex[Sh::NE];
 #pragma unroll
     for (int k = 0; k < KMAX; ++k)
 #pragma unroll
         for (int j = 0; j < CT; ++j) acc[k][j] = 0.0f;
 #pragma unroll
-    for (int i = 0; i < NE; ++i) ex[i] = 0.0f;
+    for (int i = 0; i < Sh::NE; ++i) ex[i] = 0.0f;
 
     const int64_t stride = (int64_t)gridDim.x * kPB;
     for (int which = 0; which < a.ninputs; ++which) {
-        const float *in = a.in[which];
-        const float *gout = a.gout[which];
-        float *gin = a.gin[which];
-        for (int64_t p = (int64_t)blockIdx.x * kPB + threadIdx.x; p < a.n; p += stride) {
+        const float *in = pick(which, a.in[0], a.in[1]);
+        const float *gout = pick(which, a.gout[0], a.gout[1]);
+        float *gin = pick(which, a.gin[0], a.gin[1]);
+        for (int64_t p = (int64_t)blockIdx.x * kPB + threadIdx.x; p < n; p += stride) {
+            const float *ip = in + p;
             float v[KMAX];
-            project_raw<KMAX>(in, p, a.n, C, K, pp, v);
-            const float inv = ln_normalize<KMAX>(v, K, a.eps);  // v = xhat
+            project_raw<KMAX>(ip, n, C, sm, v);
+            const float inv = ln_normalize<KMAX>(v, K, a.eps);  // v = xhat, 0 beyond K
             float go[KMAX], gr[KMAX];
-            float sg = 0.0f, sgx = 0.0f;
+            float sgs = 0.0f, sgx = 0.0f;
 #pragma unroll
             for (int k = 0; k < KMAX; ++k) {
-                go[k] = k < K ? __ldg(gout + qk_index(a.planar, p, k, a.n, K)) : 0.0f;
+                go[k] = k < K ? __ldg(gout + qk_index(a.planar, p, k, n, K)) : 0.0f;
                 // rounded product, reused below: keeps gg - mean(gg) exactly 0
                 // when all gg agree (K == 1), as in the reference
-                gr[k] = __fmul_rn(go[k], k < K ? pp.g[k] : 0.0f);
-                sg += gr[k];
+                gr[k] = __fmul_rn(go[k], sg[k]);
+                sgs += gr[k];
                 sgx = fmaf(gr[k], v[k], sgx);
             }
-            const float mg = sg / (float)K, mgx = sgx / (float)K;
+            const float mg = sgs / (float)K, mgx = sgx / (float)K;
 #pragma unroll
             for (int k = 0; k < KMAX; ++k)
                 gr[k] = k < K ? inv * ((gr[k] - mg) - v[k] * mgx) : 0.0f;
-            if (do_extra) {
-                if constexpr (KMAX <= 8) {
+            if constexpr (Sh::kInline) {
+                if (do_extra) {
 #pragma unroll
                     for (int k = 0; k < KMAX; ++k) {
                         ex[k] += gr[k];
@@ -223,54 +259,68 @@ project_bwd_k(ProjArgs a, const float *__restrict__ W, const float *__restrict__
                         ex[2 * KMAX + k] += go[k];
                     }
                 }
-            }
-            if (do_gin && gin) {
-                for (int c = 0; c < C; ++c) {
-                    const float *wc = pp.W + c;
-                    float s = 0.0f;
-#pragma unroll
-                    for (int k = 0; k < KMAX; ++k)
-                        if (k < K) s = fmaf(gr[k], wc[(int64_t)k * C], s);
-                    gin[(int64_t)c * a.n + p] += s;
-                }
-            }
-            if (do_w) {
-#pragma unroll
-                for (int j = 0; j < CT; ++j) {
-                    if (c0 + j >= C) break;
-                    const float x = __ldg(in + (int64_t)(c0 + j) * a.n + p);
-#pragma unroll
-                    for (int k = 0; k < KMAX; ++k) acc[k][j] = fmaf(gr[k], x, acc[k][j]);
-                }
-            }
-            if constexpr (KMAX > 8) {
-                // dedicated extras tile: acc[k][0] holds gb, ggamma or gbeta
-                if (do_extra && !do_w) {
+            } else {
+                if (do_extra) {
 #pragma unroll
                     for (int k = 0; k < KMAX; ++k)
                         acc[k][0] += extra_kind == 0 ? gr[k]
                                      : extra_kind == 1 ? go[k] * v[k] : go[k];
                 }
             }
+            if (do_gin && graw_out0) {
+                float *go_ = pick(which, graw_out0, a.graw[1]) + p;
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k)
+                    if (k < K) go_[(int64_t)k * n] = gr[k];
+            }
+            if (do_gin && gin) {
+                // read-modify-write in batches of 4 with all loads first: the
+                // compiler cannot prove gp[c*n] and gp[(c+1)*n] never alias,
+                // so an interleaved loop would serialise load-after-store
+                float *gp = gin + p;
+                for (int c = 0; c < C; c += 4) {
+                    float old[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        old[j] = c + j < C ? gp[(int64_t)(c + j) * n] : 0.0f;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (c + j >= C) break;
+                        const float *wc = sm + (c + j) * KP;
+                        float s = 0.0f;
+#pragma unroll
+                        for (int k = 0; k < KMAX; ++k) s = fmaf(gr[k], wc[k], s);
+                        gp[(int64_t)(c + j) * n] = old[j] + s;
+                    }
+                }
+            }
+            if (do_w) {
+#pragma unroll
+                for (int j = 0; j < CT; ++j) {
+                    if (c0 + j < C) {
+                        const float x = __ldg(ip + (int64_t)(c0 + j) * n);
+#pragma unroll
+                        for (int k = 0; k < KMAX; ++k) acc[k][j] = fmaf(gr[k], x, acc[k][j]);
+                    }
+                }
+            }
         }
     }
 
     // fixed-order block reduction of every accumulator -> part[y][x][slot]
-    // slots: tile rows [KMAX*CT] then (inline extras) [3*KMAX]
     __shared__ float red[kPB / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    constexpr int NSLOT = KMAX * CT + NE;
-    float *dst = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NSLOT;
+    float *dst = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * Sh::NSLOT;
     auto reduce_slot = [&](float val, int slot) {
 #pragma unroll
         for (int m = 16; m > 0; m >>= 1) val += __shfl_xor_sync(0xffffffffu, val, m);
         if (lane == 0) red[wid] = val;
         __syncthreads();
         if (threadIdx.x == 0) {
-            float s = 0.0f;
+            float t = 0.0f;
 #pragma unroll
-            for (int i = 0; i < kPB / 32; ++i) s += red[i];
-            dst[slot] = s;
+            for (int i = 0; i < kPB / 32; ++i) t += red[i];
+            dst[slot] = t;
         }
         __syncthreads();
     };
@@ -279,18 +329,17 @@ project_bwd_k(ProjArgs a, const float *__restrict__ W, const float *__restrict__
 #pragma unroll
         for (int j = 0; j < CT; ++j) reduce_slot(acc[k][j], k * CT + j);
 #pragma unroll
-    for (int i = 0; i < NE; ++i) reduce_slot(ex[i], KMAX * CT + i);
+    for (int i = 0; i < Sh::NE; ++i) reduce_slot(ex[i], KMAX * CT + i);
 }
 
 // sum the per-CTA partials (fixed order) and accumulate into the parameter
 // gradients.  One block per output value.
 template <int KMAX, int CT>
 __global__ void __launch_bounds__(kPB)
-project_bwd_final_k(const float *__restrict__ part, int nparts, int ntiles, int extras_inline,
-                    int K, int C, float *__restrict__ gW, float *__restrict__ gb,
-                    float *__restrict__ gg, float *__restrict__ gbe) {
-    constexpr int NE = KMAX <= 8 ? 3 * KMAX : 1;
-    constexpr int NSLOT = KMAX * CT + NE;
+project_bwd_final_k(const float *__restrict__ part, int nparts, int ntiles, int K, int C,
+                    float *__restrict__ gW, float *__restrict__ gb, float *__restrict__ gg,
+                    float *__restrict__ gbe) {
+    using Sh = BwdShape<KMAX, CT>;
     const int o = blockIdx.x;  // output id: [0, K*C) weights, then 3K extras
     int y, slot;
     float *target;
@@ -301,7 +350,7 @@ project_bwd_final_k(const float *__restrict__ part, int nparts, int ntiles, int 
         target = gW ? gW + o : nullptr;
     } else {
         const int e = (o - K * C) / K, k = (o - K * C) % K;  // e: 0 gb, 1 gamma, 2 beta
-        if (extras_inline) {
+        if (Sh::kInline) {
             y = 0;
             slot = KMAX * CT + e * KMAX + k;
         } else {
@@ -314,7 +363,7 @@ project_bwd_final_k(const float *__restrict__ part, int nparts, int ntiles, int 
     if (!target) return;
     float v = 0.0f;
     for (int i = threadIdx.x; i < nparts; i += kPB)
-        v += part[((int64_t)y * nparts + i) * NSLOT + slot];
+        v += part[((int64_t)y * nparts + i) * Sh::NSLOT + slot];
     __shared__ float s[kPB];
     s[threadIdx.x] = v;
     __syncthreads();
@@ -325,35 +374,146 @@ project_bwd_final_k(const float *__restrict__ part, int nparts, int ntiles, int 
     if (threadIdx.x == 0) *target += s[0];
 }
 
-inline size_t proj_smem(int K, int C) {
-    const int need = K * C + 3 * K;
-    return need <= kSmemW ? (size_t)need * sizeof(float) : 0;
+// Two-phase weight gradient for multi-tile levels (C > CT): instead of
+// recomputing the projection once per channel tile, phase 1 writes the
+// pre-norm gradients graw {K, n} and phase 2 forms gW[k, c] = sum_p graw[k,p]
+// in[c,p] as a chunked outer-product reduction (shared-memory staged chunks of
+// kGP voxels, kGO outputs per thread, per-CTA partials, fixed-order final sum).
+constexpr int kGP = 32, kGO = 4;
+
+__global__ void __launch_bounds__(kPB)
+gram_k(const float *__restrict__ A0, const float *__restrict__ A1, const float *__restrict__ B0,
+       const float *__restrict__ B1, int ninputs, int K, int C, int64_t n,
+       float *__restrict__ part) {
+    extern __shared__ __align__(16) float gsm[];
+    float *As = gsm;            // [K][kGP]
+    float *Bs = gsm + K * kGP;  // [C][kGP]
+    const int KC = K * C;
+    const int obase = blockIdx.y * kPB * kGO;
+    float acc[kGO];
+    int kk[kGO], cc[kGO];
+#pragma unroll
+    for (int j = 0; j < kGO; ++j) {
+        acc[j] = 0.0f;
+        const int o = obase + j * kPB + threadIdx.x;
+        kk[j] = o < KC ? o / C : -1;
+        cc[j] = o < KC ? o % C : 0;
+    }
+    const int64_t nchunks = (n + kGP - 1) / kGP;
+    for (int which = 0; which < ninputs; ++which) {
+        const float *A = which ? A1 : A0;
+        const float *B = which ? B1 : B0;
+        for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+            const int64_t p0 = ch * kGP;
+            __syncthreads();
+            for (int i = threadIdx.x; i < (K + C) * kGP; i += kPB) {
+                const int r = i / kGP, q = i % kGP;
+                const int64_t pp = p0 + q;
+                float v = 0.0f;
+                if (pp < n) v = r < K ? __ldg(A + (int64_t)r * n + pp) : __ldg(B + (int64_t)(r - K) * n + pp);
+                gsm[i] = v;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < kGO; ++j) {
+                if (kk[j] < 0) continue;
+                const float *ar = As + kk[j] * kGP, *br = Bs + cc[j] * kGP;
+                float t = acc[j];
+#pragma unroll 8
+                for (int q = 0; q < kGP; ++q) t = fmaf(ar[q], br[q], t);
+                acc[j] = t;
+            }
+        }
+    }
+    float *dst = part + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (kPB * kGO);
+#pragma unroll
+    for (int j = 0; j < kGO; ++j) dst[j * kPB + threadIdx.x] = acc[j];
 }
 
-template <int KMAX, int CT>
-mdg_status project_bwd_launch(const ProjArgs &a, const float *W, const float *b,
+__global__ void __launch_bounds__(kPB)
+gram_final_k(const float *__restrict__ part, int nparts, int KC, float *__restrict__ gW) {
+    const int o = blockIdx.x;
+    const int y = o / (kPB * kGO), lo = o % (kPB * kGO);
+    float v = 0.0f;
+    for (int i = threadIdx.x; i < nparts; i += kPB)
+        v += part[((int64_t)y * nparts + i) * (kPB * kGO) + lo];
+    __shared__ float s[kPB];
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int m = kPB / 2; m > 0; m >>= 1) {
+        if (threadIdx.x < m) s[threadIdx.x] += s[threadIdx.x + m];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && o < KC) gW[o] += s[0];
+}
+
+template <typename Kern>
+cudaError_t allow_smem(Kern k, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int KMAX, bool EXACT>
+mdg_status project_fwd_launch(const ProjArgs &a, const float *W, const float *b, const float *g,
+                              const float *be, cudaStream_t st) {
+    const size_t smem = proj_smem_bytes(KMAX, a.C);
+    MDG_CUDA_TRY(allow_smem(project_fwd_k<KMAX, EXACT>, smem));
+    const dim3 grid(grid1d(a.n, kPB), a.ninputs);
+    project_fwd_k<KMAX, EXACT><<<grid, kPB, smem, st>>>(a, W, b, g, be);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+template <int KMAX, int CT, bool EXACT>
+mdg_status project_bwd_launch(const ProjArgs &a0, const float *W, const float *b,
                               const float *g, float *gW, float *gb, float *gg, float *gbe,
                               cudaStream_t st) {
-    const int ntiles = (a.C + CT - 1) / CT;
-    const bool want_extra = gb || gg || gbe;
-    const int extras_inline = KMAX <= 8;
-    const int ny = ntiles + ((!extras_inline && want_extra) ? 3 : 0);
+    using Sh = BwdShape<KMAX, CT>;
+    ProjArgs a = a0;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t blocks_needed = (a.n + kPB - 1) / kPB;
-    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)sms * 4 / std::max(1, ny) + 1));
-    constexpr int NE = KMAX <= 8 ? 3 * KMAX : 1;
-    constexpr int NSLOT = KMAX * CT + NE;
+    const int per_sm = KMAX <= 6 ? 2 : 1;
+    // one channel tile: gW accumulates in registers next to everything else;
+    // several: two-phase (graw to scratch, then the chunked reduction)
+    const bool two_phase = gW && a.C > CT;
+    Scratch graw;
+    if (two_phase) {
+        MDG_CUDA_TRY(graw.alloc((size_t)a.ninputs * a.K * a.n * sizeof(float), st));
+        a.graw[0] = graw.as<float>();
+        a.graw[1] = a.ninputs > 1 ? graw.as<float>() + (int64_t)a.K * a.n : nullptr;
+    }
+    const int ntiles = two_phase ? 1 : (a.C + CT - 1) / CT;
+    const bool want_extra = gb || gg || gbe;
+    const int ny = ntiles + ((!Sh::kInline && want_extra) ? 3 : 0);
+    const int gx = (int)std::max<int64_t>(
+        1, std::min<int64_t>(blocks_needed, ((int64_t)sms * per_sm * 2 + ny - 1) / ny));
     Scratch part;
-    MDG_CUDA_TRY(part.alloc((size_t)ny * gx * NSLOT * sizeof(float), st));
-    const size_t smem = proj_smem(a.K, a.C);
-    project_bwd_k<KMAX, CT><<<dim3(gx, ny), kPB, smem, st>>>(a, W, b, g, ntiles, extras_inline,
-                                                            part.as<float>());
+    MDG_CUDA_TRY(part.alloc((size_t)ny * gx * Sh::NSLOT * sizeof(float), st));
+    const size_t smem = proj_smem_bytes(KMAX, a.C);
+    MDG_CUDA_TRY(allow_smem(project_bwd_k<KMAX, CT, EXACT>, smem));
+    project_bwd_k<KMAX, CT, EXACT><<<dim3(gx, ny), kPB, smem, st>>>(a, W, b, g, ntiles,
+                                                                    part.as<float>());
     MDG_LAUNCHED();
-    if (gW || want_extra) {
+    if ((gW && !two_phase) || want_extra) {
         project_bwd_final_k<KMAX, CT><<<a.K * a.C + 3 * a.K, kPB, 0, st>>>(
-            part.as<float>(), gx, ntiles, extras_inline, a.K, a.C, gW, gb, gg, gbe);
+            part.as<float>(), gx, ntiles, a.K, a.C, two_phase ? nullptr : gW, gb, gg, gbe);
+        MDG_LAUNCHED();
+    }
+    if (two_phase) {
+        const int KC = a.K * a.C;
+        const int gy = (KC + kPB * kGO - 1) / (kPB * kGO);
+        const int64_t nchunks = (a.n + kGP - 1) / kGP;
+        const int ggx = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, (int64_t)sms * 4 / gy + 1));
+        const size_t gsmem = (size_t)(a.K + a.C) * kGP * sizeof(float);
+        MDG_CUDA_TRY(allow_smem(gram_k, gsmem));
+        Scratch gpart;
+        MDG_CUDA_TRY(gpart.alloc((size_t)gy * ggx * kPB * kGO * sizeof(float), st));
+        gram_k<<<dim3(ggx, gy), kPB, gsmem, st>>>(a.graw[0], a.graw[1], a.in[0], a.in[1],
+                                                  a.ninputs, a.K, a.C, a.n, gpart.as<float>());
+        MDG_LAUNCHED();
+        gram_final_k<<<KC, kPB, 0, st>>>(gpart.as<float>(), ggx, KC, gW);
         MDG_LAUNCHED();
     }
     return MDG_OK;
@@ -397,13 +557,15 @@ mdg_status mdg_project_qk_fwd(const float *f, const float *m, int C, int64_t n,
     a.eps = 1e-5f;
     a.planar = layout == MDG_QK_PLANAR;
     cudaStream_t st = S_(stream);
-    const dim3 grid(grid1d(n, kPB), a.ninputs);
-    const size_t smem = proj_smem(K, C);
-    if (K <= 8) project_fwd_k<8><<<grid, kPB, smem, st>>>(a, weight, bias, ln_g, ln_b);
-    else if (K <= 16) project_fwd_k<16><<<grid, kPB, smem, st>>>(a, weight, bias, ln_g, ln_b);
-    else if (K <= 32) project_fwd_k<32><<<grid, kPB, smem, st>>>(a, weight, bias, ln_g, ln_b);
-    else if (K <= 64) project_fwd_k<64><<<grid, kPB, smem, st>>>(a, weight, bias, ln_g, ln_b);
-    else project_fwd_wide_k<<<grid, kPB, 0, st>>>(a, weight, bias, ln_g, ln_b);
+    MDG_REQUIRE(K > 64 || proj_smem_bytes(K, C) <= 200 * 1024,
+                "project_qk: C * K too large for the shared-memory weight block");
+    if (K == 6) return project_fwd_launch<6, true>(a, weight, bias, ln_g, ln_b, st);
+    if (K <= 8) return project_fwd_launch<8, false>(a, weight, bias, ln_g, ln_b, st);
+    if (K <= 16) return project_fwd_launch<16, false>(a, weight, bias, ln_g, ln_b, st);
+    if (K <= 32) return project_fwd_launch<32, false>(a, weight, bias, ln_g, ln_b, st);
+    if (K <= 64) return project_fwd_launch<64, false>(a, weight, bias, ln_g, ln_b, st);
+    project_fwd_wide_k<<<dim3(grid1d(n, kPB), a.ninputs), kPB, 0, st>>>(a, weight, bias, ln_g,
+                                                                         ln_b);
     MDG_LAUNCHED();
     return MDG_OK;
 }
@@ -433,10 +595,14 @@ mdg_status mdg_project_qk_bwd(const float *f, const float *m, int C, int64_t n,
     a.eps = 1e-5f;
     a.planar = layout == MDG_QK_PLANAR;
     cudaStream_t st = S_(stream);
-    if (K <= 8) return project_bwd_launch<8, 8>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
-    if (K <= 16) return project_bwd_launch<16, 4>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
-    if (K <= 32) return project_bwd_launch<32, 2>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
-    return project_bwd_launch<64, 1>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
+    MDG_REQUIRE(proj_smem_bytes(K, C) <= 200 * 1024,
+                "project_qk_bwd: C * K too large for the shared-memory weight block");
+    // K == 6 (head_dim 6, one head: the fine levels) gets an exact instantiation
+    if (K == 6) return project_bwd_launch<6, 8, true>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
+    if (K <= 8) return project_bwd_launch<8, 8, false>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
+    if (K <= 16) return project_bwd_launch<16, 4, false>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
+    if (K <= 32) return project_bwd_launch<32, 2, false>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
+    return project_bwd_launch<64, 1, false>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
 }
 
 }  // extern "C"

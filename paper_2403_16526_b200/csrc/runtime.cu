@@ -61,6 +61,22 @@ unsigned long long *fixup_queue_ptr() {
     return queues[dev];
 }
 
+void keep_pool_mapped() {
+    static std::mutex mu;
+    static std::vector<bool> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)done.size() <= dev) done.resize(dev + 1, false);
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done[dev] = true;
+}
+
 mdg_status consume_numeric_flag(cudaStream_t st, mdg_dims3 d) {
     unsigned long long *f = numeric_flag_ptr();
     if (!f) return status_from_cuda(cudaErrorMemoryAllocation, "numeric flag");

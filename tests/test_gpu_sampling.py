@@ -133,7 +133,8 @@ def test_conv3_matches_golden(cuda):
 
 
 def test_conv3_reghead_shapes_randomised(cuda, oracle):
-    for S, d in ((1, (9, 8, 7)), (2, (6, 7, 5)), (8, (4, 3, 5)), (4, (1, 1, 1))):
+    for S, d in ((1, (9, 8, 7)), (2, (6, 7, 5)), (8, (4, 3, 5)), (4, (1, 1, 1)), (2, (40, 11, 3)),
+                 (3, (33, 17, 2))):
         x = random_feature_map(3 * S, d, 7 * S)
         k = f32(pyoracle.Rng(S).normal(3 * 3 * S * 27, 0, 0.2).reshape(3, 3 * S, 3, 3, 3))
         b = f32(pyoracle.Rng(S + 1).normal(3))
