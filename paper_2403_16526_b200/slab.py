@@ -1,0 +1,212 @@
+"""Depth-slab decomposition of the ModeT operator across ranks (SURVEY §8e,
+"Depth-slab (cfg3, cfg4)").
+
+The volume is split along z — the slowest, contiguous axis (common.hpp:56-59)
+— into one slab per rank.  The operator's 3x3x3 window reaches one plane
+across each slab face, so every rank works on its slab extended by one halo
+plane per side:
+
+* forward: the K halo planes come from the neighbours (point-to-point
+  send/recv, NCCL over NVLink on GPUs); Q halo planes are zero (their outputs
+  are discarded).  Zero K at the GLOBAL boundary is exactly the reference's
+  out-of-bounds rule (attention.hpp:77-81: the term is omitted, logit = bias;
+  q . 0 = 0 gives the same logit).
+* backward: halos of Q, K, the saved softmax statistics (LSE), SF and gSF.
+  The query-side pass (dQ, dB) runs with the halo planes' gSF zeroed, so halo
+  queries contribute nothing (they belong to the neighbour); the key-side pass
+  (dK, a gather over sources r = q - off(o)) runs with the true halo gSF, so
+  keys on the slab face collect the contributions of sources in the
+  neighbour's planes.  At the global boundary the halo is empty: LSE = +inf
+  makes those phantom sources weigh exactly 0.
+* dB (the relative-position bias gradient) is the only quantity summed over
+  ranks: one all-reduce of S*27 floats.
+
+The compute backend is pluggable for testing (tests/test_slab.py drives the
+same decomposition with the CPU oracle over gloo); the product backend is
+:class:`CudaModeT` — libmdg's fused kernels, with no fallback.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+def split(l: int, world: int):
+    """Balanced z ranges [(z0, z1)] for `world` ranks (earlier ranks get the
+    remainder).  Every rank needs at least one plane."""
+    if world < 1 or l < world:
+        raise ValueError(f"slab: cannot split {l} planes over {world} ranks")
+    base, rem = divmod(l, world)
+    out, z = [], 0
+    for r in range(world):
+        n = base + (1 if r < rem else 0)
+        out.append((z, z + n))
+        z += n
+    return out
+
+
+@dataclass
+class Slab:
+    """This rank's piece of a {*, l, w, h} volume."""
+
+    h: int
+    w: int
+    l: int  # global depth
+    world: int
+    rank: int
+
+    def __post_init__(self):
+        self.z0, self.z1 = split(self.l, self.world)[self.rank]
+
+    @property
+    def depth(self) -> int:
+        return self.z1 - self.z0
+
+    @property
+    def dims(self):
+        """local dims (h, w, depth)"""
+        return (self.h, self.w, self.depth)
+
+    @property
+    def ext_dims(self):
+        """dims of the slab plus one halo plane per side"""
+        return (self.h, self.w, self.depth + 2)
+
+    def local(self, full: torch.Tensor) -> torch.Tensor:
+        """This rank's planes of a planar {C, l, w, h} (or {C, n}) tensor."""
+        C = full.shape[0]
+        v = full.reshape(C, self.l, self.w, self.h)
+        return v[:, self.z0:self.z1].contiguous()
+
+
+def exchange_halo(x: torch.Tensor, slab: Slab, fill: float = 0.0, group=None):
+    """x: local planes {C, depth, w, h}.  Returns the neighbours' adjacent
+    planes (lo = plane z0-1, hi = plane z1), each {C, w, h}; `fill` where the
+    neighbour does not exist (global boundary)."""
+    C = x.shape[0]
+    lo = torch.full((C, slab.w, slab.h), fill, dtype=x.dtype, device=x.device)
+    hi = torch.full((C, slab.w, slab.h), fill, dtype=x.dtype, device=x.device)
+    if slab.world == 1:
+        return lo, hi
+    first = x[:, 0].contiguous()
+    last = x[:, -1].contiguous()
+    ops = []
+    if slab.rank > 0:
+        ops.append(dist.P2POp(dist.isend, first, slab.rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, lo, slab.rank - 1, group))
+    if slab.rank < slab.world - 1:
+        ops.append(dist.P2POp(dist.isend, last, slab.rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, hi, slab.rank + 1, group))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    return lo, hi
+
+
+def extend(x: torch.Tensor, lo: torch.Tensor, hi: torch.Tensor) -> torch.Tensor:
+    """[lo, x, hi] along z: {C, depth+2, w, h}."""
+    return torch.cat([lo.unsqueeze(1), x, hi.unsqueeze(1)], dim=1).contiguous()
+
+
+def interior(x_ext: torch.Tensor) -> torch.Tensor:
+    return x_ext[:, 1:-1].contiguous()
+
+
+class CudaModeT:
+    """Product backend: libmdg's fused ModeT kernels on the extended slab
+    (planar Q/K, saved statistics = LSE {S, n})."""
+
+    saved_fill = float("inf")  # phantom sources beyond the global boundary
+
+    def __init__(self, heads: int, head_dim: int):
+        from . import ops
+
+        self.ops = ops
+        self.cfg = ops.AttentionConfig(heads, head_dim, 3)
+
+    def forward(self, Q_ext, K_ext, B, dims):
+        SF, LSE = self.ops.modet_fwd(Q_ext, K_ext, B, dims, self.cfg,
+                                     layout=self.ops.MDG_QK_PLANAR, check=False)
+        h, w, l = dims
+        return SF.view(-1, l, w, h), LSE.view(-1, l, w, h)
+
+    def check(self, dims):
+        self.ops.check_numeric(dims)
+
+    def backward_queries(self, Q_ext, K_ext, B, SF_ext, saved_ext, gSF_rows, dims, gB):
+        gQ = torch.empty_like(Q_ext)
+        self._bwd(Q_ext, K_ext, B, SF_ext, saved_ext, gSF_rows, dims, gQ, None, gB)
+        return gQ
+
+    def backward_keys(self, Q_ext, K_ext, B, SF_ext, saved_ext, gSF_ext, dims):
+        gK = torch.empty_like(K_ext)
+        self._bwd(Q_ext, K_ext, B, SF_ext, saved_ext, gSF_ext, dims, None, gK, None)
+        return gK
+
+    def _bwd(self, Q, K, B, SF, LSE, gSF, dims, gQ, gK, gB):
+        o = self.ops
+        P = o._ptr
+        L = o._capi.lib()
+        o._check(L.mdg_modet_bwd(P(Q), P(K), P(B), P(SF), P(LSE), P(gSF), o.dims3(dims),
+                                 self.cfg.heads, self.cfg.head_dim, 3, o.MDG_QK_PLANAR,
+                                 P(gQ), P(gK), P(gB), 0, o._stream()))
+
+
+class SlabModeT:
+    """ModeT forward/backward on this rank's z-slab with halo exchange.
+
+    Tensors are planar and local: Q, K {S*d, depth, w, h}; B {S, 27} (same on
+    every rank); outputs SF {3S, depth, w, h}; the backward returns local
+    gQ, gK and the all-reduced gB."""
+
+    def __init__(self, slab: Slab, heads: int, head_dim: int, backend=None, group=None,
+                 exchange=None, all_reduce=None):
+        self.slab, self.S, self.hd = slab, heads, head_dim
+        self.be = backend if backend is not None else CudaModeT(heads, head_dim)
+        self.group = group
+        # exchange(name, x, slab, fill) -> (lo, hi); the default is the
+        # point-to-point exchange over the process group
+        self.exchange = exchange or (lambda name, x, sl, fill: exchange_halo(x, sl, fill, group))
+        self.all_reduce = all_reduce or (
+            lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group))
+        self._saved = None
+
+    def _ext(self, name, x, fill=0.0):
+        lo, hi = self.exchange(name, x, self.slab, fill)
+        return extend(x, lo, hi)
+
+    def forward(self, Q, K, B):
+        s = self.slab
+        Kx = self._ext("K", K)
+        zero = torch.zeros(Q.shape[0], s.w, s.h, dtype=Q.dtype, device=Q.device)
+        Qx = extend(Q, zero, zero)  # halo queries are the neighbours' work
+        SFx, saved_x = self.be.forward(Qx, Kx, B, s.ext_dims)
+        if hasattr(self.be, "check"):
+            try:
+                self.be.check(s.ext_dims)
+            except Exception as e:  # report the global position
+                pos = getattr(e, "position", None)
+                if pos is not None and pos[2] >= 0:
+                    e.position = (pos[0], pos[1], pos[2] - 1 + s.z0, pos[3])
+                raise
+        SF, saved = interior(SFx), interior(saved_x)
+        self._saved = (Q, K, B, SF, saved)
+        return SF
+
+    def backward(self, gSF):
+        if self._saved is None:
+            raise RuntimeError("slab: backward without forward")
+        Q, K, B, SF, saved = self._saved
+        s = self.slab
+        Qx, Kx = self._ext("Q", Q), self._ext("K", K)
+        SFx, gSFx = self._ext("SF", SF), self._ext("gSF", gSF)
+        savedx = self._ext("saved", saved, fill=self.be.saved_fill)
+        zero = torch.zeros(gSF.shape[0], s.w, s.h, dtype=gSF.dtype, device=gSF.device)
+        gSF_rows = extend(gSF, zero, zero)
+        gB = torch.zeros_like(B)
+        gQx = self.be.backward_queries(Qx, Kx, B, SFx, savedx, gSF_rows, s.ext_dims, gB)
+        gKx = self.be.backward_keys(Qx, Kx, B, SFx, savedx, gSFx, s.ext_dims)
+        if s.world > 1:
+            self.all_reduce(gB)
+        return interior(gQx), interior(gKx), gB
