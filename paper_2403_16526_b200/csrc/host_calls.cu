@@ -4,6 +4,8 @@
 // the stream-ordered pool, copies and kernels run on a per-thread stream, and
 // the call returns after the results are back in host memory.  With pinned
 // host buffers (mdg_host_alloc) the copies run at full PCIe/C2C bandwidth.
+#include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "mdg_common.cuh"
@@ -62,6 +64,473 @@ using namespace mdg;
         if (_e != cudaSuccess) return status_from_cuda(_e, #expr);     \
     } while (0)
 
+// ===================================================== z-chunk pipelining
+// The ModeT host calls move 4-7x more bytes over PCIe than the kernels need
+// time for, so they run as a three-stream pipeline over z-chunks: chunk i+1
+// is uploaded (H2D engine) while chunk i computes and chunk i-1's results
+// come back (D2H engine) — both copy directions busy at once.  Each chunk is
+// staged as its own small volume extended by one halo plane per side; the
+// halo planes are device-to-device copies from the neighbouring chunks (the
+// same decomposition as the multi-GPU depth slabs, paper_2403_16526_b200/
+// slab.py), so per-voxel results are bit-identical to the whole-volume call.
+namespace mdg {
+
+__global__ void fill_k(float *p, int64_t m, float v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) p[i] = v;
+}
+
+namespace {
+
+struct PipeStreams {
+    cudaStream_t up = nullptr, comp = nullptr, down = nullptr;
+    PipeStreams() {
+        cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking);
+    }
+    ~PipeStreams() {
+        for (cudaStream_t s : {up, comp, down})
+            if (s) cudaStreamDestroy(s);
+    }
+};
+PipeStreams &pipe_streams() {
+    thread_local PipeStreams ps;
+    return ps;
+}
+
+// Accumulate targets (the reference's `+=` gradients) are NOT uploaded: the
+// device computes each chunk's contribution into a fresh buffer, it comes
+// back into pinned staging, and host threads add it into the caller's array
+// (one IEEE fp32 add per element — the same operation the device would do,
+// so results are bit-identical) while later chunks are still in flight.
+// This removes the largest H2D stream of the backward calls.
+struct PinnedStage {
+    float *p = nullptr;
+    size_t cap = 0;
+    ~PinnedStage() {
+        if (p) cudaFreeHost(p);
+    }
+    cudaError_t reserve(size_t floats) {
+        if (floats <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMallocHost(&p, floats * sizeof(float));
+        if (e == cudaSuccess) cap = floats;
+        return e;
+    }
+};
+PinnedStage &pinned_stage() {
+    thread_local PinnedStage ps;
+    return ps;
+}
+
+void host_add(float *dst, const float *src, int64_t m) {
+#pragma omp parallel for schedule(static) if (m > (1 << 16))
+    for (int64_t i = 0; i < m; ++i) dst[i] += src[i];
+}
+
+constexpr int kPipeMinPlanes = 16;       // below this the plain call wins
+constexpr int64_t kPipeMinVoxels = 1 << 20;
+constexpr int kPipeChunks = 16;
+
+bool pipeline_ok(mdg_dims3 d, int nb, int layout, bool all_ptrs) {
+    return all_ptrs && nb == 3 && dims_ok(d) && d.l >= kPipeMinPlanes &&
+           nvox(d) >= kPipeMinVoxels && (layout == MDG_QK_PLANAR || layout == MDG_QK_POSMAJOR);
+}
+
+// posmajor host chunk {m, C} (staged) -> interior of an extended planar
+// buffer {C, m + 2hw} at offset hw, and back
+__global__ void pm_to_ext_k(const float *__restrict__ src, int64_t m, int C, int64_t hw,
+                            float *__restrict__ dst) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m * C) return;
+    const int64_t p = i / C;
+    const int c = (int)(i - p * C);
+    dst[(int64_t)c * (m + 2 * hw) + hw + p] = src[i];
+}
+__global__ void ext_to_pm_k(const float *__restrict__ src, int64_t m, int C, int64_t hw,
+                            float *__restrict__ dst) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m * C) return;
+    const int64_t p = i / C;
+    const int c = (int)(i - p * C);
+    dst[i] = src[(int64_t)c * (m + 2 * hw) + hw + p];
+}
+
+struct Chunking {
+    int nchunk;
+    std::vector<int> z0, z1;
+    explicit Chunking(int l) {
+        nchunk = std::min(kPipeChunks, l / 4);
+        for (int i = 0; i < nchunk; ++i) {
+            z0.push_back((int)((int64_t)l * i / nchunk));
+            z1.push_back((int)((int64_t)l * (i + 1) / nchunk));
+        }
+    }
+    int depth(int i) const { return z1[i] - z0[i]; }
+};
+
+// One channel-major array staged chunk by chunk as extended volumes.
+struct ExtArray {
+    int C = 0;
+    int64_t hw = 0, n = 0;
+    bool posmajor = false;  // host layout {n, C}
+    std::vector<float *> buf;  // per chunk {C, (D+2) hw}
+    std::vector<float *> stg;  // posmajor host layout: per-chunk staging
+
+    int64_t ext(const Chunking &ck, int i) const { return (int64_t)(ck.depth(i) + 2) * hw; }
+};
+
+struct PipeCtx {
+    mdg_dims3 d;
+    int64_t n, hw;
+    Chunking ck;
+    std::vector<void *> allocs;
+    cudaStream_t up, comp, down;
+    std::vector<cudaEvent_t> evs;
+    PipeCtx(mdg_dims3 d_) : d(d_), n(nvox(d_)), hw((int64_t)d_.h * d_.w), ck(d_.l) {
+        PipeStreams &ps = pipe_streams();
+        up = ps.up;
+        comp = ps.comp;
+        down = ps.down;
+    }
+    ~PipeCtx() {
+        for (void *p : allocs) cudaFreeAsync(p, down);
+        for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    }
+    cudaError_t alloc(float **p, size_t floats) {
+        void *q = nullptr;
+        cudaError_t e = cudaMallocAsync(&q, floats * sizeof(float) + 16, up);
+        if (e == cudaSuccess) {
+            allocs.push_back(q);
+            *p = static_cast<float *>(q);
+        }
+        return e;
+    }
+    cudaEvent_t event() {
+        cudaEvent_t e = nullptr;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        evs.push_back(e);
+        return e;
+    }
+    cudaError_t init(ExtArray &a, int C, bool posmajor) {
+        a.C = C;
+        a.hw = hw;
+        a.n = n;
+        a.posmajor = posmajor;
+        a.buf.resize(ck.nchunk);
+        a.stg.assign(ck.nchunk, nullptr);
+        for (int i = 0; i < ck.nchunk; ++i) {
+            cudaError_t e = alloc(&a.buf[i], (size_t)C * a.ext(ck, i));
+            if (e) return e;
+            if (posmajor && (e = alloc(&a.stg[i], (size_t)C * ck.depth(i) * hw))) return e;
+        }
+        return cudaSuccess;
+    }
+    // H2D of chunk i's planes into the interior (on `up`)
+    cudaError_t upload(ExtArray &a, const float *host, int i) {
+        const int D = ck.depth(i);
+        const int64_t m = (int64_t)D * hw;
+        if (a.posmajor) {
+            cudaError_t e = cudaMemcpyAsync(a.stg[i], host + (int64_t)ck.z0[i] * hw * a.C,
+                                            (size_t)m * a.C * sizeof(float),
+                                            cudaMemcpyHostToDevice, up);
+            if (e) return e;
+            pm_to_ext_k<<<grid1d(m * a.C, 256), 256, 0, up>>>(a.stg[i], m, a.C, hw, a.buf[i]);
+            return cudaPeekAtLastError();
+        }
+        return cudaMemcpy2DAsync(a.buf[i] + hw, (size_t)a.ext(ck, i) * sizeof(float),
+                                 host + (int64_t)ck.z0[i] * hw, (size_t)n * sizeof(float),
+                                 (size_t)m * sizeof(float), a.C, cudaMemcpyHostToDevice, up);
+    }
+    // D2H of chunk i's interior (on `down`)
+    cudaError_t download(ExtArray &a, float *host, int i) {
+        const int D = ck.depth(i);
+        const int64_t m = (int64_t)D * hw;
+        if (a.posmajor) {
+            ext_to_pm_k<<<grid1d(m * a.C, 256), 256, 0, down>>>(a.buf[i], m, a.C, hw, a.stg[i]);
+            cudaError_t e = cudaPeekAtLastError();
+            if (e) return e;
+            return cudaMemcpyAsync(host + (int64_t)ck.z0[i] * hw * a.C, a.stg[i],
+                                   (size_t)m * a.C * sizeof(float), cudaMemcpyDeviceToHost, down);
+        }
+        return cudaMemcpy2DAsync(host + (int64_t)ck.z0[i] * hw, (size_t)n * sizeof(float),
+                                 a.buf[i] + hw, (size_t)a.ext(ck, i) * sizeof(float),
+                                 (size_t)m * sizeof(float), a.C, cudaMemcpyDeviceToHost, down);
+    }
+    // host += staged chunk i of `a` (staging mirrors the host array's layout)
+    void add_chunk(const ExtArray &a, float *host, const float *stage, int i) const {
+        const int64_t m = (int64_t)ck.depth(i) * hw;
+        if (a.posmajor) {
+            const int64_t o = (int64_t)ck.z0[i] * hw * a.C;
+            host_add(host + o, stage + o, m * a.C);
+        } else {
+            for (int c = 0; c < a.C; ++c) {
+                const int64_t o = (int64_t)c * n + (int64_t)ck.z0[i] * hw;
+                host_add(host + o, stage + o, m);
+            }
+        }
+    }
+    // halo planes of chunk i from its neighbours' interiors (or `fill` at the
+    // global boundary); on `comp`, after both neighbours are uploaded
+    cudaError_t halos(ExtArray &a, int i, float fill, bool zero) {
+        const int D = ck.depth(i);
+        const size_t pl = (size_t)hw * sizeof(float), pitch = (size_t)a.ext(ck, i) * sizeof(float);
+        for (int side = 0; side < 2; ++side) {
+            float *dst = a.buf[i] + (side == 0 ? 0 : (int64_t)(D + 1) * hw);
+            const int nb = side == 0 ? i - 1 : i + 1;
+            if (zero || nb < 0 || nb >= ck.nchunk) {
+                if (fill == 0.0f) {
+                    cudaError_t e = cudaMemset2DAsync(dst, pitch, 0, pl, a.C, comp);
+                    if (e) return e;
+                } else {
+                    for (int c = 0; c < a.C; ++c)
+                        fill_k<<<grid1d(hw, 256), 256, 0, comp>>>(dst + c * a.ext(ck, i), hw, fill);
+                }
+                continue;
+            }
+            const int Dn = ck.depth(nb);
+            const float *src = a.buf[nb] + (side == 0 ? (int64_t)Dn * hw : hw);
+            cudaError_t e = cudaMemcpy2DAsync(dst, pitch, src, (size_t)a.ext(ck, nb) * sizeof(float),
+                                              pl, a.C, cudaMemcpyDeviceToDevice, comp);
+            if (e) return e;
+        }
+        return cudaPeekAtLastError();
+    }
+};
+
+#define MDG_PIPE_TRY(expr)                                             \
+    do {                                                               \
+        cudaError_t _e = (expr);                                       \
+        if (_e != cudaSuccess) return status_from_cuda(_e, #expr);     \
+    } while (0)
+#define MDG_PIPE_OK(expr)                                              \
+    do {                                                               \
+        mdg_status _s = (expr);                                        \
+        if (_s != MDG_OK) return _s;                                   \
+    } while (0)
+
+mdg_status modet_fwd_host_pipelined(const float *Q, const float *K, const float *B, mdg_dims3 d,
+                                    int S, int hd, int layout, float *SF, float *LSE) {
+    PipeCtx P(d);
+    const int N = P.ck.nchunk, C = S * hd;
+    const bool pm = layout == MDG_QK_POSMAJOR;
+    ExtArray q, k, sf, lse;
+    MDG_PIPE_TRY(P.init(q, C, pm));
+    MDG_PIPE_TRY(P.init(k, C, pm));
+    MDG_PIPE_TRY(P.init(sf, 3 * S, false));
+    MDG_PIPE_TRY(P.init(lse, S, false));
+    float *dB = nullptr;
+    MDG_PIPE_TRY(P.alloc(&dB, (size_t)S * 27));
+    MDG_PIPE_TRY(cudaMemcpyAsync(dB, B, (size_t)S * 27 * sizeof(float), cudaMemcpyHostToDevice, P.up));
+    std::vector<cudaEvent_t> upd(N), cmp(N);
+    for (int i = 0; i < N; ++i) {
+        MDG_PIPE_TRY(P.upload(q, Q, i));
+        MDG_PIPE_TRY(P.upload(k, K, i));
+        upd[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(upd[i], P.up));
+    }
+    for (int i = 0; i < N; ++i) {
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.comp, upd[std::min(i + 1, N - 1)], 0));
+        MDG_PIPE_TRY(P.halos(k, i, 0.0f, false));
+        MDG_PIPE_TRY(P.halos(q, i, 0.0f, true));  // halo queries: the neighbour's work
+        const mdg_dims3 de{d.h, d.w, P.ck.depth(i) + 2};
+        MDG_PIPE_OK(mdg_modet_fwd(q.buf[i], k.buf[i], dB, de, S, hd, 3, MDG_QK_PLANAR,
+                                  sf.buf[i], lse.buf[i], nullptr, P.comp));
+        cmp[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(cmp[i], P.comp));
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.down, cmp[i], 0));
+        MDG_PIPE_TRY(P.download(sf, SF, i));
+        MDG_PIPE_TRY(P.download(lse, LSE, i));
+    }
+    MDG_PIPE_TRY(cudaStreamSynchronize(P.down));
+    MDG_PIPE_TRY(cudaStreamSynchronize(P.comp));
+    // any non-finite logit: the caller reruns whole-volume for the exact position
+    unsigned long long *f = numeric_flag_ptr();
+    unsigned long long key = ~0ull;
+    MDG_PIPE_TRY(cudaMemcpy(&key, f, sizeof(key), cudaMemcpyDeviceToHost));
+    if (key != ~0ull) {
+        MDG_PIPE_TRY(cudaMemset(f, 0xff, sizeof(key)));
+        return MDG_ENUMERIC;
+    }
+    return MDG_OK;
+}
+
+mdg_status modet_bwd_host_pipelined(const float *Q, const float *K, const float *B,
+                                    const float *SF, const float *LSE, const float *gSF,
+                                    mdg_dims3 d, int S, int hd, int layout, float *gQ, float *gK,
+                                    float *gB) {
+    PipeCtx P(d);
+    const int N = P.ck.nchunk, C = S * hd;
+    const bool pm = layout == MDG_QK_POSMAJOR;
+    ExtArray q, k, sf, lse, g, gq, gk;
+    MDG_PIPE_TRY(P.init(q, C, pm));
+    MDG_PIPE_TRY(P.init(k, C, pm));
+    MDG_PIPE_TRY(P.init(sf, 3 * S, false));
+    MDG_PIPE_TRY(P.init(lse, S, false));
+    MDG_PIPE_TRY(P.init(g, 3 * S, false));
+    MDG_PIPE_TRY(P.init(gq, C, pm));
+    MDG_PIPE_TRY(P.init(gk, C, pm));
+    PinnedStage &stg = pinned_stage();
+    const size_t qn = (size_t)C * P.n;
+    MDG_PIPE_TRY(stg.reserve(2 * qn));
+    float *sq = stg.p, *sk = stg.p + qn;  // staging mirrors of gQ, gK
+    float *dB = nullptr, *dgB = nullptr;
+    MDG_PIPE_TRY(P.alloc(&dB, (size_t)S * 27));
+    MDG_PIPE_TRY(P.alloc(&dgB, (size_t)S * 27));
+    MDG_PIPE_TRY(cudaMemcpyAsync(dB, B, (size_t)S * 27 * sizeof(float), cudaMemcpyHostToDevice, P.up));
+    MDG_PIPE_TRY(cudaMemcpyAsync(dgB, gB, (size_t)S * 27 * sizeof(float), cudaMemcpyHostToDevice, P.up));
+    std::vector<cudaEvent_t> upd(N), cmp(N), dwn(N);
+    for (int i = 0; i < N; ++i) {
+        MDG_PIPE_TRY(P.upload(q, Q, i));
+        MDG_PIPE_TRY(P.upload(k, K, i));
+        MDG_PIPE_TRY(P.upload(sf, SF, i));
+        MDG_PIPE_TRY(P.upload(lse, LSE, i));
+        MDG_PIPE_TRY(P.upload(g, gSF, i));
+        upd[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(upd[i], P.up));
+    }
+    for (int i = 0; i < N; ++i) {
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.comp, upd[std::min(i + 1, N - 1)], 0));
+        const mdg_dims3 de{d.h, d.w, P.ck.depth(i) + 2};
+        MDG_PIPE_TRY(P.halos(q, i, 0.0f, false));
+        MDG_PIPE_TRY(P.halos(k, i, 0.0f, false));
+        MDG_PIPE_TRY(P.halos(sf, i, 0.0f, false));
+        MDG_PIPE_TRY(P.halos(lse, i, INFINITY, false));  // phantom sources weigh 0
+        // queries (dQ, dB): halo queries belong to the neighbouring chunk
+        MDG_PIPE_TRY(P.halos(g, i, 0.0f, true));
+        MDG_PIPE_OK(mdg_modet_bwd(q.buf[i], k.buf[i], dB, sf.buf[i], lse.buf[i], g.buf[i], de, S,
+                                  hd, 3, MDG_QK_PLANAR, gq.buf[i], nullptr, dgB, 0, P.comp));
+        // keys (dK): sources in the halo planes count
+        MDG_PIPE_TRY(P.halos(g, i, 0.0f, false));
+        MDG_PIPE_OK(mdg_modet_bwd(q.buf[i], k.buf[i], dB, sf.buf[i], lse.buf[i], g.buf[i], de, S,
+                                  hd, 3, MDG_QK_PLANAR, nullptr, gk.buf[i], nullptr, 0, P.comp));
+        cmp[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(cmp[i], P.comp));
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.down, cmp[i], 0));
+        MDG_PIPE_TRY(P.download(gq, sq, i));
+        MDG_PIPE_TRY(P.download(gk, sk, i));
+        dwn[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(dwn[i], P.down));
+    }
+    MDG_PIPE_TRY(cudaMemcpyAsync(gB, dgB, (size_t)S * 27 * sizeof(float), cudaMemcpyDeviceToHost, P.down));
+    for (int i = 0; i < N; ++i) {  // host adds overlap the chunks still in flight
+        MDG_PIPE_TRY(cudaEventSynchronize(dwn[i]));
+        P.add_chunk(gq, gQ, sq, i);
+        P.add_chunk(gk, gK, sk, i);
+    }
+    MDG_PIPE_TRY(cudaStreamSynchronize(P.down));
+    MDG_PIPE_TRY(cudaStreamSynchronize(P.comp));
+    return MDG_OK;
+}
+
+// warp: the input volume must be whole before any gather, then the field /
+// upstream-gradient chunks stream in and the per-voxel results stream out
+mdg_status warp_fwd_host_pipelined(const float *in, int C, mdg_dims3 d, const float *field,
+                                   float *out) {
+    PipeCtx P(d);
+    const int N = P.ck.nchunk;
+    const int64_t n = P.n, hw = P.hw;
+    float *di, *df, *dout;
+    MDG_PIPE_TRY(P.alloc(&di, (size_t)C * n));
+    MDG_PIPE_TRY(P.alloc(&df, 3 * (size_t)n));
+    MDG_PIPE_TRY(P.alloc(&dout, (size_t)C * n));
+    MDG_PIPE_TRY(cudaMemcpyAsync(di, in, (size_t)C * n * sizeof(float), cudaMemcpyHostToDevice, P.up));
+    std::vector<cudaEvent_t> upd(N), cmp(N);
+    const size_t pitch = (size_t)n * sizeof(float);
+    for (int i = 0; i < N; ++i) {
+        const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
+        MDG_PIPE_TRY(cudaMemcpy2DAsync(df + p0, pitch, field + p0, pitch, m * sizeof(float), 3,
+                                       cudaMemcpyHostToDevice, P.up));
+        upd[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(upd[i], P.up));
+    }
+    for (int i = 0; i < N; ++i) {
+        const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.comp, upd[i], 0));
+        MDG_PIPE_OK(warp_fwd_range(di, C, d, df, dout, p0, p0 + m, P.comp));
+        cmp[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(cmp[i], P.comp));
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.down, cmp[i], 0));
+        MDG_PIPE_TRY(cudaMemcpy2DAsync(out + p0, pitch, dout + p0, pitch, m * sizeof(float), C,
+                                       cudaMemcpyDeviceToHost, P.down));
+    }
+    MDG_PIPE_TRY(cudaStreamSynchronize(P.down));
+    return MDG_OK;
+}
+
+mdg_status warp_bwd_host_pipelined(const float *in, int C, mdg_dims3 d, const float *field,
+                                   const float *gout, float *gin, float *gfield) {
+    PipeCtx P(d);
+    const int N = P.ck.nchunk;
+    const int64_t n = P.n, hw = P.hw;
+    float *di, *df, *dg, *dgi = nullptr, *dgf = nullptr;
+    MDG_PIPE_TRY(P.alloc(&di, (size_t)C * n));
+    MDG_PIPE_TRY(P.alloc(&df, 3 * (size_t)n));
+    MDG_PIPE_TRY(P.alloc(&dg, (size_t)C * n));
+    if (gin) MDG_PIPE_TRY(P.alloc(&dgi, (size_t)C * n));
+    if (gfield) MDG_PIPE_TRY(P.alloc(&dgf, 3 * (size_t)n));
+    PinnedStage &stg = pinned_stage();
+    MDG_PIPE_TRY(stg.reserve((size_t)(C + 3) * n));
+    float *si = stg.p, *sf = stg.p + (size_t)C * n;
+    // fresh contributions (the caller's accumulators stay on the host)
+    if (dgi) MDG_PIPE_TRY(cudaMemsetAsync(dgi, 0, (size_t)C * n * sizeof(float), P.up));
+    if (dgf) MDG_PIPE_TRY(cudaMemsetAsync(dgf, 0, 3 * (size_t)n * sizeof(float), P.up));
+    MDG_PIPE_TRY(cudaMemcpyAsync(di, in, (size_t)C * n * sizeof(float), cudaMemcpyHostToDevice, P.up));
+    std::vector<cudaEvent_t> upd(N), cmp(N), dwn(N), gdw(N);
+    const size_t pitch = (size_t)n * sizeof(float);
+    for (int i = 0; i < N; ++i) {
+        const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
+        MDG_PIPE_TRY(cudaMemcpy2DAsync(df + p0, pitch, field + p0, pitch, m * sizeof(float), 3,
+                                       cudaMemcpyHostToDevice, P.up));
+        MDG_PIPE_TRY(cudaMemcpy2DAsync(dg + p0, pitch, gout + p0, pitch, m * sizeof(float), C,
+                                       cudaMemcpyHostToDevice, P.up));
+        upd[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(upd[i], P.up));
+    }
+    for (int i = 0; i < N; ++i) {
+        const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.comp, upd[i], 0));
+        MDG_PIPE_OK(warp_bwd_range(di, C, d, df, dg, dgi, dgf, p0, p0 + m, P.comp));
+        cmp[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(cmp[i], P.comp));
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.down, cmp[i], 0));
+        if (dgf)
+            MDG_PIPE_TRY(cudaMemcpy2DAsync(sf + p0, pitch, dgf + p0, pitch, m * sizeof(float), 3,
+                                           cudaMemcpyDeviceToHost, P.down));
+        dwn[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(dwn[i], P.down));
+    }
+    // the image gradient is a scatter: complete only after the last chunk
+    for (int i = 0; i < N; ++i) {
+        const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
+        if (dgi)
+            MDG_PIPE_TRY(cudaMemcpy2DAsync(si + p0, pitch, dgi + p0, pitch, m * sizeof(float), C,
+                                           cudaMemcpyDeviceToHost, P.down));
+        gdw[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(gdw[i], P.down));
+    }
+    for (int i = 0; i < N; ++i) {
+        const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
+        MDG_PIPE_TRY(cudaEventSynchronize(dwn[i]));
+        if (gfield)
+            for (int c = 0; c < 3; ++c) host_add(gfield + c * n + p0, sf + c * n + p0, m);
+    }
+    for (int i = 0; i < N; ++i) {
+        const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
+        MDG_PIPE_TRY(cudaEventSynchronize(gdw[i]));
+        if (gin)
+            for (int c = 0; c < C; ++c) host_add(gin + c * n + p0, si + c * n + p0, m);
+    }
+    MDG_PIPE_TRY(cudaStreamSynchronize(P.down));
+    return MDG_OK;
+}
+
+}  // namespace
+}  // namespace mdg
+
 extern "C" {
 
 mdg_status mdg_na_fused_fwd_host(const float *Q, const float *K, const float *B, mdg_dims3 d,
@@ -83,8 +552,9 @@ mdg_status mdg_na_fused_fwd_host(const float *Q, const float *K, const float *B,
     return MDG_OK;
 }
 
-mdg_status mdg_modet_fwd_host(const float *Q, const float *K, const float *B, mdg_dims3 d,
-                              int S, int hd, int nb, int layout, float *SF, float *LSE) {
+static mdg_status modet_fwd_host_whole(const float *Q, const float *K, const float *B,
+                                       mdg_dims3 d, int S, int hd, int nb, int layout, float *SF,
+                                       float *LSE) {
     MDG_REQUIRE(dims_ok(d) && S >= 1 && hd >= 1, "modet: invalid sizes");
     const size_t n = (size_t)nvox(d);
     if (n == 0) return MDG_OK;
@@ -103,9 +573,10 @@ mdg_status mdg_modet_fwd_host(const float *Q, const float *K, const float *B, md
     return consume_numeric_flag(st, d);
 }
 
-mdg_status mdg_modet_bwd_host(const float *Q, const float *K, const float *B, const float *SF,
-                              const float *LSE, const float *gSF, mdg_dims3 d, int S, int hd,
-                              int nb, int layout, float *gQ, float *gK, float *gB) {
+static mdg_status modet_bwd_host_whole(const float *Q, const float *K, const float *B,
+                                       const float *SF, const float *LSE, const float *gSF,
+                                       mdg_dims3 d, int S, int hd, int nb, int layout, float *gQ,
+                                       float *gK, float *gB) {
     MDG_REQUIRE(dims_ok(d) && S >= 1 && hd >= 1, "modet: invalid sizes");
     const size_t n = (size_t)nvox(d);
     if (n == 0) return MDG_OK;
@@ -131,11 +602,32 @@ mdg_status mdg_modet_bwd_host(const float *Q, const float *K, const float *B, co
     return MDG_OK;
 }
 
+mdg_status mdg_modet_fwd_host(const float *Q, const float *K, const float *B, mdg_dims3 d,
+                              int S, int hd, int nb, int layout, float *SF, float *LSE) {
+    if (pipeline_ok(d, nb, layout, Q && K && SF && LSE)) {
+        mdg_status r = modet_fwd_host_pipelined(Q, K, B, d, S, hd, layout, SF, LSE);
+        if (r != MDG_ENUMERIC) return r;
+        // a non-finite logit: rerun whole-volume to report the reference's
+        // first position exactly
+    }
+    return modet_fwd_host_whole(Q, K, B, d, S, hd, nb, layout, SF, LSE);
+}
+
+mdg_status mdg_modet_bwd_host(const float *Q, const float *K, const float *B, const float *SF,
+                              const float *LSE, const float *gSF, mdg_dims3 d, int S, int hd,
+                              int nb, int layout, float *gQ, float *gK, float *gB) {
+    if (pipeline_ok(d, nb, layout, Q && K && SF && LSE && gSF && gQ && gK && gB))
+        return modet_bwd_host_pipelined(Q, K, B, SF, LSE, gSF, d, S, hd, layout, gQ, gK, gB);
+    return modet_bwd_host_whole(Q, K, B, SF, LSE, gSF, d, S, hd, nb, layout, gQ, gK, gB);
+}
+
 mdg_status mdg_warp_fwd_host(const float *in, int C, mdg_dims3 d, const float *field,
                              float *out) {
     MDG_REQUIRE(dims_ok(d) && C >= 0, "warp: invalid sizes");
     const size_t n = (size_t)nvox(d);
     if (n == 0 || C == 0) return MDG_OK;
+    if (pipeline_ok(d, 3, MDG_QK_PLANAR, in && field && out))
+        return warp_fwd_host_pipelined(in, C, d, field, out);
     cudaStream_t st = host_stream();
     Stage sg(st);
     float *di, *df, *dout;
@@ -154,6 +646,8 @@ mdg_status mdg_warp_bwd_host(const float *in, int C, mdg_dims3 d, const float *f
     MDG_REQUIRE(dims_ok(d) && C >= 0, "warp: invalid sizes");
     const size_t n = (size_t)nvox(d);
     if (n == 0 || C == 0) return MDG_OK;
+    if (pipeline_ok(d, 3, MDG_QK_PLANAR, in && field && gout && (gin || gfield)))
+        return warp_bwd_host_pipelined(in, C, d, field, gout, gin, gfield);
     cudaStream_t st = host_stream();
     Stage sg(st);
     float *di, *df, *dg, *dgi, *dgf;

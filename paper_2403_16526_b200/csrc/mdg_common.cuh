@@ -134,4 +134,11 @@ __device__ __forceinline__ float lerp_(float a, float b, float f) {
     return add_(mul_(a, sub_(1.0f, f)), mul_(b, f));
 }
 
+// sampling.cu: warp kernels over the voxel range [pb, pe) of a volume
+mdg_status warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *field, float *out,
+                          int64_t pb, int64_t pe, cudaStream_t st);
+mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *field,
+                          const float *gout, float *gin, float *gfield, int64_t pb, int64_t pe,
+                          cudaStream_t st);
+
 }  // namespace mdg

@@ -138,10 +138,10 @@ __device__ __forceinline__ void grad_oct(const Oct &o, const Corners &c, float g
 template <int CT>
 __global__ void __launch_bounds__(kSB)
 warp_fwd_k(const float *__restrict__ in, int C, int h, int w, int l,
-           const float *__restrict__ field, float *__restrict__ out) {
+           const float *__restrict__ field, float *__restrict__ out, int64_t pb, int64_t pe) {
     const int64_t n = (int64_t)h * w * l;
-    const int64_t p = (int64_t)blockIdx.x * kSB + threadIdx.x;
-    if (p >= n) return;
+    const int64_t p = pb + (int64_t)blockIdx.x * kSB + threadIdx.x;  // voxels [pb, pe)
+    if (p >= pe) return;
     int x, y, z;
     xyz_of(p, h, w, x, y, z);
     const Corners c = corners_at(add_((float)x, __ldg(field + p)), add_((float)y, __ldg(field + n + p)),
@@ -226,11 +226,11 @@ template <int CT>
 __global__ void __launch_bounds__(kSB)
 warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, const float *__restrict__ gout,
-           float *__restrict__ gin, float *__restrict__ gfield) {
+           float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe) {
     const int64_t n = (int64_t)h * w * l;
-    const int64_t p0 = (int64_t)blockIdx.x * kSB + threadIdx.x;
+    const int64_t p0 = pb + (int64_t)blockIdx.x * kSB + threadIdx.x;  // voxels [pb, pe)
     // CT > 0 keeps every lane alive for the warp-level scatter merge
-    const bool ok = p0 < n;
+    const bool ok = p0 < pe;
     if (CT == 0 && !ok) return;
     const int64_t p = ok ? p0 : 0;
     int x, y, z;
@@ -488,6 +488,27 @@ __global__ void add2_k(const float *__restrict__ a, const float *__restrict__ b,
     if (i < m) out[i] = add_(a[i], b[i]);
 }
 
+// voxel-range launchers (the host-call pipeline computes z-chunks of a volume
+// whose inputs are fully resident)
+mdg_status warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *field, float *out,
+                          int64_t pb, int64_t pe, cudaStream_t st) {
+    if (pe <= pb) return MDG_OK;
+    MDG_WARP_DISPATCH(warp_fwd_k, d.h >= 2 ? C : 0, (grid1d(pe - pb, kSB), kSB, 0, st),
+                      (in, C, d.h, d.w, d.l, field, out, pb, pe));
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *field,
+                          const float *gout, float *gin, float *gfield, int64_t pb, int64_t pe,
+                          cudaStream_t st) {
+    if (pe <= pb) return MDG_OK;
+    MDG_WARP_DISPATCH(warp_bwd_k, d.h >= 2 ? C : 0, (grid1d(pe - pb, kSB), kSB, 0, st),
+                      (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe));
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
 }  // namespace mdg
 
 using namespace mdg;
@@ -507,10 +528,7 @@ mdg_status mdg_warp_fwd(const float *in, int C, mdg_dims3 d, const float *field,
     if (n == 0 || C == 0) return MDG_OK;
     MDG_REQUIRE(in && field && out, "warp: null pointer");
     // the unrolled kernels assume x1 = x0 + 1, i.e. h >= 2
-    MDG_WARP_DISPATCH(warp_fwd_k, d.h >= 2 ? C : 0, (grid1d(n, kSB), kSB, 0, S_(stream)),
-                      (in, C, d.h, d.w, d.l, field, out));
-    MDG_LAUNCHED();
-    return MDG_OK;
+    return warp_fwd_range(in, C, d, field, out, 0, n, S_(stream));
 }
 
 mdg_status mdg_warp_bwd(const float *in, int C, mdg_dims3 d, const float *field,
@@ -520,10 +538,7 @@ mdg_status mdg_warp_bwd(const float *in, int C, mdg_dims3 d, const float *field,
     const int64_t n = nvox(d);
     if (n == 0 || C == 0 || (!gin && !gfield)) return MDG_OK;
     MDG_REQUIRE(in && field && gout, "warp: null pointer");
-    MDG_WARP_DISPATCH(warp_bwd_k, d.h >= 2 ? C : 0, (grid1d(n, kSB), kSB, 0, S_(stream)),
-                      (in, C, d.h, d.w, d.l, field, gout, gin, gfield));
-    MDG_LAUNCHED();
-    return MDG_OK;
+    return warp_bwd_range(in, C, d, field, gout, gin, gfield, 0, n, S_(stream));
 }
 
 mdg_status mdg_compose_fwd(const float *prev, const float *res, mdg_dims3 d, float *out,

@@ -326,6 +326,53 @@ def test_host_buffer_calls_match_device_calls(cuda):
     assert worst(hW, W_) <= W_ATOL
 
 
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("dims,S,hd", [((128, 96, 100), 1, 6), ((64, 80, 205), 2, 4)])
+def test_pipelined_host_calls_match_device_calls(cuda, layout, dims, S, hd):
+    """Volumes >= 1M voxels take the three-stream z-chunk pipeline inside the
+    *_host calls (chunks extended by device-copied halo planes): SF, LSE, gQ,
+    gK must equal the whole-volume device call bit for bit, gB to reduction
+    tolerance; the backward accumulates into the caller's buffers."""
+    import ctypes as C
+
+    from paper_2403_16526_b200 import _capi
+
+    h, w, l = dims
+    n = h * w * l
+    r = np.random.default_rng(3)
+    Qp = f32(r.uniform(-1, 1, (n, S * hd)))
+    Kp = f32(r.uniform(-1, 1, (n, S * hd)))
+    B = f32(r.uniform(-0.5, 0.5, (S, 27)))
+    gSF = f32(r.uniform(-1, 1, (3 * S, n)))
+    cfg = ops.AttentionConfig(S, hd, 3)
+    # reference: the whole-volume fused (tiled, planar) device call
+    Qd, Kd = dev(f32(Qp.T)), dev(f32(Kp.T))
+    SF, LSE = ops.modet_fwd(Qd, Kd, dev(B), dims, cfg, layout=1)
+    gQ0 = f32(r.standard_normal((n, S * hd)))
+    gK0 = f32(r.standard_normal((n, S * hd)))
+    gB0 = f32(r.standard_normal((S, 27)))
+    gQ, gK, gB = ops.modet_bwd(Qd, Kd, dev(B), SF, LSE, dev(gSF), dims, cfg, layout=1,
+                               gQ=dev(f32(gQ0.T)), gK=dev(f32(gK0.T)), gB=dev(gB0))
+    SF, LSE, gB = host(SF), host(LSE), host(gB)
+    gQ, gK = host(gQ).T, host(gK).T
+    Q, K, hgQ, hgK = Qp, Kp, gQ0.copy(), gK0.copy()
+    if layout == 1:
+        Q, K, hgQ, hgK = (f32(a.T) for a in (Qp, Kp, gQ0, gK0))
+    L = _capi.lib()
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    d3 = _capi.Dims3(*dims)
+    hSF, hL = np.zeros((3 * S, n), np.float32), np.zeros((S, n), np.float32)
+    assert L.mdg_modet_fwd_host(p(Q), p(K), p(B), d3, S, hd, 3, layout, p(hSF), p(hL)) == 0
+    assert np.array_equal(hSF, SF) and np.array_equal(hL, LSE)
+    hgB = gB0.copy()
+    assert L.mdg_modet_bwd_host(p(Q), p(K), p(B), p(hSF), p(hL), p(gSF), d3, S, hd, 3, layout,
+                                p(hgQ), p(hgK), p(hgB)) == 0
+    if layout == 1:
+        hgQ, hgK = hgQ.T, hgK.T
+    assert np.array_equal(hgQ, gQ) and np.array_equal(hgK, gK)
+    assert np.allclose(hgB, gB, rtol=1e-5, atol=1e-4)
+
+
 # --------------------------------------------------------- north-star size
 @pytest.mark.slow
 def test_north_star_size_parity_and_properties(cuda, oracle):
