@@ -324,8 +324,11 @@ def run_e2e(args, L, host_in, world, dev):
 
         dist.barrier()
     t0 = time.perf_counter()
+    per_step = []
     for _ in range(steps):
+        ts = time.perf_counter()
         step()
+        per_step.append((time.perf_counter() - ts) * 1e3)
     dt = (time.perf_counter() - t0) / steps
     if world > 1:
         import torch.distributed as dist
@@ -334,12 +337,16 @@ def run_e2e(args, L, host_in, world, dev):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
     f4 = 4
+    # bytes the calls move over PCIe (counted from the tensors they copy); the
+    # gradient accumulators stay on the host (host-side += of the device
+    # contribution), so they cross only once, device -> host
     h2d = (2 * n * S * HD + 27 * S) * f4 \
-        + (2 * n * S * HD + 27 * S + 4 * n * S + 3 * n * S + 2 * n * S * HD + 27 * S) * f4 \
-        + (CH * n + 3 * n) * f4 + (2 * CH * n + 3 * n + CH * n + 3 * n) * f4
+        + (2 * n * S * HD + 27 * S + 3 * n * S + n * S + 3 * n * S + 27 * S) * f4 \
+        + (CH * n + 3 * n) * f4 + (2 * CH * n + 3 * n) * f4
     d2h = (4 * n * S) * f4 + (2 * n * S * HD + 27 * S) * f4 + CH * n * f4 + (CH * n + 3 * n) * f4
     return {"value": round(world * n / dt / 1e9, 5), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 3),
+            "ms_steps": [round(x, 2) for x in per_step],
             "api": "mdg_modet_fwd_host + mdg_modet_bwd_host + mdg_warp_fwd_host + "
                    "mdg_warp_bwd_host (pinned host buffers)", "steps": steps}
 

@@ -5,7 +5,12 @@
 // the call returns after the results are back in host memory.  With pinned
 // host buffers (mdg_host_alloc) the copies run at full PCIe/C2C bandwidth.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "mdg_common.cuh"
@@ -126,9 +131,83 @@ PinnedStage &pinned_stage() {
     return ps;
 }
 
+// A small persistent pool for the host-side adds.  Workers block on a
+// condition variable between jobs (no spinning), so they never compete with
+// the thread that is feeding the copy engines.
+class AddPool {
+  public:
+    AddPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        nthreads_ = (int)std::min(8u, std::max(1u, hw / 2));
+        for (int t = 1; t < nthreads_; ++t) workers_.emplace_back([this, t] { loop(t); });
+    }
+    ~AddPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto &w : workers_) w.join();
+    }
+    void add(float *dst, const float *src, int64_t m) {
+        if (m < (1 << 18) || nthreads_ == 1) {
+            add_range(dst, src, 0, m);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = dst;
+            src_ = src;
+            m_ = m;
+            pending_ = nthreads_ - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        slice(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [this] { return pending_ == 0; });
+    }
+
+  private:
+    static void add_range(float *d, const float *s, int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i) d[i] += s[i];
+    }
+    void slice(int t) {
+        const int64_t a = m_ * t / nthreads_, b = m_ * (t + 1) / nthreads_;
+        add_range(dst_, src_, a, b);
+    }
+    void loop(int t) {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+            }
+            slice(t);
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (--pending_ == 0) done_.notify_one();
+            }
+        }
+    }
+    int nthreads_ = 1;
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    uint64_t gen_ = 0;
+    int pending_ = 0;
+    bool stop_ = false;
+    float *dst_ = nullptr;
+    const float *src_ = nullptr;
+    int64_t m_ = 0;
+};
+
 void host_add(float *dst, const float *src, int64_t m) {
-#pragma omp parallel for schedule(static) if (m > (1 << 16))
-    for (int64_t i = 0; i < m; ++i) dst[i] += src[i];
+    static AddPool pool;
+    pool.add(dst, src, m);
 }
 
 constexpr int kPipeMinPlanes = 16;       // below this the plain call wins
@@ -183,11 +262,49 @@ struct ExtArray {
     int64_t ext(const Chunking &ck, int i) const { return (int64_t)(ck.depth(i) + 2) * hw; }
 };
 
+// Per-thread device workspace for the pipeline: a list of blocks handed out by
+// a bump cursor that is rewound at the start of every call.  Every call
+// drains its streams before returning, so the next call may reuse the memory;
+// after the first calls no allocation happens at all (stream-ordered pool
+// allocations across three streams would keep growing the pool instead).
+struct DevArena {
+    struct Block {
+        char *p;
+        size_t size;
+    };
+    std::vector<Block> blocks;
+    size_t bi = 0, off = 0;
+    ~DevArena() {
+        for (auto &b : blocks) cudaFree(b.p);
+    }
+    void rewind() { bi = off = 0; }
+    cudaError_t take(void **out, size_t bytes) {
+        bytes = (bytes + 255) / 256 * 256;
+        while (bi < blocks.size() && off + bytes > blocks[bi].size) {
+            ++bi;
+            off = 0;
+        }
+        if (bi == blocks.size()) {
+            Block b{nullptr, std::max(bytes, (size_t)256 << 20)};
+            cudaError_t e = cudaMalloc(&b.p, b.size);
+            if (e != cudaSuccess) return e;
+            blocks.push_back(b);
+            off = 0;
+        }
+        *out = blocks[bi].p + off;
+        off += bytes;
+        return cudaSuccess;
+    }
+};
+DevArena &dev_arena() {
+    thread_local DevArena a;
+    return a;
+}
+
 struct PipeCtx {
     mdg_dims3 d;
     int64_t n, hw;
     Chunking ck;
-    std::vector<void *> allocs;
     cudaStream_t up, comp, down;
     std::vector<cudaEvent_t> evs;
     PipeCtx(mdg_dims3 d_) : d(d_), n(nvox(d_)), hw((int64_t)d_.h * d_.w), ck(d_.l) {
@@ -195,18 +312,21 @@ struct PipeCtx {
         up = ps.up;
         comp = ps.comp;
         down = ps.down;
+        dev_arena().rewind();
+        keep_pool_mapped();  // kernels' own scratch (cudaMallocAsync) stays mapped
     }
     ~PipeCtx() {
-        for (void *p : allocs) cudaFreeAsync(p, down);
+        // callers drain the streams before returning; make sure of it on the
+        // error paths too before the workspace is handed to the next call
+        cudaStreamSynchronize(up);
+        cudaStreamSynchronize(comp);
+        cudaStreamSynchronize(down);
         for (cudaEvent_t e : evs) cudaEventDestroy(e);
     }
     cudaError_t alloc(float **p, size_t floats) {
         void *q = nullptr;
-        cudaError_t e = cudaMallocAsync(&q, floats * sizeof(float) + 16, up);
-        if (e == cudaSuccess) {
-            allocs.push_back(q);
-            *p = static_cast<float *>(q);
-        }
+        cudaError_t e = dev_arena().take(&q, floats * sizeof(float) + 16);
+        if (e == cudaSuccess) *p = static_cast<float *>(q);
         return e;
     }
     cudaEvent_t event() {
@@ -362,6 +482,7 @@ mdg_status modet_bwd_host_pipelined(const float *Q, const float *K, const float 
                                     const float *SF, const float *LSE, const float *gSF,
                                     mdg_dims3 d, int S, int hd, int layout, float *gQ, float *gK,
                                     float *gB) {
+    const auto te = std::chrono::steady_clock::now();
     PipeCtx P(d);
     const int N = P.ck.nchunk, C = S * hd;
     const bool pm = layout == MDG_QK_POSMAJOR;
@@ -416,11 +537,22 @@ mdg_status modet_bwd_host_pipelined(const float *Q, const float *K, const float 
         MDG_PIPE_TRY(cudaEventRecord(dwn[i], P.down));
     }
     MDG_PIPE_TRY(cudaMemcpyAsync(gB, dgB, (size_t)S * 27 * sizeof(float), cudaMemcpyDeviceToHost, P.down));
+    const bool trace = getenv("MDG_PIPE_TRACE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+    double t_wait = 0, t_add = 0;
     for (int i = 0; i < N; ++i) {  // host adds overlap the chunks still in flight
+        const double a0 = ms();
         MDG_PIPE_TRY(cudaEventSynchronize(dwn[i]));
+        const double a1 = ms();
         P.add_chunk(gq, gQ, sq, i);
         P.add_chunk(gk, gK, sk, i);
+        t_wait += a1 - a0;
+        t_add += ms() - a1;
     }
+    if (trace)
+        fprintf(stderr, "modet_bwd_host pipeline: enqueue %.2f ms, adds %.2f ms, waits %.2f ms\n",
+                std::chrono::duration<double, std::milli>(t0 - te).count(), t_add, t_wait);
     MDG_PIPE_TRY(cudaStreamSynchronize(P.down));
     MDG_PIPE_TRY(cudaStreamSynchronize(P.comp));
     return MDG_OK;

@@ -1004,6 +1004,7 @@ static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, co
         const int nzc = (d.l + zc - 1) / zc;
         const int ncta = gx * gy * nzc;
         float *part = nullptr;
+        keep_pool_mapped();  // no remapping of this scratch after every sync
         if ((e = cudaMallocAsync(&part, (size_t)S * ncta * 27 * sizeof(float), st))) return e;
         const size_t sm = (2 * (D * RG::HCH + (D + 7) * RG::OCH) + kTail) * sizeof(float);
         Maps m{};

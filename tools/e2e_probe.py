@@ -44,3 +44,10 @@ def duplex():
     with torch.cuda.stream(s1): dbuf.copy_(big, non_blocking=True)
     with torch.cuda.stream(s2): big2.copy_(dbuf2, non_blocking=True)
 print("duplex GB/s (sum of both directions)", round(bw(duplex, 2 * (256 << 20)), 1))
+seq = list(calls.values())
+for rep in range(4):
+    t0 = time.perf_counter()
+    tt = []
+    for fn in seq:
+        t1 = time.perf_counter(); assert fn() == 0; tt.append((time.perf_counter() - t1) * 1e3)
+    print("sequence", round((time.perf_counter() - t0) * 1e3, 2), "ms", [round(x, 2) for x in tt])
