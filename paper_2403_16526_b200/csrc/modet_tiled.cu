@@ -124,12 +124,20 @@ struct MapsA {
     CUtensorMap q, lse, g, sf;
 };
 struct Maps {
-    CUtensorMap k;  // set K
-    MapsA a;        // set A
+    CUtensorMap k;    // set K
+    MapsA a;          // set A
+    CUtensorMap aux;  // column kernel: per-source {LSE*log2e, gSF.SF} from the row kernel
 };
 
 struct Ptrs {
     const float *K, *Q, *LSE, *gSF, *SF;  // head-offset bases
+    const float *AUX = nullptr;           // {2, n} of this head (column kernel)
+    // column-kernel halo channel c: Q (D), aux (2), gSF (3)
+    __device__ __forceinline__ const float *c_src(int c, int D, int64_t n) const {
+        if (c < D) return Q + (int64_t)c * n;
+        if (c < D + 2) return AUX + (int64_t)(c - D) * n;
+        return gSF + (int64_t)(c - D - 2) * n;
+    }
     __device__ __forceinline__ const float *a(int c, int D, int64_t n) const {
         if (c < D) return Q + (int64_t)c * n;
         if (c == D) return LSE;
@@ -229,6 +237,29 @@ __device__ __forceinline__ void init_bars(uint64_t *bar) {
         mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+}
+
+// Buffer release without a block barrier (TMA path).  Each of the 8 compute
+// warps bumps the buffer's counter once it has finished reading it; the warp
+// that brings it to 8 re-arms the buffer: it resets the counter and issues the
+// TMA loads of the step two ahead.  No warp ever waits for another — only for
+// its data (the full mbarrier) — so warps drift freely within the one step of
+// slack the double buffer gives.
+constexpr int kWarps = 8;
+__device__ __forceinline__ bool last_out(int *cnt) {
+    __syncwarp();
+    bool last = false;
+    if ((threadIdx.x & 31) == 0) {
+        __threadfence_block();  // release this warp's reads of the buffer
+        last = atomicAdd(cnt, 1) == kWarps - 1;
+        if (last) {
+            *cnt = 0;
+            __threadfence_block();
+            // generic-proxy reads ordered before the async-proxy (TMA) refill
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        }
+    }
+    return last;
 }
 
 // bias pairs {B*log2e, B*log2e} for the 27 window slots of head s
@@ -370,10 +401,11 @@ __device__ __forceinline__ void fwd_slot(const float2 (&q)[(D + 1) / 2], Soft &s
 
 template <int D, bool TMA>
 __device__ __forceinline__ void fwd_stage(float *buf, const Maps &m, uint64_t *bar, int p,
-                                          int x0, int y0, int s, const Ptrs &P, const Vol &v) {
+                                          int x0, int y0, int s, const Ptrs &P, const Vol &v,
+                                          bool issuer) {
     float *own = buf + D * FG::HCH;
     if (TMA) {
-        if (threadIdx.x == 0) {
+        if (issuer) {
             mbar_expect_tx(bar, D * (FG::PY * kBoxX + FG::OCH) * 4);
 #pragma unroll
             for (int c = 0; c < D; ++c) {
@@ -410,7 +442,10 @@ modet_fwd_tiled_k(const __grid_constant__ Maps maps, const float *__restrict__ Q
     load_bias2(sB2, B, s);
     if (TMA) init_bars(bar);
     __syncthreads();
-    fwd_stage<D, TMA>(smem, maps, &bar[0], zb - 1, x0, y0, s, P, v);
+    // (the forward keeps one block barrier per step: with three resident CTAs
+    // per SM the barrier wait is hidden, and it measured faster than the
+    // counter-based release the backward kernels use)
+    fwd_stage<D, TMA>(smem, maps, &bar[0], zb - 1, x0, y0, s, P, v, threadIdx.x == 0);
     FwdSlots<D> S_;
     march(zb, ze, [&](int p, auto NEW_, auto MID_, auto OLD_) {
         constexpr int NEW = decltype(NEW_)::value, MID = decltype(MID_)::value,
@@ -420,7 +455,8 @@ modet_fwd_tiled_k(const __grid_constant__ Maps maps, const float *__restrict__ Q
         else cp_wait_all();
         __syncthreads();
         if (p + 1 <= ze)
-            fwd_stage<D, TMA>(smem + (b ^ 1) * BUF, maps, &bar[b ^ 1], p + 1, x0, y0, s, P, v);
+            fwd_stage<D, TMA>(smem + (b ^ 1) * BUF, maps, &bar[b ^ 1], p + 1, x0, y0, s, P, v,
+                              threadIdx.x == 0);
         const float *buf = smem + b * BUF;
         const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
         if (has_new) {
@@ -519,10 +555,11 @@ __device__ __forceinline__ void row_slot(RowSlots<D> &R, int j, float (&db)[27],
 
 template <int D, bool TMA>
 __device__ __forceinline__ void row_stage(float *buf, const Maps &m, uint64_t *bar, int p,
-                                          int x0, int y0, int s, const Ptrs &P, const Vol &v) {
+                                          int x0, int y0, int s, const Ptrs &P, const Vol &v,
+                                          bool issuer) {
     float *own = buf + D * RG::HCH;
     if (TMA) {
-        if (threadIdx.x == 0) {
+        if (issuer) {
             mbar_expect_tx(bar, (D * RG::PY * kBoxX + (D + 7) * RG::OCH) * 4);
 #pragma unroll
             for (int c = 0; c < D; ++c) {
@@ -549,7 +586,7 @@ modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                 const float *__restrict__ K, const float *__restrict__ B,
                 const float *__restrict__ SF, const float *__restrict__ LSE,
                 const float *__restrict__ gSF, Vol v, int zc, float *__restrict__ gQ,
-                float *__restrict__ gBpart) {
+                float *__restrict__ gBpart, float *__restrict__ aux) {
     constexpr int D2 = (D + 1) / 2;
     constexpr int BUF = D * RG::HCH + (D + 7) * RG::OCH;
     extern __shared__ __align__(128) float smem[];
@@ -565,10 +602,13 @@ modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
     float *gQh = gQ ? gQ + so * D : nullptr;
     const int x = x0 + tx, y = y0 + ty;
     const bool vv = x < v.h && y < v.w;
+    int *cnt = reinterpret_cast<int *>(smem + 2 * BUF + 8 + 64);
     load_bias2(sB2, B, s);
     if (TMA) init_bars(bar);
+    if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
     __syncthreads();
-    row_stage<D, TMA>(smem, maps, &bar[0], zb - 1, x0, y0, s, P, v);
+    row_stage<D, TMA>(smem, maps, &bar[0], zb - 1, x0, y0, s, P, v, threadIdx.x == 0);
+    if (TMA) row_stage<D, TMA>(smem + BUF, maps, &bar[1], zb, x0, y0, s, P, v, threadIdx.x == 0);
     // Slots are computed unconditionally (no per-slot branches, so the three
     // slots' dependency chains interleave); a slot that holds no voxel has
     // LSE = +inf, q = g = 0, i.e. W = 0 and dl = 0 exactly: nothing reaches dB.
@@ -587,11 +627,15 @@ modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
         constexpr int NEW = decltype(NEW_)::value, MID = decltype(MID_)::value,
                       OLD = decltype(OLD_)::value;
         const int j = p - zb + 1, b = j & 1;
-        if (TMA) mbar_wait(&bar[b], (j >> 1) & 1);
-        else cp_wait_all();
-        __syncthreads();
-        if (p + 1 <= ze)
-            row_stage<D, TMA>(smem + (b ^ 1) * BUF, maps, &bar[b ^ 1], p + 1, x0, y0, s, P, v);
+        if (TMA) {
+            mbar_wait(&bar[b], (j >> 1) & 1);
+        } else {
+            cp_wait_all();
+            __syncthreads();
+            if (p + 1 <= ze)
+                row_stage<D, TMA>(smem + (b ^ 1) * BUF, maps, &bar[b ^ 1], p + 1, x0, y0, s, P,
+                                  v, true);
+        }
         const float *buf = smem + b * BUF;
         const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
         if (has_new) {
@@ -614,6 +658,12 @@ modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
             R.gz[NEW] = gz;
             R.dot[NEW] = gx * own[(D + 4) * RG::OCH] + gy * own[(D + 5) * RG::OCH] +
                          gz * own[(D + 6) * RG::OCH];
+            // the column kernel's per-source statistics: {LSE*log2e, gSF.SF}
+            if (vv && aux) {
+                const int64_t off = (int64_t)(p + 1) * v.hw + (int64_t)y * v.h + x;
+                aux[2 * so + off] = R.L[NEW];
+                aux[2 * so + v.n + off] = R.dot[NEW];
+            }
         } else {
             R.L[NEW] = INFINITY;  // past the chunk end: the slot goes idle
         }
@@ -641,6 +691,8 @@ modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                 row_slot<D, 2, 1>(R, OLD, db, kr, sB2);
             }
         }
+        if (TMA && last_out(&cnt[b]) && p + 2 <= ze)
+            row_stage<D, TMA>(smem + b * BUF, maps, &bar[b], p + 2, x0, y0, s, P, v, true);
         if (has_old && vv && gQh) {
             const int64_t off = (int64_t)(p - 1) * v.hw + (int64_t)y * v.h + x;
 #pragma unroll
@@ -714,7 +766,9 @@ __device__ __forceinline__ void col_slot(ColSlots<D> &C_, int j, const SrcStrip<
         float2 acc = f2(sB2[ob + dxi].x, 0.0f);
 #pragma unroll
         for (int c = 0; c < D2; ++c) acc = fma2(S.q[c][si], C_.k[j][c], acc);
-        const float W = ex2(acc.x + acc.y - S.L[si]);
+        // in-volume sources have l <= L; the clamp keeps W finite for the
+        // zero-filled out-of-volume records (L = 0), whose cf is exactly 0
+        const float W = ex2(fminf(acc.x + acc.y - S.L[si], 126.0f));
         // gSF_r.off(o) - gSF_r.SF_r
         float cf = -S.dt[si];
         if (DYI == 0) cf -= S.gy[si];
@@ -729,44 +783,30 @@ __device__ __forceinline__ void col_slot(ColSlots<D> &C_, int j, const SrcStrip<
     }
 }
 
-// out-of-volume sources get LSE = +inf, i.e. W = 0 exactly: the reference
-// only scatters from in-bounds sources (attention.hpp:155)
-template <int D>
-__device__ __forceinline__ void col_transform(float *buf, int x0, int y0, int z, const Vol &v) {
-    constexpr int CH = CG::HCH;
-    const bool zok = z >= 0 && z < v.l;
-    for (int i = threadIdx.x; i < CG::PY * CG::RL; i += blockDim.x) {
-        const int ry = i / CG::RL, rx = i - ry * CG::RL;
-        const int gx = x0 - 1 + rx, gy = y0 - 1 + ry;
-        const bool in = zok && gx >= 0 && gx < v.h && gy >= 0 && gy < v.w;
-        float *e = buf + ry * kBoxX + kXOff + rx;
-        e[D * CH] = in ? e[D * CH] * kLog2e : INFINITY;
-        e[(D + 4) * CH] = e[(D + 1) * CH] * e[(D + 4) * CH] + e[(D + 2) * CH] * e[(D + 5) * CH] +
-                          e[(D + 3) * CH] * e[(D + 6) * CH];
-    }
-}
-
+// staged source records: Q (D ch), aux {LSE*log2e, gSF.SF} (2), gSF (3) as
+// halo planes; own: K (D)
 template <int D, bool TMA>
 __device__ __forceinline__ void col_stage(float *buf, const Maps &m, uint64_t *bar, int p,
-                                          int x0, int y0, int s, const Ptrs &P, const Vol &v) {
-    float *own = buf + (D + 7) * CG::HCH;
+                                          int x0, int y0, int s, const Ptrs &P, const Vol &v,
+                                          bool issuer) {
+    float *own = buf + (D + 5) * CG::HCH;
     if (TMA) {
-        if (threadIdx.x == 0) {
-            mbar_expect_tx(bar, ((D + 7) * CG::PY * kBoxX + D * CG::OCH) * 4);
+        if (issuer) {
+            mbar_expect_tx(bar, ((D + 5) * CG::PY * kBoxX + D * CG::OCH) * 4);
 #pragma unroll
             for (int c = 0; c < D; ++c) {
                 tma4(buf + c * CG::HCH, &m.a.q, x0 - 4, y0 - 1, p, s * D + c, bar);
                 tma4(own + c * CG::OCH, &m.k, x0, y0, p + 1, s * D + c, bar);
             }
-            tma4(buf + D * CG::HCH, &m.a.lse, x0 - 4, y0 - 1, p, s, bar);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                tma4(buf + (D + 1 + c) * CG::HCH, &m.a.g, x0 - 4, y0 - 1, p, 3 * s + c, bar);
-                tma4(buf + (D + 4 + c) * CG::HCH, &m.a.sf, x0 - 4, y0 - 1, p, 3 * s + c, bar);
-            }
+            for (int c = 0; c < 2; ++c)
+                tma4(buf + (D + c) * CG::HCH, &m.aux, x0 - 4, y0 - 1, p, 2 * s + c, bar);
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                tma4(buf + (D + 2 + c) * CG::HCH, &m.a.g, x0 - 4, y0 - 1, p, 3 * s + c, bar);
         }
     } else {
-        cp_halo<D + 7, CTX, CTY>(buf, [&](int c) { return P.a(c, D, v.n); }, p, x0, y0, v);
+        cp_halo<D + 5, CTX, CTY>(buf, [&](int c) { return P.c_src(c, D, v.n); }, p, x0, y0, v);
         cp_own<D, CTX, CTY>(own, [&](int c) { return P.k(c, v.n); }, p + 1, x0, y0, v);
         cp_commit();
     }
@@ -777,9 +817,10 @@ __global__ void __launch_bounds__(256, (D <= 6 ? 2 : 1))
 modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                 const float *__restrict__ K, const float *__restrict__ B,
                 const float *__restrict__ SF, const float *__restrict__ LSE,
-                const float *__restrict__ gSF, Vol v, int zc, float *__restrict__ gK) {
+                const float *__restrict__ gSF, Vol v, int zc, float *__restrict__ gK,
+                const float *__restrict__ aux) {
     constexpr int D2 = (D + 1) / 2;
-    constexpr int BUF = (D + 7) * CG::HCH + D * CG::OCH;
+    constexpr int BUF = (D + 5) * CG::HCH + D * CG::OCH;
     extern __shared__ __align__(128) float smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * BUF);
     float2 *sB2 = reinterpret_cast<float2 *>(smem + 2 * BUF + 8);
@@ -789,31 +830,36 @@ modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
     const int s = blockIdx.z / nzc;
     const int zb = (blockIdx.z - s * nzc) * zc, ze = min(zb + zc, v.l);
     const int64_t so = (int64_t)s * v.n;
-    const Ptrs P{K + so * D, Q + so * D, LSE + so, gSF + 3 * so, SF + 3 * so};
+    Ptrs P{K + so * D, Q + so * D, LSE + so, gSF + 3 * so, SF + 3 * so};
+    P.AUX = aux + 2 * so;
     float *gKh = gK + so * D;
     const int x = x0 + tx, y = y0 + ty;
     const bool vv = x < v.h && y < v.w;
+    int *cnt = reinterpret_cast<int *>(smem + 2 * BUF + 8 + 64);
     load_bias2(sB2, B, s);
     if (TMA) init_bars(bar);
+    if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
     __syncthreads();
-    col_stage<D, TMA>(smem, maps, &bar[0], zb - 1, x0, y0, s, P, v);
+    col_stage<D, TMA>(smem, maps, &bar[0], zb - 1, x0, y0, s, P, v, threadIdx.x == 0);
+    if (TMA) col_stage<D, TMA>(smem + BUF, maps, &bar[1], zb, x0, y0, s, P, v, threadIdx.x == 0);
     ColSlots<D> C_;
     march(zb, ze, [&](int p, auto NEW_, auto MID_, auto OLD_) {
         constexpr int NEW = decltype(NEW_)::value, MID = decltype(MID_)::value,
                       OLD = decltype(OLD_)::value;
         const int j = p - zb + 1, b = j & 1;
-        if (TMA) mbar_wait(&bar[b], (j >> 1) & 1);
-        else cp_wait_all();
-        __syncthreads();
-        float *buf = smem + b * BUF;
-        col_transform<D>(buf, x0, y0, p, v);
-        // generic-proxy writes to a buffer the TMA (async proxy) refills later
-        if (TMA) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        if (p + 1 <= ze)
-            col_stage<D, TMA>(smem + (b ^ 1) * BUF, maps, &bar[b ^ 1], p + 1, x0, y0, s, P, v);
+        if (TMA) {
+            mbar_wait(&bar[b], (j >> 1) & 1);
+        } else {
+            cp_wait_all();
+            __syncthreads();
+            if (p + 1 <= ze)
+                col_stage<D, TMA>(smem + (b ^ 1) * BUF, maps, &bar[b ^ 1], p + 1, x0, y0, s, P,
+                                  v, true);
+        }
+        const float *buf = smem + b * BUF;
         const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
         if (has_new) {
-            const float *own = buf + (D + 7) * CG::HCH + ty * CTX + tx;
+            const float *own = buf + (D + 5) * CG::HCH + ty * CTX + tx;
 #pragma unroll
             for (int c = 0; c < D2; ++c) {
                 const float a = own[(2 * c) * CG::OCH];
@@ -822,7 +868,6 @@ modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                 C_.dk[NEW][c] = f2(0.0f, 0.0f);
             }
         }
-        __syncthreads();  // transform visible
 #pragma unroll
         for (int dyi = 0; dyi < 3; ++dyi) {
             // window row dy = dyi-1 links key row y to source row y - dy
@@ -838,10 +883,10 @@ modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 S.L[i] = rowp[D * CG::HCH + i];
-                S.gx[i] = rowp[(D + 1) * CG::HCH + i];
-                S.gy[i] = rowp[(D + 2) * CG::HCH + i];
-                S.gz[i] = rowp[(D + 3) * CG::HCH + i];
-                S.dt[i] = rowp[(D + 4) * CG::HCH + i];
+                S.dt[i] = rowp[(D + 1) * CG::HCH + i];
+                S.gx[i] = rowp[(D + 2) * CG::HCH + i];
+                S.gy[i] = rowp[(D + 3) * CG::HCH + i];
+                S.gz[i] = rowp[(D + 4) * CG::HCH + i];
             }
             // key z sees sources in plane p at window offset dz = z - p
             if (dyi == 0) {
@@ -858,6 +903,8 @@ modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                 col_slot<D, 2, -1>(C_, OLD, S, sB2);
             }
         }
+        if (TMA && last_out(&cnt[b]) && p + 2 <= ze)
+            col_stage<D, TMA>(smem + b * BUF, maps, &bar[b], p + 2, x0, y0, s, P, v, true);
         if (has_old && vv) {
             const int64_t off = (int64_t)(p - 1) * v.hw + (int64_t)y * v.h + x;
 #pragma unroll
@@ -944,8 +991,9 @@ static void set_smem(KFn k, size_t sm) {
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
 }
 
-// shared memory: two buffers + 2 mbarriers (8 floats) + 27 bias pairs
-constexpr size_t kTail = 8 + 64;
+// shared memory: two buffers + 2 mbarriers (8 floats) + 27 bias pairs (64)
+// + 2 buffer-release counters
+constexpr size_t kTail = 8 + 64 + 8;
 
 template <int D>
 static cudaError_t fwd_launch(const float *Q, const float *K, const float *B, mdg_dims3 d, int S,
@@ -978,17 +1026,19 @@ static cudaError_t fwd_launch(const float *Q, const float *K, const float *B, md
 template <int D, bool TMA, bool ACC>
 static void row_launch(dim3 g, size_t sm, cudaStream_t st, const Maps &m, const float *Q,
                        const float *K, const float *B, const float *SF, const float *LSE,
-                       const float *gSF, const Vol &v, int zc, float *gQ, float *part) {
+                       const float *gSF, const Vol &v, int zc, float *gQ, float *part,
+                       float *aux) {
     set_smem(modet_bwd_row_k<D, TMA, ACC>, sm);
-    modet_bwd_row_k<D, TMA, ACC><<<g, 256, sm, st>>>(m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part);
+    modet_bwd_row_k<D, TMA, ACC><<<g, 256, sm, st>>>(m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part,
+                                                     aux);
 }
 
 template <int D, bool TMA, bool ACC>
 static void col_launch(dim3 g, size_t sm, cudaStream_t st, const Maps &m, const float *Q,
                        const float *K, const float *B, const float *SF, const float *LSE,
-                       const float *gSF, const Vol &v, int zc, float *gK) {
+                       const float *gSF, const Vol &v, int zc, float *gK, const float *aux) {
     set_smem(modet_bwd_col_k<D, TMA, ACC>, sm);
-    modet_bwd_col_k<D, TMA, ACC><<<g, 256, sm, st>>>(m, Q, K, B, SF, LSE, gSF, v, zc, gK);
+    modet_bwd_col_k<D, TMA, ACC><<<g, 256, sm, st>>>(m, Q, K, B, SF, LSE, gSF, v, zc, gK, aux);
 }
 
 template <int D>
@@ -998,13 +1048,17 @@ static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, co
     const Vol v{d.h, d.w, d.l, (int64_t)d.h * d.w * d.l, (int64_t)d.h * d.w};
     const bool tma = tma_ok(v, {Q, K, SF, LSE, gSF});
     cudaError_t e = cudaSuccess;
-    if (gQ || gB) {
+    // the row kernel always runs when dK is wanted: it writes the per-source
+    // statistics {LSE*log2e, gSF.SF} the column kernel gathers
+    float *aux = nullptr;
+    keep_pool_mapped();
+    if (gK && (e = cudaMallocAsync(&aux, (size_t)2 * S * v.n * sizeof(float), st))) return e;
+    if (gQ || gB || gK) {
         const int gx = (d.h + RTX - 1) / RTX, gy = (d.w + RTY - 1) / RTY;
         const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 2 : 1);
         const int nzc = (d.l + zc - 1) / zc;
         const int ncta = gx * gy * nzc;
         float *part = nullptr;
-        keep_pool_mapped();  // no remapping of this scratch after every sync
         if ((e = cudaMallocAsync(&part, (size_t)S * ncta * 27 * sizeof(float), st))) return e;
         const size_t sm = (2 * (D * RG::HCH + (D + 7) * RG::OCH) + kTail) * sizeof(float);
         Maps m{};
@@ -1012,11 +1066,11 @@ static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, co
                        make_maps_a(&m.a, Q, LSE, gSF, SF, v, S, D, RTX, RTY);
         const dim3 g(gx, gy, S * nzc);
         if (t) {
-            if (acc) row_launch<D, true, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part);
-            else row_launch<D, true, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part);
+            if (acc) row_launch<D, true, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part, aux);
+            else row_launch<D, true, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part, aux);
         } else {
-            if (acc) row_launch<D, false, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part);
-            else row_launch<D, false, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part);
+            if (acc) row_launch<D, false, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part, aux);
+            else row_launch<D, false, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gQ, part, aux);
         }
         g_launches.fetch_add(1);
         if (gB) {
@@ -1030,19 +1084,23 @@ static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, co
         const int gx = (d.h + CTX - 1) / CTX, gy = (d.w + CTY - 1) / CTY;
         const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 2 : 1);
         const int nzc = (d.l + zc - 1) / zc;
-        const size_t sm = (2 * ((D + 7) * CG::HCH + D * CG::OCH) + kTail) * sizeof(float);
+        const size_t sm = (2 * ((D + 5) * CG::HCH + D * CG::OCH) + kTail) * sizeof(float);
         Maps m{};
-        const bool t = tma && make_map(&m.k, K, v, S * D, CTX, CTY) &&
-                       make_maps_a(&m.a, Q, LSE, gSF, SF, v, S, D, kBoxX, CG::PY);
+        const bool t = tma && reinterpret_cast<uintptr_t>(aux) % 16 == 0 &&
+                       make_map(&m.k, K, v, S * D, CTX, CTY) &&
+                       make_map(&m.a.q, Q, v, S * D, kBoxX, CG::PY) &&
+                       make_map(&m.a.g, gSF, v, 3 * S, kBoxX, CG::PY) &&
+                       make_map(&m.aux, aux, v, 2 * S, kBoxX, CG::PY);
         const dim3 g(gx, gy, S * nzc);
         if (t) {
-            if (acc) col_launch<D, true, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK);
-            else col_launch<D, true, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK);
+            if (acc) col_launch<D, true, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK, aux);
+            else col_launch<D, true, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK, aux);
         } else {
-            if (acc) col_launch<D, false, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK);
-            else col_launch<D, false, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK);
+            if (acc) col_launch<D, false, true>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK, aux);
+            else col_launch<D, false, false>(g, sm, st, m, Q, K, B, SF, LSE, gSF, v, zc, gK, aux);
         }
         g_launches.fetch_add(1);
+        cudaFreeAsync(aux, st);
         if ((e = cudaPeekAtLastError())) return e;
     }
     return e;
