@@ -138,7 +138,7 @@ class AddPool {
   public:
     AddPool() {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        nthreads_ = (int)std::min(8u, std::max(1u, hw / 2));
+        nthreads_ = (int)std::min(12u, std::max(1u, hw * 3 / 4));
         for (int t = 1; t < nthreads_; ++t) workers_.emplace_back([this, t] { loop(t); });
     }
     ~AddPool() {
@@ -150,16 +150,19 @@ class AddPool {
         cv_.notify_all();
         for (auto &w : workers_) w.join();
     }
-    void add(float *dst, const float *src, int64_t m) {
-        if (m < (1 << 18) || nthreads_ == 1) {
-            add_range(dst, src, 0, m);
+    // dst[r*stride + i] += src[r*stride + i] for r < rows, i < m
+    void add(float *dst, const float *src, int64_t m, int rows, int64_t stride) {
+        dst_ = dst;
+        src_ = src;
+        m_ = m;
+        rows_ = rows;
+        stride_ = stride;
+        if (m * rows < (1 << 18) || nthreads_ == 1) {
+            span(0, m * rows);
             return;
         }
         {
             std::lock_guard<std::mutex> lk(mu_);
-            dst_ = dst;
-            src_ = src;
-            m_ = m;
             pending_ = nthreads_ - 1;
             ++gen_;
         }
@@ -170,12 +173,20 @@ class AddPool {
     }
 
   private:
-    static void add_range(float *d, const float *s, int64_t a, int64_t b) {
-        for (int64_t i = a; i < b; ++i) d[i] += s[i];
+    // flat element range [a, b) of the rows x m job
+    void span(int64_t a, int64_t b) {
+        while (a < b) {
+            const int64_t r = a / m_, i0 = a - r * m_;
+            const int64_t i1 = std::min<int64_t>(m_, i0 + (b - a));
+            float *d = dst_ + r * stride_;
+            const float *sp = src_ + r * stride_;
+            for (int64_t i = i0; i < i1; ++i) d[i] += sp[i];
+            a += i1 - i0;
+        }
     }
     void slice(int t) {
-        const int64_t a = m_ * t / nthreads_, b = m_ * (t + 1) / nthreads_;
-        add_range(dst_, src_, a, b);
+        const int64_t tot = m_ * rows_;
+        span(tot * t / nthreads_, tot * (t + 1) / nthreads_);
     }
     void loop(int t) {
         uint64_t seen = 0;
@@ -202,13 +213,19 @@ class AddPool {
     bool stop_ = false;
     float *dst_ = nullptr;
     const float *src_ = nullptr;
-    int64_t m_ = 0;
+    int64_t m_ = 0, stride_ = 0;
+    int rows_ = 1;
 };
 
-void host_add(float *dst, const float *src, int64_t m) {
+AddPool &add_pool() {
     static AddPool pool;
-    pool.add(dst, src, m);
+    return pool;
 }
+// dst[r*stride + i] += src[r*stride + i]  (one fp32 add per element)
+void host_add_rows(float *dst, const float *src, int64_t m, int rows, int64_t stride) {
+    add_pool().add(dst, src, m, rows, stride);
+}
+void host_add(float *dst, const float *src, int64_t m) { host_add_rows(dst, src, m, 1, 0); }
 
 constexpr int kPipeMinPlanes = 16;       // below this the plain call wins
 constexpr int64_t kPipeMinVoxels = 1 << 20;
@@ -387,10 +404,8 @@ struct PipeCtx {
             const int64_t o = (int64_t)ck.z0[i] * hw * a.C;
             host_add(host + o, stage + o, m * a.C);
         } else {
-            for (int c = 0; c < a.C; ++c) {
-                const int64_t o = (int64_t)c * n + (int64_t)ck.z0[i] * hw;
-                host_add(host + o, stage + o, m);
-            }
+            const int64_t o = (int64_t)ck.z0[i] * hw;
+            host_add_rows(host + o, stage + o, m, a.C, n);
         }
     }
     // halo planes of chunk i from its neighbours' interiors (or `fill` at the
@@ -648,13 +663,13 @@ mdg_status warp_bwd_host_pipelined(const float *in, int C, mdg_dims3 d, const fl
         const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
         MDG_PIPE_TRY(cudaEventSynchronize(dwn[i]));
         if (gfield)
-            for (int c = 0; c < 3; ++c) host_add(gfield + c * n + p0, sf + c * n + p0, m);
+            host_add_rows(gfield + p0, sf + p0, m, 3, n);
     }
     for (int i = 0; i < N; ++i) {
         const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
         MDG_PIPE_TRY(cudaEventSynchronize(gdw[i]));
         if (gin)
-            for (int c = 0; c < C; ++c) host_add(gin + c * n + p0, si + c * n + p0, m);
+            host_add_rows(gin + p0, si + p0, m, C, n);
     }
     MDG_PIPE_TRY(cudaStreamSynchronize(P.down));
     return MDG_OK;
