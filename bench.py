@@ -249,6 +249,10 @@ def run_ours(args):
     # ---------------- e2e: the reference-facing host-buffer C-ABI calls
     e2e = None if args.no_e2e else run_e2e(args, L, host_in, world, dev)
 
+    # ---------------- the decoding pyramid around the op,
+    # reported beside the headline (it is not part of `value`)
+    pyramid = None if args.no_pyramid else run_pyramid(dev)
+
     peak, peak_kind = load_peak()
     dom = max(per_op, key=lambda k: per_op[k])
     achieved = BYTES[dom] * n / (per_op[dom] * 1e-3) / 1e9
@@ -274,6 +278,7 @@ def run_ours(args):
                           "frac": round(step_bytes / (ms_max * 1e-3) / 1e9 / peak, 4),
                           "bytes_per_step": step_bytes},
         "e2e": e2e,
+        "pyramid": pyramid,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -283,6 +288,59 @@ def run_ours(args):
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_pyramid(dev, reps=5):
+    """Decoder pyramid (build_pipeline minus the encoder, small preset: heads
+    8,4,2,1,1, hd 6, channels 128..8) on synthetic features at 160x192x224:
+    device time of one forward and one backward (CUDA events)."""
+    import torch
+
+    from paper_2403_16526_b200 import ops
+
+    dims = [DIMS]
+    for _ in range(4):
+        dims.append(tuple((v + 1) // 2 for v in dims[-1]))
+    dims = dims[::-1]
+    chans, heads = (128, 64, 32, 16, 8), (8, 4, 2, 1, 1)
+    g = torch.Generator(device=dev).manual_seed(0)
+    ff = [torch.randn(c, d[2], d[1], d[0], device=dev, generator=g) for c, d in zip(chans, dims)]
+    mf = [torch.randn(c, d[2], d[1], d[0], device=dev, generator=g) for c, d in zip(chans, dims)]
+    lps = []
+    for c, Sh in zip(chans, heads):
+        K = Sh * HD
+        lps.append(ops.LevelParams(
+            ops.ProjectionParams(torch.randn(K, c, device=dev, generator=g) * 0.3,
+                                 torch.zeros(K, device=dev), torch.ones(K, device=dev),
+                                 torch.zeros(K, device=dev)),
+            torch.randn(Sh, 27, device=dev, generator=g) * 0.5,
+            torch.randn(3, 3 * Sh, 3, 3, 3, device=dev, generator=g) * 0.01,
+            torch.zeros(3, device=dev)))
+    cfg = ops.ModelConfig(heads_per_level=heads, head_dim=HD)
+    pyr = ops.Pyramid(cfg, dims, chans, check_finite=False)
+    gphi = torch.randn(3, DIMS[2], DIMS[1], DIMS[0], device=dev, generator=g)
+    grads = [p.zeros_like() for p in lps]
+    gf = [torch.zeros_like(t) for t in ff]
+    gm = [torch.zeros_like(t) for t in mf]
+    for _ in range(2):
+        pyr.forward(ff, mf, lps)
+        pyr.backward(gphi, grads, gf, gm)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    tf, tb = [], []
+    for _ in range(reps):
+        e[0].record()
+        pyr.forward(ff, mf, lps)
+        e[1].record()
+        pyr.backward(gphi, grads, gf, gm)
+        e[2].record()
+        torch.cuda.synchronize()
+        tf.append(e[0].elapsed_time(e[1]))
+        tb.append(e[1].elapsed_time(e[2]))
+    return {"workload": "decoder pyramid (build_pipeline minus encoder), small preset, "
+                        "160x192x224 fine level, synthetic features",
+            "fwd_ms": round(statistics.median(tf), 3), "bwd_ms": round(statistics.median(tb), 3),
+            "arena_mib": round(pyr.device_bytes / 2 ** 20, 1)}
 
 
 def run_e2e(args, L, host_in, world, dev):
@@ -473,6 +531,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling)")
+    ap.add_argument("--no-pyramid", action="store_true", help="skip the pyramid timing")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps

@@ -324,7 +324,7 @@ template <int OC>
 __global__ void __launch_bounds__(kTX *kTY, 2)
 conv3_bwd_w_tiled_k(const float *__restrict__ in, int ic, int h, int w, int l,
                     const float *__restrict__ gout, float *__restrict__ part) {
-    __shared__ float slab[kSlab];
+    __shared__ float slab[2][kSlab];
     __shared__ float red[kTX * kTY / 32];
     const int ci = blockIdx.y;
     const int tx = threadIdx.x % kTX, ty = threadIdx.x / kTX;
@@ -339,12 +339,40 @@ conv3_bwd_w_tiled_k(const float *__restrict__ in, int ic, int h, int w, int l,
         for (int t = 0; t < 27; ++t) acc[co][t] = 0.0f;
     }
     const float *src = in + (int64_t)ci * n;
-    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    // double-buffered staging: tile i+1's slab streams in (cp.async, zero
+    // fill outside the volume) while tile i is accumulated
+    auto stage_async = [&](float *dst, int ti) {
         const int bx = ti % ntx, by = (ti / ntx) % nty, bz = ti / (ntx * nty);
         const int x0 = bx * kTX, y0 = by * kTY, z0 = bz * kV;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        for (int r = wid; r < kStageRows; r += 8) {
+            const int dz = r / kHY, yy = r - dz * kHY;
+            const int gy = y0 - 1 + yy, gz = z0 - 1 + dz;
+            const bool rowok = gy >= 0 && gy < w && gz >= 0 && gz < l;
+            const float *srow = src + ((int64_t)(rowok ? gz : 0) * w + (rowok ? gy : 0)) * h;
+            for (int xx = lane; xx < kHX; xx += 32) {
+                const int gx = x0 - 1 + xx;
+                const bool ok = rowok && gx >= 0 && gx < h;
+                const unsigned d = (unsigned)__cvta_generic_to_shared(dst + r * kHX + xx);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d),
+                             "l"(ok ? srow + gx : src), "r"(ok ? 4 : 0));
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    int buf = 0;
+    if ((int)blockIdx.x < ntiles) stage_async(slab[0], blockIdx.x);
+    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        const int tn = ti + gridDim.x;
+        if (tn < ntiles) {
+            stage_async(slab[buf ^ 1], tn);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
+        }
         __syncthreads();
-        stage_slab<1>(slab, src, 1, h, w, l, x0, y0, z0);
-        __syncthreads();
+        const int bx = ti % ntx, by = (ti / ntx) % nty, bz = ti / (ntx * nty);
+        const int x0 = bx * kTX, y0 = by * kTY, z0 = bz * kV;
         const int x = x0 + tx, y = y0 + ty;
         const bool inxy = x < h && y < w;
         const int64_t p0 = ((int64_t)z0 * w + y) * h + x;
@@ -358,7 +386,7 @@ conv3_bwd_w_tiled_k(const float *__restrict__ in, int ic, int h, int w, int l,
                 accb[co] += g[v][co];
             }
         }
-        const float *tp = slab + ty * kHX + tx;
+        const float *tp = slab[buf] + ty * kHX + tx;
 #pragma unroll
         for (int t = 0; t < 27; ++t) {
             const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
@@ -369,6 +397,8 @@ conv3_bwd_w_tiled_k(const float *__restrict__ in, int ic, int h, int w, int l,
                 for (int co = 0; co < OC; ++co) acc[co][t] = fmaf(g[v][co], xv, acc[co][t]);
             }
         }
+        __syncthreads();  // buffer `buf` is refilled two tiles later
+        buf ^= 1;
     }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     float *dst = part + ((int64_t)ci * gridDim.x + blockIdx.x) * (OC * 28);

@@ -134,6 +134,14 @@ __device__ __forceinline__ float lerp_(float a, float b, float f) {
     return add_(mul_(a, sub_(1.0f, f)), mul_(b, f));
 }
 
+// project.cu: the projection backward; bit i of gin_set makes input i's
+// gradient an overwrite instead of an accumulation (internal buffers)
+mdg_status project_qk_bwd_impl(const float *f, const float *m, int C, int64_t n,
+                               const float *weight, const float *bias, const float *ln_g, int K,
+                               int layout, const float *gQ, const float *gK, float *gf,
+                               float *gm, float *gweight, float *gbias, float *gln_g,
+                               float *gln_b, int gin_set, cudaStream_t stream);
+
 // sampling.cu: warp kernels over the voxel range [pb, pe) of a volume
 mdg_status warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *field, float *out,
                           int64_t pb, int64_t pe, cudaStream_t st);

@@ -27,6 +27,7 @@ struct ProjArgs {
     const float *gout[2];
     float *gin[2];
     float *graw[2];  // two-phase backward: pre-norm gradients {K, n} written here
+    int gin_set;     // bit i: overwrite gin[i] instead of accumulating (internal callers)
     int ninputs;
     int C, K;
     int64_t n;
@@ -278,11 +279,12 @@ project_bwd_k(ProjArgs a, const float *__restrict__ W, const float *__restrict__
                 // compiler cannot prove gp[c*n] and gp[(c+1)*n] never alias,
                 // so an interleaved loop would serialise load-after-store
                 float *gp = gin + p;
+                const bool set = (a.gin_set >> which) & 1;
                 for (int c = 0; c < C; c += 4) {
                     float old[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        old[j] = c + j < C ? gp[(int64_t)(c + j) * n] : 0.0f;
+                        old[j] = (c + j < C && !set) ? gp[(int64_t)(c + j) * n] : 0.0f;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         if (c + j >= C) break;
@@ -290,7 +292,7 @@ project_bwd_k(ProjArgs a, const float *__restrict__ W, const float *__restrict__
                         float s = 0.0f;
 #pragma unroll
                         for (int k = 0; k < KMAX; ++k) s = fmaf(gr[k], wc[k], s);
-                        gp[(int64_t)(c + j) * n] = old[j] + s;
+                        gp[(int64_t)(c + j) * n] = set ? s : old[j] + s;
                     }
                 }
             }
@@ -575,6 +577,18 @@ mdg_status mdg_project_qk_bwd(const float *f, const float *m, int C, int64_t n,
                               int layout, const float *gQ, const float *gK, float *gf,
                               float *gm, float *gweight, float *gbias, float *gln_g,
                               float *gln_b, void *stream) {
+    return mdg::project_qk_bwd_impl(f, m, C, n, weight, bias, ln_g, K, layout, gQ, gK, gf, gm,
+                                    gweight, gbias, gln_g, gln_b, 0, S_(stream));
+}
+
+}  // extern "C"
+
+namespace mdg {
+mdg_status project_qk_bwd_impl(const float *f, const float *m, int C, int64_t n,
+                               const float *weight, const float *bias, const float *ln_g, int K,
+                               int layout, const float *gQ, const float *gK, float *gf,
+                               float *gm, float *gweight, float *gbias, float *gln_g,
+                               float *gln_b, int gin_set, cudaStream_t stream) {
     mdg_status s = check_proj(C, n, K, layout);
     if (s != MDG_OK) return s;
     if (n == 0) return MDG_OK;
@@ -594,7 +608,8 @@ mdg_status mdg_project_qk_bwd(const float *f, const float *m, int C, int64_t n,
     a.n = n;
     a.eps = 1e-5f;
     a.planar = layout == MDG_QK_PLANAR;
-    cudaStream_t st = S_(stream);
+    a.gin_set = gin_set;
+    cudaStream_t st = stream;
     MDG_REQUIRE(proj_smem_bytes(K, C) <= 200 * 1024,
                 "project_qk_bwd: C * K too large for the shared-memory weight block");
     // K == 6 (head_dim 6, one head: the fine levels) gets an exact instantiation
@@ -605,4 +620,4 @@ mdg_status mdg_project_qk_bwd(const float *f, const float *m, int C, int64_t n,
     return project_bwd_launch<64, 1, false>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
 }
 
-}  // extern "C"
+}  // namespace mdg

@@ -284,17 +284,14 @@ mdg_status mdg_pyramid_backward(mdg_pyramid *p, const float *gphi, const mdg_lev
                               c.neighborhood, MDG_QK_PLANAR, p->g_q, p->g_k, gB, 0, st));
         // projection: K came from m_in (warped moving features) for k > 0
         const float *m_in = k > 0 ? L.m_in : p->m_saved[k];
-        float *g_min = nullptr;
-        if (k > 0) {
-            MDG_TRY(zero(p->g_min, (int64_t)L.C * L.n, st));
-            g_min = p->g_min;
-        } else if (gm) {
-            g_min = gm[k];
-        }
-        MDG_TRY(mdg_project_qk_bwd(p->f_saved[k], m_in, L.C, L.n, P.proj_w, P.proj_b, P.ln_g,
-                                   L.K, MDG_QK_PLANAR, p->g_q, p->g_k, gf ? gf[k] : nullptr,
-                                   g_min, G ? G->proj_w : nullptr, G ? G->proj_b : nullptr,
-                                   G ? G->ln_g : nullptr, G ? G->ln_b : nullptr, st));
+        // the warped-moving gradient of k > 0 is an internal buffer: written,
+        // not accumulated (saves its memset and read)
+        float *g_min = k > 0 ? p->g_min : (gm ? gm[k] : nullptr);
+        MDG_TRY(project_qk_bwd_impl(p->f_saved[k], m_in, L.C, L.n, P.proj_w, P.proj_b, P.ln_g,
+                                    L.K, MDG_QK_PLANAR, p->g_q, p->g_k, gf ? gf[k] : nullptr,
+                                    g_min, G ? G->proj_w : nullptr, G ? G->proj_b : nullptr,
+                                    G ? G->ln_g : nullptr, G ? G->ln_b : nullptr,
+                                    k > 0 ? 2 : 0, st));
         if (k > 0) {
             if (c.check_finite)
                 MDG_TRY(check_seq(p, p->g_min, (int64_t)L.C * L.n, tag + "warp", st));

@@ -21,7 +21,7 @@ constexpr int kSB = 256;
 
 struct Corners {
     Ax ax, ay, az;
-    int64_t o00, o10, o01, o11;  // plane offsets of the (y,z) corner rows
+    int o00, o10, o01, o11;  // plane offsets of the (y,z) corner rows (n < 2^31)
 };
 
 __device__ __forceinline__ Corners corners_at(float cx, float cy, float cz, int h, int w, int l) {
@@ -29,7 +29,7 @@ __device__ __forceinline__ Corners corners_at(float cx, float cy, float cz, int 
     c.ax = resolve_axis(cx, h);
     c.ay = resolve_axis(cy, w);
     c.az = resolve_axis(cz, l);
-    const int64_t sy = h, sz = (int64_t)h * w;
+    const int sy = h, sz = h * w;
     c.o00 = c.az.i0 * sz + c.ay.i0 * sy;
     c.o10 = c.az.i0 * sz + c.ay.i1 * sy;
     c.o01 = c.az.i1 * sz + c.ay.i0 * sy;
@@ -39,12 +39,14 @@ __device__ __forceinline__ Corners corners_at(float cx, float cy, float cz, int 
 
 // sampling.hpp:53-68
 __device__ __forceinline__ float sample(const float *__restrict__ pl, const Corners &c) {
-    const int x0 = c.ax.i0, x1 = c.ax.i1;
+    const int x0 = c.ax.i0, dx = c.ax.i1 - c.ax.i0;  // dx = 0 on a collapsed axis
     const float fx = c.ax.f;
-    const float c00 = lerp_(__ldg(pl + c.o00 + x0), __ldg(pl + c.o00 + x1), fx);
-    const float c10 = lerp_(__ldg(pl + c.o10 + x0), __ldg(pl + c.o10 + x1), fx);
-    const float c01 = lerp_(__ldg(pl + c.o01 + x0), __ldg(pl + c.o01 + x1), fx);
-    const float c11 = lerp_(__ldg(pl + c.o11 + x0), __ldg(pl + c.o11 + x1), fx);
+    const float *r00 = pl + (c.o00 + x0), *r10 = pl + (c.o10 + x0);
+    const float *r01 = pl + (c.o01 + x0), *r11 = pl + (c.o11 + x0);
+    const float c00 = lerp_(__ldg(r00), __ldg(r00 + dx), fx);
+    const float c10 = lerp_(__ldg(r10), __ldg(r10 + dx), fx);
+    const float c01 = lerp_(__ldg(r01), __ldg(r01 + dx), fx);
+    const float c11 = lerp_(__ldg(r11), __ldg(r11 + dx), fx);
     const float c0 = lerp_(c00, c10, c.ay.f);
     const float c1 = lerp_(c01, c11, c.ay.f);
     return lerp_(c0, c1, c.az.f);
@@ -53,11 +55,13 @@ __device__ __forceinline__ float sample(const float *__restrict__ pl, const Corn
 // sampling.hpp:73-99 (zero on dead axes)
 __device__ __forceinline__ void sample_grad(const float *__restrict__ pl, const Corners &c,
                                             float g[3]) {
-    const int x0 = c.ax.i0, x1 = c.ax.i1;
-    const float v000 = __ldg(pl + c.o00 + x0), v100 = __ldg(pl + c.o00 + x1);
-    const float v010 = __ldg(pl + c.o10 + x0), v110 = __ldg(pl + c.o10 + x1);
-    const float v001 = __ldg(pl + c.o01 + x0), v101 = __ldg(pl + c.o01 + x1);
-    const float v011 = __ldg(pl + c.o11 + x0), v111 = __ldg(pl + c.o11 + x1);
+    const int x0 = c.ax.i0, dx = c.ax.i1 - c.ax.i0;
+    const float *r00 = pl + (c.o00 + x0), *r10 = pl + (c.o10 + x0);
+    const float *r01 = pl + (c.o01 + x0), *r11 = pl + (c.o11 + x0);
+    const float v000 = __ldg(r00), v100 = __ldg(r00 + dx);
+    const float v010 = __ldg(r10), v110 = __ldg(r10 + dx);
+    const float v001 = __ldg(r01), v101 = __ldg(r01 + dx);
+    const float v011 = __ldg(r11), v111 = __ldg(r11 + dx);
     const float fx = c.ax.f, fy = c.ay.f, fz = c.az.f;
     const float gx = sub_(1.0f, fx), gy = sub_(1.0f, fy), gz = sub_(1.0f, fz);
     g[0] = g[1] = g[2] = 0.0f;
@@ -74,18 +78,20 @@ __device__ __forceinline__ void sample_grad(const float *__restrict__ pl, const 
 
 // sampling.hpp:103-118 with native fp32 reductions
 __device__ __forceinline__ void scatter(float *__restrict__ gp, const Corners &c, float g) {
-    const int x0 = c.ax.i0, x1 = c.ax.i1;
+    const int x0 = c.ax.i0, dx = c.ax.i1 - c.ax.i0;
     const float wx0 = sub_(1.0f, c.ax.f), wx1 = c.ax.f;
     const float wy0 = sub_(1.0f, c.ay.f), wy1 = c.ay.f;
     const float wz0 = sub_(1.0f, c.az.f), wz1 = c.az.f;
-    atomicAdd(gp + c.o00 + x0, mul_(mul_(mul_(g, wx0), wy0), wz0));
-    atomicAdd(gp + c.o00 + x1, mul_(mul_(mul_(g, wx1), wy0), wz0));
-    atomicAdd(gp + c.o10 + x0, mul_(mul_(mul_(g, wx0), wy1), wz0));
-    atomicAdd(gp + c.o10 + x1, mul_(mul_(mul_(g, wx1), wy1), wz0));
-    atomicAdd(gp + c.o01 + x0, mul_(mul_(mul_(g, wx0), wy0), wz1));
-    atomicAdd(gp + c.o01 + x1, mul_(mul_(mul_(g, wx1), wy0), wz1));
-    atomicAdd(gp + c.o11 + x0, mul_(mul_(mul_(g, wx0), wy1), wz1));
-    atomicAdd(gp + c.o11 + x1, mul_(mul_(mul_(g, wx1), wy1), wz1));
+    float *r00 = gp + (c.o00 + x0), *r10 = gp + (c.o10 + x0);
+    float *r01 = gp + (c.o01 + x0), *r11 = gp + (c.o11 + x0);
+    atomicAdd(r00, mul_(mul_(mul_(g, wx0), wy0), wz0));
+    atomicAdd(r00 + dx, mul_(mul_(mul_(g, wx1), wy0), wz0));
+    atomicAdd(r10, mul_(mul_(mul_(g, wx0), wy1), wz0));
+    atomicAdd(r10 + dx, mul_(mul_(mul_(g, wx1), wy1), wz0));
+    atomicAdd(r01, mul_(mul_(mul_(g, wx0), wy0), wz1));
+    atomicAdd(r01 + dx, mul_(mul_(mul_(g, wx1), wy0), wz1));
+    atomicAdd(r11, mul_(mul_(mul_(g, wx0), wy1), wz1));
+    atomicAdd(r11 + dx, mul_(mul_(mul_(g, wx1), wy1), wz1));
 }
 
 // voxel counts are < 2^31 (dims_ok), so the decomposition runs in 32-bit
@@ -103,10 +109,11 @@ struct Oct {
     float v000, v100, v010, v110, v001, v101, v011, v111;
 };
 __device__ __forceinline__ Oct load_oct(const float *__restrict__ pl, const Corners &c) {
-    const int x0 = c.ax.i0, x1 = c.ax.i1;
-    return Oct{__ldg(pl + c.o00 + x0), __ldg(pl + c.o00 + x1), __ldg(pl + c.o10 + x0),
-               __ldg(pl + c.o10 + x1), __ldg(pl + c.o01 + x0), __ldg(pl + c.o01 + x1),
-               __ldg(pl + c.o11 + x0), __ldg(pl + c.o11 + x1)};
+    const int x0 = c.ax.i0, dx = c.ax.i1 - c.ax.i0;
+    const float *r00 = pl + (c.o00 + x0), *r10 = pl + (c.o10 + x0);
+    const float *r01 = pl + (c.o01 + x0), *r11 = pl + (c.o11 + x0);
+    return Oct{__ldg(r00), __ldg(r00 + dx), __ldg(r10), __ldg(r10 + dx),
+               __ldg(r01), __ldg(r01 + dx), __ldg(r11), __ldg(r11 + dx)};
 }
 // sampling.hpp:53-68 on loaded corners
 __device__ __forceinline__ float lerp_oct(const Oct &o, const Corners &c) {
@@ -148,8 +155,8 @@ warp_fwd_k(const float *__restrict__ in, int C, int h, int w, int l,
                                  add_((float)z, __ldg(field + 2 * n + p)), h, w, l);
     if (CT > 0) {
         // 32-bit element offsets of the 4 corner rows (x0 corner; x1 = +1)
-        const int r00 = (int)(c.o00 + c.ax.i0), r10 = (int)(c.o10 + c.ax.i0);
-        const int r01 = (int)(c.o01 + c.ax.i0), r11 = (int)(c.o11 + c.ax.i0);
+        const int r00 = c.o00 + c.ax.i0, r10 = c.o10 + c.ax.i0;
+        const int r01 = c.o01 + c.ax.i0, r11 = c.o11 + c.ax.i0;
         const float fx = c.ax.f, fy = c.ay.f, fz = c.az.f;
         const float2 FX = make_float2(fx, fx), GX = make_float2(sub_(1.0f, fx), sub_(1.0f, fx));
         const float2 FY = make_float2(fy, fy), GY = make_float2(sub_(1.0f, fy), sub_(1.0f, fy));
@@ -226,7 +233,8 @@ template <int CT>
 __global__ void __launch_bounds__(kSB)
 warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, const float *__restrict__ gout,
-           float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe) {
+           float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe,
+           int compose) {
     const int64_t n = (int64_t)h * w * l;
     const int64_t p0 = pb + (int64_t)blockIdx.x * kSB + threadIdx.x;  // voxels [pb, pe)
     // CT > 0 keeps every lane alive for the warp-level scatter merge
@@ -241,8 +249,8 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
     if (CT > 0) {
         // channel pairs; corner rows as 32-bit element offsets (x1 = x0 + 1;
         // the launcher routes h == 1, where x1 == x0, to the CT == 0 kernel)
-        const int r00 = (int)(c.o00 + c.ax.i0), r10 = (int)(c.o10 + c.ax.i0);
-        const int r01 = (int)(c.o01 + c.ax.i0), r11 = (int)(c.o11 + c.ax.i0);
+        const int r00 = c.o00 + c.ax.i0, r10 = c.o10 + c.ax.i0;
+        const int r01 = c.o01 + c.ax.i0, r11 = c.o11 + c.ax.i0;
         XMerge mg;
         if (gin) {
             xmerge_row(r00, ok, mg.in[0], mg.out[0]);
@@ -335,9 +343,18 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
         }
     }
     if (gfield && ok) {
-        gfield[p] = add_(gfield[p], gx);
-        gfield[n + p] = add_(gfield[n + p], gy);
-        gfield[2 * n + p] = add_(gfield[2 * n + p], gz);
+        if (compose) {
+            // op_compose = op_add(res, op_warp(prev, res)) (ops.hpp:295-298): the
+            // add node replays first (gres += gout), then the warp adds its
+            // coordinate gradient (tape.hpp:146-156)
+            gfield[p] = add_(add_(gfield[p], __ldg(gout + p)), gx);
+            gfield[n + p] = add_(add_(gfield[n + p], __ldg(gout + n + p)), gy);
+            gfield[2 * n + p] = add_(add_(gfield[2 * n + p], __ldg(gout + 2 * n + p)), gz);
+        } else {
+            gfield[p] = add_(gfield[p], gx);
+            gfield[n + p] = add_(gfield[n + p], gy);
+            gfield[2 * n + p] = add_(gfield[2 * n + p], gz);
+        }
     }
 }
 
@@ -504,7 +521,7 @@ mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
                           cudaStream_t st) {
     if (pe <= pb) return MDG_OK;
     MDG_WARP_DISPATCH(warp_bwd_k, d.h >= 2 ? C : 0, (grid1d(pe - pb, kSB), kSB, 0, st),
-                      (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe));
+                      (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe, 0));
     MDG_LAUNCHED();
     return MDG_OK;
 }
@@ -560,6 +577,13 @@ mdg_status mdg_compose_bwd(const float *prev, const float *res, mdg_dims3 d,
     if (n == 0 || (!gprev && !gres)) return MDG_OK;
     MDG_REQUIRE(prev && res && gout, "compose: null pointer");
     MDG_REQUIRE(!(gprev && gprev == gres), "compose: gprev and gres must not alias");
+    if (d.h >= 2 && gres) {
+        // the warp backward with C = 3 (x-merged scatter) plus the add node
+        warp_bwd_k<3><<<grid1d(n, kSB), kSB, 0, S_(stream)>>>(prev, 3, d.h, d.w, d.l, res, gout,
+                                                              gprev, gres, 0, n, 1);
+        MDG_LAUNCHED();
+        return MDG_OK;
+    }
     compose_bwd_k<<<grid1d(n, kSB), kSB, 0, S_(stream)>>>(prev, res, d.h, d.w, d.l, gout, gprev,
                                                           gres);
     MDG_LAUNCHED();
