@@ -229,12 +229,11 @@ __device__ __forceinline__ void scatter_row2(float *ia, float *ib, bool two, boo
 
 // --------------------------------------------------------------- warp bwd
 // sampling.hpp:139-167 (gfield: same per-channel order => bit-exact)
-template <int CT>
+template <int CT, bool COMPOSE = false>
 __global__ void __launch_bounds__(kSB)
 warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, const float *__restrict__ gout,
-           float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe,
-           int compose) {
+           float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe) {
     const int64_t n = (int64_t)h * w * l;
     const int64_t p0 = pb + (int64_t)blockIdx.x * kSB + threadIdx.x;  // voxels [pb, pe)
     // CT > 0 keeps every lane alive for the warp-level scatter merge
@@ -343,7 +342,7 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
         }
     }
     if (gfield && ok) {
-        if (compose) {
+        if (COMPOSE) {
             // op_compose = op_add(res, op_warp(prev, res)) (ops.hpp:295-298): the
             // add node replays first (gres += gout), then the warp adds its
             // coordinate gradient (tape.hpp:146-156)
@@ -521,7 +520,7 @@ mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
                           cudaStream_t st) {
     if (pe <= pb) return MDG_OK;
     MDG_WARP_DISPATCH(warp_bwd_k, d.h >= 2 ? C : 0, (grid1d(pe - pb, kSB), kSB, 0, st),
-                      (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe, 0));
+                      (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe));
     MDG_LAUNCHED();
     return MDG_OK;
 }
@@ -579,8 +578,8 @@ mdg_status mdg_compose_bwd(const float *prev, const float *res, mdg_dims3 d,
     MDG_REQUIRE(!(gprev && gprev == gres), "compose: gprev and gres must not alias");
     if (d.h >= 2 && gres) {
         // the warp backward with C = 3 (x-merged scatter) plus the add node
-        warp_bwd_k<3><<<grid1d(n, kSB), kSB, 0, S_(stream)>>>(prev, 3, d.h, d.w, d.l, res, gout,
-                                                              gprev, gres, 0, n, 1);
+        warp_bwd_k<3, true><<<grid1d(n, kSB), kSB, 0, S_(stream)>>>(prev, 3, d.h, d.w, d.l, res,
+                                                                    gout, gprev, gres, 0, n);
         MDG_LAUNCHED();
         return MDG_OK;
     }
