@@ -2,41 +2,43 @@
 //
 // Layout: Q, K planar {S*d, n}; head s owns channel planes s*d .. s*d+d-1.
 //
-// Every kernel is a z-marching CTA: it owns an x-y column tile and walks a
-// chunk of z.  Step p consumes one shared-memory buffer holding
+// Every kernel is a z-marching CTA of 32 x 8 threads: it owns an x-y column
+// tile (one voxel column per thread) and walks a chunk of z.  Step p consumes
+// one shared-memory buffer holding
 //   * the HALO plane p of the arrays the thread GATHERS from (tile + 1-voxel
 //     x/y halo), and
 //   * the tile INTERIOR of the arrays the thread OWNS, at plane p+1 (the voxel
 //     that enters the in-flight window this step),
-// double-buffered so step p+1's buffer lands while step p computes.  Staging
-// is 4-D TMA box loads (cp.async.bulk.tensor, one elected thread, mbarrier
-// completion).  TMA's hardware out-of-bounds zero fill is exactly the
+// double-buffered.  Staging is 4-D TMA box loads (cp.async.bulk.tensor, one
+// issuing thread, mbarrier completion); TMA's out-of-bounds zero fill is the
 // reference's "out-of-bounds key contributes nothing, logit = bias" rule
 // (attention.hpp:77-81).  The innermost TMA start coordinate must be 16-byte
-// aligned, so halo boxes start at x0-4 and are 40 wide (the logical halo
-// column rx lives at physical column rx+3).  Volumes whose row pitch is not a
-// multiple of 16 bytes (h % 4 != 0) use 4-byte cp.async into the same layout.
+// aligned, so halo boxes start at x0-4 and are 40 wide (logical halo column rx
+// lives at physical column rx+3).  Volumes whose row pitch is not a multiple
+// of 16 bytes (h % 4 != 0) use 4-byte cp.async into the same layout.
 //
 // A staged x-strip is read from shared memory ONCE per step and used by the
 // three voxels of the thread's column that have plane p in their 3x3x3 window
-// (z = p+1, p, p-1: the "in-flight" slots).
-//
-// Arithmetic runs on Blackwell's packed FP32 pipe (FFMA2 / FADD2 / FMUL2):
-// the forward and column kernels pair the thread's two x-adjacent voxels, the
-// row kernel pairs channels.  A 3-register FFMA issues every 2 cycles per
-// SMSP, so the packed form doubles the FP32 work per issue slot.
+// (z = p+1, p, p-1: the "in-flight" slots).  Slot arithmetic is unconditional
+// (idle slots carry LSE = +inf / zero data), so the three slots' dependency
+// chains interleave.  Channels are processed in pairs on Blackwell's packed
+// FP32 pipe (FFMA2 / FADD2 / FMUL2), which doubles FP32 work per issue slot.
 //
 //   fwd  (modet_fwd_tiled_k): 27 logits per voxel in log2 units (q pre-scaled
-//        by log2 e), online softmax one 3-logit x-row at a time: the first row
-//        sets the reference max, later rows rescale (warp-uniform, rare) only
-//        when the running max grows by > 16 in log2 units; fused
-//        offset-weighted sums.  Writes SF {3S,n}, LSE {S,n} (natural log).
+//        by log2 e); branch-free online softmax one 3-logit x-row at a time —
+//        the first row sets the reference max, later rows never rescale;
+//        voxels whose sum overflowed or that saw a non-finite logit are queued
+//        and recomputed exactly by modet_fwd_fixup_k.  Writes SF {3S,n} and
+//        LSE {S,n} (natural log).  One block barrier per step (3 CTAs/SM).
 //   bwd  row kernel (modet_bwd_row_k): p as query.  W = exp2(l - LSE*log2e)
 //        recomputed, dl = W*(gSF.off(o) - gSF.SF) (since <W, gW> = gSF.SF),
-//        dQ_p += dl*K_{p+o}, per-CTA dB partials (deterministic reduce).
+//        dQ_p += dl*K_{p+o}, per-CTA dB partials (deterministic reduce), and
+//        the per-voxel {LSE*log2e, gSF.SF} the column kernel consumes.
 //   bwd  column kernel (modet_bwd_col_k): q as key, gathering from staged
 //        sources r = q - off(o): dK_q += dl(r,o)*Q_r.  The reference's scatter
 //        (attention.hpp:159-162) as a gather: no atomics, fixed order.
+//   Both backward kernels release buffers without a block barrier: the last
+//   warp to finish a step re-arms that buffer's TMA for the step two ahead.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -49,7 +51,6 @@ namespace tiled {
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
-constexpr float kRescale = 16.0f;  // lazy-rescale threshold (log2 units)
 constexpr int kXOff = 3;           // physical column of logical halo column 0
 constexpr int kBoxX = 40;          // halo box width (starts at x0 - 4)
 
@@ -458,7 +459,7 @@ modet_fwd_tiled_k(const __grid_constant__ Maps maps, const float *__restrict__ Q
             fwd_stage<D, TMA>(smem + (b ^ 1) * BUF, maps, &bar[b ^ 1], p + 1, x0, y0, s, P, v,
                               threadIdx.x == 0);
         const float *buf = smem + b * BUF;
-        const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
+        const bool has_new = p + 1 < ze, has_old = p - 1 >= zb;
         if (has_new) {
             const float *own = buf + D * FG::HCH + ty * FTX + tx;
 #pragma unroll
@@ -637,7 +638,7 @@ modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                                   v, true);
         }
         const float *buf = smem + b * BUF;
-        const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
+        const bool has_new = p + 1 < ze, has_old = p - 1 >= zb;
         if (has_new) {
             // own data of the voxel entering the window; zero outside the
             // volume (TMA / cp.async zero fill) => dl == 0 there
@@ -857,7 +858,7 @@ modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                                   v, true);
         }
         const float *buf = smem + b * BUF;
-        const bool has_new = p + 1 < ze, has_mid = p >= zb && p < ze, has_old = p - 1 >= zb;
+        const bool has_new = p + 1 < ze, has_old = p - 1 >= zb;
         if (has_new) {
             const float *own = buf + (D + 5) * CG::HCH + ty * CTX + tx;
 #pragma unroll
