@@ -230,7 +230,7 @@ __device__ __forceinline__ void scatter_row2(float *ia, float *ib, bool two, boo
 // --------------------------------------------------------------- warp bwd
 // sampling.hpp:139-167 (gfield: same per-channel order => bit-exact)
 template <int CT, bool COMPOSE = false>
-__global__ void __launch_bounds__(kSB)
+__global__ void __launch_bounds__(kSB, 4)
 warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, const float *__restrict__ gout,
            float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe) {
@@ -267,30 +267,20 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
         auto m2 = [](float2 a, float2 b) { return make_float2(mul_(a.x, b.x), mul_(a.y, b.y)); };
         auto a2 = [](float2 a, float2 b) { return make_float2(add_(a.x, b.x), add_(a.y, b.y)); };
         auto s2 = [](float2 a, float2 b) { return make_float2(sub_(a.x, b.x), sub_(a.y, b.y)); };
+        // every channel's upstream gradient up front: loads cannot move across
+        // the scatter's atomics, so loading per channel pair would expose one
+        // memory latency per pair
+        float gv[CT > 0 ? CT : 1];
+#pragma unroll
+        for (int ch = 0; ch < CT; ++ch) gv[ch] = __ldg(gout + (int64_t)ch * n + p);
+        // phase 1, gfield: loads and arithmetic only (no atomics in between,
+        // so corner loads of different channel pairs can be in flight together)
 #pragma unroll
         for (int ch = 0; ch < CT; ch += 2) {
             const bool two = ch + 1 < CT;
             const float *a = in + (int64_t)ch * n, *b = two ? a + n : a;
-            const float ga = __ldg(gout + (int64_t)ch * n + p);
-            const float gb = two ? __ldg(gout + (int64_t)(ch + 1) * n + p) : 0.0f;
-            const float2 g2 = make_float2(ga, gb);
-            if (gin) {
-                // terms ((g*wx)*wy)*wz exactly as sampling.hpp:110-117, with the
-                // shared prefixes computed once
-                const float2 gx0 = m2(g2, GX), gx1 = m2(g2, FX);
-                const float2 g00 = m2(gx0, GY), g10 = m2(gx1, GY), g01 = m2(gx0, FY),
-                             g11 = m2(gx1, FY);
-                const float2 t000 = m2(g00, GZ), t100 = m2(g10, GZ), t010 = m2(g01, GZ),
-                             t110 = m2(g11, GZ), t001 = m2(g00, FZ), t101 = m2(g10, FZ),
-                             t011 = m2(g01, FZ), t111 = m2(g11, FZ);
-                // (a zero gradient gives exact zero terms: the reference's skip
-                // of g == 0 channels, sampling.hpp:152, changes nothing)
-                float *ia = gin + (int64_t)ch * n, *ib = ia + n;
-                scatter_row2(ia, ib, two, ok, r00, t000, t100, mg.in[0], mg.out[0]);
-                scatter_row2(ia, ib, two, ok, r10, t010, t110, mg.in[1], mg.out[1]);
-                scatter_row2(ia, ib, two, ok, r01, t001, t101, mg.in[2], mg.out[2]);
-                scatter_row2(ia, ib, two, ok, r11, t011, t111, mg.in[3], mg.out[3]);
-            }
+            const float ga = gv[ch];
+            const float gb = two ? gv[ch + 1] : 0.0f;
             if (gfield) {
                 const float2 v000 = make_float2(__ldg(a + r00), __ldg(b + r00));
                 const float2 v100 = make_float2(__ldg(a + r00 + 1), __ldg(b + r00 + 1));
@@ -325,6 +315,31 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
                     gy = add_(gy, mul_(gb, cgy.y));
                     gz = add_(gz, mul_(gb, cgz.y));
                 }
+            }
+        }
+        // phase 2, gin: the 8-corner scatter
+#pragma unroll
+        for (int ch = 0; ch < CT; ch += 2) {
+            const bool two = ch + 1 < CT;
+            const float ga = gv[ch];
+            const float gb = two ? gv[ch + 1] : 0.0f;
+            const float2 g2 = make_float2(ga, gb);
+            if (gin) {
+                // terms ((g*wx)*wy)*wz exactly as sampling.hpp:110-117, with the
+                // shared prefixes computed once
+                const float2 gx0 = m2(g2, GX), gx1 = m2(g2, FX);
+                const float2 g00 = m2(gx0, GY), g10 = m2(gx1, GY), g01 = m2(gx0, FY),
+                             g11 = m2(gx1, FY);
+                const float2 t000 = m2(g00, GZ), t100 = m2(g10, GZ), t010 = m2(g01, GZ),
+                             t110 = m2(g11, GZ), t001 = m2(g00, FZ), t101 = m2(g10, FZ),
+                             t011 = m2(g01, FZ), t111 = m2(g11, FZ);
+                // (a zero gradient gives exact zero terms: the reference's skip
+                // of g == 0 channels, sampling.hpp:152, changes nothing)
+                float *ia = gin + (int64_t)ch * n, *ib = ia + n;
+                scatter_row2(ia, ib, two, ok, r00, t000, t100, mg.in[0], mg.out[0]);
+                scatter_row2(ia, ib, two, ok, r10, t010, t110, mg.in[1], mg.out[1]);
+                scatter_row2(ia, ib, two, ok, r01, t001, t101, mg.in[2], mg.out[2]);
+                scatter_row2(ia, ib, two, ok, r11, t011, t111, mg.in[3], mg.out[3]);
             }
         }
     } else {
