@@ -169,22 +169,41 @@ warp_fwd_k(const float *__restrict__ in, int C, int h, int w, int l,
             return make_float2(add_(mul_(a.x, g.x), mul_(b.x, f.x)),
                                add_(mul_(a.y, g.y), mul_(b.y, f.y)));
         };
+        // two channel pairs' corner loads (32 values) in flight at once
+        constexpr int G = CT >= 4 ? 4 : 2;
 #pragma unroll
-        for (int ch = 0; ch + 1 < CT; ch += 2) {
-            const float *a = in + (int64_t)ch * n, *b = a + n;
-            const float2 v000 = make_float2(__ldg(a + r00), __ldg(b + r00));
-            const float2 v100 = make_float2(__ldg(a + r00 + 1), __ldg(b + r00 + 1));
-            const float2 v010 = make_float2(__ldg(a + r10), __ldg(b + r10));
-            const float2 v110 = make_float2(__ldg(a + r10 + 1), __ldg(b + r10 + 1));
-            const float2 v001 = make_float2(__ldg(a + r01), __ldg(b + r01));
-            const float2 v101 = make_float2(__ldg(a + r01 + 1), __ldg(b + r01 + 1));
-            const float2 v011 = make_float2(__ldg(a + r11), __ldg(b + r11));
-            const float2 v111 = make_float2(__ldg(a + r11 + 1), __ldg(b + r11 + 1));
+        for (int cg = 0; cg + 1 < CT; cg += G) {
+            float v[G][8];
+#pragma unroll
+            for (int k = 0; k < G; ++k) {
+                if (cg + k >= CT) break;
+                const float *a = in + (int64_t)(cg + k) * n;
+                v[k][0] = __ldg(a + r00);
+                v[k][1] = __ldg(a + r00 + 1);
+                v[k][2] = __ldg(a + r10);
+                v[k][3] = __ldg(a + r10 + 1);
+                v[k][4] = __ldg(a + r01);
+                v[k][5] = __ldg(a + r01 + 1);
+                v[k][6] = __ldg(a + r11);
+                v[k][7] = __ldg(a + r11 + 1);
+            }
+#pragma unroll
+        for (int ch = cg; ch + 1 < CT && ch < cg + G; ch += 2) {
+            const int k = ch - cg;
+            const float2 v000 = make_float2(v[k][0], v[k + 1][0]);
+            const float2 v100 = make_float2(v[k][1], v[k + 1][1]);
+            const float2 v010 = make_float2(v[k][2], v[k + 1][2]);
+            const float2 v110 = make_float2(v[k][3], v[k + 1][3]);
+            const float2 v001 = make_float2(v[k][4], v[k + 1][4]);
+            const float2 v101 = make_float2(v[k][5], v[k + 1][5]);
+            const float2 v011 = make_float2(v[k][6], v[k + 1][6]);
+            const float2 v111 = make_float2(v[k][7], v[k + 1][7]);
             const float2 c0 = lerp2(lerp2(v000, v100, GX, FX), lerp2(v010, v110, GX, FX), GY, FY);
             const float2 c1 = lerp2(lerp2(v001, v101, GX, FX), lerp2(v011, v111, GX, FX), GY, FY);
             const float2 r = lerp2(c0, c1, GZ, FZ);
             out[(int64_t)ch * n + p] = r.x;
             out[(int64_t)(ch + 1) * n + p] = r.y;
+        }
         }
         if (CT & 1) {
             const int ch = CT - 1;
