@@ -184,6 +184,21 @@ mdg_status mdg_project_qk_bwd(const float *f, const float *m, int C, int64_t n,
                               float *gm, float *gweight, float *gbias, float *gln_g,
                               float *gln_b, void *stream);
 
+/* ===================== registration objective (§8f) =====================
+ * op_total_loss (objective.hpp:71-78): warped = warp(moving, phi);
+ *   total = NCC(fixed, warped; window) + lambda * grad_reg(phi)
+ * (op_ncc_loss objective.hpp:39-69, op_grad_reg ops.hpp:326-382).  fixed,
+ * moving: single-channel volumes {n}; phi {3, n}.  `terms` (device, 3 floats)
+ * receives {total, ncc, reg}; `warped` (nullable) the warped moving image. */
+mdg_status mdg_total_loss_fwd(const float *fixed, const float *moving, const float *phi,
+                              mdg_dims3 d, int window, float lambda, float *terms,
+                              float *warped, void *stream);
+/* backward of `seed * total`: accumulates gphi {3, n} and gmoving {n}
+ * (each nullable) */
+mdg_status mdg_total_loss_bwd(const float *fixed, const float *moving, const float *phi,
+                              mdg_dims3 d, int window, float lambda, float seed, float *gphi,
+                              float *gmoving, void *stream);
+
 /* ======================== decoding pyramid driver ========================
  * The decoder half of build_pipeline (engine.hpp:179-219) on device-resident
  * encoder features: per level k (coarse -> fine)

@@ -95,6 +95,8 @@ class _Lib:
             self._decoder = sig("decoder", ii, ii, _i, _i, _i, ii, ii, ii, ii, pp, pp, pp, _f,
                                 _f, pp, pp, pp, pp)
             self._perr = sig("pipeline_error", C.c_char_p)
+            self._tloss = sig("total_loss", ii, _f, _f, _f, ii, ii, ii, ii, C.c_float, _f, _f,
+                              _f, _f)
             self._lpc = sig("level_param_count", i64, ii, ii, ii, ii)
 
     # -- Q/K projection (ops.hpp:387-497, attention.hpp:351-356) -----------
@@ -167,6 +169,19 @@ class _Lib:
         if rc:
             raise RuntimeError(self._perr().decode())
         return (phi, res, (gparams, gf, gm)) if gphi is not None else (phi, res)
+
+    def total_loss(self, fixed, moving, phi, window=9, lam=1.0, grads=True):
+        """Reference op_total_loss: ({total, ncc, reg}, warped, gphi, gmoving)."""
+        l, w, h = phi.shape[1:]
+        terms = np.zeros(3, np.float32)
+        warped = np.zeros_like(moving)
+        gphi = np.zeros_like(phi) if grads else None
+        gm = np.zeros_like(moving) if grads else None
+        rc = self._tloss(_fp(fixed), _fp(moving), _fp(phi), h, w, l, window, lam, _fp(terms),
+                         _fp(warped), _fp(gphi), _fp(gm))
+        if rc:
+            raise RuntimeError(self._perr().decode())
+        return terms, warped, gphi, gm
 
     def level_param_count(self, C_, S, hd, nb=3):
         return int(self._lpc(C_, S, hd, nb))

@@ -168,4 +168,36 @@ int mdr_decoder(int levels, const int *dims, const int *channels, const int *hea
     return 0;
 }
 
+// op_total_loss (objective.hpp:71-78) = op_ncc_loss(fixed, warp(moving, phi))
+// + lambda * op_grad_reg(phi), forward and the tape backward with seed 1.
+// Single-channel volumes {h,w,l}; phi {3,h,w,l}.  Writes the loss terms
+// (total, ncc, reg) and accumulates gphi / gmoving (nullable).
+int mdr_total_loss(const float *fixed, const float *moving, const float *phi, int h, int w,
+                   int l, int window, float lambda, float *terms, float *warped, float *gphi,
+                   float *gmoving) {
+    try {
+        Tape<float> t;
+        Var f = t.input(tensor_from(fixed, {1, h, w, l}));
+        Var m = t.input(tensor_from(moving, {1, h, w, l}));
+        Var ph = t.input(tensor_from(phi, {3, h, w, l}));
+        Var wv = op_warp(t, m, ph);
+        Var ncc = op_ncc_loss(t, f, wv, window);
+        Var reg = op_grad_reg(t, ph);
+        Var total = lambda == 0.0f ? ncc : op_add(t, ncc, op_scale(t, reg, lambda));
+        terms[0] = t.scalar(total);
+        terms[1] = t.scalar(ncc);
+        terms[2] = t.scalar(reg);
+        if (warped) std::memcpy(warped, t.value(wv).data.data(), (size_t)h * w * l * sizeof(float));
+        if (gphi || gmoving) {
+            t.backward(total);
+            add_into(gphi, t.grad(ph));
+            add_into(gmoving, t.grad(m));
+        }
+    } catch (const std::exception &e) {
+        g_perr = e.what();
+        return 1;
+    }
+    return 0;
+}
+
 }  // extern "C"

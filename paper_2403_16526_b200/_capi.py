@@ -89,6 +89,8 @@ SIGNATURES = {
     "mdg_project_qk_fwd": (_st, [_p, _p, _i, C.c_int64, _p, _p, _p, _p, _i, _i, _p, _p, _p]),
     "mdg_project_qk_bwd": (_st, [_p, _p, _i, C.c_int64, _p, _p, _p, _i, _i, _p, _p, _p, _p,
                                  _p, _p, _p, _p, _p]),
+    "mdg_total_loss_fwd": (_st, [_p, _p, _p, Dims3, _i, _f, _p, _p, _p]),
+    "mdg_total_loss_bwd": (_st, [_p, _p, _p, Dims3, _i, _f, _f, _p, _p, _p]),
     "mdg_pyramid_create": (_st, [C.POINTER(PyramidConfig), C.POINTER(_p)]),
     "mdg_pyramid_destroy": (None, [_p]),
     "mdg_pyramid_forward": (_st, [_p, C.POINTER(_p), C.POINTER(_p), C.POINTER(LevelParams), _p,

@@ -1,0 +1,345 @@
+// loss.cu — the registration objective on sm_100a:
+//   total = NCC(fixed, warp(moving, phi)) + lambda * grad_reg(phi)
+// (objective.hpp:39-78, op_boxsum ops.hpp:301-320, kern::boxsum1d ops.hpp:103-125,
+// op_grad_reg ops.hpp:326-382).
+//
+// NCC: the five windowed statistics (sums of f, g, f^2, g^2, f*g over the
+// zero-padded (2r+1)^3 box) are three separable box-sum passes over a
+// 5-channel product volume; every box sum adds its taps in the reference's
+// order, so the statistics are bit-identical to kern::boxsum1d.  Window counts
+// are the exact integer products cx*cy*cz (what the reference's box sum of
+// ones yields).  The per-voxel cc and the means are deterministic
+// fixed-order reductions (fp32 tolerance vs the reference's sequential sum).
+// Backward: the per-voxel adjoint of cc goes back through the box sums (a
+// zero-padded box sum is self-adjoint, ops.hpp:311) into dL/dwarped, then the
+// warp backward gives dL/dphi (+ dL/dmoving); grad_reg adds its stencil.
+#include <algorithm>
+
+#include "mdg_common.cuh"
+
+namespace mdg {
+
+constexpr int kLB = 256;
+constexpr float kNccEps = 1e-5f;  // objective.hpp:34
+
+struct LDims {
+    int h, w, l;
+    int n;
+};
+
+__device__ __forceinline__ void lxyz(int p, const LDims &d, int &x, int &y, int &z) {
+    const int t = p / d.h;
+    x = p - t * d.h;
+    z = t / d.w;
+    y = t - z * d.w;
+}
+
+// kern::boxsum1d along `axis` for C channel planes: taps t0..t1 in order
+__global__ void __launch_bounds__(kLB)
+box_axis_k(const float *__restrict__ in, int C, LDims d, int axis, int r,
+           float *__restrict__ out) {
+    const int64_t total = (int64_t)C * d.n;
+    for (int64_t i = (int64_t)blockIdx.x * kLB + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * kLB) {
+        const int c = (int)(i / d.n), p = (int)(i - (int64_t)c * d.n);
+        int x, y, z;
+        lxyz(p, d, x, y, z);
+        const int pos = axis == 0 ? x : (axis == 1 ? y : z);
+        const int len = axis == 0 ? d.h : (axis == 1 ? d.w : d.l);
+        const int stride = axis == 0 ? 1 : (axis == 1 ? d.h : d.h * d.w);
+        const int t0 = max(0, pos - r), t1 = min(len - 1, pos + r);
+        const float *src = in + (int64_t)c * d.n + (p - pos * stride);
+        float s = 0.0f;
+        for (int t = t0; t <= t1; ++t) s = add_(s, src[t * stride]);
+        out[i] = s;
+    }
+}
+
+// {f, g, f*f, g*g, f*g} (op_mul, objective.hpp:57-59)
+__global__ void __launch_bounds__(kLB)
+ncc_products_k(const float *__restrict__ f, const float *__restrict__ g, int n,
+               float *__restrict__ out) {
+    const int p = blockIdx.x * kLB + threadIdx.x;
+    if (p >= n) return;
+    const float a = f[p], b = g[p];
+    out[p] = a;
+    out[n + p] = b;
+    out[2 * n + p] = mul_(a, a);
+    out[3 * n + p] = mul_(b, b);
+    out[4 * n + p] = mul_(a, b);
+}
+
+__device__ __forceinline__ float win_count(int x, int y, int z, const LDims &d, int r) {
+    const int cx = min(x + r, d.h - 1) - max(x - r, 0) + 1;
+    const int cy = min(y + r, d.w - 1) - max(y - r, 0) + 1;
+    const int cz = min(z + r, d.l - 1) - max(z - r, 0) + 1;
+    return (float)(cx * cy * cz);
+}
+
+struct NccTerms {
+    float cross, vf, vg, den, cnt, sf, sg;
+};
+// objective.hpp:62-68, same operation order
+__device__ __forceinline__ NccTerms ncc_terms(const float *S, int p, int n, float cnt) {
+    NccTerms t;
+    t.sf = S[p];
+    t.sg = S[n + p];
+    const float sff = S[2 * n + p], sgg = S[3 * n + p], sfg = S[4 * n + p];
+    t.cnt = cnt;
+    t.cross = sub_(sfg, __fdiv_rn(mul_(t.sf, t.sg), cnt));
+    t.vf = sub_(sff, __fdiv_rn(mul_(t.sf, t.sf), cnt));
+    t.vg = sub_(sgg, __fdiv_rn(mul_(t.sg, t.sg), cnt));
+    t.den = add_(mul_(t.vf, t.vg), kNccEps);
+    return t;
+}
+
+// per-CTA partial sums of cc; slot 1..9: grad_reg sums per (component, axis)
+__global__ void __launch_bounds__(kLB)
+ncc_cc_k(const float *__restrict__ S, LDims d, int r, float *__restrict__ part) {
+    float acc = 0.0f;
+    for (int p = blockIdx.x * kLB + threadIdx.x; p < d.n; p += gridDim.x * kLB) {
+        int x, y, z;
+        lxyz(p, d, x, y, z);
+        const NccTerms t = ncc_terms(S, p, d.n, win_count(x, y, z, d, r));
+        acc += __fdiv_rn(mul_(t.cross, t.cross), t.den);
+    }
+    __shared__ float red[kLB];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int m = kLB / 2; m > 0; m >>= 1) {
+        if (threadIdx.x < m) red[threadIdx.x] += red[threadIdx.x + m];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// op_grad_reg sums: for component c and axis a, sum of squared forward
+// differences over the defined positions
+__global__ void __launch_bounds__(kLB)
+grad_reg_k(const float *__restrict__ phi, LDims d, float *__restrict__ part) {
+    float acc[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) acc[i] = 0.0f;
+    const int strides[3] = {1, d.h, d.h * d.w};
+    for (int p = blockIdx.x * kLB + threadIdx.x; p < d.n; p += gridDim.x * kLB) {
+        int x, y, z;
+        lxyz(p, d, x, y, z);
+        const bool ok[3] = {x < d.h - 1, y < d.w - 1, z < d.l - 1};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float *u = phi + (int64_t)c * d.n;
+            const float u0 = u[p];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                if (ok[a]) {
+                    const float df = sub_(u[p + strides[a]], u0);
+                    acc[c * 3 + a] = fmaf(df, df, acc[c * 3 + a]);
+                }
+        }
+    }
+    __shared__ float red[kLB / 32][9];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        float v = acc[i];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+        if (lane == 0) red[wid][i] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 9) {
+        float v = 0.0f;
+        for (int w = 0; w < kLB / 32; ++w) v += red[w][threadIdx.x];
+        part[(int64_t)blockIdx.x * 9 + threadIdx.x] = v;
+    }
+}
+
+// final: terms[0] = total, [1] = ncc, [2] = reg (fixed-order sums)
+__global__ void __launch_bounds__(kLB)
+loss_final_k(const float *__restrict__ cc_part, int ncc_parts, const float *__restrict__ reg_part,
+             int reg_parts, LDims d, float lambda, float *__restrict__ terms) {
+    __shared__ float s[kLB];
+    __shared__ float regs[9];
+    float v = 0.0f;
+    for (int i = threadIdx.x; i < ncc_parts; i += kLB) v += cc_part[i];
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int m = kLB / 2; m > 0; m >>= 1) {
+        if (threadIdx.x < m) s[threadIdx.x] += s[threadIdx.x + m];
+        __syncthreads();
+    }
+    const float cc_sum = s[0];
+    if (threadIdx.x < 9) {
+        float r = 0.0f;
+        if (reg_part)
+            for (int i = 0; i < reg_parts; ++i) r += reg_part[(int64_t)i * 9 + threadIdx.x];
+        regs[threadIdx.x] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // objective.hpp:69: -mean(cc);  ops.hpp:336-355: sum_c sum_a s/defined / 3
+        const float ncc = -(cc_sum * (1.0f / (float)d.n));
+        const int dims[3] = {d.h, d.w, d.l};
+        float tot = 0.0f;
+        for (int c = 0; c < 3; ++c)
+            for (int a = 0; a < 3; ++a) {
+                const int64_t defined = (int64_t)d.n - d.n / dims[a];
+                tot += regs[c * 3 + a] / (float)defined;
+            }
+        const float reg = reg_part ? tot / 3.0f : 0.0f;
+        terms[1] = ncc;
+        terms[2] = reg;
+        terms[0] = lambda == 0.0f ? ncc : ncc + reg * lambda;
+    }
+}
+
+// per-voxel adjoint of cc into the three statistics that depend on g:
+// G = {dL/dsg, dL/dsgg, dL/dsfg}, with dL/dcc = -seed / n
+__global__ void __launch_bounds__(kLB)
+ncc_adjoint_k(const float *__restrict__ S, LDims d, int r, float gcc, float *__restrict__ G) {
+    const int p = blockIdx.x * kLB + threadIdx.x;
+    if (p >= d.n) return;
+    int x, y, z;
+    lxyz(p, d, x, y, z);
+    const NccTerms t = ncc_terms(S, p, d.n, win_count(x, y, z, d, r));
+    const float inv_den = 1.0f / t.den;
+    const float a = t.cross;
+    // cc = a^2 / den, den = vf*vg + eps
+    const float g_cross = gcc * 2.0f * a * inv_den;
+    const float g_vg = -gcc * a * a * inv_den * inv_den * t.vf;
+    // cross = sfg - sf*sg/cnt;  vg = sgg - sg*sg/cnt
+    const float g_sg = -(g_cross * t.sf + 2.0f * g_vg * t.sg) / t.cnt;
+    G[p] = g_sg;
+    G[d.n + p] = g_vg;
+    G[2 * d.n + p] = g_cross;
+}
+
+// dL/dwarped = box(G_sg) + 2 g box(G_sgg) + f box(G_sfg)
+__global__ void __launch_bounds__(kLB)
+ncc_gwarped_k(const float *__restrict__ BG, const float *__restrict__ f,
+              const float *__restrict__ g, int n, float *__restrict__ gw) {
+    const int p = blockIdx.x * kLB + threadIdx.x;
+    if (p >= n) return;
+    gw[p] = BG[p] + 2.0f * g[p] * BG[n + p] + f[p] * BG[2 * n + p];
+}
+
+// op_grad_reg backward (ops.hpp:360-378): gphi += coeff*diff at p+stride,
+// -= at p; as a gather per voxel (no atomics)
+__global__ void __launch_bounds__(kLB)
+grad_reg_bwd_k(const float *__restrict__ phi, LDims d, float g, float *__restrict__ gphi) {
+    const int p = blockIdx.x * kLB + threadIdx.x;
+    if (p >= d.n) return;
+    int x, y, z;
+    lxyz(p, d, x, y, z);
+    const int dims[3] = {d.h, d.w, d.l};
+    const int pos[3] = {x, y, z};
+    const int strides[3] = {1, d.h, d.h * d.w};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float *u = phi + (int64_t)c * d.n;
+        float acc = 0.0f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int64_t defined = (int64_t)d.n - d.n / dims[a];
+            const float coeff = 2.0f * g / (3.0f * (float)defined);
+            if (pos[a] > 0) acc += coeff * (u[p] - u[p - strides[a]]);          // as p + stride
+            if (pos[a] < dims[a] - 1) acc -= coeff * (u[p + strides[a]] - u[p]);  // as p
+        }
+        gphi[(int64_t)c * d.n + p] += acc;
+    }
+}
+
+// three separable passes a -> b -> a -> b (both buffers owned scratch);
+// the box sum ends in b
+static mdg_status box3(float *a, int C, const LDims &d, int r, float *b, cudaStream_t st) {
+    const unsigned g = (unsigned)std::min<int64_t>(grid1d((int64_t)C * d.n, kLB), 148 * 16);
+    box_axis_k<<<g, kLB, 0, st>>>(a, C, d, 0, r, b);
+    MDG_LAUNCHED();
+    box_axis_k<<<g, kLB, 0, st>>>(b, C, d, 1, r, a);
+    MDG_LAUNCHED();
+    box_axis_k<<<g, kLB, 0, st>>>(a, C, d, 2, r, b);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+static mdg_status check_loss(mdg_dims3 dd, int window, float lambda) {
+    MDG_REQUIRE(dims_ok(dd) && nvox(dd) > 0, "ncc_loss: invalid dims " + dims_str(dd));
+    MDG_REQUIRE(window >= 3 && window % 2 == 1, "ncc_loss: window must be odd and >= 3");
+    MDG_REQUIRE(lambda >= 0.0f, "loss: lambda must be >= 0");
+    MDG_REQUIRE(lambda == 0.0f || (dd.h >= 2 && dd.w >= 2 && dd.l >= 2),
+                "grad_reg requires dims >= 2 per axis");
+    return MDG_OK;
+}
+
+}  // namespace mdg
+
+using namespace mdg;
+
+extern "C" {
+
+mdg_status mdg_total_loss_fwd(const float *fixed, const float *moving, const float *phi,
+                              mdg_dims3 dd, int window, float lambda, float *terms,
+                              float *warped, void *stream) {
+    if (mdg_status e = check_loss(dd, window, lambda)) return e;
+    MDG_REQUIRE(fixed && moving && phi && terms, "total_loss: null pointer");
+    cudaStream_t st = S_(stream);
+    const LDims d{dd.h, dd.w, dd.l, (int)nvox(dd)};
+    const int r = window / 2;
+    Scratch sc;
+    const int ncc_parts = (int)std::min<int64_t>(grid1d(d.n, kLB), 148 * 8);
+    const int reg_parts = ncc_parts;
+    MDG_CUDA_TRY(sc.alloc(((size_t)11 * d.n + ncc_parts + 9 * reg_parts + 64) * sizeof(float), st));
+    float *w = warped ? warped : sc.as<float>() + (size_t)10 * d.n;
+    float *prod = sc.as<float>(), *tmp = prod + (size_t)5 * d.n;
+    float *cc_part = prod + (size_t)11 * d.n, *reg_part = cc_part + ncc_parts;
+    // warped = warp(moving, phi) (objective.hpp:74)
+    if (mdg_status e = mdg_warp_fwd(moving, 1, dd, phi, w, st)) return e;
+    ncc_products_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(fixed, w, d.n, prod);
+    MDG_LAUNCHED();
+    if (mdg_status e = box3(prod, 5, d, r, tmp, st)) return e;  // statistics in tmp
+    ncc_cc_k<<<ncc_parts, kLB, 0, st>>>(tmp, d, r, cc_part);
+    MDG_LAUNCHED();
+    if (lambda != 0.0f) {
+        grad_reg_k<<<reg_parts, kLB, 0, st>>>(phi, d, reg_part);
+        MDG_LAUNCHED();
+    }
+    loss_final_k<<<1, kLB, 0, st>>>(cc_part, ncc_parts, lambda != 0.0f ? reg_part : nullptr,
+                                    reg_parts, d, lambda, terms);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+mdg_status mdg_total_loss_bwd(const float *fixed, const float *moving, const float *phi,
+                              mdg_dims3 dd, int window, float lambda, float seed,
+                              float *gphi, float *gmoving, void *stream) {
+    if (mdg_status e = check_loss(dd, window, lambda)) return e;
+    MDG_REQUIRE(fixed && moving && phi, "total_loss: null pointer");
+    if (!gphi && !gmoving) return MDG_OK;
+    cudaStream_t st = S_(stream);
+    const LDims d{dd.h, dd.w, dd.l, (int)nvox(dd)};
+    const int r = window / 2;
+    Scratch sc;
+    MDG_CUDA_TRY(sc.alloc((size_t)15 * d.n * sizeof(float), st));
+    float *P = sc.as<float>(), *S = P + (size_t)5 * d.n, *G = P + (size_t)10 * d.n;
+    float *w = P + (size_t)13 * d.n, *gw = P + (size_t)14 * d.n;
+    // recompute the forward statistics (cheaper than keeping 5 volumes alive)
+    if (mdg_status e = mdg_warp_fwd(moving, 1, dd, phi, w, st)) return e;
+    ncc_products_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(fixed, w, d.n, P);
+    MDG_LAUNCHED();
+    if (mdg_status e = box3(P, 5, d, r, S, st)) return e;
+    // dL/dcc = seed * (-1) * (1/n)  (op_scale / op_mean_all backward)
+    const float gcc = -seed * (1.0f / (float)d.n);
+    ncc_adjoint_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(S, d, r, gcc, G);
+    MDG_LAUNCHED();
+    if (mdg_status e = box3(G, 3, d, r, P, st)) return e;  // self-adjoint; result in P
+    ncc_gwarped_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(P, fixed, w, d.n, gw);
+    MDG_LAUNCHED();
+    if (mdg_status e = mdg_warp_bwd(moving, 1, dd, phi, gw, gmoving, gphi, st)) return e;
+    if (gphi && lambda != 0.0f) {
+        grad_reg_bwd_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(phi, d, seed * lambda, gphi);
+        MDG_LAUNCHED();
+    }
+    return MDG_OK;
+}
+
+}  // extern "C"

@@ -469,6 +469,41 @@ class LevelParams:
 
 
 @dataclass
+class LossConfig:
+    """objective.hpp:21-31 (lambda, NCC window)."""
+
+    lam: float = 1.0
+    ncc_window: int = 9
+
+
+def total_loss(fixed, moving, phi, cfg: LossConfig = LossConfig(), want_warped=False):
+    """op_total_loss forward (objective.hpp:71-78).  fixed / moving {1,l,w,h}
+    (or {l,w,h}), phi {3,l,w,h}.  Returns a device tensor {total, ncc, reg}
+    (and the warped moving image)."""
+    l, w, h = phi.shape[-3:]
+    if fixed.numel() != l * w * h or moving.shape != fixed.shape:
+        raise InvalidInput("ncc_loss: expects single-channel volumes of the field's dims")
+    terms = _empty(3, like=phi)
+    warped = torch.empty_like(moving) if want_warped else None
+    _check(_capi.lib().mdg_total_loss_fwd(_ptr(fixed), _ptr(moving), _ptr(phi),
+                                          dims3((h, w, l)), cfg.ncc_window, float(cfg.lam),
+                                          _ptr(terms), _ptr(warped), _stream()))
+    return (terms, warped) if want_warped else terms
+
+
+def total_loss_bwd(fixed, moving, phi, cfg: LossConfig = LossConfig(), seed=1.0, gphi=None,
+                   gmoving=None):
+    """Backward of seed * total: accumulates into (and returns) gphi, gmoving."""
+    l, w, h = phi.shape[-3:]
+    gphi = torch.zeros_like(phi) if gphi is None else gphi
+    gmoving = torch.zeros_like(moving) if gmoving is None else gmoving
+    _check(_capi.lib().mdg_total_loss_bwd(_ptr(fixed), _ptr(moving), _ptr(phi),
+                                          dims3((h, w, l)), cfg.ncc_window, float(cfg.lam),
+                                          float(seed), _ptr(gphi), _ptr(gmoving), _stream()))
+    return gphi, gmoving
+
+
+@dataclass
 class ModelConfig:
     """engine.hpp:30-78 (decoder part): heads coarse -> fine, head_dim,
     neighborhood, diffeomorphic + ss_steps."""
