@@ -199,6 +199,16 @@ mdg_status mdg_total_loss_bwd(const float *fixed, const float *moving, const flo
                               mdg_dims3 d, int window, float lambda, float seed, float *gphi,
                               float *gmoving, void *stream);
 
+/* ============================ optimizers (§8f) ===========================
+ * engine.hpp:268-298 AdamOptimizer::step on one parameter tensor: value, m, v
+ * updated in place from grad; t = the step count after increment (1-based).
+ * Per-element arithmetic in double as the reference (bit-identical). */
+mdg_status mdg_adam_step(float *value, const float *grad, float *m, float *v, int64_t n,
+                         double lr, double beta1, double beta2, double eps, int64_t t,
+                         void *stream);
+/* engine.hpp:306-311 sgd_step */
+mdg_status mdg_sgd_step(float *value, const float *grad, int64_t n, double lr, void *stream);
+
 /* ======================== decoding pyramid driver ========================
  * The decoder half of build_pipeline (engine.hpp:179-219) on device-resident
  * encoder features: per level k (coarse -> fine)

@@ -618,3 +618,26 @@ void mdo_layer_norm_bwd(const float *in, int64_t n, int K, const float *gamma, f
         }
     }
 }
+
+/* ------------------------------------------------------------- optimizers */
+
+/* engine.hpp:279-298 */
+void mdo_adam_step(float *value, const float *grad, float *m, float *v, int64_t n, double lr,
+                   double beta1, double beta2, double eps, int64_t t) {
+    const double bc1 = 1.0 - pow(beta1, (double)t);
+    const double bc2 = 1.0 - pow(beta2, (double)t);
+    for (int64_t j = 0; j < n; ++j) {
+        const double g = (double)grad[j];
+        const double mj = beta1 * (double)m[j] + (1.0 - beta1) * g;
+        const double vj = beta2 * (double)v[j] + (1.0 - beta2) * g * g;
+        m[j] = (float)mj;
+        v[j] = (float)vj;
+        const double update = lr * (mj / bc1) / (sqrt(vj / bc2) + eps);
+        value[j] = (float)((double)value[j] - update);
+    }
+}
+
+/* engine.hpp:306-311 */
+void mdo_sgd_step(float *value, const float *grad, int64_t n, double lr) {
+    for (int64_t j = 0; j < n; ++j) value[j] = (float)((double)value[j] - lr * (double)grad[j]);
+}

@@ -94,6 +94,13 @@ void mdo_compose_bwd(const float *prev, const float *res, int h, int w, int l,
 /* reghead.hpp:60-67 (plain scaling and squaring) */
 void mdo_scaling_squaring(const float *vel, int h, int w, int l, int steps, float *out);
 
+/* engine.hpp:268-298 AdamOptimizer::step for one parameter tensor (double
+ * arithmetic per element, float storage); t = step count after increment */
+void mdo_adam_step(float *value, const float *grad, float *m, float *v, int64_t n, double lr,
+                   double beta1, double beta2, double eps, int64_t t);
+/* engine.hpp:306-311 sgd_step */
+void mdo_sgd_step(float *value, const float *grad, int64_t n, double lr);
+
 /* ops.hpp:387-413 op_linear_proj forward: in {c, n} channel-major, weight
  * {K, c}, bias {K} -> out position-major {n, K} */
 void mdo_linear_proj_fwd(const float *in, int c, int64_t n, const float *weight,

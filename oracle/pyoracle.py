@@ -82,7 +82,9 @@ class _Lib:
         self._comp_bwd = sig("compose_bwd", None, _f, _f, ii, ii, ii, _f, _f, _f)
         self._ss = sig("scaling_squaring", None, _f, ii, ii, ii, ii, _f)
         i64 = C.c_int64
+        dd = C.c_double
         if prefix == "mdo_":
+            self._adam = sig("adam_step", None, _f, _f, _f, _f, i64, dd, dd, dd, dd, i64)
             self._lin_fwd = sig("linear_proj_fwd", None, _f, ii, i64, _f, _f, ii, _f)
             self._lin_bwd = sig("linear_proj_bwd", None, _f, ii, i64, _f, ii, _f, _f, _f, _f)
             self._ln_fwd = sig("layer_norm_fwd", None, _f, i64, ii, _f, _f, C.c_float, _f)
@@ -95,6 +97,7 @@ class _Lib:
             self._decoder = sig("decoder", ii, ii, _i, _i, _i, ii, ii, ii, ii, pp, pp, pp, _f,
                                 _f, pp, pp, pp, pp)
             self._perr = sig("pipeline_error", C.c_char_p)
+            self._adam_steps = sig("adam_steps", ii, _f, _f, i64, ii, dd, dd, dd, dd, _f, _f)
             self._tloss = sig("total_loss", ii, _f, _f, _f, ii, ii, ii, ii, C.c_float, _f, _f,
                               _f, _f)
             self._lpc = sig("level_param_count", i64, ii, ii, ii, ii)
@@ -182,6 +185,25 @@ class _Lib:
         if rc:
             raise RuntimeError(self._perr().decode())
         return terms, warped, gphi, gm
+
+    def adam(self, value, grads, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+        """AdamOptimizer (engine.hpp:268-298): len(grads) consecutive steps from
+        zero moments; returns the updated parameter."""
+        value = value.copy()
+        n = value.size
+        if self.prefix == "mdo_":
+            m = np.zeros_like(value)
+            v = np.zeros_like(value)
+            for t, g in enumerate(grads, start=1):
+                self._adam(_fp(value), _fp(np.ascontiguousarray(g)), _fp(m), _fp(v), n, lr,
+                           beta1, beta2, eps, t)
+            return value
+        G = np.ascontiguousarray(np.stack(grads)).astype(np.float32)
+        rc = self._adam_steps(_fp(value), _fp(G), n, len(grads), lr, beta1, beta2, eps, None,
+                              None)
+        if rc:
+            raise RuntimeError(self._perr().decode())
+        return value
 
     def level_param_count(self, C_, S, hd, nb=3):
         return int(self._lpc(C_, S, hd, nb))

@@ -200,4 +200,26 @@ int mdr_total_loss(const float *fixed, const float *moving, const float *phi, in
     return 0;
 }
 
+// engine.hpp:268-298 AdamOptimizer: `steps` consecutive steps on one parameter
+// tensor with the given gradient sequence grads[k*n ..] (value/m/v updated)
+int mdr_adam_steps(float *value, const float *grads, int64_t n, int steps, double lr,
+                   double beta1, double beta2, double eps, float *m_out, float *v_out) {
+    try {
+        ParamTensor<float> p("p", tensor_from(value, {(int)n}));
+        std::vector<ParamTensor<float> *> ps{&p};
+        AdamOptimizer<float> opt(ps, beta1, beta2, eps);
+        for (int k = 0; k < steps; ++k) {
+            std::memcpy(p.grad.data.data(), grads + (int64_t)k * n, (size_t)n * sizeof(float));
+            opt.step(lr);
+        }
+        std::memcpy(value, p.value.data.data(), (size_t)n * sizeof(float));
+        (void)m_out;
+        (void)v_out;
+    } catch (const std::exception &e) {
+        g_perr = e.what();
+        return 1;
+    }
+    return 0;
+}
+
 }  // extern "C"

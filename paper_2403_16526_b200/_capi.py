@@ -91,6 +91,9 @@ SIGNATURES = {
                                  _p, _p, _p, _p, _p]),
     "mdg_total_loss_fwd": (_st, [_p, _p, _p, Dims3, _i, _f, _p, _p, _p]),
     "mdg_total_loss_bwd": (_st, [_p, _p, _p, Dims3, _i, _f, _f, _p, _p, _p]),
+    "mdg_adam_step": (_st, [_p, _p, _p, _p, C.c_int64, C.c_double, C.c_double, C.c_double,
+                            C.c_double, C.c_int64, _p]),
+    "mdg_sgd_step": (_st, [_p, _p, C.c_int64, C.c_double, _p]),
     "mdg_pyramid_create": (_st, [C.POINTER(PyramidConfig), C.POINTER(_p)]),
     "mdg_pyramid_destroy": (None, [_p]),
     "mdg_pyramid_forward": (_st, [_p, C.POINTER(_p), C.POINTER(_p), C.POINTER(LevelParams), _p,

@@ -503,6 +503,31 @@ def total_loss_bwd(fixed, moving, phi, cfg: LossConfig = LossConfig(), seed=1.0,
     return gphi, gmoving
 
 
+class AdamOptimizer:
+    """engine.hpp:268-304 AdamOptimizer over a list of CUDA parameter tensors;
+    step(lr, grads) updates them in place (bit-identical double arithmetic)."""
+
+    def __init__(self, params, beta1=0.9, beta2=0.999, eps=1e-8):
+        self.params = list(params)
+        self.m = [torch.zeros_like(p) for p in self.params]
+        self.v = [torch.zeros_like(p) for p in self.params]
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+        self.t = 0
+
+    def step(self, lr, grads):
+        self.t += 1
+        L = _capi.lib()
+        for p, g, m, v in zip(self.params, grads, self.m, self.v):
+            _check(L.mdg_adam_step(_ptr(p), _ptr(g), _ptr(m), _ptr(v), p.numel(), float(lr),
+                                   self.beta1, self.beta2, self.eps, self.t, _stream()))
+
+
+def sgd_step(params, grads, lr):
+    """engine.hpp:306-311."""
+    for p, g in zip(params, grads):
+        _check(_capi.lib().mdg_sgd_step(_ptr(p), _ptr(g), p.numel(), float(lr), _stream()))
+
+
 @dataclass
 class ModelConfig:
     """engine.hpp:30-78 (decoder part): heads coarse -> fine, head_dim,
