@@ -337,9 +337,40 @@ def run_pyramid(dev, reps=5):
         torch.cuda.synchronize()
         tf.append(e[0].elapsed_time(e[1]))
         tb.append(e[1].elapsed_time(e[2]))
+    # one decoder PO iteration (engine.hpp:377-411 minus the encoder): pyramid
+    # forward -> loss (NCC + grad_reg on the full-resolution images) -> loss
+    # backward -> pyramid backward -> Adam over every decoder parameter
+    fixed = torch.rand(1, DIMS[2], DIMS[1], DIMS[0], device=dev, generator=g)
+    moving = torch.rand(1, DIMS[2], DIMS[1], DIMS[0], device=dev, generator=g)
+    params = [t for lp in lps for t in lp.tensors()]
+    opt = ops.AdamOptimizer(params)
+    lcfg = ops.LossConfig(lam=1.0, ncc_window=9)
+
+    def po_iter():
+        for gr in grads:
+            for t in gr.tensors():
+                t.zero_()
+        phi = pyr.forward(ff, mf, lps)
+        ops.total_loss(fixed, moving, phi, lcfg)
+        gphi_ = ops.total_loss_bwd(fixed, moving, phi, lcfg)[0]
+        pyr.backward(gphi_, grads, gf, gm)
+        opt.step(1e-4, [t for gr in grads for t in gr.tensors()])
+
+    po_iter()
+    torch.cuda.synchronize()
+    tp = []
+    for _ in range(reps):
+        e[0].record()
+        po_iter()
+        e[1].record()
+        torch.cuda.synchronize()
+        tp.append(e[0].elapsed_time(e[1]))
     return {"workload": "decoder pyramid (build_pipeline minus encoder), small preset, "
                         "160x192x224 fine level, synthetic features",
             "fwd_ms": round(statistics.median(tf), 3), "bwd_ms": round(statistics.median(tb), 3),
+            "po_iter_ms": round(statistics.median(tp), 3),
+            "po_iter_note": "pyramid fwd + NCC/grad_reg loss fwd+bwd + pyramid bwd + Adam; "
+                            "the encoder (SURVEY 8f rank 2) is not built",
             "arena_mib": round(pyr.device_bytes / 2 ** 20, 1)}
 
 
