@@ -34,24 +34,75 @@ __device__ __forceinline__ void lxyz(int p, const LDims &d, int &x, int &y, int 
     y = t - z * d.w;
 }
 
-// kern::boxsum1d along `axis` for C channel planes: taps t0..t1 in order
+// kern::boxsum1d along `axis` for C channel planes (blockIdx.y = channel).
+// Each thread produces kStrip consecutive outputs along the summed axis from
+// one register window of taps (each output still adds its own taps t0..t1 in
+// order, so the sums are bit-identical to the reference); lanes run along x,
+// so every tap load is coalesced.  For the x axis the strip runs along y
+// instead (x stays the lane axis).
+constexpr int kStrip = 4;
+constexpr int kMaxR = 12;
+
+template <int AX, int R>
 __global__ void __launch_bounds__(kLB)
-box_axis_k(const float *__restrict__ in, int C, LDims d, int axis, int r,
-           float *__restrict__ out) {
-    const int64_t total = (int64_t)C * d.n;
-    for (int64_t i = (int64_t)blockIdx.x * kLB + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * kLB) {
-        const int c = (int)(i / d.n), p = (int)(i - (int64_t)c * d.n);
-        int x, y, z;
-        lxyz(p, d, x, y, z);
-        const int pos = axis == 0 ? x : (axis == 1 ? y : z);
-        const int len = axis == 0 ? d.h : (axis == 1 ? d.w : d.l);
-        const int stride = axis == 0 ? 1 : (axis == 1 ? d.h : d.h * d.w);
-        const int t0 = max(0, pos - r), t1 = min(len - 1, pos + r);
-        const float *src = in + (int64_t)c * d.n + (p - pos * stride);
-        float s = 0.0f;
-        for (int t = t0; t <= t1; ++t) s = add_(s, src[t * stride]);
-        out[i] = s;
+box_axis_k(const float *__restrict__ in, LDims d, float *__restrict__ out) {
+    constexpr int r = R;
+    const int c = blockIdx.y;
+    const int len = AX == 0 ? d.h : (AX == 1 ? d.w : d.l);
+    const int stride = AX == 0 ? 1 : (AX == 1 ? d.h : d.h * d.w);
+    // work item = (x, strip along the pass axis or along y for AX == 0, rest)
+    const int hs = AX == 0 ? d.h : d.h;
+    const int ns = AX == 0 ? (d.w + kStrip - 1) / kStrip : (len + kStrip - 1) / kStrip;
+    const int other = AX == 0 ? d.l : (AX == 1 ? d.l : d.w);
+    const int items = hs * ns * other;
+    const float *src = in + (int64_t)c * d.n;
+    float *dst = out + (int64_t)c * d.n;
+    for (int it = blockIdx.x * kLB + threadIdx.x; it < items; it += gridDim.x * kLB) {
+        const int x = it % hs;
+        const int rest = it / hs;
+        const int si = rest % ns, o = rest / ns;
+        if (AX == 0) {
+            // one output per (x, y) of the strip, taps in order from L1
+            const int z = o;
+#pragma unroll
+            for (int k = 0; k < kStrip; ++k) {
+                const int y = si * kStrip + k;
+                if (y < d.w) {
+                    const float *row = src + ((int64_t)z * d.w + y) * d.h;
+                    float s = 0.0f;
+#pragma unroll
+                    for (int q = 0; q < 2 * R + 1; ++q) {
+                        const int t = x - r + q;
+                        if (t >= 0 && t < d.h) s = add_(s, __ldg(row + t));
+                    }
+                    dst[((int64_t)z * d.w + y) * d.h + x] = s;
+                }
+            }
+        } else {
+            const int i0 = si * kStrip;
+            // base of the line through (x, ., o) / (x, o, .)
+            const int64_t base = AX == 1 ? (int64_t)o * d.h * d.w + x : (int64_t)o * d.h + x;
+            // taps i0-r .. i0+kStrip-1+r (clamped) in registers
+            float v[kStrip + 2 * R];
+#pragma unroll
+            for (int q = 0; q < kStrip + 2 * R; ++q) {
+                const int t = i0 - r + q;
+                v[q] = (t >= 0 && t < len) ? src[base + (int64_t)t * stride] : 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < kStrip; ++k) {
+                const int i = i0 + k;
+                if (i >= len) break;
+                const int t0 = max(0, i - r), t1 = min(len - 1, i + r);
+                float s = 0.0f;
+#pragma unroll
+                for (int q = 0; q < 2 * R + 1; ++q) {
+                    const int t = i - r + q;
+                    if (t >= t0 && t <= t1) s = add_(s, v[k + q]);
+                }
+                dst[base + (int64_t)i * stride] = s;
+            }
+        }
     }
 }
 
@@ -251,20 +302,33 @@ grad_reg_bwd_k(const float *__restrict__ phi, LDims d, float g, float *__restric
 
 // three separable passes a -> b -> a -> b (both buffers owned scratch);
 // the box sum ends in b
+template <int R>
+static void box3_r(float *a, int C, const LDims &d, float *b, cudaStream_t st) {
+    const dim3 g((unsigned)std::min<int64_t>(grid1d(d.n / kStrip + d.h * d.w, kLB), 148 * 8),
+                 (unsigned)C);
+    box_axis_k<0, R><<<g, kLB, 0, st>>>(a, d, b);
+    box_axis_k<1, R><<<g, kLB, 0, st>>>(b, d, a);
+    box_axis_k<2, R><<<g, kLB, 0, st>>>(a, d, b);
+}
+
 static mdg_status box3(float *a, int C, const LDims &d, int r, float *b, cudaStream_t st) {
-    const unsigned g = (unsigned)std::min<int64_t>(grid1d((int64_t)C * d.n, kLB), 148 * 16);
-    box_axis_k<<<g, kLB, 0, st>>>(a, C, d, 0, r, b);
-    MDG_LAUNCHED();
-    box_axis_k<<<g, kLB, 0, st>>>(b, C, d, 1, r, a);
-    MDG_LAUNCHED();
-    box_axis_k<<<g, kLB, 0, st>>>(a, C, d, 2, r, b);
-    MDG_LAUNCHED();
+    switch (r) {
+#define MDG_BOX(RV) \
+    case RV: box3_r<RV>(a, C, d, b, st); break;
+        MDG_BOX(1) MDG_BOX(2) MDG_BOX(3) MDG_BOX(4) MDG_BOX(5) MDG_BOX(6) MDG_BOX(7)
+        MDG_BOX(8) MDG_BOX(9) MDG_BOX(10) MDG_BOX(11) MDG_BOX(12)
+#undef MDG_BOX
+        default: MDG_REQUIRE(false, "ncc_loss: window > 25 is not supported");
+    }
+    g_launches.fetch_add(3);
+    MDG_CUDA_TRY(cudaPeekAtLastError());
     return MDG_OK;
 }
 
 static mdg_status check_loss(mdg_dims3 dd, int window, float lambda) {
     MDG_REQUIRE(dims_ok(dd) && nvox(dd) > 0, "ncc_loss: invalid dims " + dims_str(dd));
     MDG_REQUIRE(window >= 3 && window % 2 == 1, "ncc_loss: window must be odd and >= 3");
+    MDG_REQUIRE(window / 2 <= kMaxR, "ncc_loss: window > 25 is not supported");
     MDG_REQUIRE(lambda >= 0.0f, "loss: lambda must be >= 0");
     MDG_REQUIRE(lambda == 0.0f || (dd.h >= 2 && dd.w >= 2 && dd.l >= 2),
                 "grad_reg requires dims >= 2 per axis");
