@@ -13,9 +13,12 @@ for _ in range(3):
     ops.total_loss(fixed, moving, phi, cfg); ops.total_loss_bwd(fixed, moving, phi, cfg)
 torch.cuda.synchronize()
 e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-e[0].record(); ops.total_loss(fixed, moving, phi, cfg); e[1].record()
-ops.total_loss_bwd(fixed, moving, phi, cfg); e[2].record(); torch.cuda.synchronize()
-print(f"loss fwd {e[0].elapsed_time(e[1]):.3f} ms  bwd {e[1].elapsed_time(e[2]):.3f} ms")
+gphi = torch.zeros_like(phi); gm = torch.zeros_like(moving)
+for _ in range(5):
+    e[0].record(); ops.total_loss(fixed, moving, phi, cfg); e[1].record()
+    ops.total_loss_bwd(fixed, moving, phi, cfg, gphi=gphi, gmoving=gm); e[2].record()
+    torch.cuda.synchronize()
+    print(f"loss fwd {e[0].elapsed_time(e[1]):.3f} ms  bwd {e[1].elapsed_time(e[2]):.3f} ms")
 if os.environ.get("PROFILE"):
     from torch.profiler import profile, ProfilerActivity
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
