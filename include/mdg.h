@@ -209,6 +209,17 @@ mdg_status mdg_adam_step(float *value, const float *grad, float *m, float *v, in
 /* engine.hpp:306-311 sgd_step */
 mdg_status mdg_sgd_step(float *value, const float *grad, int64_t n, double lr, void *stream);
 
+/* ========================= label evaluation (§8f) ========================
+ * metrics.cpp:145-164 warp_labels: nearest-neighbour pull of int32 labels by
+ * phi {3, n} (floor(x + phi + 0.5f), clamped) — bit-identical */
+mdg_status mdg_warp_labels(const int *labels, mdg_dims3 d, const float *phi, int *out,
+                           void *stream);
+/* metrics.cpp:100-129 mean_dice over the labels present in a or b (label 0
+ * excluded); labels must lie in [0, max_label].  Synchronous (the result is a
+ * host double); bit-identical to the reference. */
+mdg_status mdg_mean_dice(const int *a, const int *b, int64_t n, int max_label, double *dice,
+                         void *stream);
+
 /* ======================== decoding pyramid driver ========================
  * The decoder half of build_pipeline (engine.hpp:179-219) on device-resident
  * encoder features: per level k (coarse -> fine)

@@ -67,6 +67,10 @@ class _Lib:
                                    C.c_float, C.c_float, _f)
             self._attn_bench = sig("attention_bench_fused_ms", C.c_double, ii, ii, ii, ii, ii,
                                    ii, C.c_uint64)
+            self._synth = sig("make_synth_pair", None, ii, ii, ii, C.c_uint64, C.c_float, _f, _f,
+                              _i, _i, _f)
+            self._warp_labels = sig("warp_labels", None, _i, ii, ii, ii, _f, _i)
+            self._mean_dice = sig("mean_dice", C.c_double, _i, _i, ii, ii, ii)
         self._na_bwd = sig("na_bwd", None, _f, _f, _f, ii, ii, ii, ii, ii, ii, _f, _f, _f, _f)
         self._sf_fwd = sig("subfields_fwd", None, _f, ii, ii, ii, ii, ii, _f)
         self._sf_bwd = sig("subfields_bwd", None, ii, ii, ii, ii, ii, _f, _f)
@@ -204,6 +208,30 @@ class _Lib:
         if rc:
             raise RuntimeError(self._perr().decode())
         return value
+
+    def synth_pair(self, dims, seed=1, max_disp=2.0):
+        """synth.cpp make_synth_pair: (fixed, moving, labels_fixed, labels_moving, gt)."""
+        h, w, l = dims
+        f = np.zeros((1, l, w, h), np.float32)
+        m = np.zeros_like(f)
+        lf = np.zeros((l, w, h), np.int32)
+        lm = np.zeros_like(lf)
+        gt = np.zeros((3, l, w, h), np.float32)
+        ip = lambda a: a.ctypes.data_as(_i)  # noqa: E731
+        self._synth(h, w, l, seed, max_disp, _fp(f), _fp(m), ip(lf), ip(lm), _fp(gt))
+        return f, m, lf, lm, gt
+
+    def warp_labels(self, labels, phi):
+        l, w, h = phi.shape[1:]
+        out = np.zeros_like(labels)
+        ip = lambda a: np.ascontiguousarray(a).ctypes.data_as(_i)  # noqa: E731
+        self._warp_labels(ip(labels), h, w, l, _fp(phi), out.ctypes.data_as(_i))
+        return out
+
+    def mean_dice(self, a, b):
+        l, w, h = a.shape[-3:]
+        ip = lambda x: np.ascontiguousarray(x, np.int32).ctypes.data_as(_i)  # noqa: E731
+        return float(self._mean_dice(ip(a), ip(b), h, w, l))
 
     def level_param_count(self, C_, S, hd, nb=3):
         return int(self._lpc(C_, S, hd, nb))

@@ -13,6 +13,7 @@
 
 #include "mdreg/attention.hpp"
 #include "mdreg/bench.hpp"
+#include "mdreg/metrics.hpp"
 #include "mdreg/field_ops.hpp"
 #include "mdreg/reghead.hpp"
 #include "mdreg/sampling.hpp"
@@ -169,6 +170,40 @@ double mdr_attention_bench_fused_ms(int h, int w, int l, int S, int hd, int reps
                                     std::uint64_t seed) {
     BenchReport r = run_attention_bench(D(h, w, l), S, hd, reps, seed);
     return r.fused.time_ms;
+}
+
+// synth.cpp make_synth_pair: images, label volumes and the ground-truth field
+void mdr_make_synth_pair(int h, int w, int l, std::uint64_t seed, float max_disp, float *fixed,
+                         float *moving, int *labels_fixed, int *labels_moving, float *gt) {
+    SynthConfig cfg;
+    cfg.dims = D(h, w, l);
+    cfg.seed = seed;
+    cfg.max_disp = max_disp;
+    SynthPair sp = make_synth_pair(cfg);
+    const size_t n = sp.fixed.data.size();
+    std::memcpy(fixed, sp.fixed.data.data(), n * sizeof(float));
+    std::memcpy(moving, sp.moving.data.data(), n * sizeof(float));
+    std::memcpy(labels_fixed, sp.labels_fixed.data.data(), n * sizeof(int));
+    std::memcpy(labels_moving, sp.labels_moving.data.data(), n * sizeof(int));
+    std::memcpy(gt, sp.gt_field.data.data(), 3 * n * sizeof(float));
+}
+
+// metrics.cpp:145-164 warp_labels (nearest neighbour)
+void mdr_warp_labels(const int *labels, int h, int w, int l, const float *phi, int *out) {
+    LabelVolume lv(D(h, w, l));
+    std::memcpy(lv.data.data(), labels, lv.data.size() * sizeof(int));
+    DisplacementField f(D(h, w, l));
+    std::memcpy(f.data.data(), phi, f.data.size() * sizeof(float));
+    LabelVolume o = warp_labels(lv, f);
+    std::memcpy(out, o.data.data(), o.data.size() * sizeof(int));
+}
+
+// metrics.cpp:123-129 mean_dice
+double mdr_mean_dice(const int *a, const int *b, int h, int w, int l) {
+    LabelVolume la(D(h, w, l)), lb(D(h, w, l));
+    std::memcpy(la.data.data(), a, la.data.size() * sizeof(int));
+    std::memcpy(lb.data.data(), b, lb.data.size() * sizeof(int));
+    return mean_dice(la, lb);
 }
 
 }  // extern "C"

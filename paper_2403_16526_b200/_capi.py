@@ -94,6 +94,8 @@ SIGNATURES = {
     "mdg_adam_step": (_st, [_p, _p, _p, _p, C.c_int64, C.c_double, C.c_double, C.c_double,
                             C.c_double, C.c_int64, _p]),
     "mdg_sgd_step": (_st, [_p, _p, C.c_int64, C.c_double, _p]),
+    "mdg_warp_labels": (_st, [_p, Dims3, _p, _p, _p]),
+    "mdg_mean_dice": (_st, [_p, _p, C.c_int64, _i, C.POINTER(C.c_double), _p]),
     "mdg_pyramid_create": (_st, [C.POINTER(PyramidConfig), C.POINTER(_p)]),
     "mdg_pyramid_destroy": (None, [_p]),
     "mdg_pyramid_forward": (_st, [_p, C.POINTER(_p), C.POINTER(_p), C.POINTER(LevelParams), _p,

@@ -503,6 +503,38 @@ def total_loss_bwd(fixed, moving, phi, cfg: LossConfig = LossConfig(), seed=1.0,
     return gphi, gmoving
 
 
+def _iptr(t, name="labels"):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.int32 \
+            or not t.is_contiguous():
+        raise InvalidInput(f"{name}: must be a contiguous CUDA int32 tensor")
+    return t.data_ptr()
+
+
+def warp_labels(labels, phi):
+    """metrics.cpp:145-164: nearest-neighbour warp of an int32 label volume
+    {l,w,h} (or {1,l,w,h}) by phi {3,l,w,h} (bit-identical)."""
+    l, w, h = phi.shape[-3:]
+    if labels.numel() != l * w * h:
+        raise InvalidInput("warp_labels: dims mismatch")
+    out = torch.empty_like(labels)
+    _check(_capi.lib().mdg_warp_labels(_iptr(labels), dims3((h, w, l)), _ptr(phi),
+                                       _iptr(out, "out"), _stream()))
+    return out
+
+
+def mean_dice(a, b, max_label=None):
+    """metrics.cpp:100-129 mean Dice over the labels present (0 excluded);
+    returns a Python float (bit-identical to the reference's double)."""
+    if a.shape != b.shape:
+        raise InvalidInput("dice: dims mismatch")
+    if max_label is None:
+        max_label = int(torch.maximum(a.max(), b.max()).item()) if a.numel() else 0
+    out = C.c_double()
+    _check(_capi.lib().mdg_mean_dice(_iptr(a, "a"), _iptr(b, "b"), a.numel(), int(max_label),
+                                     C.byref(out), _stream()))
+    return out.value
+
+
 class AdamOptimizer:
     """engine.hpp:268-304 AdamOptimizer over a list of CUDA parameter tensors;
     step(lr, grads) updates them in place (bit-identical double arithmetic)."""
