@@ -220,6 +220,33 @@ mdg_status mdg_warp_labels(const int *labels, mdg_dims3 d, const float *phi, int
 mdg_status mdg_mean_dice(const int *a, const int *b, int64_t n, int max_label, double *dice,
                          void *stream);
 
+/* ============================ encoder (§8f) ===============================
+ * op_encode (encoder.hpp:102-116): five shared-weight conv blocks
+ * (conv3 -> InstanceNorm -> LeakyReLU, twice; encoder.hpp:87-91) with 2x
+ * average pooling between levels (sampling.hpp:171-219).  Channels at level L
+ * are base << (L-1).  The object owns the saved activations of one image. */
+typedef struct {
+    const float *w1, *b1, *g1, *be1; /* conv1 {C,Cin,3,3,3}, {C}; norm1 gamma/beta {C} */
+    const float *w2, *b2, *g2, *be2; /* conv2 {C,C,3,3,3}, ... */
+} mdg_block_params;
+typedef struct {
+    float *w1, *b1, *g1, *be1, *w2, *b2, *g2, *be2; /* accumulated; nullable */
+} mdg_block_grads;
+typedef struct mdg_encoder mdg_encoder;
+/* dims of the full-resolution image (>= 16 per axis, encoder.hpp:95-99) */
+mdg_status mdg_encoder_create(mdg_dims3 d, int base_channels, int levels, float slope,
+                              mdg_encoder **out);
+void mdg_encoder_destroy(mdg_encoder *e);
+/* image {1, n}; params[levels]; features[L] {C_L, n_L}, fine -> coarse
+ * (op_encode's order) */
+mdg_status mdg_encoder_forward(mdg_encoder *e, const float *image,
+                               const mdg_block_params *params, float *const *features,
+                               void *stream);
+/* backward of the last forward: gfeatures[L] (entries nullable) -> param
+ * grads (accumulated) and gimage (accumulated, nullable) */
+mdg_status mdg_encoder_backward(mdg_encoder *e, const float *const *gfeatures,
+                                const mdg_block_grads *grads, float *gimage, void *stream);
+
 /* ======================== decoding pyramid driver ========================
  * The decoder half of build_pipeline (engine.hpp:179-219) on device-resident
  * encoder features: per level k (coarse -> fine)

@@ -102,6 +102,12 @@ class _Lib:
                                 _f, pp, pp, pp, pp)
             self._perr = sig("pipeline_error", C.c_char_p)
             self._adam_steps = sig("adam_steps", ii, _f, _f, i64, ii, dd, dd, dd, dd, _f, _f)
+            self._mcount = sig("model_param_count", i64, C.c_uint64)
+            self._mparams = sig("model_params", ii, C.c_uint64, _f, C.POINTER(i64))
+            pp = C.POINTER(_f)
+            self._encode = sig("encode", ii, _f, ii, ii, ii, _f, pp, pp, _f, _f)
+            self._loss_step = sig("loss_step", ii, _f, _f, ii, ii, ii, _f, C.c_float, ii,
+                                  C.POINTER(dd), _f, _f)
             self._tloss = sig("total_loss", ii, _f, _f, _f, ii, ii, ii, ii, C.c_float, _f, _f,
                               _f, _f)
             self._lpc = sig("level_param_count", i64, ii, ii, ii, ii)
@@ -232,6 +238,44 @@ class _Lib:
         l, w, h = a.shape[-3:]
         ip = lambda x: np.ascontiguousarray(x, np.int32).ctypes.data_as(_i)  # noqa: E731
         return float(self._mean_dice(ip(a), ip(b), h, w, l))
+
+    def model_params(self, seed=42):
+        """init_model(small_preset, seed): (packed values, per-tensor sizes)."""
+        n = int(self._mcount(seed))
+        out = np.zeros(n, np.float32)
+        sizes = (C.c_int64 * 128)()
+        cnt = self._mparams(seed, _fp(out), sizes)
+        return out, [int(sizes[i]) for i in range(cnt)]
+
+    def encode(self, image, packed, gfeat=None):
+        """op_encode of one image {1,l,w,h}: features (fine -> coarse) and, with
+        gfeat, (gpacked, gimage) of sum_L <feat_L, gfeat_L>."""
+        l, w, h = image.shape[1:]
+        dims = [(h, w, l)]
+        for _ in range(4):
+            dims.append(tuple((v + 1) // 2 for v in dims[-1]))
+        feats = [np.zeros((8 << k, d[2], d[1], d[0]), np.float32) for k, d in enumerate(dims)]
+        P = C.POINTER(C.c_float)
+        fa = (P * 5)(*[_fp(f) for f in feats])
+        ga = (P * 5)(*[_fp(g) for g in gfeat]) if gfeat is not None else None
+        gp = np.zeros_like(packed) if gfeat is not None else None
+        gi = np.zeros_like(image) if gfeat is not None else None
+        rc = self._encode(_fp(image), h, w, l, _fp(packed), fa, ga, _fp(gp), _fp(gi))
+        if rc:
+            raise RuntimeError(self._perr().decode())
+        return (feats, gp, gi) if gfeat is not None else feats
+
+    def loss_step(self, fixed, moving, packed, lam=1.0, window=9, grads=True):
+        """run_loss_step (engine.hpp:316-340): (loss, gpacked, phi)."""
+        l, w, h = fixed.shape[1:]
+        loss = C.c_double()
+        gp = np.zeros_like(packed) if grads else None
+        phi = np.zeros((3, l, w, h), np.float32)
+        rc = self._loss_step(_fp(fixed), _fp(moving), h, w, l, _fp(packed), lam, window,
+                             C.byref(loss), _fp(gp), _fp(phi))
+        if rc:
+            raise RuntimeError(self._perr().decode())
+        return loss.value, gp, phi
 
     def level_param_count(self, C_, S, hd, nb=3):
         return int(self._lpc(C_, S, hd, nb))

@@ -31,6 +31,8 @@ void add_into(float *dst, const Tensor<float> &g) {
     for (std::size_t i = 0; i < g.data.size(); ++i) dst[i] += g.data[i];
 }
 
+Dims3 D3(int h, int w, int l) { return Dims3{h, w, l}; }
+
 int64_t level_param_count(int C, int S, int hd, int nb) {
     const int64_t K = (int64_t)S * hd, win = (int64_t)nb * nb * nb;
     return K * C + 3 * K + S * win + 3 * 3 * S * 27 + 3;
@@ -215,6 +217,111 @@ int mdr_adam_steps(float *value, const float *grads, int64_t n, int steps, doubl
         std::memcpy(value, p.value.data.data(), (size_t)n * sizeof(float));
         (void)m_out;
         (void)v_out;
+    } catch (const std::exception &e) {
+        g_perr = e.what();
+        return 1;
+    }
+    return 0;
+}
+
+// ---- full model (encoder + decoder) ------------------------------------------
+// ModelParams::all_tensors order (engine.hpp:121-133): 5 encoder blocks x
+// {w1,b1,n1g,n1b,w2,b2,n2g,n2b}, then 5 levels x {proj.w,proj.b,ln_g,ln_b,
+// bias_b,reghead.w,reghead.b}; packed back to back.
+static int64_t model_count(ModelParams<float> &mp) {
+    int64_t t = 0;
+    for (auto *p : mp.all_tensors()) t += p->value.size();
+    return t;
+}
+
+int64_t mdr_model_param_count(std::uint64_t seed) {
+    ModelParams<float> mp = init_model<float>(ModelConfig::small_preset(), seed);
+    return model_count(mp);
+}
+
+// init_model(small_preset, seed) values, packed; per-tensor sizes in sizes[75]
+int mdr_model_params(std::uint64_t seed, float *out, int64_t *sizes) {
+    ModelParams<float> mp = init_model<float>(ModelConfig::small_preset(), seed);
+    int i = 0;
+    for (auto *p : mp.all_tensors()) {
+        std::memcpy(out, p->value.data.data(), p->value.data.size() * sizeof(float));
+        out += p->value.data.size();
+        if (sizes) sizes[i] = p->value.size();
+        ++i;
+    }
+    return i;
+}
+
+static void load_params(ModelParams<float> &mp, const float *packed) {
+    for (auto *p : mp.all_tensors()) {
+        std::memcpy(p->value.data.data(), packed, p->value.data.size() * sizeof(float));
+        packed += p->value.data.size();
+    }
+}
+
+// op_encode (encoder.hpp:102-116) of one image with the packed model's
+// encoder blocks; features[5] written (fine -> coarse); with gfeat the tape
+// backward of sum_L <features_L, gfeat_L> accumulates the packed parameter
+// gradient (whole-model layout, only encoder entries touched) and gimage
+int mdr_encode(const float *image, int h, int w, int l, const float *packed,
+               float *const *features, const float *const *gfeat, float *gpacked, float *gimage) {
+    try {
+        ModelParams<float> mp = init_model<float>(ModelConfig::small_preset(), 1);
+        load_params(mp, packed);
+        Tape<float> t;
+        Var img = t.input(tensor_from(image, {1, h, w, l}));
+        std::vector<ConvBlockVars> blocks;
+        for (auto &b : mp.encoder_blocks) blocks.push_back(leaf_conv_block(t, b));
+        std::vector<Var> feats = op_encode(t, img, blocks, mp.cfg.encoder);
+        for (size_t k = 0; k < feats.size(); ++k) {
+            const Tensor<float> &v = t.value(feats[k]);
+            std::memcpy(features[k], v.data.data(), v.data.size() * sizeof(float));
+        }
+        if (!gfeat) return 0;
+        Var loss;
+        bool first = true;
+        for (size_t k = 0; k < feats.size(); ++k) {
+            if (!gfeat[k]) continue;
+            Var term = op_sum_all(t, op_mul(t, feats[k], t.input(tensor_from(gfeat[k], t.value(feats[k]).shape))));
+            loss = first ? term : op_add(t, loss, term);
+            first = false;
+        }
+        for (auto *p : mp.all_tensors()) p->zero_grad();
+        t.backward(loss);
+        if (gpacked)
+            for (auto *p : mp.all_tensors()) {
+                add_into(gpacked, p->grad);
+                gpacked += p->grad.data.size();
+            }
+        add_into(gimage, t.grad(img));
+    } catch (const std::exception &e) {
+        g_perr = e.what();
+        return 1;
+    }
+    return 0;
+}
+
+// run_loss_step (engine.hpp:316-340) with the packed model: returns the loss,
+// accumulates the packed gradient of every parameter and writes phi
+int mdr_loss_step(const float *fixed, const float *moving, int h, int w, int l,
+                  const float *packed, float lambda, int window, double *loss, float *gpacked,
+                  float *phi) {
+    try {
+        ModelParams<float> mp = init_model<float>(ModelConfig::small_preset(), 1);
+        load_params(mp, packed);
+        Volume f(D3(h, w, l)), m(D3(h, w, l));
+        std::memcpy(f.data.data(), fixed, f.data.size() * sizeof(float));
+        std::memcpy(m.data.data(), moving, m.data.size() * sizeof(float));
+        auto params = mp.all_tensors();
+        LossConfig lc{lambda, window};
+        RegistrationResult rr;
+        *loss = run_loss_step(f, m, mp, lc, params, gpacked != nullptr, phi ? &rr : nullptr);
+        if (gpacked)
+            for (auto *p : params) {
+                add_into(gpacked, p->grad);
+                gpacked += p->grad.data.size();
+            }
+        if (phi) std::memcpy(phi, rr.phi.data.data(), rr.phi.data.size() * sizeof(float));
     } catch (const std::exception &e) {
         g_perr = e.what();
         return 1;

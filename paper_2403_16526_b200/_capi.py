@@ -54,6 +54,19 @@ class LevelGrads(C.Structure):
     _fields_ = [(f, C.c_void_p) for f in LEVEL_FIELDS]
 
 
+BLOCK_FIELDS = ("w1", "b1", "g1", "be1", "w2", "b2", "g2", "be2")
+
+
+class BlockParams(C.Structure):
+    """mdg_block_params (ConvBlockParams, encoder.hpp:45-48)."""
+
+    _fields_ = [(f, C.c_void_p) for f in BLOCK_FIELDS]
+
+
+class BlockGrads(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in BLOCK_FIELDS]
+
+
 _p = C.c_void_p  # device or host pointer
 _i = C.c_int
 _f = C.c_float
@@ -96,6 +109,10 @@ SIGNATURES = {
     "mdg_sgd_step": (_st, [_p, _p, C.c_int64, C.c_double, _p]),
     "mdg_warp_labels": (_st, [_p, Dims3, _p, _p, _p]),
     "mdg_mean_dice": (_st, [_p, _p, C.c_int64, _i, C.POINTER(C.c_double), _p]),
+    "mdg_encoder_create": (_st, [Dims3, _i, _i, _f, C.POINTER(_p)]),
+    "mdg_encoder_destroy": (None, [_p]),
+    "mdg_encoder_forward": (_st, [_p, _p, C.POINTER(BlockParams), C.POINTER(_p), _p]),
+    "mdg_encoder_backward": (_st, [_p, C.POINTER(_p), C.POINTER(BlockGrads), _p, _p]),
     "mdg_pyramid_create": (_st, [C.POINTER(PyramidConfig), C.POINTER(_p)]),
     "mdg_pyramid_destroy": (None, [_p]),
     "mdg_pyramid_forward": (_st, [_p, C.POINTER(_p), C.POINTER(_p), C.POINTER(LevelParams), _p,

@@ -1,0 +1,546 @@
+// encoder.cu — the feature encoder's kernels on sm_100a:
+// conv blocks (conv3 -> InstanceNorm -> LeakyReLU, twice) and 2x average
+// pooling (encoder.hpp:87-116, ops.hpp:58-99, 137-238, sampling.hpp:171-219).
+//
+// conv3 (any ic -> oc): one CTA computes a 32x8x4 voxel block for 8 output
+// channels.  Input channels stream through shared memory four at a time (the
+// 6x10x34 slab with a zero halo, batched loads), the weights of the chunk sit
+// in shared memory as [ci][tap][oc] so each tap is one broadcast float2-pair
+// read, and every thread accumulates its 4 voxels x 8 channels on the packed
+// FP32 pipe (FFMA2 with a broadcast input value).  The input gradient is the
+// same kernel with the flipped, transposed kernel and accumulation into the
+// existing gradient; the kernel gradient is a per-block outer-product sum
+// over shared-memory tiles with a fixed-order cross-block reduction.
+// Accumulation is FMA-contracted: results match the CPU reference to fp32
+// tolerance (tests: relative norm 1e-4).
+#include <algorithm>
+
+#include "mdg_common.cuh"
+
+namespace mdg {
+namespace enc {
+
+constexpr int TX = 32, TY = 8, TV = 4;               // voxel block
+constexpr int HX = TX + 2, HY = TY + 2, HZ = TV + 2;  // slab with halo
+constexpr int SLAB = HZ * HY * HX;                    // one channel
+constexpr int CIB = 4;                                // input channels per stage
+constexpr int OCB = 8;                                // output channels per CTA
+constexpr int NT = TX * TY;
+
+struct D3 {
+    int h, w, l, n;
+};
+
+// input channels [c0, c0+nch) of `src`, planes z0-1 .. z0+TV, rows y0-1 ..,
+// columns x0-1 .., zero outside the volume; all loads issued before stores
+template <int MAXCH>
+__device__ __forceinline__ void stage1(float *dst, const float *__restrict__ src, int nch,
+                                       const D3 &d, int x0, int y0, int z0) {
+    constexpr int kRows = HZ * HY;
+    constexpr int kIt = (MAXCH * kRows + 7) / 8;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int gx0 = x0 - 1 + lane, gx1 = x0 + 31 + lane;
+    const bool okx0 = gx0 >= 0 && gx0 < d.h, okx1 = lane < 2 && gx1 < d.h;
+    float v0[kIt], v1[kIt];
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+        const int r = wid + 8 * it;
+        v0[it] = v1[it] = 0.0f;
+        if (r < nch * kRows) {
+            const int c = r / kRows, rr = r - c * kRows;
+            const int dz = rr / HY, yy = rr - dz * HY;
+            const int gy = y0 - 1 + yy, gz = z0 - 1 + dz;
+            if (gy >= 0 && gy < d.w && gz >= 0 && gz < d.l) {
+                const float *row = src + (int64_t)c * d.n + ((int64_t)gz * d.w + gy) * d.h;
+                if (okx0) v0[it] = __ldg(row + gx0);
+                if (okx1) v1[it] = __ldg(row + gx1);
+            }
+        }
+    }
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+        const int r = wid + 8 * it;
+        if (r < nch * kRows) {
+            dst[r * HX + lane] = v0[it];
+            if (lane < 2) dst[r * HX + 32 + lane] = v1[it];
+        }
+    }
+}
+
+// up to CIB channels, two at a time (bounded register window)
+__device__ __forceinline__ void stage(float *dst, const float *__restrict__ src, int nch,
+                                      const D3 &d, int x0, int y0, int z0) {
+    for (int c = 0; c < nch; c += 2)
+        stage1<2>(dst + c * SLAB, src + (int64_t)c * d.n, min(2, nch - c), d, x0, y0, z0);
+}
+
+// wT[c][t][o] (o padded to a multiple of OCB with zeros) from the reference
+// layout w[oc][ic][27]:  fwd: c = ci, o = co, tap t;  flip (input gradient):
+// c = co, o = ci, tap 26 - t
+__global__ void wprep_k(const float *__restrict__ w, int oc, int ic, int flip, int opad,
+                        float *__restrict__ wT) {
+    const int cin = flip ? oc : ic, cout = flip ? ic : oc;
+    const int total = cin * 27 * opad;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int o = i % opad, t = (i / opad) % 27, c = i / (27 * opad);
+        float v = 0.0f;
+        if (o < cout) v = flip ? w[((int64_t)c * ic + o) * 27 + (26 - t)] : w[((int64_t)o * ic + c) * 27 + t];
+        wT[i] = v;
+    }
+}
+
+// out[o][p] (+)= bias[o] + sum_c sum_t wT[c][t][o] * in[c][p + off(t)]
+template <bool ACC>
+__global__ void __launch_bounds__(NT, 2)
+conv3g_k(const float *__restrict__ in, int cin, D3 d, const float *__restrict__ wT, int opad,
+         const float *__restrict__ bias, int cout, float *__restrict__ out) {
+    __shared__ __align__(16) float slab[CIB * SLAB];
+    __shared__ __align__(16) float ws[CIB * 27 * OCB];
+    const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+    const int nzb = (d.l + TV - 1) / TV;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int zb = blockIdx.z % nzb, ob = blockIdx.z / nzb;
+    const int z0 = zb * TV, o0 = ob * OCB;
+    float2 acc[TV][OCB / 2];
+#pragma unroll
+    for (int j = 0; j < OCB / 2; ++j) {
+        const float b0 = (!ACC && bias && o0 + 2 * j < cout) ? bias[o0 + 2 * j] : 0.0f;
+        const float b1 = (!ACC && bias && o0 + 2 * j + 1 < cout) ? bias[o0 + 2 * j + 1] : 0.0f;
+#pragma unroll
+        for (int v = 0; v < TV; ++v) acc[v][j] = make_float2(b0, b1);
+    }
+    const float *tp = slab + ty * HX + tx;
+    for (int c0 = 0; c0 < cin; c0 += CIB) {
+        const int nch = min(CIB, cin - c0);
+        __syncthreads();
+        stage(slab, in + (int64_t)c0 * d.n, nch, d, x0, y0, z0);
+        for (int i = threadIdx.x; i < nch * 27 * OCB; i += NT) {
+            const int c = i / (27 * OCB), r = i - c * 27 * OCB;
+            ws[i] = wT[((int64_t)(c0 + c) * 27) * opad + (r / OCB) * opad + o0 + (r % OCB)];
+        }
+        __syncthreads();
+        for (int c = 0; c < nch; ++c) {
+            const float *sp = tp + c * SLAB;
+            const float4 *wc = reinterpret_cast<const float4 *>(ws + c * 27 * OCB);
+#pragma unroll
+            for (int t = 0; t < 27; ++t) {
+                const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
+                const float4 wa = wc[2 * t], wb = wc[2 * t + 1];
+                const float2 w2[4] = {make_float2(wa.x, wa.y), make_float2(wa.z, wa.w),
+                                      make_float2(wb.x, wb.y), make_float2(wb.z, wb.w)};
+#pragma unroll
+                for (int v = 0; v < TV; ++v) {
+                    const float xv = sp[((v + dz) * HY + dy) * HX + dx];
+                    const float2 x2 = make_float2(xv, xv);
+#pragma unroll
+                    for (int j = 0; j < OCB / 2; ++j) acc[v][j] = __ffma2_rn(x2, w2[j], acc[v][j]);
+                }
+            }
+        }
+    }
+    const int x = x0 + tx, y = y0 + ty;
+    if (x >= d.h || y >= d.w) return;
+#pragma unroll
+    for (int v = 0; v < TV; ++v) {
+        const int z = z0 + v;
+        if (z >= d.l) break;
+        const int64_t p = ((int64_t)z * d.w + y) * d.h + x;
+#pragma unroll
+        for (int j = 0; j < OCB / 2; ++j) {
+            const int o = o0 + 2 * j;
+            if (o < cout) {
+                float *q = out + (int64_t)o * d.n + p;
+                *q = ACC ? *q + acc[v][j].x : acc[v][j].x;
+            }
+            if (o + 1 < cout) {
+                float *q = out + (int64_t)(o + 1) * d.n + p;
+                *q = ACC ? *q + acc[v][j].y : acc[v][j].y;
+            }
+        }
+    }
+}
+
+// kernel / bias gradient partials of one voxel block:
+//   part[blk][o][c][t] = sum_p gout[o][p] * in[c][p + off(t)]   (o in the
+//   CTA's 8-channel block, c in its 4-channel block), partb[blk][o] = sum gout
+__global__ void __launch_bounds__(NT)
+conv3g_wgrad_k(const float *__restrict__ in, int cin, D3 d, const float *__restrict__ gout,
+               int cout, float *__restrict__ part, float *__restrict__ partb) {
+    extern __shared__ __align__(16) float wsm[];  // slab [CIB*SLAB] | gout tile [OCB][1024]
+    float *slab = wsm;
+    float(*gs)[TV * TY * TX] = reinterpret_cast<float(*)[TV * TY * TX]>(wsm + CIB * SLAB);
+    const int nbx = gridDim.x;  // blocks over (x, y, z) tiles
+    const int ntx = (d.h + TX - 1) / TX, nty = (d.w + TY - 1) / TY;
+    const int blk = blockIdx.x;
+    const int bx = blk % ntx, by = (blk / ntx) % nty, bz = blk / (ntx * nty);
+    const int x0 = bx * TX, y0 = by * TY, z0 = bz * TV;
+    const int o0 = blockIdx.y * OCB, c0 = blockIdx.z * CIB;
+    const int nch = min(CIB, cin - c0);
+    stage(slab, in + (int64_t)c0 * d.n, nch, d, x0, y0, z0);
+    for (int i = threadIdx.x; i < OCB * TV * TY * TX; i += NT) {
+        const int o = i / (TV * TY * TX), r = i - o * (TV * TY * TX);
+        const int v = r / (TY * TX), yy = (r / TX) % TY, xx = r % TX;
+        const int x = x0 + xx, y = y0 + yy, z = z0 + v;
+        float g = 0.0f;
+        if (o0 + o < cout && x < d.h && y < d.w && z < d.l)
+            g = __ldg(gout + (int64_t)(o0 + o) * d.n + ((int64_t)z * d.w + y) * d.h + x);
+        gs[o][r] = g;
+    }
+    __syncthreads();
+    // outputs (o, c, t): 8 * nch * 27, strided over the threads
+    const int nout = OCB * nch * 27;
+    for (int k = threadIdx.x; k < nout; k += NT) {
+        const int o = k / (nch * 27), c = (k / 27) % nch, t = k % 27;
+        const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
+        const float *sl = slab + c * SLAB + (dz * HY + dy) * HX + dx;
+        const float *gv = gs[o];
+        float acc = 0.0f;
+        for (int v = 0; v < TV; ++v)
+            for (int yy = 0; yy < TY; ++yy) {
+                const float *srow = sl + (v * HY + yy) * HX;
+                const float *grow = gv + (v * TY + yy) * TX;
+#pragma unroll 8
+                for (int xx = 0; xx < TX; ++xx) acc = fmaf(grow[xx], srow[xx], acc);
+            }
+        part[(((int64_t)blk * gridDim.y + blockIdx.y) * gridDim.z + blockIdx.z) * (OCB * CIB * 27) +
+             (o * CIB + c) * 27 + t] = acc;
+    }
+    if (blockIdx.z == 0 && threadIdx.x < OCB) {
+        float s = 0.0f;
+        for (int r = 0; r < TV * TY * TX; ++r) s += gs[threadIdx.x][r];
+        partb[((int64_t)blk * gridDim.y + blockIdx.y) * OCB + threadIdx.x] = s;
+    }
+    (void)nbx;
+}
+
+// fixed-order sum of the per-block partials into gk[o][c][t] (+=) and gb[o]
+__global__ void __launch_bounds__(256)
+conv3g_wgrad_final_k(const float *__restrict__ part, const float *__restrict__ partb, int nblk,
+                     int noy, int ncz, int cout, int cin, float *__restrict__ gk,
+                     float *__restrict__ gb) {
+    const int idx = blockIdx.x;  // (o, c, t) or bias slots at the end
+    const int nw = cout * cin * 27;
+    float v = 0.0f;
+    if (idx < nw) {
+        const int o = idx / (cin * 27), c = (idx / 27) % cin, t = idx % 27;
+        const int oy = o / OCB, ol = o % OCB, cz = c / CIB, cl = c % CIB;
+        for (int b = threadIdx.x; b < nblk; b += 256)
+            v += part[(((int64_t)b * noy + oy) * ncz + cz) * (OCB * CIB * 27) + (ol * CIB + cl) * 27 + t];
+    } else {
+        const int o = idx - nw, oy = o / OCB, ol = o % OCB;
+        for (int b = threadIdx.x; b < nblk; b += 256) v += partb[((int64_t)b * noy + oy) * OCB + ol];
+    }
+    __shared__ float s[256];
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int m = 128; m > 0; m >>= 1) {
+        if (threadIdx.x < m) s[threadIdx.x] += s[threadIdx.x + m];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (idx < nw) {
+            if (gk) gk[idx] += s[0];
+        } else if (gb) {
+            gb[idx - nw] += s[0];
+        }
+    }
+}
+
+// ------------------------------------------------ instance norm + leaky relu
+// per-channel partial sums (pass 1: x, pass 2: (x - mean)^2 with mean given)
+__global__ void __launch_bounds__(256)
+chan_sum_k(const float *__restrict__ x, int n, const float *__restrict__ mean,
+           float *__restrict__ part) {
+    const int c = blockIdx.y;
+    const float *src = x + (int64_t)c * n;
+    const float mu = mean ? mean[c] : 0.0f;
+    float a = 0.0f;
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        const float v = src[i];
+        if (mean) {
+            const float t = v - mu;
+            a = fmaf(t, t, a);
+        } else {
+            a += v;
+        }
+    }
+    __shared__ float s[256];
+    s[threadIdx.x] = a;
+    __syncthreads();
+    for (int m = 128; m > 0; m >>= 1) {
+        if (threadIdx.x < m) s[threadIdx.x] += s[threadIdx.x + m];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[(int64_t)c * gridDim.x + blockIdx.x] = s[0];
+}
+
+// stat[c] = sum(part[c]) / n; if inv: stat = 1 / sqrt(stat + eps)
+__global__ void __launch_bounds__(256)
+chan_final_k(const float *__restrict__ part, int nparts, int n, int inv, float eps,
+             float *__restrict__ stat) {
+    const int c = blockIdx.x;
+    float v = 0.0f;
+    for (int i = threadIdx.x; i < nparts; i += 256) v += part[(int64_t)c * nparts + i];
+    __shared__ float s[256];
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int m = 128; m > 0; m >>= 1) {
+        if (threadIdx.x < m) s[threadIdx.x] += s[threadIdx.x + m];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const float r = s[0] / (float)n;
+        stat[c] = inv ? 1.0f / sqrtf(r + eps) : r;
+    }
+}
+
+// z = lrelu(gamma (x - mean) inv + beta)   (ops.hpp:184-185, 230)
+__global__ void __launch_bounds__(256)
+in_apply_k(const float *__restrict__ x, int n, const float *__restrict__ mean,
+           const float *__restrict__ inv, const float *__restrict__ g,
+           const float *__restrict__ b, float slope, float *__restrict__ z) {
+    const int c = blockIdx.y;
+    const float mu = mean[c], iv = inv[c], gg = g[c], bb = b[c];
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        const float y = gg * (x[(int64_t)c * n + i] - mu) * iv + bb;
+        z[(int64_t)c * n + i] = y > 0.0f ? y : slope * y;
+    }
+}
+
+// backward sums per channel: gy = gz * lrelu'(y), xh = (x - mean) inv:
+// part[c][blk] = {sum gy, sum gy * xh}
+__global__ void __launch_bounds__(256)
+in_bwd_sum_k(const float *__restrict__ x, const float *__restrict__ gz, int n,
+             const float *__restrict__ mean, const float *__restrict__ inv,
+             const float *__restrict__ g, const float *__restrict__ b, float slope,
+             float *__restrict__ part) {
+    const int c = blockIdx.y;
+    const float mu = mean[c], iv = inv[c], gg = g[c], bb = b[c];
+    float sg = 0.0f, sgx = 0.0f;
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        const float xh = (x[(int64_t)c * n + i] - mu) * iv;
+        const float y = gg * xh + bb;
+        const float gy = gz[(int64_t)c * n + i] * (y > 0.0f ? 1.0f : slope);
+        sg += gy;
+        sgx = fmaf(gy, xh, sgx);
+    }
+    __shared__ float s[2][256];
+    s[0][threadIdx.x] = sg;
+    s[1][threadIdx.x] = sgx;
+    __syncthreads();
+    for (int m = 128; m > 0; m >>= 1) {
+        if (threadIdx.x < m) {
+            s[0][threadIdx.x] += s[0][threadIdx.x + m];
+            s[1][threadIdx.x] += s[1][threadIdx.x + m];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[((int64_t)c * gridDim.x + blockIdx.x) * 2] = s[0][0];
+        part[((int64_t)c * gridDim.x + blockIdx.x) * 2 + 1] = s[1][0];
+    }
+}
+
+// sums[c] = {sum gy, sum gy xh}; gamma/beta grads accumulate
+__global__ void __launch_bounds__(256)
+in_bwd_final_k(const float *__restrict__ part, int nparts, float *__restrict__ sums,
+               float *__restrict__ gg, float *__restrict__ gb) {
+    const int c = blockIdx.x;
+    float a = 0.0f, bsum = 0.0f;
+    for (int i = threadIdx.x; i < nparts; i += 256) {
+        a += part[((int64_t)c * nparts + i) * 2];
+        bsum += part[((int64_t)c * nparts + i) * 2 + 1];
+    }
+    __shared__ float s[2][256];
+    s[0][threadIdx.x] = a;
+    s[1][threadIdx.x] = bsum;
+    __syncthreads();
+    for (int m = 128; m > 0; m >>= 1) {
+        if (threadIdx.x < m) {
+            s[0][threadIdx.x] += s[0][threadIdx.x + m];
+            s[1][threadIdx.x] += s[1][threadIdx.x + m];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        sums[2 * c] = s[0][0];
+        sums[2 * c + 1] = s[1][0];
+        if (gg) gg[c] += s[1][0];  // ops.hpp:204-205: gs += sum_gx, gb += sum_g
+        if (gb) gb[c] += s[0][0];
+    }
+}
+
+// gx = (gamma inv) (gy - mean(gy) - xh mean(gy xh))   (ops.hpp:206-212);
+// written (not accumulated): the conv output it feeds is internal
+__global__ void __launch_bounds__(256)
+in_bwd_apply_k(const float *__restrict__ x, const float *__restrict__ gz, int n,
+               const float *__restrict__ mean, const float *__restrict__ inv,
+               const float *__restrict__ g, const float *__restrict__ b, float slope,
+               const float *__restrict__ sums, float *__restrict__ gx) {
+    const int c = blockIdx.y;
+    const float mu = mean[c], iv = inv[c], gg = g[c], bb = b[c];
+    const float k = gg * iv, mg = sums[2 * c] / (float)n, mgx = sums[2 * c + 1] / (float)n;
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        const float xh = (x[(int64_t)c * n + i] - mu) * iv;
+        const float y = gg * xh + bb;
+        const float gy = gz[(int64_t)c * n + i] * (y > 0.0f ? 1.0f : slope);
+        gx[(int64_t)c * n + i] = k * (gy - mg - xh * mgx);
+    }
+}
+
+// ------------------------------------------------------------ avg pooling 2x
+// sampling.hpp:171-191 (replicate padding for odd dims)
+__global__ void __launch_bounds__(256)
+avgpool_fwd_k(const float *__restrict__ in, int C, D3 d, D3 od, float *__restrict__ out) {
+    const int64_t total = (int64_t)C * od.n;
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * 256) {
+        const int c = (int)(i / od.n), o = (int)(i - (int64_t)c * od.n);
+        const int t = o / od.h, x = o - t * od.h, z = t / od.w, y = t - z * od.w;
+        const float *pl = in + (int64_t)c * d.n;
+        float s = 0.0f;
+        for (int dz = 0; dz < 2; ++dz)
+            for (int dy = 0; dy < 2; ++dy)
+                for (int dx = 0; dx < 2; ++dx) {
+                    const int xi = min(2 * x + dx, d.h - 1), yi = min(2 * y + dy, d.w - 1),
+                              zi = min(2 * z + dz, d.l - 1);
+                    s += pl[((int64_t)zi * d.w + yi) * d.h + xi];
+                }
+        out[i] = s / 8.0f;
+    }
+}
+
+// sampling.hpp:194-219 as a gather: input (x,y,z) gets g/8 of its output
+// cell once per (dx,dy,dz) that clamps onto it
+__global__ void __launch_bounds__(256)
+avgpool_bwd_k(const float *__restrict__ gout, int C, D3 d, D3 od, float *__restrict__ gin) {
+    const int64_t total = (int64_t)C * d.n;
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * 256) {
+        const int c = (int)(i / d.n), p = (int)(i - (int64_t)c * d.n);
+        const int t = p / d.h, x = p - t * d.h, z = t / d.w, y = t - z * d.w;
+        const int mx = (x == d.h - 1 && (d.h & 1)) ? 2 : 1;
+        const int my = (y == d.w - 1 && (d.w & 1)) ? 2 : 1;
+        const int mz = (z == d.l - 1 && (d.l & 1)) ? 2 : 1;
+        const float g = gout[(int64_t)c * od.n + ((int64_t)(z / 2) * od.w + y / 2) * od.h + x / 2] / 8.0f;
+        float a = gin[i];
+        for (int k = 0; k < mx * my * mz; ++k) a += g;
+        gin[i] = a;
+    }
+}
+
+}  // namespace enc
+
+using namespace enc;
+
+static unsigned grid_for(int64_t n, int per = 256) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + per - 1) / per, 148 * 8));
+}
+
+// ---------------------------------------------------------------- internal
+mdg_status enc_conv3_fwd(const float *in, int ic, mdg_dims3 dd, const float *w, const float *b,
+                         int oc, float *out, cudaStream_t st) {
+    const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
+    const int opad = (oc + OCB - 1) / OCB * OCB;
+    Scratch wt;
+    MDG_CUDA_TRY(wt.alloc((size_t)ic * 27 * opad * sizeof(float), st));
+    wprep_k<<<grid_for((int64_t)ic * 27 * opad), 256, 0, st>>>(w, oc, ic, 0, opad, wt.as<float>());
+    MDG_LAUNCHED();
+    const dim3 g((d.h + TX - 1) / TX, (d.w + TY - 1) / TY, ((d.l + TV - 1) / TV) * (opad / OCB));
+    conv3g_k<false><<<g, NT, 0, st>>>(in, ic, d, wt.as<float>(), opad, b, oc, out);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 dd, const float *w, int oc,
+                         const float *gout, float *gin, float *gw, float *gb, cudaStream_t st) {
+    const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
+    if (gin) {
+        const int ipad = (ic + OCB - 1) / OCB * OCB;
+        Scratch wt;
+        MDG_CUDA_TRY(wt.alloc((size_t)oc * 27 * ipad * sizeof(float), st));
+        wprep_k<<<grid_for((int64_t)oc * 27 * ipad), 256, 0, st>>>(w, oc, ic, 1, ipad,
+                                                                   wt.as<float>());
+        MDG_LAUNCHED();
+        const dim3 g((d.h + TX - 1) / TX, (d.w + TY - 1) / TY,
+                     ((d.l + TV - 1) / TV) * (ipad / OCB));
+        conv3g_k<true><<<g, NT, 0, st>>>(gout, oc, d, wt.as<float>(), ipad, nullptr, ic, gin);
+        MDG_LAUNCHED();
+    }
+    if (gw || gb) {
+        const int nblk = ((d.h + TX - 1) / TX) * ((d.w + TY - 1) / TY) * ((d.l + TV - 1) / TV);
+        const int noy = (oc + OCB - 1) / OCB, ncz = (ic + CIB - 1) / CIB;
+        Scratch part;
+        const size_t np = (size_t)nblk * noy * ncz * OCB * CIB * 27;
+        MDG_CUDA_TRY(part.alloc((np + (size_t)nblk * noy * OCB) * sizeof(float), st));
+        MDG_CUDA_TRY(cudaMemsetAsync(part.p, 0, (np + (size_t)nblk * noy * OCB) * sizeof(float), st));
+        float *pb = part.as<float>() + np;
+        const size_t smem = (size_t)(CIB * SLAB + OCB * TV * TY * TX) * sizeof(float);
+        MDG_CUDA_TRY(cudaFuncSetAttribute(conv3g_wgrad_k,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        conv3g_wgrad_k<<<dim3(nblk, noy, ncz), NT, smem, st>>>(in, ic, d, gout, oc,
+                                                               part.as<float>(), pb);
+        MDG_LAUNCHED();
+        conv3g_wgrad_final_k<<<oc * ic * 27 + oc, 256, 0, st>>>(part.as<float>(), pb, nblk, noy,
+                                                                ncz, oc, ic, gw, gb);
+        MDG_LAUNCHED();
+    }
+    return MDG_OK;
+}
+
+// z = lrelu(IN(x)); mean / inv (per channel) saved for the backward
+mdg_status enc_in_lrelu_fwd(const float *x, int C, int64_t n, const float *g, const float *b,
+                            float slope, float *z, float *mean, float *inv, cudaStream_t st) {
+    const unsigned gx = std::min<unsigned>(grid_for(n), 256);
+    Scratch part;
+    MDG_CUDA_TRY(part.alloc((size_t)C * gx * sizeof(float), st));
+    chan_sum_k<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, nullptr, part.as<float>());
+    MDG_LAUNCHED();
+    chan_final_k<<<C, 256, 0, st>>>(part.as<float>(), gx, (int)n, 0, 0.0f, mean);
+    MDG_LAUNCHED();
+    chan_sum_k<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, mean, part.as<float>());
+    MDG_LAUNCHED();
+    chan_final_k<<<C, 256, 0, st>>>(part.as<float>(), gx, (int)n, 1, 1e-5f, inv);
+    MDG_LAUNCHED();
+    in_apply_k<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, mean, inv, g, b, slope, z);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+// gx = d/dx of lrelu(IN(x)) applied to gz (written); gamma/beta grads accumulate
+mdg_status enc_in_lrelu_bwd(const float *x, const float *gz, int C, int64_t n, const float *g,
+                            const float *b, float slope, const float *mean, const float *inv,
+                            float *gx, float *gg, float *gbeta, cudaStream_t st) {
+    const unsigned nb = std::min<unsigned>(grid_for(n), 256);
+    Scratch part;
+    MDG_CUDA_TRY(part.alloc(((size_t)C * nb * 2 + 2 * C) * sizeof(float), st));
+    float *sums = part.as<float>() + (size_t)C * nb * 2;
+    in_bwd_sum_k<<<dim3(nb, C), 256, 0, st>>>(x, gz, (int)n, mean, inv, g, b, slope,
+                                             part.as<float>());
+    MDG_LAUNCHED();
+    in_bwd_final_k<<<C, 256, 0, st>>>(part.as<float>(), nb, sums, gg, gbeta);
+    MDG_LAUNCHED();
+    in_bwd_apply_k<<<dim3(nb, C), 256, 0, st>>>(x, gz, (int)n, mean, inv, g, b, slope, sums, gx);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+mdg_status enc_avgpool_fwd(const float *in, int C, mdg_dims3 dd, float *out, cudaStream_t st) {
+    const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
+    const int oh = (dd.h + 1) / 2, ow = (dd.w + 1) / 2, ol = (dd.l + 1) / 2;
+    const D3 od{oh, ow, ol, oh * ow * ol};
+    avgpool_fwd_k<<<grid_for((int64_t)C * od.n), 256, 0, st>>>(in, C, d, od, out);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+mdg_status enc_avgpool_bwd(const float *gout, int C, mdg_dims3 dd, float *gin, cudaStream_t st) {
+    const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
+    const int oh = (dd.h + 1) / 2, ow = (dd.w + 1) / 2, ol = (dd.l + 1) / 2;
+    const D3 od{oh, ow, ol, oh * ow * ol};
+    avgpool_bwd_k<<<grid_for((int64_t)C * d.n), 256, 0, st>>>(gout, C, d, od, gin);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+}  // namespace mdg

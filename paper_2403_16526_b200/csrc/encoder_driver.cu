@@ -1,0 +1,185 @@
+// encoder_driver.cu — op_encode (encoder.hpp:102-116) as native host code
+// over the encoder kernels: a device arena per encoder object holds every
+// level's saved activations (conv outputs, InstanceNorm statistics, pooled
+// inputs); the backward replays the tape order of the reference (coarse level
+// first; the pooling backward feeds the finer level's feature gradient).
+#include <algorithm>
+#include <vector>
+
+#include "mdg_common.cuh"
+
+using namespace mdg;
+
+#define ENC_TRY(expr)                      \
+    do {                                   \
+        mdg_status _s = (expr);            \
+        if (_s != MDG_OK) return _s;       \
+    } while (0)
+
+struct mdg_encoder {
+    struct Level {
+        mdg_dims3 d;
+        int64_t n;
+        int cin, c;
+        float *x;          // block input (level 1: the image, not owned)
+        float *a1, *z1, *a2, *z2;  // conv1 out, block mid, conv2 out, block out (copy)
+        float *st1, *st2;  // mean | inv per channel (2C each)
+        float *gz;         // gradient of the block output
+    };
+    std::vector<Level> lv;
+    float slope = 0.2f;
+    float *scratch_a = nullptr, *scratch_b = nullptr;  // max C*n each
+    void *arena = nullptr;
+    int64_t bytes = 0;
+    std::vector<mdg_block_params> p_saved;
+    bool have_forward = false;
+};
+
+namespace {
+struct Carve2 {
+    char *base;
+    int64_t off = 0;
+    float *take(int64_t floats) {
+        float *p = reinterpret_cast<float *>(base ? base + off : nullptr);
+        off += ((floats * (int64_t)sizeof(float) + 255) / 256) * 256;
+        return p;
+    }
+};
+
+void enc_layout(mdg_encoder *e, Carve2 &cv, mdg_dims3 d0, int base, int levels) {
+    e->lv.resize(levels);
+    mdg_dims3 d = d0;
+    int64_t mx = 0;
+    for (int k = 0; k < levels; ++k) {
+        auto &L = e->lv[k];
+        if (k > 0) d = mdg_dims3{(d.h + 1) / 2, (d.w + 1) / 2, (d.l + 1) / 2};
+        L.d = d;
+        L.n = nvox(d);
+        L.c = base << k;
+        L.cin = k == 0 ? 1 : (base << (k - 1));
+        L.x = k == 0 ? nullptr : cv.take((int64_t)L.cin * L.n);
+        L.a1 = cv.take((int64_t)L.c * L.n);
+        L.z1 = cv.take((int64_t)L.c * L.n);
+        L.a2 = cv.take((int64_t)L.c * L.n);
+        L.z2 = cv.take((int64_t)L.c * L.n);
+        L.st1 = cv.take(2 * (int64_t)L.c);
+        L.st2 = cv.take(2 * (int64_t)L.c);
+        L.gz = cv.take((int64_t)L.c * L.n);
+        mx = std::max<int64_t>(mx, (int64_t)L.c * L.n);
+    }
+    e->scratch_a = cv.take(mx);
+    e->scratch_b = cv.take(mx);
+}
+}  // namespace
+
+extern "C" {
+
+mdg_status mdg_encoder_create(mdg_dims3 d, int base_channels, int levels, float slope,
+                              mdg_encoder **out) {
+    MDG_REQUIRE(out, "encoder: null pointer");
+    *out = nullptr;
+    MDG_REQUIRE(base_channels >= 1, "encoder: base_channels must be >= 1");
+    MDG_REQUIRE(levels == 5, "encoder: levels is fixed at 5");
+    MDG_REQUIRE(dims_ok(d), "encoder: invalid dims " + dims_str(d));
+    MDG_REQUIRE(d.h >= 16 && d.w >= 16 && d.l >= 16,
+                "encode: volume " + dims_str(d) + " too small for 5 pyramid levels (needs dims >= 16)");
+    mdg_encoder *e = new mdg_encoder;
+    e->slope = slope;
+    Carve2 dry{nullptr};
+    enc_layout(e, dry, d, base_channels, levels);
+    e->bytes = dry.off;
+    void *mem = nullptr;
+    cudaError_t err = cudaMalloc(&mem, (size_t)e->bytes);
+    if (err != cudaSuccess) {
+        delete e;
+        return status_from_cuda(err, "encoder arena");
+    }
+    e->arena = mem;
+    Carve2 cv{reinterpret_cast<char *>(mem)};
+    enc_layout(e, cv, d, base_channels, levels);
+    *out = e;
+    return MDG_OK;
+}
+
+void mdg_encoder_destroy(mdg_encoder *e) {
+    if (!e) return;
+    if (e->arena) cudaFree(e->arena);
+    delete e;
+}
+
+mdg_status mdg_encoder_forward(mdg_encoder *e, const float *image, const mdg_block_params *params,
+                               float *const *features, void *stream) {
+    MDG_REQUIRE(e && image && params && features, "encoder: null pointer");
+    cudaStream_t st = S_(stream);
+    e->p_saved.assign(params, params + e->lv.size());
+    for (size_t k = 0; k < e->lv.size(); ++k) {
+        auto &L = e->lv[k];
+        const mdg_block_params &P = params[k];
+        MDG_REQUIRE(P.w1 && P.b1 && P.g1 && P.be1 && P.w2 && P.b2 && P.g2 && P.be2 && features[k],
+                    "encoder: null parameter or feature buffer");
+        const float *x = image;
+        if (k > 0) {
+            ENC_TRY(enc_avgpool_fwd(e->lv[k - 1].z2, L.cin, e->lv[k - 1].d, L.x, st));
+            x = L.x;
+        } else {
+            L.x = const_cast<float *>(image);
+        }
+        ENC_TRY(enc_conv3_fwd(x, L.cin, L.d, P.w1, P.b1, L.c, L.a1, st));
+        ENC_TRY(enc_in_lrelu_fwd(L.a1, L.c, L.n, P.g1, P.be1, e->slope, L.z1, L.st1,
+                                 L.st1 + L.c, st));
+        ENC_TRY(enc_conv3_fwd(L.z1, L.c, L.d, P.w2, P.b2, L.c, L.a2, st));
+        ENC_TRY(enc_in_lrelu_fwd(L.a2, L.c, L.n, P.g2, P.be2, e->slope, L.z2, L.st2,
+                                 L.st2 + L.c, st));
+        MDG_CUDA_TRY(cudaMemcpyAsync(features[k], L.z2, (size_t)L.c * L.n * sizeof(float),
+                                     cudaMemcpyDeviceToDevice, st));
+    }
+    e->have_forward = true;
+    return MDG_OK;
+}
+
+mdg_status mdg_encoder_backward(mdg_encoder *e, const float *const *gfeatures,
+                                const mdg_block_grads *grads, float *gimage, void *stream) {
+    MDG_REQUIRE(e && gfeatures, "encoder: null pointer");
+    MDG_REQUIRE(e->have_forward, "encoder: backward without a forward");
+    cudaStream_t st = S_(stream);
+    const int levels = (int)e->lv.size();
+    for (int k = 0; k < levels; ++k) {
+        auto &L = e->lv[k];
+        if (gfeatures[k])
+            MDG_CUDA_TRY(cudaMemcpyAsync(L.gz, gfeatures[k], (size_t)L.c * L.n * sizeof(float),
+                                         cudaMemcpyDeviceToDevice, st));
+        else
+            MDG_CUDA_TRY(cudaMemsetAsync(L.gz, 0, (size_t)L.c * L.n * sizeof(float), st));
+    }
+    for (int k = levels - 1; k >= 0; --k) {
+        auto &L = e->lv[k];
+        const mdg_block_params &P = e->p_saved[k];
+        const mdg_block_grads *G = grads ? &grads[k] : nullptr;
+        float *ga = e->scratch_a, *gz1 = e->scratch_b;
+        // block output z2 = lrelu(IN2(a2))
+        ENC_TRY(enc_in_lrelu_bwd(L.a2, L.gz, L.c, L.n, P.g2, P.be2, e->slope, L.st2,
+                                 L.st2 + L.c, ga, G ? G->g2 : nullptr, G ? G->be2 : nullptr,
+                                 st));
+        MDG_CUDA_TRY(cudaMemsetAsync(gz1, 0, (size_t)L.c * L.n * sizeof(float), st));
+        ENC_TRY(enc_conv3_bwd(L.z1, L.c, L.d, P.w2, L.c, ga, gz1, G ? G->w2 : nullptr,
+                              G ? G->b2 : nullptr, st));
+        // z1 = lrelu(IN1(a1)); ga reused
+        ENC_TRY(enc_in_lrelu_bwd(L.a1, gz1, L.c, L.n, P.g1, P.be1, e->slope, L.st1,
+                                 L.st1 + L.c, ga, G ? G->g1 : nullptr, G ? G->be1 : nullptr,
+                                 st));
+        // conv1 input gradient: into the finer level's pooled-output gradient
+        float *gx = nullptr;
+        if (k > 0) {
+            gx = gz1;  // scratch (C_in <= C)
+            MDG_CUDA_TRY(cudaMemsetAsync(gx, 0, (size_t)L.cin * L.n * sizeof(float), st));
+        } else {
+            gx = gimage;
+        }
+        ENC_TRY(enc_conv3_bwd(L.x, L.cin, L.d, P.w1, L.c, ga, gx, G ? G->w1 : nullptr,
+                              G ? G->b1 : nullptr, st));
+        if (k > 0) ENC_TRY(enc_avgpool_bwd(gx, L.cin, e->lv[k - 1].d, e->lv[k - 1].gz, st));
+    }
+    return MDG_OK;
+}
+
+}  // extern "C"

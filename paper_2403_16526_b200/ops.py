@@ -660,6 +660,124 @@ class Pyramid:
         return grads, gf, gm
 
 
+@dataclass
+class BlockParams:
+    """encoder.hpp:45-48 ConvBlockParams: w1 {C,Cin,3,3,3}, b1/g1/be1 {C},
+    w2 {C,C,3,3,3}, b2/g2/be2 {C}."""
+
+    w1: torch.Tensor
+    b1: torch.Tensor
+    g1: torch.Tensor
+    be1: torch.Tensor
+    w2: torch.Tensor
+    b2: torch.Tensor
+    g2: torch.Tensor
+    be2: torch.Tensor
+
+    def tensors(self):
+        return [self.w1, self.b1, self.g1, self.be1, self.w2, self.b2, self.g2, self.be2]
+
+    def zeros_like(self):
+        return BlockParams(*[torch.zeros_like(t) for t in self.tensors()])
+
+
+class Encoder:
+    """op_encode (encoder.hpp:102-116) on one image at a time; the object owns
+    the saved activations of its last forward (one per image of a pair)."""
+
+    def __init__(self, dims, base_channels=8, levels=5, slope=0.2):
+        self._L = _capi.lib()
+        h = C.c_void_p()
+        _check(self._L.mdg_encoder_create(dims3(dims), base_channels, levels, float(slope),
+                                          C.byref(h)))
+        self._h = h
+        self.dims = [tuple(int(v) for v in dims)]
+        for _ in range(levels - 1):
+            self.dims.append(halved(self.dims[-1]))
+        self.channels = [base_channels << k for k in range(levels)]
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._L.mdg_encoder_destroy(self._h)
+        except Exception:
+            pass
+
+    def forward(self, image, blocks):
+        feats = [torch.empty(c, d[2], d[1], d[0], dtype=torch.float32, device=image.device)
+                 for c, d in zip(self.channels, self.dims)]
+        bp = (_capi.BlockParams * len(blocks))()
+        for i, b in enumerate(blocks):
+            for f, t in zip(_capi.BLOCK_FIELDS, b.tensors()):
+                setattr(bp[i], f, _ptr(t))
+        fp = (C.c_void_p * len(feats))(*[_ptr(t) for t in feats])
+        self._keep = (image, list(blocks))  # the backward reads the image and weights
+        _check(self._L.mdg_encoder_forward(self._h, _ptr(image), bp, fp, _stream()))
+        return feats
+
+    def backward(self, gfeats, grads, gimage=None):
+        gp = (C.c_void_p * len(gfeats))(*[_ptr(t) if t is not None else None for t in gfeats])
+        gb = (_capi.BlockGrads * len(grads))()
+        for i, g in enumerate(grads):
+            for f, t in zip(_capi.BLOCK_FIELDS, g.tensors()):
+                setattr(gb[i], f, _ptr(t))
+        _check(self._L.mdg_encoder_backward(self._h, gp, gb, _ptr(gimage), _stream()))
+
+
+class Model:
+    """ModelParams (engine.hpp:114-140) of the small preset as device tensors,
+    in the ModelParams::all_tensors order (5 encoder blocks, then 5 decoder
+    levels coarse -> fine), plus one pairwise-optimisation step
+    (run_loss_step engine.hpp:316-340 + an Adam update)."""
+
+    def __init__(self, tensors, dims, cfg: ModelConfig = None, loss: LossConfig = None,
+                 base_channels=8):
+        self.cfg = cfg or ModelConfig()
+        self.loss_cfg = loss or LossConfig()
+        self.tensors = list(tensors)
+        assert len(self.tensors) == 75, "expects the 75 ModelParams tensors"
+        self.blocks = [BlockParams(*self.tensors[8 * k:8 * k + 8]) for k in range(5)]
+        self.levels = [LevelParams.from_tensors(self.tensors[40 + 7 * k:47 + 7 * k])
+                       for k in range(5)]
+        self.enc_f = Encoder(dims, base_channels)
+        self.enc_m = Encoder(dims, base_channels)
+        pdims = self.enc_f.dims[::-1]
+        pch = self.enc_f.channels[::-1]
+        self.pyr = Pyramid(self.cfg, pdims, pch)
+        self.grads = [torch.zeros_like(t) for t in self.tensors]
+        self.opt = AdamOptimizer(self.tensors)
+
+    def _grad_structs(self):
+        gb = [BlockParams(*self.grads[8 * k:8 * k + 8]) for k in range(5)]
+        gl = [LevelParams.from_tensors(self.grads[40 + 7 * k:47 + 7 * k]) for k in range(5)]
+        return gb, gl
+
+    def loss_step(self, fixed, moving, backward=True):
+        """Forward (encoder x2 -> pyramid -> loss) and, optionally, the backward
+        into self.grads (zeroed first).  Returns (terms {total,ncc,reg}, phi)."""
+        ff = self.enc_f.forward(fixed, self.blocks)
+        mf = self.enc_m.forward(moving, self.blocks)
+        phi = self.pyr.forward(ff[::-1], mf[::-1], self.levels)
+        terms = total_loss(fixed, moving, phi, self.loss_cfg)
+        if backward:
+            for g in self.grads:
+                g.zero_()
+            gphi = total_loss_bwd(fixed, moving, phi, self.loss_cfg)[0]
+            gb, gl = self._grad_structs()
+            gf = [torch.zeros_like(t) for t in ff[::-1]]
+            gm = [torch.zeros_like(t) for t in mf[::-1]]
+            self.pyr.backward(gphi, gl, gf, gm)
+            self.enc_f.backward(gf[::-1], gb)
+            self.enc_m.backward(gm[::-1], gb)
+        return terms, phi
+
+    def po_step(self, fixed, moving, lr=1e-4):
+        """One PO iteration (engine.hpp:389-398): loss + backward + Adam."""
+        terms, phi = self.loss_step(fixed, moving, backward=True)
+        self.opt.step(lr, self.grads)
+        return terms, phi
+
+
 def launch_count() -> int:
     return int(_capi.lib().mdg_launch_count())
 

@@ -1,0 +1,115 @@
+"""The encoder and a full PO loss step on the GPU vs the
+REFERENCE (oracle/_ref): op_encode (encoder.hpp:102-116) features and
+gradients, and run_loss_step (engine.hpp:316-340: encoder x2 -> pyramid ->
+NCC + grad_reg) loss, phi and every one of the 75 parameter gradients of the
+small preset.
+
+Tolerances: features / phi / gradients by relative norm (SURVEY §8c
+protocol).  Conv biases that feed an InstanceNorm have an identically-zero
+true gradient (the norm removes per-channel constants), so theirs is pure
+rounding noise on both sides and is checked by an absolute bound instead."""
+import numpy as np
+import pytest
+import torch
+
+from _util import f32, rel_norm
+from paper_2403_16526_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+PRE_NORM_BIAS = {8 * k + i for k in range(5) for i in (1, 5)}  # b1, b2 of each block
+
+
+def split(packed, sizes):
+    out, o = [], 0
+    for s in sizes:
+        out.append(packed[o:o + s])
+        o += s
+    return out
+
+
+def shapes(sizes):
+    """ModelParams::all_tensors shapes of the small preset."""
+    sh = []
+    base = 8
+    for k in range(5):
+        c, cin = base << k, (1 if k == 0 else base << (k - 1))
+        sh += [(c, cin, 3, 3, 3), (c,), (c,), (c,), (c, c, 3, 3, 3), (c,), (c,), (c,)]
+    heads, chans = (8, 4, 2, 1, 1), (128, 64, 32, 16, 8)
+    for S, C in zip(heads, chans):
+        K = S * 6
+        sh += [(K, C), (K,), (K,), (K,), (S, 27), (3, 3 * S, 3, 3, 3), (3,)]
+    assert [int(np.prod(s)) for s in sh] == sizes
+    return sh
+
+
+def device_tensors(packed, sizes):
+    return [torch.from_numpy(np.ascontiguousarray(a.reshape(s))).cuda()
+            for a, s in zip(split(packed, sizes), shapes(sizes))]
+
+
+def perturbed_model(ref, seed):
+    """init_model(small_preset) with decoder weights enlarged so the attention
+    and the residuals are far from their near-identity initial values."""
+    packed, sizes = ref.model_params(42)
+    r = np.random.default_rng(seed)
+    parts = split(packed.copy(), sizes)
+    for k in range(5):
+        S = (8, 4, 2, 1, 1)[k]
+        i = 40 + 7 * k
+        parts[i][:] = r.standard_normal(parts[i].size) * 0.3      # proj.w
+        parts[i + 4][:] = r.standard_normal(parts[i + 4].size) * 0.5  # bias_b
+        parts[i + 5][:] = r.standard_normal(parts[i + 5].size) * (0.3 / np.sqrt(81 * S))
+    return f32(np.concatenate(parts)), sizes
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 16), (20, 18, 17)])
+def test_encoder_matches_reference(cuda, ref, dims):
+    h, w, l = dims
+    packed, sizes = ref.model_params(42)
+    r = np.random.default_rng(1)
+    img = f32(r.uniform(0, 1, (1, l, w, h)))
+    enc = ops.Encoder(dims)
+    gfeat = [f32(r.standard_normal((c, d[2], d[1], d[0]))) for c, d in zip(enc.channels, enc.dims)]
+    feats_r, gp_r, gi_r = ref.encode(img, packed, gfeat)
+    T = device_tensors(packed, sizes)
+    blocks = [ops.BlockParams(*T[8 * k:8 * k + 8]) for k in range(5)]
+    feats = enc.forward(torch.from_numpy(img).cuda(), blocks)
+    for a, b in zip(feats, feats_r):
+        assert rel_norm(a.cpu().numpy(), b) <= 1e-4, rel_norm(a.cpu().numpy(), b)
+    grads = [b.zeros_like() for b in blocks]
+    gimg = torch.zeros(1, l, w, h, device="cuda")
+    enc.backward([torch.from_numpy(g).cuda() for g in gfeat], grads, gimg)
+    torch.cuda.synchronize()
+    ours = [t.cpu().numpy().ravel() for g in grads for t in g.tensors()]
+    theirs = split(gp_r, sizes)[:40]
+    for i, (a, b) in enumerate(zip(ours, theirs)):
+        if i in PRE_NORM_BIAS:
+            blk = theirs[8 * (i // 8):8 * (i // 8) + 8]
+            scale = max(1.0, max(float(np.abs(t).max()) for t in blk))
+            assert np.abs(a - b).max() <= 1e-4 * scale, i
+        else:
+            assert rel_norm(a, b) <= 1e-4, (i, rel_norm(a, b))
+    assert rel_norm(gimg.cpu().numpy(), gi_r) <= 1e-4
+
+
+def test_full_loss_step_matches_reference(cuda, ref):
+    dims = (16, 16, 16)
+    h, w, l = dims
+    f, m, lf, lm, gt = ref.synth_pair(dims, seed=3)
+    packed, sizes = perturbed_model(ref, 5)
+    loss_r, gp_r, phi_r = ref.loss_step(f, m, packed, lam=1.0, window=9)
+    model = ops.Model(device_tensors(packed, sizes), dims)
+    terms, phi = model.loss_step(torch.from_numpy(f).cuda(), torch.from_numpy(m).cuda())
+    torch.cuda.synchronize()
+    assert abs(float(terms[0]) - loss_r) <= 1e-4 * abs(loss_r) + 1e-6, (float(terms[0]), loss_r)
+    assert rel_norm(phi.cpu().numpy(), phi_r) <= 1e-4, rel_norm(phi.cpu().numpy(), phi_r)
+    theirs = split(gp_r, sizes)
+    worst = 0.0
+    for i, (a, b) in enumerate(zip(model.grads, theirs)):
+        a = a.cpu().numpy().ravel()
+        if i in PRE_NORM_BIAS:
+            continue
+        worst = max(worst, rel_norm(a, b))
+        assert rel_norm(a, b) <= 1e-3, (i, rel_norm(a, b))
+    print("worst per-tensor relative gradient error", worst)
