@@ -252,6 +252,7 @@ def run_ours(args):
     # ---------------- the decoding pyramid around the op,
     # reported beside the headline (it is not part of `value`)
     pyramid = None if args.no_pyramid else run_pyramid(dev)
+    po = None if args.no_po else run_po(dev, world, args.po_pairs)
 
     peak, peak_kind = load_peak()
     dom = max(per_op, key=lambda k: per_op[k])
@@ -279,6 +280,7 @@ def run_ours(args):
                           "bytes_per_step": step_bytes},
         "e2e": e2e,
         "pyramid": pyramid,
+        "po": po,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -368,10 +370,63 @@ def run_pyramid(dev, reps=5):
     return {"workload": "decoder pyramid (build_pipeline minus encoder), small preset, "
                         "160x192x224 fine level, synthetic features",
             "fwd_ms": round(statistics.median(tf), 3), "bwd_ms": round(statistics.median(tb), 3),
-            "po_iter_ms": round(statistics.median(tp), 3),
-            "po_iter_note": "pyramid fwd + NCC/grad_reg loss fwd+bwd + pyramid bwd + Adam; "
-                            "the encoder (SURVEY 8f rank 2) is not built",
+            "decoder_iter_ms": round(statistics.median(tp), 3),
+            "decoder_iter_note": "pyramid fwd + NCC/grad_reg loss fwd+bwd + pyramid bwd + "
+                                 "Adam with the encoder features held fixed (the full "
+                                 "iteration is under 'po')",
             "arena_mib": round(pyr.device_bytes / 2 ** 20, 1)}
+
+
+def run_po(dev, world, pairs=0, reps=5):
+    """Pairwise optimisation (engine.hpp:377-411) of the full small-preset
+    model at 160x192x224: ms per PO iteration (encoder x2 -> pyramid -> NCC +
+    grad_reg -> backward -> Adam), and pairs/sec for 50-iteration pairs
+    (50 iterations + the final evaluation forward).  `pairs` > 0 runs that many
+    complete pairs and times them; otherwise pairs/sec is derived from the
+    measured iteration and forward times (labelled)."""
+    import torch
+
+    from paper_2403_16526_b200 import ops
+
+    h, w, l = DIMS
+    params = [t.to(dev) for t in ops.init_model(42)]
+    model = ops.Model(params, DIMS)
+    rng = ops.Rng(11)
+    fixed = rng.uniform((1, l, w, h), 0.0, 1.0).to(dev)
+    moving = rng.uniform((1, l, w, h), 0.0, 1.0).to(dev)
+    for _ in range(2):
+        model.po_step(fixed, moving)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ti, tf = [], []
+    for _ in range(reps):
+        e[0].record()
+        model.po_step(fixed, moving)
+        e[1].record()
+        model.loss_step(fixed, moving, backward=False)
+        e[2].record()
+        torch.cuda.synchronize()
+        ti.append(e[0].elapsed_time(e[1]))
+        tf.append(e[1].elapsed_time(e[2]))
+    it_ms, fwd_ms = statistics.median(ti), statistics.median(tf)
+    out = {"workload": "PO of the small-preset model at 160x192x224 (synthetic pair, "
+                       "init_model(42) weights)",
+           "iter_ms": round(it_ms, 3), "final_forward_ms": round(fwd_ms, 3),
+           "iters_per_pair": 50,
+           "pairs_per_sec": round(world * 1e3 / (50 * it_ms + fwd_ms), 4),
+           "pairs_per_sec_kind": "derived: world / (50 x iter + final forward), timed on the device"}
+    if pairs > 0:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(pairs):
+            m = ops.Model([t.to(dev) for t in ops.init_model(42)], DIMS)
+            for _ in range(50):
+                m.po_step(fixed, moving)
+            m.loss_step(fixed, moving, backward=False)
+        torch.cuda.synchronize()
+        out["pairs_run"] = pairs
+        out["pairs_per_sec_measured"] = round(world * pairs / (time.perf_counter() - t0), 4)
+    return out
 
 
 def run_e2e(args, L, host_in, world, dev):
@@ -563,6 +618,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling)")
     ap.add_argument("--no-pyramid", action="store_true", help="skip the pyramid timing")
+    ap.add_argument("--no-po", action="store_true", help="skip the PO-iteration timing")
+    ap.add_argument("--po-pairs", type=int, default=0,
+                    help="run this many complete 50-iteration pairs (pairs/sec measured)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps

@@ -162,22 +162,27 @@ conv3g_k(const float *__restrict__ in, int cin, D3 d, const float *__restrict__ 
 
 // kernel / bias gradient partials of one voxel block:
 //   part[blk][o][c][t] = sum_p gout[o][p] * in[c][p + off(t)]   (o in the
-//   CTA's 8-channel block, c in its 4-channel block), partb[blk][o] = sum gout
-__global__ void __launch_bounds__(NT)
+//   CTA's 8-channel block, c in its 4-channel block), partb[blk][o] = sum gout.
+// Lanes run along x (conflict-free shared-memory rows).  A warp owns kernel
+// rows (c, dz, dy); per voxel row each lane loads the three input taps and the
+// eight gout values of its column and accumulates 8 x 3 products (4 x 3 FFMA2
+// on channel pairs); the warp reduces the 24 sums at the end of the row set.
+constexpr int WG_NT = 288;  // 9 warps x 4 kernel rows = 36 = CIB * 9
+
+__global__ void __launch_bounds__(WG_NT)
 conv3g_wgrad_k(const float *__restrict__ in, int cin, D3 d, const float *__restrict__ gout,
                int cout, float *__restrict__ part, float *__restrict__ partb) {
     extern __shared__ __align__(16) float wsm[];  // slab [CIB*SLAB] | gout tile [OCB][1024]
     float *slab = wsm;
     float(*gs)[TV * TY * TX] = reinterpret_cast<float(*)[TV * TY * TX]>(wsm + CIB * SLAB);
-    const int nbx = gridDim.x;  // blocks over (x, y, z) tiles
     const int ntx = (d.h + TX - 1) / TX, nty = (d.w + TY - 1) / TY;
     const int blk = blockIdx.x;
     const int bx = blk % ntx, by = (blk / ntx) % nty, bz = blk / (ntx * nty);
     const int x0 = bx * TX, y0 = by * TY, z0 = bz * TV;
     const int o0 = blockIdx.y * OCB, c0 = blockIdx.z * CIB;
     const int nch = min(CIB, cin - c0);
-    stage(slab, in + (int64_t)c0 * d.n, nch, d, x0, y0, z0);
-    for (int i = threadIdx.x; i < OCB * TV * TY * TX; i += NT) {
+    if (threadIdx.x < NT) stage(slab, in + (int64_t)c0 * d.n, nch, d, x0, y0, z0);
+    for (int i = threadIdx.x; i < OCB * TV * TY * TX; i += blockDim.x) {
         const int o = i / (TV * TY * TX), r = i - o * (TV * TY * TX);
         const int v = r / (TY * TX), yy = (r / TX) % TY, xx = r % TX;
         const int x = x0 + xx, y = y0 + yy, z = z0 + v;
@@ -187,38 +192,67 @@ conv3g_wgrad_k(const float *__restrict__ in, int cin, D3 d, const float *__restr
         gs[o][r] = g;
     }
     __syncthreads();
-    // outputs (o, c, t): 8 * nch * 27, strided over the threads
-    const int nout = OCB * nch * 27;
-    for (int k = threadIdx.x; k < nout; k += NT) {
-        const int o = k / (nch * 27), c = (k / 27) % nch, t = k % 27;
-        const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
-        const float *sl = slab + c * SLAB + (dz * HY + dy) * HX + dx;
-        const float *gv = gs[o];
-        float acc = 0.0f;
-        for (int v = 0; v < TV; ++v)
-            for (int yy = 0; yy < TY; ++yy) {
-                const float *srow = sl + (v * HY + yy) * HX;
-                const float *grow = gv + (v * TY + yy) * TX;
-#pragma unroll 8
-                for (int xx = 0; xx < TX; ++xx) acc = fmaf(grow[xx], srow[xx], acc);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float *dstb = part + (((int64_t)blk * gridDim.y + blockIdx.y) * gridDim.z + blockIdx.z) *
+                             (OCB * CIB * 27);
+    for (int it = 0; it < 4; ++it) {
+        const int row = wid * 4 + it;  // (c, dz, dy)
+        const int c = row / 9, dz = (row % 9) / 3, dy = row % 3;
+        float2 acc[3][OCB / 2];
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+            for (int j = 0; j < OCB / 2; ++j) acc[dx][j] = make_float2(0.0f, 0.0f);
+        if (c < nch) {
+#pragma unroll 2
+            for (int vy = 0; vy < TV * TY; ++vy) {
+                const int v = vy / TY, yy = vy % TY;
+                const float *srow = slab + c * SLAB + ((v + dz) * HY + yy + dy) * HX + lane;
+                const float sv[3] = {srow[0], srow[1], srow[2]};
+                float2 g2[OCB / 2];
+#pragma unroll
+                for (int j = 0; j < OCB / 2; ++j)
+                    g2[j] = make_float2(gs[2 * j][vy * TX + lane], gs[2 * j + 1][vy * TX + lane]);
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx) {
+                    const float2 s2 = make_float2(sv[dx], sv[dx]);
+#pragma unroll
+                    for (int j = 0; j < OCB / 2; ++j) acc[dx][j] = __ffma2_rn(g2[j], s2, acc[dx][j]);
+                }
             }
-        part[(((int64_t)blk * gridDim.y + blockIdx.y) * gridDim.z + blockIdx.z) * (OCB * CIB * 27) +
-             (o * CIB + c) * 27 + t] = acc;
+        }
+        // warp reduction of the 24 sums (fixed butterfly order)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+            for (int j = 0; j < OCB / 2; ++j) {
+                float ax = acc[dx][j].x, ay = acc[dx][j].y;
+#pragma unroll
+                for (int m = 16; m > 0; m >>= 1) {
+                    ax += __shfl_xor_sync(0xffffffffu, ax, m);
+                    ay += __shfl_xor_sync(0xffffffffu, ay, m);
+                }
+                if (lane == 0) {
+                    const int t = dz * 9 + dy * 3 + dx;
+                    dstb[((2 * j) * CIB + c) * 27 + t] = ax;
+                    dstb[((2 * j + 1) * CIB + c) * 27 + t] = ay;
+                }
+            }
     }
     if (blockIdx.z == 0 && threadIdx.x < OCB) {
-        float s = 0.0f;
-        for (int r = 0; r < TV * TY * TX; ++r) s += gs[threadIdx.x][r];
-        partb[((int64_t)blk * gridDim.y + blockIdx.y) * OCB + threadIdx.x] = s;
+        float sb = 0.0f;
+        for (int r = 0; r < TV * TY * TX; ++r) sb += gs[threadIdx.x][r];
+        partb[((int64_t)blk * gridDim.y + blockIdx.y) * OCB + threadIdx.x] = sb;
     }
-    (void)nbx;
 }
 
-// fixed-order sum of the per-block partials into gk[o][c][t] (+=) and gb[o]
+// fixed-order sum of the per-CTA partials into gk[o][c][t] (+=) and gb[o]
+// for many partials: one 256-thread block per output value
 __global__ void __launch_bounds__(256)
-conv3g_wgrad_final_k(const float *__restrict__ part, const float *__restrict__ partb, int nblk,
-                     int noy, int ncz, int cout, int cin, float *__restrict__ gk,
-                     float *__restrict__ gb) {
-    const int idx = blockIdx.x;  // (o, c, t) or bias slots at the end
+conv3g_wgrad_tree_k(const float *__restrict__ part, const float *__restrict__ partb, int nblk,
+                    int noy, int ncz, int cout, int cin, float *__restrict__ gk,
+                    float *__restrict__ gb) {
+    const int idx = blockIdx.x;
     const int nw = cout * cin * 27;
     float v = 0.0f;
     if (idx < nw) {
@@ -230,19 +264,41 @@ conv3g_wgrad_final_k(const float *__restrict__ part, const float *__restrict__ p
         const int o = idx - nw, oy = o / OCB, ol = o % OCB;
         for (int b = threadIdx.x; b < nblk; b += 256) v += partb[((int64_t)b * noy + oy) * OCB + ol];
     }
-    __shared__ float s[256];
-    s[threadIdx.x] = v;
+    __shared__ float sm[256];
+    sm[threadIdx.x] = v;
     __syncthreads();
     for (int m = 128; m > 0; m >>= 1) {
-        if (threadIdx.x < m) s[threadIdx.x] += s[threadIdx.x + m];
+        if (threadIdx.x < m) sm[threadIdx.x] += sm[threadIdx.x + m];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
         if (idx < nw) {
-            if (gk) gk[idx] += s[0];
+            if (gk) gk[idx] += sm[0];
         } else if (gb) {
-            gb[idx - nw] += s[0];
+            gb[idx - nw] += sm[0];
         }
+    }
+}
+
+// few partials: one thread per output value
+__global__ void __launch_bounds__(256)
+conv3g_wgrad_final_k(const float *__restrict__ part, const float *__restrict__ partb, int nblk,
+                     int noy, int ncz, int cout, int cin, float *__restrict__ gk,
+                     float *__restrict__ gb) {
+    const int idx = blockIdx.x * 256 + threadIdx.x;
+    const int nw = cout * cin * 27;
+    if (idx >= nw + cout) return;
+    float v = 0.0f;
+    if (idx < nw) {
+        const int o = idx / (cin * 27), c = (idx / 27) % cin, t = idx % 27;
+        const int oy = o / OCB, ol = o % OCB, cz = c / CIB, cl = c % CIB;
+        for (int b = 0; b < nblk; ++b)
+            v += part[(((int64_t)b * noy + oy) * ncz + cz) * (OCB * CIB * 27) + (ol * CIB + cl) * 27 + t];
+        if (gk) gk[idx] += v;
+    } else {
+        const int o = idx - nw, oy = o / OCB, ol = o % OCB;
+        for (int b = 0; b < nblk; ++b) v += partb[((int64_t)b * noy + oy) * OCB + ol];
+        if (gb) gb[o] += v;
     }
 }
 
@@ -468,21 +524,25 @@ mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 dd, const float *w, 
         MDG_LAUNCHED();
     }
     if (gw || gb) {
-        const int nblk = ((d.h + TX - 1) / TX) * ((d.w + TY - 1) / TY) * ((d.l + TV - 1) / TV);
+        const int ntiles = ((d.h + TX - 1) / TX) * ((d.w + TY - 1) / TY) * ((d.l + TV - 1) / TV);
         const int noy = (oc + OCB - 1) / OCB, ncz = (ic + CIB - 1) / CIB;
+        const int nblk = ntiles;  // one CTA per voxel block
         Scratch part;
         const size_t np = (size_t)nblk * noy * ncz * OCB * CIB * 27;
         MDG_CUDA_TRY(part.alloc((np + (size_t)nblk * noy * OCB) * sizeof(float), st));
-        MDG_CUDA_TRY(cudaMemsetAsync(part.p, 0, (np + (size_t)nblk * noy * OCB) * sizeof(float), st));
         float *pb = part.as<float>() + np;
         const size_t smem = (size_t)(CIB * SLAB + OCB * TV * TY * TX) * sizeof(float);
         MDG_CUDA_TRY(cudaFuncSetAttribute(conv3g_wgrad_k,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        conv3g_wgrad_k<<<dim3(nblk, noy, ncz), NT, smem, st>>>(in, ic, d, gout, oc,
-                                                               part.as<float>(), pb);
+        conv3g_wgrad_k<<<dim3(nblk, noy, ncz), WG_NT, smem, st>>>(in, ic, d, gout, oc,
+                                                                  part.as<float>(), pb);
         MDG_LAUNCHED();
-        conv3g_wgrad_final_k<<<oc * ic * 27 + oc, 256, 0, st>>>(part.as<float>(), pb, nblk, noy,
-                                                                ncz, oc, ic, gw, gb);
+        if (nblk >= 64)
+            conv3g_wgrad_tree_k<<<oc * ic * 27 + oc, 256, 0, st>>>(part.as<float>(), pb, nblk,
+                                                                   noy, ncz, oc, ic, gw, gb);
+        else
+            conv3g_wgrad_final_k<<<(oc * ic * 27 + oc + 255) / 256, 256, 0, st>>>(
+                part.as<float>(), pb, nblk, noy, ncz, oc, ic, gw, gb);
         MDG_LAUNCHED();
     }
     return MDG_OK;

@@ -724,6 +724,36 @@ class Encoder:
         _check(self._L.mdg_encoder_backward(self._h, gp, gb, _ptr(gimage), _stream()))
 
 
+def init_model(seed=42, base_channels=8, heads=(8, 4, 2, 1, 1), head_dim=6):
+    """init_model(ModelConfig::small_preset(), seed) (engine.hpp:143-166): the
+    75 parameter tensors in ModelParams::all_tensors order, drawn from the
+    reference's Rng stream in the reference's order (bit-identical values).
+    Host (CPU) tensors; move them to the device for ops.Model."""
+    r = Rng(seed)
+    out = []
+
+    def kaiming(oc, ic):  # make_conv_block (encoder.hpp:52-57)
+        bound = (6.0 / (ic * 27.0)) ** 0.5
+        return r.uniform((oc, ic, 3, 3, 3), -bound, bound)
+
+    for k in range(5):
+        c = base_channels << k
+        cin = 1 if k == 0 else base_channels << (k - 1)
+        w1 = kaiming(c, cin)
+        w2 = kaiming(c, c)
+        out += [w1, torch.zeros(c), torch.ones(c), torch.zeros(c),
+                w2, torch.zeros(c), torch.ones(c), torch.zeros(c)]
+    for k in range(5):
+        cin = base_channels << (4 - k)
+        S = heads[k]
+        K = S * head_dim
+        pw = r.normal((K, cin), 0.0, 1e-5)          # make_projection_params
+        rh = r.normal((3, 3 * S, 3, 3, 3), 0.0, 1e-5)  # make_reghead_params
+        out += [pw, torch.zeros(K), torch.ones(K), torch.zeros(K), torch.zeros(S, 27), rh,
+                torch.zeros(3)]
+    return out
+
+
 class Model:
     """ModelParams (engine.hpp:114-140) of the small preset as device tensors,
     in the ModelParams::all_tensors order (5 encoder blocks, then 5 decoder

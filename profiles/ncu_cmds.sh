@@ -4,7 +4,7 @@
 RX=${1:-'modet|warp_fwd_k|warp_bwd_k'}
 SKIP=${2:-15}
 CNT=${3:-5}
-CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-pyramid"
+CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-pyramid --no-po"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
