@@ -169,7 +169,7 @@ conv3g_k(const float *__restrict__ in, int cin, D3 d, const float *__restrict__ 
 // on channel pairs); the warp reduces the 24 sums at the end of the row set.
 constexpr int WG_NT = 288;  // 9 warps x 4 kernel rows = 36 = CIB * 9
 
-__global__ void __launch_bounds__(WG_NT)
+__global__ void __launch_bounds__(WG_NT, 3)
 conv3g_wgrad_k(const float *__restrict__ in, int cin, D3 d, const float *__restrict__ gout,
                int cout, float *__restrict__ part, float *__restrict__ partb) {
     extern __shared__ __align__(16) float wsm[];  // slab [CIB*SLAB] | gout tile [OCB][1024]
@@ -204,7 +204,6 @@ conv3g_wgrad_k(const float *__restrict__ in, int cin, D3 d, const float *__restr
 #pragma unroll
             for (int j = 0; j < OCB / 2; ++j) acc[dx][j] = make_float2(0.0f, 0.0f);
         if (c < nch) {
-#pragma unroll 2
             for (int vy = 0; vy < TV * TY; ++vy) {
                 const int v = vy / TY, yy = vy % TY;
                 const float *srow = slab + c * SLAB + ((v + dz) * HY + yy + dy) * HX + lane;

@@ -20,3 +20,7 @@ tot = sum(agg.values())
 for k, v in sorted(agg.items(), key=lambda x: -x[1])[:22]:
     print(f"{k:50s} {cnt[k]:4d} {v/1e3:8.2f} ms {100*v/tot:5.1f}%")
 print(f"total {tot/1e3:.2f} ms")
+if os.environ.get("EVENTS"):
+    for ev in prof.events():
+        if ev.device_type.name == "CUDA" and os.environ["EVENTS"] in ev.name:
+            print(f"  {ev.name[:50]:50s} {ev.device_time:9.1f} us")
