@@ -108,6 +108,8 @@ class _Lib:
             self._encode = sig("encode", ii, _f, ii, ii, ii, _f, pp, pp, _f, _f)
             self._loss_step = sig("loss_step", ii, _f, _f, ii, ii, ii, _f, C.c_float, ii,
                                   C.POINTER(dd), _f, _f)
+            self._po = sig("pairwise_optimize", ii, _f, _f, _i, _i, ii, ii, ii, _f, ii, dd, dd,
+                           ii, C.POINTER(dd), C.POINTER(dd), _f)
             self._tloss = sig("total_loss", ii, _f, _f, _f, ii, ii, ii, ii, C.c_float, _f, _f,
                               _f, _f)
             self._lpc = sig("level_param_count", i64, ii, ii, ii, ii)
@@ -276,6 +278,20 @@ class _Lib:
         if rc:
             raise RuntimeError(self._perr().decode())
         return loss.value, gp, phi
+
+    def pairwise_optimize(self, fixed, moving, lf, lm, packed, iters, lr=1e-4, lam=1.0,
+                          window=9):
+        """pairwise_optimize (engine.hpp:377-411): (loss_trace, dice_trace, phi)."""
+        l, w, h = fixed.shape[1:]
+        lt = (C.c_double * (iters + 1))()
+        dt = (C.c_double * (iters + 1))()
+        phi = np.zeros((3, l, w, h), np.float32)
+        ip = lambda a: np.ascontiguousarray(a, np.int32).ctypes.data_as(_i)  # noqa: E731
+        rc = self._po(_fp(fixed), _fp(moving), ip(lf), ip(lm), h, w, l, _fp(packed), iters, lr,
+                      lam, window, lt, dt, _fp(phi))
+        if rc:
+            raise RuntimeError(self._perr().decode())
+        return list(lt), list(dt), phi
 
     def level_param_count(self, C_, S, hd, nb=3):
         return int(self._lpc(C_, S, hd, nb))

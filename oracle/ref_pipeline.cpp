@@ -329,4 +329,35 @@ int mdr_loss_step(const float *fixed, const float *moving, int h, int w, int l,
     return 0;
 }
 
+// pairwise_optimize (engine.hpp:377-411) from the packed model: loss and
+// Dice traces (iters + 1 entries each) and the final phi
+int mdr_pairwise_optimize(const float *fixed, const float *moving, const int *labels_fixed,
+                          const int *labels_moving, int h, int w, int l, const float *packed,
+                          int iters, double lr, double lambda, int window, double *loss_trace,
+                          double *dice_trace, float *phi) {
+    try {
+        ModelParams<float> mp = init_model<float>(ModelConfig::small_preset(), 1);
+        load_params(mp, packed);
+        Volume f(D3(h, w, l)), m(D3(h, w, l));
+        std::memcpy(f.data.data(), fixed, f.data.size() * sizeof(float));
+        std::memcpy(m.data.data(), moving, m.data.size() * sizeof(float));
+        LabelVolume lf(D3(h, w, l)), lm(D3(h, w, l));
+        std::memcpy(lf.data.data(), labels_fixed, lf.data.size() * sizeof(int));
+        std::memcpy(lm.data.data(), labels_moving, lm.data.size() * sizeof(int));
+        OptimConfig oc;
+        oc.po_iters = iters;
+        oc.lr_init = lr;
+        oc.lambda = lambda;
+        oc.ncc_window = window;
+        PoResult r = pairwise_optimize(f, m, mp, oc, &lf, &lm);
+        for (size_t i = 0; i < r.loss_trace.size(); ++i) loss_trace[i] = r.loss_trace[i];
+        for (size_t i = 0; i < r.dice_trace.size(); ++i) dice_trace[i] = r.dice_trace[i];
+        std::memcpy(phi, r.reg.phi.data.data(), r.reg.phi.data.size() * sizeof(float));
+    } catch (const std::exception &e) {
+        g_perr = e.what();
+        return 1;
+    }
+    return 0;
+}
+
 }  // extern "C"

@@ -807,6 +807,26 @@ class Model:
         self.opt.step(lr, self.grads)
         return terms, phi
 
+    def pairwise_optimize(self, fixed, moving, iters=50, lr=1e-4, labels_fixed=None,
+                          labels_moving=None):
+        """pairwise_optimize (engine.hpp:377-411): `iters` updates then a final
+        evaluation; returns (loss_trace, dice_trace, phi) like PoResult."""
+        loss_trace, dice_trace = [], []
+        with_dice = labels_fixed is not None and labels_moving is not None
+        phi = None
+        for i in range(iters + 1):
+            last = i == iters
+            terms, phi = self.loss_step(fixed, moving, backward=not last)
+            loss = float(terms[0])  # synchronises: the reference checks the loss
+            if not (loss == loss and abs(loss) != float("inf")):
+                raise NumericError(f"optimization: non-finite loss ({loss})")
+            loss_trace.append(loss)
+            if with_dice:
+                dice_trace.append(mean_dice(labels_fixed, warp_labels(labels_moving, phi)))
+            if not last:
+                self.opt.step(lr, self.grads)
+        return loss_trace, dice_trace, phi
+
 
 def launch_count() -> int:
     return int(_capi.lib().mdg_launch_count())
