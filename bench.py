@@ -409,6 +409,12 @@ def run_po(dev, world, pairs=0, reps=5):
         ti.append(e[0].elapsed_time(e[1]))
         tf.append(e[1].elapsed_time(e[2]))
     it_ms, fwd_ms = statistics.median(ti), statistics.median(tf)
+    if world > 1:  # the slowest rank sets the pair rate
+        import torch.distributed as dist
+
+        t = torch.tensor([it_ms, fwd_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        it_ms, fwd_ms = float(t[0].item()), float(t[1].item())
     out = {"workload": "PO of the small-preset model at 160x192x224 (synthetic pair, "
                        "init_model(42) weights)",
            "iter_ms": round(it_ms, 3), "final_forward_ms": round(fwd_ms, 3),
