@@ -247,6 +247,36 @@ mdg_status mdg_encoder_forward(mdg_encoder *e, const float *image,
 mdg_status mdg_encoder_backward(mdg_encoder *e, const float *const *gfeatures,
                                 const mdg_block_grads *grads, float *gimage, void *stream);
 
+/* ========================== whole model (§8f) =============================
+ * ModelParams of ModelConfig::small_preset (engine.hpp:38-44, 114-140) and
+ * one run_loss_step (engine.hpp:316-340) / Adam update (engine.hpp:389-398)
+ * as one native object: encoder x2 -> decoding pyramid -> total loss, the
+ * backward into the 75 parameter gradients, and AdamOptimizer::step.  The
+ * 75 tensors follow ModelParams::all_tensors (engine.hpp:121-133). */
+typedef struct mdg_model mdg_model;
+/* number of parameter tensors (75) and, if `sizes` is non-NULL, the element
+ * count of each; returns the total element count */
+int64_t mdg_model_param_count(int *ntensors, int64_t *sizes);
+/* init_model(small_preset, seed) (engine.hpp:143-166) into HOST buffers
+ * params_host[75] — bit-identical to the reference's Rng draws */
+mdg_status mdg_model_init(uint64_t seed, float *const *params_host);
+/* params[75]: DEVICE tensors, caller-owned, updated in place by adam_step.
+ * lambda / ncc_window: LossConfig (objective.hpp:21-31).  check_finite: as
+ * mdg_pyramid_config::check_finite. */
+mdg_status mdg_model_create(mdg_dims3 d, float *const *params, float lambda, int ncc_window,
+                            int check_finite, mdg_model **out);
+void mdg_model_destroy(mdg_model *m);
+/* the 75 device gradient tensors (valid until destroy) */
+float *const *mdg_model_grads(mdg_model *m);
+/* fixed, moving: device {n}.  terms (device, 3 floats, nullable) <- {total,
+ * ncc, reg}; phi (device {3, n}, nullable) <- the field.  backward != 0 also
+ * zeroes and fills the gradients. */
+mdg_status mdg_model_loss_step(mdg_model *m, const float *fixed, const float *moving,
+                               int backward, float *terms, float *phi, void *stream);
+/* AdamOptimizer::step (engine.hpp:268-298; beta 0.9/0.999, eps 1e-8) over all
+ * 75 tensors with the gradients of the last backward */
+mdg_status mdg_model_adam_step(mdg_model *m, double lr, void *stream);
+
 /* ======================== decoding pyramid driver ========================
  * The decoder half of build_pipeline (engine.hpp:179-219) on device-resident
  * encoder features: per level k (coarse -> fine)

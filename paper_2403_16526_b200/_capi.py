@@ -113,6 +113,13 @@ SIGNATURES = {
     "mdg_encoder_destroy": (None, [_p]),
     "mdg_encoder_forward": (_st, [_p, _p, C.POINTER(BlockParams), C.POINTER(_p), _p]),
     "mdg_encoder_backward": (_st, [_p, C.POINTER(_p), C.POINTER(BlockGrads), _p, _p]),
+    "mdg_model_param_count": (C.c_int64, [C.POINTER(_i), C.POINTER(C.c_int64)]),
+    "mdg_model_init": (_st, [C.c_uint64, C.POINTER(_p)]),
+    "mdg_model_create": (_st, [Dims3, C.POINTER(_p), _f, _i, _i, C.POINTER(_p)]),
+    "mdg_model_destroy": (None, [_p]),
+    "mdg_model_grads": (C.POINTER(_p), [_p]),
+    "mdg_model_loss_step": (_st, [_p, _p, _p, _i, _p, _p, _p]),
+    "mdg_model_adam_step": (_st, [_p, C.c_double, _p]),
     "mdg_pyramid_create": (_st, [C.POINTER(PyramidConfig), C.POINTER(_p)]),
     "mdg_pyramid_destroy": (None, [_p]),
     "mdg_pyramid_forward": (_st, [_p, C.POINTER(_p), C.POINTER(_p), C.POINTER(LevelParams), _p,

@@ -1,0 +1,252 @@
+// model_driver.cu — the whole registration model as one native object:
+// run_loss_step (engine.hpp:316-340) and pairwise_optimize's update
+// (engine.hpp:389-398) composed from the encoder, pyramid, loss and Adam entry
+// points, with no framework underneath: parameters, gradients, Adam moments
+// and every intermediate live in device memory owned by the object or the
+// caller; one stream; the loss is the only value read back (on request).
+//
+// Parameters follow ModelParams::all_tensors (engine.hpp:121-133): five
+// encoder blocks {w1,b1,n1g,n1b,w2,b2,n2g,n2b}, then five decoder levels,
+// coarse -> fine, {proj.w,proj.b,ln_g,ln_b,bias_b,reghead.w,reghead.b}.
+#include <cmath>
+#include <vector>
+
+#include "mdg_common.cuh"
+
+using namespace mdg;
+
+#define MD_TRY(expr)                      \
+    do {                                  \
+        mdg_status _s = (expr);           \
+        if (_s != MDG_OK) return _s;      \
+    } while (0)
+
+struct mdg_model {
+    mdg_dims3 d;
+    int64_t n = 0;
+    float lambda = 1.0f;
+    int window = 9;
+    std::vector<float *> params;    // 75, caller-owned
+    std::vector<int64_t> sizes;     // elements per tensor
+    std::vector<float *> grads, m, v;  // owned (one arena)
+    void *arena = nullptr;
+    mdg_encoder *enc_f = nullptr, *enc_m = nullptr;
+    mdg_pyramid *pyr = nullptr;
+    std::vector<float *> ff, mf, gf, gm;  // features / their gradients (fine -> coarse)
+    float *phi = nullptr, *gphi = nullptr, *terms = nullptr;
+    int64_t t = 0;
+    double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+};
+
+namespace {
+// small preset (engine.hpp:38-44): base 8, heads {8,4,2,1,1}, hd 6
+constexpr int kBase = 8, kLevels = 5, kHd = 6;
+const int kHeads[kLevels] = {8, 4, 2, 1, 1};
+
+std::vector<int64_t> model_sizes() {
+    std::vector<int64_t> s;
+    for (int k = 0; k < kLevels; ++k) {
+        const int64_t c = kBase << k, cin = k == 0 ? 1 : kBase << (k - 1);
+        s.insert(s.end(), {c * cin * 27, c, c, c, c * c * 27, c, c, c});
+    }
+    for (int k = 0; k < kLevels; ++k) {
+        const int64_t cin = kBase << (kLevels - 1 - k), S = kHeads[k], K = S * kHd;
+        s.insert(s.end(), {K * cin, K, K, K, S * 27, 3 * 3 * S * 27, 3});
+    }
+    return s;
+}
+}  // namespace
+
+extern "C" {
+
+int64_t mdg_model_param_count(int *ntensors, int64_t *sizes) {
+    const auto s = model_sizes();
+    if (ntensors) *ntensors = (int)s.size();
+    int64_t tot = 0;
+    for (size_t i = 0; i < s.size(); ++i) {
+        if (sizes) sizes[i] = s[i];
+        tot += s[i];
+    }
+    return tot;
+}
+
+mdg_status mdg_model_init(uint64_t seed, float *const *params_host) {
+    // init_model(small_preset, seed) (engine.hpp:143-166) on host buffers,
+    // drawn from the reference Rng stream in the reference order
+    MDG_REQUIRE(params_host, "model: null pointer");
+    const auto s = model_sizes();
+    mdg_rng *r = mdg_rng_new(seed);
+    int i = 0;
+    for (int k = 0; k < kLevels; ++k) {
+        const int c = kBase << k, cin = k == 0 ? 1 : kBase << (k - 1);
+        const double b1 = std::sqrt(6.0 / (cin * 27.0)), b2 = std::sqrt(6.0 / (c * 27.0));
+        mdg_rng_fill_uniform(r, params_host[i], s[i], -b1, b1);
+        for (int j = 1; j < 4; ++j)
+            for (int64_t e = 0; e < s[i + j]; ++e) params_host[i + j][e] = j == 2 ? 1.0f : 0.0f;
+        mdg_rng_fill_uniform(r, params_host[i + 4], s[i + 4], -b2, b2);
+        for (int j = 5; j < 8; ++j)
+            for (int64_t e = 0; e < s[i + j]; ++e) params_host[i + j][e] = j == 6 ? 1.0f : 0.0f;
+        i += 8;
+    }
+    for (int k = 0; k < kLevels; ++k) {
+        mdg_rng_fill_normal(r, params_host[i], s[i], 0.0, 1e-5);
+        for (int j = 1; j < 5; ++j)
+            for (int64_t e = 0; e < s[i + j]; ++e) params_host[i + j][e] = j == 2 ? 1.0f : 0.0f;
+        mdg_rng_fill_normal(r, params_host[i + 5], s[i + 5], 0.0, 1e-5);
+        for (int64_t e = 0; e < s[i + 6]; ++e) params_host[i + 6][e] = 0.0f;
+        i += 7;
+    }
+    mdg_rng_free(r);
+    return MDG_OK;
+}
+
+mdg_status mdg_model_create(mdg_dims3 d, float *const *params, float lambda, int ncc_window,
+                            int check_finite, mdg_model **out) {
+    MDG_REQUIRE(params && out, "model: null pointer");
+    *out = nullptr;
+    MDG_REQUIRE(lambda >= 0.0f, "loss: lambda must be >= 0");
+    MDG_REQUIRE(ncc_window >= 3 && ncc_window % 2 == 1, "loss: ncc_window must be odd and >= 3");
+    mdg_model *m = new mdg_model;
+    m->d = d;
+    m->n = nvox(d);
+    m->lambda = lambda;
+    m->window = ncc_window;
+    m->sizes = model_sizes();
+    m->params.assign(params, params + m->sizes.size());
+    auto fail = [&](mdg_status st) {
+        mdg_model_destroy(m);
+        return st;
+    };
+    mdg_status st = mdg_encoder_create(d, kBase, kLevels, 0.2f, &m->enc_f);
+    if (st == MDG_OK) st = mdg_encoder_create(d, kBase, kLevels, 0.2f, &m->enc_m);
+    if (st != MDG_OK) return fail(st);
+    mdg_pyramid_config pc{};
+    pc.levels = kLevels;
+    std::vector<mdg_dims3> dims{d};
+    for (int k = 1; k < kLevels; ++k) {
+        const mdg_dims3 p = dims.back();
+        dims.push_back(mdg_dims3{(p.h + 1) / 2, (p.w + 1) / 2, (p.l + 1) / 2});
+    }
+    for (int k = 0; k < kLevels; ++k) {  // coarse -> fine
+        pc.heads[k] = kHeads[k];
+        pc.channels[k] = kBase << (kLevels - 1 - k);
+        pc.dims[k] = dims[kLevels - 1 - k];
+    }
+    pc.head_dim = kHd;
+    pc.neighborhood = 3;
+    pc.diffeomorphic = 0;
+    pc.ss_steps = 7;
+    pc.check_finite = check_finite;
+    if ((st = mdg_pyramid_create(&pc, &m->pyr)) != MDG_OK) return fail(st);
+    // arena: grads + Adam moments + features + their grads + phi/gphi/terms
+    int64_t tot = 0;
+    for (int64_t s : m->sizes) tot += (s + 63) / 64 * 64;
+    int64_t feat = 0;
+    for (int k = 0; k < kLevels; ++k) feat += (int64_t)(kBase << k) * nvox(dims[k]) + 64;
+    const size_t bytes = ((size_t)3 * tot + 4 * (size_t)feat + 6 * (size_t)m->n + 64) * sizeof(float);
+    cudaError_t e = cudaMalloc(&m->arena, bytes);
+    if (e != cudaSuccess) return fail(status_from_cuda(e, "model arena"));
+    cudaMemset(m->arena, 0, bytes);
+    float *p = static_cast<float *>(m->arena);
+    for (auto *vec : {&m->grads, &m->m, &m->v})
+        for (int64_t s : m->sizes) {
+            vec->push_back(p);
+            p += (s + 63) / 64 * 64;
+        }
+    for (auto *vec : {&m->ff, &m->mf, &m->gf, &m->gm})
+        for (int k = 0; k < kLevels; ++k) {
+            vec->push_back(p);
+            p += (int64_t)(kBase << k) * nvox(dims[k]) + 64;
+        }
+    m->phi = p;
+    p += 3 * m->n;
+    m->gphi = p;
+    p += 3 * m->n;
+    m->terms = p;
+    *out = m;
+    return MDG_OK;
+}
+
+void mdg_model_destroy(mdg_model *m) {
+    if (!m) return;
+    if (m->enc_f) mdg_encoder_destroy(m->enc_f);
+    if (m->enc_m) mdg_encoder_destroy(m->enc_m);
+    if (m->pyr) mdg_pyramid_destroy(m->pyr);
+    if (m->arena) cudaFree(m->arena);
+    delete m;
+}
+
+float *const *mdg_model_grads(mdg_model *m) { return m ? m->grads.data() : nullptr; }
+
+mdg_status mdg_model_loss_step(mdg_model *m, const float *fixed, const float *moving,
+                               int backward, float *terms, float *phi, void *stream) {
+    MDG_REQUIRE(m && fixed && moving, "model: null pointer");
+    cudaStream_t st = S_(stream);
+    std::vector<mdg_block_params> bp(kLevels);
+    std::vector<mdg_block_grads> bg(kLevels);
+    std::vector<mdg_level_params> lp(kLevels);
+    std::vector<mdg_level_grads> lg(kLevels);
+    for (int k = 0; k < kLevels; ++k) {
+        float *const *P = m->params.data() + 8 * k;
+        float *const *G = m->grads.data() + 8 * k;
+        bp[k] = mdg_block_params{P[0], P[1], P[2], P[3], P[4], P[5], P[6], P[7]};
+        bg[k] = mdg_block_grads{G[0], G[1], G[2], G[3], G[4], G[5], G[6], G[7]};
+        float *const *Q = m->params.data() + 40 + 7 * k;
+        float *const *H = m->grads.data() + 40 + 7 * k;
+        lp[k] = mdg_level_params{Q[0], Q[1], Q[2], Q[3], Q[4], Q[5], Q[6]};
+        lg[k] = mdg_level_grads{H[0], H[1], H[2], H[3], H[4], H[5], H[6]};
+    }
+    // run_loss_step: encoder x2 -> pyramid (coarse -> fine) -> loss
+    MD_TRY(mdg_encoder_forward(m->enc_f, fixed, bp.data(), m->ff.data(), st));
+    MD_TRY(mdg_encoder_forward(m->enc_m, moving, bp.data(), m->mf.data(), st));
+    std::vector<const float *> fc(kLevels), mc(kLevels);
+    for (int k = 0; k < kLevels; ++k) {
+        fc[k] = m->ff[kLevels - 1 - k];
+        mc[k] = m->mf[kLevels - 1 - k];
+    }
+    MD_TRY(mdg_pyramid_forward(m->pyr, fc.data(), mc.data(), lp.data(), m->phi, nullptr, st));
+    MD_TRY(mdg_total_loss_fwd(fixed, moving, m->phi, m->d, m->window, m->lambda, m->terms,
+                              nullptr, st));
+    if (terms)
+        MDG_CUDA_TRY(cudaMemcpyAsync(terms, m->terms, 3 * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    if (phi)
+        MDG_CUDA_TRY(cudaMemcpyAsync(phi, m->phi, 3 * m->n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    if (!backward) return MDG_OK;
+    // zero_grads + tape backward (engine.hpp:332-334)
+    for (size_t i = 0; i < m->grads.size(); ++i)
+        MDG_CUDA_TRY(cudaMemsetAsync(m->grads[i], 0, m->sizes[i] * sizeof(float), st));
+    MDG_CUDA_TRY(cudaMemsetAsync(m->gphi, 0, 3 * m->n * sizeof(float), st));
+    MD_TRY(mdg_total_loss_bwd(fixed, moving, m->phi, m->d, m->window, m->lambda, 1.0f, m->gphi,
+                              nullptr, st));
+    std::vector<float *> gfc(kLevels), gmc(kLevels);
+    for (int k = 0; k < kLevels; ++k) {
+        gfc[k] = m->gf[kLevels - 1 - k];
+        gmc[k] = m->gm[kLevels - 1 - k];
+    }
+    // feature gradients accumulate: clear them first
+    {
+        mdg_dims3 dk = m->d;
+        for (int k = 0; k < kLevels; ++k) {
+            const size_t bytes = (size_t)(kBase << k) * nvox(dk) * sizeof(float);
+            MDG_CUDA_TRY(cudaMemsetAsync(m->gf[k], 0, bytes, st));
+            MDG_CUDA_TRY(cudaMemsetAsync(m->gm[k], 0, bytes, st));
+            dk = mdg_dims3{(dk.h + 1) / 2, (dk.w + 1) / 2, (dk.l + 1) / 2};
+        }
+    }
+    MD_TRY(mdg_pyramid_backward(m->pyr, m->gphi, lg.data(), gfc.data(), gmc.data(), st));
+    std::vector<const float *> gfe(m->gf.begin(), m->gf.end()), gme(m->gm.begin(), m->gm.end());
+    MD_TRY(mdg_encoder_backward(m->enc_f, gfe.data(), bg.data(), nullptr, st));
+    MD_TRY(mdg_encoder_backward(m->enc_m, gme.data(), bg.data(), nullptr, st));
+    return MDG_OK;
+}
+
+mdg_status mdg_model_adam_step(mdg_model *m, double lr, void *stream) {
+    MDG_REQUIRE(m, "model: null pointer");
+    ++m->t;
+    for (size_t i = 0; i < m->params.size(); ++i)
+        MD_TRY(mdg_adam_step(m->params[i], m->grads[i], m->m[i], m->v[i], m->sizes[i], lr,
+                             m->beta1, m->beta2, m->eps, m->t, stream));
+    return MDG_OK;
+}
+
+}  // extern "C"

@@ -828,6 +828,103 @@ class Model:
         return loss_trace, dice_trace, phi
 
 
+def init_model_native(seed=42):
+    """mdg_model_init: init_model(small_preset, seed) drawn by libmdg on the
+    host (no device needed); the same 75 tensors as init_model()."""
+    L = _capi.lib()
+    nt = C.c_int(0)
+    L.mdg_model_param_count(C.byref(nt), None)
+    sizes = (C.c_int64 * nt.value)()
+    L.mdg_model_param_count(None, sizes)
+    shapes = [t.shape for t in _preset_meta()]
+    out = [torch.empty(int(s), dtype=torch.float32) for s in sizes]
+    ptrs = (C.c_void_p * nt.value)(*[t.data_ptr() for t in out])
+    _check(L.mdg_model_init(seed, ptrs))
+    return [t.view(s) for t, s in zip(out, shapes)]
+
+
+def _preset_meta(base_channels=8, heads=(8, 4, 2, 1, 1), head_dim=6):
+    out = []
+    for k in range(5):
+        c = base_channels << k
+        cin = 1 if k == 0 else base_channels << (k - 1)
+        out += [torch.empty(c, cin, 3, 3, 3, device="meta")] + \
+               [torch.empty(c, device="meta")] * 3 + \
+               [torch.empty(c, c, 3, 3, 3, device="meta")] + [torch.empty(c, device="meta")] * 3
+    for k in range(5):
+        cin, S = base_channels << (4 - k), heads[k]
+        K = S * head_dim
+        out += [torch.empty(K, cin, device="meta")] + [torch.empty(K, device="meta")] * 3 + \
+               [torch.empty(S, 27, device="meta"), torch.empty(3, 3 * S, 3, 3, 3, device="meta"),
+                torch.empty(3, device="meta")]
+    return out
+
+
+class NativeModel:
+    """The whole model as libmdg's native object (mdg_model_*): encoder x2 ->
+    pyramid -> loss -> backward -> Adam composed in C++ with no framework
+    underneath.  Same contract as Model; `tensors` are the 75 device
+    parameters (updated in place by po_step)."""
+
+    def __init__(self, tensors, dims, loss: LossConfig = None, check_finite=False):
+        self._L = _capi.lib()
+        self.tensors = list(tensors)
+        if len(self.tensors) != 75:
+            raise InvalidInput("model: expects the 75 ModelParams tensors")
+        self.dims = tuple(int(v) for v in dims)
+        lc = loss or LossConfig()
+        ptrs = (C.c_void_p * 75)(*[_ptr(t) for t in self.tensors])
+        h = C.c_void_p()
+        _check(self._L.mdg_model_create(dims3(dims), ptrs, float(lc.lam), int(lc.ncc_window),
+                                        1 if check_finite else 0, C.byref(h)))
+        self._h = h
+        n = voxel_count(self.dims)
+        dev = self.tensors[0].device
+        self._terms = torch.empty(3, device=dev)
+        self._phi = torch.empty(3, *self.dims[::-1], device=dev)
+        self.n = n
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._L.mdg_model_destroy(h)
+            self._h = None
+
+    @property
+    def grads(self):
+        g = self._L.mdg_model_grads(self._h)
+        out = []
+        for i, t in enumerate(self.tensors):
+            ptr = g[i]
+            out.append(_wrap_device(ptr, t.shape, t.device))
+        return out
+
+    def loss_step(self, fixed, moving, backward=True):
+        _check(self._L.mdg_model_loss_step(self._h, _ptr(fixed, "fixed"), _ptr(moving, "moving"),
+                                           1 if backward else 0, _ptr(self._terms),
+                                           _ptr(self._phi), _stream()))
+        return self._terms.clone(), self._phi.clone()
+
+    def po_step(self, fixed, moving, lr=1e-4):
+        terms, phi = self.loss_step(fixed, moving, backward=True)
+        _check(self._L.mdg_model_adam_step(self._h, float(lr), _stream()))
+        return terms, phi
+
+
+def _wrap_device(ptr, shape, device):
+    """A torch view of libmdg-owned device memory (float32, contiguous); valid
+    while the owning object lives."""
+    n = 1
+    for s in shape:
+        n *= int(s)
+
+    class _A:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+
+    return torch.as_tensor(_A(), device=device).view(shape)
+
+
 def launch_count() -> int:
     return int(_capi.lib().mdg_launch_count())
 

@@ -138,3 +138,55 @@ def test_pairwise_optimization_dice_gate(cuda, ref):
     # rounding-level gradient differences of near-zero gradients):
     # the final field agrees to 1e-2 relative norm
     assert rel_norm(phi_g.cpu().numpy(), phi_r) <= 1e-2
+
+
+def test_native_model_matches_reference_and_python_driver(cuda, ref):
+    """mdg_model_* (the whole loss step + Adam composed in C++) against the
+    reference run_loss_step, and step-for-step against ops.Model."""
+    dims = (16, 16, 16)
+    f, m, lf, lm, gt = ref.synth_pair(dims, seed=3)
+    packed, sizes = perturbed_model(ref, 5)
+    loss_r, gp_r, phi_r = ref.loss_step(f, m, packed, lam=1.0, window=9)
+    fd, md = torch.from_numpy(f).cuda(), torch.from_numpy(m).cuda()
+    nat = ops.NativeModel(device_tensors(packed, sizes), dims)
+    terms, phi = nat.loss_step(fd, md)
+    torch.cuda.synchronize()
+    assert abs(float(terms[0]) - loss_r) <= 1e-4 * abs(loss_r) + 1e-6, (float(terms[0]), loss_r)
+    assert rel_norm(phi.cpu().numpy(), phi_r) <= 1e-4
+    theirs = split(gp_r, sizes)
+    for i, (a, b) in enumerate(zip(nat.grads, theirs)):
+        if i in PRE_NORM_BIAS:
+            continue
+        assert rel_norm(a.cpu().numpy().ravel(), b) <= 1e-3, i
+    # a few Adam iterations: same trajectory as the Python-composed driver
+    py = ops.Model(device_tensors(packed, sizes), dims)
+    for _ in range(3):
+        t_n, _ = nat.po_step(fd, md)
+        t_p, _ = py.po_step(fd, md)
+        assert abs(float(t_n[0]) - float(t_p[0])) <= 1e-5 * abs(float(t_p[0])) + 1e-7
+    tn, phin = nat.loss_step(fd, md, backward=False)
+    tp, phip = py.loss_step(fd, md, backward=False)
+    assert abs(float(tn[0]) - float(tp[0])) <= 1e-5 * abs(float(tp[0])) + 1e-7
+    assert rel_norm(phin.cpu().numpy(), phip.cpu().numpy()) <= 1e-3
+
+
+def test_native_model_rejects_bad_config(cuda, ref):
+    packed, sizes = perturbed_model(ref, 5)
+    params = device_tensors(packed, sizes)
+    with pytest.raises(ops.InvalidInput):
+        ops.NativeModel(params, (8, 8, 8))  # too small for five levels
+    with pytest.raises(ops.InvalidInput):
+        ops.NativeModel(params, (16, 16, 16), loss=ops.LossConfig(ncc_window=4))
+
+
+def test_po_main_cli_runs():
+    """examples/po_main: the C++ PO program (include/mdg.h + libmdg only)."""
+    import json
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(__file__), "..", "examples", "po_main")
+    out = subprocess.run([exe, "32", "32", "32", "--iters", "4", "--quiet"], check=True,
+                         capture_output=True, text=True, timeout=300).stdout
+    rec = json.loads(out.strip().splitlines()[-1])
+    assert rec["iters"] == 4 and rec["params"] > 0 and rec["launches"] > 0
