@@ -232,6 +232,16 @@ typedef struct {
 typedef struct {
     float *w1, *b1, *g1, *be1, *w2, *b2, *g2, *be2; /* accumulated; nullable */
 } mdg_block_grads;
+/* The encoder's conv3 on its own (op_conv3d ops.hpp:137-238, any channel
+ * counts): out {oc, n} = conv(in {ic, n}, w {oc, ic, 3,3,3}) + b.  FMA-
+ * contracted fp32 (relative-norm parity, not bit-exact: the bit-exact
+ * reference-order kernel is mdg_conv3_fwd).  Backward ACCUMULATES gin, gw, gb
+ * (each nullable). */
+mdg_status mdg_encoder_conv3_fwd(const float *in, int ic, mdg_dims3 d, const float *w,
+                                 const float *b, int oc, float *out, void *stream);
+mdg_status mdg_encoder_conv3_bwd(const float *in, int ic, mdg_dims3 d, const float *w, int oc,
+                                 const float *gout, float *gin, float *gw, float *gb,
+                                 void *stream);
 typedef struct mdg_encoder mdg_encoder;
 /* dims of the full-resolution image (>= 16 per axis, encoder.hpp:95-99) */
 mdg_status mdg_encoder_create(mdg_dims3 d, int base_channels, int levels, float slope,

@@ -109,6 +109,8 @@ SIGNATURES = {
     "mdg_sgd_step": (_st, [_p, _p, C.c_int64, C.c_double, _p]),
     "mdg_warp_labels": (_st, [_p, Dims3, _p, _p, _p]),
     "mdg_mean_dice": (_st, [_p, _p, C.c_int64, _i, C.POINTER(C.c_double), _p]),
+    "mdg_encoder_conv3_fwd": (_st, [_p, _i, Dims3, _p, _p, _i, _p, _p]),
+    "mdg_encoder_conv3_bwd": (_st, [_p, _i, Dims3, _p, _i, _p, _p, _p, _p, _p]),
     "mdg_encoder_create": (_st, [Dims3, _i, _i, _f, C.POINTER(_p)]),
     "mdg_encoder_destroy": (None, [_p]),
     "mdg_encoder_forward": (_st, [_p, _p, C.POINTER(BlockParams), C.POINTER(_p), _p]),

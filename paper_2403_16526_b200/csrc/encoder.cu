@@ -13,7 +13,12 @@
 // over shared-memory tiles with a fixed-order cross-block reduction.
 // Accumulation is FMA-contracted: results match the CPU reference to fp32
 // tolerance (tests: relative norm 1e-4).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "mdg_common.cuh"
 
@@ -157,6 +162,145 @@ conv3g_k(const float *__restrict__ in, int cin, D3 d, const float *__restrict__ 
                 *q = ACC ? *q + acc[v][j].y : acc[v][j].y;
             }
         }
+    }
+}
+
+// ---- TMA-staged variant (h % 4 == 0, 16-B aligned planes): the chunk's
+// slab is ONE 4-D box load {40, 10, 6, CIB} (x0-4 .. x0+35 so the start is
+// 16-B aligned; faces and missing channels zero-filled by the TMA unit) and
+// its weights one bulk copy from the blocked layout wB[ob][c][t][8]; two
+// buffers on mbarriers, so staging costs the threads nothing and overlaps
+// the previous chunk's FMAs.
+constexpr int PX = 40, XO = 3;            // TMA row pitch, offset of x0-1
+constexpr int SLABT = HZ * HY * PX;       // one channel
+constexpr int WCH = 27 * OCB;             // weights of one input channel
+constexpr int TBUF = CIB * SLABT + CIB * WCH;  // floats per stage buffer
+constexpr size_t TSMEM = (2 * (size_t)TBUF + 8) * sizeof(float);
+
+__device__ __forceinline__ unsigned s32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void t_wait(uint64_t *b, unsigned phase) {
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(s32(b)), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+
+template <bool ACC>
+__global__ void __launch_bounds__(NT, 2)
+conv3t_k(const __grid_constant__ CUtensorMap map, int cin, D3 d, const float *__restrict__ wB,
+         int cpad, const float *__restrict__ bias, int cout, float *__restrict__ out) {
+    extern __shared__ __align__(128) float tsm[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(tsm + 2 * TBUF);
+    const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+    const int nzb = (d.l + TV - 1) / TV;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int zb = blockIdx.z % nzb, ob = blockIdx.z / nzb;
+    const int z0 = zb * TV, o0 = ob * OCB;
+    const int nck = (cin + CIB - 1) / CIB;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s32(&bar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s32(&bar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int k) {
+        float *b = tsm + (k & 1) * TBUF;
+        uint64_t *mb = &bar[k & 1];
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s32(mb)),
+                     "r"((unsigned)(TBUF * sizeof(float)))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(s32(b)),
+            "l"(&map), "r"(x0 - 4), "r"(y0 - 1), "r"(z0 - 1), "r"(k * CIB), "r"(s32(mb))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];\n" ::"r"(s32(b + CIB * SLABT)),
+            "l"(wB + ((int64_t)ob * cpad + k * CIB) * WCH), "r"((unsigned)(CIB * WCH * sizeof(float))),
+            "r"(s32(mb))
+            : "memory");
+    };
+    if (threadIdx.x == 0) {
+        issue(0);
+        if (nck > 1) issue(1);
+    }
+    float2 acc[TV][OCB / 2];
+#pragma unroll
+    for (int j = 0; j < OCB / 2; ++j) {
+        const float b0 = (!ACC && bias && o0 + 2 * j < cout) ? bias[o0 + 2 * j] : 0.0f;
+        const float b1 = (!ACC && bias && o0 + 2 * j + 1 < cout) ? bias[o0 + 2 * j + 1] : 0.0f;
+#pragma unroll
+        for (int v = 0; v < TV; ++v) acc[v][j] = make_float2(b0, b1);
+    }
+    for (int k = 0; k < nck; ++k) {
+        const float *b = tsm + (k & 1) * TBUF;
+        t_wait(&bar[k & 1], (k >> 1) & 1);
+        const int nch = min(CIB, cin - k * CIB);
+        const float *tp = b + ty * PX + tx + XO;
+        for (int c = 0; c < nch; ++c) {
+            const float *sp = tp + c * SLABT;
+            const float4 *wc = reinterpret_cast<const float4 *>(b + CIB * SLABT + c * WCH);
+#pragma unroll
+            for (int t = 0; t < 27; ++t) {
+                const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
+                const float4 wa = wc[2 * t], wb = wc[2 * t + 1];
+                const float2 w2[4] = {make_float2(wa.x, wa.y), make_float2(wa.z, wa.w),
+                                      make_float2(wb.x, wb.y), make_float2(wb.z, wb.w)};
+#pragma unroll
+                for (int v = 0; v < TV; ++v) {
+                    const float xv = sp[((v + dz) * HY + dy) * PX + dx];
+                    const float2 x2 = make_float2(xv, xv);
+#pragma unroll
+                    for (int j = 0; j < OCB / 2; ++j) acc[v][j] = __ffma2_rn(x2, w2[j], acc[v][j]);
+                }
+            }
+        }
+        __syncthreads();  // every warp is done with buffer k & 1
+        if (threadIdx.x == 0 && k + 2 < nck) issue(k + 2);
+    }
+    const int x = x0 + tx, y = y0 + ty;
+    if (x >= d.h || y >= d.w) return;
+#pragma unroll
+    for (int v = 0; v < TV; ++v) {
+        const int z = z0 + v;
+        if (z >= d.l) break;
+        const int64_t p = ((int64_t)z * d.w + y) * d.h + x;
+#pragma unroll
+        for (int j = 0; j < OCB / 2; ++j) {
+            const int o = o0 + 2 * j;
+            if (o < cout) {
+                float *q = out + (int64_t)o * d.n + p;
+                *q = ACC ? *q + acc[v][j].x : acc[v][j].x;
+            }
+            if (o + 1 < cout) {
+                float *q = out + (int64_t)(o + 1) * d.n + p;
+                *q = ACC ? *q + acc[v][j].y : acc[v][j].y;
+            }
+        }
+    }
+}
+
+// blocked weights for conv3t_k: wB[ob][c][t][j] = w of output ob*8+j, input c
+// (c < cpad, zero-padded), tap t; flip as wprep_k
+__global__ void wprep_blocked_k(const float *__restrict__ w, int oc, int ic, int flip, int cpad,
+                                int nob, float *__restrict__ wB) {
+    const int cin = flip ? oc : ic, cout = flip ? ic : oc;
+    const int total = nob * cpad * WCH;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int j = i % OCB, t = (i / OCB) % 27, c = (i / WCH) % cpad, ob = i / (WCH * cpad);
+        const int o = ob * OCB + j;
+        float v = 0.0f;
+        if (o < cout && c < cin)
+            v = flip ? w[((int64_t)c * ic + o) * 27 + (26 - t)] : w[((int64_t)o * ic + c) * 27 + t];
+        wB[i] = v;
     }
 }
 
@@ -493,14 +637,89 @@ static unsigned grid_for(int64_t n, int per = 256) {
 }
 
 // ---------------------------------------------------------------- internal
+// algorithm choice: the implicit GEMM (encoder_igemm.cu) for wide-channel
+// levels (>= 32 output channels of the pass), the tiled slab kernel otherwise.
+// MDG_ENC_ALGO=tiled|igemm forces one (benchmarking).
+static int enc_algo() {
+    static int a = [] {
+        const char *e = std::getenv("MDG_ENC_ALGO");
+        if (!e) return 0;
+        return std::strcmp(e, "tiled") == 0   ? 1
+               : std::strcmp(e, "igemm") == 0 ? 2
+               : std::strcmp(e, "slab") == 0  ? 3
+                                              : 0;
+    }();
+    return a;
+}
+static bool use_igemm(int cout, int cin, const D3 &d) {
+    if ((int64_t)cin * d.n >= (int64_t(1) << 31)) return false;
+    const int a = enc_algo();
+    return a == 2 || (a == 0 && cout >= 32);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    }();
+    return fn;
+}
+
+// 4-D map {h, w, l, C} with the conv3t_k box {40, 10, 6, CIB}; false when TMA
+// cannot take the volume (row pitch not a multiple of 16 B, misaligned base)
+static bool conv_map(CUtensorMap *m, const float *base, const D3 &d, int C) {
+    if (enc_algo() == 3 || d.h % 4 != 0 || reinterpret_cast<uintptr_t>(base) % 16 != 0 ||
+        !tmap_fn())
+        return false;
+    const cuuint64_t dims[4] = {(cuuint64_t)d.h, (cuuint64_t)d.w, (cuuint64_t)d.l, (cuuint64_t)C};
+    const cuuint64_t strides[3] = {(cuuint64_t)d.h * 4, (cuuint64_t)d.h * d.w * 4,
+                                   (cuuint64_t)d.n * 4};
+    const cuuint32_t box[4] = {PX, HY, HZ, CIB};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    return tmap_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(base), dims,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// conv3t_k launch: blocked weights + the TMA kernel (ACC: accumulate, no bias)
+template <bool ACC>
+static mdg_status conv3t_launch(const CUtensorMap &map, const float *w, int oc, int ic, bool flip,
+                                const D3 &d, const float *bias, float *out, cudaStream_t st) {
+    const int cin = flip ? oc : ic, cout = flip ? ic : oc;
+    const int cpad = (cin + CIB - 1) / CIB * CIB, nob = (cout + OCB - 1) / OCB;
+    Scratch wb;
+    MDG_CUDA_TRY(wb.alloc((size_t)nob * cpad * WCH * sizeof(float), st));
+    wprep_blocked_k<<<grid_for((int64_t)nob * cpad * WCH), 256, 0, st>>>(w, oc, ic, flip ? 1 : 0,
+                                                                         cpad, nob, wb.as<float>());
+    MDG_LAUNCHED();
+    MDG_CUDA_TRY(cudaFuncSetAttribute(conv3t_k<ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)TSMEM));
+    const dim3 g((d.h + TX - 1) / TX, (d.w + TY - 1) / TY, ((d.l + TV - 1) / TV) * nob);
+    conv3t_k<ACC><<<g, NT, TSMEM, st>>>(map, cin, d, wb.as<float>(), cpad, bias, cout, out);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
 mdg_status enc_conv3_fwd(const float *in, int ic, mdg_dims3 dd, const float *w, const float *b,
                          int oc, float *out, cudaStream_t st) {
     const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
-    const int opad = (oc + OCB - 1) / OCB * OCB;
+    const bool ig = use_igemm(oc, ic, d);
+    CUtensorMap map;
+    if (!ig && conv_map(&map, in, d, ic))
+        return conv3t_launch<false>(map, w, oc, ic, false, d, b, out, st);
+    const int tile = ig ? igemm_fwd_bn(oc) : OCB;
+    const int opad = (oc + tile - 1) / tile * tile;
     Scratch wt;
     MDG_CUDA_TRY(wt.alloc((size_t)ic * 27 * opad * sizeof(float), st));
     wprep_k<<<grid_for((int64_t)ic * 27 * opad), 256, 0, st>>>(w, oc, ic, 0, opad, wt.as<float>());
     MDG_LAUNCHED();
+    if (ig) return igemm_conv_fwd(in, ic, dd, wt.as<float>(), opad, b, oc, false, out, st);
     const dim3 g((d.h + TX - 1) / TX, (d.w + TY - 1) / TY, ((d.l + TV - 1) / TV) * (opad / OCB));
     conv3g_k<false><<<g, NT, 0, st>>>(in, ic, d, wt.as<float>(), opad, b, oc, out);
     MDG_LAUNCHED();
@@ -511,17 +730,33 @@ mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 dd, const float *w, 
                          const float *gout, float *gin, float *gw, float *gb, cudaStream_t st) {
     const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
     if (gin) {
-        const int ipad = (ic + OCB - 1) / OCB * OCB;
-        Scratch wt;
-        MDG_CUDA_TRY(wt.alloc((size_t)oc * 27 * ipad * sizeof(float), st));
-        wprep_k<<<grid_for((int64_t)oc * 27 * ipad), 256, 0, st>>>(w, oc, ic, 1, ipad,
-                                                                   wt.as<float>());
-        MDG_LAUNCHED();
-        const dim3 g((d.h + TX - 1) / TX, (d.w + TY - 1) / TY,
-                     ((d.l + TV - 1) / TV) * (ipad / OCB));
-        conv3g_k<true><<<g, NT, 0, st>>>(gout, oc, d, wt.as<float>(), ipad, nullptr, ic, gin);
-        MDG_LAUNCHED();
+        const bool ig = use_igemm(ic, oc, d);
+        CUtensorMap map;
+        if (!ig && conv_map(&map, gout, d, oc)) {
+            const mdg_status s2 = conv3t_launch<true>(map, w, oc, ic, true, d, nullptr, gin, st);
+            if (s2 != MDG_OK) return s2;
+        } else {
+            const int tile = ig ? igemm_fwd_bn(ic) : OCB;
+            const int ipad = (ic + tile - 1) / tile * tile;
+            Scratch wt;
+            MDG_CUDA_TRY(wt.alloc((size_t)oc * 27 * ipad * sizeof(float), st));
+            wprep_k<<<grid_for((int64_t)oc * 27 * ipad), 256, 0, st>>>(w, oc, ic, 1, ipad,
+                                                                       wt.as<float>());
+            MDG_LAUNCHED();
+            if (ig) {
+                const mdg_status s =
+                    igemm_conv_fwd(gout, oc, dd, wt.as<float>(), ipad, nullptr, ic, true, gin, st);
+                if (s != MDG_OK) return s;
+            } else {
+                const dim3 g((d.h + TX - 1) / TX, (d.w + TY - 1) / TY,
+                             ((d.l + TV - 1) / TV) * (ipad / OCB));
+                conv3g_k<true><<<g, NT, 0, st>>>(gout, oc, d, wt.as<float>(), ipad, nullptr, ic,
+                                                 gin);
+                MDG_LAUNCHED();
+            }
+        }
     }
+    if ((gw || gb) && use_igemm(oc, ic, d)) return igemm_conv_wgrad(in, ic, dd, gout, oc, gw, gb, st);
     if (gw || gb) {
         const int ntiles = ((d.h + TX - 1) / TX) * ((d.w + TY - 1) / TY) * ((d.l + TV - 1) / TV);
         const int noy = (oc + OCB - 1) / OCB, ncz = (ic + CIB - 1) / CIB;

@@ -74,6 +74,25 @@ void enc_layout(mdg_encoder *e, Carve2 &cv, mdg_dims3 d0, int base, int levels) 
 
 extern "C" {
 
+mdg_status mdg_encoder_conv3_fwd(const float *in, int ic, mdg_dims3 d, const float *w,
+                                 const float *b, int oc, float *out, void *stream) {
+    MDG_REQUIRE(ic >= 1 && oc >= 1, "conv3: channel counts must be >= 1");
+    MDG_REQUIRE(dims_ok(d), "conv3: invalid dims " + dims_str(d));
+    if (nvox(d) == 0) return MDG_OK;
+    MDG_REQUIRE(in && w && out, "conv3: null pointer");
+    return enc_conv3_fwd(in, ic, d, w, b, oc, out, S_(stream));
+}
+
+mdg_status mdg_encoder_conv3_bwd(const float *in, int ic, mdg_dims3 d, const float *w, int oc,
+                                 const float *gout, float *gin, float *gw, float *gb,
+                                 void *stream) {
+    MDG_REQUIRE(ic >= 1 && oc >= 1, "conv3: channel counts must be >= 1");
+    MDG_REQUIRE(dims_ok(d), "conv3: invalid dims " + dims_str(d));
+    if (nvox(d) == 0) return MDG_OK;
+    MDG_REQUIRE(in && w && gout, "conv3: null pointer");
+    return enc_conv3_bwd(in, ic, d, w, oc, gout, gin, gw, gb, S_(stream));
+}
+
 mdg_status mdg_encoder_create(mdg_dims3 d, int base_channels, int levels, float slope,
                               mdg_encoder **out) {
     MDG_REQUIRE(out, "encoder: null pointer");

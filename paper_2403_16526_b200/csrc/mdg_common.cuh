@@ -154,6 +154,14 @@ mdg_status enc_in_lrelu_bwd(const float *x, const float *gz, int C, int64_t n, c
                             float *gx, float *gg, float *gbeta, cudaStream_t st);
 mdg_status enc_avgpool_fwd(const float *in, int C, mdg_dims3 d, float *out, cudaStream_t st);
 mdg_status enc_avgpool_bwd(const float *gout, int C, mdg_dims3 d, float *gin, cudaStream_t st);
+namespace enc {
+// encoder_igemm.cu: implicit-GEMM conv for the deep levels
+int igemm_fwd_bn(int cout);  // N tile (32 or 64): the weight padding it needs
+mdg_status igemm_conv_fwd(const float *in, int cin, mdg_dims3 d, const float *wT, int opad,
+                          const float *bias, int cout, bool acc_out, float *out, cudaStream_t st);
+mdg_status igemm_conv_wgrad(const float *in, int cin, mdg_dims3 d, const float *gout, int cout,
+                            float *gk, float *gb, cudaStream_t st);
+}  // namespace enc
 
 // sampling.cu: warp kernels over the voxel range [pb, pe) of a volume
 mdg_status warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *field, float *out,
