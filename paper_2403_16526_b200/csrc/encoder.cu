@@ -304,6 +304,200 @@ __global__ void wprep_blocked_k(const float *__restrict__ w, int oc, int ic, int
     }
 }
 
+// ---- TMA-staged kernel gradient for narrow outputs (cout <= 16 per pass of
+// 8).  gk[o][c][t] = sum_p gout[o][p] * in[c][p + off(t)].  A CTA owns a 32x8
+// x-y tile, a z range, 8 output channels and WC input channels; each z step
+// stages ZW planes of gout ({32, 8, ZW, 8} box) and ZW+2 planes of input
+// ({40, 10, ZW+2, WC} box, faces zero-filled) by TMA into a double buffer.
+// Warp (c, dz), lane x: per voxel it reads one new input row triple (the
+// y-sliding window keeps the other two) and the 8 gout values, and issues
+// 36 FFMA2 into 9 taps x 8 channels of register accumulators.  Zero fill
+// makes out-of-volume voxels contribute exactly 0, so there are no bounds
+// checks.  At the end each warp reduces its 72 sums across lanes (fixed
+// butterfly) into a per-CTA partial; a fixed-order pass adds the partials.
+constexpr int ZW = 2;
+template <int WC>
+struct WT {
+    static constexpr int IN = WC * (ZW + 2) * HY * PX;  // input floats per stage
+    static constexpr int GO = OCB * ZW * TY * TX;         // gout floats per stage
+    static constexpr int BUF = IN + GO;
+    static constexpr size_t SMEM = (2 * (size_t)BUF + 8) * sizeof(float);
+    static constexpr int NTH = 3 * WC * 32;
+};
+
+template <int WC>
+__global__ void __launch_bounds__(3 * WC * 32)
+conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap gmap,
+         int cin, int cout, D3 d, int zper, int ncc, float *__restrict__ part,
+         float *__restrict__ partb) {
+    using W = WT<WC>;
+    extern __shared__ __align__(128) float wsm2[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(wsm2 + 2 * W::BUF);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int cl = wid / 3, dz = wid % 3;
+    const int ntx = (d.h + TX - 1) / TX;
+    const int x0 = (blockIdx.x % ntx) * TX, y0 = (blockIdx.x / ntx) * TY;
+    const int zb0 = blockIdx.y * zper, zb1 = min(d.l, zb0 + zper);
+    const int ob = blockIdx.z / ncc, cc = blockIdx.z % ncc;
+    const int c0 = cc * WC;
+    const int nsteps = (zb1 - zb0 + ZW - 1) / ZW;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s32(&bar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s32(&bar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int k) {
+        float *b = wsm2 + (k & 1) * W::BUF;
+        uint64_t *mb = &bar[k & 1];
+        const int z = zb0 + k * ZW;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s32(mb)),
+                     "r"((unsigned)(W::BUF * sizeof(float)))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(s32(b)),
+            "l"(&imap), "r"(x0 - 4), "r"(y0 - 1), "r"(z - 1), "r"(c0), "r"(s32(mb))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(s32(b + W::IN)),
+            "l"(&gmap), "r"(x0), "r"(y0), "r"(z), "r"(ob * OCB), "r"(s32(mb))
+            : "memory");
+    };
+    if (threadIdx.x == 0) {
+        if (nsteps > 0) issue(0);
+        if (nsteps > 1) issue(1);
+    }
+    float2 acc[9][OCB / 2];
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+#pragma unroll
+        for (int j = 0; j < OCB / 2; ++j) acc[k][j] = make_float2(0.0f, 0.0f);
+    float2 gsum[OCB / 2];
+#pragma unroll
+    for (int j = 0; j < OCB / 2; ++j) gsum[j] = make_float2(0.0f, 0.0f);
+    const bool bias_warp = cc == 0 && wid == 0;
+
+    for (int k = 0; k < nsteps; ++k) {
+        const float *b = wsm2 + (k & 1) * W::BUF;
+        t_wait(&bar[k & 1], (k >> 1) & 1);
+        if (c0 + cl < cin) {
+#pragma unroll
+            for (int v = 0; v < ZW; ++v) {
+                const float *ip = b + ((cl * (ZW + 2) + v + dz) * HY) * PX + lane + XO;
+                const float *gp = b + W::IN + (v * TY) * TX + lane;
+                float r0[3], r1[3];
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx) {
+                    r0[dx] = ip[dx];
+                    r1[dx] = ip[PX + dx];
+                }
+#pragma unroll
+                for (int y = 0; y < TY; ++y) {
+                    float r2[3];
+#pragma unroll
+                    for (int dx = 0; dx < 3; ++dx) r2[dx] = ip[(y + 2) * PX + dx];
+                    float2 g2[OCB / 2];
+#pragma unroll
+                    for (int j = 0; j < OCB / 2; ++j)
+                        g2[j] = make_float2(gp[(2 * j) * (ZW * TY * TX) + y * TX],
+                                            gp[(2 * j + 1) * (ZW * TY * TX) + y * TX]);
+#pragma unroll
+                    for (int dx = 0; dx < 3; ++dx) {
+                        const float2 s0 = make_float2(r0[dx], r0[dx]);
+                        const float2 s1 = make_float2(r1[dx], r1[dx]);
+                        const float2 s2 = make_float2(r2[dx], r2[dx]);
+#pragma unroll
+                        for (int j = 0; j < OCB / 2; ++j) {
+                            acc[dx][j] = __ffma2_rn(s0, g2[j], acc[dx][j]);
+                            acc[3 + dx][j] = __ffma2_rn(s1, g2[j], acc[3 + dx][j]);
+                            acc[6 + dx][j] = __ffma2_rn(s2, g2[j], acc[6 + dx][j]);
+                        }
+                    }
+                    if (bias_warp)
+#pragma unroll
+                        for (int j = 0; j < OCB / 2; ++j) gsum[j] = __fadd2_rn(gsum[j], g2[j]);
+#pragma unroll
+                    for (int dx = 0; dx < 3; ++dx) {
+                        r0[dx] = r1[dx];
+                        r1[dx] = r2[dx];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && k + 2 < nsteps) issue(k + 2);
+    }
+    // per-CTA partial: part[((ob*ncc + cc)*nblk + blk)][o][c][t]
+    const int nblk = gridDim.x * gridDim.y, blk = blockIdx.y * gridDim.x + blockIdx.x;
+    float *dst = part + ((int64_t)blockIdx.z * nblk + blk) * (OCB * WC * 27);
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+#pragma unroll
+        for (int j = 0; j < OCB / 2; ++j) {
+            float ax = acc[k][j].x, ay = acc[k][j].y;
+#pragma unroll
+            for (int m = 16; m > 0; m >>= 1) {
+                ax += __shfl_xor_sync(0xffffffffu, ax, m);
+                ay += __shfl_xor_sync(0xffffffffu, ay, m);
+            }
+            if (lane == 0) {
+                const int t = dz * 9 + k;  // k = dy*3 + dx
+                dst[((2 * j) * WC + cl) * 27 + t] = ax;
+                dst[((2 * j + 1) * WC + cl) * 27 + t] = ay;
+            }
+        }
+    if (cc == 0) {
+        if (wid == 0) {
+#pragma unroll
+            for (int j = 0; j < OCB / 2; ++j) {
+                float ax = gsum[j].x, ay = gsum[j].y;
+#pragma unroll
+                for (int m = 16; m > 0; m >>= 1) {
+                    ax += __shfl_xor_sync(0xffffffffu, ax, m);
+                    ay += __shfl_xor_sync(0xffffffffu, ay, m);
+                }
+                if (lane == 0) {
+                    partb[((int64_t)ob * nblk + blk) * OCB + 2 * j] = ax;
+                    partb[((int64_t)ob * nblk + blk) * OCB + 2 * j + 1] = ay;
+                }
+            }
+        }
+    }
+}
+
+// gk[o][c][t] += sum_blk part; gb[o] += sum_blk partb (one warp per value,
+// lanes stride the CTAs, fixed butterfly)
+template <int WC>
+__global__ void __launch_bounds__(256)
+conv3w_sum_k(const float *__restrict__ part, const float *__restrict__ partb, int nblk, int ncc,
+             int cout, int cin, float *__restrict__ gk, float *__restrict__ gb) {
+    const int nw = cout * cin * 27;
+    const int idx = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (idx >= nw + cout) return;
+    float v = 0.0f;
+    if (idx < nw) {
+        const int o = idx / (cin * 27), c = (idx / 27) % cin, t = idx % 27;
+        const int ob = o / OCB, ol = o % OCB, cc = c / WC, cw = c % WC;
+        const float *src = part + (int64_t)(ob * ncc + cc) * nblk * (OCB * WC * 27) +
+                           (ol * WC + cw) * 27 + t;
+        for (int b = lane; b < nblk; b += 32) v += src[(int64_t)b * (OCB * WC * 27)];
+    } else {
+        const int o = idx - nw, ob = o / OCB, ol = o % OCB;
+        for (int b = lane; b < nblk; b += 32) v += partb[((int64_t)ob * nblk + b) * OCB + ol];
+    }
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    if (lane == 0) {
+        if (idx < nw) {
+            if (gk) gk[idx] += v;
+        } else if (gb) {
+            gb[idx - nw] += v;
+        }
+    }
+}
+
 // kernel / bias gradient partials of one voxel block:
 //   part[blk][o][c][t] = sum_p gout[o][p] * in[c][p + off(t)]   (o in the
 //   CTA's 8-channel block, c in its 4-channel block), partb[blk][o] = sum gout.
@@ -637,9 +831,10 @@ static unsigned grid_for(int64_t n, int per = 256) {
 }
 
 // ---------------------------------------------------------------- internal
-// algorithm choice: the implicit GEMM (encoder_igemm.cu) for wide-channel
-// levels (>= 32 output channels of the pass), the tiled slab kernel otherwise.
-// MDG_ENC_ALGO=tiled|igemm forces one (benchmarking).
+// algorithm choice (MDG_ENC_ALGO=tiled|igemm|slab forces one, benchmarking):
+// TMA slab kernels (conv3t_k / conv3w_k), the implicit GEMM
+// (encoder_igemm.cu), or the thread-staged slab kernels (conv3g_k /
+// conv3g_wgrad_k) for volumes TMA cannot tile.
 static int enc_algo() {
     static int a = [] {
         const char *e = std::getenv("MDG_ENC_ALGO");
@@ -651,10 +846,13 @@ static int enc_algo() {
     }();
     return a;
 }
+// auto (measured at the small-preset levels, tools/bench_conv.py): the TMA
+// slab kernels from ~32K voxels up when the rows are 16-B pitched; the
+// implicit GEMM for smaller (deeper) levels with >= 32 output channels.
 static bool use_igemm(int cout, int cin, const D3 &d) {
     if ((int64_t)cin * d.n >= (int64_t(1) << 31)) return false;
     const int a = enc_algo();
-    return a == 2 || (a == 0 && cout >= 32);
+    return a == 2 || (a == 0 && cout >= 32 && (d.n < 32768 || d.h % 4 != 0));
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_fn() {
@@ -704,6 +902,67 @@ static mdg_status conv3t_launch(const CUtensorMap &map, const float *w, int oc, 
     conv3t_k<ACC><<<g, NT, TSMEM, st>>>(map, cin, d, wb.as<float>(), cpad, bias, cout, out);
     MDG_LAUNCHED();
     return MDG_OK;
+}
+
+static bool map4(CUtensorMap *m, const float *base, const D3 &d, int C, cuuint32_t bx,
+                 cuuint32_t by, cuuint32_t bz, cuuint32_t bc) {
+    if (enc_algo() == 3 || d.h % 4 != 0 || reinterpret_cast<uintptr_t>(base) % 16 != 0 ||
+        !tmap_fn())
+        return false;
+    const cuuint64_t dims[4] = {(cuuint64_t)d.h, (cuuint64_t)d.w, (cuuint64_t)d.l, (cuuint64_t)C};
+    const cuuint64_t strides[3] = {(cuuint64_t)d.h * 4, (cuuint64_t)d.h * d.w * 4,
+                                   (cuuint64_t)d.n * 4};
+    const cuuint32_t box[4] = {bx, by, bz, bc};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    return tmap_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(base), dims,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TMA kernel gradient (conv3w_k); false if the volume does not take TMA
+template <int WC>
+static bool conv3w_try(const float *in, int ic, const D3 &d, const float *gout, int oc, float *gk,
+                       float *gb, cudaStream_t st, mdg_status *rc) {
+    using W = WT<WC>;
+    CUtensorMap im, gm;
+    if (!map4(&im, in, d, ic, PX, HY, ZW + 2, WC) || !map4(&gm, gout, d, oc, TX, TY, ZW, OCB))
+        return false;
+    *rc = MDG_OK;
+    const int ntx = (d.h + TX - 1) / TX, nty = (d.w + TY - 1) / TY;
+    const int nob = (oc + OCB - 1) / OCB, ncc = (ic + WC - 1) / WC;
+    const int base = ntx * nty * nob * ncc;
+    // z split: ~4 waves of CTAs at 2-3 resident per SM, >= 8 planes each
+    const int want = 148 * 3 * 4;
+    int nz = std::max(1, std::min((want + base - 1) / base, (d.l + 7) / 8));
+    int zper = (d.l + nz - 1) / nz;
+    zper = (zper + ZW - 1) / ZW * ZW;
+    nz = (d.l + zper - 1) / zper;
+    const int nblk = ntx * nty * nz;
+    Scratch part;
+    const size_t np = (size_t)nob * ncc * nblk * OCB * WC * 27;
+    cudaError_t e = part.alloc((np + (size_t)nob * nblk * OCB) * sizeof(float), st);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(conv3w_k<WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)W::SMEM);
+    if (e != cudaSuccess) {
+        *rc = status_from_cuda(e, "conv3w");
+        return true;
+    }
+    float *pb = part.as<float>() + np;
+    conv3w_k<WC><<<dim3(ntx * nty, nz, nob * ncc), W::NTH, W::SMEM, st>>>(
+        im, gm, ic, oc, d, zper, ncc, part.as<float>(), pb);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if ((e = cudaPeekAtLastError()) != cudaSuccess) {
+        *rc = status_from_cuda(e, "conv3w_k");
+        return true;
+    }
+    const int nout = oc * ic * 27 + oc;
+    conv3w_sum_k<WC><<<(nout + 7) / 8, 256, 0, st>>>(part.as<float>(), pb, nblk, ncc, oc, ic, gk,
+                                                     gb);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if ((e = cudaPeekAtLastError()) != cudaSuccess) *rc = status_from_cuda(e, "conv3w_sum_k");
+    return true;
 }
 
 mdg_status enc_conv3_fwd(const float *in, int ic, mdg_dims3 dd, const float *w, const float *b,
@@ -757,6 +1016,12 @@ mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 dd, const float *w, 
         }
     }
     if ((gw || gb) && use_igemm(oc, ic, d)) return igemm_conv_wgrad(in, ic, dd, gout, oc, gw, gb, st);
+    if (gw || gb) {
+        mdg_status rc = MDG_OK;
+        if (ic == 1 ? conv3w_try<1>(in, ic, d, gout, oc, gw, gb, st, &rc)
+                    : conv3w_try<2>(in, ic, d, gout, oc, gw, gb, st, &rc))
+            return rc;
+    }
     if (gw || gb) {
         const int ntiles = ((d.h + TX - 1) / TX) * ((d.w + TY - 1) / TY) * ((d.l + TV - 1) / TV);
         const int noy = (oc + OCB - 1) / OCB, ncz = (ic + CIB - 1) / CIB;
