@@ -640,68 +640,122 @@ conv3g_wgrad_final_k(const float *__restrict__ part, const float *__restrict__ p
 }
 
 // ------------------------------------------------ instance norm + leaky relu
+// Channel-plane loops: one grid row per channel, float4 when n % 4 == 0 (the
+// planes are then 16-B aligned), two loads in flight per thread.
+template <bool VEC>
+struct Plane {
+    static constexpr int W = VEC ? 4 : 1;
+};
+__device__ __forceinline__ float4 ld4(const float *p, int i) {
+    return reinterpret_cast<const float4 *>(p)[i];
+}
+__device__ __forceinline__ void st4(float *p, int i, float4 v) {
+    reinterpret_cast<float4 *>(p)[i] = v;
+}
+__device__ __forceinline__ float el(const float4 &v, int k) {
+    return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+}
+
+template <int NV>
+__device__ __forceinline__ void block_sum(float (&v)[NV], float *out) {
+    __shared__ float red[NV][8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], m);
+        if (lane == 0) red[k][wid] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        float a = 0.0f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) a += red[threadIdx.x][w];
+        out[threadIdx.x] = a;
+    }
+}
+
 // per-channel partial sums (pass 1: x, pass 2: (x - mean)^2 with mean given)
+template <bool VEC>
 __global__ void __launch_bounds__(256)
 chan_sum_k(const float *__restrict__ x, int n, const float *__restrict__ mean,
            float *__restrict__ part) {
     const int c = blockIdx.y;
     const float *src = x + (int64_t)c * n;
     const float mu = mean ? mean[c] : 0.0f;
-    float a = 0.0f;
-    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
-        const float v = src[i];
-        if (mean) {
-            const float t = v - mu;
-            a = fmaf(t, t, a);
+    float a[1] = {0.0f};
+    const int nv = VEC ? n >> 2 : n;
+#pragma unroll 2
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < nv; i += gridDim.x * 256) {
+        if (VEC) {
+            const float4 v = ld4(src, i);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (mean) {
+                    const float t = el(v, k) - mu;
+                    a[0] = fmaf(t, t, a[0]);
+                } else {
+                    a[0] += el(v, k);
+                }
+            }
         } else {
-            a += v;
+            const float v = src[i];
+            if (mean) {
+                const float t = v - mu;
+                a[0] = fmaf(t, t, a[0]);
+            } else {
+                a[0] += v;
+            }
         }
     }
-    __shared__ float s[256];
-    s[threadIdx.x] = a;
-    __syncthreads();
-    for (int m = 128; m > 0; m >>= 1) {
-        if (threadIdx.x < m) s[threadIdx.x] += s[threadIdx.x + m];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) part[(int64_t)c * gridDim.x + blockIdx.x] = s[0];
+    block_sum<1>(a, part + (int64_t)c * gridDim.x + blockIdx.x);
 }
 
-// stat[c] = sum(part[c]) / n; if inv: stat = 1 / sqrt(stat + eps)
+// stat[c] = sum(part[c]) / n  (inv: 1 / sqrt(. + eps)); fixed order
 __global__ void __launch_bounds__(256)
 chan_final_k(const float *__restrict__ part, int nparts, int n, int inv, float eps,
              float *__restrict__ stat) {
     const int c = blockIdx.x;
-    float v = 0.0f;
-    for (int i = threadIdx.x; i < nparts; i += 256) v += part[(int64_t)c * nparts + i];
-    __shared__ float s[256];
-    s[threadIdx.x] = v;
+    float v[1] = {0.0f};
+    for (int i = threadIdx.x; i < nparts; i += 256) v[0] += part[(int64_t)c * nparts + i];
+    __shared__ float r;
+    block_sum<1>(v, &r);
     __syncthreads();
-    for (int m = 128; m > 0; m >>= 1) {
-        if (threadIdx.x < m) s[threadIdx.x] += s[threadIdx.x + m];
-        __syncthreads();
-    }
     if (threadIdx.x == 0) {
-        const float r = s[0] / (float)n;
-        stat[c] = inv ? 1.0f / sqrtf(r + eps) : r;
+        const float m = r / (float)n;
+        stat[c] = inv ? 1.0f / sqrtf(m + eps) : m;
     }
 }
 
 // z = lrelu(gamma (x - mean) inv + beta)   (ops.hpp:184-185, 230)
+template <bool VEC>
 __global__ void __launch_bounds__(256)
 in_apply_k(const float *__restrict__ x, int n, const float *__restrict__ mean,
            const float *__restrict__ inv, const float *__restrict__ g,
            const float *__restrict__ b, float slope, float *__restrict__ z) {
     const int c = blockIdx.y;
     const float mu = mean[c], iv = inv[c], gg = g[c], bb = b[c];
-    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
-        const float y = gg * (x[(int64_t)c * n + i] - mu) * iv + bb;
-        z[(int64_t)c * n + i] = y > 0.0f ? y : slope * y;
+    const float *src = x + (int64_t)c * n;
+    float *dst = z + (int64_t)c * n;
+    auto f = [&](float xv) {
+        const float y = gg * (xv - mu) * iv + bb;
+        return y > 0.0f ? y : slope * y;
+    };
+    const int nv = VEC ? n >> 2 : n;
+#pragma unroll 2
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < nv; i += gridDim.x * 256) {
+        if (VEC) {
+            const float4 v = ld4(src, i);
+            st4(dst, i, make_float4(f(v.x), f(v.y), f(v.z), f(v.w)));
+        } else {
+            dst[i] = f(src[i]);
+        }
     }
 }
 
 // backward sums per channel: gy = gz * lrelu'(y), xh = (x - mean) inv:
 // part[c][blk] = {sum gy, sum gy * xh}
+template <bool VEC>
 __global__ void __launch_bounds__(256)
 in_bwd_sum_k(const float *__restrict__ x, const float *__restrict__ gz, int n,
              const float *__restrict__ mean, const float *__restrict__ inv,
@@ -709,29 +763,32 @@ in_bwd_sum_k(const float *__restrict__ x, const float *__restrict__ gz, int n,
              float *__restrict__ part) {
     const int c = blockIdx.y;
     const float mu = mean[c], iv = inv[c], gg = g[c], bb = b[c];
-    float sg = 0.0f, sgx = 0.0f;
-    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
-        const float xh = (x[(int64_t)c * n + i] - mu) * iv;
+    const float *xs = x + (int64_t)c * n, *gs = gz + (int64_t)c * n;
+    float a[2] = {0.0f, 0.0f};
+    auto acc = [&](float xv, float gv) {
+        const float xh = (xv - mu) * iv;
         const float y = gg * xh + bb;
-        const float gy = gz[(int64_t)c * n + i] * (y > 0.0f ? 1.0f : slope);
-        sg += gy;
-        sgx = fmaf(gy, xh, sgx);
-    }
-    __shared__ float s[2][256];
-    s[0][threadIdx.x] = sg;
-    s[1][threadIdx.x] = sgx;
-    __syncthreads();
-    for (int m = 128; m > 0; m >>= 1) {
-        if (threadIdx.x < m) {
-            s[0][threadIdx.x] += s[0][threadIdx.x + m];
-            s[1][threadIdx.x] += s[1][threadIdx.x + m];
+        const float gy = gv * (y > 0.0f ? 1.0f : slope);
+        a[0] += gy;
+        a[1] = fmaf(gy, xh, a[1]);
+    };
+    const int nv = VEC ? n >> 2 : n;
+#pragma unroll 2
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < nv; i += gridDim.x * 256) {
+        if (VEC) {
+            const float4 xv = ld4(xs, i), gv = ld4(gs, i);
+            acc(xv.x, gv.x);
+            acc(xv.y, gv.y);
+            acc(xv.z, gv.z);
+            acc(xv.w, gv.w);
+        } else {
+            acc(xs[i], gs[i]);
         }
-        __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        part[((int64_t)c * gridDim.x + blockIdx.x) * 2] = s[0][0];
-        part[((int64_t)c * gridDim.x + blockIdx.x) * 2 + 1] = s[1][0];
-    }
+    __shared__ float r[2];
+    block_sum<2>(a, r);
+    __syncthreads();
+    if (threadIdx.x < 2) part[((int64_t)c * gridDim.x + blockIdx.x) * 2 + threadIdx.x] = r[threadIdx.x];
 }
 
 // sums[c] = {sum gy, sum gy xh}; gamma/beta grads accumulate
@@ -739,32 +796,25 @@ __global__ void __launch_bounds__(256)
 in_bwd_final_k(const float *__restrict__ part, int nparts, float *__restrict__ sums,
                float *__restrict__ gg, float *__restrict__ gb) {
     const int c = blockIdx.x;
-    float a = 0.0f, bsum = 0.0f;
+    float a[2] = {0.0f, 0.0f};
     for (int i = threadIdx.x; i < nparts; i += 256) {
-        a += part[((int64_t)c * nparts + i) * 2];
-        bsum += part[((int64_t)c * nparts + i) * 2 + 1];
+        a[0] += part[((int64_t)c * nparts + i) * 2];
+        a[1] += part[((int64_t)c * nparts + i) * 2 + 1];
     }
-    __shared__ float s[2][256];
-    s[0][threadIdx.x] = a;
-    s[1][threadIdx.x] = bsum;
+    __shared__ float r[2];
+    block_sum<2>(a, r);
     __syncthreads();
-    for (int m = 128; m > 0; m >>= 1) {
-        if (threadIdx.x < m) {
-            s[0][threadIdx.x] += s[0][threadIdx.x + m];
-            s[1][threadIdx.x] += s[1][threadIdx.x + m];
-        }
-        __syncthreads();
-    }
     if (threadIdx.x == 0) {
-        sums[2 * c] = s[0][0];
-        sums[2 * c + 1] = s[1][0];
-        if (gg) gg[c] += s[1][0];  // ops.hpp:204-205: gs += sum_gx, gb += sum_g
-        if (gb) gb[c] += s[0][0];
+        sums[2 * c] = r[0];
+        sums[2 * c + 1] = r[1];
+        if (gg) gg[c] += r[1];  // ops.hpp:204-205: gs += sum_gx, gb += sum_g
+        if (gb) gb[c] += r[0];
     }
 }
 
 // gx = (gamma inv) (gy - mean(gy) - xh mean(gy xh))   (ops.hpp:206-212);
 // written (not accumulated): the conv output it feeds is internal
+template <bool VEC>
 __global__ void __launch_bounds__(256)
 in_bwd_apply_k(const float *__restrict__ x, const float *__restrict__ gz, int n,
                const float *__restrict__ mean, const float *__restrict__ inv,
@@ -773,58 +823,87 @@ in_bwd_apply_k(const float *__restrict__ x, const float *__restrict__ gz, int n,
     const int c = blockIdx.y;
     const float mu = mean[c], iv = inv[c], gg = g[c], bb = b[c];
     const float k = gg * iv, mg = sums[2 * c] / (float)n, mgx = sums[2 * c + 1] / (float)n;
-    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
-        const float xh = (x[(int64_t)c * n + i] - mu) * iv;
+    const float *xs = x + (int64_t)c * n, *gs = gz + (int64_t)c * n;
+    float *dst = gx + (int64_t)c * n;
+    auto f = [&](float xv, float gv) {
+        const float xh = (xv - mu) * iv;
         const float y = gg * xh + bb;
-        const float gy = gz[(int64_t)c * n + i] * (y > 0.0f ? 1.0f : slope);
-        gx[(int64_t)c * n + i] = k * (gy - mg - xh * mgx);
+        const float gy = gv * (y > 0.0f ? 1.0f : slope);
+        return k * (gy - mg - xh * mgx);
+    };
+    const int nv = VEC ? n >> 2 : n;
+#pragma unroll 2
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < nv; i += gridDim.x * 256) {
+        if (VEC) {
+            const float4 xv = ld4(xs, i), gv = ld4(gs, i);
+            st4(dst, i, make_float4(f(xv.x, gv.x), f(xv.y, gv.y), f(xv.z, gv.z), f(xv.w, gv.w)));
+        } else {
+            dst[i] = f(xs[i], gs[i]);
+        }
     }
 }
 
 // ------------------------------------------------------------ avg pooling 2x
-// sampling.hpp:171-191 (replicate padding for odd dims)
+// sampling.hpp:171-191 (replicate padding for odd dims); one thread per
+// output voxel, grid row per channel, 32-bit index math
 __global__ void __launch_bounds__(256)
-avgpool_fwd_k(const float *__restrict__ in, int C, D3 d, D3 od, float *__restrict__ out) {
-    const int64_t total = (int64_t)C * od.n;
-    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * 256) {
-        const int c = (int)(i / od.n), o = (int)(i - (int64_t)c * od.n);
+avgpool_fwd_k(const float *__restrict__ in, D3 d, D3 od, float *__restrict__ out) {
+    const int c = blockIdx.y;
+    const float *pl = in + (int64_t)c * d.n;
+    for (int o = blockIdx.x * 256 + threadIdx.x; o < od.n; o += gridDim.x * 256) {
         const int t = o / od.h, x = o - t * od.h, z = t / od.w, y = t - z * od.w;
-        const float *pl = in + (int64_t)c * d.n;
+        const int x0 = 2 * x, x1 = min(2 * x + 1, d.h - 1);
         float s = 0.0f;
+#pragma unroll
         for (int dz = 0; dz < 2; ++dz)
-            for (int dy = 0; dy < 2; ++dy)
-                for (int dx = 0; dx < 2; ++dx) {
-                    const int xi = min(2 * x + dx, d.h - 1), yi = min(2 * y + dy, d.w - 1),
-                              zi = min(2 * z + dz, d.l - 1);
-                    s += pl[((int64_t)zi * d.w + yi) * d.h + xi];
-                }
-        out[i] = s / 8.0f;
+#pragma unroll
+            for (int dy = 0; dy < 2; ++dy) {
+                const int yi = min(2 * y + dy, d.w - 1), zi = min(2 * z + dz, d.l - 1);
+                const float *row = pl + (zi * d.w + yi) * d.h;
+                s += row[x0];
+                s += row[x1];
+            }
+        out[(int64_t)c * od.n + o] = s / 8.0f;
     }
 }
 
 // sampling.hpp:194-219 as a gather: input (x,y,z) gets g/8 of its output
-// cell once per (dx,dy,dz) that clamps onto it
+// cell once per (dx,dy,dz) that clamps onto it.  One thread per x pair (the
+// pair shares its output cell).
 __global__ void __launch_bounds__(256)
-avgpool_bwd_k(const float *__restrict__ gout, int C, D3 d, D3 od, float *__restrict__ gin) {
-    const int64_t total = (int64_t)C * d.n;
-    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * 256) {
-        const int c = (int)(i / d.n), p = (int)(i - (int64_t)c * d.n);
-        const int t = p / d.h, x = p - t * d.h, z = t / d.w, y = t - z * d.w;
-        const int mx = (x == d.h - 1 && (d.h & 1)) ? 2 : 1;
+avgpool_bwd_k(const float *__restrict__ gout, D3 d, D3 od, float *__restrict__ gin) {
+    const int c = blockIdx.y;
+    const int hp = (d.h + 1) >> 1, npair = hp * d.w * d.l;
+    const float *gp = gout + (int64_t)c * od.n;
+    float *ip = gin + (int64_t)c * d.n;
+    for (int q = blockIdx.x * 256 + threadIdx.x; q < npair; q += gridDim.x * 256) {
+        const int t = q / hp, xp = q - t * hp, z = t / d.w, y = t - z * d.w;
         const int my = (y == d.w - 1 && (d.w & 1)) ? 2 : 1;
         const int mz = (z == d.l - 1 && (d.l & 1)) ? 2 : 1;
-        const float g = gout[(int64_t)c * od.n + ((int64_t)(z / 2) * od.w + y / 2) * od.h + x / 2] / 8.0f;
-        float a = gin[i];
-        for (int k = 0; k < mx * my * mz; ++k) a += g;
-        gin[i] = a;
+        const float g = gp[((z >> 1) * od.w + (y >> 1)) * od.h + xp] / 8.0f;
+        const int x = 2 * xp, p = (z * d.w + y) * d.h + x;
+        float a = ip[p];
+        const int m0 = (x == d.h - 1) ? 2 * my * mz : my * mz;  // odd h: last x clamps twice
+        for (int k = 0; k < m0; ++k) a += g;
+        ip[p] = a;
+        if (x + 1 < d.h) {
+            float a1 = ip[p + 1];
+            for (int k = 0; k < my * mz; ++k) a1 += g;
+            ip[p + 1] = a1;
+        }
     }
 }
 
 }  // namespace enc
 
 using namespace enc;
+
+// blocks per channel row for a plane of `items`: ~8 resident 256-thread
+// blocks per SM over all C rows, at most one item per thread
+static unsigned plane_blocks(int64_t items, int C) {
+    const int64_t want = std::max<int64_t>(1, (148 * 8 + C - 1) / C);
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, want));
+}
 
 static unsigned grid_for(int64_t n, int per = 256) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + per - 1) / per, 148 * 8));
@@ -1050,18 +1129,21 @@ mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 dd, const float *w, 
 // z = lrelu(IN(x)); mean / inv (per channel) saved for the backward
 mdg_status enc_in_lrelu_fwd(const float *x, int C, int64_t n, const float *g, const float *b,
                             float slope, float *z, float *mean, float *inv, cudaStream_t st) {
-    const unsigned gx = std::min<unsigned>(grid_for(n), 256);
+    const bool vec = n % 4 == 0;
+    const unsigned gx = plane_blocks(vec ? n / 4 : n, C);
     Scratch part;
     MDG_CUDA_TRY(part.alloc((size_t)C * gx * sizeof(float), st));
-    chan_sum_k<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, nullptr, part.as<float>());
+    auto sum = vec ? chan_sum_k<true> : chan_sum_k<false>;
+    sum<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, nullptr, part.as<float>());
     MDG_LAUNCHED();
     chan_final_k<<<C, 256, 0, st>>>(part.as<float>(), gx, (int)n, 0, 0.0f, mean);
     MDG_LAUNCHED();
-    chan_sum_k<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, mean, part.as<float>());
+    sum<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, mean, part.as<float>());
     MDG_LAUNCHED();
     chan_final_k<<<C, 256, 0, st>>>(part.as<float>(), gx, (int)n, 1, 1e-5f, inv);
     MDG_LAUNCHED();
-    in_apply_k<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, mean, inv, g, b, slope, z);
+    (vec ? in_apply_k<true> : in_apply_k<false>)<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, mean, inv,
+                                                                            g, b, slope, z);
     MDG_LAUNCHED();
     return MDG_OK;
 }
@@ -1070,16 +1152,18 @@ mdg_status enc_in_lrelu_fwd(const float *x, int C, int64_t n, const float *g, co
 mdg_status enc_in_lrelu_bwd(const float *x, const float *gz, int C, int64_t n, const float *g,
                             const float *b, float slope, const float *mean, const float *inv,
                             float *gx, float *gg, float *gbeta, cudaStream_t st) {
-    const unsigned nb = std::min<unsigned>(grid_for(n), 256);
+    const bool vec = n % 4 == 0;
+    const unsigned nb = plane_blocks(vec ? n / 4 : n, C);
     Scratch part;
     MDG_CUDA_TRY(part.alloc(((size_t)C * nb * 2 + 2 * C) * sizeof(float), st));
     float *sums = part.as<float>() + (size_t)C * nb * 2;
-    in_bwd_sum_k<<<dim3(nb, C), 256, 0, st>>>(x, gz, (int)n, mean, inv, g, b, slope,
-                                             part.as<float>());
+    (vec ? in_bwd_sum_k<true> : in_bwd_sum_k<false>)<<<dim3(nb, C), 256, 0, st>>>(
+        x, gz, (int)n, mean, inv, g, b, slope, part.as<float>());
     MDG_LAUNCHED();
     in_bwd_final_k<<<C, 256, 0, st>>>(part.as<float>(), nb, sums, gg, gbeta);
     MDG_LAUNCHED();
-    in_bwd_apply_k<<<dim3(nb, C), 256, 0, st>>>(x, gz, (int)n, mean, inv, g, b, slope, sums, gx);
+    (vec ? in_bwd_apply_k<true> : in_bwd_apply_k<false>)<<<dim3(nb, C), 256, 0, st>>>(
+        x, gz, (int)n, mean, inv, g, b, slope, sums, gx);
     MDG_LAUNCHED();
     return MDG_OK;
 }
@@ -1088,7 +1172,7 @@ mdg_status enc_avgpool_fwd(const float *in, int C, mdg_dims3 dd, float *out, cud
     const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
     const int oh = (dd.h + 1) / 2, ow = (dd.w + 1) / 2, ol = (dd.l + 1) / 2;
     const D3 od{oh, ow, ol, oh * ow * ol};
-    avgpool_fwd_k<<<grid_for((int64_t)C * od.n), 256, 0, st>>>(in, C, d, od, out);
+    avgpool_fwd_k<<<dim3(plane_blocks(od.n, C), C), 256, 0, st>>>(in, d, od, out);
     MDG_LAUNCHED();
     return MDG_OK;
 }
@@ -1097,7 +1181,8 @@ mdg_status enc_avgpool_bwd(const float *gout, int C, mdg_dims3 dd, float *gin, c
     const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
     const int oh = (dd.h + 1) / 2, ow = (dd.w + 1) / 2, ol = (dd.l + 1) / 2;
     const D3 od{oh, ow, ol, oh * ow * ol};
-    avgpool_bwd_k<<<grid_for((int64_t)C * d.n), 256, 0, st>>>(gout, C, d, od, gin);
+    avgpool_bwd_k<<<dim3(plane_blocks((int64_t)((dd.h + 1) / 2) * dd.w * dd.l, C), C), 256, 0, st>>>(
+        gout, d, od, gin);
     MDG_LAUNCHED();
     return MDG_OK;
 }
