@@ -753,17 +753,58 @@ in_apply_k(const float *__restrict__ x, int n, const float *__restrict__ mean,
     }
 }
 
+// Gradient of a block output: its feature gradient (nullable) plus, when `pg`
+// is set, the 2x average-pool backward of the coarser level's input gradient
+// (sampling.hpp:194-219), added exactly as the separate pass would: the cell
+// value g/8 once per (dx, dy, dz) that clamps onto the voxel, in order.
+struct PoolSrc {
+    const float *g;  // {C, od.n} or nullptr
+    D3 d, od;        // fine / coarse dims
+};
+__device__ __forceinline__ float gz_at(const float *gz, const PoolSrc &ps, int c, int p) {
+    float a = gz ? gz[(int64_t)c * ps.d.n + p] : 0.0f;
+    if (ps.g) {
+        const int t = p / ps.d.h, x = p - t * ps.d.h, z = t / ps.d.w, y = t - z * ps.d.w;
+        const int mx = (x == ps.d.h - 1 && (ps.d.h & 1)) ? 2 : 1;
+        const int my = (y == ps.d.w - 1 && (ps.d.w & 1)) ? 2 : 1;
+        const int mz = (z == ps.d.l - 1 && (ps.d.l & 1)) ? 2 : 1;
+        const float g =
+            ps.g[(int64_t)c * ps.od.n + ((z >> 1) * ps.od.w + (y >> 1)) * ps.od.h + (x >> 1)] / 8.0f;
+        for (int k = 0; k < mx * my * mz; ++k) a += g;
+    }
+    return a;
+}
+// four x-consecutive voxels from p0 (p0 % 4 == 0, h % 4 == 0 so one row and mx = 1)
+__device__ __forceinline__ float4 gz_at4(const float *gz, const PoolSrc &ps, int c, int i4) {
+    float4 a = gz ? ld4(gz + (int64_t)c * ps.d.n, i4) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (ps.g) {
+        const int p = 4 * i4;
+        const int t = p / ps.d.h, x = p - t * ps.d.h, z = t / ps.d.w, y = t - z * ps.d.w;
+        const int my = (y == ps.d.w - 1 && (ps.d.w & 1)) ? 2 : 1;
+        const int mz = (z == ps.d.l - 1 && (ps.d.l & 1)) ? 2 : 1;
+        const float *row = ps.g + (int64_t)c * ps.od.n + ((z >> 1) * ps.od.w + (y >> 1)) * ps.od.h;
+        const float g0 = row[x >> 1] / 8.0f, g1 = row[(x >> 1) + 1] / 8.0f;
+        for (int k = 0; k < my * mz; ++k) {
+            a.x += g0;
+            a.y += g0;
+            a.z += g1;
+            a.w += g1;
+        }
+    }
+    return a;
+}
+
 // backward sums per channel: gy = gz * lrelu'(y), xh = (x - mean) inv:
 // part[c][blk] = {sum gy, sum gy * xh}
 template <bool VEC>
 __global__ void __launch_bounds__(256)
-in_bwd_sum_k(const float *__restrict__ x, const float *__restrict__ gz, int n,
+in_bwd_sum_k(const float *__restrict__ x, const float *__restrict__ gz, PoolSrc ps, int n,
              const float *__restrict__ mean, const float *__restrict__ inv,
              const float *__restrict__ g, const float *__restrict__ b, float slope,
              float *__restrict__ part) {
     const int c = blockIdx.y;
     const float mu = mean[c], iv = inv[c], gg = g[c], bb = b[c];
-    const float *xs = x + (int64_t)c * n, *gs = gz + (int64_t)c * n;
+    const float *xs = x + (int64_t)c * n;
     float a[2] = {0.0f, 0.0f};
     auto acc = [&](float xv, float gv) {
         const float xh = (xv - mu) * iv;
@@ -776,13 +817,13 @@ in_bwd_sum_k(const float *__restrict__ x, const float *__restrict__ gz, int n,
 #pragma unroll 2
     for (int i = blockIdx.x * 256 + threadIdx.x; i < nv; i += gridDim.x * 256) {
         if (VEC) {
-            const float4 xv = ld4(xs, i), gv = ld4(gs, i);
+            const float4 xv = ld4(xs, i), gv = gz_at4(gz, ps, c, i);
             acc(xv.x, gv.x);
             acc(xv.y, gv.y);
             acc(xv.z, gv.z);
             acc(xv.w, gv.w);
         } else {
-            acc(xs[i], gs[i]);
+            acc(xs[i], gz_at(gz, ps, c, i));
         }
     }
     __shared__ float r[2];
@@ -816,14 +857,14 @@ in_bwd_final_k(const float *__restrict__ part, int nparts, float *__restrict__ s
 // written (not accumulated): the conv output it feeds is internal
 template <bool VEC>
 __global__ void __launch_bounds__(256)
-in_bwd_apply_k(const float *__restrict__ x, const float *__restrict__ gz, int n,
+in_bwd_apply_k(const float *__restrict__ x, const float *__restrict__ gz, PoolSrc ps, int n,
                const float *__restrict__ mean, const float *__restrict__ inv,
                const float *__restrict__ g, const float *__restrict__ b, float slope,
                const float *__restrict__ sums, float *__restrict__ gx) {
     const int c = blockIdx.y;
     const float mu = mean[c], iv = inv[c], gg = g[c], bb = b[c];
     const float k = gg * iv, mg = sums[2 * c] / (float)n, mgx = sums[2 * c + 1] / (float)n;
-    const float *xs = x + (int64_t)c * n, *gs = gz + (int64_t)c * n;
+    const float *xs = x + (int64_t)c * n;
     float *dst = gx + (int64_t)c * n;
     auto f = [&](float xv, float gv) {
         const float xh = (xv - mu) * iv;
@@ -835,10 +876,10 @@ in_bwd_apply_k(const float *__restrict__ x, const float *__restrict__ gz, int n,
 #pragma unroll 2
     for (int i = blockIdx.x * 256 + threadIdx.x; i < nv; i += gridDim.x * 256) {
         if (VEC) {
-            const float4 xv = ld4(xs, i), gv = ld4(gs, i);
+            const float4 xv = ld4(xs, i), gv = gz_at4(gz, ps, c, i);
             st4(dst, i, make_float4(f(xv.x, gv.x), f(xv.y, gv.y), f(xv.z, gv.z), f(xv.w, gv.w)));
         } else {
-            dst[i] = f(xs[i], gs[i]);
+            dst[i] = f(xs[i], gz_at(gz, ps, c, i));
         }
     }
 }
@@ -1065,13 +1106,16 @@ mdg_status enc_conv3_fwd(const float *in, int ic, mdg_dims3 dd, const float *w, 
 }
 
 mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 dd, const float *w, int oc,
-                         const float *gout, float *gin, float *gw, float *gb, cudaStream_t st) {
+                         const float *gout, float *gin, float *gw, float *gb, cudaStream_t st,
+                         bool gin_acc) {
     const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
     if (gin) {
         const bool ig = use_igemm(ic, oc, d);
         CUtensorMap map;
         if (!ig && conv_map(&map, gout, d, oc)) {
-            const mdg_status s2 = conv3t_launch<true>(map, w, oc, ic, true, d, nullptr, gin, st);
+            const mdg_status s2 =
+                gin_acc ? conv3t_launch<true>(map, w, oc, ic, true, d, nullptr, gin, st)
+                        : conv3t_launch<false>(map, w, oc, ic, true, d, nullptr, gin, st);
             if (s2 != MDG_OK) return s2;
         } else {
             const int tile = ig ? igemm_fwd_bn(ic) : OCB;
@@ -1083,13 +1127,13 @@ mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 dd, const float *w, 
             MDG_LAUNCHED();
             if (ig) {
                 const mdg_status s =
-                    igemm_conv_fwd(gout, oc, dd, wt.as<float>(), ipad, nullptr, ic, true, gin, st);
+                    igemm_conv_fwd(gout, oc, dd, wt.as<float>(), ipad, nullptr, ic, gin_acc, gin, st);
                 if (s != MDG_OK) return s;
             } else {
                 const dim3 g((d.h + TX - 1) / TX, (d.w + TY - 1) / TY,
                              ((d.l + TV - 1) / TV) * (ipad / OCB));
-                conv3g_k<true><<<g, NT, 0, st>>>(gout, oc, d, wt.as<float>(), ipad, nullptr, ic,
-                                                 gin);
+                (gin_acc ? conv3g_k<true> : conv3g_k<false>)<<<g, NT, 0, st>>>(
+                    gout, oc, d, wt.as<float>(), ipad, nullptr, ic, gin);
                 MDG_LAUNCHED();
             }
         }
@@ -1149,21 +1193,25 @@ mdg_status enc_in_lrelu_fwd(const float *x, int C, int64_t n, const float *g, co
 }
 
 // gx = d/dx of lrelu(IN(x)) applied to gz (written); gamma/beta grads accumulate
-mdg_status enc_in_lrelu_bwd(const float *x, const float *gz, int C, int64_t n, const float *g,
-                            const float *b, float slope, const float *mean, const float *inv,
-                            float *gx, float *gg, float *gbeta, cudaStream_t st) {
-    const bool vec = n % 4 == 0;
+mdg_status enc_in_lrelu_bwd(const float *x, const float *gz, const float *pg, mdg_dims3 fd,
+                            int C, int64_t n, const float *g, const float *b, float slope,
+                            const float *mean, const float *inv, float *gx, float *gg,
+                            float *gbeta, cudaStream_t st) {
+    const D3 d{fd.h, fd.w, fd.l, fd.h * fd.w * fd.l};
+    const int oh = (fd.h + 1) / 2, ow = (fd.w + 1) / 2, ol = (fd.l + 1) / 2;
+    const PoolSrc ps{pg, d, D3{oh, ow, ol, oh * ow * ol}};
+    const bool vec = n % 4 == 0 && fd.h % 4 == 0;
     const unsigned nb = plane_blocks(vec ? n / 4 : n, C);
     Scratch part;
     MDG_CUDA_TRY(part.alloc(((size_t)C * nb * 2 + 2 * C) * sizeof(float), st));
     float *sums = part.as<float>() + (size_t)C * nb * 2;
     (vec ? in_bwd_sum_k<true> : in_bwd_sum_k<false>)<<<dim3(nb, C), 256, 0, st>>>(
-        x, gz, (int)n, mean, inv, g, b, slope, part.as<float>());
+        x, gz, ps, (int)n, mean, inv, g, b, slope, part.as<float>());
     MDG_LAUNCHED();
     in_bwd_final_k<<<C, 256, 0, st>>>(part.as<float>(), nb, sums, gg, gbeta);
     MDG_LAUNCHED();
     (vec ? in_bwd_apply_k<true> : in_bwd_apply_k<false>)<<<dim3(nb, C), 256, 0, st>>>(
-        x, gz, (int)n, mean, inv, g, b, slope, sums, gx);
+        x, gz, ps, (int)n, mean, inv, g, b, slope, sums, gx);
     MDG_LAUNCHED();
     return MDG_OK;
 }

@@ -22,9 +22,8 @@ struct mdg_encoder {
         int64_t n;
         int cin, c;
         float *x;          // block input (level 1: the image, not owned)
-        float *a1, *z1, *a2, *z2;  // conv1 out, block mid, conv2 out, block out (copy)
-        float *st1, *st2;  // mean | inv per channel (2C each)
-        float *gz;         // gradient of the block output
+        float *a1, *z1, *a2;  // conv1 out, block mid, conv2 out (block out: features[k])
+        float *st1, *st2;     // mean | inv per channel (2C each)
     };
     std::vector<Level> lv;
     float slope = 0.2f;
@@ -61,10 +60,8 @@ void enc_layout(mdg_encoder *e, Carve2 &cv, mdg_dims3 d0, int base, int levels) 
         L.a1 = cv.take((int64_t)L.c * L.n);
         L.z1 = cv.take((int64_t)L.c * L.n);
         L.a2 = cv.take((int64_t)L.c * L.n);
-        L.z2 = cv.take((int64_t)L.c * L.n);
         L.st1 = cv.take(2 * (int64_t)L.c);
         L.st2 = cv.take(2 * (int64_t)L.c);
-        L.gz = cv.take((int64_t)L.c * L.n);
         mx = std::max<int64_t>(mx, (int64_t)L.c * L.n);
     }
     e->scratch_a = cv.take(mx);
@@ -138,7 +135,7 @@ mdg_status mdg_encoder_forward(mdg_encoder *e, const float *image, const mdg_blo
                     "encoder: null parameter or feature buffer");
         const float *x = image;
         if (k > 0) {
-            ENC_TRY(enc_avgpool_fwd(e->lv[k - 1].z2, L.cin, e->lv[k - 1].d, L.x, st));
+            ENC_TRY(enc_avgpool_fwd(features[k - 1], L.cin, e->lv[k - 1].d, L.x, st));
             x = L.x;
         } else {
             L.x = const_cast<float *>(image);
@@ -147,10 +144,8 @@ mdg_status mdg_encoder_forward(mdg_encoder *e, const float *image, const mdg_blo
         ENC_TRY(enc_in_lrelu_fwd(L.a1, L.c, L.n, P.g1, P.be1, e->slope, L.z1, L.st1,
                                  L.st1 + L.c, st));
         ENC_TRY(enc_conv3_fwd(L.z1, L.c, L.d, P.w2, P.b2, L.c, L.a2, st));
-        ENC_TRY(enc_in_lrelu_fwd(L.a2, L.c, L.n, P.g2, P.be2, e->slope, L.z2, L.st2,
+        ENC_TRY(enc_in_lrelu_fwd(L.a2, L.c, L.n, P.g2, P.be2, e->slope, features[k], L.st2,
                                  L.st2 + L.c, st));
-        MDG_CUDA_TRY(cudaMemcpyAsync(features[k], L.z2, (size_t)L.c * L.n * sizeof(float),
-                                     cudaMemcpyDeviceToDevice, st));
     }
     e->have_forward = true;
     return MDG_OK;
@@ -162,41 +157,28 @@ mdg_status mdg_encoder_backward(mdg_encoder *e, const float *const *gfeatures,
     MDG_REQUIRE(e->have_forward, "encoder: backward without a forward");
     cudaStream_t st = S_(stream);
     const int levels = (int)e->lv.size();
-    for (int k = 0; k < levels; ++k) {
-        auto &L = e->lv[k];
-        if (gfeatures[k])
-            MDG_CUDA_TRY(cudaMemcpyAsync(L.gz, gfeatures[k], (size_t)L.c * L.n * sizeof(float),
-                                         cudaMemcpyDeviceToDevice, st));
-        else
-            MDG_CUDA_TRY(cudaMemsetAsync(L.gz, 0, (size_t)L.c * L.n * sizeof(float), st));
-    }
+    const float *pool = nullptr;  // input gradient of the coarser level (pooled from this one)
     for (int k = levels - 1; k >= 0; --k) {
         auto &L = e->lv[k];
         const mdg_block_params &P = e->p_saved[k];
         const mdg_block_grads *G = grads ? &grads[k] : nullptr;
         float *ga = e->scratch_a, *gz1 = e->scratch_b;
-        // block output z2 = lrelu(IN2(a2))
-        ENC_TRY(enc_in_lrelu_bwd(L.a2, L.gz, L.c, L.n, P.g2, P.be2, e->slope, L.st2,
-                                 L.st2 + L.c, ga, G ? G->g2 : nullptr, G ? G->be2 : nullptr,
-                                 st));
-        MDG_CUDA_TRY(cudaMemsetAsync(gz1, 0, (size_t)L.c * L.n * sizeof(float), st));
+        // block output z2 = lrelu(IN2(a2)); its gradient = gfeatures[k] + pool bwd
+        ENC_TRY(enc_in_lrelu_bwd(L.a2, gfeatures[k], pool, L.d, L.c, L.n, P.g2, P.be2, e->slope,
+                                 L.st2, L.st2 + L.c, ga, G ? G->g2 : nullptr,
+                                 G ? G->be2 : nullptr, st));
         ENC_TRY(enc_conv3_bwd(L.z1, L.c, L.d, P.w2, L.c, ga, gz1, G ? G->w2 : nullptr,
-                              G ? G->b2 : nullptr, st));
+                              G ? G->b2 : nullptr, st, /*gin_acc=*/false));
         // z1 = lrelu(IN1(a1)); ga reused
-        ENC_TRY(enc_in_lrelu_bwd(L.a1, gz1, L.c, L.n, P.g1, P.be1, e->slope, L.st1,
+        ENC_TRY(enc_in_lrelu_bwd(L.a1, gz1, nullptr, L.d, L.c, L.n, P.g1, P.be1, e->slope, L.st1,
                                  L.st1 + L.c, ga, G ? G->g1 : nullptr, G ? G->be1 : nullptr,
                                  st));
-        // conv1 input gradient: into the finer level's pooled-output gradient
-        float *gx = nullptr;
-        if (k > 0) {
-            gx = gz1;  // scratch (C_in <= C)
-            MDG_CUDA_TRY(cudaMemsetAsync(gx, 0, (size_t)L.cin * L.n * sizeof(float), st));
-        } else {
-            gx = gimage;
-        }
+        // conv1 input gradient: overwritten into scratch for the finer level's
+        // fused pool backward, or accumulated into the image gradient
+        float *gx = k > 0 ? gz1 : gimage;
         ENC_TRY(enc_conv3_bwd(L.x, L.cin, L.d, P.w1, L.c, ga, gx, G ? G->w1 : nullptr,
-                              G ? G->b1 : nullptr, st));
-        if (k > 0) ENC_TRY(enc_avgpool_bwd(gx, L.cin, e->lv[k - 1].d, e->lv[k - 1].gz, st));
+                              G ? G->b1 : nullptr, st, /*gin_acc=*/k == 0));
+        pool = gx;
     }
     return MDG_OK;
 }

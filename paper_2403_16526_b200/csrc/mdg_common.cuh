@@ -145,13 +145,18 @@ mdg_status project_qk_bwd_impl(const float *f, const float *m, int C, int64_t n,
 // encoder.cu: conv block pieces (internal; driven by encoder_driver.cu)
 mdg_status enc_conv3_fwd(const float *in, int ic, mdg_dims3 d, const float *w, const float *b,
                          int oc, float *out, cudaStream_t st);
+// gin_acc: accumulate into gin (else overwrite)
 mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 d, const float *w, int oc,
-                         const float *gout, float *gin, float *gw, float *gb, cudaStream_t st);
+                         const float *gout, float *gin, float *gw, float *gb, cudaStream_t st,
+                         bool gin_acc = true);
 mdg_status enc_in_lrelu_fwd(const float *x, int C, int64_t n, const float *g, const float *b,
                             float slope, float *z, float *mean, float *inv, cudaStream_t st);
-mdg_status enc_in_lrelu_bwd(const float *x, const float *gz, int C, int64_t n, const float *g,
-                            const float *b, float slope, const float *mean, const float *inv,
-                            float *gx, float *gg, float *gbeta, cudaStream_t st);
+// gz: gradient of the block output (nullable); pg: the coarser level's input
+// gradient whose 2x pool backward is added on the fly (nullable); fd: dims
+mdg_status enc_in_lrelu_bwd(const float *x, const float *gz, const float *pg, mdg_dims3 fd,
+                            int C, int64_t n, const float *g, const float *b, float slope,
+                            const float *mean, const float *inv, float *gx, float *gg,
+                            float *gbeta, cudaStream_t st);
 mdg_status enc_avgpool_fwd(const float *in, int C, mdg_dims3 d, float *out, cudaStream_t st);
 mdg_status enc_avgpool_bwd(const float *gout, int C, mdg_dims3 d, float *gin, cudaStream_t st);
 namespace enc {
