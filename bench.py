@@ -390,7 +390,7 @@ def run_po(dev, world, pairs=0, reps=5):
 
     h, w, l = DIMS
     params = [t.to(dev) for t in ops.init_model(42)]
-    model = ops.Model(params, DIMS)
+    model = ops.NativeModel(params, DIMS)  # mdg_model_*: the C++ model driver
     rng = ops.Rng(11)
     fixed = rng.uniform((1, l, w, h), 0.0, 1.0).to(dev)
     moving = rng.uniform((1, l, w, h), 0.0, 1.0).to(dev)
@@ -416,7 +416,7 @@ def run_po(dev, world, pairs=0, reps=5):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         it_ms, fwd_ms = float(t[0].item()), float(t[1].item())
     out = {"workload": "PO of the small-preset model at 160x192x224 (synthetic pair, "
-                       "init_model(42) weights)",
+                       "init_model(42) weights), native model driver (mdg_model_*)",
            "iter_ms": round(it_ms, 3), "final_forward_ms": round(fwd_ms, 3),
            "iters_per_pair": 50,
            "pairs_per_sec": round(world * 1e3 / (50 * it_ms + fwd_ms), 4),
@@ -425,7 +425,7 @@ def run_po(dev, world, pairs=0, reps=5):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(pairs):
-            m = ops.Model([t.to(dev) for t in ops.init_model(42)], DIMS)
+            m = ops.NativeModel([t.to(dev) for t in ops.init_model(42)], DIMS)
             for _ in range(50):
                 m.po_step(fixed, moving)
             m.loss_step(fixed, moving, backward=False)
