@@ -333,6 +333,7 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
     using W = WT<WC>;
     extern __shared__ __align__(128) float wsm2[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(wsm2 + 2 * W::BUF);
+    int *cnt = reinterpret_cast<int *>(wsm2 + 2 * W::BUF + 4);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int cl = wid / 3, dz = wid % 3;
     const int ntx = (d.h + TX - 1) / TX;
@@ -345,6 +346,7 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s32(&bar[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s32(&bar[1])));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        cnt[0] = cnt[1] = 0;
     }
     __syncthreads();
     auto issue = [&](int k) {
@@ -374,10 +376,13 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
     for (int k = 0; k < 9; ++k)
 #pragma unroll
         for (int j = 0; j < OCB / 2; ++j) acc[k][j] = make_float2(0.0f, 0.0f);
-    float2 gsum[OCB / 2];
+    // bias gradient: in the first channel chunk, warp w sums the channel pairs
+    // j with j % NW == w (spreads the extra adds over the warps)
+    constexpr int NW = W::NTH / 32, NS = (OCB / 2 + NW - 1) / NW;
+    float2 gsum[NS];
 #pragma unroll
-    for (int j = 0; j < OCB / 2; ++j) gsum[j] = make_float2(0.0f, 0.0f);
-    const bool bias_warp = cc == 0 && wid == 0;
+    for (int q = 0; q < NS; ++q) gsum[q] = make_float2(0.0f, 0.0f);
+    const bool bias_warp = cc == 0 && wid < OCB / 2;
 
     for (int k = 0; k < nsteps; ++k) {
         const float *b = wsm2 + (k & 1) * W::BUF;
@@ -415,9 +420,11 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
                             acc[6 + dx][j] = __ffma2_rn(s2, g2[j], acc[6 + dx][j]);
                         }
                     }
-                    if (bias_warp)
+                    if (bias_warp) {
 #pragma unroll
-                        for (int j = 0; j < OCB / 2; ++j) gsum[j] = __fadd2_rn(gsum[j], g2[j]);
+                        for (int j = 0; j < OCB / 2; ++j)
+                            if (j % NW == wid) gsum[j / NW] = __fadd2_rn(gsum[j / NW], g2[j]);
+                    }
 #pragma unroll
                     for (int dx = 0; dx < 3; ++dx) {
                         r0[dx] = r1[dx];
@@ -426,8 +433,18 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
                 }
             }
         }
-        __syncthreads();
-        if (threadIdx.x == 0 && k + 2 < nsteps) issue(k + 2);
+        // release the buffer without a block barrier: the last warp out
+        // re-arms it with the step two ahead (warps drift within the slack)
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&cnt[k & 1], 1) == W::NTH / 32 - 1) {
+                cnt[k & 1] = 0;
+                __threadfence_block();
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                if (k + 2 < nsteps) issue(k + 2);
+            }
+        }
     }
     // per-CTA partial: part[((ob*ncc + cc)*nblk + blk)][o][c][t]
     const int nblk = gridDim.x * gridDim.y, blk = blockIdx.y * gridDim.x + blockIdx.x;
@@ -448,20 +465,20 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
                 dst[((2 * j + 1) * WC + cl) * 27 + t] = ay;
             }
         }
-    if (cc == 0) {
-        if (wid == 0) {
+    if (bias_warp) {
 #pragma unroll
-            for (int j = 0; j < OCB / 2; ++j) {
-                float ax = gsum[j].x, ay = gsum[j].y;
+        for (int q = 0; q < NS; ++q) {
+            const int j = wid + q * NW;
+            if (j >= OCB / 2) break;
+            float ax = gsum[q].x, ay = gsum[q].y;
 #pragma unroll
-                for (int m = 16; m > 0; m >>= 1) {
-                    ax += __shfl_xor_sync(0xffffffffu, ax, m);
-                    ay += __shfl_xor_sync(0xffffffffu, ay, m);
-                }
-                if (lane == 0) {
-                    partb[((int64_t)ob * nblk + blk) * OCB + 2 * j] = ax;
-                    partb[((int64_t)ob * nblk + blk) * OCB + 2 * j + 1] = ay;
-                }
+            for (int m = 16; m > 0; m >>= 1) {
+                ax += __shfl_xor_sync(0xffffffffu, ax, m);
+                ay += __shfl_xor_sync(0xffffffffu, ay, m);
+            }
+            if (lane == 0) {
+                partb[((int64_t)ob * nblk + blk) * OCB + 2 * j] = ax;
+                partb[((int64_t)ob * nblk + blk) * OCB + 2 * j + 1] = ay;
             }
         }
     }

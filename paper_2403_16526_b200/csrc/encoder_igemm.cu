@@ -191,8 +191,8 @@ cudaError_t launch_fwd(const float *in, int cin, DI d, const float *wT, int opad
     using T = Tile<BN>;
     const int mt = (d.n + T::BM - 1) / T::BM, nt = (cout + BN - 1) / BN;
     const int tiles = mt * nt;
-    const int want = 148 * 2 * 3;  // ~3 waves at 2 CTAs/SM
-    int nsplit = std::max(1, std::min(cin, (want + tiles - 1) / tiles));
+    const int want = 148 * 2 * 2;  // ~2 waves at 2 CTAs/SM, >= 8 channels per split
+    int nsplit = std::max(1, std::min(std::max(1, cin / 8), (want + tiles - 1) / tiles));
     const int cps = (cin + nsplit - 1) / nsplit;
     nsplit = (cin + cps - 1) / cps;
     const size_t smem = 2 * (size_t)T::STAGE * sizeof(float);
@@ -333,34 +333,30 @@ igemm_wgrad_k(const float *__restrict__ in, int cin, DI d, const float *__restri
 }
 
 // gk[o][c][t] += sum_kb part[kb][tile(o, ct)][...]; gb[o] += sum_kb partb.
-// One warp per output value, lanes stride the partials, fixed butterfly.
+// One thread per output value walking the partials in kb order (fixed order;
+// consecutive threads read consecutive addresses of each partial tile).
 template <int BM>
 __global__ void __launch_bounds__(256)
 igemm_wgrad_sum_k(const float *__restrict__ part, const float *__restrict__ partb, int nkb,
                   int nmy, int nnz, int cout, int cin, float *__restrict__ gk,
                   float *__restrict__ gb) {
     constexpr int BN = NT * TM * TN / BM;
-    const int nw = cout * cin * 27;
-    const int idx = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    const int nct = cin * 27, nw = cout * nct;
+    const int idx = blockIdx.x * 256 + threadIdx.x;
     if (idx >= nw + cout) return;
     float v = 0.0f;
     if (idx < nw) {
-        const int o = idx / (cin * 27), ct = idx - o * (cin * 27);
+        const int o = idx / nct, ct = idx - o * nct;
         const int my = o / BM, ol = o - my * BM, nz = ct / BN, cl = ct - nz * BN;
-        for (int b = lane; b < nkb; b += 32)
-            v += part[(((int64_t)b * nmy + my) * nnz + nz) * (BM * BN) + ol * BN + cl];
+        const float *src = part + ((int64_t)(my * nnz + nz) * BM + ol) * BN + cl;
+        const int64_t stride = (int64_t)nmy * nnz * BM * BN;
+#pragma unroll 4
+        for (int b = 0; b < nkb; ++b) v += src[b * stride];
+        if (gk) gk[idx] += v;
     } else {
         const int o = idx - nw, my = o / BM, ol = o - my * BM;
-        for (int b = lane; b < nkb; b += 32) v += partb[((int64_t)b * nmy + my) * BM + ol];
-    }
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-    if (lane == 0) {
-        if (idx < nw) {
-            if (gk) gk[idx] += v;
-        } else if (gb) {
-            gb[idx - nw] += v;
-        }
+        for (int b = 0; b < nkb; ++b) v += partb[((int64_t)b * nmy + my) * BM + ol];
+        if (gb) gb[o] += v;
     }
 }
 
@@ -371,10 +367,10 @@ cudaError_t launch_wgrad(const float *in, int cin, DI d, const float *gout, int 
     constexpr int STAGE = WBK * ((BM + 4) + (BN + 4));
     const int nmy = (cout + BM - 1) / BM, nnz = (cin * 27 + BN - 1) / BN;
     const int tiles = nmy * nnz;
-    const int want = 148 * 2 * 3;
+    const int want = 148 * 2 * 2;  // ~2 waves, >= 8 voxel steps per CTA
     int nkb = std::max(1, (want + tiles - 1) / tiles);
     int chunk = (d.n + nkb - 1) / nkb;
-    chunk = std::max(WBK * 4, (chunk + WBK - 1) / WBK * WBK);
+    chunk = std::max(WBK * 8, (chunk + WBK - 1) / WBK * WBK);
     nkb = (d.n + chunk - 1) / chunk;
     const size_t smem = 2 * (size_t)STAGE * sizeof(float);
     cudaError_t e = cudaFuncSetAttribute(igemm_wgrad_k<BM>,
@@ -389,8 +385,8 @@ cudaError_t launch_wgrad(const float *in, int cin, DI d, const float *gout, int 
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if ((e = cudaPeekAtLastError()) != cudaSuccess) return e;
     const int nout = cout * cin * 27 + cout;
-    igemm_wgrad_sum_k<BM><<<(nout + 7) / 8, 256, 0, st>>>(part.as<float>(), pb, nkb, nmy, nnz,
-                                                          cout, cin, gk, gb);
+    igemm_wgrad_sum_k<BM><<<(nout + 255) / 256, 256, 0, st>>>(part.as<float>(), pb, nkb, nmy,
+                                                              nnz, cout, cin, gk, gb);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaPeekAtLastError();
 }

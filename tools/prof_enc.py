@@ -25,7 +25,7 @@ tr = json.load(open(path))
 tot = 0.0
 for e in tr["traceEvents"]:
     if e.get("cat") == "kernel":
-        nm = e["name"].split("(")[0].replace("void ", "")[:34]
+        nm = e["name"].replace("void ", "").replace("(anonymous namespace)::", "").split("(")[0][-34:]
         a = e.get("args", {})
         tot += e["dur"]
         if e["dur"] > 20:

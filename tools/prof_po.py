@@ -17,7 +17,7 @@ for ev in prof.events():
     if ev.device_type.name == "CUDA":
         k = ev.name.split("(")[0][:50]; agg[k] += ev.device_time; cnt[k] += 1
 tot = sum(agg.values())
-for k, v in sorted(agg.items(), key=lambda x: -x[1])[:22]:
+for k, v in sorted(agg.items(), key=lambda x: -x[1])[:60]:
     print(f"{k:50s} {cnt[k]:4d} {v/1e3:8.2f} ms {100*v/tot:5.1f}%")
 print(f"total {tot/1e3:.2f} ms")
 if os.environ.get("EVENTS"):
