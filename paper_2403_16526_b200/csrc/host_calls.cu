@@ -5,6 +5,7 @@
 // the call returns after the results are back in host memory.  With pinned
 // host buffers (mdg_host_alloc) the copies run at full PCIe/C2C bandwidth.
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -575,32 +576,131 @@ mdg_status modet_bwd_host_pipelined(const float *Q, const float *K, const float 
 
 // warp: the input volume must be whole before any gather, then the field /
 // upstream-gradient chunks stream in and the per-voxel results stream out
+// ---------------------------------------------------------- warp pipelines
+// The warp's gather (and its backward's scatter) reach is data-dependent, so
+// the field is uploaded first and a device pass computes, per z-chunk, the
+// exact range of z rows its samples can touch: every corner row is a clamped
+// floor(z + phi_z) or that + 1 (resolve_axis), and clamping is monotone, so
+// [clamp(floor(min)), clamp(floor(max) + 1)] over the chunk bounds them (any
+// non-finite coordinate widens it to the whole volume).  The input then
+// streams chunk by chunk and chunk i computes as soon as the rows it reaches
+// have arrived; the scattered input gradient is downloaded row-chunk by
+// row-chunk as soon as no later chunk can reach it.  Same kernels, same
+// per-voxel arithmetic as the whole-volume call: results are identical.
+__global__ void __launch_bounds__(256)
+reach_k(const float *__restrict__ fz, int h, int w, int l, const int *__restrict__ z0s,
+        const int *__restrict__ z1s, int *__restrict__ lo, int *__restrict__ hi) {
+    const int i = blockIdx.y;
+    const int hw = h * w, pb = z0s[i] * hw, pe = z1s[i] * hw;
+    int a = INT_MAX, b = INT_MIN;
+    for (int p = pb + blockIdx.x * 256 + threadIdx.x; p < pe; p += gridDim.x * 256) {
+        const float zs = __fadd_rn((float)(p / hw), fz[p]);
+        if (!isfinite(zs)) {
+            a = 0;
+            b = l - 1;
+        } else {
+            const int r = (int)floorf(fminf(fmaxf(zs, -2.0f), (float)l + 1.0f));
+            a = min(a, r);
+            b = max(b, r + 1);
+        }
+    }
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) {
+        a = min(a, __shfl_xor_sync(0xffffffffu, a, m));
+        b = max(b, __shfl_xor_sync(0xffffffffu, b, m));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&lo[i], a);
+        atomicMax(&hi[i], b);
+    }
+}
+
+struct Reach {
+    std::vector<int> lo, hi;     // touched z rows per chunk (clamped)
+    std::vector<int> need;       // last input chunk chunk i reads
+    std::vector<int> last;       // last compute chunk that can reach row chunk j
+};
+
+// field (all chunks, on `up`) -> reach on `comp` -> host; the caller keeps
+// enqueueing uploads on `up` while this waits.  `dz` = device z plane of phi.
+static cudaError_t reach_enqueue(PipeCtx &P, const float *dz, int *dbuf, int *hbuf) {
+    const int N = P.ck.nchunk;
+    cudaError_t e = cudaMemcpyAsync(dbuf + 2 * N, P.ck.z0.data(), N * sizeof(int),
+                                    cudaMemcpyHostToDevice, P.comp);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dbuf + 3 * N, P.ck.z1.data(), N * sizeof(int), cudaMemcpyHostToDevice,
+                            P.comp);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dbuf, 0x7f, N * sizeof(int), P.comp);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dbuf + N, 0x80, N * sizeof(int), P.comp);
+    if (e != cudaSuccess) return e;
+    reach_k<<<dim3(32, N), 256, 0, P.comp>>>(dz, P.d.h, P.d.w, P.d.l, dbuf + 2 * N, dbuf + 3 * N,
+                                            dbuf, dbuf + N);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if ((e = cudaPeekAtLastError()) != cudaSuccess) return e;
+    return cudaMemcpyAsync(hbuf, dbuf, 2 * N * sizeof(int), cudaMemcpyDeviceToHost, P.comp);
+}
+
+static Reach reach_decode(const PipeCtx &P, const int *hbuf) {
+    const int N = P.ck.nchunk, l = P.d.l;
+    Reach r;
+    r.lo.resize(N);
+    r.hi.resize(N);
+    r.need.resize(N);
+    r.last.assign(N, -1);
+    auto chunk_of = [&](int z) {
+        int c = 0;
+        while (c + 1 < N && P.ck.z0[c + 1] <= z) ++c;
+        return c;
+    };
+    for (int i = 0; i < N; ++i) {
+        r.lo[i] = std::max(0, std::min(hbuf[i], l - 1));
+        r.hi[i] = std::min(l - 1, std::max(hbuf[N + i], 0));
+        if (r.hi[i] < r.lo[i]) r.hi[i] = r.lo[i];
+        // inputs arrive in z order; also wait for chunk i's own rows (gout)
+        r.need[i] = std::max(chunk_of(r.hi[i]), i);
+        for (int j = chunk_of(r.lo[i]); j <= chunk_of(r.hi[i]); ++j) r.last[j] = std::max(r.last[j], i);
+    }
+    return r;
+}
+
 mdg_status warp_fwd_host_pipelined(const float *in, int C, mdg_dims3 d, const float *field,
                                    float *out) {
     PipeCtx P(d);
     const int N = P.ck.nchunk;
     const int64_t n = P.n, hw = P.hw;
-    float *di, *df, *dout;
+    const size_t pitch = (size_t)n * sizeof(float);
+    float *di, *df, *dout, *dr;
     MDG_PIPE_TRY(P.alloc(&di, (size_t)C * n));
     MDG_PIPE_TRY(P.alloc(&df, 3 * (size_t)n));
     MDG_PIPE_TRY(P.alloc(&dout, (size_t)C * n));
-    MDG_PIPE_TRY(cudaMemcpyAsync(di, in, (size_t)C * n * sizeof(float), cudaMemcpyHostToDevice, P.up));
-    std::vector<cudaEvent_t> upd(N), cmp(N);
-    const size_t pitch = (size_t)n * sizeof(float);
+    MDG_PIPE_TRY(P.alloc(&dr, 4 * (size_t)N));
+    PinnedStage &stg = pinned_stage();
+    MDG_PIPE_TRY(stg.reserve(2 * (size_t)N));
+    int *hr = reinterpret_cast<int *>(stg.p);
+    MDG_PIPE_TRY(cudaMemcpyAsync(df, field, 3 * pitch, cudaMemcpyHostToDevice, P.up));
+    cudaEvent_t fev = P.event();
+    MDG_PIPE_TRY(cudaEventRecord(fev, P.up));
+    MDG_PIPE_TRY(cudaStreamWaitEvent(P.comp, fev, 0));
+    MDG_PIPE_TRY(reach_enqueue(P, df + 2 * n, reinterpret_cast<int *>(dr), hr));
+    cudaEvent_t rev = P.event();
+    MDG_PIPE_TRY(cudaEventRecord(rev, P.comp));
+    std::vector<cudaEvent_t> upd(N);
     for (int i = 0; i < N; ++i) {
         const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
-        MDG_PIPE_TRY(cudaMemcpy2DAsync(df + p0, pitch, field + p0, pitch, m * sizeof(float), 3,
+        MDG_PIPE_TRY(cudaMemcpy2DAsync(di + p0, pitch, in + p0, pitch, m * sizeof(float), C,
                                        cudaMemcpyHostToDevice, P.up));
         upd[i] = P.event();
         MDG_PIPE_TRY(cudaEventRecord(upd[i], P.up));
     }
+    MDG_PIPE_TRY(cudaEventSynchronize(rev));
+    const Reach R = reach_decode(P, hr);
     for (int i = 0; i < N; ++i) {
         const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
-        MDG_PIPE_TRY(cudaStreamWaitEvent(P.comp, upd[i], 0));
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.comp, upd[R.need[i]], 0));
         MDG_PIPE_OK(warp_fwd_range(di, C, d, df, dout, p0, p0 + m, P.comp));
-        cmp[i] = P.event();
-        MDG_PIPE_TRY(cudaEventRecord(cmp[i], P.comp));
-        MDG_PIPE_TRY(cudaStreamWaitEvent(P.down, cmp[i], 0));
+        cudaEvent_t ce = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(ce, P.comp));
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.down, ce, 0));
         MDG_PIPE_TRY(cudaMemcpy2DAsync(out + p0, pitch, dout + p0, pitch, m * sizeof(float), C,
                                        cudaMemcpyDeviceToHost, P.down));
     }
@@ -613,63 +713,73 @@ mdg_status warp_bwd_host_pipelined(const float *in, int C, mdg_dims3 d, const fl
     PipeCtx P(d);
     const int N = P.ck.nchunk;
     const int64_t n = P.n, hw = P.hw;
-    float *di, *df, *dg, *dgi = nullptr, *dgf = nullptr;
+    const size_t pitch = (size_t)n * sizeof(float);
+    float *di, *df, *dg, *dgi = nullptr, *dgf = nullptr, *dr;
     MDG_PIPE_TRY(P.alloc(&di, (size_t)C * n));
     MDG_PIPE_TRY(P.alloc(&df, 3 * (size_t)n));
     MDG_PIPE_TRY(P.alloc(&dg, (size_t)C * n));
+    MDG_PIPE_TRY(P.alloc(&dr, 4 * (size_t)N));
     if (gin) MDG_PIPE_TRY(P.alloc(&dgi, (size_t)C * n));
     if (gfield) MDG_PIPE_TRY(P.alloc(&dgf, 3 * (size_t)n));
     PinnedStage &stg = pinned_stage();
-    MDG_PIPE_TRY(stg.reserve((size_t)(C + 3) * n));
+    MDG_PIPE_TRY(stg.reserve((size_t)(C + 3) * n + 2 * (size_t)N));
     float *si = stg.p, *sf = stg.p + (size_t)C * n;
+    int *hr = reinterpret_cast<int *>(stg.p + (size_t)(C + 3) * n);
     // fresh contributions (the caller's accumulators stay on the host)
-    if (dgi) MDG_PIPE_TRY(cudaMemsetAsync(dgi, 0, (size_t)C * n * sizeof(float), P.up));
-    if (dgf) MDG_PIPE_TRY(cudaMemsetAsync(dgf, 0, 3 * (size_t)n * sizeof(float), P.up));
-    MDG_PIPE_TRY(cudaMemcpyAsync(di, in, (size_t)C * n * sizeof(float), cudaMemcpyHostToDevice, P.up));
-    std::vector<cudaEvent_t> upd(N), cmp(N), dwn(N), gdw(N);
-    const size_t pitch = (size_t)n * sizeof(float);
+    if (dgi) MDG_PIPE_TRY(cudaMemsetAsync(dgi, 0, (size_t)C * n * sizeof(float), P.comp));
+    if (dgf) MDG_PIPE_TRY(cudaMemsetAsync(dgf, 0, 3 * (size_t)n * sizeof(float), P.comp));
+    MDG_PIPE_TRY(cudaMemcpyAsync(df, field, 3 * pitch, cudaMemcpyHostToDevice, P.up));
+    cudaEvent_t fev = P.event();
+    MDG_PIPE_TRY(cudaEventRecord(fev, P.up));
+    MDG_PIPE_TRY(cudaStreamWaitEvent(P.comp, fev, 0));
+    MDG_PIPE_TRY(reach_enqueue(P, df + 2 * n, reinterpret_cast<int *>(dr), hr));
+    cudaEvent_t rev = P.event();
+    MDG_PIPE_TRY(cudaEventRecord(rev, P.comp));
+    std::vector<cudaEvent_t> upd(N), fdw(N), gdw(N, nullptr);
     for (int i = 0; i < N; ++i) {
         const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
-        MDG_PIPE_TRY(cudaMemcpy2DAsync(df + p0, pitch, field + p0, pitch, m * sizeof(float), 3,
+        MDG_PIPE_TRY(cudaMemcpy2DAsync(di + p0, pitch, in + p0, pitch, m * sizeof(float), C,
                                        cudaMemcpyHostToDevice, P.up));
         MDG_PIPE_TRY(cudaMemcpy2DAsync(dg + p0, pitch, gout + p0, pitch, m * sizeof(float), C,
                                        cudaMemcpyHostToDevice, P.up));
         upd[i] = P.event();
         MDG_PIPE_TRY(cudaEventRecord(upd[i], P.up));
     }
+    MDG_PIPE_TRY(cudaEventSynchronize(rev));
+    const Reach R = reach_decode(P, hr);
+    std::vector<std::vector<int>> gin_after(N);  // row chunks final after compute i
+    for (int j = 0; j < N; ++j) gin_after[std::max(R.last[j], 0)].push_back(j);
     for (int i = 0; i < N; ++i) {
         const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
-        MDG_PIPE_TRY(cudaStreamWaitEvent(P.comp, upd[i], 0));
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.comp, upd[R.need[i]], 0));
         MDG_PIPE_OK(warp_bwd_range(di, C, d, df, dg, dgi, dgf, p0, p0 + m, P.comp));
-        cmp[i] = P.event();
-        MDG_PIPE_TRY(cudaEventRecord(cmp[i], P.comp));
-        MDG_PIPE_TRY(cudaStreamWaitEvent(P.down, cmp[i], 0));
+        cudaEvent_t ce = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(ce, P.comp));
+        MDG_PIPE_TRY(cudaStreamWaitEvent(P.down, ce, 0));
         if (dgf)
             MDG_PIPE_TRY(cudaMemcpy2DAsync(sf + p0, pitch, dgf + p0, pitch, m * sizeof(float), 3,
                                            cudaMemcpyDeviceToHost, P.down));
-        dwn[i] = P.event();
-        MDG_PIPE_TRY(cudaEventRecord(dwn[i], P.down));
+        fdw[i] = P.event();
+        MDG_PIPE_TRY(cudaEventRecord(fdw[i], P.down));
+        for (int j : gin_after[i]) {
+            const int64_t q0 = (int64_t)P.ck.z0[j] * hw, mq = (int64_t)P.ck.depth(j) * hw;
+            if (dgi)
+                MDG_PIPE_TRY(cudaMemcpy2DAsync(si + q0, pitch, dgi + q0, pitch, mq * sizeof(float),
+                                               C, cudaMemcpyDeviceToHost, P.down));
+            gdw[j] = P.event();
+            MDG_PIPE_TRY(cudaEventRecord(gdw[j], P.down));
+        }
     }
-    // the image gradient is a scatter: complete only after the last chunk
+    // host adds in download order
     for (int i = 0; i < N; ++i) {
         const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
-        if (dgi)
-            MDG_PIPE_TRY(cudaMemcpy2DAsync(si + p0, pitch, dgi + p0, pitch, m * sizeof(float), C,
-                                           cudaMemcpyDeviceToHost, P.down));
-        gdw[i] = P.event();
-        MDG_PIPE_TRY(cudaEventRecord(gdw[i], P.down));
-    }
-    for (int i = 0; i < N; ++i) {
-        const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
-        MDG_PIPE_TRY(cudaEventSynchronize(dwn[i]));
-        if (gfield)
-            host_add_rows(gfield + p0, sf + p0, m, 3, n);
-    }
-    for (int i = 0; i < N; ++i) {
-        const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
-        MDG_PIPE_TRY(cudaEventSynchronize(gdw[i]));
-        if (gin)
-            host_add_rows(gin + p0, si + p0, m, C, n);
+        MDG_PIPE_TRY(cudaEventSynchronize(fdw[i]));
+        if (gfield) host_add_rows(gfield + p0, sf + p0, m, 3, n);
+        for (int j : gin_after[i]) {
+            const int64_t q0 = (int64_t)P.ck.z0[j] * hw, mq = (int64_t)P.ck.depth(j) * hw;
+            MDG_PIPE_TRY(cudaEventSynchronize(gdw[j]));
+            if (gin) host_add_rows(gin + q0, si + q0, mq, C, n);
+        }
     }
     MDG_PIPE_TRY(cudaStreamSynchronize(P.down));
     return MDG_OK;

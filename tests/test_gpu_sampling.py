@@ -181,12 +181,16 @@ def test_north_star_size_warp_c8(cuda, oracle):
     assert rel_close(host(gin), rgin)
 
 
+@pytest.mark.parametrize("reach", ["small", "far", "nonfinite"])
 @pytest.mark.parametrize("C", [8, 3, 5])
-def test_pipelined_warp_host_calls_match_device(cuda, C):
-    """>= 1M voxels: warp_fwd_host / warp_bwd_host run the z-chunk pipeline
-    (field / gout chunks streamed, contributions added into the caller's host
-    accumulators by host threads).  out and gfield are bit-identical to the
-    device call; gin (fp32 atomics) to scatter tolerance."""
+def test_pipelined_warp_host_calls_match_device(cuda, C, reach):
+    """>= 1M voxels: warp_fwd_host / warp_bwd_host run the reach-aware z-chunk
+    pipeline (field first, per-chunk sampled z range on the device, input
+    chunks streamed, the scattered gradient downloaded as rows become final,
+    contributions added into the caller's host accumulators by host threads).
+    out and gfield are bit-identical to the device call; gin (fp32 atomics) to
+    scatter tolerance.  `reach`: small field, far-reaching z displacements
+    (several chunks, both directions), and non-finite entries."""
     import ctypes as C_
 
     from paper_2403_16526_b200 import _capi
@@ -196,6 +200,13 @@ def test_pipelined_warp_host_calls_match_device(cuda, C):
     r = np.random.default_rng(C)
     vol = f32(r.standard_normal((C, l, w, h)))
     fld = f32(r.uniform(-2.5, 2.5, (3, l, w, h)))
+    if reach == "far":
+        fld[2, 10:20] += 37.0    # forward several chunks
+        fld[2, 70:75] -= 55.5    # backward several chunks
+        fld[2, 95:] += 1e9       # far outside (clamped)
+    elif reach == "nonfinite":
+        fld[2, 40, 3, 5] = np.nan
+        fld[0, 60, 7, 9] = np.inf
     g = f32(r.standard_normal((C, l, w, h)))
     gin0 = f32(r.standard_normal((C, l, w, h)))
     gf0 = f32(r.standard_normal((3, l, w, h)))
@@ -207,8 +218,8 @@ def test_pipelined_warp_host_calls_match_device(cuda, C):
     d3 = _capi.Dims3(*dims)
     out = np.zeros_like(vol)
     assert L.mdg_warp_fwd_host(p(vol), C, d3, p(fld), p(out)) == 0
-    assert np.array_equal(out, out_d)
+    assert np.array_equal(out, out_d, equal_nan=True)
     gin, gf = gin0.copy(), gf0.copy()
     assert L.mdg_warp_bwd_host(p(vol), C, d3, p(fld), p(g), p(gin), p(gf)) == 0
-    assert np.array_equal(gf, gf_d)
-    assert rel_close(gin, gin_d, 1e-5, 1e-4)
+    assert np.array_equal(gf, gf_d, equal_nan=True)
+    np.testing.assert_allclose(gin, gin_d, rtol=1e-4, atol=1e-5, equal_nan=True)
