@@ -437,7 +437,9 @@ def run_po(dev, world, pairs=0, reps=5):
 
 def run_e2e(args, L, host_in, world, dev):
     """Same metric through the host-buffer drop-ins (mdg_*_host): pinned host
-    inputs in, host outputs back, copies inside the timed region."""
+    inputs in, host outputs back, copies inside the timed region.  Same
+    semantics as the device step: the ModeT backward overwrites gQ/gK/gB
+    (accumulate=0), the warp backward accumulates (the reference's rule)."""
     import torch
 
     from paper_2403_16526_b200 import ops
@@ -459,7 +461,7 @@ def run_e2e(args, L, host_in, world, dev):
                                   p(outs["SF"]), p(outs["LSE"]))
         rc |= L.mdg_modet_bwd_host(p(pin["Q"]), p(pin["K"]), p(pin["B"]), p(outs["SF"]),
                                    p(outs["LSE"]), p(pin["gSF"]), d3, S, HD, NB, LAYOUT,
-                                   p(outs["gQ"]), p(outs["gK"]), p(outs["gB"]))
+                                   p(outs["gQ"]), p(outs["gK"]), p(outs["gB"]), 0)
         rc |= L.mdg_warp_fwd_host(p(pin["feat"]), CH, d3, p(pin["field"]), p(outs["warped"]))
         rc |= L.mdg_warp_bwd_host(p(pin["feat"]), CH, d3, p(pin["field"]), p(pin["gout"]),
                                   p(outs["gin"]), p(outs["gfield"]))

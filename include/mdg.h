@@ -364,9 +364,12 @@ mdg_status mdg_na_fused_fwd_host(const float *Q, const float *K, const float *B,
                                  int S, int hd, int nb, float *W);
 mdg_status mdg_modet_fwd_host(const float *Q, const float *K, const float *B, mdg_dims3 d,
                               int S, int hd, int nb, int layout, float *SF, float *LSE);
+/* accumulate: as mdg_modet_bwd (1: gQ/gK/gB +=, the reference's rule;
+ * 0: overwritten, e.g. for a tape's zero-initialised gradients) */
 mdg_status mdg_modet_bwd_host(const float *Q, const float *K, const float *B, const float *SF,
                               const float *LSE, const float *gSF, mdg_dims3 d, int S, int hd,
-                              int nb, int layout, float *gQ, float *gK, float *gB);
+                              int nb, int layout, float *gQ, float *gK, float *gB,
+                              int accumulate);
 mdg_status mdg_warp_fwd_host(const float *in, int C, mdg_dims3 d, const float *field,
                              float *out);
 mdg_status mdg_warp_bwd_host(const float *in, int C, mdg_dims3 d, const float *field,

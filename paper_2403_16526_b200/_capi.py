@@ -133,7 +133,7 @@ SIGNATURES = {
     "mdg_qk_planar_to_posmajor": (_st, [_p, C.c_int64, _i, _p, _p]),
     "mdg_na_fused_fwd_host": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _p]),
     "mdg_modet_fwd_host": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p]),
-    "mdg_modet_bwd_host": (_st, [_p, _p, _p, _p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p]),
+    "mdg_modet_bwd_host": (_st, [_p, _p, _p, _p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p, _i]),
     "mdg_warp_fwd_host": (_st, [_p, _i, Dims3, _p, _p]),
     "mdg_warp_bwd_host": (_st, [_p, _i, Dims3, _p, _p, _p, _p]),
     "mdg_rng_new": (_p, [C.c_uint64]),

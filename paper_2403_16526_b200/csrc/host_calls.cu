@@ -497,7 +497,7 @@ mdg_status modet_fwd_host_pipelined(const float *Q, const float *K, const float 
 mdg_status modet_bwd_host_pipelined(const float *Q, const float *K, const float *B,
                                     const float *SF, const float *LSE, const float *gSF,
                                     mdg_dims3 d, int S, int hd, int layout, float *gQ, float *gK,
-                                    float *gB) {
+                                    float *gB, bool acc) {
     const auto te = std::chrono::steady_clock::now();
     PipeCtx P(d);
     const int N = P.ck.nchunk, C = S * hd;
@@ -510,15 +510,22 @@ mdg_status modet_bwd_host_pipelined(const float *Q, const float *K, const float 
     MDG_PIPE_TRY(P.init(g, 3 * S, false));
     MDG_PIPE_TRY(P.init(gq, C, pm));
     MDG_PIPE_TRY(P.init(gk, C, pm));
+    // accumulate: contributions land in pinned staging and host threads add
+    // them into the caller's arrays; overwrite: straight into the caller's
+    // arrays (no host pass)
     PinnedStage &stg = pinned_stage();
     const size_t qn = (size_t)C * P.n;
-    MDG_PIPE_TRY(stg.reserve(2 * qn));
-    float *sq = stg.p, *sk = stg.p + qn;  // staging mirrors of gQ, gK
+    if (acc) MDG_PIPE_TRY(stg.reserve(2 * qn));
+    float *sq = acc ? stg.p : gQ, *sk = acc ? stg.p + qn : gK;
     float *dB = nullptr, *dgB = nullptr;
     MDG_PIPE_TRY(P.alloc(&dB, (size_t)S * 27));
     MDG_PIPE_TRY(P.alloc(&dgB, (size_t)S * 27));
     MDG_PIPE_TRY(cudaMemcpyAsync(dB, B, (size_t)S * 27 * sizeof(float), cudaMemcpyHostToDevice, P.up));
-    MDG_PIPE_TRY(cudaMemcpyAsync(dgB, gB, (size_t)S * 27 * sizeof(float), cudaMemcpyHostToDevice, P.up));
+    if (acc)
+        MDG_PIPE_TRY(cudaMemcpyAsync(dgB, gB, (size_t)S * 27 * sizeof(float),
+                                     cudaMemcpyHostToDevice, P.up));
+    else
+        MDG_PIPE_TRY(cudaMemsetAsync(dgB, 0, (size_t)S * 27 * sizeof(float), P.up));
     std::vector<cudaEvent_t> upd(N), cmp(N), dwn(N);
     for (int i = 0; i < N; ++i) {
         MDG_PIPE_TRY(P.upload(q, Q, i));
@@ -561,8 +568,10 @@ mdg_status modet_bwd_host_pipelined(const float *Q, const float *K, const float 
         const double a0 = ms();
         MDG_PIPE_TRY(cudaEventSynchronize(dwn[i]));
         const double a1 = ms();
-        P.add_chunk(gq, gQ, sq, i);
-        P.add_chunk(gk, gK, sk, i);
+        if (acc) {
+            P.add_chunk(gq, gQ, sq, i);
+            P.add_chunk(gk, gK, sk, i);
+        }
         t_wait += a1 - a0;
         t_add += ms() - a1;
     }
@@ -574,8 +583,6 @@ mdg_status modet_bwd_host_pipelined(const float *Q, const float *K, const float 
     return MDG_OK;
 }
 
-// warp: the input volume must be whole before any gather, then the field /
-// upstream-gradient chunks stream in and the per-voxel results stream out
 // ---------------------------------------------------------- warp pipelines
 // The warp's gather (and its backward's scatter) reach is data-dependent, so
 // the field is uploaded first and a device pass computes, per z-chunk, the
@@ -833,7 +840,7 @@ static mdg_status modet_fwd_host_whole(const float *Q, const float *K, const flo
 static mdg_status modet_bwd_host_whole(const float *Q, const float *K, const float *B,
                                        const float *SF, const float *LSE, const float *gSF,
                                        mdg_dims3 d, int S, int hd, int nb, int layout, float *gQ,
-                                       float *gK, float *gB) {
+                                       float *gK, float *gB, bool acc) {
     MDG_REQUIRE(dims_ok(d) && S >= 1 && hd >= 1, "modet: invalid sizes");
     const size_t n = (size_t)nvox(d);
     if (n == 0) return MDG_OK;
@@ -846,11 +853,11 @@ static mdg_status modet_bwd_host_whole(const float *Q, const float *K, const flo
     MDG_STAGE_TRY(sg.get(&dSF, SF, 3 * n * S, true));
     MDG_STAGE_TRY(sg.get(&dL, LSE, n * S, true));
     MDG_STAGE_TRY(sg.get(&dG, gSF, 3 * n * S, true));
-    MDG_STAGE_TRY(sg.get(&dgQ, gQ, n * S * hd, true));  // accumulate targets go up too
-    MDG_STAGE_TRY(sg.get(&dgK, gK, n * S * hd, true));
-    MDG_STAGE_TRY(sg.get(&dgB, gB, (size_t)S * 27, true));
-    mdg_status r =
-        mdg_modet_bwd(dQ, dK, dB, dSF, dL, dG, d, S, hd, nb, layout, dgQ, dgK, dgB, 1, st);
+    MDG_STAGE_TRY(sg.get(&dgQ, gQ, n * S * hd, acc));  // accumulate targets go up too
+    MDG_STAGE_TRY(sg.get(&dgK, gK, n * S * hd, acc));
+    MDG_STAGE_TRY(sg.get(&dgB, gB, (size_t)S * 27, acc));
+    mdg_status r = mdg_modet_bwd(dQ, dK, dB, dSF, dL, dG, d, S, hd, nb, layout, dgQ, dgK, dgB,
+                                 acc ? 1 : 0, st);
     if (r != MDG_OK) return r;
     MDG_STAGE_TRY(sg.down(gQ, dgQ, n * S * hd));
     MDG_STAGE_TRY(sg.down(gK, dgK, n * S * hd));
@@ -872,10 +879,13 @@ mdg_status mdg_modet_fwd_host(const float *Q, const float *K, const float *B, md
 
 mdg_status mdg_modet_bwd_host(const float *Q, const float *K, const float *B, const float *SF,
                               const float *LSE, const float *gSF, mdg_dims3 d, int S, int hd,
-                              int nb, int layout, float *gQ, float *gK, float *gB) {
+                              int nb, int layout, float *gQ, float *gK, float *gB,
+                              int accumulate) {
     if (pipeline_ok(d, nb, layout, Q && K && SF && LSE && gSF && gQ && gK && gB))
-        return modet_bwd_host_pipelined(Q, K, B, SF, LSE, gSF, d, S, hd, layout, gQ, gK, gB);
-    return modet_bwd_host_whole(Q, K, B, SF, LSE, gSF, d, S, hd, nb, layout, gQ, gK, gB);
+        return modet_bwd_host_pipelined(Q, K, B, SF, LSE, gSF, d, S, hd, layout, gQ, gK, gB,
+                                        accumulate != 0);
+    return modet_bwd_host_whole(Q, K, B, SF, LSE, gSF, d, S, hd, nb, layout, gQ, gK, gB,
+                                accumulate != 0);
 }
 
 mdg_status mdg_warp_fwd_host(const float *in, int C, mdg_dims3 d, const float *field,

@@ -319,7 +319,7 @@ def test_host_buffer_calls_match_device_calls(cuda):
     assert np.array_equal(hSF, SF) and np.array_equal(hL, LSE)
     hgQ, hgK, hgB = np.zeros_like(Q), np.zeros_like(K), np.zeros_like(B)
     assert L.mdg_modet_bwd_host(p(Q), p(K), p(B), p(hSF), p(hL), p(gSF), d3, S, hd, 3, 0,
-                                p(hgQ), p(hgK), p(hgB)) == 0
+                                p(hgQ), p(hgK), p(hgB), 1) == 0
     assert np.array_equal(hgQ, gQ) and np.array_equal(hgK, gK) and np.array_equal(hgB, gB)
     hW = np.zeros((S, n, 27), np.float32)
     assert L.mdg_na_fused_fwd_host(p(Q), p(K), p(B), d3, S, hd, 3, p(hW)) == 0
@@ -327,12 +327,14 @@ def test_host_buffer_calls_match_device_calls(cuda):
 
 
 @pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("acc", [1, 0])
 @pytest.mark.parametrize("dims,S,hd", [((128, 96, 100), 1, 6), ((64, 80, 205), 2, 4)])
-def test_pipelined_host_calls_match_device_calls(cuda, layout, dims, S, hd):
+def test_pipelined_host_calls_match_device_calls(cuda, layout, dims, S, hd, acc):
     """Volumes >= 1M voxels take the three-stream z-chunk pipeline inside the
     *_host calls (chunks extended by device-copied halo planes): SF, LSE, gQ,
     gK must equal the whole-volume device call bit for bit, gB to reduction
-    tolerance; the backward accumulates into the caller's buffers."""
+    tolerance; the backward accumulates into the caller's buffers (acc=1) or
+    overwrites them (acc=0)."""
     import ctypes as C
 
     from paper_2403_16526_b200 import _capi
@@ -351,8 +353,11 @@ def test_pipelined_host_calls_match_device_calls(cuda, layout, dims, S, hd):
     gQ0 = f32(r.standard_normal((n, S * hd)))
     gK0 = f32(r.standard_normal((n, S * hd)))
     gB0 = f32(r.standard_normal((S, 27)))
+    z = np.zeros_like
     gQ, gK, gB = ops.modet_bwd(Qd, Kd, dev(B), SF, LSE, dev(gSF), dims, cfg, layout=1,
-                               gQ=dev(f32(gQ0.T)), gK=dev(f32(gK0.T)), gB=dev(gB0))
+                               gQ=dev(f32((gQ0 if acc else z(gQ0)).T)),
+                               gK=dev(f32((gK0 if acc else z(gK0)).T)),
+                               gB=dev(gB0 if acc else z(gB0)))
     SF, LSE, gB = host(SF), host(LSE), host(gB)
     gQ, gK = host(gQ).T, host(gK).T
     Q, K, hgQ, hgK = Qp, Kp, gQ0.copy(), gK0.copy()
@@ -366,7 +371,7 @@ def test_pipelined_host_calls_match_device_calls(cuda, layout, dims, S, hd):
     assert np.array_equal(hSF, SF) and np.array_equal(hL, LSE)
     hgB = gB0.copy()
     assert L.mdg_modet_bwd_host(p(Q), p(K), p(B), p(hSF), p(hL), p(gSF), d3, S, hd, 3, layout,
-                                p(hgQ), p(hgK), p(hgB)) == 0
+                                p(hgQ), p(hgK), p(hgB), acc) == 0
     if layout == 1:
         hgQ, hgK = hgQ.T, hgK.T
     assert np.array_equal(hgQ, gQ) and np.array_equal(hgK, gK)

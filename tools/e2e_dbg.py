@@ -17,7 +17,7 @@ d3 = ops.dims3(bench.DIMS)
 p = lambda t: t.data_ptr()
 calls = [
  lambda: L.mdg_modet_fwd_host(p(pin["Q"]), p(pin["K"]), p(pin["B"]), d3, S, HD, 3, 1, p(outs["SF"]), p(outs["LSE"])),
- lambda: L.mdg_modet_bwd_host(p(pin["Q"]), p(pin["K"]), p(pin["B"]), p(outs["SF"]), p(outs["LSE"]), p(pin["gSF"]), d3, S, HD, 3, 1, p(outs["gQ"]), p(outs["gK"]), p(outs["gB"])),
+ lambda: L.mdg_modet_bwd_host(p(pin["Q"]), p(pin["K"]), p(pin["B"]), p(outs["SF"]), p(outs["LSE"]), p(pin["gSF"]), d3, S, HD, 3, 1, p(outs["gQ"]), p(outs["gK"]), p(outs["gB"]), 0),
  lambda: L.mdg_warp_fwd_host(p(pin["feat"]), CH, d3, p(pin["field"]), p(outs["warped"])),
  lambda: L.mdg_warp_bwd_host(p(pin["feat"]), CH, d3, p(pin["field"]), p(pin["gout"]), p(outs["gin"]), p(outs["gfield"])),
 ]

@@ -19,7 +19,7 @@ d3 = ops.dims3(bench.DIMS)
 p = lambda t: t.data_ptr()
 calls = {
     "modet_fwd_host": lambda: L.mdg_modet_fwd_host(p(host["Q"]), p(host["K"]), p(host["B"]), d3, S, HD, 3, 1, p(outs["SF"]), p(outs["LSE"])),
-    "modet_bwd_host": lambda: L.mdg_modet_bwd_host(p(host["Q"]), p(host["K"]), p(host["B"]), p(outs["SF"]), p(outs["LSE"]), p(host["gSF"]), d3, S, HD, 3, 1, p(outs["gQ"]), p(outs["gK"]), p(outs["gB"])),
+    "modet_bwd_host": lambda: L.mdg_modet_bwd_host(p(host["Q"]), p(host["K"]), p(host["B"]), p(outs["SF"]), p(outs["LSE"]), p(host["gSF"]), d3, S, HD, 3, 1, p(outs["gQ"]), p(outs["gK"]), p(outs["gB"]), 0),
     "warp_fwd_host": lambda: L.mdg_warp_fwd_host(p(host["feat"]), CH, d3, p(host["field"]), p(outs["warped"])),
     "warp_bwd_host": lambda: L.mdg_warp_bwd_host(p(host["feat"]), CH, d3, p(host["field"]), p(host["gout"]), p(outs["gin"]), p(outs["gfield"])),
 }
