@@ -159,6 +159,22 @@ mdg_status enc_in_lrelu_bwd(const float *x, const float *gz, const float *pg, md
                             float *gbeta, cudaStream_t st);
 mdg_status enc_avgpool_fwd(const float *in, int C, mdg_dims3 d, float *out, cudaStream_t st);
 mdg_status enc_avgpool_bwd(const float *gout, int C, mdg_dims3 d, float *gin, cudaStream_t st);
+// optim.cu: AdamOptimizer::step over a whole parameter list in one launch
+// (same per-element double arithmetic as mdg_adam_step: bit-identical)
+struct AdamTensor {
+    float *value;
+    const float *grad;
+    float *m, *v;
+    int64_t n;
+};
+constexpr int kMaxAdamTensors = 80;
+struct AdamList {
+    AdamTensor t[kMaxAdamTensors];
+    int count;
+};
+mdg_status adam_multi(const AdamList &L, double lr, double b1, double b2, double eps, int64_t t,
+                      cudaStream_t st);
+
 namespace enc {
 // encoder_igemm.cu: implicit-GEMM conv for the deep levels
 int igemm_fwd_bn(int cout);  // N tile (32 or 64): the weight padding it needs

@@ -8,12 +8,21 @@
 // Parameters follow ModelParams::all_tensors (engine.hpp:121-133): five
 // encoder blocks {w1,b1,n1g,n1b,w2,b2,n2g,n2b}, then five decoder levels,
 // coarse -> fine, {proj.w,proj.b,ln_g,ln_b,bias_b,reghead.w,reghead.b}.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
 #include "mdg_common.cuh"
 
 using namespace mdg;
+
+namespace {
+__global__ void add_k(float *__restrict__ dst, const float *__restrict__ src, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] += src[i];
+}
+}  // namespace
 
 #define MD_TRY(expr)                      \
     do {                                  \
@@ -29,7 +38,12 @@ struct mdg_model {
     std::vector<float *> params;    // 75, caller-owned
     std::vector<int64_t> sizes;     // elements per tensor
     std::vector<float *> grads, m, v;  // owned (one arena)
+    std::vector<float *> grads_mv;     // the moving-image encoder's own gradients
+    float *grads_base = nullptr, *grads_mv_base = nullptr;
+    int64_t grads_len = 0, enc_len = 0;  // padded floats: all grads / encoder part
     void *arena = nullptr;
+    cudaStream_t s2 = nullptr;           // second stream: the moving-image encoder
+    cudaEvent_t ev[4] = {};
     mdg_encoder *enc_f = nullptr, *enc_m = nullptr;
     mdg_pyramid *pyr = nullptr;
     std::vector<float *> ff, mf, gf, gm;  // features / their gradients (fine -> coarse)
@@ -138,20 +152,44 @@ mdg_status mdg_model_create(mdg_dims3 d, float *const *params, float lambda, int
     pc.ss_steps = 7;
     pc.check_finite = check_finite;
     if ((st = mdg_pyramid_create(&pc, &m->pyr)) != MDG_OK) return fail(st);
-    // arena: grads + Adam moments + features + their grads + phi/gphi/terms
-    int64_t tot = 0;
-    for (int64_t s : m->sizes) tot += (s + 63) / 64 * 64;
+    // arena: grads | moving-encoder grads | Adam moments | features + their
+    // grads | phi/gphi/terms.  Tensors padded to 64 floats; the padding stays
+    // zero, so the gradient blocks can be cleared and summed as flat ranges.
+    int64_t tot = 0, enc = 0;
+    for (size_t i = 0; i < m->sizes.size(); ++i) {
+        const int64_t pad = (m->sizes[i] + 63) / 64 * 64;
+        tot += pad;
+        if (i < 40) enc += pad;
+    }
+    m->grads_len = tot;
+    m->enc_len = enc;
     int64_t feat = 0;
     for (int k = 0; k < kLevels; ++k) feat += (int64_t)(kBase << k) * nvox(dims[k]) + 64;
-    const size_t bytes = ((size_t)3 * tot + 4 * (size_t)feat + 6 * (size_t)m->n + 64) * sizeof(float);
+    const size_t bytes =
+        ((size_t)3 * tot + enc + 4 * (size_t)feat + 6 * (size_t)m->n + 64) * sizeof(float);
     cudaError_t e = cudaMalloc(&m->arena, bytes);
     if (e != cudaSuccess) return fail(status_from_cuda(e, "model arena"));
     cudaMemset(m->arena, 0, bytes);
+    if ((e = cudaStreamCreateWithFlags(&m->s2, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(status_from_cuda(e, "model stream"));
+    for (auto &ev : m->ev)
+        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+            return fail(status_from_cuda(e, "model events"));
     float *p = static_cast<float *>(m->arena);
-    for (auto *vec : {&m->grads, &m->m, &m->v})
-        for (int64_t s : m->sizes) {
+    m->grads_base = p;
+    for (int64_t sz : m->sizes) {
+        m->grads.push_back(p);
+        p += (sz + 63) / 64 * 64;
+    }
+    m->grads_mv_base = p;
+    for (int i = 0; i < 40; ++i) {
+        m->grads_mv.push_back(p);
+        p += (m->sizes[i] + 63) / 64 * 64;
+    }
+    for (auto *vec : {&m->m, &m->v})
+        for (int64_t sz : m->sizes) {
             vec->push_back(p);
-            p += (s + 63) / 64 * 64;
+            p += (sz + 63) / 64 * 64;
         }
     for (auto *vec : {&m->ff, &m->mf, &m->gf, &m->gm})
         for (int k = 0; k < kLevels; ++k) {
@@ -173,6 +211,9 @@ void mdg_model_destroy(mdg_model *m) {
     if (m->enc_m) mdg_encoder_destroy(m->enc_m);
     if (m->pyr) mdg_pyramid_destroy(m->pyr);
     if (m->arena) cudaFree(m->arena);
+    if (m->s2) cudaStreamDestroy(m->s2);
+    for (auto ev : m->ev)
+        if (ev) cudaEventDestroy(ev);
     delete m;
 }
 
@@ -196,9 +237,19 @@ mdg_status mdg_model_loss_step(mdg_model *m, const float *fixed, const float *mo
         lp[k] = mdg_level_params{Q[0], Q[1], Q[2], Q[3], Q[4], Q[5], Q[6]};
         lg[k] = mdg_level_grads{H[0], H[1], H[2], H[3], H[4], H[5], H[6]};
     }
-    // run_loss_step: encoder x2 -> pyramid (coarse -> fine) -> loss
+    std::vector<mdg_block_grads> bgm(kLevels);
+    for (int k = 0; k < kLevels; ++k) {
+        float *const *G = m->grads_mv.data() + 8 * k;
+        bgm[k] = mdg_block_grads{G[0], G[1], G[2], G[3], G[4], G[5], G[6], G[7]};
+    }
+    // run_loss_step: encoder x2 (concurrently: the moving image's on a second
+    // stream) -> pyramid (coarse -> fine) -> loss
+    MDG_CUDA_TRY(cudaEventRecord(m->ev[0], st));
+    MDG_CUDA_TRY(cudaStreamWaitEvent(m->s2, m->ev[0], 0));
+    MD_TRY(mdg_encoder_forward(m->enc_m, moving, bp.data(), m->mf.data(), m->s2));
     MD_TRY(mdg_encoder_forward(m->enc_f, fixed, bp.data(), m->ff.data(), st));
-    MD_TRY(mdg_encoder_forward(m->enc_m, moving, bp.data(), m->mf.data(), st));
+    MDG_CUDA_TRY(cudaEventRecord(m->ev[1], m->s2));
+    MDG_CUDA_TRY(cudaStreamWaitEvent(st, m->ev[1], 0));
     std::vector<const float *> fc(kLevels), mc(kLevels);
     for (int k = 0; k < kLevels; ++k) {
         fc[k] = m->ff[kLevels - 1 - k];
@@ -213,8 +264,8 @@ mdg_status mdg_model_loss_step(mdg_model *m, const float *fixed, const float *mo
         MDG_CUDA_TRY(cudaMemcpyAsync(phi, m->phi, 3 * m->n * sizeof(float), cudaMemcpyDeviceToDevice, st));
     if (!backward) return MDG_OK;
     // zero_grads + tape backward (engine.hpp:332-334)
-    for (size_t i = 0; i < m->grads.size(); ++i)
-        MDG_CUDA_TRY(cudaMemsetAsync(m->grads[i], 0, m->sizes[i] * sizeof(float), st));
+    MDG_CUDA_TRY(cudaMemsetAsync(m->grads_base, 0,
+                                 (size_t)(m->grads_len + m->enc_len) * sizeof(float), st));
     MDG_CUDA_TRY(cudaMemsetAsync(m->gphi, 0, 3 * m->n * sizeof(float), st));
     MD_TRY(mdg_total_loss_bwd(fixed, moving, m->phi, m->d, m->window, m->lambda, 1.0f, m->gphi,
                               nullptr, st));
@@ -234,19 +285,29 @@ mdg_status mdg_model_loss_step(mdg_model *m, const float *fixed, const float *mo
         }
     }
     MD_TRY(mdg_pyramid_backward(m->pyr, m->gphi, lg.data(), gfc.data(), gmc.data(), st));
+    // both encoders' backward concurrently; the moving one into its own
+    // gradient block, summed into the shared weights' gradients after the join
+    MDG_CUDA_TRY(cudaEventRecord(m->ev[2], st));
+    MDG_CUDA_TRY(cudaStreamWaitEvent(m->s2, m->ev[2], 0));
     std::vector<const float *> gfe(m->gf.begin(), m->gf.end()), gme(m->gm.begin(), m->gm.end());
+    MD_TRY(mdg_encoder_backward(m->enc_m, gme.data(), bgm.data(), nullptr, m->s2));
     MD_TRY(mdg_encoder_backward(m->enc_f, gfe.data(), bg.data(), nullptr, st));
-    MD_TRY(mdg_encoder_backward(m->enc_m, gme.data(), bg.data(), nullptr, st));
+    MDG_CUDA_TRY(cudaEventRecord(m->ev[3], m->s2));
+    MDG_CUDA_TRY(cudaStreamWaitEvent(st, m->ev[3], 0));
+    add_k<<<(unsigned)std::min<int64_t>((m->enc_len + 255) / 256, 148 * 4), 256, 0, st>>>(
+        m->grads_base, m->grads_mv_base, m->enc_len);
+    MDG_LAUNCHED();
     return MDG_OK;
 }
 
 mdg_status mdg_model_adam_step(mdg_model *m, double lr, void *stream) {
     MDG_REQUIRE(m, "model: null pointer");
     ++m->t;
-    for (size_t i = 0; i < m->params.size(); ++i)
-        MD_TRY(mdg_adam_step(m->params[i], m->grads[i], m->m[i], m->v[i], m->sizes[i], lr,
-                             m->beta1, m->beta2, m->eps, m->t, stream));
-    return MDG_OK;
+    AdamList L{};
+    L.count = (int)m->params.size();
+    for (int i = 0; i < L.count; ++i)
+        L.t[i] = AdamTensor{m->params[i], m->grads[i], m->m[i], m->v[i], m->sizes[i]};
+    return adam_multi(L, lr, m->beta1, m->beta2, m->eps, m->t, S_(stream));
 }
 
 }  // extern "C"

@@ -29,6 +29,37 @@ __global__ void adam_k(float *__restrict__ value, const float *__restrict__ grad
     }
 }
 
+// every tensor of a parameter list in one launch: grid row = tensor
+__global__ void adam_multi_k(AdamList L, double lr, double b1, double b2, double eps, double bc1,
+                             double bc2) {
+    const AdamTensor &T = L.t[blockIdx.y];
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < T.n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const double g = (double)T.grad[j];
+        const double mj = __dadd_rn(__dmul_rn(b1, (double)T.m[j]), __dmul_rn(1.0 - b1, g));
+        const double vj =
+            __dadd_rn(__dmul_rn(b2, (double)T.v[j]), __dmul_rn(__dmul_rn(1.0 - b2, g), g));
+        T.m[j] = (float)mj;
+        T.v[j] = (float)vj;
+        const double upd = __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mj, bc1)),
+                                     __dadd_rn(__dsqrt_rn(__ddiv_rn(vj, bc2)), eps));
+        T.value[j] = (float)__dsub_rn((double)T.value[j], upd);
+    }
+}
+
+mdg_status adam_multi(const AdamList &L, double lr, double b1, double b2, double eps, int64_t t,
+                      cudaStream_t st) {
+    if (L.count == 0) return MDG_OK;
+    const double bc1 = 1.0 - std::pow(b1, (double)t);
+    const double bc2 = 1.0 - std::pow(b2, (double)t);
+    int64_t mx = 0;
+    for (int i = 0; i < L.count; ++i) mx = std::max(mx, L.t[i].n);
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid1d(mx, 256), 64));
+    adam_multi_k<<<dim3(gx, L.count), 256, 0, st>>>(L, lr, b1, b2, eps, bc1, bc2);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
 __global__ void sgd_k(float *__restrict__ value, const float *__restrict__ grad, int64_t n,
                       double lr) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
