@@ -5,7 +5,7 @@ import torch
 from torch.profiler import profile, ProfilerActivity
 from paper_2403_16526_b200 import ops
 h, w, l = 160, 192, 224
-model = ops.Model([t.cuda() for t in ops.init_model(42)], (h, w, l))
+model = ops.NativeModel([t.cuda() for t in ops.init_model(42)], (h, w, l))
 r = ops.Rng(11)
 f = r.uniform((1, l, w, h)).cuda(); m = r.uniform((1, l, w, h)).cuda()
 for _ in range(2): model.po_step(f, m)
