@@ -54,7 +54,8 @@ typedef enum {
     MDG_OK = 0,
     MDG_EINVAL = 1,
     MDG_ENUMERIC = 2,
-    MDG_ECUDA = 3
+    MDG_ECUDA = 3,
+    MDG_EPARSE = 4 /* parse_error: malformed or truncated files (common.hpp:29-32) */
 } mdg_status;
 
 /* Q/K layouts accepted by the fused tier. */
@@ -383,6 +384,58 @@ mdg_rng *mdg_rng_new(uint64_t seed);
 void mdg_rng_free(mdg_rng *r);
 void mdg_rng_fill_uniform(mdg_rng *r, float *out, int64_t n, double lo, double hi);
 void mdg_rng_fill_normal(mdg_rng *r, float *out, int64_t n, double mean, double sd);
+
+/* ====================== file formats (§8f rank 4) =========================
+ * Host-side, no device needed.  Byte-identical to the reference's writers
+ * and accepting what they write, with the same checks: raw volumes with a
+ * JSON sidecar (io.hpp:23-34, io_raw.cpp) and the MDT2 checkpoint
+ * (io.hpp:40-45, checkpoint.cpp).  Loaders called with a NULL data pointer
+ * fill the header only (to size the buffer). */
+#define MDG_RAW_F32 0
+#define MDG_RAW_U16 1
+typedef struct {
+    mdg_dims3 dims;
+    float spacing[3];
+    int dtype;    /* MDG_RAW_F32 / MDG_RAW_U16 */
+    int channels; /* 1 (volume, labels) or 3 (field) */
+} mdg_raw_header;
+/* load_raw_volume / load_raw_field / load_raw_labels (io_raw.cpp:142-169);
+ * f32 payloads are checked finite; labels are u16 on disk, int here */
+mdg_status mdg_raw_load_volume(const char *json_path, mdg_raw_header *hdr, float *out);
+mdg_status mdg_raw_load_field(const char *json_path, mdg_raw_header *hdr, float *out);
+mdg_status mdg_raw_load_labels(const char *json_path, mdg_raw_header *hdr, int *out);
+/* load_nifti (io.hpp:36-38, nifti.cpp): single-file NIfTI-1 (u8 / i16 / f32,
+ * scl_slope / scl_inter applied when slope != 0) into an f32 volume */
+mdg_status mdg_nifti_load(const char *path, mdg_raw_header *hdr, float *out);
+/* save_raw (io_raw.cpp:120-140): writes <base>.json and <base>.raw */
+mdg_status mdg_raw_save_volume(const char *base, mdg_dims3 d, const float spacing[3],
+                               const float *data);
+mdg_status mdg_raw_save_field(const char *base, mdg_dims3 d, const float *data);
+mdg_status mdg_raw_save_labels(const char *base, mdg_dims3 d, const float spacing[3],
+                               const int *labels);
+
+/* ModelConfig (engine.hpp:30-78) as stored in a checkpoint */
+#define MDG_ENC_LEVELS 5
+typedef struct {
+    int base_channels;
+    float leaky_slope;
+    int heads_per_level[MDG_ENC_LEVELS]; /* coarse -> fine */
+    int head_dim;
+    int neighborhood;
+    int diffeomorphic;
+    int ss_steps;
+} mdg_model_config;
+mdg_status mdg_model_config_small_preset(mdg_model_config *cfg);
+/* ModelParams::all_tensors layout for a config: tensor count, element counts
+ * (sizes nullable); returns the total */
+int64_t mdg_config_param_count(const mdg_model_config *cfg, int *ntensors, int64_t *sizes);
+/* the reference's name of tensor i ("enc.l1.conv1.w", ..., "lvl4.reghead.b") */
+mdg_status mdg_config_tensor_name(const mdg_model_config *cfg, int i, char *buf, int cap);
+/* save_checkpoint / load_checkpoint (checkpoint.cpp:85-145): host tensors in
+ * all_tensors order; load with tensors == NULL reads the config only */
+mdg_status mdg_checkpoint_save(const char *path, const mdg_model_config *cfg,
+                               const float *const *tensors);
+mdg_status mdg_checkpoint_load(const char *path, mdg_model_config *cfg, float *const *tensors);
 
 /* pinned host memory for the host-buffer path */
 void *mdg_host_alloc(size_t bytes);

@@ -13,7 +13,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmdg.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "mdg.h")
 
-MDG_OK, MDG_EINVAL, MDG_ENUMERIC, MDG_ECUDA = 0, 1, 2, 3
+MDG_OK, MDG_EINVAL, MDG_ENUMERIC, MDG_ECUDA, MDG_EPARSE = 0, 1, 2, 3, 4
+MDG_RAW_F32, MDG_RAW_U16 = 0, 1
+ENC_LEVELS = 5
 MDG_QK_POSMAJOR, MDG_QK_PLANAR = 0, 1
 
 
@@ -55,6 +57,21 @@ class LevelGrads(C.Structure):
 
 
 BLOCK_FIELDS = ("w1", "b1", "g1", "be1", "w2", "b2", "g2", "be2")
+
+
+class RawHeader(C.Structure):
+    """mdg_raw_header."""
+
+    _fields_ = [("dims", Dims3), ("spacing", C.c_float * 3), ("dtype", C.c_int),
+                ("channels", C.c_int)]
+
+
+class ModelConfigC(C.Structure):
+    """mdg_model_config (ModelConfig engine.hpp:30-78 as stored in a checkpoint)."""
+
+    _fields_ = [("base_channels", C.c_int), ("leaky_slope", C.c_float),
+                ("heads_per_level", C.c_int * ENC_LEVELS), ("head_dim", C.c_int),
+                ("neighborhood", C.c_int), ("diffeomorphic", C.c_int), ("ss_steps", C.c_int)]
 
 
 class BlockParams(C.Structure):
@@ -136,6 +153,19 @@ SIGNATURES = {
     "mdg_modet_bwd_host": (_st, [_p, _p, _p, _p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p, _i]),
     "mdg_warp_fwd_host": (_st, [_p, _i, Dims3, _p, _p]),
     "mdg_warp_bwd_host": (_st, [_p, _i, Dims3, _p, _p, _p, _p]),
+    "mdg_raw_load_volume": (_st, [C.c_char_p, C.POINTER(RawHeader), _p]),
+    "mdg_raw_load_field": (_st, [C.c_char_p, C.POINTER(RawHeader), _p]),
+    "mdg_raw_load_labels": (_st, [C.c_char_p, C.POINTER(RawHeader), _p]),
+    "mdg_nifti_load": (_st, [C.c_char_p, C.POINTER(RawHeader), _p]),
+    "mdg_raw_save_volume": (_st, [C.c_char_p, Dims3, C.POINTER(C.c_float), _p]),
+    "mdg_raw_save_field": (_st, [C.c_char_p, Dims3, _p]),
+    "mdg_raw_save_labels": (_st, [C.c_char_p, Dims3, C.POINTER(C.c_float), _p]),
+    "mdg_model_config_small_preset": (_st, [C.POINTER(ModelConfigC)]),
+    "mdg_config_param_count": (C.c_int64, [C.POINTER(ModelConfigC), C.POINTER(_i),
+                                           C.POINTER(C.c_int64)]),
+    "mdg_config_tensor_name": (_st, [C.POINTER(ModelConfigC), _i, C.c_char_p, _i]),
+    "mdg_checkpoint_save": (_st, [C.c_char_p, C.POINTER(ModelConfigC), C.POINTER(_p)]),
+    "mdg_checkpoint_load": (_st, [C.c_char_p, C.POINTER(ModelConfigC), C.POINTER(_p)]),
     "mdg_rng_new": (_p, [C.c_uint64]),
     "mdg_rng_free": (None, [_p]),
     "mdg_rng_fill_uniform": (None, [_p, _p, C.c_int64, C.c_double, C.c_double]),

@@ -36,6 +36,10 @@ class NumericError(RuntimeError):
     position = None  # (x, y, z, head) for attention errors
 
 
+class ParseError(RuntimeError):
+    """mdreg::parse_error — malformed or truncated files (common.hpp:29-32)."""
+
+
 class CudaError(RuntimeError):
     """A CUDA runtime failure inside libmdg."""
 
@@ -47,6 +51,8 @@ def _check(status: int):
     msg = L.mdg_last_error().decode()
     if status == _capi.MDG_EINVAL:
         raise InvalidInput(msg)
+    if status == _capi.MDG_EPARSE:
+        raise ParseError(msg)
     if status == _capi.MDG_ENUMERIC:
         e = NumericError(msg)
         pos = [C.c_int() for _ in range(4)]
@@ -951,3 +957,137 @@ class Rng:
         out = torch.empty(shape, dtype=torch.float32) if out is None else out
         self._L.mdg_rng_fill_normal(self._h, out.data_ptr(), out.numel(), mean, sd)
         return out
+
+
+# ------------------------------------------------------------- file formats
+# The reference's raw volume + JSON sidecar (io_raw.cpp) and MDT2 checkpoint
+# (checkpoint.cpp) through libmdg's native readers / writers: host numpy
+# arrays in the reference layouts ({l, w, h} volumes, {3, l, w, h} fields).
+def _raw_load(fn, path, dtype, channels):
+    import numpy as np
+
+    L = _capi.lib()
+    h = _capi.RawHeader()
+    _check(getattr(L, fn)(str(path).encode(), C.byref(h), None))
+    d = h.dims
+    shape = ((channels,) if channels > 1 else ()) + (d.l, d.w, d.h)
+    out = np.empty(shape, dtype=dtype)
+    _check(getattr(L, fn)(str(path).encode(), C.byref(h), out.ctypes.data_as(C.c_void_p)))
+    return out, tuple(float(v) for v in h.spacing)
+
+
+def load_raw_volume(json_path):
+    """load_raw_volume (io_raw.cpp:142-152) -> (f32 {l,w,h}, spacing)."""
+    import numpy as np
+
+    return _raw_load("mdg_raw_load_volume", json_path, np.float32, 1)
+
+
+def load_raw_field(json_path):
+    """load_raw_field (io_raw.cpp:160-169) -> f32 {3,l,w,h}."""
+    import numpy as np
+
+    return _raw_load("mdg_raw_load_field", json_path, np.float32, 3)[0]
+
+
+def load_raw_labels(json_path):
+    """load_raw_labels (io_raw.cpp:154-158) -> (int32 {l,w,h}, spacing)."""
+    import numpy as np
+
+    return _raw_load("mdg_raw_load_labels", json_path, np.int32, 1)
+
+
+def load_nifti(path):
+    """load_nifti (nifti.cpp:36-105) -> (f32 {l,w,h}, spacing)."""
+    import numpy as np
+
+    return _raw_load("mdg_nifti_load", path, np.float32, 1)
+
+
+def _dims_of(a, channels):
+    if a.ndim != 3 + (1 if channels > 1 else 0):
+        raise InvalidInput("raw: array rank does not match")
+    ll, w, h = a.shape[-3:]
+    return Dims3(h, w, ll)
+
+
+def save_raw_volume(base, vol, spacing=(1.0, 1.0, 1.0)):
+    import numpy as np
+
+    a = np.ascontiguousarray(vol, dtype=np.float32)
+    sp = (C.c_float * 3)(*spacing)
+    _check(_capi.lib().mdg_raw_save_volume(str(base).encode(), _dims_of(a, 1), sp,
+                                           a.ctypes.data_as(C.c_void_p)))
+
+
+def save_raw_field(base, field):
+    import numpy as np
+
+    a = np.ascontiguousarray(field, dtype=np.float32)
+    _check(_capi.lib().mdg_raw_save_field(str(base).encode(), _dims_of(a, 3),
+                                          a.ctypes.data_as(C.c_void_p)))
+
+
+def save_raw_labels(base, labels, spacing=(1.0, 1.0, 1.0)):
+    import numpy as np
+
+    a = np.ascontiguousarray(labels, dtype=np.int32)
+    sp = (C.c_float * 3)(*spacing)
+    _check(_capi.lib().mdg_raw_save_labels(str(base).encode(), _dims_of(a, 1), sp,
+                                           a.ctypes.data_as(C.c_void_p)))
+
+
+def model_config(base_channels=8, leaky_slope=0.2, heads_per_level=(8, 4, 2, 1, 1), head_dim=6,
+                 neighborhood=3, diffeomorphic=False, ss_steps=7):
+    """A checkpoint ModelConfig (defaults: small_preset, engine.hpp:38-44)."""
+    c = _capi.ModelConfigC()
+    c.base_channels, c.leaky_slope = int(base_channels), float(leaky_slope)
+    for i, v in enumerate(heads_per_level):
+        c.heads_per_level[i] = int(v)
+    c.head_dim, c.neighborhood = int(head_dim), int(neighborhood)
+    c.diffeomorphic, c.ss_steps = 1 if diffeomorphic else 0, int(ss_steps)
+    return c
+
+
+def config_tensors(cfg):
+    """(names, sizes) of ModelParams::all_tensors for a config."""
+    L = _capi.lib()
+    nt = C.c_int(0)
+    L.mdg_config_param_count(C.byref(cfg), C.byref(nt), None)
+    sizes = (C.c_int64 * nt.value)()
+    L.mdg_config_param_count(C.byref(cfg), None, sizes)
+    names = []
+    buf = C.create_string_buffer(128)
+    for i in range(nt.value):
+        _check(L.mdg_config_tensor_name(C.byref(cfg), i, buf, 128))
+        names.append(buf.value.decode())
+    return names, [int(s) for s in sizes]
+
+
+def save_checkpoint(path, tensors, cfg=None):
+    """save_checkpoint (checkpoint.cpp:85-104): host float32 tensors in
+    all_tensors order (numpy or CPU torch)."""
+    import numpy as np
+
+    cfg = cfg or model_config()
+    arrs = [np.ascontiguousarray(np.asarray(t), dtype=np.float32) for t in tensors]
+    names, sizes = config_tensors(cfg)
+    if len(arrs) != len(sizes) or any(a.size != s for a, s in zip(arrs, sizes)):
+        raise InvalidInput("checkpoint: tensors do not match the config's layout")
+    ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    _check(_capi.lib().mdg_checkpoint_save(str(path).encode(), C.byref(cfg), ptrs))
+
+
+def load_checkpoint(path):
+    """load_checkpoint (checkpoint.cpp:106-145) -> (config, [float32 arrays],
+    names)."""
+    import numpy as np
+
+    L = _capi.lib()
+    cfg = _capi.ModelConfigC()
+    _check(L.mdg_checkpoint_load(str(path).encode(), C.byref(cfg), None))
+    names, sizes = config_tensors(cfg)
+    arrs = [np.empty(s, dtype=np.float32) for s in sizes]
+    ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    _check(L.mdg_checkpoint_load(str(path).encode(), C.byref(cfg), ptrs))
+    return cfg, arrs, names
