@@ -117,6 +117,14 @@ mdg_status mdg_warp_fwd(const float *in, int C, mdg_dims3 d, const float *field,
 /* sampling.hpp:139-167 kern::warp_bwd (accumulates; gin/gfield nullable) */
 mdg_status mdg_warp_bwd(const float *in, int C, mdg_dims3 d, const float *field,
                         const float *gout, float *gin, float *gfield, void *stream);
+/* the same two calls over the voxel range [pb, pe) only (arrays full-size,
+ * global coordinates): a z-slab's share (depth-slab decomposition) or a
+ * pipeline chunk.  Bit-identical per voxel to the whole-volume calls. */
+mdg_status mdg_warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *field,
+                              float *out, int64_t pb, int64_t pe, void *stream);
+mdg_status mdg_warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *field,
+                              const float *gout, float *gin, float *gfield, int64_t pb,
+                              int64_t pe, void *stream);
 /* sampling.hpp:225-242 kern::upsample2_fwd (target range checked as in
  * sampling.hpp:266-271 -> MDG_EINVAL) */
 mdg_status mdg_upsample2_fwd(const float *in, int C, mdg_dims3 d, mdg_dims3 td, float scale,

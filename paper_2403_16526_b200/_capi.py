@@ -110,6 +110,8 @@ SIGNATURES = {
     "mdg_upsample2_bwd": (_st, [_i, Dims3, Dims3, _f, _p, _p, _p]),
     "mdg_conv3_fwd": (_st, [_p, _i, Dims3, _p, _p, _i, _p, _p]),
     "mdg_conv3_bwd": (_st, [_p, _i, Dims3, _p, _i, _p, _p, _p, _p, _p]),
+    "mdg_warp_fwd_range": (_st, [_p, _i, Dims3, _p, _p, C.c_int64, C.c_int64, _p]),
+    "mdg_warp_bwd_range": (_st, [_p, _i, Dims3, _p, _p, _p, _p, C.c_int64, C.c_int64, _p]),
     "mdg_compose_fwd": (_st, [_p, _p, Dims3, _p, _p]),
     "mdg_compose_bwd": (_st, [_p, _p, Dims3, _p, _p, _p, _p]),
     "mdg_scaling_squaring_fwd": (_st, [_p, Dims3, _i, _p, _p, _p]),

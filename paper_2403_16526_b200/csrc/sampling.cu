@@ -591,6 +591,27 @@ mdg_status mdg_warp_bwd(const float *in, int C, mdg_dims3 d, const float *field,
     return warp_bwd_range(in, C, d, field, gout, gin, gfield, 0, n, S_(stream));
 }
 
+mdg_status mdg_warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *field,
+                              float *out, int64_t pb, int64_t pe, void *stream) {
+    if (mdg_status e = check_field_dims(d, "warp")) return e;
+    MDG_REQUIRE(C >= 0, "warp: channels must be >= 0");
+    MDG_REQUIRE(0 <= pb && pb <= pe && pe <= nvox(d), "warp: voxel range out of bounds");
+    if (pe == pb || C == 0) return MDG_OK;
+    MDG_REQUIRE(in && field && out, "warp: null pointer");
+    return warp_fwd_range(in, C, d, field, out, pb, pe, S_(stream));
+}
+
+mdg_status mdg_warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *field,
+                              const float *gout, float *gin, float *gfield, int64_t pb,
+                              int64_t pe, void *stream) {
+    if (mdg_status e = check_field_dims(d, "warp")) return e;
+    MDG_REQUIRE(C >= 0, "warp: channels must be >= 0");
+    MDG_REQUIRE(0 <= pb && pb <= pe && pe <= nvox(d), "warp: voxel range out of bounds");
+    if (pe == pb || C == 0 || (!gin && !gfield)) return MDG_OK;
+    MDG_REQUIRE(in && field && gout, "warp: null pointer");
+    return warp_bwd_range(in, C, d, field, gout, gin, gfield, pb, pe, S_(stream));
+}
+
 mdg_status mdg_compose_fwd(const float *prev, const float *res, mdg_dims3 d, float *out,
                            void *stream) {
     if (mdg_status e = check_field_dims(d, "compose")) return e;

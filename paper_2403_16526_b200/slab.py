@@ -210,3 +210,189 @@ class SlabModeT:
         if s.world > 1:
             self.all_reduce(gB)
         return interior(gQx), interior(gKx), gB
+
+
+# ----------------------------------------------------------------- the warp
+# The trilinear warp's reach is data-dependent: voxel p reads (and its
+# backward scatters into) the z rows floor(z + phi_z) and +1, so a slab needs
+# R = ceil(max |phi_z|) + 1 planes beyond each face ("Warp:
+# ceil(max|phi_z|)+1 planes after an ncclAllReduce(max)").  R is all-reduced
+# so every rank knows every other rank's range; planes then move point to
+# point between the owning and the needing ranks (a halo may span several
+# slabs when R exceeds a slab's depth).  Each rank runs the warp kernels over
+# its own voxel range in GLOBAL coordinates (full-size buffers, global dims),
+# so clamping and the boundary rules are the whole-volume ones: out and
+# gfield are identical to the whole-volume call.  The scattered input
+# gradient's contributions to other ranks' planes are sent back and summed by
+# the owner in rank order.
+
+
+def warp_reach(field_local: torch.Tensor, l: int) -> int:
+    """ceil(max |phi_z|) + 1 over this rank's voxels (the whole depth if any
+    z displacement is non-finite)."""
+    fz = field_local[2]
+    if fz.numel() == 0:
+        return 1
+    if not bool(torch.isfinite(fz).all()):
+        return l
+    return min(l, int(torch.ceil(fz.abs().max()).item()) + 1)
+
+
+def _need(sl: Slab, z0: int, z1: int, R: int):
+    return max(0, z0 - R), min(sl.l, z1 + R)
+
+
+def _p2p(ops_list):
+    if ops_list:
+        for req in dist.batch_isend_irecv(ops_list):
+            req.wait()
+
+
+def exchange_planes(x: torch.Tensor, sl: Slab, R: int, group=None) -> torch.Tensor:
+    """Global planes [z0-R, z1+R) (clipped) of a {C, depth, w, h} slab-local
+    tensor, gathered from their owners."""
+    ranges = split(sl.l, sl.world)
+    lo, hi = _need(sl, sl.z0, sl.z1, R)
+    C = x.shape[0]
+    out = torch.empty(C, hi - lo, sl.w, sl.h, dtype=x.dtype, device=x.device)
+    out[:, sl.z0 - lo:sl.z1 - lo] = x
+    ops_list, keep = [], []
+    for q, (a, b) in enumerate(ranges):
+        if q == sl.rank:
+            continue
+        qlo, qhi = _need(sl, a, b, R)
+        s0, s1 = max(sl.z0, qlo), min(sl.z1, qhi)  # mine, needed by q
+        if s0 < s1:
+            t = x[:, s0 - sl.z0:s1 - sl.z0].contiguous()
+            keep.append(t)
+            ops_list.append(dist.P2POp(dist.isend, t, q, group))
+        r0, r1 = max(a, lo), min(b, hi)  # q's, needed by me
+        if r0 < r1:
+            t = torch.empty(C, r1 - r0, sl.w, sl.h, dtype=x.dtype, device=x.device)
+            keep.append((t, r0))
+            ops_list.append(dist.P2POp(dist.irecv, t, q, group))
+    _p2p(ops_list)
+    for item in keep:
+        if isinstance(item, tuple):
+            t, r0 = item
+            out[:, r0 - lo:r0 - lo + t.shape[1]] = t
+    return out
+
+
+def reduce_planes(contrib: torch.Tensor, sl: Slab, R: int, group=None) -> torch.Tensor:
+    """contrib: this rank's additions to the global planes [z0-R, z1+R)
+    (clipped).  Returns this rank's planes summed over all ranks' additions,
+    in rank order."""
+    ranges = split(sl.l, sl.world)
+    lo, hi = _need(sl, sl.z0, sl.z1, R)
+    ops_list, recvd = [], {}
+    for q, (a, b) in enumerate(ranges):
+        if q == sl.rank:
+            continue
+        s0, s1 = max(a, lo), min(b, hi)  # my additions to q's planes
+        if s0 < s1:
+            ops_list.append(dist.P2POp(dist.isend, contrib[:, s0 - lo:s1 - lo].contiguous(), q,
+                                       group))
+        qlo, qhi = _need(sl, a, b, R)
+        r0, r1 = max(sl.z0, qlo), min(sl.z1, qhi)  # q's additions to mine
+        if r0 < r1:
+            t = torch.empty(contrib.shape[0], r1 - r0, sl.w, sl.h, dtype=contrib.dtype,
+                            device=contrib.device)
+            recvd[q] = (t, r0)
+            ops_list.append(dist.P2POp(dist.irecv, t, q, group))
+    _p2p(ops_list)
+    out = torch.zeros(contrib.shape[0], sl.depth, sl.w, sl.h, dtype=contrib.dtype,
+                      device=contrib.device)
+    for q in range(sl.world):  # fixed order
+        if q == sl.rank:
+            out += contrib[:, sl.z0 - lo:sl.z1 - lo]
+        elif q in recvd:
+            t, r0 = recvd[q]
+            out[:, r0 - sl.z0:r0 - sl.z0 + t.shape[1]] += t
+    return out
+
+
+class CudaWarp:
+    """Product backend: libmdg's warp kernels over a voxel range of full-size
+    buffers (mdg_warp_fwd_range / mdg_warp_bwd_range)."""
+
+    def fwd_range(self, vol, field, out, dims, pb, pe):
+        from . import ops
+
+        L = ops._capi.lib()
+        P = ops._ptr
+        ops._check(L.mdg_warp_fwd_range(P(vol), vol.shape[0], ops.dims3(dims), P(field), P(out),
+                                        pb, pe, ops._stream()))
+
+    def bwd_range(self, vol, field, gout, gin, gfield, dims, pb, pe):
+        from . import ops
+
+        L = ops._capi.lib()
+        P = ops._ptr
+        ops._check(L.mdg_warp_bwd_range(P(vol), vol.shape[0], ops.dims3(dims), P(field), P(gout),
+                                        P(gin), P(gfield), pb, pe, ops._stream()))
+
+
+class SlabWarp:
+    """Trilinear warp forward/backward on this rank's z-slab.  in {C, depth,
+    w, h}, field {3, depth, w, h} (this rank's voxels' displacements, global
+    voxel units); forward returns the rank's warped planes, backward (of the
+    last forward) the rank's gin and gfield (fresh, not accumulated)."""
+
+    def __init__(self, slab: Slab, backend=None, group=None, exchange=None, reduce=None,
+                 all_reduce_max=None):
+        self.slab = slab
+        self.be = backend if backend is not None else CudaWarp()
+        self.group = group
+        self.exchange = exchange or (lambda name, x, sl, R: exchange_planes(x, sl, R, group))
+        self.reduce = reduce or (lambda name, c, sl, R: reduce_planes(c, sl, R, group))
+
+        def _max(v):
+            t = torch.tensor([v], dtype=torch.int64)
+            if slab.world > 1:
+                if dist.get_backend(group) == "nccl":
+                    t = t.cuda()
+                dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+            return int(t.item())
+
+        self.all_reduce_max = all_reduce_max or _max
+        self._saved = None
+
+    def _full(self, C, ref):
+        s = self.slab
+        return torch.zeros(C, s.l, s.w, s.h, dtype=ref.dtype, device=ref.device)
+
+    def forward(self, vol, field):
+        s = self.slab
+        R = self.all_reduce_max(warp_reach(field, s.l))
+        lo, hi = _need(s, s.z0, s.z1, R)
+        C = vol.shape[0]
+        vol_full, field_full = self._full(C, vol), self._full(3, field)
+        vol_full[:, lo:hi] = self.exchange("in", vol, s, R)
+        field_full[:, s.z0:s.z1] = field
+        out_full = self._full(C, vol)
+        hw = s.h * s.w
+        dims = (s.h, s.w, s.l)
+        self.be.fwd_range(vol_full, field_full, out_full, dims, s.z0 * hw, s.z1 * hw)
+        self._saved = (vol_full, field_full, R)
+        return out_full[:, s.z0:s.z1].contiguous()
+
+    def backward_local(self, gout):
+        """(this rank's gin additions to planes [z0-R, z1+R), its gfield)"""
+        if self._saved is None:
+            raise RuntimeError("slab: backward without forward")
+        vol_full, field_full, R = self._saved
+        s = self.slab
+        gout_full, gin_full = self._full(vol_full.shape[0], gout), self._full(vol_full.shape[0], gout)
+        gfield_full = self._full(3, gout)
+        gout_full[:, s.z0:s.z1] = gout
+        hw = s.h * s.w
+        self.be.bwd_range(vol_full, field_full, gout_full, gin_full, gfield_full,
+                          (s.h, s.w, s.l), s.z0 * hw, s.z1 * hw)
+        lo, hi = _need(s, s.z0, s.z1, R)
+        return gin_full[:, lo:hi].contiguous(), gfield_full[:, s.z0:s.z1].contiguous()
+
+    def backward(self, gout):
+        contrib, gfield = self.backward_local(gout)
+        gin = self.reduce("gin", contrib, self.slab, self._saved[2])
+        return gin, gfield

@@ -65,3 +65,52 @@ def test_slab_modet_cuda_matches_full_volume(cuda, world, dims, S, hd):
     assert np.array_equal(cat([o[1] for o in outs]), full(gK))
     gB_sum = sum(o[2] for o in outs)  # the all-reduce, done by hand here
     assert np.allclose(gB_sum.cpu().numpy(), gB.cpu().numpy(), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("world,dims,C,zreach", [(2, (20, 12, 16), 8, 2.5), (4, (16, 9, 12), 3, 4.2)])
+def test_slab_warp_cuda_matches_full_volume(cuda, world, dims, C, zreach):
+    """SlabWarp with the libmdg range kernels, ranks run in turn with a
+    simulated plane exchange / reduction: out and gfield equal the
+    whole-volume warp bit for bit, gin to atomic-order tolerance."""
+    h, w, l = dims
+    r = np.random.default_rng(9)
+    vol = torch.from_numpy(f32(r.standard_normal((C, l, w, h)))).cuda()
+    fld = torch.from_numpy(f32(np.stack([r.uniform(-1.5, 1.5, (l, w, h)),
+                                         r.uniform(-1.5, 1.5, (l, w, h)),
+                                         r.uniform(-zreach, zreach, (l, w, h))]))).cuda()
+    gout = torch.from_numpy(f32(r.standard_normal((C, l, w, h)))).cuda()
+    out = ops.warp(vol, fld)
+    gin, gfield = ops.warp_bwd(vol, fld, gout)
+
+    slabs = [slabmod.Slab(h, w, l, world, rk) for rk in range(world)]
+    R = max(slabmod.warp_reach(sl.local(fld), l) for sl in slabs)
+
+    def exchange(name, x, sl, R_):
+        lo, hi = max(0, sl.z0 - R_), min(l, sl.z1 + R_)
+        return vol[:, lo:hi].clone()  # what the owners would send
+
+    contribs = {}
+
+    def reduce(name, c, sl, R_):
+        acc = torch.zeros(c.shape[0], sl.depth, w, h, device=c.device)
+        for q in slabs:  # rank order, as reduce_planes
+            cq = contribs[q.rank]
+            qlo = max(0, q.z0 - R_)
+            a, b = max(sl.z0, qlo), min(sl.z1, qlo + cq.shape[1])
+            if a < b:
+                acc[:, a - sl.z0:b - sl.z0] += cq[:, a - qlo:b - qlo]
+        return acc
+
+    mods = [slabmod.SlabWarp(sl, exchange=exchange, reduce=reduce, all_reduce_max=lambda v: R)
+            for sl in slabs]
+    outs = [m.forward(sl.local(vol), sl.local(fld)) for m, sl in zip(mods, slabs)]
+    loc = [m.backward_local(sl.local(gout)) for m, sl in zip(mods, slabs)]
+    for sl, (c, _) in zip(slabs, loc):
+        contribs[sl.rank] = c
+    gins = [reduce("gin", loc[i][0], sl, R) for i, sl in enumerate(slabs)]
+    torch.cuda.synchronize()
+    cat = lambda ts: np.concatenate([t.cpu().numpy() for t in ts], axis=1)  # noqa: E731
+    full = lambda t: t.reshape(t.shape[0], l, w, h).cpu().numpy()  # noqa: E731
+    assert R > 1 and np.array_equal(cat(outs), full(out))
+    assert np.array_equal(cat([g for _, g in loc]), full(gfield))
+    assert np.allclose(cat(gins), full(gin), rtol=1e-5, atol=1e-5)

@@ -127,3 +127,80 @@ def test_slab_modet_over_gloo_matches_full_volume(oracle, tmp_path, world, dims,
     for p in parts:  # all-reduced: identical on every rank
         assert np.array_equal(p["gB"], parts[0]["gB"])
     assert np.allclose(parts[0]["gB"], gB.numpy(), rtol=1e-5, atol=1e-6)
+
+
+# ------------------------------------------------------------ slab warp
+class OracleWarp:
+    """Test backend for SlabWarp: the CPU oracle's whole-volume warp, used
+    over the rank's voxel range only."""
+
+    def __init__(self):
+        import pyoracle
+
+        self.m = pyoracle.mdo()
+
+    def fwd_range(self, vol, field, out, dims, pb, pe):
+        o = self.m.warp_fwd(f32(vol.numpy()), f32(field.numpy()))
+        C = vol.shape[0]
+        out.view(C, -1)[:, pb:pe] = torch.from_numpy(o.reshape(C, -1)[:, pb:pe])
+
+    def bwd_range(self, vol, field, gout, gin, gfield, dims, pb, pe):
+        gi, gf = self.m.warp_bwd(f32(vol.numpy()), f32(field.numpy()), f32(gout.numpy()))
+        gin += torch.from_numpy(gi)
+        gfield.view(3, -1)[:, pb:pe] = torch.from_numpy(gf.reshape(3, -1)[:, pb:pe])
+
+
+def _warp_case(dims, C, seed, zreach):
+    h, w, l = dims
+    r = np.random.default_rng(seed)
+    vol = f32(r.standard_normal((C, l, w, h)))
+    fld = f32(np.stack([r.uniform(-1.5, 1.5, (l, w, h)), r.uniform(-1.5, 1.5, (l, w, h)),
+                        r.uniform(-zreach, zreach, (l, w, h))]))
+    gout = f32(r.standard_normal((C, l, w, h)))
+    return vol, fld, gout
+
+
+def _warp_worker(rank, world, port, dims, C, zreach, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        vol, fld, gout = (torch.from_numpy(a) for a in _warp_case(dims, C, 21, zreach))
+        sl = slabmod.Slab(*dims, world=world, rank=rank)
+        op = slabmod.SlabWarp(sl, backend=OracleWarp())
+        out = op.forward(sl.local(vol), sl.local(fld))
+        gin, gfield = op.backward(sl.local(gout))
+        np.savez(os.path.join(out_dir, f"w{rank}.npz"), out=out.numpy(), gin=gin.numpy(),
+                 gfield=gfield.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dims,C,zreach", [(2, (6, 5, 7), 3, 1.7), (3, (5, 4, 9), 2, 3.6)])
+def test_slab_warp_over_gloo_matches_full_volume(oracle, tmp_path, world, dims, C, zreach):
+    """z reach all-reduced, planes gathered from (possibly several) owning
+    ranks, the scattered input gradient returned to its owners: out and
+    gfield bit for bit, gin to summation-order tolerance."""
+    mp.start_processes(_warp_worker, args=(world, _free_port(), dims, C, zreach, str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    vol, fld, gout = _warp_case(dims, C, 21, zreach)
+    be = OracleWarp()
+    out = be.m.warp_fwd(vol, fld)
+    gin, gfield = be.m.warp_bwd(vol, fld, gout)
+    parts = [dict(np.load(tmp_path / f"w{r}.npz")) for r in range(world)]
+    cat = lambda k: np.concatenate([p[k] for p in parts], axis=1)  # noqa: E731
+    assert np.array_equal(cat("out"), out)
+    assert np.array_equal(cat("gfield"), gfield)
+    assert np.allclose(cat("gin"), gin, rtol=1e-5, atol=1e-5)
+
+
+def test_warp_reach():
+    f = torch.zeros(3, 4, 3, 3)
+    assert slabmod.warp_reach(f, 10) == 1
+    f[2, 1, 1, 1] = -2.3
+    assert slabmod.warp_reach(f, 10) == 4
+    f[2, 0, 0, 0] = float("nan")
+    assert slabmod.warp_reach(f, 10) == 10
