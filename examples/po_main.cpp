@@ -1,7 +1,7 @@
 // po_main.cpp — pairwise optimisation (engine.hpp:377-411) of the small-preset
 // model driven from C++ through include/mdg.h alone: no Python, no PyTorch.
 //
-//   po_main [h w l] [--iters N] [--lr X] [--seed S] [--pairs P] [--quiet]
+//   po_main [h w l] [--iters N] [--lr X] [--seed S] [--pairs P] [--quiet] [--eager]
 //
 // Per pair: init_model(seed) on the host (the reference Rng stream), upload,
 // then N updates of run_loss_step + Adam and a final evaluation forward; the
@@ -37,7 +37,7 @@
     } while (0)
 
 int main(int argc, char **argv) {
-    int dims[3] = {160, 192, 224}, nd = 0, iters = 50, pairs = 1, quiet = 0;
+    int dims[3] = {160, 192, 224}, nd = 0, iters = 50, pairs = 1, quiet = 0, eager = 0;
     double lr = 1e-4;
     unsigned long long seed = 42;
     for (int i = 1; i < argc; ++i) {
@@ -47,6 +47,7 @@ int main(int argc, char **argv) {
         else if (a == "--seed" && i + 1 < argc) seed = std::strtoull(argv[++i], nullptr, 10);
         else if (a == "--pairs" && i + 1 < argc) pairs = std::atoi(argv[++i]);
         else if (a == "--quiet") quiet = 1;
+        else if (a == "--eager") eager = 1;
         else if (nd < 3) dims[nd++] = std::atoi(a.c_str());
         else {
             std::fprintf(stderr, "usage: %s [h w l] [--iters N] [--lr X] [--seed S] [--pairs P]\n",
@@ -106,8 +107,14 @@ int main(int argc, char **argv) {
         for (int it = 0; it <= iters; ++it) {
             const bool last = it == iters;
             CK(cudaEventRecord(e0, st));
-            MK(mdg_model_loss_step(m, fixed, moving, last ? 0 : 1, terms_d, nullptr, st));
-            if (!last) MK(mdg_model_adam_step(m, lr, st));
+            if (last) {
+                MK(mdg_model_loss_step(m, fixed, moving, 0, terms_d, nullptr, st));
+            } else if (eager) {
+                MK(mdg_model_loss_step(m, fixed, moving, 1, terms_d, nullptr, st));
+                MK(mdg_model_adam_step(m, lr, st));
+            } else {
+                MK(mdg_model_po_step(m, fixed, moving, lr, terms_d, st));  // CUDA graph
+            }
             CK(cudaEventRecord(e1, st));
             CK(cudaMemcpyAsync(terms_h, terms_d, 3 * sizeof(float), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));

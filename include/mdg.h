@@ -295,6 +295,13 @@ mdg_status mdg_model_loss_step(mdg_model *m, const float *fixed, const float *mo
 /* AdamOptimizer::step (engine.hpp:268-298; beta 0.9/0.999, eps 1e-8) over all
  * 75 tensors with the gradients of the last backward */
 mdg_status mdg_model_adam_step(mdg_model *m, double lr, void *stream);
+/* one PO iteration, loss_step(backward) + adam_step, launched as a CUDA graph
+ * captured on the first call and replayed while fixed/moving/terms/lr/stream
+ * stay the same (re-captured otherwise) */
+mdg_status mdg_model_po_step(mdg_model *m, const float *fixed, const float *moving, double lr,
+                             float *terms, void *stream);
+/* the model's field {3, n} of the last loss step (device; valid until the next) */
+const float *mdg_model_phi(const mdg_model *m);
 
 /* ======================== decoding pyramid driver ========================
  * The decoder half of build_pipeline (engine.hpp:179-219) on device-resident

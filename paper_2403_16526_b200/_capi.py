@@ -141,6 +141,8 @@ SIGNATURES = {
     "mdg_model_grads": (C.POINTER(_p), [_p]),
     "mdg_model_loss_step": (_st, [_p, _p, _p, _i, _p, _p, _p]),
     "mdg_model_adam_step": (_st, [_p, C.c_double, _p]),
+    "mdg_model_po_step": (_st, [_p, _p, _p, C.c_double, _p, _p]),
+    "mdg_model_phi": (_p, [_p]),
     "mdg_pyramid_create": (_st, [C.POINTER(PyramidConfig), C.POINTER(_p)]),
     "mdg_pyramid_destroy": (None, [_p]),
     "mdg_pyramid_forward": (_st, [_p, C.POINTER(_p), C.POINTER(_p), C.POINTER(LevelParams), _p,

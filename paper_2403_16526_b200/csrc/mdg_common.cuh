@@ -174,6 +174,10 @@ struct AdamList {
 };
 mdg_status adam_multi(const AdamList &L, double lr, double b1, double b2, double eps, int64_t t,
                       cudaStream_t st);
+// the same with the step count on the device (++*d_t) and the bias
+// corrections from a host-computed table: replayable in a CUDA graph
+mdg_status adam_multi_dev(const AdamList &L, double lr, double b1, double b2, double eps,
+                          int64_t *d_t, const double *d_bc, cudaStream_t st);
 
 namespace enc {
 // encoder_igemm.cu: implicit-GEMM conv for the deep levels

@@ -10,6 +10,8 @@
 // coarse -> fine, {proj.w,proj.b,ln_g,ln_b,bias_b,reghead.w,reghead.b}.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "mdg_common.cuh"
@@ -44,6 +46,26 @@ struct mdg_model {
     void *arena = nullptr;
     cudaStream_t s2 = nullptr;           // second stream: the moving-image encoder
     cudaEvent_t ev[4] = {};
+    // Adam's step count lives on the device (graph replays); bias
+    // corrections 1 - beta^t come from a host-computed table (std::pow)
+    int64_t *d_t = nullptr;
+    double *d_bc = nullptr;
+    int64_t tmax = 0;
+    // CUDA graph of one PO iteration (mdg_model_po_step) and its key
+    cudaGraphExec_t gexec = nullptr;
+    const float *g_fixed = nullptr, *g_moving = nullptr;
+    float *g_terms = nullptr;
+    double g_lr = 0.0;
+    cudaStream_t g_stream = nullptr;
+    int64_t g_tmax = 0;
+    bool graph_off = false;
+    // key of the previous call: capture only on the second consecutive call
+    // with the same key (the first runs eagerly and initialises lazily
+    // allocated device state, which must not happen inside a capture)
+    const float *k_fixed = nullptr, *k_moving = nullptr;
+    float *k_terms = nullptr;
+    double k_lr = -1.0;
+    cudaStream_t k_stream = nullptr;
     mdg_encoder *enc_f = nullptr, *enc_m = nullptr;
     mdg_pyramid *pyr = nullptr;
     std::vector<float *> ff, mf, gf, gm;  // features / their gradients (fine -> coarse)
@@ -175,6 +197,9 @@ mdg_status mdg_model_create(mdg_dims3 d, float *const *params, float lambda, int
     for (auto &ev : m->ev)
         if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
             return fail(status_from_cuda(e, "model events"));
+    if ((e = cudaMalloc(&m->d_t, sizeof(int64_t))) != cudaSuccess)
+        return fail(status_from_cuda(e, "model step counter"));
+    cudaMemset(m->d_t, 0, sizeof(int64_t));
     float *p = static_cast<float *>(m->arena);
     m->grads_base = p;
     for (int64_t sz : m->sizes) {
@@ -212,12 +237,16 @@ void mdg_model_destroy(mdg_model *m) {
     if (m->pyr) mdg_pyramid_destroy(m->pyr);
     if (m->arena) cudaFree(m->arena);
     if (m->s2) cudaStreamDestroy(m->s2);
+    if (m->gexec) cudaGraphExecDestroy(m->gexec);
+    if (m->d_t) cudaFree(m->d_t);
+    if (m->d_bc) cudaFree(m->d_bc);
     for (auto ev : m->ev)
         if (ev) cudaEventDestroy(ev);
     delete m;
 }
 
 float *const *mdg_model_grads(mdg_model *m) { return m ? m->grads.data() : nullptr; }
+const float *mdg_model_phi(const mdg_model *m) { return m ? m->phi : nullptr; }
 
 mdg_status mdg_model_loss_step(mdg_model *m, const float *fixed, const float *moving,
                                int backward, float *terms, float *phi, void *stream) {
@@ -300,14 +329,114 @@ mdg_status mdg_model_loss_step(mdg_model *m, const float *fixed, const float *mo
     return MDG_OK;
 }
 
-mdg_status mdg_model_adam_step(mdg_model *m, double lr, void *stream) {
-    MDG_REQUIRE(m, "model: null pointer");
-    ++m->t;
+// grow the bias-correction table to cover step t (AdamOptimizer::step,
+// engine.hpp:281-282: bc = 1 - beta^t in double with std::pow)
+static mdg_status ensure_bc(mdg_model *m, int64_t t) {
+    if (t <= m->tmax && m->d_bc) return MDG_OK;
+    int64_t cap = std::max<int64_t>(1024, m->tmax);
+    while (cap < t) cap *= 2;
+    std::vector<double> bc(2 * (size_t)cap);
+    for (int64_t i = 1; i <= cap; ++i) {
+        bc[2 * (i - 1)] = 1.0 - std::pow(m->beta1, (double)i);
+        bc[2 * (i - 1) + 1] = 1.0 - std::pow(m->beta2, (double)i);
+    }
+    double *nb = nullptr;
+    MDG_CUDA_TRY(cudaMalloc(&nb, bc.size() * sizeof(double)));
+    MDG_CUDA_TRY(cudaMemcpy(nb, bc.data(), bc.size() * sizeof(double), cudaMemcpyHostToDevice));
+    if (m->d_bc) {
+        cudaDeviceSynchronize();
+        cudaFree(m->d_bc);
+    }
+    m->d_bc = nb;
+    m->tmax = cap;
+    return MDG_OK;
+}
+
+static AdamList adam_list(const mdg_model *m) {
     AdamList L{};
     L.count = (int)m->params.size();
     for (int i = 0; i < L.count; ++i)
         L.t[i] = AdamTensor{m->params[i], m->grads[i], m->m[i], m->v[i], m->sizes[i]};
-    return adam_multi(L, lr, m->beta1, m->beta2, m->eps, m->t, S_(stream));
+    return L;
+}
+
+mdg_status mdg_model_adam_step(mdg_model *m, double lr, void *stream) {
+    MDG_REQUIRE(m, "model: null pointer");
+    ++m->t;
+    MD_TRY(ensure_bc(m, m->t));
+    return adam_multi_dev(adam_list(m), lr, m->beta1, m->beta2, m->eps, m->d_t, m->d_bc,
+                          S_(stream));
+}
+
+// One PO iteration (run_loss_step + AdamOptimizer::step, engine.hpp:389-398)
+// replayed from a CUDA graph: the ~430 launches of both streams are captured
+// once and re-launched as one graph while the inputs, outputs, lr and stream
+// stay the same (the step count is device-side, so replays need no host
+// writes).  A capture failure falls back to eager launches of the same work.
+mdg_status mdg_model_po_step(mdg_model *m, const float *fixed, const float *moving, double lr,
+                             float *terms, void *stream) {
+    MDG_REQUIRE(m && fixed && moving, "model: null pointer");
+    cudaStream_t st = S_(stream);
+    const int64_t t = m->t + 1;
+    MD_TRY(ensure_bc(m, t + 1024));  // table headroom: no re-capture for a while
+    const bool same = m->gexec && fixed == m->g_fixed && moving == m->g_moving &&
+                      terms == m->g_terms && lr == m->g_lr && st == m->g_stream &&
+                      m->tmax == m->g_tmax;
+    if (std::getenv("MDG_GRAPH_TRACE"))
+        std::fprintf(stderr, "po_step t=%lld gexec=%d same=%d off=%d keys %d%d%d%d%d%d\n",
+                     (long long)t, m->gexec != nullptr, same, m->graph_off, fixed == m->g_fixed,
+                     moving == m->g_moving, terms == m->g_terms, lr == m->g_lr,
+                     st == m->g_stream, m->tmax == m->g_tmax);
+    const bool repeat = fixed == m->k_fixed && moving == m->k_moving && terms == m->k_terms &&
+                        lr == m->k_lr && st == m->k_stream;
+    m->k_fixed = fixed;
+    m->k_moving = moving;
+    m->k_terms = terms;
+    m->k_lr = lr;
+    m->k_stream = st;
+    if (!same && repeat && !m->graph_off) {
+        if (m->gexec) cudaGraphExecDestroy(m->gexec);
+        m->gexec = nullptr;
+        cudaGraph_t g = nullptr;
+        bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+        if (ok) {
+            const mdg_status s1 = mdg_model_loss_step(m, fixed, moving, 1, terms, nullptr, st);
+            const mdg_status s2 =
+                s1 == MDG_OK ? adam_multi_dev(adam_list(m), lr, m->beta1, m->beta2, m->eps,
+                                              m->d_t, m->d_bc, st)
+                             : s1;
+            const cudaError_t e = cudaStreamEndCapture(st, &g);
+            const cudaError_t ei = (s2 == MDG_OK && e == cudaSuccess && g)
+                                       ? cudaGraphInstantiate(&m->gexec, g, 0)
+                                       : cudaErrorUnknown;
+            ok = ei == cudaSuccess;
+            if (std::getenv("MDG_GRAPH_TRACE"))
+                std::fprintf(stderr, "capture: loss=%d adam=%d end=%s inst=%s last=%s msg=%s\n",
+                             (int)s1, (int)s2, cudaGetErrorString(e), cudaGetErrorString(ei),
+                             cudaGetErrorString(cudaPeekAtLastError()), mdg_last_error());
+            if (g) cudaGraphDestroy(g);
+        }
+        if (!ok) {
+            cudaGetLastError();  // clear the capture error; run eagerly from now on
+            if (m->gexec) cudaGraphExecDestroy(m->gexec);
+            m->gexec = nullptr;
+            m->graph_off = true;
+        } else {
+            m->g_fixed = fixed;
+            m->g_moving = moving;
+            m->g_terms = terms;
+            m->g_lr = lr;
+            m->g_stream = st;
+            m->g_tmax = m->tmax;
+        }
+    }
+    ++m->t;
+    if (m->gexec && (same || repeat)) {
+        MDG_CUDA_TRY(cudaGraphLaunch(m->gexec, st));
+        return MDG_OK;
+    }
+    MD_TRY(mdg_model_loss_step(m, fixed, moving, 1, terms, nullptr, st));
+    return adam_multi_dev(adam_list(m), lr, m->beta1, m->beta2, m->eps, m->d_t, m->d_bc, st);
 }
 
 }  // extern "C"

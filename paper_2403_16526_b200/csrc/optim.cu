@@ -47,6 +47,42 @@ __global__ void adam_multi_k(AdamList L, double lr, double b1, double b2, double
     }
 }
 
+// device-side step count (graph replays): t = ++*d_t, bias corrections from
+// the host-computed table d_bc[2 (t-1) + {0, 1}] (std::pow, as above)
+__global__ void adam_tick_k(int64_t *d_t) { ++*d_t; }
+
+__global__ void adam_multi_dev_k(AdamList L, double lr, double b1, double b2, double eps,
+                                 const int64_t *__restrict__ d_t, const double *__restrict__ d_bc) {
+    const AdamTensor &T = L.t[blockIdx.y];
+    const int64_t t = *d_t;
+    const double bc1 = d_bc[2 * (t - 1)], bc2 = d_bc[2 * (t - 1) + 1];
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < T.n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const double g = (double)T.grad[j];
+        const double mj = __dadd_rn(__dmul_rn(b1, (double)T.m[j]), __dmul_rn(1.0 - b1, g));
+        const double vj =
+            __dadd_rn(__dmul_rn(b2, (double)T.v[j]), __dmul_rn(__dmul_rn(1.0 - b2, g), g));
+        T.m[j] = (float)mj;
+        T.v[j] = (float)vj;
+        const double upd = __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mj, bc1)),
+                                     __dadd_rn(__dsqrt_rn(__ddiv_rn(vj, bc2)), eps));
+        T.value[j] = (float)__dsub_rn((double)T.value[j], upd);
+    }
+}
+
+mdg_status adam_multi_dev(const AdamList &L, double lr, double b1, double b2, double eps,
+                          int64_t *d_t, const double *d_bc, cudaStream_t st) {
+    adam_tick_k<<<1, 1, 0, st>>>(d_t);
+    MDG_LAUNCHED();
+    if (L.count == 0) return MDG_OK;
+    int64_t mx = 0;
+    for (int i = 0; i < L.count; ++i) mx = std::max(mx, L.t[i].n);
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid1d(mx, 256), 64));
+    adam_multi_dev_k<<<dim3(gx, L.count), 256, 0, st>>>(L, lr, b1, b2, eps, d_t, d_bc);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
 mdg_status adam_multi(const AdamList &L, double lr, double b1, double b2, double eps, int64_t t,
                       cudaStream_t st) {
     if (L.count == 0) return MDG_OK;

@@ -911,10 +911,17 @@ class NativeModel:
                                            _ptr(self._phi), _stream()))
         return self._terms.clone(), self._phi.clone()
 
-    def po_step(self, fixed, moving, lr=1e-4):
-        terms, phi = self.loss_step(fixed, moving, backward=True)
-        _check(self._L.mdg_model_adam_step(self._h, float(lr), _stream()))
-        return terms, phi
+    def po_step(self, fixed, moving, lr=1e-4, graph=True):
+        """loss + backward + Adam; graph=True replays the iteration as one
+        CUDA graph (mdg_model_po_step).  Returns (terms, phi)."""
+        if not graph:
+            terms, phi = self.loss_step(fixed, moving, backward=True)
+            _check(self._L.mdg_model_adam_step(self._h, float(lr), _stream()))
+            return terms, phi
+        _check(self._L.mdg_model_po_step(self._h, _ptr(fixed, "fixed"), _ptr(moving, "moving"),
+                                         float(lr), _ptr(self._terms), _stream()))
+        phi = _wrap_device(self._L.mdg_model_phi(self._h), self._phi.shape, self._phi.device)
+        return self._terms.clone(), phi.clone()
 
 
 def _wrap_device(ptr, shape, device):

@@ -242,3 +242,22 @@ def test_encoder_conv3_fwd_bwd(cuda, ic, oc, dims):
     assert rel_norm((gin - 1).cpu().numpy(), xr.grad.cpu().numpy()) <= 1e-5
     assert rel_norm(gw.cpu().numpy(), wr.grad.cpu().numpy()) <= 1e-5
     assert rel_norm(gb.cpu().numpy(), br.grad.cpu().numpy()) <= 1e-5
+
+
+def test_native_model_graph_replay_matches_eager(cuda, ref):
+    """mdg_model_po_step (one CUDA graph per iteration, step count on the
+    device) follows the eager loss_step + adam_step trajectory."""
+    dims = (16, 16, 16)
+    f, m, lf, lm, gt = ref.synth_pair(dims, seed=3)
+    packed, sizes = perturbed_model(ref, 5)
+    fd, md = torch.from_numpy(f).cuda(), torch.from_numpy(m).cuda()
+    a = ops.NativeModel(device_tensors(packed, sizes), dims)
+    b = ops.NativeModel(device_tensors(packed, sizes), dims)
+    for _ in range(4):
+        ta, pa = a.po_step(fd, md, graph=True)
+        tb, pb = b.po_step(fd, md, graph=False)
+        assert abs(float(ta[0]) - float(tb[0])) <= 1e-5 * abs(float(tb[0])) + 1e-7
+    for i, (x, y) in enumerate(zip(a.tensors, b.tensors)):
+        if i in PRE_NORM_BIAS:  # gradient is cancellation noise; Adam moves it by +-lr
+            continue
+        assert rel_norm(x.cpu().numpy(), y.cpu().numpy()) <= 1e-4, i
