@@ -220,7 +220,10 @@ mdg_status mdg_pyramid_forward(mdg_pyramid *p, const float *const *f_feats,
                               MDG_QK_PLANAR, L.SF, L.LSE, nullptr, st));
         if (c.check_finite) MDG_TRY(mdg_check_numeric(L.d, st));
         float *rh_out = c.diffeomorphic ? L.vel : L.res;
-        MDG_TRY(mdg_conv3_fwd(L.SF, 3 * L.S, L.d, P.rh_w, P.rh_b, 3, rh_out, st));
+        // RegHead conv on the encoder's FMA-contracted kernels (TMA slab /
+        // implicit GEMM): the fused tier's parity is tolerance-based, the
+        // bit-exact reference-order kernel stays behind mdg_conv3_fwd
+        MDG_TRY(enc_conv3_fwd(L.SF, 3 * L.S, L.d, P.rh_w, P.rh_b, 3, rh_out, st));
         if (c.diffeomorphic)
             MDG_TRY(mdg_scaling_squaring_fwd(L.vel, L.d, c.ss_steps, L.res, L.ss_saved, st));
         float *phi_k = (k == c.levels - 1) ? phi : (k == 0 ? L.res : L.phi);
@@ -273,9 +276,9 @@ mdg_status mdg_pyramid_backward(mdg_pyramid *p, const float *gphi, const mdg_lev
             g_rh = p->g_vel;
         }
         // RegHead (reghead.hpp:42-47)
-        MDG_TRY(zero(p->g_sf, 3 * (int64_t)L.S * L.n, st));
-        MDG_TRY(mdg_conv3_bwd(L.SF, 3 * L.S, L.d, P.rh_w, 3, g_rh, p->g_sf,
-                              G ? G->rh_w : nullptr, G ? G->rh_b : nullptr, st));
+        MDG_TRY(enc_conv3_bwd(L.SF, 3 * L.S, L.d, P.rh_w, 3, g_rh, p->g_sf,
+                              G ? G->rh_w : nullptr, G ? G->rh_b : nullptr, st,
+                              /*gin_acc=*/false));
         if (c.check_finite)
             MDG_TRY(check_seq(p, p->g_sf, 3 * (int64_t)L.S * L.n, tag + "subfields", st));
         // ModeT (fused na_fused + subfields backward); gQ/gK overwritten
