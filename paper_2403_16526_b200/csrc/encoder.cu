@@ -165,6 +165,48 @@ conv3g_k(const float *__restrict__ in, int cin, D3 d, const float *__restrict__ 
     }
 }
 
+// per channel: Chan's parallel combination (in double, fixed tile order) of
+// the per-tile (sum, M2) pairs -> mean[c] and inv[c] = 1/sqrt(var + eps),
+// var = M2 / n (op_instance_norm ops.hpp:170-181: biased variance)
+__global__ void __launch_bounds__(256)
+in_stats_k(const float2 *__restrict__ stats, D3 d, int ntx, int nty, int ntz, float eps,
+           float *__restrict__ mean, float *__restrict__ inv) {
+    const int c = blockIdx.x, ntiles = ntx * nty * ntz;
+    const float2 *st = stats + (int64_t)c * ntiles;
+    double n = 0.0, mu = 0.0, m2 = 0.0;
+    for (int t = threadIdx.x; t < ntiles; t += 256) {
+        const int bx = t % ntx, by = (t / ntx) % nty, bz = t / (ntx * nty);
+        const double nb = (double)min(TX, d.h - bx * TX) * min(TY, d.w - by * TY) *
+                          min(TV, d.l - bz * TV);
+        const float2 v = st[t];
+        const double mb = (double)v.x / nb, tot = n + nb, dl = mb - mu;
+        mu += dl * nb / tot;
+        m2 += (double)v.y + dl * dl * n * nb / tot;
+        n = tot;
+    }
+    __shared__ double sn[256], smu[256], sm2[256];
+    sn[threadIdx.x] = n;
+    smu[threadIdx.x] = mu;
+    sm2[threadIdx.x] = m2;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if (threadIdx.x < h) {
+            const double na = sn[threadIdx.x], nb = sn[threadIdx.x + h], tot = na + nb;
+            if (nb > 0.0) {
+                const double dl = smu[threadIdx.x + h] - smu[threadIdx.x];
+                smu[threadIdx.x] += dl * nb / tot;
+                sm2[threadIdx.x] += sm2[threadIdx.x + h] + dl * dl * na * nb / tot;
+                sn[threadIdx.x] = tot;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        mean[c] = (float)smu[0];
+        inv[c] = 1.0f / sqrtf((float)(sm2[0] / sn[0]) + eps);
+    }
+}
+
 // ---- TMA-staged variant (h % 4 == 0, 16-B aligned planes): the chunk's
 // slab is ONE 4-D box load {40, 10, 6, CIB} (x0-4 .. x0+35 so the start is
 // 16-B aligned; faces and missing channels zero-filled by the TMA unit) and
@@ -195,7 +237,8 @@ __device__ __forceinline__ void t_wait(uint64_t *b, unsigned phase) {
 template <bool ACC>
 __global__ void __launch_bounds__(NT, 2)
 conv3t_k(const __grid_constant__ CUtensorMap map, int cin, D3 d, const float *__restrict__ wB,
-         int cpad, const float *__restrict__ bias, int cout, float *__restrict__ out) {
+         int cpad, const float *__restrict__ bias, int cout, float *__restrict__ out,
+         float2 *__restrict__ stats) {
     extern __shared__ __align__(128) float tsm[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(tsm + 2 * TBUF);
     const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
@@ -267,6 +310,72 @@ conv3t_k(const __grid_constant__ CUtensorMap map, int cin, D3 d, const float *__
         if (threadIdx.x == 0 && k + 2 < nck) issue(k + 2);
     }
     const int x = x0 + tx, y = y0 + ty;
+    if (!ACC && stats) {
+        // InstanceNorm statistics of this tile per output channel: the sum,
+        // then M2 about the tile mean (two block reductions); the per-tile
+        // (sum, M2) pairs are combined in a fixed order by in_stats_k
+        __shared__ float red[8][OCB];
+        __shared__ float tmean[OCB];
+        const int nx = min(TX, d.h - x0), ny = min(TY, d.w - y0), nz = min(TV, d.l - z0);
+        const float cnt = (float)(nx * ny * nz);
+        const bool inxy = x < d.h && y < d.w;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        float s[OCB];
+#pragma unroll
+        for (int j = 0; j < OCB; ++j) s[j] = 0.0f;
+#pragma unroll
+        for (int v = 0; v < TV; ++v)
+            if (inxy && z0 + v < d.l)
+#pragma unroll
+                for (int j = 0; j < OCB / 2; ++j) {
+                    s[2 * j] += acc[v][j].x;
+                    s[2 * j + 1] += acc[v][j].y;
+                }
+#pragma unroll
+        for (int j = 0; j < OCB; ++j) {
+#pragma unroll
+            for (int m = 16; m > 0; m >>= 1) s[j] += __shfl_xor_sync(0xffffffffu, s[j], m);
+            if (lane == 0) red[wid][j] = s[j];
+        }
+        __syncthreads();
+        if (threadIdx.x < OCB) {
+            float a = 0.0f;
+#pragma unroll
+            for (int w8 = 0; w8 < 8; ++w8) a += red[w8][threadIdx.x];
+            tmean[threadIdx.x] = a / cnt;
+            s[0] = a;  // keep the sum for the write below
+        }
+        __syncthreads();
+        float q[OCB];
+#pragma unroll
+        for (int j = 0; j < OCB; ++j) q[j] = 0.0f;
+#pragma unroll
+        for (int v = 0; v < TV; ++v)
+            if (inxy && z0 + v < d.l)
+#pragma unroll
+                for (int j = 0; j < OCB / 2; ++j) {
+                    const float a = acc[v][j].x - tmean[2 * j], b = acc[v][j].y - tmean[2 * j + 1];
+                    q[2 * j] = fmaf(a, a, q[2 * j]);
+                    q[2 * j + 1] = fmaf(b, b, q[2 * j + 1]);
+                }
+        float sum_keep = s[0];
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < OCB; ++j) {
+#pragma unroll
+            for (int m = 16; m > 0; m >>= 1) q[j] += __shfl_xor_sync(0xffffffffu, q[j], m);
+            if (lane == 0) red[wid][j] = q[j];
+        }
+        __syncthreads();
+        if (threadIdx.x < OCB && o0 + threadIdx.x < cout) {
+            float m2 = 0.0f;
+#pragma unroll
+            for (int w8 = 0; w8 < 8; ++w8) m2 += red[w8][threadIdx.x];
+            const int ntiles = gridDim.x * gridDim.y * ((d.l + TV - 1) / TV);
+            const int tile = (zb * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+            stats[(int64_t)(o0 + threadIdx.x) * ntiles + tile] = make_float2(sum_keep, m2);
+        }
+    }
     if (x >= d.h || y >= d.w) return;
 #pragma unroll
     for (int v = 0; v < TV; ++v) {
@@ -1025,7 +1134,8 @@ static bool conv_map(CUtensorMap *m, const float *base, const D3 &d, int C) {
 // conv3t_k launch: blocked weights + the TMA kernel (ACC: accumulate, no bias)
 template <bool ACC>
 static mdg_status conv3t_launch(const CUtensorMap &map, const float *w, int oc, int ic, bool flip,
-                                const D3 &d, const float *bias, float *out, cudaStream_t st) {
+                                const D3 &d, const float *bias, float *out, cudaStream_t st,
+                                float *norm_stats = nullptr) {
     const int cin = flip ? oc : ic, cout = flip ? ic : oc;
     const int cpad = (cin + CIB - 1) / CIB * CIB, nob = (cout + OCB - 1) / OCB;
     Scratch wb;
@@ -1036,8 +1146,18 @@ static mdg_status conv3t_launch(const CUtensorMap &map, const float *w, int oc, 
     MDG_CUDA_TRY(cudaFuncSetAttribute(conv3t_k<ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)TSMEM));
     const dim3 g((d.h + TX - 1) / TX, (d.w + TY - 1) / TY, ((d.l + TV - 1) / TV) * nob);
-    conv3t_k<ACC><<<g, NT, TSMEM, st>>>(map, cin, d, wb.as<float>(), cpad, bias, cout, out);
+    Scratch sp;
+    const int ntx = g.x, nty = g.y, ntz = (d.l + TV - 1) / TV;
+    if (norm_stats)
+        MDG_CUDA_TRY(sp.alloc((size_t)cout * ntx * nty * ntz * sizeof(float2), st));
+    conv3t_k<ACC><<<g, NT, TSMEM, st>>>(map, cin, d, wb.as<float>(), cpad, bias, cout, out,
+                                        norm_stats ? sp.as<float2>() : nullptr);
     MDG_LAUNCHED();
+    if (norm_stats) {
+        in_stats_k<<<cout, 256, 0, st>>>(sp.as<float2>(), d, ntx, nty, ntz, 1e-5f, norm_stats,
+                                         norm_stats + cout);
+        MDG_LAUNCHED();
+    }
     return MDG_OK;
 }
 
@@ -1103,12 +1223,19 @@ static bool conv3w_try(const float *in, int ic, const D3 &d, const float *gout, 
 }
 
 mdg_status enc_conv3_fwd(const float *in, int ic, mdg_dims3 dd, const float *w, const float *b,
-                         int oc, float *out, cudaStream_t st) {
+                         int oc, float *out, cudaStream_t st, float *norm_stats,
+                         bool *stats_done) {
     const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
+    if (stats_done) *stats_done = false;
     const bool ig = use_igemm(oc, ic, d);
     CUtensorMap map;
-    if (!ig && conv_map(&map, in, d, ic))
-        return conv3t_launch<false>(map, w, oc, ic, false, d, b, out, st);
+    if (!ig && conv_map(&map, in, d, ic)) {
+        const bool want = norm_stats && stats_done;
+        const mdg_status s =
+            conv3t_launch<false>(map, w, oc, ic, false, d, b, out, st, want ? norm_stats : nullptr);
+        if (s == MDG_OK && want) *stats_done = true;
+        return s;
+    }
     const int tile = ig ? igemm_fwd_bn(oc) : OCB;
     const int opad = (oc + tile - 1) / tile * tile;
     Scratch wt;
@@ -1203,6 +1330,18 @@ mdg_status enc_in_lrelu_fwd(const float *x, int C, int64_t n, const float *g, co
     MDG_LAUNCHED();
     chan_final_k<<<C, 256, 0, st>>>(part.as<float>(), gx, (int)n, 1, 1e-5f, inv);
     MDG_LAUNCHED();
+    (vec ? in_apply_k<true> : in_apply_k<false>)<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, mean, inv,
+                                                                            g, b, slope, z);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+// z = lrelu(IN(x)) with mean / inv already known (fused into the conv)
+mdg_status enc_in_lrelu_apply(const float *x, int C, int64_t n, const float *g, const float *b,
+                              float slope, float *z, const float *mean, const float *inv,
+                              cudaStream_t st) {
+    const bool vec = n % 4 == 0;
+    const unsigned gx = plane_blocks(vec ? n / 4 : n, C);
     (vec ? in_apply_k<true> : in_apply_k<false>)<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, mean, inv,
                                                                             g, b, slope, z);
     MDG_LAUNCHED();

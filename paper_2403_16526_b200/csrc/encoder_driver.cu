@@ -140,12 +140,21 @@ mdg_status mdg_encoder_forward(mdg_encoder *e, const float *image, const mdg_blo
         } else {
             L.x = const_cast<float *>(image);
         }
-        ENC_TRY(enc_conv3_fwd(x, L.cin, L.d, P.w1, P.b1, L.c, L.a1, st));
-        ENC_TRY(enc_in_lrelu_fwd(L.a1, L.c, L.n, P.g1, P.be1, e->slope, L.z1, L.st1,
-                                 L.st1 + L.c, st));
-        ENC_TRY(enc_conv3_fwd(L.z1, L.c, L.d, P.w2, P.b2, L.c, L.a2, st));
-        ENC_TRY(enc_in_lrelu_fwd(L.a2, L.c, L.n, P.g2, P.be2, e->slope, features[k], L.st2,
-                                 L.st2 + L.c, st));
+        bool fused = false;
+        ENC_TRY(enc_conv3_fwd(x, L.cin, L.d, P.w1, P.b1, L.c, L.a1, st, L.st1, &fused));
+        if (fused)
+            ENC_TRY(enc_in_lrelu_apply(L.a1, L.c, L.n, P.g1, P.be1, e->slope, L.z1, L.st1,
+                                       L.st1 + L.c, st));
+        else
+            ENC_TRY(enc_in_lrelu_fwd(L.a1, L.c, L.n, P.g1, P.be1, e->slope, L.z1, L.st1,
+                                     L.st1 + L.c, st));
+        ENC_TRY(enc_conv3_fwd(L.z1, L.c, L.d, P.w2, P.b2, L.c, L.a2, st, L.st2, &fused));
+        if (fused)
+            ENC_TRY(enc_in_lrelu_apply(L.a2, L.c, L.n, P.g2, P.be2, e->slope, features[k], L.st2,
+                                       L.st2 + L.c, st));
+        else
+            ENC_TRY(enc_in_lrelu_fwd(L.a2, L.c, L.n, P.g2, P.be2, e->slope, features[k], L.st2,
+                                     L.st2 + L.c, st));
     }
     e->have_forward = true;
     return MDG_OK;

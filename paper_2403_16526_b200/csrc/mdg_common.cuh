@@ -143,8 +143,15 @@ mdg_status project_qk_bwd_impl(const float *f, const float *m, int C, int64_t n,
                                float *gln_b, int gin_set, cudaStream_t stream);
 
 // encoder.cu: conv block pieces (internal; driven by encoder_driver.cu)
+// norm_stats (2*oc floats: mean | inv) + stats_done: when the conv path can
+// fuse the InstanceNorm statistics into its epilogue it fills them and sets
+// *stats_done (otherwise the caller runs enc_in_lrelu_fwd's own passes)
 mdg_status enc_conv3_fwd(const float *in, int ic, mdg_dims3 d, const float *w, const float *b,
-                         int oc, float *out, cudaStream_t st);
+                         int oc, float *out, cudaStream_t st, float *norm_stats = nullptr,
+                         bool *stats_done = nullptr);
+mdg_status enc_in_lrelu_apply(const float *x, int C, int64_t n, const float *g, const float *b,
+                              float slope, float *z, const float *mean, const float *inv,
+                              cudaStream_t st);
 // gin_acc: accumulate into gin (else overwrite)
 mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 d, const float *w, int oc,
                          const float *gout, float *gin, float *gw, float *gb, cudaStream_t st,
