@@ -445,10 +445,13 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
     int *cnt = reinterpret_cast<int *>(wsm2 + 2 * W::BUF + 4);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int cl = wid / 3, dz = wid % 3;
+    // grid x = (x-y tile, channel chunk) with the chunk fastest: the chunks of
+    // one tile run side by side and share its gout planes through L2
     const int ntx = (d.h + TX - 1) / TX;
-    const int x0 = (blockIdx.x % ntx) * TX, y0 = (blockIdx.x / ntx) * TY;
+    const int cc = blockIdx.x % ncc, txy = blockIdx.x / ncc;
+    const int x0 = (txy % ntx) * TX, y0 = (txy / ntx) * TY;
     const int zb0 = blockIdx.y * zper, zb1 = min(d.l, zb0 + zper);
-    const int ob = blockIdx.z / ncc, cc = blockIdx.z % ncc;
+    const int ob = blockIdx.z;
     const int c0 = cc * WC;
     const int nsteps = (zb1 - zb0 + ZW - 1) / ZW;
     if (threadIdx.x == 0) {
@@ -556,8 +559,9 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
         }
     }
     // per-CTA partial: part[((ob*ncc + cc)*nblk + blk)][o][c][t]
-    const int nblk = gridDim.x * gridDim.y, blk = blockIdx.y * gridDim.x + blockIdx.x;
-    float *dst = part + ((int64_t)blockIdx.z * nblk + blk) * (OCB * WC * 27);
+    const int nxy = gridDim.x / ncc;
+    const int nblk = nxy * gridDim.y, blk = blockIdx.y * nxy + txy;
+    float *dst = part + ((int64_t)(ob * ncc + cc) * nblk + blk) * (OCB * WC * 27);
 #pragma unroll
     for (int k = 0; k < 9; ++k)
 #pragma unroll
@@ -1207,7 +1211,7 @@ static bool conv3w_try(const float *in, int ic, const D3 &d, const float *gout, 
         return true;
     }
     float *pb = part.as<float>() + np;
-    conv3w_k<WC><<<dim3(ntx * nty, nz, nob * ncc), W::NTH, W::SMEM, st>>>(
+    conv3w_k<WC><<<dim3(ntx * nty * ncc, nz, nob), W::NTH, W::SMEM, st>>>(
         im, gm, ic, oc, d, zper, ncc, part.as<float>(), pb);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if ((e = cudaPeekAtLastError()) != cudaSuccess) {

@@ -43,6 +43,45 @@ __device__ __forceinline__ void lxyz(int p, const LDims &d, int &x, int &y, int 
 constexpr int kStrip = 4;
 constexpr int kMaxR = 12;
 
+// x pass, one warp per row: the row (zero-padded by R each side) is staged in
+// shared memory with coalesced loads, then lane i sums the taps of outputs
+// i, i+32, ... in the reference's order (bit-identical to box_axis_k<0>)
+constexpr int kRowMax = 2048;  // h + 2R must fit a warp's row buffer
+template <int R>
+__global__ void __launch_bounds__(kLB)
+box_x_rows_k(const float *__restrict__ in, LDims d, float *__restrict__ out) {
+    extern __shared__ float rows_sm[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int hp = d.h + 2 * R;
+    float *row = rows_sm + wid * hp;
+    const int c = blockIdx.y;
+    const int nrows = d.w * d.l;
+    const float *src = in + (int64_t)c * d.n;
+    float *dst = out + (int64_t)c * d.n;
+    for (int rr = blockIdx.x * (kLB / 32) + wid; rr < nrows; rr += gridDim.x * (kLB / 32)) {
+        const float *s = src + (int64_t)rr * d.h;
+        for (int i = lane; i < hp; i += 32) {
+            const int t = i - R;
+            row[i] = (t >= 0 && t < d.h) ? __ldg(s + t) : 0.0f;
+        }
+        __syncwarp();
+        for (int x = lane; x < d.h; x += 32) {
+            // taps t = x-R .. x+R clamped to the row: the zero padding must not
+            // be added (0 + v == v, but the reference starts at the first
+            // in-range tap), so sum only the in-range ones, in order
+            const int t0 = max(0, x - R), t1 = min(d.h - 1, x + R);
+            float acc = 0.0f;
+#pragma unroll
+            for (int q = 0; q < 2 * R + 1; ++q) {
+                const int t = x - R + q;
+                if (t >= t0 && t <= t1) acc = __fadd_rn(acc, row[t + R]);
+            }
+            dst[(int64_t)rr * d.h + x] = acc;
+        }
+        __syncwarp();
+    }
+}
+
 template <int AX, int R>
 __global__ void __launch_bounds__(kLB)
 box_axis_k(const float *__restrict__ in, LDims d, float *__restrict__ out) {
@@ -306,7 +345,17 @@ template <int R>
 static void box3_r(float *a, int C, const LDims &d, float *b, cudaStream_t st) {
     const dim3 g((unsigned)std::min<int64_t>(grid1d(d.n / kStrip + d.h * d.w, kLB), 148 * 8),
                  (unsigned)C);
-    box_axis_k<0, R><<<g, kLB, 0, st>>>(a, d, b);
+    if (d.h + 2 * R <= kRowMax) {
+        const size_t sm = (size_t)(kLB / 32) * (d.h + 2 * R) * sizeof(float);
+        if (sm > 48 * 1024)
+            cudaFuncSetAttribute(box_x_rows_k<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm);
+        const unsigned gx = (unsigned)std::max<int64_t>(
+            1, std::min<int64_t>(((int64_t)d.w * d.l + kLB / 32 - 1) / (kLB / 32), 148 * 8));
+        box_x_rows_k<R><<<dim3(gx, (unsigned)C), kLB, sm, st>>>(a, d, b);
+    } else {
+        box_axis_k<0, R><<<g, kLB, 0, st>>>(a, d, b);
+    }
     box_axis_k<1, R><<<g, kLB, 0, st>>>(b, d, a);
     box_axis_k<2, R><<<g, kLB, 0, st>>>(a, d, b);
 }
