@@ -46,17 +46,18 @@ struct DI {
 
 constexpr int NT = 256, TM = 8, TN = 4;
 
+// fwd / bwd_in tile: BM = 256 voxels (one gathering thread per voxel, taps
+// unrolled at compile time) x BN output channels; thread tile 8 voxels x FTN
+// channels (FTN = 8 for BN = 64: 32 FFMA2 per 4 LDS.128 per tap)
 template <int BN>
-struct Tile {
-    static constexpr int WTN = (BN / TN) >= 8 ? 8 : BN / TN;  // lanes along N per warp
-    static constexpr int WTM = 32 / WTN;                      // lanes along M per warp
-    static constexpr int BM = NT * TM * TN / BN;              // 128 / 256
-    static constexpr int WM = BM / (TM * WTM);                // warps along M
-    static constexpr int G = NT / BM;                         // gather tap groups
-    static constexpr int TPT = (27 + G - 1) / G;              // taps gathered per thread
-    static constexpr int ROW = BM + BN;                       // floats per staged tap row
-    static constexpr int STAGE = 27 * ROW;                    // floats per stage (1 channel)
-    static_assert((BM / TM) * (BN / TN) == NT, "tile");
+struct FTile {
+    static constexpr int BM = NT, FTM = 8, FTN = BN >= 64 ? 8 : 4;
+    static constexpr int WTN = BN / FTN;      // lanes along N per warp (8)
+    static constexpr int WTM = 32 / WTN;      // lanes along M per warp (4)
+    static constexpr int WM = BM / (FTM * WTM);
+    static constexpr int ROW = BM + BN;       // floats per staged tap row
+    static constexpr int STAGE = 27 * ROW;    // one input channel
+    static_assert(WTN * WTM == 32 && WM * (BN / (FTN * WTN)) == NT / 32, "tile");
 };
 
 // ------------------------------------------------------------ fwd / bwd_in
@@ -65,44 +66,34 @@ __global__ void __launch_bounds__(NT, 2)
 igemm_fwd_k(const float *__restrict__ in, int cin, DI d, const float *__restrict__ wT, int opad,
             const float *__restrict__ bias, int cout, int acc_out, int cps,
             float *__restrict__ out, float *__restrict__ part) {
-    using T = Tile<BN>;
+    using T = FTile<BN>;
+    constexpr int FTM = T::FTM, FTN = T::FTN;
     extern __shared__ __align__(16) float smem[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int p0 = blockIdx.x * T::BM, n0 = blockIdx.y * BN;
     const int cb = blockIdx.z * cps, ce = min(cin, cb + cps);
 
-    // gather role: voxel gm, taps tg + G*k
-    const int gm = tid % T::BM, tg = tid / T::BM;
-    const int gp = p0 + gm;
-    int x = 0, y = 0, z = 0;
-    const bool live = gp < d.n;
-    if (live) {
-        z = gp / d.hw;
-        const int r = gp - z * d.hw;
-        y = r / d.h;
-        x = r - y * d.h;
-    }
-    int toff[T::TPT];
-    unsigned tmask = 0;
+    // gather role: this thread's voxel; the 27 taps' validity as one mask
+    const int gp = p0 + tid;
+    unsigned vm = 0;
+    if (gp < d.n) {
+        const int z = gp / d.hw, r = gp - z * d.hw, y = r / d.h, x = r - y * d.h;
+        const unsigned mx = (x > 0 ? 1u : 0u) | 2u | (x < d.h - 1 ? 4u : 0u);
+        const unsigned my = (y > 0 ? 1u : 0u) | 2u | (y < d.w - 1 ? 4u : 0u);
+        const unsigned mz = (z > 0 ? 1u : 0u) | 2u | (z < d.l - 1 ? 4u : 0u);
 #pragma unroll
-    for (int k = 0; k < T::TPT; ++k) {
-        const int t = tg + T::G * k;
-        const int dz = t / 9 - 1, dy = (t / 3) % 3 - 1, dx = t % 3 - 1;
-        toff[k] = dz * d.hw + dy * d.h + dx;
-        const bool ok = t < 27 && live && (unsigned)(x + dx) < (unsigned)d.h &&
-                        (unsigned)(y + dy) < (unsigned)d.w && (unsigned)(z + dz) < (unsigned)d.l;
-        tmask |= (ok ? 1u : 0u) << k;
+        for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy)
+                if ((mz >> dz) & (my >> dy) & 1u) vm |= mx << (dz * 9 + dy * 3);
     }
-
     auto stage = [&](int c, float *buf) {
         const float *src = in + (int64_t)c * d.n + gp;
 #pragma unroll
-        for (int k = 0; k < T::TPT; ++k) {
-            const int t = tg + T::G * k;
-            if (t < 27) {
-                const bool ok = (tmask >> k) & 1u;
-                cpa4(buf + t * T::ROW + gm, ok ? src + toff[k] : in, ok);
-            }
+        for (int t = 0; t < 27; ++t) {
+            const int off = (t / 9 - 1) * d.hw + ((t / 3) % 3 - 1) * d.h + (t % 3 - 1);
+            const bool ok = (vm >> t) & 1u;
+            cpa4(buf + t * T::ROW + tid, ok ? src + off : in, ok);
         }
         const float *wr = wT + (int64_t)c * 27 * opad + n0;
         for (int i = tid; i < 27 * (BN / 4); i += NT) {
@@ -112,15 +103,14 @@ igemm_fwd_k(const float *__restrict__ in, int cin, DI d, const float *__restrict
         cp_commit();
     };
 
-    // compute role: warp tile WTM x WTN lanes
     const int lm = lane % T::WTM, ln = lane / T::WTM;
     const int wm = wid % T::WM, wn = wid / T::WM;
-    const int m0 = (wm * T::WTM + lm) * TM, nn0 = (wn * T::WTN + ln) * TN;
-    float2 acc[TM][TN / 2];
+    const int m0 = (wm * T::WTM + lm) * FTM, nn0 = (wn * T::WTN + ln) * FTN;
+    float2 acc[FTM][FTN / 2];
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
+    for (int i = 0; i < FTM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN / 2; ++j) acc[i][j] = make_float2(0.0f, 0.0f);
+        for (int j = 0; j < FTN / 2; ++j) acc[i][j] = make_float2(0.0f, 0.0f);
 
     if (cb < ce) stage(cb, smem);
     for (int c = cb; c < ce; ++c) {
@@ -132,19 +122,24 @@ igemm_fwd_k(const float *__restrict__ in, int cin, DI d, const float *__restrict
             cp_wait<0>();
         }
         __syncthreads();
-#pragma unroll 9
+#pragma unroll 3
         for (int t = 0; t < 27; ++t) {
             const float *row = cur + t * T::ROW;
             const float4 a0 = *reinterpret_cast<const float4 *>(row + m0);
             const float4 a1 = *reinterpret_cast<const float4 *>(row + m0 + 4);
-            const float4 b = *reinterpret_cast<const float4 *>(row + T::BM + nn0);
-            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float2 b01 = make_float2(b.x, b.y), b23 = make_float2(b.z, b.w);
+            float2 b2[FTN / 2];
 #pragma unroll
-            for (int i = 0; i < TM; ++i) {
+            for (int q = 0; q < FTN / 4; ++q) {
+                const float4 b = *reinterpret_cast<const float4 *>(row + T::BM + nn0 + 4 * q);
+                b2[2 * q] = make_float2(b.x, b.y);
+                b2[2 * q + 1] = make_float2(b.z, b.w);
+            }
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+            for (int i = 0; i < FTM; ++i) {
                 const float2 ai = make_float2(av[i], av[i]);
-                acc[i][0] = __ffma2_rn(ai, b01, acc[i][0]);
-                acc[i][1] = __ffma2_rn(ai, b23, acc[i][1]);
+#pragma unroll
+                for (int j = 0; j < FTN / 2; ++j) acc[i][j] = __ffma2_rn(ai, b2[j], acc[i][j]);
             }
         }
         __syncthreads();
@@ -152,13 +147,13 @@ igemm_fwd_k(const float *__restrict__ in, int cin, DI d, const float *__restrict
 
     // epilogue
 #pragma unroll
-    for (int j = 0; j < TN; ++j) {
+    for (int j = 0; j < FTN; ++j) {
         const int o = n0 + nn0 + j;
         if (o >= cout) continue;
         const float bo = (part || acc_out || !bias) ? 0.0f : bias[o];
         float *dst = part ? part + ((int64_t)blockIdx.z * cout + o) * d.n : out + (int64_t)o * d.n;
 #pragma unroll
-        for (int i = 0; i < TM; ++i) {
+        for (int i = 0; i < FTM; ++i) {
             const int p = p0 + m0 + i;
             if (p < d.n) {
                 const float v = (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
@@ -188,7 +183,7 @@ igemm_splitk_sum_k(const float *__restrict__ part, int nsplit, int cout, int n,
 template <int BN>
 cudaError_t launch_fwd(const float *in, int cin, DI d, const float *wT, int opad,
                        const float *bias, int cout, bool acc_out, float *out, cudaStream_t st) {
-    using T = Tile<BN>;
+    using T = FTile<BN>;
     const int mt = (d.n + T::BM - 1) / T::BM, nt = (cout + BN - 1) / BN;
     const int tiles = mt * nt;
     const int want = 148 * 2 * 2;  // ~2 waves at 2 CTAs/SM, >= 8 channels per split
