@@ -394,20 +394,25 @@ def run_po(dev, world, pairs=0, reps=5):
     rng = ops.Rng(11)
     fixed = rng.uniform((1, l, w, h), 0.0, 1.0).to(dev)
     moving = rng.uniform((1, l, w, h), 0.0, 1.0).to(dev)
-    for _ in range(2):
-        model.po_step(fixed, moving)
-    torch.cuda.synchronize()
+    # a dedicated stream: the legacy default stream cannot be captured, and the
+    # iteration runs as one CUDA graph (mdg_model_po_step)
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(torch.cuda.current_stream())
     e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     ti, tf = [], []
-    for _ in range(reps):
-        e[0].record()
-        model.po_step(fixed, moving)
-        e[1].record()
-        model.loss_step(fixed, moving, backward=False)
-        e[2].record()
+    with torch.cuda.stream(side):
+        for _ in range(3):  # eager, capture, replay
+            model.po_step(fixed, moving)
         torch.cuda.synchronize()
-        ti.append(e[0].elapsed_time(e[1]))
-        tf.append(e[1].elapsed_time(e[2]))
+        for _ in range(reps):
+            e[0].record()
+            model.po_step(fixed, moving)
+            e[1].record()
+            model.loss_step(fixed, moving, backward=False)
+            e[2].record()
+            torch.cuda.synchronize()
+            ti.append(e[0].elapsed_time(e[1]))
+            tf.append(e[1].elapsed_time(e[2]))
     it_ms, fwd_ms = statistics.median(ti), statistics.median(tf)
     if world > 1:  # the slowest rank sets the pair rate
         import torch.distributed as dist
@@ -416,7 +421,8 @@ def run_po(dev, world, pairs=0, reps=5):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         it_ms, fwd_ms = float(t[0].item()), float(t[1].item())
     out = {"workload": "PO of the small-preset model at 160x192x224 (synthetic pair, "
-                       "init_model(42) weights), native model driver (mdg_model_*)",
+                       "init_model(42) weights), native model driver (mdg_model_*), "
+                       "one CUDA graph per iteration",
            "iter_ms": round(it_ms, 3), "final_forward_ms": round(fwd_ms, 3),
            "iters_per_pair": 50,
            "pairs_per_sec": round(world * 1e3 / (50 * it_ms + fwd_ms), 4),
@@ -424,11 +430,12 @@ def run_po(dev, world, pairs=0, reps=5):
     if pairs > 0:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(pairs):
-            m = ops.NativeModel([t.to(dev) for t in ops.init_model(42)], DIMS)
-            for _ in range(50):
-                m.po_step(fixed, moving)
-            m.loss_step(fixed, moving, backward=False)
+        with torch.cuda.stream(side):
+            for _ in range(pairs):
+                m = ops.NativeModel([t.to(dev) for t in ops.init_model(42)], DIMS)
+                for _ in range(50):
+                    m.po_step(fixed, moving)
+                m.loss_step(fixed, moving, backward=False)
         torch.cuda.synchronize()
         out["pairs_run"] = pairs
         out["pairs_per_sec_measured"] = round(world * pairs / (time.perf_counter() - t0), 4)
