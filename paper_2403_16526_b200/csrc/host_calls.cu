@@ -717,6 +717,11 @@ mdg_status warp_fwd_host_pipelined(const float *in, int C, mdg_dims3 d, const fl
 
 mdg_status warp_bwd_host_pipelined(const float *in, int C, mdg_dims3 d, const float *field,
                                    const float *gout, float *gin, float *gfield) {
+    const auto te = std::chrono::steady_clock::now();
+    auto since = [&] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te)
+            .count();
+    };
     PipeCtx P(d);
     const int N = P.ck.nchunk;
     const int64_t n = P.n, hw = P.hw;
@@ -752,7 +757,9 @@ mdg_status warp_bwd_host_pipelined(const float *in, int C, mdg_dims3 d, const fl
         upd[i] = P.event();
         MDG_PIPE_TRY(cudaEventRecord(upd[i], P.up));
     }
+    const double t_enq_up = since();
     MDG_PIPE_TRY(cudaEventSynchronize(rev));
+    const double t_reach = since();
     const Reach R = reach_decode(P, hr);
     std::vector<std::vector<int>> gin_after(N);  // row chunks final after compute i
     for (int j = 0; j < N; ++j) gin_after[std::max(R.last[j], 0)].push_back(j);
@@ -778,17 +785,32 @@ mdg_status warp_bwd_host_pipelined(const float *in, int C, mdg_dims3 d, const fl
         }
     }
     // host adds in download order
+    const double t_enq = since();
+    double t_wait = 0.0, t_add = 0.0;
     for (int i = 0; i < N; ++i) {
         const int64_t p0 = (int64_t)P.ck.z0[i] * hw, m = (int64_t)P.ck.depth(i) * hw;
+        double a0 = since();
         MDG_PIPE_TRY(cudaEventSynchronize(fdw[i]));
+        double a1 = since();
+        t_wait += a1 - a0;
         if (gfield) host_add_rows(gfield + p0, sf + p0, m, 3, n);
+        t_add += since() - a1;
         for (int j : gin_after[i]) {
             const int64_t q0 = (int64_t)P.ck.z0[j] * hw, mq = (int64_t)P.ck.depth(j) * hw;
+            a0 = since();
             MDG_PIPE_TRY(cudaEventSynchronize(gdw[j]));
+            a1 = since();
+            t_wait += a1 - a0;
             if (gin) host_add_rows(gin + q0, si + q0, mq, C, n);
+            t_add += since() - a1;
         }
     }
     MDG_PIPE_TRY(cudaStreamSynchronize(P.down));
+    if (getenv("MDG_PIPE_TRACE"))
+        fprintf(stderr,
+                "warp_bwd_host pipeline: uploads enqueued %.2f, reach known %.2f, all enqueued "
+                "%.2f, waits %.2f, adds %.2f, total %.2f ms\n",
+                t_enq_up, t_reach, t_enq, t_wait, t_add, since());
     return MDG_OK;
 }
 
