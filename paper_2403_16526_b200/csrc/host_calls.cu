@@ -140,6 +140,8 @@ class AddPool {
     AddPool() {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         nthreads_ = (int)std::min(12u, std::max(1u, hw * 3 / 4));
+        if (const char *e = std::getenv("MDG_ADD_THREADS"))  // tuning override
+            nthreads_ = std::max(1, std::min(64, std::atoi(e)));
         for (int t = 1; t < nthreads_; ++t) workers_.emplace_back([this, t] { loop(t); });
     }
     ~AddPool() {
