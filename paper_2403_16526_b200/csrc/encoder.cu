@@ -425,26 +425,29 @@ __global__ void wprep_blocked_k(const float *__restrict__ w, int oc, int ic, int
 // checks.  At the end each warp reduces its 72 sums across lanes (fixed
 // butterfly) into a per-CTA partial; a fixed-order pass adds the partials.
 constexpr int ZW = 2;
-template <int WC>
+template <int WC, int OH = 1>  // OH: output-channel halves per (c, dz) warp
 struct WT {
     static constexpr int IN = WC * (ZW + 2) * HY * PX;  // input floats per stage
     static constexpr int GO = OCB * ZW * TY * TX;         // gout floats per stage
     static constexpr int BUF = IN + GO;
     static constexpr size_t SMEM = (2 * (size_t)BUF + 8) * sizeof(float);
-    static constexpr int NTH = 3 * WC * 32;
+    static constexpr int NTH = 3 * WC * 32 * OH;
+    static constexpr int OPW = OCB / OH;  // output channels per warp
 };
 
-template <int WC>
-__global__ void __launch_bounds__(3 * WC * 32)
+template <int WC, int OH = 1>
+__global__ void __launch_bounds__(3 * WC * 32 * OH)
 conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap gmap,
          int cin, int cout, D3 d, int zper, int ncc, float *__restrict__ part,
          float *__restrict__ partb) {
-    using W = WT<WC>;
+    using W = WT<WC, OH>;
+    constexpr int PJ = W::OPW / 2;  // channel pairs per warp
     extern __shared__ __align__(128) float wsm2[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(wsm2 + 2 * W::BUF);
     int *cnt = reinterpret_cast<int *>(wsm2 + 2 * W::BUF + 4);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int cl = wid / 3, dz = wid % 3;
+    const int hh = wid % OH, cl = wid / (3 * OH), dz = (wid / OH) % 3;
+    const int ob0 = hh * W::OPW;  // this warp's first output channel (in the block of 8)
     // grid x = (x-y tile, channel chunk) with the chunk fastest: the chunks of
     // one tile run side by side and share its gout planes through L2
     const int ntx = (d.h + TX - 1) / TX;
@@ -483,18 +486,18 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
         if (nsteps > 0) issue(0);
         if (nsteps > 1) issue(1);
     }
-    float2 acc[9][OCB / 2];
+    float2 acc[9][PJ];
 #pragma unroll
     for (int k = 0; k < 9; ++k)
 #pragma unroll
-        for (int j = 0; j < OCB / 2; ++j) acc[k][j] = make_float2(0.0f, 0.0f);
-    // bias gradient: in the first channel chunk, warp w sums the channel pairs
-    // j with j % NW == w (spreads the extra adds over the warps)
-    constexpr int NW = W::NTH / 32, NS = (OCB / 2 + NW - 1) / NW;
+        for (int j = 0; j < PJ; ++j) acc[k][j] = make_float2(0.0f, 0.0f);
+    // bias gradient: in the first channel chunk, the warps of input channel 0
+    // (dz = 0..2, each half) sum their pairs j with j % 3 == dz
+    constexpr int NS = (PJ + 2) / 3;
     float2 gsum[NS];
 #pragma unroll
     for (int q = 0; q < NS; ++q) gsum[q] = make_float2(0.0f, 0.0f);
-    const bool bias_warp = cc == 0 && wid < OCB / 2;
+    const bool bias_warp = cc == 0 && cl == 0;
 
     for (int k = 0; k < nsteps; ++k) {
         const float *b = wsm2 + (k & 1) * W::BUF;
@@ -515,18 +518,18 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
                     float r2[3];
 #pragma unroll
                     for (int dx = 0; dx < 3; ++dx) r2[dx] = ip[(y + 2) * PX + dx];
-                    float2 g2[OCB / 2];
+                    float2 g2[PJ];
 #pragma unroll
-                    for (int j = 0; j < OCB / 2; ++j)
-                        g2[j] = make_float2(gp[(2 * j) * (ZW * TY * TX) + y * TX],
-                                            gp[(2 * j + 1) * (ZW * TY * TX) + y * TX]);
+                    for (int j = 0; j < PJ; ++j)
+                        g2[j] = make_float2(gp[(ob0 + 2 * j) * (ZW * TY * TX) + y * TX],
+                                            gp[(ob0 + 2 * j + 1) * (ZW * TY * TX) + y * TX]);
 #pragma unroll
                     for (int dx = 0; dx < 3; ++dx) {
                         const float2 s0 = make_float2(r0[dx], r0[dx]);
                         const float2 s1 = make_float2(r1[dx], r1[dx]);
                         const float2 s2 = make_float2(r2[dx], r2[dx]);
 #pragma unroll
-                        for (int j = 0; j < OCB / 2; ++j) {
+                        for (int j = 0; j < PJ; ++j) {
                             acc[dx][j] = __ffma2_rn(s0, g2[j], acc[dx][j]);
                             acc[3 + dx][j] = __ffma2_rn(s1, g2[j], acc[3 + dx][j]);
                             acc[6 + dx][j] = __ffma2_rn(s2, g2[j], acc[6 + dx][j]);
@@ -534,8 +537,8 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
                     }
                     if (bias_warp) {
 #pragma unroll
-                        for (int j = 0; j < OCB / 2; ++j)
-                            if (j % NW == wid) gsum[j / NW] = __fadd2_rn(gsum[j / NW], g2[j]);
+                        for (int j = 0; j < PJ; ++j)
+                            if (j % 3 == dz) gsum[j / 3] = __fadd2_rn(gsum[j / 3], g2[j]);
                     }
 #pragma unroll
                     for (int dx = 0; dx < 3; ++dx) {
@@ -565,7 +568,7 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
 #pragma unroll
     for (int k = 0; k < 9; ++k)
 #pragma unroll
-        for (int j = 0; j < OCB / 2; ++j) {
+        for (int j = 0; j < PJ; ++j) {
             float ax = acc[k][j].x, ay = acc[k][j].y;
 #pragma unroll
             for (int m = 16; m > 0; m >>= 1) {
@@ -574,15 +577,15 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
             }
             if (lane == 0) {
                 const int t = dz * 9 + k;  // k = dy*3 + dx
-                dst[((2 * j) * WC + cl) * 27 + t] = ax;
-                dst[((2 * j + 1) * WC + cl) * 27 + t] = ay;
+                dst[((ob0 + 2 * j) * WC + cl) * 27 + t] = ax;
+                dst[((ob0 + 2 * j + 1) * WC + cl) * 27 + t] = ay;
             }
         }
     if (bias_warp) {
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
-            const int j = wid + q * NW;
-            if (j >= OCB / 2) break;
+            const int j = dz + 3 * q;
+            if (j >= PJ) break;
             float ax = gsum[q].x, ay = gsum[q].y;
 #pragma unroll
             for (int m = 16; m > 0; m >>= 1) {
@@ -590,8 +593,8 @@ conv3w_k(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUten
                 ay += __shfl_xor_sync(0xffffffffu, ay, m);
             }
             if (lane == 0) {
-                partb[((int64_t)ob * nblk + blk) * OCB + 2 * j] = ax;
-                partb[((int64_t)ob * nblk + blk) * OCB + 2 * j + 1] = ay;
+                partb[((int64_t)ob * nblk + blk) * OCB + ob0 + 2 * j] = ax;
+                partb[((int64_t)ob * nblk + blk) * OCB + ob0 + 2 * j + 1] = ay;
             }
         }
     }
@@ -1182,10 +1185,10 @@ static bool map4(CUtensorMap *m, const float *base, const D3 &d, int C, cuuint32
 }
 
 // TMA kernel gradient (conv3w_k); false if the volume does not take TMA
-template <int WC>
+template <int WC, int OH>
 static bool conv3w_try(const float *in, int ic, const D3 &d, const float *gout, int oc, float *gk,
                        float *gb, cudaStream_t st, mdg_status *rc) {
-    using W = WT<WC>;
+    using W = WT<WC, OH>;
     CUtensorMap im, gm;
     if (!map4(&im, in, d, ic, PX, HY, ZW + 2, WC) || !map4(&gm, gout, d, oc, TX, TY, ZW, OCB))
         return false;
@@ -1204,14 +1207,14 @@ static bool conv3w_try(const float *in, int ic, const D3 &d, const float *gout, 
     const size_t np = (size_t)nob * ncc * nblk * OCB * WC * 27;
     cudaError_t e = part.alloc((np + (size_t)nob * nblk * OCB) * sizeof(float), st);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(conv3w_k<WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(conv3w_k<WC, OH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)W::SMEM);
     if (e != cudaSuccess) {
         *rc = status_from_cuda(e, "conv3w");
         return true;
     }
     float *pb = part.as<float>() + np;
-    conv3w_k<WC><<<dim3(ntx * nty * ncc, nz, nob), W::NTH, W::SMEM, st>>>(
+    conv3w_k<WC, OH><<<dim3(ntx * nty * ncc, nz, nob), W::NTH, W::SMEM, st>>>(
         im, gm, ic, oc, d, zper, ncc, part.as<float>(), pb);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if ((e = cudaPeekAtLastError()) != cudaSuccess) {
@@ -1289,9 +1292,15 @@ mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 dd, const float *w, 
     if ((gw || gb) && use_igemm(oc, ic, d)) return igemm_conv_wgrad(in, ic, dd, gout, oc, gw, gb, st);
     if (gw || gb) {
         mdg_status rc = MDG_OK;
-        if (ic == 1 ? conv3w_try<1>(in, ic, d, gout, oc, gw, gb, st, &rc)
-                    : conv3w_try<2>(in, ic, d, gout, oc, gw, gb, st, &rc))
-            return rc;
+        static const int oh = [] {
+            const char *e = std::getenv("MDG_CONV3W_OH");  // tuning override
+            return e && std::atoi(e) == 1 ? 1 : 2;
+        }();
+        const bool done = ic == 1 ? (oh == 1 ? conv3w_try<1, 1>(in, ic, d, gout, oc, gw, gb, st, &rc)
+                                             : conv3w_try<1, 2>(in, ic, d, gout, oc, gw, gb, st, &rc))
+                                  : (oh == 1 ? conv3w_try<2, 1>(in, ic, d, gout, oc, gw, gb, st, &rc)
+                                             : conv3w_try<2, 2>(in, ic, d, gout, oc, gw, gb, st, &rc));
+        if (done) return rc;
     }
     if (gw || gb) {
         const int ntiles = ((d.h + TX - 1) / TX) * ((d.w + TY - 1) / TY) * ((d.l + TV - 1) / TV);
