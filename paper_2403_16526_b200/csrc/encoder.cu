@@ -424,7 +424,7 @@ __global__ void wprep_blocked_k(const float *__restrict__ w, int oc, int ic, int
 // makes out-of-volume voxels contribute exactly 0, so there are no bounds
 // checks.  At the end each warp reduces its 72 sums across lanes (fixed
 // butterfly) into a per-CTA partial; a fixed-order pass adds the partials.
-constexpr int ZW = 2;
+constexpr int ZW = 4;
 template <int WC, int OH = 1>  // OH: output-channel halves per (c, dz) warp
 struct WT {
     static constexpr int IN = WC * (ZW + 2) * HY * PX;  // input floats per stage
