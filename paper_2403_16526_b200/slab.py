@@ -178,6 +178,12 @@ class SlabModeT:
 
     def forward(self, Q, K, B):
         s = self.slab
+        if s.world == 1 and isinstance(self.be, CudaModeT):
+            # one slab = the whole volume: the fused operator directly
+            SF, LSE = self.be.forward(Q, K, B, s.dims)
+            self.be.check(s.dims)
+            self._saved = (Q, K, B, SF, LSE, True)
+            return SF
         Kx = self._ext("K", K)
         zero = torch.zeros(Q.shape[0], s.w, s.h, dtype=Q.dtype, device=Q.device)
         Qx = extend(Q, zero, zero)  # halo queries are the neighbours' work
@@ -191,14 +197,20 @@ class SlabModeT:
                     e.position = (pos[0], pos[1], pos[2] - 1 + s.z0, pos[3])
                 raise
         SF, saved = interior(SFx), interior(saved_x)
-        self._saved = (Q, K, B, SF, saved)
+        self._saved = (Q, K, B, SF, saved, False)
         return SF
 
     def backward(self, gSF):
         if self._saved is None:
             raise RuntimeError("slab: backward without forward")
-        Q, K, B, SF, saved = self._saved
+        Q, K, B, SF, saved, whole = self._saved
         s = self.slab
+        if whole:
+            gB = torch.zeros_like(B)
+            gQ = torch.empty_like(Q)
+            gK = torch.empty_like(K)
+            self.be._bwd(Q, K, B, SF, saved, gSF, s.dims, gQ, gK, gB)
+            return gQ, gK, gB
         Qx, Kx = self._ext("Q", Q), self._ext("K", K)
         SFx, gSFx = self._ext("SF", SF), self._ext("gSF", gSF)
         savedx = self._ext("saved", saved, fill=self.be.saved_fill)
@@ -357,20 +369,35 @@ class SlabWarp:
 
         self.all_reduce_max = all_reduce_max or _max
         self._saved = None
+        self._bufs = {}
 
-    def _full(self, C, ref):
+    def _full(self, name, C, ref):
+        """persistent full-size buffer: the kernels only read the planes each
+        call refreshes (the reach window, this rank's voxels), so stale planes
+        elsewhere are never touched"""
         s = self.slab
-        return torch.zeros(C, s.l, s.w, s.h, dtype=ref.dtype, device=ref.device)
+        key = (name, C, ref.dtype, ref.device)
+        b = self._bufs.get(key)
+        if b is None:
+            b = torch.zeros(C, s.l, s.w, s.h, dtype=ref.dtype, device=ref.device)
+            self._bufs[key] = b
+        return b
 
     def forward(self, vol, field):
         s = self.slab
+        if s.world == 1 and isinstance(self.be, CudaWarp):
+            # one slab = the whole volume: the whole-volume kernels directly
+            out = torch.empty_like(vol)
+            self.be.fwd_range(vol, field, out, (s.h, s.w, s.l), 0, s.h * s.w * s.l)
+            self._saved = (vol, field, None)
+            return out
         R = self.all_reduce_max(warp_reach(field, s.l))
         lo, hi = _need(s, s.z0, s.z1, R)
         C = vol.shape[0]
-        vol_full, field_full = self._full(C, vol), self._full(3, field)
+        vol_full, field_full = self._full("in", C, vol), self._full("field", 3, field)
         vol_full[:, lo:hi] = self.exchange("in", vol, s, R)
         field_full[:, s.z0:s.z1] = field
-        out_full = self._full(C, vol)
+        out_full = self._full("out", C, vol)
         hw = s.h * s.w
         dims = (s.h, s.w, s.l)
         self.be.fwd_range(vol_full, field_full, out_full, dims, s.z0 * hw, s.z1 * hw)
@@ -383,16 +410,26 @@ class SlabWarp:
             raise RuntimeError("slab: backward without forward")
         vol_full, field_full, R = self._saved
         s = self.slab
-        gout_full, gin_full = self._full(vol_full.shape[0], gout), self._full(vol_full.shape[0], gout)
-        gfield_full = self._full(3, gout)
-        gout_full[:, s.z0:s.z1] = gout
         hw = s.h * s.w
+        if R is None:  # world == 1: whole-volume kernels on the caller's tensors
+            gin, gfield = torch.zeros_like(vol_full), torch.zeros_like(field_full)
+            self.be.bwd_range(vol_full, field_full, gout, gin, gfield, (s.h, s.w, s.l), 0,
+                              s.l * hw)
+            return gin, gfield
+        C = vol_full.shape[0]
+        lo, hi = _need(s, s.z0, s.z1, R)
+        gout_full = self._full("gout", C, gout)
+        gin_full, gfield_full = self._full("gin", C, gout), self._full("gfield", 3, gout)
+        gout_full[:, s.z0:s.z1] = gout
+        gin_full[:, lo:hi].zero_()  # the scatter's reach
+        gfield_full[:, s.z0:s.z1].zero_()
         self.be.bwd_range(vol_full, field_full, gout_full, gin_full, gfield_full,
                           (s.h, s.w, s.l), s.z0 * hw, s.z1 * hw)
-        lo, hi = _need(s, s.z0, s.z1, R)
-        return gin_full[:, lo:hi].contiguous(), gfield_full[:, s.z0:s.z1].contiguous()
+        return gin_full[:, lo:hi].clone(), gfield_full[:, s.z0:s.z1].clone()
 
     def backward(self, gout):
         contrib, gfield = self.backward_local(gout)
+        if self._saved[2] is None:  # world == 1: contrib is the whole gin
+            return contrib, gfield
         gin = self.reduce("gin", contrib, self.slab, self._saved[2])
         return gin, gfield

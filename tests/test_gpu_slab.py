@@ -53,7 +53,7 @@ def test_slab_modet_cuda_matches_full_volume(cuda, world, dims, S, hd):
         ex.put("K", sl.rank, sl.local(K))
     sfs = [m.forward(sl.local(Q), sl.local(K), B) for m, sl in zip(mods, slabs)]
     for m, sl in zip(mods, slabs):  # what each rank publishes before its backward
-        _, _, _, sf, saved = m._saved
+        _, _, _, sf, saved, _ = m._saved
         for name, t in (("Q", sl.local(Q)), ("SF", sf), ("saved", saved), ("gSF", sl.local(gSF))):
             ex.put(name, sl.rank, t)
     outs = [m.backward(sl.local(gSF)) for m, sl in zip(mods, slabs)]
