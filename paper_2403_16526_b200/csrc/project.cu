@@ -449,6 +449,69 @@ gram_final_k(const float *__restrict__ part, int nparts, int KC, float *__restri
     if (threadIdx.x == 0 && o < KC) gW[o] += s[0];
 }
 
+// the weight gradient of the large two-phase level (K = 6, C = 16): each
+// thread streams its own voxels (coalesced global loads) and keeps all 96
+// (k, c) sums in registers; one fixed-order block reduction per block, then
+// gram16_final_k adds the block partials in block order
+template <int K, int C>  // K: rows of A per block tile (blockIdx.y), C: all of B
+__global__ void __launch_bounds__(kPB, 1)
+gram16_k(const float *__restrict__ A0, const float *__restrict__ A1, const float *__restrict__ B0,
+         const float *__restrict__ B1, int ninputs, int64_t n, float *__restrict__ part) {
+    A0 += (int64_t)blockIdx.y * K * n;
+    if (A1) A1 += (int64_t)blockIdx.y * K * n;
+    float acc[K][C];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[k][c] = 0.0f;
+    for (int which = 0; which < ninputs; ++which) {
+        const float *A = which ? A1 : A0;
+        const float *B = which ? B1 : B0;
+        for (int64_t p = (int64_t)blockIdx.x * kPB + threadIdx.x; p < n;
+             p += (int64_t)gridDim.x * kPB) {
+            float a[K], b[C];
+#pragma unroll
+            for (int k = 0; k < K; ++k) a[k] = __ldg(A + (int64_t)k * n + p);
+#pragma unroll
+            for (int c = 0; c < C; ++c) b[c] = __ldg(B + (int64_t)c * n + p);
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int c = 0; c < C; ++c) acc[k][c] = fmaf(a[k], b[c], acc[k][c]);
+        }
+    }
+    __shared__ float red[kPB / 32][K * C];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            float v = acc[k][c];
+#pragma unroll
+            for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+            if (lane == 0) red[wid][k * C + c] = v;
+        }
+    __syncthreads();
+    if (threadIdx.x < K * C) {
+        float v = 0.0f;
+#pragma unroll
+        for (int w8 = 0; w8 < kPB / 32; ++w8) v += red[w8][threadIdx.x];
+        part[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (K * C) + threadIdx.x] = v;
+    }
+}
+
+// gW[k][c] += sum over blocks (fixed order); tiles of KT rows of k
+__global__ void __launch_bounds__(kPB)
+gram16_final_k(const float *__restrict__ part, int nblk, int KT, int K, int C,
+               float *__restrict__ gW) {
+    const int o = blockIdx.x * kPB + threadIdx.x;
+    if (o >= K * C) return;
+    const int k = o / C, c = o % C, y = k / KT, kk = k % KT;
+    float v = 0.0f;
+    for (int b = 0; b < nblk; ++b) v += part[((int64_t)y * nblk + b) * (KT * C) + kk * C + c];
+    gW[o] += v;
+}
+
 template <typename Kern>
 cudaError_t allow_smem(Kern k, size_t bytes) {
     if (bytes <= 48 * 1024) return cudaSuccess;
@@ -503,7 +566,26 @@ mdg_status project_bwd_launch(const ProjArgs &a0, const float *W, const float *b
             part.as<float>(), gx, ntiles, a.K, a.C, two_phase ? nullptr : gW, gb, gg, gbe);
         MDG_LAUNCHED();
     }
-    if (two_phase) {
+    if (two_phase && ((a.K == 6 && a.C == 16) || (a.K == 12 && a.C == 32))) {
+        // register-tiled weight gradient for the two large two-phase levels
+        const int KT = a.C == 16 ? 6 : 3, nty = a.K / KT;
+        const int nblk = (int)std::max<int64_t>(
+            1, std::min<int64_t>((a.n + kPB - 1) / kPB, (int64_t)sms * 2 / nty));
+        Scratch gpart;
+        MDG_CUDA_TRY(gpart.alloc((size_t)nty * nblk * KT * a.C * sizeof(float), st));
+        if (a.C == 16)
+            gram16_k<6, 16><<<dim3(nblk, nty), kPB, 0, st>>>(a.graw[0], a.graw[1], a.in[0],
+                                                             a.in[1], a.ninputs, a.n,
+                                                             gpart.as<float>());
+        else
+            gram16_k<3, 32><<<dim3(nblk, nty), kPB, 0, st>>>(a.graw[0], a.graw[1], a.in[0],
+                                                             a.in[1], a.ninputs, a.n,
+                                                             gpart.as<float>());
+        MDG_LAUNCHED();
+        gram16_final_k<<<(a.K * a.C + kPB - 1) / kPB, kPB, 0, st>>>(gpart.as<float>(), nblk, KT,
+                                                                   a.K, a.C, gW);
+        MDG_LAUNCHED();
+    } else if (two_phase) {
         const int KC = a.K * a.C;
         const int gy = (KC + kPB * kGO - 1) / (kPB * kGO);
         const int64_t nchunks = (a.n + kGP - 1) / kGP;
