@@ -297,3 +297,24 @@ def test_po_recovers_known_translation(cuda, ref):
     assert int(fg.sum()) > 0 and epe <= 0.5
     assert float(t1[0]) < float(t0[0])
     assert dice1 > dice0
+
+
+def test_po_traces_repeatable(cuda, ref):
+    """test_engine.cpp:194-213 asks for bitwise-identical PO traces from fixed
+    seeds.  The GPU path is deterministic except for the fp32 atomics of the
+    scatters (warp / compose input gradients), so two runs agree to rounding
+    level rather than bit for bit."""
+    dims = (16, 16, 16)
+    f, m, _, _, _ = ref.synth_pair(dims, seed=14, max_disp=1.0)
+    fd, md = torch.from_numpy(f).cuda(), torch.from_numpy(m).cuda()
+    traces = []
+    for _ in range(2):
+        params = [t.cuda() for t in ops.init_model(21)]
+        model = ops.NativeModel(params, dims, loss=ops.LossConfig(lam=0.5, ncc_window=9))
+        tr = []
+        for _ in range(5):
+            t, _ = model.po_step(fd, md, graph=False)
+            tr.append(float(t[0]))
+        traces.append(np.array(tr))
+    print("trace diff", np.abs(traces[0] - traces[1]).max())
+    assert np.allclose(traces[0], traces[1], rtol=1e-5, atol=1e-7)
