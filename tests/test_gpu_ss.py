@@ -1,9 +1,14 @@
-"""Scaling and squaring on the GPU against the reference's known-answer
-properties (test_reghead.cpp:120-198): zero and constant velocities are exact,
-T = 7 matches dense forward-Euler integration, small velocities integrate
-fold-free, forward and backward integrations are mutually inverse, and the
-result converges in T.  Velocities come from the reference's own
-make_smooth_velocity (synth.cpp:75-90)."""
+"""Known-answer properties of the field operators on the GPU, restated from
+the reference's tests.
+
+Scaling and squaring (test_reghead.cpp:120-198): zero and constant velocities
+are exact, T = 7 matches dense forward-Euler integration, small velocities
+integrate fold-free, forward and backward integrations are mutually inverse,
+and the result converges in T (velocities from the reference's
+make_smooth_velocity, synth.cpp:75-90).  Compose (test_field_ops.cpp:112-160):
+zero is the identity, constants add, warping by a composite matches
+sequential warps, and composition is associative (the reference's own
+smooth_field / smooth_image test data)."""
 import numpy as np
 import pytest
 import torch
@@ -70,3 +75,72 @@ def test_ss_converges_in_steps(cuda, ref):
     a = ops.scaling_squaring(v, 7)
     b = ops.scaling_squaring(v, 8)
     assert float((a - b).abs().max()) <= 1e-3
+
+
+# ---- compose known answers (test_field_ops.cpp:112-160)
+def test_compose_identity_and_constants(cuda):
+    g = torch.Generator().manual_seed(11)
+    f = (torch.rand(3, 5, 5, 5, generator=g) * 2 - 1).cuda()
+    zero = torch.zeros_like(f)
+    assert torch.allclose(ops.compose(f, zero), f, rtol=1e-6, atol=0)
+    assert torch.allclose(ops.compose(zero, f), f, rtol=1e-6, atol=1e-7)
+    a = torch.zeros(3, 4, 4, 4, device="cuda")
+    b = torch.zeros_like(a)
+    a[0], a[2] = 0.4, -0.2
+    b[0], b[1] = 0.3, 0.1
+    c = ops.compose(a, b)
+    for comp, want in ((0, 0.7), (1, 0.1), (2, -0.2)):
+        assert torch.allclose(c[comp], torch.full_like(c[comp], want), rtol=1e-6, atol=0)
+
+
+def _rng_draws(seed, specs):
+    r = ops.Rng(seed)
+    return [float(r.uniform((1,), lo, hi)[0]) for lo, hi in specs]
+
+
+def _smooth_field(dims, amplitude, waves, seed):
+    """test_field_ops.cpp:15-34 smooth_field (the reference's test data)."""
+    h, w, l = dims
+    z, y, x = np.meshgrid(np.arange(l), np.arange(w), np.arange(h), indexing="ij")
+    r = ops.Rng(seed)
+    out = np.zeros((3, l, w, h), np.float32)
+    tp = np.float32(2.0 * 3.14159265)
+    for comp in range(3):
+        ax, px, py, pz = (float(r.uniform((1,), lo, hi)[0])
+                          for lo, hi in ((0.2, 1.0), (0.0, 6.28), (0.0, 6.28), (0.0, 6.28)))
+        out[comp] = (np.float32(amplitude) * np.float32(ax)
+                     * np.sin(tp * x / np.float32(waves * h) + np.float32(px))
+                     * np.cos(tp * y / np.float32(waves * w) + np.float32(py))
+                     * np.sin(tp * z / np.float32(waves * l) + np.float32(pz))).astype(np.float32)
+    return torch.from_numpy(out).cuda()
+
+
+def _smooth_image(dims, waves, seed):
+    """test_field_ops.cpp:36-48 smooth_image."""
+    h, w, l = dims
+    z, y, x = np.meshgrid(np.arange(l), np.arange(w), np.arange(h), indexing="ij")
+    p1, p2 = _rng_draws(seed, ((0.0, 6.28), (0.0, 6.28)))
+    tp = np.float32(2.0 * 3.14159265)
+    v = np.float32(0.6) * (np.sin(tp * x / np.float32(waves * h) + np.float32(p1))
+                           * np.cos(tp * (y + z) / np.float32(waves * (w + l)) + np.float32(p2))
+                           + np.float32(0.5) * np.cos(tp * z / np.float32(waves * l)
+                                                      + np.float32(p1)))
+    return torch.from_numpy(v.astype(np.float32)).cuda().view(1, l, w, h).contiguous()
+
+
+def test_compose_matches_sequential_warps(cuda):
+    dims = (8, 8, 8)
+    img = _smooth_image(dims, 2.5, 13)
+    prev = _smooth_field(dims, 0.8, 2.5, 17)
+    res = _smooth_field(dims, 0.8, 2.5, 19)
+    once = ops.warp(img, ops.compose(prev, res))
+    twice = ops.warp(ops.warp(img, prev), res)
+    assert float((once - twice).abs().max()) <= 2e-2
+
+
+def test_compose_associative(cuda):
+    dims = (8, 8, 8)
+    a, b, c = (_smooth_field(dims, 0.9, 3.5, s) for s in (23, 29, 31))
+    left = ops.compose(ops.compose(a, b), c)
+    right = ops.compose(a, ops.compose(b, c))
+    assert float((left - right).abs().max()) <= 5e-2
