@@ -234,21 +234,11 @@ __device__ __forceinline__ void t_wait(uint64_t *b, unsigned phase) {
     } while (!done);
 }
 
-// the next InstanceNorm+LReLU backward's per-channel sums, fused into the
-// epilogue of the conv that produces its upstream gradient (x = the norm's
-// input, gz = this conv's output): part[c][tile] = {sum gy, sum gy * xh} with
-// gy = gz * lrelu'(g xh + b), xh = (x - mean) inv  (as in_bwd_sum_k)
-struct NormBwdArgs {
-    const float *x, *mean, *inv, *g, *b;
-    float slope;
-    float2 *part;
-};
-
 template <bool ACC>
 __global__ void __launch_bounds__(NT, 2)
 conv3t_k(const __grid_constant__ CUtensorMap map, int cin, D3 d, const float *__restrict__ wB,
          int cpad, const float *__restrict__ bias, int cout, float *__restrict__ out,
-         float2 *__restrict__ stats, NormBwdArgs nbw) {
+         float2 *__restrict__ stats) {
     extern __shared__ __align__(128) float tsm[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(tsm + 2 * TBUF);
     const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
@@ -384,57 +374,6 @@ conv3t_k(const __grid_constant__ CUtensorMap map, int cin, D3 d, const float *__
             const int ntiles = gridDim.x * gridDim.y * ((d.l + TV - 1) / TV);
             const int tile = (zb * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
             stats[(int64_t)(o0 + threadIdx.x) * ntiles + tile] = make_float2(sum_keep, m2);
-        }
-    }
-    if (!ACC && nbw.x) {
-        __shared__ float nred[8][2 * OCB];
-        const bool inxy = x < d.h && y < d.w;
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        float sg[OCB], sx[OCB];
-#pragma unroll
-        for (int j = 0; j < OCB; ++j) sg[j] = sx[j] = 0.0f;
-#pragma unroll
-        for (int j = 0; j < OCB; ++j) {
-            const int o = o0 + j;
-            if (o >= cout) continue;
-            const float mu = nbw.mean[o], iv = nbw.inv[o], gg = nbw.g[o], bb = nbw.b[o];
-#pragma unroll
-            for (int v = 0; v < TV; ++v) {
-                const int z = z0 + v;
-                if (inxy && z < d.l) {
-                    const float gz = (j & 1) ? acc[v][j >> 1].y : acc[v][j >> 1].x;
-                    const float xv = __ldg(nbw.x + (int64_t)o * d.n + ((int64_t)z * d.w + y) * d.h + x);
-                    const float xh = (xv - mu) * iv;
-                    const float yy = gg * xh + bb;
-                    const float gy = gz * (yy > 0.0f ? 1.0f : nbw.slope);
-                    sg[j] += gy;
-                    sx[j] = fmaf(gy, xh, sx[j]);
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < OCB; ++j) {
-#pragma unroll
-            for (int m = 16; m > 0; m >>= 1) {
-                sg[j] += __shfl_xor_sync(0xffffffffu, sg[j], m);
-                sx[j] += __shfl_xor_sync(0xffffffffu, sx[j], m);
-            }
-            if (lane == 0) {
-                nred[wid][2 * j] = sg[j];
-                nred[wid][2 * j + 1] = sx[j];
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x < OCB && o0 + threadIdx.x < cout) {
-            float a = 0.0f, bsum = 0.0f;
-#pragma unroll
-            for (int w8 = 0; w8 < 8; ++w8) {
-                a += nred[w8][2 * threadIdx.x];
-                bsum += nred[w8][2 * threadIdx.x + 1];
-            }
-            const int ntiles = gridDim.x * gridDim.y * ((d.l + TV - 1) / TV);
-            const int tile = (zb * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-            nbw.part[(int64_t)(o0 + threadIdx.x) * ntiles + tile] = make_float2(a, bsum);
         }
     }
     if (x >= d.h || y >= d.w) return;
@@ -1203,7 +1142,7 @@ static bool conv_map(CUtensorMap *m, const float *base, const D3 &d, int C) {
 template <bool ACC>
 static mdg_status conv3t_launch(const CUtensorMap &map, const float *w, int oc, int ic, bool flip,
                                 const D3 &d, const float *bias, float *out, cudaStream_t st,
-                                float *norm_stats = nullptr, NormBwdFuse *nf = nullptr) {
+                                float *norm_stats = nullptr) {
     const int cin = flip ? oc : ic, cout = flip ? ic : oc;
     const int cpad = (cin + CIB - 1) / CIB * CIB, nob = (cout + OCB - 1) / OCB;
     Scratch wb;
@@ -1214,24 +1153,13 @@ static mdg_status conv3t_launch(const CUtensorMap &map, const float *w, int oc, 
     MDG_CUDA_TRY(cudaFuncSetAttribute(conv3t_k<ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)TSMEM));
     const dim3 g((d.h + TX - 1) / TX, (d.w + TY - 1) / TY, ((d.l + TV - 1) / TV) * nob);
-    Scratch sp, np;
+    Scratch sp;
     const int ntx = g.x, nty = g.y, ntz = (d.l + TV - 1) / TV;
-    const int ntiles = ntx * nty * ntz;
-    if (norm_stats) MDG_CUDA_TRY(sp.alloc((size_t)cout * ntiles * sizeof(float2), st));
-    NormBwdArgs nbw{};
-    if (!ACC && nf) {
-        MDG_CUDA_TRY(np.alloc((size_t)cout * ntiles * sizeof(float2), st));
-        nbw = NormBwdArgs{nf->x, nf->mean, nf->inv, nf->g, nf->b, nf->slope, np.as<float2>()};
-    }
+    if (norm_stats)
+        MDG_CUDA_TRY(sp.alloc((size_t)cout * ntx * nty * ntz * sizeof(float2), st));
     conv3t_k<ACC><<<g, NT, TSMEM, st>>>(map, cin, d, wb.as<float>(), cpad, bias, cout, out,
-                                        norm_stats ? sp.as<float2>() : nullptr, nbw);
+                                        norm_stats ? sp.as<float2>() : nullptr);
     MDG_LAUNCHED();
-    if (!ACC && nf) {
-        in_bwd_final_k<<<cout, 256, 0, st>>>(reinterpret_cast<const float *>(np.as<float2>()),
-                                             ntiles, nf->sums, nf->gg, nf->gbeta);
-        MDG_LAUNCHED();
-        nf->done = true;
-    }
     if (norm_stats) {
         in_stats_k<<<cout, 256, 0, st>>>(sp.as<float2>(), d, ntx, nty, ntz, 1e-5f, norm_stats,
                                          norm_stats + cout);
@@ -1330,8 +1258,7 @@ mdg_status enc_conv3_fwd(const float *in, int ic, mdg_dims3 dd, const float *w, 
 
 mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 dd, const float *w, int oc,
                          const float *gout, float *gin, float *gw, float *gb, cudaStream_t st,
-                         bool gin_acc, NormBwdFuse *nf) {
-    if (nf) nf->done = false;
+                         bool gin_acc) {
     const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
     if (gin) {
         const bool ig = use_igemm(ic, oc, d);
@@ -1339,8 +1266,7 @@ mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 dd, const float *w, 
         if (!ig && conv_map(&map, gout, d, oc)) {
             const mdg_status s2 =
                 gin_acc ? conv3t_launch<true>(map, w, oc, ic, true, d, nullptr, gin, st)
-                        : conv3t_launch<false>(map, w, oc, ic, true, d, nullptr, gin, st, nullptr,
-                                               nf);
+                        : conv3t_launch<false>(map, w, oc, ic, true, d, nullptr, gin, st);
             if (s2 != MDG_OK) return s2;
         } else {
             const int tile = ig ? igemm_fwd_bn(ic) : OCB;
@@ -1419,19 +1345,6 @@ mdg_status enc_in_lrelu_fwd(const float *x, int C, int64_t n, const float *g, co
     MDG_LAUNCHED();
     (vec ? in_apply_k<true> : in_apply_k<false>)<<<dim3(gx, C), 256, 0, st>>>(x, (int)n, mean, inv,
                                                                             g, b, slope, z);
-    MDG_LAUNCHED();
-    return MDG_OK;
-}
-
-// the norm backward's apply pass with the sums from the fused conv epilogue
-mdg_status enc_in_lrelu_bwd_apply(const float *x, const float *gz, int C, int64_t n,
-                                  const float *g, const float *b, float slope, const float *mean,
-                                  const float *inv, const float *sums, float *gx, cudaStream_t st) {
-    const bool vec = n % 4 == 0;
-    const unsigned nb = plane_blocks(vec ? n / 4 : n, C);
-    const PoolSrc ps{nullptr, D3{0, 0, 0, (int)n}, D3{0, 0, 0, 0}};
-    (vec ? in_bwd_apply_k<true> : in_bwd_apply_k<false>)<<<dim3(nb, C), 256, 0, st>>>(
-        x, gz, ps, (int)n, mean, inv, g, b, slope, sums, gx);
     MDG_LAUNCHED();
     return MDG_OK;
 }

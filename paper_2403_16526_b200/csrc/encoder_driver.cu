@@ -28,7 +28,6 @@ struct mdg_encoder {
     std::vector<Level> lv;
     float slope = 0.2f;
     float *scratch_a = nullptr, *scratch_b = nullptr;  // max C*n each
-    float *nsums = nullptr;  // 2 * max C: the fused norm-backward sums
     void *arena = nullptr;
     int64_t bytes = 0;
     std::vector<mdg_block_params> p_saved;
@@ -67,7 +66,6 @@ void enc_layout(mdg_encoder *e, Carve2 &cv, mdg_dims3 d0, int base, int levels) 
     }
     e->scratch_a = cv.take(mx);
     e->scratch_b = cv.take(mx);
-    e->nsums = cv.take(2 * (int64_t)(base << (levels - 1)));
 }
 }  // namespace
 
@@ -178,21 +176,12 @@ mdg_status mdg_encoder_backward(mdg_encoder *e, const float *const *gfeatures,
         ENC_TRY(enc_in_lrelu_bwd(L.a2, gfeatures[k], pool, L.d, L.c, L.n, P.g2, P.be2, e->slope,
                                  L.st2, L.st2 + L.c, ga, G ? G->g2 : nullptr,
                                  G ? G->be2 : nullptr, st));
-        // conv2's input gradient gz1, with z1 = lrelu(IN1(a1))'s backward sums
-        // fused into its epilogue when the TMA path runs
-        NormBwdFuse nf{L.a1,           L.st1,   L.st1 + L.c,          P.g1,
-                       P.be1,          e->slope, e->nsums,            G ? G->g1 : nullptr,
-                       G ? G->be1 : nullptr, false};
         ENC_TRY(enc_conv3_bwd(L.z1, L.c, L.d, P.w2, L.c, ga, gz1, G ? G->w2 : nullptr,
-                              G ? G->b2 : nullptr, st, /*gin_acc=*/false, &nf));
-        // ga reused
-        if (nf.done)
-            ENC_TRY(enc_in_lrelu_bwd_apply(L.a1, gz1, L.c, L.n, P.g1, P.be1, e->slope, L.st1,
-                                           L.st1 + L.c, e->nsums, ga, st));
-        else
-            ENC_TRY(enc_in_lrelu_bwd(L.a1, gz1, nullptr, L.d, L.c, L.n, P.g1, P.be1, e->slope,
-                                     L.st1, L.st1 + L.c, ga, G ? G->g1 : nullptr,
-                                     G ? G->be1 : nullptr, st));
+                              G ? G->b2 : nullptr, st, /*gin_acc=*/false));
+        // z1 = lrelu(IN1(a1)); ga reused
+        ENC_TRY(enc_in_lrelu_bwd(L.a1, gz1, nullptr, L.d, L.c, L.n, P.g1, P.be1, e->slope, L.st1,
+                                 L.st1 + L.c, ga, G ? G->g1 : nullptr, G ? G->be1 : nullptr,
+                                 st));
         // conv1 input gradient: overwritten into scratch for the finer level's
         // fused pool backward, or accumulated into the image gradient
         float *gx = k > 0 ? gz1 : gimage;

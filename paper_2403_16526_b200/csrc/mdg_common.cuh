@@ -152,24 +152,10 @@ mdg_status enc_conv3_fwd(const float *in, int ic, mdg_dims3 d, const float *w, c
 mdg_status enc_in_lrelu_apply(const float *x, int C, int64_t n, const float *g, const float *b,
                               float slope, float *z, const float *mean, const float *inv,
                               cudaStream_t st);
-// the next InstanceNorm+LReLU backward's sums fused into the input-gradient
-// conv (when its TMA path runs): x / mean / inv / g / b of that norm, sums
-// (device, 2C) receives {sum gy, sum gy xh} per channel, gg / gbeta (nullable)
-// accumulate; done reports whether the fused path ran
-struct NormBwdFuse {
-    const float *x, *mean, *inv, *g, *b;
-    float slope;
-    float *sums, *gg, *gbeta;
-    bool done;
-};
 // gin_acc: accumulate into gin (else overwrite)
 mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 d, const float *w, int oc,
                          const float *gout, float *gin, float *gw, float *gb, cudaStream_t st,
-                         bool gin_acc = true, NormBwdFuse *nf = nullptr);
-// the norm backward's apply pass with the sums already known (fused)
-mdg_status enc_in_lrelu_bwd_apply(const float *x, const float *gz, int C, int64_t n,
-                                  const float *g, const float *b, float slope, const float *mean,
-                                  const float *inv, const float *sums, float *gx, cudaStream_t st);
+                         bool gin_acc = true);
 mdg_status enc_in_lrelu_fwd(const float *x, int C, int64_t n, const float *g, const float *b,
                             float slope, float *z, float *mean, float *inv, cudaStream_t st);
 // gz: gradient of the block output (nullable); pg: the coarser level's input
