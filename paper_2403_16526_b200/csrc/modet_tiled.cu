@@ -978,10 +978,12 @@ static bool make_maps_a(MapsA *m, const float *Q, const float *LSE, const float 
            make_map(&m->g, gSF, v, 3 * S, bx, by) && make_map(&m->sf, SF, v, 3 * S, bx, by);
 }
 
-static int pick_zc(int tiles, int l, int per_sm) {
-    // enough CTAs for `per_sm` resident per SM on 148 SMs (x2 for balance),
-    // chunks of >= 8 planes
-    const int want = 148 * per_sm * 2;
+static int pick_zc(int tiles, int l, int per_sm, int waves) {
+    // about `waves` x (per_sm resident per SM on 148 SMs) CTAs, chunks of
+    // >= 8 planes.  Measured at 160x192x224 (S = 1): forward best at 3,
+    // backward at 5 (shorter chunks balance the last wave; 2 was 4-8 %
+    // slower, 8+ pays too many chunk prologues)
+    const int want = 148 * per_sm * waves;
     int nzc = (want + tiles - 1) / max(tiles, 1);
     nzc = max(1, min(nzc, (l + 7) / 8));
     return (l + nzc - 1) / nzc;
@@ -1001,7 +1003,7 @@ static cudaError_t fwd_launch(const float *Q, const float *K, const float *B, md
                               float *SF, float *LSE, unsigned long long *flag, cudaStream_t st) {
     const Vol v{d.h, d.w, d.l, (int64_t)d.h * d.w * d.l, (int64_t)d.h * d.w};
     const int gx = (d.h + FTX - 1) / FTX, gy = (d.w + FTY - 1) / FTY;
-    const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 3 : 2);
+    const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 3 : 2, 3);
     const int nzc = (d.l + zc - 1) / zc;
     const size_t sm = (2 * D * (FG::HCH + FG::OCH) + kTail) * sizeof(float);
     Maps m{};
@@ -1056,7 +1058,7 @@ static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, co
     if (gK && (e = cudaMallocAsync(&aux, (size_t)2 * S * v.n * sizeof(float), st))) return e;
     if (gQ || gB || gK) {
         const int gx = (d.h + RTX - 1) / RTX, gy = (d.w + RTY - 1) / RTY;
-        const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 2 : 1);
+        const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 2 : 1, 5);
         const int nzc = (d.l + zc - 1) / zc;
         const int ncta = gx * gy * nzc;
         float *part = nullptr;
@@ -1083,7 +1085,7 @@ static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, co
     }
     if (gK) {
         const int gx = (d.h + CTX - 1) / CTX, gy = (d.w + CTY - 1) / CTY;
-        const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 2 : 1);
+        const int zc = pick_zc(gx * gy * S, d.l, D <= 6 ? 2 : 1, 5);
         const int nzc = (d.l + zc - 1) / zc;
         const size_t sm = (2 * ((D + 5) * CG::HCH + D * CG::OCH) + kTail) * sizeof(float);
         Maps m{};
