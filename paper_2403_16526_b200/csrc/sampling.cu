@@ -143,7 +143,7 @@ __device__ __forceinline__ void grad_oct(const Oct &o, const Corners &c, float g
 // 8*CT corner loads issued before any interpolation (memory-level
 // parallelism); CT == 0: runtime channel loop.
 template <int CT>
-__global__ void __launch_bounds__(kSB)
+__global__ void __launch_bounds__(kSB, CT > 0 ? 8 : 1)
 warp_fwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, float *__restrict__ out, int64_t pb, int64_t pe) {
     const int64_t n = (int64_t)h * w * l;
@@ -249,7 +249,7 @@ __device__ __forceinline__ void scatter_row2(float *ia, float *ib, bool two, boo
 // --------------------------------------------------------------- warp bwd
 // sampling.hpp:139-167 (gfield: same per-channel order => bit-exact)
 template <int CT, bool COMPOSE = false>
-__global__ void __launch_bounds__(kSB, 4)
+__global__ void __launch_bounds__(kSB, CT == 16 ? 4 : 5)
 warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, const float *__restrict__ gout,
            float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe) {
