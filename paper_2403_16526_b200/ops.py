@@ -923,6 +923,29 @@ class NativeModel:
         phi = _wrap_device(self._L.mdg_model_phi(self._h), self._phi.shape, self._phi.device)
         return self._terms.clone(), phi.clone()
 
+    def pairwise_optimize(self, fixed, moving, iters=50, lr=1e-4, labels_fixed=None,
+                          labels_moving=None, graph=True):
+        """pairwise_optimize (engine.hpp:377-411) on the native driver: `iters`
+        Adam updates (each one CUDA graph replay) then a final evaluation
+        forward.  Returns (loss_trace, dice_trace, phi) like PoResult; the loss
+        is read back and checked finite every iteration as the reference does."""
+        loss_trace, dice_trace = [], []
+        with_dice = labels_fixed is not None and labels_moving is not None
+        phi = None
+        for i in range(iters + 1):
+            last = i == iters
+            if last:
+                terms, phi = self.loss_step(fixed, moving, backward=False)
+            else:  # the returned loss/phi are the forward before this update
+                terms, phi = self.po_step(fixed, moving, lr, graph=graph)
+            loss = float(terms[0])
+            if not (loss == loss and abs(loss) != float("inf")):
+                raise NumericError(f"optimization: non-finite loss ({loss})")
+            loss_trace.append(loss)
+            if with_dice:
+                dice_trace.append(mean_dice(labels_fixed, warp_labels(labels_moving, phi)))
+        return loss_trace, dice_trace, phi
+
 
 def _wrap_device(ptr, shape, device):
     """A torch view of libmdg-owned device memory (float32, contiguous); valid
