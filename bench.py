@@ -47,11 +47,11 @@ BYTES = {
     "warp_fwd": 4 * (3 + 2 * CH),
     "warp_bwd": 4 * (6 + 3 * CH),
 }
-KERNEL_NAMES = {  # op -> the dominant CUDA kernel it launches
-    "modet_fwd": "modet_fwd_k",
-    "modet_bwd": "modet_bwd_k",
-    "warp_fwd": "warp_fwd_k",
-    "warp_bwd": "warp_bwd_k",
+KERNEL_NAMES = {  # op -> the CUDA kernels it launches (ncu names, in launch order)
+    "modet_fwd": ["modet_fwd_tiled_k", "modet_fwd_fixup_k"],
+    "modet_bwd": ["modet_bwd_row_k", "modet_bwd_col_k", "reduce_db_k"],
+    "warp_fwd": ["warp_fwd_k"],
+    "warp_bwd": ["warp_bwd_k"],
 }
 
 
@@ -65,13 +65,26 @@ def load_peak():
 
 
 def load_ncu_traffic():
-    """dram bytes per launch from the committed ncu --set full summary."""
+    """dram bytes per launch of each kernel, from the committed ncu --set full
+    capture of this bench's step (profiles/ncu_traffic.json, written by
+    profiles/summarize_ncu.py)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             return json.load(f)
     except Exception:
         return {}
+
+
+def op_traffic(op):
+    """ncu DRAM bytes of one launch of `op` (sum over its kernels), or None
+    when the committed capture lacks one of them."""
+    t = load_ncu_traffic().get("kernels", {})
+    vals = [t.get(k, {}).get("dram_bytes") for k in KERNEL_NAMES[op]]
+    vals = [v for k, v in zip(KERNEL_NAMES[op], vals) if v is not None or k in t]
+    if not vals or any(v is None for v in vals):
+        return None
+    return int(sum(vals))
 
 
 # ------------------------------------------------------------ clock sampler
@@ -147,16 +160,9 @@ def make_inputs(rank: int):
     B = r.uniform((S, 27), -0.5, 0.5)
     gSF = ops.Rng(6 + base).uniform((3 * S, n), -1.0, 1.0)
     feat = ops.Rng(7 + base).normal((CH, l, w, h))
-    # smooth displacement: low-frequency sinusoids, amplitude 2 voxels
-    zz, yy, xx = torch.meshgrid(torch.arange(l, dtype=torch.float32),
-                                torch.arange(w, dtype=torch.float32),
-                                torch.arange(h, dtype=torch.float32), indexing="ij")
-    ph = ops.Rng(8 + base).uniform((9,), 0.0, 6.28).tolist()
-    field = torch.stack([
-        2.0 * torch.sin(xx / 23.0 + ph[0]) * torch.cos(yy / 29.0 + ph[1]) * torch.sin(zz / 31.0 + ph[2]),
-        2.0 * torch.cos(xx / 27.0 + ph[3]) * torch.sin(yy / 19.0 + ph[4]) * torch.cos(zz / 25.0 + ph[5]),
-        2.0 * torch.sin(xx / 21.0 + ph[6]) * torch.sin(yy / 33.0 + ph[7]) * torch.cos(zz / 17.0 + ph[8]),
-    ]).contiguous()
+    # phi = make_smooth_velocity(dims, seed 11, 2.0 vox, sigma 4)
+    # (synth.cpp:75-90, native and bit-identical)
+    field = ops.make_smooth_velocity(DIMS, 11 + base, 2.0, 4.0)
     gout = ops.Rng(9 + base).normal((CH, l, w, h))
     return dict(Q=Q, K=K, B=B, gSF=gSF, feat=feat, field=field, gout=gout)
 
@@ -254,10 +260,16 @@ def run_ours(args):
     pyramid = None if args.no_pyramid else run_pyramid(dev)
     po = None if args.no_po else run_po(dev, world, args.po_pairs)
 
+    # the warp's worst case for gather locality: i.i.d. random_field (test_util.hpp:40-48)
+    warp_rf = None if args.no_random_field else run_warp_random_field(L, d3, feat, gout, rank,
+                                                                     dev, st)
+    # config 2: the registration forward at 160x192x160 (LPBA-shaped)
+    cfg2 = None if args.no_cfg2 else run_cfg2(dev)
+
     peak, peak_kind = load_peak()
     dom = max(per_op, key=lambda k: per_op[k])
     achieved = BYTES[dom] * n / (per_op[dom] * 1e-3) / 1e9
-    traffic = load_ncu_traffic().get(KERNEL_NAMES[dom])
+    traffic = op_traffic(dom)
     step_bytes = sum(BYTES.values()) * n
     result = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
@@ -269,16 +281,22 @@ def run_ours(args):
                    "parallelism": f"pair-parallel x{world} (independent volume per GPU)",
                    "l2": "inputs larger than L2 (step footprint ~1.4 GB), no flush"},
         "per_op_ms": {k: round(v, 4) for k, v in per_op.items()},
-        "roofline": {"bound": "hbm", "kernel": KERNEL_NAMES[dom],
+        "roofline": {"bound": "hbm", "op": dom, "kernel": " + ".join(KERNEL_NAMES[dom]),
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full of this step)",
                      "peak_kind": peak_kind,
                      "bytes_per_launch": BYTES[dom] * n},
+        "roofline_per_op": {op: {"ms": round(per_op[op], 4), "alg_bytes": BYTES[op] * n,
+                                 "frac": round(BYTES[op] * n / (per_op[op] * 1e-3) / 1e9 / peak, 4),
+                                 "ncu_dram_bytes": op_traffic(op)} for op in ops_order},
         "roofline_step": {"achieved": round(step_bytes / (ms_max * 1e-3) / 1e9, 1),
                           "peak": peak, "unit": "GB/s",
                           "frac": round(step_bytes / (ms_max * 1e-3) / 1e9 / peak, 4),
                           "bytes_per_step": step_bytes},
         "e2e": e2e,
+        "warp_random_field": warp_rf,
+        "cfg2": cfg2,
         "pyramid": pyramid,
         "po": po,
         "gpu_launches": int(launches),
@@ -290,6 +308,72 @@ def run_ours(args):
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_warp_random_field(L, d3, feat, gout, rank, dev, st, reps=10):
+    """Warp fwd + bwd (C=8) at 160x192x224 with the i.i.d. random_field
+    displacement (|phi| in [0.3, 2] voxels, random sign per entry): the gather
+    / scatter locality worst case, timed beside the smooth-field headline."""
+    import torch
+
+    from paper_2403_16526_b200 import ops
+
+    fld = ops.random_field(DIMS, 12 + 1000 * rank, 2.0).to(dev)
+    out = torch.empty_like(feat)
+    gin, gf = torch.zeros_like(feat), torch.zeros_like(fld)
+    sp = st.cuda_stream
+
+    def go(ev=None):
+        if ev: ev[0].record(st)
+        L.mdg_warp_fwd(feat.data_ptr(), CH, d3, fld.data_ptr(), out.data_ptr(), sp)
+        if ev: ev[1].record(st)
+        L.mdg_warp_bwd(feat.data_ptr(), CH, d3, fld.data_ptr(), gout.data_ptr(), gin.data_ptr(),
+                       gf.data_ptr(), sp)
+        if ev: ev[2].record(st)
+
+    for _ in range(3):
+        go()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(reps)]
+    for e in evs:
+        go(e)
+    torch.cuda.synchronize()
+    n = DIMS[0] * DIMS[1] * DIMS[2]
+    f = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
+    b = statistics.median(e[1].elapsed_time(e[2]) for e in evs)
+    return {"field": "random_field(dims, seed 12, mag 2.0) (test_util.hpp:40-48)",
+            "warp_fwd_ms": round(f, 4), "warp_bwd_ms": round(b, 4),
+            "Gvoxel_per_s": round(n / ((f + b) * 1e-3) / 1e9, 3)}
+
+
+def run_cfg2(dev, reps=5):
+    """BASELINE config 2: the registration forward (encoder x2 -> 5-level
+    ModeT pyramid with RegHead and warps -> NCC/grad_reg loss) of the small
+    preset on the synthetic LPBA-shaped pair make_synth_pair(160x192x160,
+    seed 1), init_model(42) weights, native driver; device time per forward."""
+    import torch
+
+    from paper_2403_16526_b200 import ops
+
+    dims = (160, 192, 160)
+    f, m, _, _, _ = ops.synth_pair(dims, seed=1, max_disp=2.0)
+    f, m = f.to(dev), m.to(dev)
+    model = ops.NativeModel([t.to(dev) for t in ops.init_model(42)], dims)
+    for _ in range(2):
+        model.loss_step(f, m, backward=False)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ts = []
+    for _ in range(reps):
+        e[0].record()
+        model.loss_step(f, m, backward=False)
+        e[1].record()
+        torch.cuda.synchronize()
+        ts.append(e[0].elapsed_time(e[1]))
+    ms = statistics.median(ts)
+    del model
+    return {"workload": "registration forward (encoder x2 + 5-level pyramid + loss), small "
+                        "preset, make_synth_pair(160x192x160, seed 1)",
+            "fwd_ms": round(ms, 3), "pairs_per_sec_forward_only": round(1e3 / ms, 2)}
 
 
 def run_pyramid(dev, reps=5):
@@ -388,12 +472,11 @@ def run_po(dev, world, pairs=0, reps=5):
 
     from paper_2403_16526_b200 import ops
 
-    h, w, l = DIMS
     params = [t.to(dev) for t in ops.init_model(42)]
     model = ops.NativeModel(params, DIMS)  # mdg_model_*: the C++ model driver
-    rng = ops.Rng(11)
-    fixed = rng.uniform((1, l, w, h), 0.0, 1.0).to(dev)
-    moving = rng.uniform((1, l, w, h), 0.0, 1.0).to(dev)
+    # make_synth_pair(dims, seed, max_disp 2.0), native, bit-identical
+    fixed, moving, _, _, _ = ops.synth_pair(DIMS, seed=1, max_disp=2.0)
+    fixed, moving = fixed.to(dev), moving.to(dev)
     # a dedicated stream: the legacy default stream cannot be captured, and the
     # iteration runs as one CUDA graph (mdg_model_po_step)
     side = torch.cuda.Stream(device=dev)
@@ -420,7 +503,7 @@ def run_po(dev, world, pairs=0, reps=5):
         t = torch.tensor([it_ms, fwd_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         it_ms, fwd_ms = float(t[0].item()), float(t[1].item())
-    out = {"workload": "PO of the small-preset model at 160x192x224 (synthetic pair, "
+    out = {"workload": "PO of the small-preset model at 160x192x224 (make_synth_pair seed 1, "
                        "init_model(42) weights), native model driver (mdg_model_*), "
                        "one CUDA graph per iteration",
            "iter_ms": round(it_ms, 3), "final_forward_ms": round(fwd_ms, 3),
@@ -520,7 +603,9 @@ def run_e2e(args, L, host_in, world, dev):
 
 
 # ----------------------------------------------------- reference CPU arm
-REF_SLAB_Z = 8  # each worker's bounded sample: a 160x192x8 depth slab
+REF_SLAB_Z = 32  # each worker's bounded sample: a 160x192x32 depth slab (W alone
+                 # is 106 MB per worker: not cache-resident; 2 of 32 planes are
+                 # slab boundaries)
 
 
 def _ref_worker_inputs(seed):
@@ -536,7 +621,8 @@ def _ref_worker_inputs(seed):
     B = f(r.uniform(S * 27, -0.5, 0.5).reshape(S, 27))
     gSF = f(pyoracle.Rng(seed + 1).uniform(3 * S * n, -1, 1).reshape(3 * S, REF_SLAB_Z, w, h))
     feat = f(pyoracle.Rng(seed + 2).normal(CH * n).reshape(CH, REF_SLAB_Z, w, h))
-    fld = f(pyoracle.Rng(seed + 3).uniform(3 * n, -2, 2).reshape(3, REF_SLAB_Z, w, h))
+    # the same field distribution as the GPU arm: make_smooth_velocity (synth.cpp:75-90)
+    fld = f(pyoracle.ref().make_smooth_velocity(dims, seed + 3, 2.0, 4.0))
     gout = f(pyoracle.Rng(seed + 4).normal(CH * n).reshape(CH, REF_SLAB_Z, w, h))
     return dims, (Q, K, B, gSF, feat, fld, gout)
 
@@ -560,7 +646,7 @@ def _cpu_run(kind, threads, steps, warmup):
     import pyoracle
 
     if kind == "reference":
-        lib = pyoracle.ref()
+        lib = pyoracle.ref_fast()  # -O3, native ISA
     else:
         lib = pyoracle.mdo()
     work = [_ref_worker_inputs(100 + 17 * i) for i in range(threads)]
@@ -601,6 +687,7 @@ def cpu_baseline(seconds):
     if steps > 1:
         v, dt, nvox = _cpu_run(kind, threads, steps, 0)
     return {"value": round(v, 6), "unit": UNIT, "cores": threads, "kind": kind,
+            "build": os.path.basename(pyoracle.ref_fast_path()) if kind == "reference" else "mdo",
             "sample": f"{threads} threads x one 160x192x{REF_SLAB_Z} slab each "
                       f"({nvox} voxels/step), {steps} step(s) of {dt:.2f}s: "
                       "na_fused_fwd+subfields_fwd+subfields_bwd+na_fused_bwd+warp_fwd+warp_bwd",
@@ -625,6 +712,7 @@ def run_reference(args):
         "config": {"workload": "L1 160x192x224: ModeT fwd+bwd (S=1,d=6,nb=3) + warp fwd+bwd (C=8)",
                    "sample": f"per step: {threads} CPU threads, one 160x192x{REF_SLAB_Z} slab each"},
         "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": threads, "kind": kind,
+                         "build": os.path.basename(pyoracle.ref_fast_path()),
                          "sample": f"{threads} x 160x192x{REF_SLAB_Z} slabs ({nvox} voxels) per step"},
         "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -643,6 +731,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling)")
     ap.add_argument("--no-pyramid", action="store_true", help="skip the pyramid timing")
     ap.add_argument("--no-po", action="store_true", help="skip the PO-iteration timing")
+    ap.add_argument("--no-random-field", action="store_true",
+                    help="skip the random_field warp timing")
+    ap.add_argument("--no-cfg2", action="store_true", help="skip the config-2 forward timing")
     ap.add_argument("--po-pairs", type=int, default=1,
                     help="run this many complete 50-iteration pairs (pairs/sec measured, "
                          "wall clock: model setup + 50 updates + the final evaluation)")

@@ -399,6 +399,18 @@ mdg_rng *mdg_rng_new(uint64_t seed);
 void mdg_rng_free(mdg_rng *r);
 void mdg_rng_fill_uniform(mdg_rng *r, float *out, int64_t n, double lo, double hi);
 void mdg_rng_fill_normal(mdg_rng *r, float *out, int64_t n, double mean, double sd);
+/* synth.cpp:75-90 make_smooth_velocity(dims, seed, magnitude, sigma): host
+ * {3, n}, bit-identical to the reference */
+mdg_status mdg_synth_smooth_velocity(mdg_dims3 d, uint64_t seed, float magnitude, float sigma,
+                                     float *out);
+/* tests/test_util.hpp:40-48 random_field(dims, seed, mag): i.i.d. entries of
+ * magnitude in [0.15, 1] * mag with random sign; host {3, n} */
+mdg_status mdg_synth_random_field(mdg_dims3 d, uint64_t seed, float mag, float *out);
+/* synth.cpp:92-192 make_synth_pair with SynthConfig defaults except seed and
+ * max_disp: host outputs {n} images, {n} labels, {3, n} ground truth
+ * (nullable).  Uses the device (scaling-and-squaring and warps). */
+mdg_status mdg_synth_pair(mdg_dims3 d, uint64_t seed, float max_disp, float *fixed,
+                          float *moving, int *labels_fixed, int *labels_moving, float *gt_field);
 
 /* ====================== file formats (§8f rank 4) =========================
  * Host-side, no device needed.  Byte-identical to the reference's writers

@@ -503,3 +503,42 @@ def ref() -> _Lib:
     if "ref" not in _cache:
         _cache["ref"] = _Lib(LIB_REF, "mdr_")
     return _cache["ref"]
+
+
+def _host_isa() -> str:
+    """x86-64 micro-architecture level of this host: v4 (AVX-512 F/BW/CD/DQ/VL)
+    or v3 (AVX2 + FMA + BMI2), else '' (neither fast build can run)."""
+    try:
+        flags = set()
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    flags = set(line.split(":", 1)[1].split())
+                    break
+    except OSError:
+        return ""
+    if {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"} <= flags:
+        return "v4"
+    if {"avx2", "fma", "bmi2", "movbe"} <= flags:
+        return "v3"
+    return ""
+
+
+def ref_fast_path() -> str:
+    """The -O3 native-ISA reference build for this host (BASELINE.md §4 flags),
+    else the pinned -O2 build."""
+    isa = _host_isa()
+    for level in (("v4", "v3") if isa == "v4" else (("v3",) if isa == "v3" else ())):
+        p = os.path.join(HERE, "_ref", f"libmdreg_ref_fast_{level}.so")
+        if os.path.exists(p):
+            return p
+    return LIB_REF
+
+
+def ref_fast() -> _Lib:
+    """The reference compiled as BASELINE.md §4 times it (-O3, native ISA):
+    the bench's CPU baseline and reference arm.  Not bit-pinned (FP
+    contraction on), so parity tests use ref()."""
+    if "ref_fast" not in _cache:
+        _cache["ref_fast"] = _Lib(ref_fast_path(), "mdr_")
+    return _cache["ref_fast"]

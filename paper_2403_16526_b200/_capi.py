@@ -174,6 +174,9 @@ SIGNATURES = {
     "mdg_rng_free": (None, [_p]),
     "mdg_rng_fill_uniform": (None, [_p, _p, C.c_int64, C.c_double, C.c_double]),
     "mdg_rng_fill_normal": (None, [_p, _p, C.c_int64, C.c_double, C.c_double]),
+    "mdg_synth_smooth_velocity": (_st, [Dims3, C.c_uint64, _f, _f, _p]),
+    "mdg_synth_random_field": (_st, [Dims3, C.c_uint64, _f, _p]),
+    "mdg_synth_pair": (_st, [Dims3, C.c_uint64, _f, _p, _p, _p, _p, _p]),
     "mdg_host_alloc": (_p, [C.c_size_t]),
     "mdg_host_free": (None, [_p]),
 }

@@ -486,7 +486,8 @@ mdg_status modet_fwd_host_pipelined(const float *Q, const float *K, const float 
     MDG_PIPE_TRY(cudaStreamSynchronize(P.down));
     MDG_PIPE_TRY(cudaStreamSynchronize(P.comp));
     // any non-finite logit: the caller reruns whole-volume for the exact position
-    unsigned long long *f = numeric_flag_ptr();
+    unsigned long long *f = numeric_flag_ptr(P.comp);
+    if (!f) return status_from_cuda(cudaErrorMemoryAllocation, "numeric flag");
     unsigned long long key = ~0ull;
     MDG_PIPE_TRY(cudaMemcpy(&key, f, sizeof(key), cudaMemcpyDeviceToHost));
     if (key != ~0ull) {
@@ -880,6 +881,9 @@ static mdg_status modet_bwd_host_whole(const float *Q, const float *K, const flo
     MDG_STAGE_TRY(sg.get(&dgQ, gQ, n * S * hd, acc));  // accumulate targets go up too
     MDG_STAGE_TRY(sg.get(&dgK, gK, n * S * hd, acc));
     MDG_STAGE_TRY(sg.get(&dgB, gB, (size_t)S * 27, acc));
+    // the device call always adds into gB: with accumulate == 0 the caller's
+    // gB is not uploaded, so start it from zero (as the pipelined path does)
+    if (!acc && dgB) MDG_STAGE_TRY(cudaMemsetAsync(dgB, 0, (size_t)S * 27 * sizeof(float), st));
     mdg_status r = mdg_modet_bwd(dQ, dK, dB, dSF, dL, dG, d, S, hd, nb, layout, dgQ, dgK, dgB,
                                  acc ? 1 : 0, st);
     if (r != MDG_OK) return r;

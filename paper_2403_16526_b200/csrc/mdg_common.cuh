@@ -53,21 +53,21 @@ inline bool dims_ok(mdg_dims3 d) {
 }
 
 // ----------------------------------------------- device-side numeric flag
-// One word per device: the smallest (head*n + p) key whose attention row
+// One word per (device, stream): the smallest (head*n + p) key whose attention row
 // produced a non-finite logit, or ~0ull.  Keys follow the reference's loop
 // order (attention.hpp:91-96: head outer, then z, y, x) so atomicMin yields
 // the position the reference would have thrown at.
-unsigned long long *numeric_flag_ptr();  // device pointer for the current device
+unsigned long long *numeric_flag_ptr(cudaStream_t st);  // of (current device, st)
 // read + reset; returns true if set, and the (x,y,z,head) decoded w.r.t. the
 // dims of the call that is checking
 mdg_status consume_numeric_flag(cudaStream_t st, mdg_dims3 d);
 
-// Per-device fixup queue for the fused ModeT forward: voxel-heads whose
+// Per-(device, stream) fixup queue for the fused ModeT forward: voxel-heads whose
 // branch-free online softmax overflowed (logit spread > 2^7 in log2 units
 // above the first row's max) or saw a non-finite logit are recomputed exactly
 // by a follow-up kernel.  Layout: [0] = count (uint32), then kFixupCap keys.
 constexpr int kFixupCap = 1 << 16;
-unsigned long long *fixup_queue_ptr();
+unsigned long long *fixup_queue_ptr(cudaStream_t st);
 
 // --------------------------------------------------- stream-ordered scratch
 // cudaMallocAsync/cudaFreeAsync from the device's default mempool.  The pool's

@@ -559,9 +559,10 @@ mdg_status mdg_modet_fwd(const float *Q, const float *K, const float *B, mdg_dim
     const int64_t n = nvox(d);
     if (n == 0) return MDG_OK;
     MDG_REQUIRE(Q && K && B && SF && LSE, "modet: null pointer");
-    unsigned long long *flag = numeric_flag_ptr();
-    const dim3 g(grid1d(n, kBlock), S);
     cudaStream_t st = S_(stream);
+    unsigned long long *flag = numeric_flag_ptr(st);
+    if (!flag) return status_from_cuda(cudaErrorMemoryAllocation, "numeric flag");
+    const dim3 g(grid1d(n, kBlock), S);
     if (layout == MDG_QK_PLANAR && !W) {
         cudaError_t e = cudaSuccess;
         if (tiled_fwd(hd, Q, K, B, d, S, SF, LSE, flag, st, &e)) {
@@ -626,7 +627,8 @@ mdg_status mdg_na_fused_fwd(const float *Q, const float *K, const float *B, mdg_
     if (n == 0) return MDG_OK;
     MDG_REQUIRE(Q && K && B && W, "na_fused_fwd: null pointer");
     cudaStream_t st = S_(stream);
-    unsigned long long *flag = numeric_flag_ptr();
+    unsigned long long *flag = numeric_flag_ptr(st);
+    if (!flag) return status_from_cuda(cudaErrorMemoryAllocation, "numeric flag");
     na_fwd_ref_k<<<dim3(grid1d(n, kBlock), S), kBlock, 0, st>>>(Q, K, B, d.h, d.w, d.l, S, hd,
                                                                 nb, W, flag);
     MDG_LAUNCHED();

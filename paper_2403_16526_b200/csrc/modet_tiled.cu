@@ -291,6 +291,7 @@ modet_fwd_fixup_k(const float *__restrict__ Q, const float *__restrict__ K,
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t key = all ? i : (int64_t)fixq[1 + i];
+        if (key < 0 || key >= (int64_t)S * v.n) continue;  // defensive: never this launch's
         const int s = (int)(key / v.n);
         const int64_t p = key - (int64_t)s * v.n;
         const int x = (int)(p % v.h), y = (int)((p / v.h) % v.w), z = (int)(p / v.hw);
@@ -1010,7 +1011,7 @@ static cudaError_t fwd_launch(const float *Q, const float *K, const float *B, md
     const bool tma = tma_ok(v, {Q, K}) && make_map(&m.k, K, v, S * D, kBoxX, FG::PY) &&
                      make_map(&m.a.q, Q, v, S * D, FTX, FTY);
     const dim3 grid(gx, gy, S * nzc);
-    unsigned long long *fixq = fixup_queue_ptr();
+    unsigned long long *fixq = fixup_queue_ptr(st);
     if (!fixq) return cudaErrorMemoryAllocation;
     cudaError_t e = cudaMemsetAsync(fixq, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;

@@ -2,6 +2,7 @@
 // pinned host memory and the small exact-index entry points of libmdg.
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -16,7 +17,6 @@ thread_local std::string t_err;
 thread_local int t_pos[4] = {-1, -1, -1, -1};
 
 std::mutex g_flag_mu;
-std::vector<unsigned long long *> g_flags;  // per device
 }  // namespace
 
 void set_error(mdg_status st, const std::string &msg) {
@@ -29,36 +29,70 @@ mdg_status status_from_cuda(cudaError_t e, const char *where) {
     return MDG_ECUDA;
 }
 
-unsigned long long *numeric_flag_ptr() {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(g_flag_mu);
-    if ((int)g_flags.size() <= dev) g_flags.resize(dev + 1, nullptr);
-    if (!g_flags[dev]) {
-        unsigned long long *p = nullptr;
-        if (cudaMalloc(&p, sizeof(unsigned long long)) != cudaSuccess) return nullptr;
-        cudaMemset(p, 0xff, sizeof(unsigned long long));
-        cudaDeviceSynchronize();
-        g_flags[dev] = p;
+// Per-(device, stream) state: the numeric flag and the ModeT fixup queue.
+// Stream-ordered use keeps one stream's calls from touching another's state,
+// so concurrent streams on one device (pair-parallel host threads) are safe.
+// Created once per stream and never freed (a few hundred KB), so pointers
+// baked into a captured CUDA graph stay valid.  Creation may happen while the
+// caller's stream is being captured: it switches this thread to relaxed
+// capture mode and initialises the words on a private non-blocking stream,
+// which neither joins nor breaks the capture.
+namespace {
+struct StreamState {
+    unsigned long long *flag = nullptr, *fixq = nullptr;
+};
+struct StreamKey {
+    int dev;
+    cudaStream_t st;
+    bool operator<(const StreamKey &o) const {
+        return dev != o.dev ? dev < o.dev : (uintptr_t)st < (uintptr_t)o.st;
     }
-    return g_flags[dev];
+};
+std::map<StreamKey, StreamState> g_states;
+
+__global__ void state_init_k(unsigned long long *flag, unsigned long long *fixq) {
+    *flag = ~0ull;
+    *fixq = 0ull;
 }
 
-unsigned long long *fixup_queue_ptr() {
-    static std::vector<unsigned long long *> queues;
+StreamState *stream_state(cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_flag_mu);
-    if ((int)queues.size() <= dev) queues.resize(dev + 1, nullptr);
-    if (!queues[dev]) {
-        unsigned long long *p = nullptr;
-        if (cudaMalloc(&p, (kFixupCap + 1) * sizeof(unsigned long long)) != cudaSuccess)
-            return nullptr;
-        cudaMemset(p, 0, sizeof(unsigned long long));
-        cudaDeviceSynchronize();
-        queues[dev] = p;
+    StreamState &s = g_states[StreamKey{dev, st}];
+    if (!s.flag) {
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        void *p = nullptr;
+        cudaStream_t init = nullptr;
+        bool ok = cudaMalloc(&p, (kFixupCap + 2) * sizeof(unsigned long long)) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&init, cudaStreamNonBlocking) == cudaSuccess;
+        if (ok) {
+            auto *w = static_cast<unsigned long long *>(p);
+            state_init_k<<<1, 1, 0, init>>>(w, w + 1);
+            ok = cudaStreamSynchronize(init) == cudaSuccess;
+            if (ok) {
+                s.flag = w;
+                s.fixq = w + 1;
+            }
+        }
+        if (init) cudaStreamDestroy(init);
+        if (!ok && p) cudaFree(p);
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        if (!ok) return nullptr;
     }
-    return queues[dev];
+    return &s;
+}
+}  // namespace
+
+unsigned long long *numeric_flag_ptr(cudaStream_t st) {
+    StreamState *s = stream_state(st);
+    return s ? s->flag : nullptr;
+}
+
+unsigned long long *fixup_queue_ptr(cudaStream_t st) {
+    StreamState *s = stream_state(st);
+    return s ? s->fixq : nullptr;
 }
 
 void keep_pool_mapped() {
@@ -78,7 +112,7 @@ void keep_pool_mapped() {
 }
 
 mdg_status consume_numeric_flag(cudaStream_t st, mdg_dims3 d) {
-    unsigned long long *f = numeric_flag_ptr();
+    unsigned long long *f = numeric_flag_ptr(st);
     if (!f) return status_from_cuda(cudaErrorMemoryAllocation, "numeric flag");
     unsigned long long key = ~0ull;
     MDG_CUDA_TRY(cudaMemcpyAsync(&key, f, sizeof(key), cudaMemcpyDeviceToHost, st));

@@ -877,6 +877,14 @@ class NativeModel:
         self.tensors = list(tensors)
         if len(self.tensors) != 75:
             raise InvalidInput("model: expects the 75 ModelParams tensors")
+        nt = C.c_int()
+        sizes = (C.c_int64 * 128)()
+        self._L.mdg_model_param_count(C.byref(nt), sizes)
+        for i, t in enumerate(self.tensors):
+            _ptr(t, f"model tensor {i}")
+            if t.numel() != sizes[i]:
+                raise InvalidInput(f"model: tensor {i} has {t.numel()} elements, the model "
+                                   f"expects {sizes[i]}")
         self.dims = tuple(int(v) for v in dims)
         lc = loss or LossConfig()
         ptrs = (C.c_void_p * 75)(*[_ptr(t) for t in self.tensors])
@@ -905,7 +913,14 @@ class NativeModel:
             out.append(_wrap_device(ptr, t.shape, t.device))
         return out
 
+    def _check_images(self, fixed, moving):
+        for name, t in (("fixed", fixed), ("moving", moving)):
+            if t.numel() != self.n:
+                raise InvalidInput(f"model: {name} image has {t.numel()} voxels, the model "
+                                   f"was created for {self.n}")
+
     def loss_step(self, fixed, moving, backward=True):
+        self._check_images(fixed, moving)
         _check(self._L.mdg_model_loss_step(self._h, _ptr(fixed, "fixed"), _ptr(moving, "moving"),
                                            1 if backward else 0, _ptr(self._terms),
                                            _ptr(self._phi), _stream()))
@@ -914,6 +929,7 @@ class NativeModel:
     def po_step(self, fixed, moving, lr=1e-4, graph=True):
         """loss + backward + Adam; graph=True replays the iteration as one
         CUDA graph (mdg_model_po_step).  Returns (terms, phi)."""
+        self._check_images(fixed, moving)
         if not graph:
             terms, phi = self.loss_step(fixed, moving, backward=True)
             _check(self._L.mdg_model_adam_step(self._h, float(lr), _stream()))
@@ -987,6 +1003,42 @@ class Rng:
         out = torch.empty(shape, dtype=torch.float32) if out is None else out
         self._L.mdg_rng_fill_normal(self._h, out.data_ptr(), out.numel(), mean, sd)
         return out
+
+
+# ---------------------------------------------------------- synthetic inputs
+def make_smooth_velocity(dims, seed, magnitude, sigma):
+    """make_smooth_velocity (synth.cpp:75-90) on the host: {3, l, w, h} float32
+    CPU tensor, bit-identical to the reference."""
+    h, w, l = dims
+    out = torch.empty(3, l, w, h, dtype=torch.float32)
+    _check(_capi.lib().mdg_synth_smooth_velocity(dims3(dims), seed, magnitude, sigma,
+                                                 out.data_ptr()))
+    return out
+
+
+def random_field(dims, seed, mag):
+    """test::random_field (tests/test_util.hpp:40-48): i.i.d. displacement
+    entries, the warp's worst case for gather locality.  {3, l, w, h} CPU."""
+    h, w, l = dims
+    out = torch.empty(3, l, w, h, dtype=torch.float32)
+    _check(_capi.lib().mdg_synth_random_field(dims3(dims), seed, mag, out.data_ptr()))
+    return out
+
+
+def synth_pair(dims, seed=1, max_disp=2.0):
+    """make_synth_pair (synth.cpp:92-192, SynthConfig defaults otherwise):
+    (fixed {1,l,w,h}, moving, labels_fixed {l,w,h} int32, labels_moving, gt
+    {3,l,w,h}) as CPU tensors.  Needs the device (the ground truth's
+    scaling-and-squaring and the warps run there, bit-exact)."""
+    h, w, l = dims
+    f = torch.empty(1, l, w, h, dtype=torch.float32)
+    m = torch.empty_like(f)
+    lf = torch.empty(l, w, h, dtype=torch.int32)
+    lm = torch.empty_like(lf)
+    gt = torch.empty(3, l, w, h, dtype=torch.float32)
+    _check(_capi.lib().mdg_synth_pair(dims3(dims), seed, max_disp, f.data_ptr(), m.data_ptr(),
+                                      lf.data_ptr(), lm.data_ptr(), gt.data_ptr()))
+    return f, m, lf, lm, gt
 
 
 # ------------------------------------------------------------- file formats

@@ -39,7 +39,14 @@ def run_pairs(n_pairs: int, register: Callable[[int], dict], group=None) -> List
     world, rank = _world(group)
     mine = []
     for i in shard(n_pairs, world, rank):
-        r = dict(register(i))
+        # a failing pair must not leave the other ranks blocked in the gather:
+        # its error travels with the results and is re-raised on every rank
+        try:
+            r = dict(register(i))
+        except Exception as e:  # noqa: BLE001
+            if world == 1:
+                raise
+            r = {"error": f"{type(e).__name__}: {e}"}
         r["pair"] = i
         mine.append(r)
     if world == 1:
@@ -47,6 +54,10 @@ def run_pairs(n_pairs: int, register: Callable[[int], dict], group=None) -> List
     parts: List[Optional[list]] = [None] * world
     dist.all_gather_object(parts, mine, group=group)
     out = sorted((r for p in parts for r in p), key=lambda r: r["pair"])
+    errs = [r for r in out if "error" in r]
+    if errs:
+        raise RuntimeError("run_pairs: " + "; ".join(f"pair {r['pair']}: {r['error']}"
+                                                       for r in errs))
     if [r["pair"] for r in out] != list(range(n_pairs)):
         raise RuntimeError("run_pairs: gathered results do not cover every pair once")
     return out

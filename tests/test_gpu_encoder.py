@@ -115,25 +115,49 @@ def test_full_loss_step_matches_reference(cuda, ref):
     print("worst per-tensor relative gradient error", worst)
 
 
-def test_pairwise_optimization_dice_gate(cuda, ref):
-    """The north star's Dice gate: pairwise optimisation of a synthetic pair
-    with labels (synth.cpp) on the GPU vs the reference pairwise_optimize —
-    loss traces to 1e-4 relative and the Dice trace within 1e-3 at every step
-    (measured: loss 7e-5, Dice 7e-4 after three Adam steps)."""
-    dims = (32, 32, 32)
-    f, m, lf, lm, gt = ref.synth_pair(dims, seed=4, max_disp=2.0)
-    packed, sizes = perturbed_model(ref, 6)
-    iters = 3
-    loss_r, dice_r, phi_r = ref.pairwise_optimize(f, m, lf, lm, packed, iters, lr=1e-4)
+_PO_CACHE = {}
+
+
+def reference_po(ref, dims, iters, seed=4, model_seed=6):
+    """The reference pairwise_optimize (engine.hpp:377-411) on synth_pair(dims,
+    seed) with perturbed_model(model_seed) weights, memoised per session (the
+    50-iteration CPU run is shared by the Python- and native-driver gates)."""
+    key = (tuple(dims), iters, seed, model_seed)
+    if key not in _PO_CACHE:
+        f, m, lf, lm, gt = ref.synth_pair(dims, seed=seed, max_disp=2.0)
+        packed, sizes = perturbed_model(ref, model_seed)
+        loss_r, dice_r, phi_r = ref.pairwise_optimize(f, m, lf, lm, packed, iters, lr=1e-4)
+        _PO_CACHE[key] = (f, m, lf, lm, packed, sizes, loss_r, dice_r, phi_r)
+    return _PO_CACHE[key]
+
+
+def check_po_traces(loss_g, dice_g, loss_r, dice_r):
+    """The north-star gate at every step: loss to 1e-4 relative, Dice within
+    1e-3 (north_star; engine.hpp:389-403 evaluates both after each update)."""
+    assert len(loss_g) == len(loss_r) and len(dice_g) == len(dice_r)
+    lerr = max(abs(a - b) / max(abs(b), 1e-12) for a, b in zip(loss_g, loss_r))
+    derr = max(abs(a - b) for a, b in zip(dice_g, dice_r))
+    print(f"max loss rel err {lerr:.3g}, max Dice err {derr:.3g} over {len(loss_r)} steps")
+    for i, (a, b) in enumerate(zip(loss_g, loss_r)):
+        assert abs(a - b) <= 1e-4 * abs(b) + 1e-6, (i, loss_g, loss_r)
+    for i, (a, b) in enumerate(zip(dice_g, dice_r)):
+        assert abs(a - b) <= 1e-3, (i, dice_g, dice_r)
+
+
+@pytest.mark.parametrize("dims", [(32, 32, 32), pytest.param((64, 64, 64),
+                                                             marks=pytest.mark.slow)])
+def test_pairwise_optimization_dice_gate(cuda, ref, dims):
+    """The north star's Dice gate at the configs' PO length: 50 Adam
+    iterations (+ the final evaluation forward) of a synthetic labelled pair
+    (synth.cpp) on the GPU (Python-composed driver, ops.Model) vs the
+    reference pairwise_optimize."""
+    iters = 50
+    f, m, lf, lm, packed, sizes, loss_r, dice_r, phi_r = reference_po(ref, dims, iters)
     model = ops.Model(device_tensors(packed, sizes), dims)
     loss_g, dice_g, phi_g = model.pairwise_optimize(
         torch.from_numpy(f).cuda(), torch.from_numpy(m).cuda(), iters, lr=1e-4,
         labels_fixed=torch.from_numpy(lf).cuda(), labels_moving=torch.from_numpy(lm).cuda())
-    print("loss", loss_g, loss_r, "dice", dice_g, dice_r)
-    for a, b in zip(loss_g, loss_r):
-        assert abs(a - b) <= 1e-4 * abs(b) + 1e-6, (loss_g, loss_r)
-    for a, b in zip(dice_g, dice_r):
-        assert abs(a - b) <= 1e-3, (dice_g, dice_r)
+    check_po_traces(loss_g, dice_g, loss_r, dice_r)
     # trajectories are not elementwise-equal after Adam steps (it normalises
     # rounding-level gradient differences of near-zero gradients; SURVEY §8c):
     # the final field agrees to 1e-2 relative norm

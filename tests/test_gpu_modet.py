@@ -191,10 +191,12 @@ def test_fused_forward_negative_inf_bias_raises(cuda, oracle):
     assert ei.value.position == bad
 
 
-def test_config1_32cubed_s8_d8(cuda, oracle):
+@pytest.mark.parametrize("layout", [MDG_QK_PLANAR, MDG_QK_POSMAJOR])
+def test_config1_32cubed_s8_d8(cuda, oracle, layout):
     """BASELINE configs[0]: 32^3, 8 heads x 8 channels; inputs in the order of
     the reference bench (bench.cpp:28-35): Rng(5) Q, K ~ U(-1,1), B ~ U(-.5,.5);
-    upstream gradient Rng(6) U(-1,1)."""
+    upstream gradient Rng(6) U(-1,1).  PLANAR runs the production tiled TMA
+    kernels (modet_tiled.cu), POSMAJOR the position-major fallback."""
     dims, S, hd = (32, 32, 32), 8, 8
     n = 32 ** 3
     r = pyoracle.Rng(5)
@@ -203,7 +205,7 @@ def test_config1_32cubed_s8_d8(cuda, oracle):
     B = f32(r.uniform(S * 27, -0.5, 0.5).reshape(S, 27))
     gSF = f32(pyoracle.Rng(6).uniform(3 * S * n, -1, 1).reshape(3 * S, 32, 32, 32))
     W0, SF0, gQ0, gK0, gB0 = oracle_modet(oracle, Q, K, B, dims, S, hd, gSF)
-    W, SF, LSE, gQ, gK, gB = run_fused(Q, K, B, dims, S, hd, gSF)
+    W, SF, LSE, gQ, gK, gB = run_fused(Q, K, B, dims, S, hd, gSF, layout)
     assert worst(W, W0) <= W_ATOL
     assert rel_close(SF, SF0.reshape(SF.shape), FLOW_ATOL, FLOW_RTOL)
     assert grad_ok(gQ, gQ0) and grad_ok(gK, gK0) and grad_ok(gB, gB0)
@@ -300,7 +302,11 @@ def test_layout_adapters_roundtrip(cuda):
     assert np.array_equal(host(ops.qk_planar_to_posmajor(p)), host(x))
 
 
-def test_host_buffer_calls_match_device_calls(cuda):
+@pytest.mark.parametrize("acc", [1, 0])
+def test_host_buffer_calls_match_device_calls(cuda, acc):
+    """Small volumes take the whole-volume host path.  acc=0 overwrites the
+    caller's gradients (gB included: its host value is never uploaded, here
+    pre-filled with garbage), acc=1 adds into them."""
     import ctypes as C
 
     from paper_2403_16526_b200 import _capi
@@ -318,8 +324,10 @@ def test_host_buffer_calls_match_device_calls(cuda):
     assert L.mdg_modet_fwd_host(p(Q), p(K), p(B), d3, S, hd, 3, 0, p(hSF), p(hL)) == 0
     assert np.array_equal(hSF, SF) and np.array_equal(hL, LSE)
     hgQ, hgK, hgB = np.zeros_like(Q), np.zeros_like(K), np.zeros_like(B)
+    if not acc:
+        hgQ[:], hgK[:], hgB[:] = 7.0, -3.0, 1e30
     assert L.mdg_modet_bwd_host(p(Q), p(K), p(B), p(hSF), p(hL), p(gSF), d3, S, hd, 3, 0,
-                                p(hgQ), p(hgK), p(hgB), 1) == 0
+                                p(hgQ), p(hgK), p(hgB), acc) == 0
     assert np.array_equal(hgQ, gQ) and np.array_equal(hgK, gK) and np.array_equal(hgB, gB)
     hW = np.zeros((S, n, 27), np.float32)
     assert L.mdg_na_fused_fwd_host(p(Q), p(K), p(B), d3, S, hd, 3, p(hW)) == 0
@@ -406,3 +414,50 @@ def test_north_star_size_parity_and_properties(cuda, oracle):
     del W0
     assert rel_close(SFh, SF0.reshape(3, n), FLOW_ATOL, FLOW_RTOL)
     assert grad_ok(host(gQ), gQ0) and grad_ok(host(gK), gK0) and grad_ok(host(gB), gB0)
+
+
+def test_two_streams_same_device_fixup_isolated(cuda, oracle):
+    """The fixup queue and numeric flag are per (device, stream): two streams
+    running forwards with overflowing logits at the same time (different
+    volume sizes, so a shared queue would also decode positions against the
+    wrong dims) must each get the exact softmax, and a non-finite logit on one
+    stream must be reported on that stream only."""
+    cases = []
+    for dims, seed in (((20, 9, 7), 3), ((12, 16, 11), 8)):
+        S, hd = 2, 6
+        n = dims[0] * dims[1] * dims[2]
+        Q, K = random_qk(dims, S * hd, seed), random_qk(dims, S * hd, seed + 1)
+        B = f32(pyoracle.Rng(seed + 2).normal(S * 27).reshape(S, 27))
+        B[0, 18:] += 95.0  # every voxel overflows the first-row max -> fixup
+        B[1, 26] += 300.0
+        W0, bad = oracle.na_fwd(Q, K, B, dims, S, hd)
+        assert bad is None
+        SF0 = oracle.subfields_fwd(W0, dims, S).reshape(3 * S, n)
+        cases.append((dims, dev(Q.T.copy()), dev(K.T.copy()), dev(B), SF0))
+    cfg = ops.AttentionConfig(2, 6, 3)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [[], []]
+    for _ in range(20):
+        for i, (dims, Qd, Kd, Bd, _) in enumerate(cases):
+            with torch.cuda.stream(streams[i]):
+                outs[i].append(ops.modet_fwd(Qd, Kd, Bd, dims, cfg, layout=MDG_QK_PLANAR,
+                                             check=False)[0])
+    for i, (dims, *_rest) in enumerate(cases):  # no stray flag on either stream
+        with torch.cuda.stream(streams[i]):
+            ops.check_numeric(dims)
+    torch.cuda.synchronize()
+    for i, (dims, _, _, _, SF0) in enumerate(cases):
+        for SF in outs[i]:
+            assert rel_close(host(SF), SF0, FLOW_ATOL, FLOW_RTOL), (i, dims)
+    # a -inf bias on stream 0 only: stream 1 stays clean
+    dims, Qd, Kd, Bd, _ = cases[0]
+    Bbad = Bd.clone()
+    Bbad[0, 3] = -float("inf")
+    with torch.cuda.stream(streams[0]):
+        with pytest.raises(ops.NumericError):
+            ops.modet_fwd(Qd, Kd, Bbad, dims, cfg, layout=MDG_QK_PLANAR)
+    with torch.cuda.stream(streams[1]):
+        d1, Q1, K1, B1, SF1 = cases[1]
+        SF, _ = ops.modet_fwd(Q1, K1, B1, d1, cfg, layout=MDG_QK_PLANAR)
+    torch.cuda.synchronize()
+    assert rel_close(host(SF), SF1, FLOW_ATOL, FLOW_RTOL)
