@@ -42,6 +42,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "mdg_common.cuh"
@@ -922,6 +923,385 @@ modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
     });
 }
 
+// ======================================================= bwd: single pass
+// modet_bwd_fused_k — the whole backward (dQ, dK, dB) from ONE evaluation of
+// each logit.  A CTA owns a 32x8 column tile and marches K planes p through
+// its z chunk; source voxels r (the attention rows, attention.hpp:127-166)
+// sit in three in-flight slots (planes p+1, p, p-1) and meet the keys of
+// plane p.  For every (source, window slot) pair the thread computes
+//   W  = exp2(l*log2e - LSE*log2e)         (l = B[o] + Q_r . K_q, q = r + off(o))
+//   dl = W * (gSF_r . off(o) - gSF_r . SF_r)   (<W, gW> = gSF . SF)
+// and uses it three times: dQ_r += dl K_q (registers, across the three steps
+// the source is in flight), dB[o] += dl, and the key's contribution
+// dl Q_r.  All keys a step touches lie in plane p, so the three slots'
+// contributions to one key sum in registers; the x-neighbour terms move by
+// warp shuffle and the y-neighbour terms through a small shared-memory
+// exchange (one block barrier per step).  Keys on the tile edge also receive
+// terms from sources outside the tile: three extra warps recompute those
+// ring sources (the 1-voxel ring of the 34x10 source region; only the 9 of
+// 27 window slots whose key falls inside the tile), so every key of the tile
+// is complete inside its CTA — no atomics, no cross-CTA pass, a fixed
+// summation order (deterministic).  Per voxel: 27 logits (+11 % ring work)
+// instead of the two-pass kernels' 54, and no per-source side planes.
+//   warps 0-7: tile rows; warp 8: source row y0-1 (keys of row y0, dy=+1);
+//   warp 9: source row y0+8 (keys of row y0+7, dy=-1); warp 10: source
+//   columns x0-1 (lanes 0-9) and x0+32 (lanes 16-25), rows y0-1 .. y0+8.
+constexpr int kFW = 11;               // warps per CTA
+constexpr int kFRows = 10;            // box rows: y0-1 .. y0+8
+// floats per staged channel: the 40 x 10 box, padded so every channel starts
+// on a 128-byte boundary (TMA destination alignment)
+constexpr int kFBox = up32(kBoxX * kFRows);
+
+template <int D>
+struct FG1 {
+    static constexpr int D2 = (D + 1) / 2;
+    static constexpr int NOWN = D + 7;                 // Q (D), LSE, gSF (3), SF (3)
+    static constexpr int BUF = (D + NOWN) * kFBox;     // K box of plane p + own box of p+1
+    static constexpr int YX = 2 * 2 * RTY * RTX * D2;  // float2: [par][dir][pair][row][x]
+    static constexpr int XX = 2 * 2 * RTY * 3 * D2;    // float2: [par][side][row][dyi][pair]
+};
+
+// one in-flight source slot
+template <int D>
+struct Src {
+    static constexpr int D2 = (D + 1) / 2;
+    float2 q[D2];   // Q_r * log2e, channel pairs
+    float2 dq[D2];  // dQ_r accumulator
+    float Lh;       // LSE * log2e / 2 (+inf: no source)
+    float gx, gy, gz, dot;
+    float mask;     // 1: counts towards dB (interior source of this chunk)
+};
+
+template <int D>
+__device__ __forceinline__ void src_load(Src<D> &s, const float *own, int pos, bool valid,
+                                         bool interior) {
+    constexpr int D2 = (D + 1) / 2;
+#pragma unroll
+    for (int c = 0; c < D2; ++c) {
+        const float a = own[(2 * c) * kFBox + pos];
+        const float b = 2 * c + 1 < D ? own[(2 * c + 1) * kFBox + pos] : 0.0f;
+        s.q[c] = mul2(f2(a, b), dup2(kLog2e));
+        s.dq[c] = f2(0.0f, 0.0f);
+    }
+    s.Lh = valid ? own[D * kFBox + pos] * (0.5f * kLog2e) : INFINITY;
+    s.gx = own[(D + 1) * kFBox + pos];
+    s.gy = own[(D + 2) * kFBox + pos];
+    s.gz = own[(D + 3) * kFBox + pos];
+    s.dot = s.gx * own[(D + 4) * kFBox + pos] + s.gy * own[(D + 5) * kFBox + pos] +
+            s.gz * own[(D + 6) * kFBox + pos];
+    s.mask = interior ? 1.0f : 0.0f;
+}
+
+// dl of source slot s against key k (channel pairs).  The logit in log2
+// units minus LSE*log2e is (h + sum_even) + (h + sum_odd) with
+// h = (B*log2e - LSE*log2e) / 2 broadcast into both lanes of the packed
+// accumulator (no pair set-up per logit); bh = B*log2e / 2.
+template <int D>
+__device__ __forceinline__ float dl_of(const Src<D> &s, const float2 *k, float bh, float cf) {
+    constexpr int D2 = (D + 1) / 2;
+    float2 acc = fma2(s.q[0], k[0], dup2(bh - s.Lh));
+#pragma unroll
+    for (int c = 1; c < D2; ++c) acc = fma2(s.q[c], k[c], acc);
+    return ex2(acc.x + acc.y) * cf;
+}
+
+// tile row: the three slots against key row dy = DYI-1 of plane p.  Returns
+// (in c3) each dx's summed key contribution (in log2e-scaled units); DQ:
+// dQ and dB (interior rows only).
+template <int D, int DYI, bool DQ>
+__device__ __forceinline__ void fused_row(Src<D> (&S)[3], const float *kb, int kpos,
+                                          const float *sB, float (&db)[27],
+                                          float2 (&c3)[3][(D + 1) / 2]) {
+    constexpr int D2 = (D + 1) / 2;
+    float2 kr[3][D2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int c = 0; c < D2; ++c)
+            kr[i][c] = f2(kb[(2 * c) * kFBox + kpos + i],
+                          2 * c + 1 < D ? kb[(2 * c + 1) * kFBox + kpos + i] : 0.0f);
+    // slot 0: NEW (source plane p+1, dz = -1), 1: MID (p, 0), 2: OLD (p-1, +1)
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) {
+        Src<D> &s = S[jj];
+        const int dz = jj - 1;
+        float cb = -s.dot;
+        if (dz > 0) cb += s.gz;
+        if (dz < 0) cb -= s.gz;
+        if (DYI == 0) cb -= s.gy;
+        if (DYI == 2) cb += s.gy;
+        const int ob = (dz + 1) * 9 + DYI * 3;
+        const float cf[3] = {cb - s.gx, cb, cb + s.gx};
+#pragma unroll
+        for (int dxi = 0; dxi < 3; ++dxi) {
+            const float dl = dl_of<D>(s, kr[dxi], sB[ob + dxi], cf[dxi]);
+            const float2 dl2 = dup2(dl);
+            if (DQ) {
+                db[ob + dxi] = fmaf(dl, s.mask, db[ob + dxi]);
+#pragma unroll
+                for (int c = 0; c < D2; ++c) s.dq[c] = fma2(dl2, kr[dxi][c], s.dq[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < D2; ++c)
+                c3[dxi][c] = jj == 0 ? mul2(dl2, s.q[c]) : fma2(dl2, s.q[c], c3[dxi][c]);
+        }
+    }
+}
+
+// keys of one row: lane x collects dx = 0 from itself, dx = +1 from lane x-1
+// and dx = -1 from lane x+1 (in that order)
+template <int D>
+__device__ __forceinline__ void xcombine(float2 (&c3)[3][(D + 1) / 2], float2 *R) {
+    constexpr int D2 = (D + 1) / 2;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int c = 0; c < D2; ++c) {
+        float2 up, dn;
+        up.x = __shfl_up_sync(0xffffffffu, c3[2][c].x, 1);
+        up.y = __shfl_up_sync(0xffffffffu, c3[2][c].y, 1);
+        dn.x = __shfl_down_sync(0xffffffffu, c3[0][c].x, 1);
+        dn.y = __shfl_down_sync(0xffffffffu, c3[0][c].y, 1);
+        if (lane == 0) up = f2(0.0f, 0.0f);
+        if (lane == 31) dn = f2(0.0f, 0.0f);
+        R[c] = add2(add2(c3[1][c], up), dn);
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void fused_stage(float *buf, const Maps &m, uint64_t *bar, int p,
+                                            int x0, int y0, int s) {
+    float *own = buf + D * kFBox;
+    mbar_expect_tx(bar, (2 * D + 7) * kBoxX * kFRows * 4);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+        tma4(buf + c * kFBox, &m.k, x0 - 4, y0 - 1, p, s * D + c, bar);
+        tma4(own + c * kFBox, &m.a.q, x0 - 4, y0 - 1, p + 1, s * D + c, bar);
+    }
+    tma4(own + D * kFBox, &m.a.lse, x0 - 4, y0 - 1, p + 1, s, bar);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        tma4(own + (D + 1 + c) * kFBox, &m.a.g, x0 - 4, y0 - 1, p + 1, 3 * s + c, bar);
+        tma4(own + (D + 4 + c) * kFBox, &m.a.sf, x0 - 4, y0 - 1, p + 1, 3 * s + c, bar);
+    }
+}
+
+template <int D, bool ACC>
+__global__ void __launch_bounds__(kFW * 32, 1)
+modet_bwd_fused_k(const __grid_constant__ Maps maps, const float *__restrict__ B, Vol v, int zc,
+                  float *__restrict__ gQ, float *__restrict__ gK, float *__restrict__ gBpart) {
+    using G = FG1<D>;
+    constexpr int D2 = G::D2;
+    extern __shared__ __align__(128) float smem[];
+    float2 *ybuf = reinterpret_cast<float2 *>(smem + 2 * G::BUF);
+    float2 *xbuf = ybuf + G::YX;
+    float *sB = reinterpret_cast<float *>(xbuf + G::XX);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sB + 32);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int x0 = blockIdx.x * RTX, y0 = blockIdx.y * RTY;
+    const int nzc = (v.l + zc - 1) / zc;
+    const int s = blockIdx.z / nzc;
+    const int zb = (blockIdx.z - s * nzc) * zc, ze = min(zb + zc, v.l);
+    const int64_t so = (int64_t)s * v.n;
+    if (threadIdx.x < 27) sB[threadIdx.x] = B[s * 27 + threadIdx.x] * (0.5f * kLog2e);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fused_stage<D>(smem, maps, &bar[0], zb - 2, x0, y0, s);
+        fused_stage<D>(smem + G::BUF, maps, &bar[1], zb - 1, x0, y0, s);
+    }
+    // this thread's source position (box row br in 0..9, box column bc)
+    int br, bc;
+    bool xside_right = false, active = true;
+    if (wid < 8) {
+        br = wid + 1;
+        bc = lane + 4;
+    } else if (wid < 10) {
+        br = wid == 8 ? 0 : 9;
+        bc = lane + 4;
+    } else {
+        xside_right = lane >= 16;
+        br = lane & 15;
+        bc = xside_right ? 36 : 3;
+        active = br < kFRows;
+        if (!active) br = 0;
+    }
+    const int sx = x0 - 4 + bc, sy = y0 - 1 + br;
+    const bool in_xy = active && sx >= 0 && sx < v.h && sy >= 0 && sy < v.w;
+    const int pos = br * kBoxX + bc;
+    Src<D> S[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+#pragma unroll
+        for (int c = 0; c < D2; ++c) S[j].q[c] = S[j].dq[c] = f2(0.0f, 0.0f);
+        S[j].Lh = INFINITY;
+        S[j].gx = S[j].gy = S[j].gz = S[j].dot = S[j].mask = 0.0f;
+    }
+    float db[27];
+#pragma unroll
+    for (int o = 0; o < 27; ++o) db[o] = 0.0f;
+    float *gQh = gQ ? gQ + so * D : nullptr;
+    float *gKh = gK ? gK + so * D : nullptr;
+    // slots: S[0] = source plane p+1 (NEW), S[1] = p (MID), S[2] = p-1 (OLD);
+    // rotated by register moves at the end of each step (one copy of the
+    // step body: the unrolled three-step rotation overflowed the i-cache)
+    for (int p = zb - 2; p <= ze; ++p) {
+        constexpr int NEW = 0, OLD = 2;
+        const int j = p - (zb - 2), b = j & 1, par = j & 1;
+        mbar_wait(&bar[b], (j >> 1) & 1);
+        const float *buf = smem + b * G::BUF;
+        {   // the source entering the window: plane p+1 (the chunk's ring planes
+            // zb-1 and ze feed keys only; beyond them the slot idles)
+            const int z = p + 1;
+            const bool valid = in_xy && z >= 0 && z >= zb - 1 && z <= ze && z < v.l;
+            src_load<D>(S[NEW], buf + D * kFBox, pos, valid,
+                        valid && wid < 8 && z >= zb && z < ze);
+        }
+        float2 own[D2];
+        if (p >= zb - 1) {
+            float2 c3[3][D2];
+            if (wid < 8) {
+                float2 R[D2];
+                // key rows dy = -1, 0, +1 (box rows wid, wid+1, wid+2)
+                fused_row<D, 0, true>(S, buf, wid * kBoxX + lane + 3, sB, db, c3);
+                xcombine<D>(c3, R);
+                if (wid >= 1)
+#pragma unroll
+                    for (int c = 0; c < D2; ++c)
+                        ybuf[(((par * 2 + 1) * D2 + c) * RTY + wid - 1) * RTX + lane] = R[c];
+                fused_row<D, 1, true>(S, buf, (wid + 1) * kBoxX + lane + 3, sB, db, c3);
+                xcombine<D>(c3, own);
+                fused_row<D, 2, true>(S, buf, (wid + 2) * kBoxX + lane + 3, sB, db, c3);
+                xcombine<D>(c3, R);
+                if (wid <= 6)
+#pragma unroll
+                    for (int c = 0; c < D2; ++c)
+                        ybuf[(((par * 2 + 0) * D2 + c) * RTY + wid + 1) * RTX + lane] = R[c];
+            } else if (wid == 8) {  // source row y0-1 -> keys of row y0 (dy = +1)
+                float2 R[D2];
+                fused_row<D, 2, false>(S, buf, 1 * kBoxX + lane + 3, sB, db, c3);
+                xcombine<D>(c3, R);
+#pragma unroll
+                for (int c = 0; c < D2; ++c)
+                    ybuf[(((par * 2 + 0) * D2 + c) * RTY + 0) * RTX + lane] = R[c];
+            } else if (wid == 9) {  // source row y0+8 -> keys of row y0+7 (dy = -1)
+                float2 R[D2];
+                fused_row<D, 0, false>(S, buf, 8 * kBoxX + lane + 3, sB, db, c3);
+                xcombine<D>(c3, R);
+#pragma unroll
+                for (int c = 0; c < D2; ++c)
+                    ybuf[(((par * 2 + 1) * D2 + c) * RTY + RTY - 1) * RTX + lane] = R[c];
+            } else {  // x ring: dx = +1 (left column) / -1 (right), dy = -1, 0, +1
+                const int dxi = xside_right ? 0 : 2;
+                const int kc = xside_right ? 35 : 4;
+#pragma unroll
+                for (int dyi = 0; dyi < 3; ++dyi) {
+                    const int kr_ = br + dyi - 1;  // key box row
+                    float2 k[D2], acc[D2];
+                    const int kp = (kr_ < 0 ? 0 : (kr_ > 9 ? 9 : kr_)) * kBoxX + kc;
+#pragma unroll
+                    for (int c = 0; c < D2; ++c) {
+                        k[c] = f2(buf[(2 * c) * kFBox + kp],
+                                  2 * c + 1 < D ? buf[(2 * c + 1) * kFBox + kp] : 0.0f);
+                        acc[c] = f2(0.0f, 0.0f);
+                    }
+#pragma unroll
+                    for (int jj = 0; jj < 3; ++jj) {
+                        const Src<D> &sr = S[jj];
+                        const int dz = jj - 1;
+                        const float cf = -sr.dot + (dyi == 0 ? -sr.gy : (dyi == 2 ? sr.gy : 0.0f)) +
+                                   (dz > 0 ? sr.gz : (dz < 0 ? -sr.gz : 0.0f)) +
+                                   (xside_right ? -sr.gx : sr.gx);
+                        const float dl =
+                            dl_of<D>(sr, k, sB[(dz + 1) * 9 + dyi * 3 + dxi], cf);
+                        const float2 dl2 = dup2(dl);
+#pragma unroll
+                        for (int c = 0; c < D2; ++c) acc[c] = fma2(dl2, sr.q[c], acc[c]);
+                    }
+                    // key row (tile-relative) = box row - 1
+                    if (active && kr_ >= 1 && kr_ <= RTY)
+#pragma unroll
+                        for (int c = 0; c < D2; ++c)
+                            xbuf[(((par * 2 + (xside_right ? 1 : 0)) * RTY + kr_ - 1) * 3 + dyi) *
+                                     D2 + c] = acc[c];
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && p + 2 <= ze) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            fused_stage<D>(smem + b * G::BUF, maps, &bar[b], p + 2, x0, y0, s);
+        }
+        if (wid < 8) {
+            const int x = x0 + lane, y = y0 + wid;
+            const bool vv = x < v.h && y < v.w;
+            // keys of plane p: ((from row above + own row) + from row below) + x ring
+            if (p >= zb && p < ze && vv && gKh) {
+                const int64_t off = (int64_t)p * v.hw + (int64_t)y * v.h + x;
+#pragma unroll
+                for (int c = 0; c < D2; ++c) {
+                    float2 t = add2(ybuf[(((par * 2 + 0) * D2 + c) * RTY + wid) * RTX + lane],
+                                    own[c]);
+                    t = add2(t, ybuf[(((par * 2 + 1) * D2 + c) * RTY + wid) * RTX + lane]);
+                    if (lane == 0 || lane == 31) {
+                        const int sd = lane == 31 ? 1 : 0;
+#pragma unroll
+                        for (int dyi = 0; dyi < 3; ++dyi)
+                            t = add2(t, xbuf[(((par * 2 + sd) * RTY + wid) * 3 + dyi) * D2 + c]);
+                    }
+                    t = mul2(t, dup2(kLn2));  // contributions carry Q * log2e
+                    float *d0 = gKh + (int64_t)(2 * c) * v.n + off;
+                    *d0 = ACC ? *d0 + t.x : t.x;
+                    if (2 * c + 1 < D) {
+                        float *d1 = d0 + v.n;
+                        *d1 = ACC ? *d1 + t.y : t.y;
+                    }
+                }
+            }
+            // the source leaving the window (plane p-1) has all 27 terms of dQ
+            if (p - 1 >= zb && p - 1 < ze && vv && gQh) {
+                const int64_t off = (int64_t)(p - 1) * v.hw + (int64_t)y * v.h + x;
+#pragma unroll
+                for (int c = 0; c < D2; ++c) {
+                    float *d0 = gQh + (int64_t)(2 * c) * v.n + off;
+                    *d0 = ACC ? *d0 + S[OLD].dq[c].x : S[OLD].dq[c].x;
+                    if (2 * c + 1 < D) {
+                        float *d1 = d0 + v.n;
+                        *d1 = ACC ? *d1 + S[OLD].dq[c].y : S[OLD].dq[c].y;
+                    }
+                }
+            }
+        }
+        S[2] = S[1];
+        S[1] = S[0];
+    }
+    // dB: per-CTA partial over the 8 tile warps (fixed order)
+    __syncthreads();
+    float *red = smem;
+    if (wid < 8) {
+#pragma unroll
+        for (int o = 0; o < 27; ++o) {
+            float a = db[o];
+#pragma unroll
+            for (int m = 16; m > 0; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
+            if (lane == 0) red[wid * 27 + o] = a;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 27) {
+        float a = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a += red[i * 27 + threadIdx.x];
+        const int cta = (blockIdx.z - s * nzc) * gridDim.x * gridDim.y + blockIdx.y * gridDim.x +
+                        blockIdx.x;
+        const int ncta = nzc * gridDim.x * gridDim.y;
+        gBpart[((int64_t)s * ncta + cta) * 27 + threadIdx.x] = a;
+    }
+}
+
 // deterministic final reduction of per-CTA dB partials (fixed order tree)
 __global__ void __launch_bounds__(256)
 reduce_db_k(const float *__restrict__ part, int nparts, float *__restrict__ gB) {
@@ -1045,6 +1425,51 @@ static void col_launch(dim3 g, size_t sm, cudaStream_t st, const Maps &m, const 
     modet_bwd_col_k<D, TMA, ACC><<<g, 256, sm, st>>>(m, Q, K, B, SF, LSE, gSF, v, zc, gK, aux);
 }
 
+template <int D, bool ACC>
+static void fused_launch(dim3 g, size_t sm, cudaStream_t st, const Maps &m, const float *B,
+                         const Vol &v, int zc, float *gQ, float *gK, float *part) {
+    set_smem(modet_bwd_fused_k<D, ACC>, sm);
+    modet_bwd_fused_k<D, ACC><<<g, kFW * 32, sm, st>>>(m, B, v, zc, gQ, gK, part);
+}
+
+// the single-pass kernel (TMA staging, head_dim <= 6: its register budget)
+template <int D>
+static bool bwd_fused(const float *Q, const float *K, const float *B, const float *SF,
+                      const float *LSE, const float *gSF, const Vol &v, int S, bool acc,
+                      float *gQ, float *gK, float *gB, cudaStream_t st, cudaError_t *err) {
+    if constexpr (D > 6) {
+        return false;
+    } else {
+        // opt-in: measured slower than the two-pass kernels at 160x192x224
+        // (0.48-0.51 vs 0.456 ms), kept for the next iteration
+        if (!std::getenv("MDG_MODET_BWD_FUSED")) return false;
+        Maps m{};
+        if (!(make_map(&m.k, K, v, S * D, kBoxX, kFRows) &&
+              make_maps_a(&m.a, Q, LSE, gSF, SF, v, S, D, kBoxX, kFRows)))
+            return false;
+        const int gx = (v.h + RTX - 1) / RTX, gy = (v.w + RTY - 1) / RTY;
+        const int zc = pick_zc(gx * gy * S, v.l, 1, 4);
+        const int nzc = (v.l + zc - 1) / zc;
+        const int ncta = gx * gy * nzc;
+        using G = FG1<D>;
+        const size_t sm = (2 * G::BUF + 2 * (G::YX + G::XX) + 32 + 8) * sizeof(float);
+        float *part = nullptr;
+        keep_pool_mapped();
+        if ((*err = cudaMallocAsync(&part, (size_t)S * ncta * 27 * sizeof(float), st))) return true;
+        const dim3 g(gx, gy, S * nzc);
+        if (acc) fused_launch<D, true>(g, sm, st, m, B, v, zc, gQ, gK, part);
+        else fused_launch<D, false>(g, sm, st, m, B, v, zc, gQ, gK, part);
+        g_launches.fetch_add(1);
+        if (gB) {
+            reduce_db_k<<<dim3(27, S), 256, 0, st>>>(part, ncta, gB);
+            g_launches.fetch_add(1);
+        }
+        cudaFreeAsync(part, st);
+        *err = cudaPeekAtLastError();
+        return true;
+    }
+}
+
 template <int D>
 static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, const float *SF,
                               const float *LSE, const float *gSF, mdg_dims3 d, int S, bool acc,
@@ -1052,6 +1477,7 @@ static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, co
     const Vol v{d.h, d.w, d.l, (int64_t)d.h * d.w * d.l, (int64_t)d.h * d.w};
     const bool tma = tma_ok(v, {Q, K, SF, LSE, gSF});
     cudaError_t e = cudaSuccess;
+    if (tma && bwd_fused<D>(Q, K, B, SF, LSE, gSF, v, S, acc, gQ, gK, gB, st, &e)) return e;
     // the row kernel always runs when dK is wanted: it writes the per-source
     // statistics {LSE*log2e, gSF.SF} the column kernel gathers
     float *aux = nullptr;
