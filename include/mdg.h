@@ -378,6 +378,22 @@ mdg_status mdg_qk_planar_to_posmajor(const float *src, int64_t n, int C, float *
  * out; device staging and the copies happen inside the call. */
 mdg_status mdg_na_fused_fwd_host(const float *Q, const float *K, const float *B, mdg_dims3 d,
                                  int S, int hd, int nb, float *W);
+/* the other reference kern:: functions on host buffers (same semantics as the
+ * device calls above: outputs overwritten, gradients accumulated) — what
+ * integration/mdreg_b200.hpp binds kern::*<float> to */
+mdg_status mdg_na_fused_bwd_host(const float *Q, const float *K, const float *W, mdg_dims3 d,
+                                 int S, int hd, int nb, const float *gW, float *gQ, float *gK,
+                                 float *gB);
+mdg_status mdg_subfields_fwd_host(const float *W, mdg_dims3 d, int S, int nb, float *out);
+mdg_status mdg_subfields_bwd_host(mdg_dims3 d, int S, int nb, const float *gout, float *gW);
+mdg_status mdg_upsample2_fwd_host(const float *in, int C, mdg_dims3 d, mdg_dims3 td,
+                                  float scale, float *out);
+mdg_status mdg_upsample2_bwd_host(int C, mdg_dims3 d, mdg_dims3 td, float scale,
+                                  const float *gout, float *gin);
+mdg_status mdg_conv3_fwd_host(const float *in, int ic, mdg_dims3 d, const float *k,
+                              const float *bias, int oc, float *out);
+mdg_status mdg_conv3_bwd_host(const float *in, int ic, mdg_dims3 d, const float *k, int oc,
+                              const float *gout, float *gin, float *gk, float *gbias);
 mdg_status mdg_modet_fwd_host(const float *Q, const float *K, const float *B, mdg_dims3 d,
                               int S, int hd, int nb, int layout, float *SF, float *LSE);
 /* accumulate: as mdg_modet_bwd (1: gQ/gK/gB +=, the reference's rule;

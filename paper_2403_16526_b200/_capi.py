@@ -153,6 +153,13 @@ SIGNATURES = {
     "mdg_qk_posmajor_to_planar": (_st, [_p, C.c_int64, _i, _p, _p]),
     "mdg_qk_planar_to_posmajor": (_st, [_p, C.c_int64, _i, _p, _p]),
     "mdg_na_fused_fwd_host": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _p]),
+    "mdg_na_fused_bwd_host": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _p, _p, _p, _p]),
+    "mdg_subfields_fwd_host": (_st, [_p, Dims3, _i, _i, _p]),
+    "mdg_subfields_bwd_host": (_st, [Dims3, _i, _i, _p, _p]),
+    "mdg_upsample2_fwd_host": (_st, [_p, _i, Dims3, Dims3, _f, _p]),
+    "mdg_upsample2_bwd_host": (_st, [_i, Dims3, Dims3, _f, _p, _p]),
+    "mdg_conv3_fwd_host": (_st, [_p, _i, Dims3, _p, _p, _i, _p]),
+    "mdg_conv3_bwd_host": (_st, [_p, _i, Dims3, _p, _i, _p, _p, _p, _p]),
     "mdg_modet_fwd_host": (_st, [_p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p]),
     "mdg_modet_bwd_host": (_st, [_p, _p, _p, _p, _p, _p, Dims3, _i, _i, _i, _i, _p, _p, _p, _i]),
     "mdg_warp_fwd_host": (_st, [_p, _i, Dims3, _p, _p]),

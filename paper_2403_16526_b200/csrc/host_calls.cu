@@ -841,6 +841,142 @@ mdg_status mdg_na_fused_fwd_host(const float *Q, const float *K, const float *B,
     return MDG_OK;
 }
 
+// The remaining reference kern:: entry points as host-buffer calls (the
+// drop-in binding of integration/mdreg_b200.hpp): inputs up, accumulate
+// targets up (the reference's +=), outputs down, synchronous.
+mdg_status mdg_na_fused_bwd_host(const float *Q, const float *K, const float *W, mdg_dims3 d,
+                                 int S, int hd, int nb, const float *gW, float *gQ, float *gK,
+                                 float *gB) {
+    MDG_REQUIRE(dims_ok(d) && S >= 1 && hd >= 1, "na_fused_bwd: invalid sizes");
+    const size_t n = (size_t)nvox(d), win = (size_t)nb * nb * nb;
+    if (n == 0) return MDG_OK;
+    cudaStream_t st = host_stream();
+    Stage sg(st);
+    float *dQ, *dK, *dW, *dgW, *dgQ, *dgK, *dgB;
+    MDG_STAGE_TRY(sg.get(&dQ, Q, n * S * hd, true));
+    MDG_STAGE_TRY(sg.get(&dK, K, n * S * hd, true));
+    MDG_STAGE_TRY(sg.get(&dW, W, (size_t)S * n * win, true));
+    MDG_STAGE_TRY(sg.get(&dgW, gW, (size_t)S * n * win, true));
+    MDG_STAGE_TRY(sg.get(&dgQ, gQ, n * S * hd, true));
+    MDG_STAGE_TRY(sg.get(&dgK, gK, n * S * hd, true));
+    MDG_STAGE_TRY(sg.get(&dgB, gB, (size_t)S * win, true));
+    mdg_status r = mdg_na_fused_bwd(dQ, dK, dW, d, S, hd, nb, dgW, dgQ, dgK, dgB, st);
+    if (r != MDG_OK) return r;
+    MDG_STAGE_TRY(sg.down(gQ, dgQ, n * S * hd));
+    MDG_STAGE_TRY(sg.down(gK, dgK, n * S * hd));
+    MDG_STAGE_TRY(sg.down(gB, dgB, (size_t)S * win));
+    MDG_STAGE_TRY(cudaStreamSynchronize(st));
+    return MDG_OK;
+}
+
+mdg_status mdg_subfields_fwd_host(const float *W, mdg_dims3 d, int S, int nb, float *out) {
+    MDG_REQUIRE(dims_ok(d) && S >= 1, "subfields: invalid sizes");
+    const size_t n = (size_t)nvox(d), win = (size_t)nb * nb * nb;
+    if (n == 0) return MDG_OK;
+    cudaStream_t st = host_stream();
+    Stage sg(st);
+    float *dW, *dout;
+    MDG_STAGE_TRY(sg.get(&dW, W, (size_t)S * n * win, true));
+    MDG_STAGE_TRY(sg.get(&dout, out, 3 * (size_t)S * n, false));
+    mdg_status r = mdg_subfields_fwd(dW, d, S, nb, dout, st);
+    if (r != MDG_OK) return r;
+    MDG_STAGE_TRY(sg.down(out, dout, 3 * (size_t)S * n));
+    MDG_STAGE_TRY(cudaStreamSynchronize(st));
+    return MDG_OK;
+}
+
+mdg_status mdg_subfields_bwd_host(mdg_dims3 d, int S, int nb, const float *gout, float *gW) {
+    MDG_REQUIRE(dims_ok(d) && S >= 1, "subfields: invalid sizes");
+    const size_t n = (size_t)nvox(d), win = (size_t)nb * nb * nb;
+    if (n == 0) return MDG_OK;
+    cudaStream_t st = host_stream();
+    Stage sg(st);
+    float *dg, *dgW;
+    MDG_STAGE_TRY(sg.get(&dg, gout, 3 * (size_t)S * n, true));
+    MDG_STAGE_TRY(sg.get(&dgW, gW, (size_t)S * n * win, true));
+    mdg_status r = mdg_subfields_bwd(d, S, nb, dg, dgW, st);
+    if (r != MDG_OK) return r;
+    MDG_STAGE_TRY(sg.down(gW, dgW, (size_t)S * n * win));
+    MDG_STAGE_TRY(cudaStreamSynchronize(st));
+    return MDG_OK;
+}
+
+mdg_status mdg_upsample2_fwd_host(const float *in, int C, mdg_dims3 d, mdg_dims3 td,
+                                  float scale, float *out) {
+    MDG_REQUIRE(dims_ok(d) && dims_ok(td) && C >= 0, "upsample: invalid sizes");
+    const size_t ni = (size_t)nvox(d), no = (size_t)nvox(td);
+    if (no == 0 || C == 0) return mdg_upsample2_fwd(nullptr, C, d, td, scale, nullptr, nullptr);
+    cudaStream_t st = host_stream();
+    Stage sg(st);
+    float *di, *dout;
+    MDG_STAGE_TRY(sg.get(&di, in, ni * C, true));
+    MDG_STAGE_TRY(sg.get(&dout, out, no * C, false));
+    mdg_status r = mdg_upsample2_fwd(di, C, d, td, scale, dout, st);
+    if (r != MDG_OK) return r;
+    MDG_STAGE_TRY(sg.down(out, dout, no * C));
+    MDG_STAGE_TRY(cudaStreamSynchronize(st));
+    return MDG_OK;
+}
+
+mdg_status mdg_upsample2_bwd_host(int C, mdg_dims3 d, mdg_dims3 td, float scale,
+                                  const float *gout, float *gin) {
+    MDG_REQUIRE(dims_ok(d) && dims_ok(td) && C >= 0, "upsample: invalid sizes");
+    const size_t ni = (size_t)nvox(d), no = (size_t)nvox(td);
+    if (ni == 0 || C == 0 || !gin) return mdg_upsample2_bwd(C, d, td, scale, nullptr, nullptr, nullptr);
+    cudaStream_t st = host_stream();
+    Stage sg(st);
+    float *dg, *dgi;
+    MDG_STAGE_TRY(sg.get(&dg, gout, no * C, true));
+    MDG_STAGE_TRY(sg.get(&dgi, gin, ni * C, true));
+    mdg_status r = mdg_upsample2_bwd(C, d, td, scale, dg, dgi, st);
+    if (r != MDG_OK) return r;
+    MDG_STAGE_TRY(sg.down(gin, dgi, ni * C));
+    MDG_STAGE_TRY(cudaStreamSynchronize(st));
+    return MDG_OK;
+}
+
+mdg_status mdg_conv3_fwd_host(const float *in, int ic, mdg_dims3 d, const float *k,
+                              const float *bias, int oc, float *out) {
+    MDG_REQUIRE(dims_ok(d) && ic >= 1 && oc >= 1, "conv3: invalid sizes");
+    const size_t n = (size_t)nvox(d);
+    if (n == 0) return MDG_OK;
+    cudaStream_t st = host_stream();
+    Stage sg(st);
+    float *di, *dk, *db, *dout;
+    MDG_STAGE_TRY(sg.get(&di, in, n * ic, true));
+    MDG_STAGE_TRY(sg.get(&dk, k, (size_t)oc * ic * 27, true));
+    MDG_STAGE_TRY(sg.get(&db, bias, (size_t)oc, true));
+    MDG_STAGE_TRY(sg.get(&dout, out, n * oc, false));
+    mdg_status r = mdg_conv3_fwd(di, ic, d, dk, db, oc, dout, st);
+    if (r != MDG_OK) return r;
+    MDG_STAGE_TRY(sg.down(out, dout, n * oc));
+    MDG_STAGE_TRY(cudaStreamSynchronize(st));
+    return MDG_OK;
+}
+
+mdg_status mdg_conv3_bwd_host(const float *in, int ic, mdg_dims3 d, const float *k, int oc,
+                              const float *gout, float *gin, float *gk, float *gbias) {
+    MDG_REQUIRE(dims_ok(d) && ic >= 1 && oc >= 1, "conv3: invalid sizes");
+    const size_t n = (size_t)nvox(d);
+    if (n == 0 || (!gin && !gk && !gbias)) return MDG_OK;
+    cudaStream_t st = host_stream();
+    Stage sg(st);
+    float *di, *dk, *dg, *dgi, *dgk, *dgb;
+    MDG_STAGE_TRY(sg.get(&di, in, n * ic, true));
+    MDG_STAGE_TRY(sg.get(&dk, k, (size_t)oc * ic * 27, true));
+    MDG_STAGE_TRY(sg.get(&dg, gout, n * oc, true));
+    MDG_STAGE_TRY(sg.get(&dgi, gin, n * ic, true));
+    MDG_STAGE_TRY(sg.get(&dgk, gk, (size_t)oc * ic * 27, true));
+    MDG_STAGE_TRY(sg.get(&dgb, gbias, (size_t)oc, true));
+    mdg_status r = mdg_conv3_bwd(di, ic, d, dk, oc, dg, dgi, dgk, dgb, st);
+    if (r != MDG_OK) return r;
+    MDG_STAGE_TRY(sg.down(gin, dgi, n * ic));
+    MDG_STAGE_TRY(sg.down(gk, dgk, (size_t)oc * ic * 27));
+    MDG_STAGE_TRY(sg.down(gbias, dgb, (size_t)oc));
+    MDG_STAGE_TRY(cudaStreamSynchronize(st));
+    return MDG_OK;
+}
+
 static mdg_status modet_fwd_host_whole(const float *Q, const float *K, const float *B,
                                        mdg_dims3 d, int S, int hd, int nb, int layout, float *SF,
                                        float *LSE) {

@@ -202,4 +202,11 @@ mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
                           const float *gout, float *gin, float *gfield, int64_t pb, int64_t pe,
                           cudaStream_t st);
 
+// warp_gather.cu: the warp's input gradient as a deterministic gather (after
+// warp_bwd_k has put max |phi| into rbits[0]; rbits[1..] is its scratch)
+int64_t gin_gather_scratch_words(mdg_dims3 d);
+mdg_status warp_gin_gather(const float *field, const float *gout, int C, mdg_dims3 d, float *gin,
+                           int64_t pb, int64_t pe, const unsigned *rbits, unsigned *dirty,
+                           cudaStream_t st);
+
 }  // namespace mdg

@@ -13,11 +13,14 @@
 // bit-identical, only the summation order at a shared corner varies.  The
 // upsample backward is a pure gather over the <=5 candidate fine voxels per
 // axis (no atomics).
+#include <cstdlib>
+
 #include "mdg_common.cuh"
 
 namespace mdg {
 
 constexpr int kSB = 256;
+constexpr int kGatherReach = 6;  // warp_gather.cu gather::kRMax
 
 struct Corners {
     Ax ax, ay, az;
@@ -248,21 +251,38 @@ __device__ __forceinline__ void scatter_row2(float *ia, float *ib, bool two, boo
 
 // --------------------------------------------------------------- warp bwd
 // sampling.hpp:139-167 (gfield: same per-channel order => bit-exact)
+// rbits (nullable): atomicMax of max |phi| over the voxels (float bits), the
+// displacement bound the deterministic gin gather needs (warp_gather.cu).
+// far_only: this launch is the gather's fallback scatter and runs only when
+// that bound exceeds the gather's reach (else every thread returns at once).
 template <int CT, bool COMPOSE = false>
 __global__ void __launch_bounds__(kSB, CT == 16 ? 4 : 5)
 warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, const float *__restrict__ gout,
-           float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe) {
+           float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe,
+           unsigned *__restrict__ rbits = nullptr, bool far_only = false) {
+    if (far_only && __uint_as_float(*rbits) <= (float)kGatherReach) return;
     const int64_t n = (int64_t)h * w * l;
     const int64_t p0 = pb + (int64_t)blockIdx.x * kSB + threadIdx.x;  // voxels [pb, pe)
     // CT > 0 keeps every lane alive for the warp-level scatter merge
     const bool ok = p0 < pe;
-    if (CT == 0 && !ok) return;
+    if (CT == 0 && !ok && !rbits) return;
     const int64_t p = ok ? p0 : 0;
     int x, y, z;
     xyz_of(p, h, w, x, y, z);
-    const Corners c = corners_at(add_((float)x, __ldg(field + p)), add_((float)y, __ldg(field + n + p)),
-                                 add_((float)z, __ldg(field + 2 * n + p)), h, w, l);
+    const float phx = __ldg(field + p), phy = __ldg(field + n + p), phz = __ldg(field + 2 * n + p);
+    if (rbits && !far_only) {
+        float m = ok ? fmaxf(fabsf(phx), fmaxf(fabsf(phy), fabsf(phz))) : 0.0f;
+        if (!(m == m)) m = __uint_as_float(0x7fc00000u);  // NaN: as large as it gets
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            m = __uint_as_float(max(__float_as_uint(m),
+                                    __shfl_xor_sync(0xffffffffu, __float_as_uint(m), o)));
+        if ((threadIdx.x & 31) == 0) atomicMax(rbits, __float_as_uint(m));
+    }
+    if (CT == 0 && (!ok || (!gin && !gfield))) return;
+    const Corners c = corners_at(add_((float)x, phx), add_((float)y, phy), add_((float)z, phz), h,
+                                 w, l);
     float gx = 0.0f, gy = 0.0f, gz = 0.0f;
     if (CT > 0) {
         // channel pairs; corner rows as 32-bit element offsets (x1 = x0 + 1;
@@ -549,12 +569,36 @@ mdg_status warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
     return MDG_OK;
 }
 
+// gin by the deterministic gather (warp_gather.cu) unless MDG_WARP_ATOMIC is
+// set (the previous float-atomic scatter, kept for A/B measurement)
+static bool warp_atomic_mode() {
+    static const bool v = std::getenv("MDG_WARP_ATOMIC") != nullptr;
+    return v;
+}
+
 mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *field,
                           const float *gout, float *gin, float *gfield, int64_t pb, int64_t pe,
                           cudaStream_t st) {
     if (pe <= pb) return MDG_OK;
-    MDG_WARP_DISPATCH(warp_bwd_k, d.h >= 2 ? C : 0, (grid1d(pe - pb, kSB), kSB, 0, st),
-                      (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe));
+    const int CD = d.h >= 2 ? C : 0;
+    if (!gin || warp_atomic_mode()) {
+        MDG_WARP_DISPATCH(warp_bwd_k, CD, (grid1d(pe - pb, kSB), kSB, 0, st),
+                          (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe));
+        MDG_LAUNCHED();
+        return MDG_OK;
+    }
+    // 1. gfield (gather, bit-exact) + the displacement bound; 2. gin gathered
+    // per target; 3. the atomic scatter only if the bound is out of reach
+    Scratch ws;
+    MDG_CUDA_TRY(ws.alloc(gin_gather_scratch_words(d) * sizeof(unsigned), st));
+    unsigned *rb = ws.as<unsigned>();
+    MDG_CUDA_TRY(cudaMemsetAsync(rb, 0, 2 * sizeof(unsigned), st));
+    MDG_WARP_DISPATCH(warp_bwd_k, CD, (grid1d(pe - pb, kSB), kSB, 0, st),
+                      (in, C, d.h, d.w, d.l, field, gout, nullptr, gfield, pb, pe, rb, false));
+    MDG_LAUNCHED();
+    if (mdg_status e = warp_gin_gather(field, gout, C, d, gin, pb, pe, rb, rb + 1, st)) return e;
+    MDG_WARP_DISPATCH(warp_bwd_k, CD, (grid1d(pe - pb, kSB), kSB, 0, st),
+                      (in, C, d.h, d.w, d.l, field, gout, gin, nullptr, pb, pe, rb, true));
     MDG_LAUNCHED();
     return MDG_OK;
 }
@@ -632,9 +676,25 @@ mdg_status mdg_compose_bwd(const float *prev, const float *res, mdg_dims3 d,
     MDG_REQUIRE(prev && res && gout, "compose: null pointer");
     MDG_REQUIRE(!(gprev && gprev == gres), "compose: gprev and gres must not alias");
     if (d.h >= 2 && gres) {
-        // the warp backward with C = 3 (x-merged scatter) plus the add node
-        warp_bwd_k<3, true><<<grid1d(n, kSB), kSB, 0, S_(stream)>>>(prev, 3, d.h, d.w, d.l, res,
-                                                                    gout, gprev, gres, 0, n);
+        // the warp backward with C = 3 plus the add node: gres by the gather
+        // kernel, gprev (the scatter) by the deterministic gather
+        cudaStream_t st = S_(stream);
+        if (!gprev || warp_atomic_mode()) {
+            warp_bwd_k<3, true><<<grid1d(n, kSB), kSB, 0, st>>>(prev, 3, d.h, d.w, d.l, res, gout,
+                                                                gprev, gres, 0, n);
+            MDG_LAUNCHED();
+            return MDG_OK;
+        }
+        Scratch ws;
+        MDG_CUDA_TRY(ws.alloc(gin_gather_scratch_words(d) * sizeof(unsigned), st));
+        unsigned *rb = ws.as<unsigned>();
+        MDG_CUDA_TRY(cudaMemsetAsync(rb, 0, 2 * sizeof(unsigned), st));
+        warp_bwd_k<3, true><<<grid1d(n, kSB), kSB, 0, st>>>(prev, 3, d.h, d.w, d.l, res, gout,
+                                                            nullptr, gres, 0, n, rb, false);
+        MDG_LAUNCHED();
+        if (mdg_status e = warp_gin_gather(res, gout, 3, d, gprev, 0, n, rb, rb + 1, st)) return e;
+        warp_bwd_k<3, true><<<grid1d(n, kSB), kSB, 0, st>>>(prev, 3, d.h, d.w, d.l, res, gout,
+                                                            gprev, nullptr, 0, n, rb, true);
         MDG_LAUNCHED();
         return MDG_OK;
     }

@@ -1,101 +1,167 @@
-"""Summarise an ncu capture (run here, no GPU needed):
+"""Summarise one profiles/ncu_cmds.sh capture (run here, no GPU needed):
 
-    python profiles/summarize_ncu.py gpurun_out/prof.ncu-rep gpurun_out/launches.csv rNN
+    python profiles/summarize_ncu.py <tag>        # reads gpurun_out/ncu_<tag>/
 
-Writes profiles/ncu_<tag>.md (per-kernel table + launch-share table) and
-updates profiles/ncu_traffic.json (dram bytes per launch, read by bench.py for
-roofline.traffic).
+Writes profiles/ncu_<tag>.md:
+  * the bench step: every kernel with launches, avg us, DRAM bytes per launch
+    (read + write), achieved DRAM GB/s and its fraction of the measured HBM
+    peak, and per op the SURVEY §8(d) algorithmic bytes and their fraction;
+  * one PO iteration: the same columns for every kernel it launches;
+  * the --set full captures: registers, issue activity, resident warps,
+    L1/TEX throughput, executed instructions per voxel;
+and profiles/ncu_traffic.json (per-kernel DRAM bytes per launch, read by
+bench.py for roofline.traffic).  ncu replays kernels with cold caches, so the
+absolute times are above the bench's CUDA-event times; shares agree.
 """
+import collections
 import csv
 import io
 import json
 import os
 import re
-import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-METRICS = [
-    ("gpu__time_duration.sum", "time"),
-    ("dram__bytes_read.sum", "dram_read"),
-    ("dram__bytes_write.sum", "dram_write"),
-    ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "mem_thr_%"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram_%"),
-    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "l1tex_%"),
-    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_%"),
-    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma_pipe_%"),
-    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps_active_%"),
-    ("launch__registers_per_thread", "regs"),
-    ("launch__shared_mem_per_block_static", "smem_static"),
-    ("launch__shared_mem_per_block_dynamic", "smem_dyn"),
-    ("smsp__inst_executed.sum", "inst"),
-]
+ROOT = os.path.dirname(HERE)
+NVOX = 160 * 192 * 224
+S, HD, CH = 1, 6, 8
+ALG = {  # SURVEY §8(d), bytes per voxel
+    "modet_fwd": 4 * (2 * S * HD + 3 * S), "modet_bwd": 4 * (4 * S * HD + 3 * S),
+    "warp_fwd": 4 * (3 + 2 * CH), "warp_bwd": 4 * (6 + 3 * CH)}
+OPS = {"modet_fwd": ["modet_fwd_tiled_k", "modet_fwd_fixup_k"],
+       "modet_bwd": ["modet_bwd_row_k", "modet_bwd_col_k", "modet_bwd_fused_k", "reduce_db_k"],
+       "warp_fwd": ["warp_fwd_k"], "warp_bwd": ["warp_bwd_k"]}
 SCALE = {"ms": 1e-3, "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9, "ns": 1e-9,
-         "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}
+         "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
+
+def peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6551.0
 
 
 def short(name):
-    base = re.sub(r"^void ", "", name).split("(")[0].split("<")[0]
-    return base.split("::")[-1]
+    return re.sub(r"^void ", "", name).split("(")[0].split("<")[0].split("::")[-1]
 
 
-def main(rep, launches, tag):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units = rows[0], rows[1]
-    kern = []
-    for r in rows[2:]:
-        d = {"kernel": short(r[hdr.index("Kernel Name")]), "full": r[hdr.index("Kernel Name")]}
-        for m, k in METRICS:
-            if m in hdr:
-                i = hdr.index(m)
-                v = r[i].replace(",", "")
-                try:
-                    v = float(v) * SCALE.get(units[i], 1.0)
-                except ValueError:
-                    pass
-                d[k] = v
-        kern.append(d)
-    traffic_path = os.path.join(HERE, "ncu_traffic.json")
-    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
-    lines = [f"# ncu summary {tag}", "", f"source: `{os.path.basename(rep)}` (`--set full "
-             "--clock-control none`, cold-cache replay); bench workload L1 160x192x224.", "",
-             "| kernel | time us | DRAM MB (r+w) | GB/s | mem thr % | L1 % | SM % | FMA % | "
-             "warps % | regs |", "|---|---|---|---|---|---|---|---|---|---|"]
-    for d in kern:
-        t = d.get("time", 0)
-        b = d.get("dram_read", 0) + d.get("dram_write", 0)
-        traffic[d["kernel"]] = int(b)
-        lines.append(
-            f"| {d['kernel']} | {t * 1e6:.1f} | {b / 1e6:.1f} | {b / t / 1e9 if t else 0:.0f} | "
-            f"{d.get('mem_thr_%', 0):.1f} | {d.get('l1tex_%', 0):.1f} | {d.get('sm_%', 0):.1f} | "
-            f"{d.get('fma_pipe_%', 0):.1f} | {d.get('warps_active_%', 0):.1f} | "
-            f"{d.get('regs', 0):.0f} |")
-    if launches and os.path.exists(launches):
-        txt = open(launches).read()
-        txt = txt[txt.index('"ID"'):] if '"ID"' in txt else txt
-        lr = list(csv.DictReader(io.StringIO(txt)))
-        tot = {}
-        for r in lr:
-            if r.get("Metric Name") != "gpu__time_duration.sum":
+def launches(path):
+    """{launch id: {kernel, time s, dram bytes}} from an ncu --csv --metrics log."""
+    if not os.path.exists(path):
+        return []
+    txt = open(path).read()
+    if '"ID"' not in txt:
+        return []
+    txt = txt[txt.index('"ID"'):]
+    out = collections.OrderedDict()
+    for r in csv.DictReader(io.StringIO(txt)):
+        d = out.setdefault(r["ID"], {"kernel": short(r["Kernel Name"]), "t": 0.0, "b": 0.0})
+        v = float(r["Metric Value"].replace(",", "")) * SCALE.get(r.get("Metric Unit", ""), 1.0)
+        if r["Metric Name"] == "gpu__time_duration.sum":
+            d["t"] = v
+        elif r["Metric Name"].startswith("dram__bytes"):
+            d["b"] += v
+    return list(out.values())
+
+
+def per_kernel(ls):
+    agg = collections.OrderedDict()
+    for d in ls:
+        a = agg.setdefault(d["kernel"], [0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += d["t"]
+        a[2] += d["b"]
+    return agg
+
+
+def table(agg, pk, lines, share=True):
+    tot = sum(a[1] for a in agg.values()) or 1.0
+    lines += ["| kernel | launches | avg us | DRAM MB / launch | DRAM GB/s | frac of peak |"
+              + (" share |" if share else ""),
+              "|---|---|---|---|---|---|" + ("---|" if share else "")]
+    for k, (n, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        gbs = b / t / 1e9 if t else 0.0
+        lines.append(f"| {k} | {n} | {t / n * 1e6:.1f} | {b / n / 1e6:.1f} | {gbs:.0f} | "
+                     f"{gbs / pk:.3f} |" + (f" {t / tot * 100:.1f}% |" if share else ""))
+
+
+def full_rows(d):
+    rows = []
+    for f in sorted(os.listdir(d)):
+        if not (f.startswith("full_") and f.endswith(".raw.csv")):
+            continue
+        raw = open(os.path.join(d, f)).read()
+        r = list(csv.reader(io.StringIO(raw)))
+        if len(r) < 3:
+            continue
+        h, v = r[0], r[2]
+
+        def g(n):
+            try:
+                return float(v[h.index(n)].replace(",", ""))
+            except (ValueError, IndexError):
+                return float("nan")
+        rows.append((short(v[h.index("Kernel Name")]), g("launch__registers_per_thread"),
+                     g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                     g("sm__warps_active.avg.per_cycle_active"),
+                     g("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                     g("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+                     g("smsp__inst_executed.sum") * 32 / NVOX,
+                     (g("dram__bytes_read.sum") + g("dram__bytes_write.sum")) / 1e6))
+    return rows
+
+
+def main(tag):
+    d = os.path.join(ROOT, "gpurun_out", f"ncu_{tag}")
+    pk = peak()
+    lines = [f"# ncu summary {tag}", "",
+             f"Captured by `bash profiles/ncu_cmds.sh {tag}` on one B200; peak = measured "
+             f"{pk:.0f} GB/s (MEASURED_PEAKS.json).  ncu replays each kernel with cold caches, "
+             "so its times run above the bench's CUDA-event times; the shares agree.", ""]
+    step = launches(os.path.join(d, "step_launches.csv"))
+    traffic = {"source": f"profiles/ncu_{tag}.md", "kernels": {}}
+    if step:
+        agg = per_kernel(step)
+        lines += ["## Bench step (L1 160x192x224; 5 steps: 3 warm-up + 2 timed)", ""]
+        table(agg, pk, lines)
+        lines += ["", "Per op, SURVEY §8(d) algorithmic bytes against the kernels' time "
+                  "(the roofline the bench reports):", "",
+                  "| op | kernels | alg. MB | ncu DRAM MB | DRAM / alg. | us | alg. frac of peak |",
+                  "|---|---|---|---|---|---|---|"]
+        nsteps = max(1, agg.get("warp_bwd_k", [5])[0])
+        for op, ks in OPS.items():
+            ks = [k for k in ks if k in agg]
+            if not ks:
                 continue
-            k = short(r["Kernel Name"])
-            v = float(r["Metric Value"].replace(",", "")) * SCALE.get(r.get("Metric Unit", "ns"), 1)
-            tot.setdefault(k, [0.0, 0])
-            tot[k][0] += v
-            tot[k][1] += 1
-        all_t = sum(v[0] for v in tot.values())
-        lines += ["", "Launch list (`--metrics gpu__time_duration.sum`, every launch of the "
-                  "profiled command incl. warm-up):", "", "| kernel | launches | total us | share |",
-                  "|---|---|---|---|"]
-        for k, (t, c) in sorted(tot.items(), key=lambda kv: -kv[1][0]):
-            lines.append(f"| {k} | {c} | {t * 1e6:.1f} | {t / all_t * 100:.1f}% |")
+            t = sum(agg[k][1] for k in ks) / nsteps
+            b = sum(agg[k][2] for k in ks) / nsteps
+            alg = ALG[op] * NVOX
+            lines.append(f"| {op} | {' + '.join(ks)} | {alg / 1e6:.1f} | {b / 1e6:.1f} | "
+                         f"{b / alg:.2f} | {t * 1e6:.1f} | {alg / t / 1e9 / pk:.3f} |")
+        for k, (n, t, b) in agg.items():
+            traffic["kernels"][k] = {"dram_bytes": int(b / n), "time_us": round(t / n * 1e6, 1)}
+    po = launches(os.path.join(d, "po_launches.csv"))
+    if po:
+        agg = per_kernel(po)
+        tot = sum(a[1] for a in agg.values())
+        lines += ["", f"## One PO iteration (160x192x224, eager launches): {len(po)} launches, "
+                  f"{tot * 1e3:.2f} ms summed kernel time under ncu", ""]
+        table(agg, pk, lines)
+    rows = full_rows(d)
+    if rows:
+        lines += ["", "## --set full captures (one launch each)", "",
+                  "| kernel | regs | issue active % | warps/SM | L1/TEX % | DRAM % | "
+                  "instr / voxel | DRAM MB |", "|---|---|---|---|---|---|---|---|"]
+        for r in rows:
+            lines.append("| " + " | ".join([r[0]] + [f"{x:.1f}" for x in r[1:]]) + " |")
     out = os.path.join(HERE, f"ncu_{tag}.md")
     open(out, "w").write("\n".join(lines) + "\n")
-    json.dump(traffic, open(traffic_path, "w"), indent=1, sort_keys=True)
+    if traffic["kernels"]:
+        json.dump(traffic, open(os.path.join(HERE, "ncu_traffic.json"), "w"), indent=1,
+                  sort_keys=True)
     print("\n".join(lines))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None, sys.argv[3] if len(sys.argv) > 3 else "r01")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r02")

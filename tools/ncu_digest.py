@@ -1,7 +1,7 @@
 """Digest of one ncu-rep kernel capture (run here, no GPU): key counters,
 stall-reason shares and the SASS opcode histogram.
 
-    python tools/ncu_digest.py gpurun_out/x.ncu-rep [n_voxels]
+    python tools/ncu_digest.py gpurun_out/x.ncu-rep [kernel-regex] [n_voxels]
 """
 import collections
 import csv
@@ -14,13 +14,14 @@ def ncu(rep, *args):
     return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
 
 
-def main(rep, nvox=160 * 192 * 224):
-    raw = list(csv.reader(io.StringIO(ncu(rep, "--page", "raw", "--csv"))))
+def main(rep, kern=None, nvox=160 * 192 * 224):
+    sel = ["--kernel-name", f"regex:{kern}"] if kern else []
+    raw = list(csv.reader(io.StringIO(ncu(rep, *sel, "--page", "raw", "--csv"))))
     h, v = raw[0], raw[2]
     get = lambda n: float(v[h.index(n)].replace(",", "")) if n in h else float("nan")  # noqa
     inst = get("smsp__inst_executed.sum")
     dur = get("gpu__time_duration.sum")
-    print(f"duration {dur/1e3:.1f} us  inst {inst/1e6:.1f} M  ({inst*32/nvox:.0f} thread-instr/voxel)"
+    print(f"duration {dur:.1f} (ncu units)  inst {inst/1e6:.1f} M  ({inst*32/nvox:.0f} thread-instr/voxel)"
           f"  regs {get('launch__registers_per_thread'):.0f}"
           f"  warps/SM {get('sm__warps_active.avg.per_cycle_active'):.1f}"
           f"  issue {get('smsp__issue_active.avg.pct_of_peak_sustained_active'):.1f}%"
@@ -30,8 +31,8 @@ def main(rep, nvox=160 * 192 * 224):
           and not n.endswith("not_issued")]
     tot = sum(x for x, _ in st) or 1
     print("stalls: " + ", ".join(f"{n} {100*x/tot:.0f}%" for x, n in sorted(st, reverse=True)[:8]))
-    src = list(csv.reader(io.StringIO(ncu(rep, "--page", "source", "--csv", "--print-source",
-                                          "sass"))))
+    src = list(csv.reader(io.StringIO(ncu(rep, *sel, "--page", "source", "--csv",
+                                          "--print-source", "sass"))))
     sh = src[1]
     iS, iE = sh.index("Source"), sh.index("Instructions Executed")
     ops, tot = collections.Counter(), 0
@@ -51,4 +52,5 @@ def main(rep, nvox=160 * 192 * 224):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], *(int(a) for a in sys.argv[2:]))
+    a = sys.argv[1:]
+    main(a[0], a[1] if len(a) > 1 else None, *(int(x) for x in a[2:]))
