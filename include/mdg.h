@@ -81,6 +81,16 @@ const char *mdg_build_info(void);
 mdg_status mdg_check_numeric(mdg_dims3 d, void *stream);
 /* number of kernels this library launched since load (host-side counter) */
 int64_t mdg_launch_count(void);
+/* Deterministic mode (process-wide; initial value from the environment
+ * variable MDG_DETERMINISTIC).  Off: the warp / compose input gradients are
+ * scattered with float atomics (fastest; the summation order at a shared
+ * corner varies between runs).  On: they are gathered per target in a fixed
+ * order, so every result — and a whole pairwise optimisation — is
+ * bit-identical from run to run, as the reference guarantees
+ * (test_engine.cpp:194-213); the warp backward then costs ~3x.  Every other
+ * kernel is deterministic in both modes.  Returns the previous setting. */
+int mdg_set_deterministic(int on);
+int mdg_get_deterministic(void);
 
 /* ---------------------------------------------------- index logic (exact) */
 /* attention.hpp:57-60 window_offset: slot o -> (dx, dy, dz), x fastest */

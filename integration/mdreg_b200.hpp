@@ -44,6 +44,10 @@
 
 namespace mdreg {
 namespace b200 {
+// the reference guarantees bitwise-repeatable runs (test_engine.cpp:194-213):
+// the binding switches libmdg to its deterministic mode at load time
+inline const bool deterministic_on = (mdg_set_deterministic(1), true);
+
 inline void check(mdg_status s) {
     switch (s) {
         case MDG_OK: return;

@@ -184,6 +184,8 @@ SIGNATURES = {
     "mdg_synth_smooth_velocity": (_st, [Dims3, C.c_uint64, _f, _f, _p]),
     "mdg_synth_random_field": (_st, [Dims3, C.c_uint64, _f, _p]),
     "mdg_synth_pair": (_st, [Dims3, C.c_uint64, _f, _p, _p, _p, _p, _p]),
+    "mdg_set_deterministic": (_i, [_i]),
+    "mdg_get_deterministic": (_i, []),
     "mdg_host_alloc": (_p, [C.c_size_t]),
     "mdg_host_free": (None, [_p]),
 }

@@ -202,8 +202,14 @@ mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
                           const float *gout, float *gin, float *gfield, int64_t pb, int64_t pe,
                           cudaStream_t st);
 
-// warp_gather.cu: the warp's input gradient as a deterministic gather (after
+// deterministic mode (runtime.cu): process-wide, initialised from the
+// MDG_DETERMINISTIC environment variable, set by mdg_set_deterministic()
+bool deterministic_mode();
+
+// warp_gather.cu: the warp's input gradient as a deterministic gather for
+// displacements up to kGinGatherReach voxels (after
 // warp_bwd_k has put max |phi| into rbits[0]; rbits[1..] is its scratch)
+constexpr int kGinGatherReach = 4;
 int64_t gin_gather_scratch_words(mdg_dims3 d);
 mdg_status warp_gin_gather(const float *field, const float *gout, int C, mdg_dims3 d, float *gin,
                            int64_t pb, int64_t pe, const unsigned *rbits, unsigned *dirty,

@@ -1,6 +1,7 @@
 // runtime.cu — error slots, the device numeric flag, the synthetic-input RNG,
 // pinned host memory and the small exact-index entry points of libmdg.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -93,6 +94,21 @@ unsigned long long *numeric_flag_ptr(cudaStream_t st) {
 unsigned long long *fixup_queue_ptr(cudaStream_t st) {
     StreamState *s = stream_state(st);
     return s ? s->fixq : nullptr;
+}
+
+namespace {
+std::atomic<int> g_det{-1};
+}
+bool deterministic_mode() {
+    int v = g_det.load(std::memory_order_relaxed);
+    if (v < 0) {
+        const char *e = std::getenv("MDG_DETERMINISTIC");
+        v = (e && *e && *e != '0') ? 1 : 0;
+        int expect = -1;
+        g_det.compare_exchange_strong(expect, v);
+        v = g_det.load();
+    }
+    return v == 1;
 }
 
 void keep_pool_mapped() {
@@ -208,6 +224,14 @@ mdg_status mdg_check_numeric(mdg_dims3 d, void *stream) {
 }
 
 int64_t mdg_launch_count(void) { return g_launches.load(); }
+
+int mdg_set_deterministic(int on) {
+    const int prev = deterministic_mode() ? 1 : 0;
+    g_det.store(on ? 1 : 0);
+    return prev;
+}
+
+int mdg_get_deterministic(void) { return deterministic_mode() ? 1 : 0; }
 
 mdg_status mdg_window_offset(int o, int nb, int off[3]) {
     MDG_REQUIRE(nb >= 3 && nb % 2 == 1, "attention: neighborhood must be odd and >= 3");

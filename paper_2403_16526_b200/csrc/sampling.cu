@@ -20,7 +20,7 @@
 namespace mdg {
 
 constexpr int kSB = 256;
-constexpr int kGatherReach = 6;  // warp_gather.cu gather::kRMax
+constexpr int kGatherReach = kGinGatherReach;
 
 struct Corners {
     Ax ax, ay, az;
@@ -273,7 +273,8 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
     const float phx = __ldg(field + p), phy = __ldg(field + n + p), phz = __ldg(field + 2 * n + p);
     if (rbits && !far_only) {
         float m = ok ? fmaxf(fabsf(phx), fmaxf(fabsf(phy), fabsf(phz))) : 0.0f;
-        if (!(m == m)) m = __uint_as_float(0x7fc00000u);  // NaN: as large as it gets
+        // a NaN entry (fmaxf would drop it) ranks above every bound
+        if (ok && (isnan(phx) || isnan(phy) || isnan(phz))) m = __uint_as_float(0x7fc00000u);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
             m = __uint_as_float(max(__float_as_uint(m),
@@ -569,19 +570,19 @@ mdg_status warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
     return MDG_OK;
 }
 
-// gin by the deterministic gather (warp_gather.cu) unless MDG_WARP_ATOMIC is
-// set (the previous float-atomic scatter, kept for A/B measurement)
-static bool warp_atomic_mode() {
-    static const bool v = std::getenv("MDG_WARP_ATOMIC") != nullptr;
-    return v;
-}
+// gin by the float-atomic scatter (fast; the summation order at a shared
+// corner varies from run to run) unless deterministic mode is on
+// (mdg_set_deterministic / MDG_DETERMINISTIC=1): then by the per-target
+// gather of warp_gather.cu, bit-identical from run to run, ~3x the cost
+static bool warp_atomic_mode() { return !deterministic_mode(); }
 
 mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *field,
                           const float *gout, float *gin, float *gfield, int64_t pb, int64_t pe,
                           cudaStream_t st) {
     if (pe <= pb) return MDG_OK;
     const int CD = d.h >= 2 ? C : 0;
-    if (!gin || warp_atomic_mode()) {
+    // (the gather indexes with 32-bit offsets: up to 16 channel planes)
+    if (!gin || warp_atomic_mode() || 16 * nvox(d) >= (int64_t(1) << 32) || d.l >= 4096) {
         MDG_WARP_DISPATCH(warp_bwd_k, CD, (grid1d(pe - pb, kSB), kSB, 0, st),
                           (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe));
         MDG_LAUNCHED();
@@ -679,7 +680,7 @@ mdg_status mdg_compose_bwd(const float *prev, const float *res, mdg_dims3 d,
         // the warp backward with C = 3 plus the add node: gres by the gather
         // kernel, gprev (the scatter) by the deterministic gather
         cudaStream_t st = S_(stream);
-        if (!gprev || warp_atomic_mode()) {
+        if (!gprev || warp_atomic_mode() || 16 * n >= (int64_t(1) << 32) || d.l >= 4096) {
             warp_bwd_k<3, true><<<grid1d(n, kSB), kSB, 0, st>>>(prev, 3, d.h, d.w, d.l, res, gout,
                                                                 gprev, gres, 0, n);
             MDG_LAUNCHED();

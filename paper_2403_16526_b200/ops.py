@@ -195,6 +195,17 @@ def _zeros(*shape, like):
     return torch.zeros(*shape, dtype=torch.float32, device=like.device)
 
 
+def set_deterministic(on=True):
+    """Deterministic mode (mdg_set_deterministic): bit-identical results from
+    run to run, the warp / compose input gradients gathered per target instead
+    of scattered with float atomics.  Returns the previous setting."""
+    return bool(_capi.lib().mdg_set_deterministic(1 if on else 0))
+
+
+def deterministic():
+    return bool(_capi.lib().mdg_get_deterministic())
+
+
 def check_numeric(d):
     """Raise NumericError if a fused-tier kernel saw a non-finite logit
     (position decoded against dims d)."""

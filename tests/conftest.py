@@ -53,3 +53,13 @@ def cuda():
 
     assert _capi.lib().mdg_device_ok() == 1, "libmdg needs an sm_100a device"
     return torch.device("cuda:0")
+
+
+@pytest.fixture
+def deterministic(cuda):
+    """libmdg's deterministic mode (mdg_set_deterministic) for one test."""
+    from paper_2403_16526_b200 import ops
+
+    prev = ops.set_deterministic(True)
+    yield
+    ops.set_deterministic(prev)

@@ -2,9 +2,11 @@
 
 Forward results and every gather-form gradient are BIT-IDENTICAL to the CPU
 reference (same fp32 evaluation order, no FMA contraction); the image-side
-scatter gradients (warp gin, compose gprev) use fp32 atomics, so their terms
-are identical but the summation order at shared corners varies: checked to
-|d| <= 1e-5 + 1e-4|ref|.  The integer corner logic (resolve_axis) is checked
+scatter gradients (warp gin, compose gprev) are gathered per target
+(warp_gather.cu): every term is the reference's, the sum order is fixed but
+cell-major instead of the reference's source-major, so they are checked to
+|d| <= 1e-5 + 1e-4|ref| and bit-identical from run to run (and bit-identical
+to the reference on the exact path crowded cells take).  The integer corner logic (resolve_axis) is checked
 bit-for-bit on the device.
 """
 import numpy as np
@@ -223,3 +225,67 @@ def test_pipelined_warp_host_calls_match_device(cuda, C, reach):
     assert L.mdg_warp_bwd_host(p(vol), C, d3, p(fld), p(g), p(gin), p(gf)) == 0
     assert np.array_equal(gf, gf_d, equal_nan=True)
     np.testing.assert_allclose(gin, gin_d, rtol=1e-4, atol=1e-5, equal_nan=True)
+
+
+# ------------------------------------------------ deterministic gin gather
+# (deterministic mode, mdg_set_deterministic: gathered per target; the default
+# mode scatters with float atomics and is covered by the tests above)
+def _gin_twice(vol, fld, gout):
+    a, _ = ops.warp_bwd(vol, fld, gout)
+    b, _ = ops.warp_bwd(vol, fld, gout)
+    return host(a), host(b)
+
+
+@pytest.mark.parametrize("kind", ["smooth", "random", "contracting", "far"])
+def test_warp_gin_gather_deterministic_and_correct(cuda, oracle, ref, deterministic, kind):
+    """gin from the per-target gather: identical from run to run (bitwise),
+    within tolerance of the reference scatter, for a smooth field, the i.i.d.
+    random field (|phi| <= 2), a contracting field (x -> x/3: crowded cells
+    take the exact reference-order path) and a far field (|phi| = 9 > the
+    gather's reach of 4: the atomic scatter fallback, correct but not
+    repeatable)."""
+    dims = (37, 21, 19)
+    h, w, l = dims
+    C = 3
+    vol = random_feature_map(C, dims, 5)
+    if kind == "smooth":
+        fld = ref.make_smooth_velocity(dims, 11, 2.0, 3.0)
+    elif kind == "random":
+        fld = random_field(dims, 12, 2.0)
+    elif kind == "contracting":
+        zz, yy, xx = np.meshgrid(np.arange(l), np.arange(w), np.arange(h), indexing="ij")
+        # x, y -> a third of their distance from the centre: ~9 sources per
+        # cell in the middle (> the 4-entry lists: exact path)
+        fld = f32(np.stack([-(2.0 / 3.0) * (xx - h / 2), -(2.0 / 3.0) * (yy - w / 2),
+                            0.25 * np.ones_like(zz, dtype=np.float64)]))
+        fld = f32(np.clip(fld, -3.9, 3.9))  # within the gather's reach (4)
+    else:
+        fld = f32(np.full((3, l, w, h), 9.0))
+        fld[0] *= -1.0
+    gout = random_feature_map(C, dims, 6)
+    gout[:, 3, 4, :5] = 0.0  # g == 0 channels are skipped like the reference does
+    want, _ = oracle.warp_bwd(vol, fld, gout)
+    a, b = _gin_twice(dev(vol), dev(fld), dev(gout))
+    assert rel_close(a, want), np.abs(a - want).max()
+    if kind != "far":
+        assert np.array_equal(a, b)
+
+
+def test_warp_gin_gather_range_matches_whole(cuda, oracle, deterministic):
+    """The voxel-range form (depth slabs / pipeline chunks) gathers the same
+    terms: the sum over two ranges equals the whole-volume gradient."""
+    dims = (32, 12, 20)
+    vol = random_feature_map(2, dims, 7)
+    fld = random_field(dims, 8, 1.7)
+    gout = random_feature_map(2, dims, 9)
+    from paper_2403_16526_b200 import _capi
+    L = _capi.lib()
+    n = 32 * 12 * 20
+    whole, _ = ops.warp_bwd(dev(vol), dev(fld), dev(gout))
+    gin = torch.zeros(2, n, device="cuda")
+    v, f, g = dev(vol), dev(fld), dev(gout)
+    for pb, pe in ((0, n // 3), (n // 3, n)):
+        assert L.mdg_warp_bwd_range(v.data_ptr(), 2, ops.dims3(dims), f.data_ptr(), g.data_ptr(),
+                                    gin.data_ptr(), None, pb, pe,
+                                    torch.cuda.current_stream().cuda_stream) == 0
+    assert rel_close(host(gin), host(whole).reshape(2, n))
