@@ -490,6 +490,20 @@ mdg_status mdg_checkpoint_save(const char *path, const mdg_model_config *cfg,
                                const float *const *tensors);
 mdg_status mdg_checkpoint_load(const char *path, mdg_model_config *cfg, float *const *tensors);
 
+/* ---- the model object for any ModelConfig (engine.hpp:30-78, 268-311) ----
+ * mdg_model_create / mdg_model_init above are this with the small preset and
+ * Adam.  optimizer: OptimizerKind (engine.hpp:80) — MDG_OPT_ADAM (the
+ * AdamOptimizer) or MDG_OPT_SGD (sgd_step); mdg_model_adam_step and
+ * mdg_model_po_step apply the configured one.  Tensor sizes of a config:
+ * mdg_config_param_count. */
+#define MDG_OPT_ADAM 0
+#define MDG_OPT_SGD 1
+mdg_status mdg_model_init_cfg(const mdg_model_config *cfg, uint64_t seed,
+                              float *const *params_host);
+mdg_status mdg_model_create_cfg(const mdg_model_config *cfg, mdg_dims3 d, float *const *params,
+                                float lambda, int ncc_window, int check_finite, int optimizer,
+                                mdg_model **out);
+
 /* pinned host memory for the host-buffer path */
 void *mdg_host_alloc(size_t bytes);
 void mdg_host_free(void *p);

@@ -293,6 +293,59 @@ class _Lib:
             raise RuntimeError(self._perr().decode())
         return list(lt), list(dt), phi
 
+    # -- any ModelConfig / optimizer (reference build only) -----------------
+    @staticmethod
+    def _cfg(base=8, heads=(8, 4, 2, 1, 1), hd=6, diffeomorphic=False, ss_steps=7):
+        return (C.c_int * 9)(base, *heads, hd, 1 if diffeomorphic else 0, ss_steps)
+
+    def model_params_cfg(self, seed=42, **cfg):
+        """init_model(cfg, seed): (packed, sizes); cfg keys: base, heads, hd,
+        diffeomorphic, ss_steps."""
+        c = self._cfg(**cfg)
+        f = self.lib.mdr_model_param_count_cfg
+        f.restype, f.argtypes = C.c_int64, [C.POINTER(C.c_int)]
+        n = int(f(c))
+        g = self.lib.mdr_model_params_cfg
+        g.restype = C.c_int
+        g.argtypes = [C.POINTER(C.c_int), C.c_uint64, _f, C.POINTER(C.c_int64)]
+        out = np.zeros(n, np.float32)
+        sizes = (C.c_int64 * 128)()
+        cnt = g(c, seed, _fp(out), sizes)
+        return out, [int(sizes[i]) for i in range(cnt)]
+
+    def loss_step_cfg(self, fixed, moving, packed, lam=1.0, window=9, grads=True, **cfg):
+        c = self._cfg(**cfg)
+        f = self.lib.mdr_loss_step_cfg
+        f.restype = C.c_int
+        f.argtypes = [C.POINTER(C.c_int), _f, _f, C.c_int, C.c_int, C.c_int, _f, C.c_float,
+                      C.c_int, C.POINTER(C.c_double), _f, _f]
+        l, w, h = fixed.shape[1:]
+        loss = C.c_double()
+        gp = np.zeros_like(packed) if grads else None
+        phi = np.zeros((3, l, w, h), np.float32)
+        if f(c, _fp(fixed), _fp(moving), h, w, l, _fp(packed), lam, window, C.byref(loss),
+             _fp(gp), _fp(phi)):
+            raise RuntimeError(self._perr().decode())
+        return loss.value, gp, phi
+
+    def pairwise_optimize_cfg(self, fixed, moving, lf, lm, packed, iters, lr=1e-4, lam=1.0,
+                              window=9, optimizer="adam", **cfg):
+        c = self._cfg(**cfg)
+        f = self.lib.mdr_pairwise_optimize_cfg
+        f.restype = C.c_int
+        f.argtypes = [C.POINTER(C.c_int), C.c_int, _f, _f, _i, _i, C.c_int, C.c_int, C.c_int,
+                      _f, C.c_int, C.c_double, C.c_double, C.c_int, C.POINTER(C.c_double),
+                      C.POINTER(C.c_double), _f]
+        l, w, h = fixed.shape[1:]
+        lt = (C.c_double * (iters + 1))()
+        dt = (C.c_double * (iters + 1))()
+        phi = np.zeros((3, l, w, h), np.float32)
+        ip = lambda a: np.ascontiguousarray(a, np.int32).ctypes.data_as(_i)  # noqa: E731
+        if f(c, 0 if optimizer == "adam" else 1, _fp(fixed), _fp(moving), ip(lf), ip(lm), h, w,
+             l, _fp(packed), iters, lr, lam, window, lt, dt, _fp(phi)):
+            raise RuntimeError(self._perr().decode())
+        return list(lt), list(dt), phi
+
     def level_param_count(self, C_, S, hd, nb=3):
         return int(self._lpc(C_, S, hd, nb))
 

@@ -360,4 +360,92 @@ int mdr_pairwise_optimize(const float *fixed, const float *moving, const int *la
     return 0;
 }
 
+// ---- any ModelConfig (engine.hpp:30-78) / optimizer (engine.hpp:80) ----
+// cfg = {base_channels, heads_per_level[5] (coarse -> fine), head_dim,
+//        diffeomorphic, ss_steps}; optimizer 0 = Adam, 1 = SGD
+static ModelConfig config_of(const int *cfg) {
+    ModelConfig c = ModelConfig::small_preset();
+    c.encoder.base_channels = cfg[0];
+    c.heads_per_level.assign(cfg + 1, cfg + 6);
+    c.head_dim = cfg[6];
+    c.diffeomorphic = cfg[7] != 0;
+    c.ss_steps = cfg[8];
+    c.validate();
+    return c;
+}
+
+int64_t mdr_model_param_count_cfg(const int *cfg) {
+    ModelParams<float> mp = init_model<float>(config_of(cfg), 1);
+    return model_count(mp);
+}
+
+int mdr_model_params_cfg(const int *cfg, std::uint64_t seed, float *out, int64_t *sizes) {
+    ModelParams<float> mp = init_model<float>(config_of(cfg), seed);
+    int i = 0;
+    for (auto *p : mp.all_tensors()) {
+        std::memcpy(out, p->value.data.data(), p->value.data.size() * sizeof(float));
+        out += p->value.data.size();
+        if (sizes) sizes[i] = p->value.size();
+        ++i;
+    }
+    return i;
+}
+
+int mdr_loss_step_cfg(const int *cfg, const float *fixed, const float *moving, int h, int w,
+                      int l, const float *packed, float lambda, int window, double *loss,
+                      float *gpacked, float *phi) {
+    try {
+        ModelParams<float> mp = init_model<float>(config_of(cfg), 1);
+        load_params(mp, packed);
+        Volume f(D3(h, w, l)), m(D3(h, w, l));
+        std::memcpy(f.data.data(), fixed, f.data.size() * sizeof(float));
+        std::memcpy(m.data.data(), moving, m.data.size() * sizeof(float));
+        auto params = mp.all_tensors();
+        LossConfig lc{lambda, window};
+        RegistrationResult rr;
+        *loss = run_loss_step(f, m, mp, lc, params, gpacked != nullptr, phi ? &rr : nullptr);
+        if (gpacked)
+            for (auto *p : params) {
+                add_into(gpacked, p->grad);
+                gpacked += p->grad.data.size();
+            }
+        if (phi) std::memcpy(phi, rr.phi.data.data(), rr.phi.data.size() * sizeof(float));
+    } catch (const std::exception &e) {
+        g_perr = e.what();
+        return 1;
+    }
+    return 0;
+}
+
+int mdr_pairwise_optimize_cfg(const int *cfg, int optimizer, const float *fixed,
+                              const float *moving, const int *labels_fixed,
+                              const int *labels_moving, int h, int w, int l, const float *packed,
+                              int iters, double lr, double lambda, int window,
+                              double *loss_trace, double *dice_trace, float *phi) {
+    try {
+        ModelParams<float> mp = init_model<float>(config_of(cfg), 1);
+        load_params(mp, packed);
+        Volume f(D3(h, w, l)), m(D3(h, w, l));
+        std::memcpy(f.data.data(), fixed, f.data.size() * sizeof(float));
+        std::memcpy(m.data.data(), moving, m.data.size() * sizeof(float));
+        LabelVolume lf(D3(h, w, l)), lm(D3(h, w, l));
+        std::memcpy(lf.data.data(), labels_fixed, lf.data.size() * sizeof(int));
+        std::memcpy(lm.data.data(), labels_moving, lm.data.size() * sizeof(int));
+        OptimConfig oc;
+        oc.po_iters = iters;
+        oc.lr_init = lr;
+        oc.lambda = lambda;
+        oc.ncc_window = window;
+        oc.optimizer = optimizer ? OptimizerKind::sgd : OptimizerKind::adam;
+        PoResult r = pairwise_optimize(f, m, mp, oc, &lf, &lm);
+        for (size_t i = 0; i < r.loss_trace.size(); ++i) loss_trace[i] = r.loss_trace[i];
+        for (size_t i = 0; i < r.dice_trace.size(); ++i) dice_trace[i] = r.dice_trace[i];
+        std::memcpy(phi, r.reg.phi.data.data(), r.reg.phi.data.size() * sizeof(float));
+    } catch (const std::exception &e) {
+        g_perr = e.what();
+        return 1;
+    }
+    return 0;
+}
+
 }  // extern "C"

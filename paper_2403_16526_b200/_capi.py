@@ -138,6 +138,9 @@ SIGNATURES = {
     "mdg_model_init": (_st, [C.c_uint64, C.POINTER(_p)]),
     "mdg_model_create": (_st, [Dims3, C.POINTER(_p), _f, _i, _i, C.POINTER(_p)]),
     "mdg_model_destroy": (None, [_p]),
+    "mdg_model_init_cfg": (_st, [C.POINTER(ModelConfigC), C.c_uint64, C.POINTER(_p)]),
+    "mdg_model_create_cfg": (_st, [C.POINTER(ModelConfigC), Dims3, C.POINTER(_p), _f, _i, _i, _i,
+                                   C.POINTER(_p)]),
     "mdg_model_grads": (C.POINTER(_p), [_p]),
     "mdg_model_loss_step": (_st, [_p, _p, _p, _i, _p, _p, _p]),
     "mdg_model_adam_step": (_st, [_p, C.c_double, _p]),

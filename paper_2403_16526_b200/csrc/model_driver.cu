@@ -33,6 +33,8 @@ __global__ void add_k(float *__restrict__ dst, const float *__restrict__ src, in
     } while (0)
 
 struct mdg_model {
+    mdg_model_config cfg{};
+    int optimizer = MDG_OPT_ADAM;
     mdg_dims3 d;
     int64_t n = 0;
     float lambda = 1.0f;
@@ -75,46 +77,57 @@ struct mdg_model {
 };
 
 namespace {
-// small preset (engine.hpp:38-44): base 8, heads {8,4,2,1,1}, hd 6
-constexpr int kBase = 8, kLevels = 5, kHd = 6;
-const int kHeads[kLevels] = {8, 4, 2, 1, 1};
+constexpr int kLevels = MDG_ENC_LEVELS;
 
-std::vector<int64_t> model_sizes() {
-    std::vector<int64_t> s;
-    for (int k = 0; k < kLevels; ++k) {
-        const int64_t c = kBase << k, cin = k == 0 ? 1 : kBase << (k - 1);
-        s.insert(s.end(), {c * cin * 27, c, c, c, c * c * 27, c, c, c});
-    }
-    for (int k = 0; k < kLevels; ++k) {
-        const int64_t cin = kBase << (kLevels - 1 - k), S = kHeads[k], K = S * kHd;
-        s.insert(s.end(), {K * cin, K, K, K, S * 27, 3 * 3 * S * 27, 3});
-    }
+// ModelParams::all_tensors element counts of a config (io.cpp layout_of)
+std::vector<int64_t> model_sizes(const mdg_model_config &c) {
+    int nt = 0;
+    mdg_config_param_count(&c, &nt, nullptr);
+    std::vector<int64_t> s((size_t)nt);
+    mdg_config_param_count(&c, &nt, s.data());
     return s;
+}
+
+mdg_model_config small_preset() {
+    mdg_model_config c{};
+    mdg_model_config_small_preset(&c);
+    return c;
+}
+
+mdg_status check_config(const mdg_model_config &c) {
+    // ModelConfig::validate (engine.hpp:62-76)
+    MDG_REQUIRE(c.base_channels >= 1, "encoder: base_channels must be >= 1");
+    for (int k = 0; k < kLevels; ++k) {
+        MDG_REQUIRE(c.heads_per_level[k] >= 1, "model: head counts must be >= 1");
+        MDG_REQUIRE(k == 0 || c.heads_per_level[k] <= c.heads_per_level[k - 1],
+                    "model: head counts must be non-increasing coarse to fine");
+    }
+    MDG_REQUIRE(c.head_dim >= 1, "model: head_dim must be >= 1");
+    MDG_REQUIRE(c.neighborhood == 3, "model: the B200 pyramid runs neighborhood 3");
+    MDG_REQUIRE(c.ss_steps >= 1, "model: ss_steps must be >= 1");
+    return MDG_OK;
 }
 }  // namespace
 
 extern "C" {
 
 int64_t mdg_model_param_count(int *ntensors, int64_t *sizes) {
-    const auto s = model_sizes();
-    if (ntensors) *ntensors = (int)s.size();
-    int64_t tot = 0;
-    for (size_t i = 0; i < s.size(); ++i) {
-        if (sizes) sizes[i] = s[i];
-        tot += s[i];
-    }
-    return tot;
+    const mdg_model_config c = small_preset();
+    return mdg_config_param_count(&c, ntensors, sizes);
 }
 
-mdg_status mdg_model_init(uint64_t seed, float *const *params_host) {
-    // init_model(small_preset, seed) (engine.hpp:143-166) on host buffers,
-    // drawn from the reference Rng stream in the reference order
-    MDG_REQUIRE(params_host, "model: null pointer");
-    const auto s = model_sizes();
+mdg_status mdg_model_init_cfg(const mdg_model_config *cfg, uint64_t seed,
+                              float *const *params_host) {
+    // init_model(cfg, seed) (engine.hpp:143-166) on host buffers, drawn from
+    // the reference Rng stream in the reference order
+    MDG_REQUIRE(cfg && params_host, "model: null pointer");
+    if (mdg_status e = check_config(*cfg)) return e;
+    const auto s = model_sizes(*cfg);
+    const int base = cfg->base_channels;
     mdg_rng *r = mdg_rng_new(seed);
     int i = 0;
     for (int k = 0; k < kLevels; ++k) {
-        const int c = kBase << k, cin = k == 0 ? 1 : kBase << (k - 1);
+        const int c = base << k, cin = k == 0 ? 1 : base << (k - 1);
         const double b1 = std::sqrt(6.0 / (cin * 27.0)), b2 = std::sqrt(6.0 / (c * 27.0));
         mdg_rng_fill_uniform(r, params_host[i], s[i], -b1, b1);
         for (int j = 1; j < 4; ++j)
@@ -136,25 +149,36 @@ mdg_status mdg_model_init(uint64_t seed, float *const *params_host) {
     return MDG_OK;
 }
 
-mdg_status mdg_model_create(mdg_dims3 d, float *const *params, float lambda, int ncc_window,
-                            int check_finite, mdg_model **out) {
-    MDG_REQUIRE(params && out, "model: null pointer");
+mdg_status mdg_model_init(uint64_t seed, float *const *params_host) {
+    const mdg_model_config c = small_preset();
+    return mdg_model_init_cfg(&c, seed, params_host);
+}
+
+mdg_status mdg_model_create_cfg(const mdg_model_config *cfg, mdg_dims3 d, float *const *params,
+                                float lambda, int ncc_window, int check_finite, int optimizer,
+                                mdg_model **out) {
+    MDG_REQUIRE(cfg && params && out, "model: null pointer");
     *out = nullptr;
+    if (mdg_status e = check_config(*cfg)) return e;
     MDG_REQUIRE(lambda >= 0.0f, "loss: lambda must be >= 0");
     MDG_REQUIRE(ncc_window >= 3 && ncc_window % 2 == 1, "loss: ncc_window must be odd and >= 3");
+    MDG_REQUIRE(optimizer == MDG_OPT_ADAM || optimizer == MDG_OPT_SGD, "model: unknown optimizer");
     mdg_model *m = new mdg_model;
+    m->cfg = *cfg;
+    m->optimizer = optimizer;
     m->d = d;
     m->n = nvox(d);
     m->lambda = lambda;
     m->window = ncc_window;
-    m->sizes = model_sizes();
+    m->sizes = model_sizes(*cfg);
     m->params.assign(params, params + m->sizes.size());
     auto fail = [&](mdg_status st) {
         mdg_model_destroy(m);
         return st;
     };
-    mdg_status st = mdg_encoder_create(d, kBase, kLevels, 0.2f, &m->enc_f);
-    if (st == MDG_OK) st = mdg_encoder_create(d, kBase, kLevels, 0.2f, &m->enc_m);
+    const int base = cfg->base_channels;
+    mdg_status st = mdg_encoder_create(d, base, kLevels, cfg->leaky_slope, &m->enc_f);
+    if (st == MDG_OK) st = mdg_encoder_create(d, base, kLevels, cfg->leaky_slope, &m->enc_m);
     if (st != MDG_OK) return fail(st);
     mdg_pyramid_config pc{};
     pc.levels = kLevels;
@@ -164,14 +188,14 @@ mdg_status mdg_model_create(mdg_dims3 d, float *const *params, float lambda, int
         dims.push_back(mdg_dims3{(p.h + 1) / 2, (p.w + 1) / 2, (p.l + 1) / 2});
     }
     for (int k = 0; k < kLevels; ++k) {  // coarse -> fine
-        pc.heads[k] = kHeads[k];
-        pc.channels[k] = kBase << (kLevels - 1 - k);
+        pc.heads[k] = cfg->heads_per_level[k];
+        pc.channels[k] = base << (kLevels - 1 - k);
         pc.dims[k] = dims[kLevels - 1 - k];
     }
-    pc.head_dim = kHd;
-    pc.neighborhood = 3;
-    pc.diffeomorphic = 0;
-    pc.ss_steps = 7;
+    pc.head_dim = cfg->head_dim;
+    pc.neighborhood = cfg->neighborhood;
+    pc.diffeomorphic = cfg->diffeomorphic;
+    pc.ss_steps = cfg->ss_steps;
     pc.check_finite = check_finite;
     if ((st = mdg_pyramid_create(&pc, &m->pyr)) != MDG_OK) return fail(st);
     // arena: grads | moving-encoder grads | Adam moments | features + their
@@ -186,7 +210,7 @@ mdg_status mdg_model_create(mdg_dims3 d, float *const *params, float lambda, int
     m->grads_len = tot;
     m->enc_len = enc;
     int64_t feat = 0;
-    for (int k = 0; k < kLevels; ++k) feat += (int64_t)(kBase << k) * nvox(dims[k]) + 64;
+    for (int k = 0; k < kLevels; ++k) feat += (int64_t)(base << k) * nvox(dims[k]) + 64;
     const size_t bytes =
         ((size_t)3 * tot + enc + 4 * (size_t)feat + 6 * (size_t)m->n + 64) * sizeof(float);
     cudaError_t e = cudaMalloc(&m->arena, bytes);
@@ -219,7 +243,7 @@ mdg_status mdg_model_create(mdg_dims3 d, float *const *params, float lambda, int
     for (auto *vec : {&m->ff, &m->mf, &m->gf, &m->gm})
         for (int k = 0; k < kLevels; ++k) {
             vec->push_back(p);
-            p += (int64_t)(kBase << k) * nvox(dims[k]) + 64;
+            p += (int64_t)(base << k) * nvox(dims[k]) + 64;
         }
     m->phi = p;
     p += 3 * m->n;
@@ -228,6 +252,13 @@ mdg_status mdg_model_create(mdg_dims3 d, float *const *params, float lambda, int
     m->terms = p;
     *out = m;
     return MDG_OK;
+}
+
+mdg_status mdg_model_create(mdg_dims3 d, float *const *params, float lambda, int ncc_window,
+                            int check_finite, mdg_model **out) {
+    const mdg_model_config c = small_preset();
+    return mdg_model_create_cfg(&c, d, params, lambda, ncc_window, check_finite, MDG_OPT_ADAM,
+                                out);
 }
 
 void mdg_model_destroy(mdg_model *m) {
@@ -307,7 +338,7 @@ mdg_status mdg_model_loss_step(mdg_model *m, const float *fixed, const float *mo
     {
         mdg_dims3 dk = m->d;
         for (int k = 0; k < kLevels; ++k) {
-            const size_t bytes = (size_t)(kBase << k) * nvox(dk) * sizeof(float);
+            const size_t bytes = (size_t)(m->cfg.base_channels << k) * nvox(dk) * sizeof(float);
             MDG_CUDA_TRY(cudaMemsetAsync(m->gf[k], 0, bytes, st));
             MDG_CUDA_TRY(cudaMemsetAsync(m->gm[k], 0, bytes, st));
             dk = mdg_dims3{(dk.h + 1) / 2, (dk.w + 1) / 2, (dk.l + 1) / 2};
@@ -360,12 +391,24 @@ static AdamList adam_list(const mdg_model *m) {
     return L;
 }
 
+// sgd_step (engine.hpp:306-311) over every tensor
+static mdg_status sgd_all(mdg_model *m, double lr, cudaStream_t st) {
+    for (size_t i = 0; i < m->params.size(); ++i)
+        MD_TRY(mdg_sgd_step(m->params[i], m->grads[i], m->sizes[i], lr, st));
+    return MDG_OK;
+}
+
+// the configured optimizer's update (graph-capturable: no host reads)
+static mdg_status update(mdg_model *m, double lr, cudaStream_t st) {
+    if (m->optimizer == MDG_OPT_SGD) return sgd_all(m, lr, st);
+    return adam_multi_dev(adam_list(m), lr, m->beta1, m->beta2, m->eps, m->d_t, m->d_bc, st);
+}
+
 mdg_status mdg_model_adam_step(mdg_model *m, double lr, void *stream) {
     MDG_REQUIRE(m, "model: null pointer");
     ++m->t;
     MD_TRY(ensure_bc(m, m->t));
-    return adam_multi_dev(adam_list(m), lr, m->beta1, m->beta2, m->eps, m->d_t, m->d_bc,
-                          S_(stream));
+    return update(m, lr, S_(stream));
 }
 
 // One PO iteration (run_loss_step + AdamOptimizer::step, engine.hpp:389-398)
@@ -401,10 +444,7 @@ mdg_status mdg_model_po_step(mdg_model *m, const float *fixed, const float *movi
         bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) == cudaSuccess;
         if (ok) {
             const mdg_status s1 = mdg_model_loss_step(m, fixed, moving, 1, terms, nullptr, st);
-            const mdg_status s2 =
-                s1 == MDG_OK ? adam_multi_dev(adam_list(m), lr, m->beta1, m->beta2, m->eps,
-                                              m->d_t, m->d_bc, st)
-                             : s1;
+            const mdg_status s2 = s1 == MDG_OK ? update(m, lr, st) : s1;
             const cudaError_t e = cudaStreamEndCapture(st, &g);
             const cudaError_t ei = (s2 == MDG_OK && e == cudaSuccess && g)
                                        ? cudaGraphInstantiate(&m->gexec, g, 0)
@@ -436,7 +476,7 @@ mdg_status mdg_model_po_step(mdg_model *m, const float *fixed, const float *movi
         return MDG_OK;
     }
     MD_TRY(mdg_model_loss_step(m, fixed, moving, 1, terms, nullptr, st));
-    return adam_multi_dev(adam_list(m), lr, m->beta1, m->beta2, m->eps, m->d_t, m->d_bc, st);
+    return update(m, lr, st);
 }
 
 }  // extern "C"

@@ -603,6 +603,121 @@ mdg_status project_bwd_launch(const ProjArgs &a0, const float *W, const float *b
     return MDG_OK;
 }
 
+// ------------------------------------------------- backward, K > 64
+// The large preset's coarse levels (K = S*hd up to 32*12 = 384) keep the
+// per-voxel values in global scratch instead of registers.  Simple and
+// deterministic (fixed loops, no atomics); these levels hold few voxels.
+// raw pre-norm values Y {K, n}
+__global__ void wide_raw_k(const float *__restrict__ in, const float *__restrict__ W,
+                           const float *__restrict__ b, int C, int K, int64_t n,
+                           float *__restrict__ Y) {
+    const int64_t i = (int64_t)blockIdx.x * kPB + threadIdx.x;
+    if (i >= (int64_t)K * n) return;
+    const int k = (int)(i / n);
+    const int64_t p = i - (int64_t)k * n;
+    float s = b[k];
+    for (int c = 0; c < C; ++c) s = fmaf(__ldg(W + (int64_t)k * C + c), __ldg(in + (int64_t)c * n + p), s);
+    Y[i] = s;
+}
+// per voxel (ops.hpp:470-493): Y <- xh, G <- graw (the pre-norm gradient)
+__global__ void wide_ln_bwd_k(float *__restrict__ Y, float *__restrict__ G,
+                              const float *__restrict__ gout, const float *__restrict__ gamma,
+                              int K, int64_t n, int planar, float eps) {
+    const int64_t p = (int64_t)blockIdx.x * kPB + threadIdx.x;
+    if (p >= n) return;
+    float mean = 0.0f;
+    for (int k = 0; k < K; ++k) mean += Y[(int64_t)k * n + p];
+    mean /= (float)K;
+    float var = 0.0f;
+    for (int k = 0; k < K; ++k) {
+        const float t = Y[(int64_t)k * n + p] - mean;
+        var = fmaf(t, t, var);
+    }
+    var /= (float)K;
+    const float inv = 1.0f / sqrtf(var + eps);
+    float sg = 0.0f, sgx = 0.0f;
+    for (int k = 0; k < K; ++k) {
+        const float xh = (Y[(int64_t)k * n + p] - mean) * inv;
+        const float go = gout[qk_index(planar, p, k, n, K)];
+        sg = fmaf(go, gamma[k], sg);
+        sgx = fmaf(go * gamma[k], xh, sgx);
+    }
+    const float mg = sg / (float)K, mgx = sgx / (float)K;
+    for (int k = 0; k < K; ++k) {
+        const float xh = (Y[(int64_t)k * n + p] - mean) * inv;
+        const float go = gout[qk_index(planar, p, k, n, K)];
+        Y[(int64_t)k * n + p] = xh;
+        G[(int64_t)k * n + p] = inv * (go * gamma[k] - mg - xh * mgx);
+    }
+}
+// gin[c] (+)= sum_k G[k] W[k,c]
+__global__ void wide_gin_k(const float *__restrict__ G, const float *__restrict__ W, int C, int K,
+                           int64_t n, float *__restrict__ gin, int set) {
+    const int64_t i = (int64_t)blockIdx.x * kPB + threadIdx.x;
+    if (i >= (int64_t)C * n) return;
+    const int c = (int)(i / n);
+    const int64_t p = i - (int64_t)c * n;
+    float s = 0.0f;
+    for (int k = 0; k < K; ++k) s = fmaf(G[(int64_t)k * n + p], __ldg(W + (int64_t)k * C + c), s);
+    gin[i] = set ? s : gin[i] + s;
+}
+// parameter gradients of one input (accumulated across the inputs in order):
+// gW[k,c] += sum_p G[k,p] in[c,p];  gb[k] += sum G;  ggamma += sum gout xh;
+// gbeta += sum gout.  One thread per (k, c) / per k, voxels in order.
+__global__ void wide_param_k(const float *__restrict__ G, const float *__restrict__ X,
+                             const float *__restrict__ in, const float *__restrict__ gout, int C,
+                             int K, int64_t n, int planar, float *__restrict__ gW,
+                             float *__restrict__ gb, float *__restrict__ gg,
+                             float *__restrict__ gbe) {
+    const int64_t i = (int64_t)blockIdx.x * kPB + threadIdx.x;
+    if (i < (int64_t)K * C && gW) {
+        const int k = (int)(i / C), c = (int)(i - (int64_t)k * C);
+        float s = 0.0f;
+        for (int64_t p = 0; p < n; ++p) s = fmaf(G[(int64_t)k * n + p], __ldg(in + (int64_t)c * n + p), s);
+        gW[i] += s;
+    }
+    if (i < K) {
+        const int k = (int)i;
+        float sb = 0.0f, sg = 0.0f, sbe = 0.0f;
+        for (int64_t p = 0; p < n; ++p) {
+            const float go = gout[qk_index(planar, p, k, n, K)];
+            sb += G[(int64_t)k * n + p];
+            sg = fmaf(go, X[(int64_t)k * n + p], sg);
+            sbe += go;
+        }
+        if (gb) gb[k] += sb;
+        if (gg) gg[k] += sg;
+        if (gbe) gbe[k] += sbe;
+    }
+}
+
+static mdg_status project_bwd_wide(const ProjArgs &a, const float *W, const float *b,
+                                   const float *g, float *gW, float *gb, float *gg, float *gbe,
+                                   cudaStream_t st) {
+    const int K = a.K, C = a.C;
+    const int64_t n = a.n;
+    Scratch ws;
+    MDG_CUDA_TRY(ws.alloc((size_t)2 * K * n * sizeof(float), st));
+    float *Y = ws.as<float>(), *G = Y + (int64_t)K * n;
+    for (int i = 0; i < a.ninputs; ++i) {
+        const float *in = a.in[i], *go = a.gout[i];
+        float *gi = a.gin[i];
+        wide_raw_k<<<grid1d((int64_t)K * n, kPB), kPB, 0, st>>>(in, W, b, C, K, n, Y);
+        MDG_LAUNCHED();
+        wide_ln_bwd_k<<<grid1d(n, kPB), kPB, 0, st>>>(Y, G, go, g, K, n, a.planar, a.eps);
+        MDG_LAUNCHED();
+        if (gi) {
+            wide_gin_k<<<grid1d((int64_t)C * n, kPB), kPB, 0, st>>>(G, W, C, K, n, gi,
+                                                                   (a.gin_set >> i) & 1);
+            MDG_LAUNCHED();
+        }
+        wide_param_k<<<grid1d((int64_t)K * C, kPB), kPB, 0, st>>>(G, Y, in, go, C, K, n,
+                                                                 a.planar, gW, gb, gg, gbe);
+        MDG_LAUNCHED();
+    }
+    return MDG_OK;
+}
+
 }  // namespace mdg
 
 using namespace mdg;
@@ -674,7 +789,6 @@ mdg_status project_qk_bwd_impl(const float *f, const float *m, int C, int64_t n,
     mdg_status s = check_proj(C, n, K, layout);
     if (s != MDG_OK) return s;
     if (n == 0) return MDG_OK;
-    MDG_REQUIRE(K <= 64, "project_qk_bwd: K > 64 not supported by the B200 path");
     MDG_REQUIRE(f && weight && bias && ln_g && gQ, "project_qk_bwd: null pointer");
     MDG_REQUIRE(!m == !gK, "project_qk_bwd: m and gK must both be given or both be NULL");
     ProjArgs a{};
@@ -692,8 +806,8 @@ mdg_status project_qk_bwd_impl(const float *f, const float *m, int C, int64_t n,
     a.planar = layout == MDG_QK_PLANAR;
     a.gin_set = gin_set;
     cudaStream_t st = stream;
-    MDG_REQUIRE(proj_smem_bytes(K, C) <= 200 * 1024,
-                "project_qk_bwd: C * K too large for the shared-memory weight block");
+    if (K > 64 || proj_smem_bytes(K, C) > 200 * 1024)
+        return project_bwd_wide(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
     // K == 6 (head_dim 6, one head: the fine levels) gets an exact instantiation
     if (K == 6) return project_bwd_launch<6, 8, true>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);
     if (K <= 8) return project_bwd_launch<8, 8, false>(a, weight, bias, ln_g, gweight, gbias, gln_g, gln_b, st);

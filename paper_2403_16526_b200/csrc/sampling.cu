@@ -231,21 +231,25 @@ __device__ __forceinline__ void xmerge_row(int r, bool ok, bool &in, bool &out) 
     in = lane > 0 && ok && up == key;
     out = __shfl_down_sync(0xffffffffu, (int)in, 1) != 0 && lane < 31;
 }
+// predicated fp32 reduction: no branch around each scatter target
+__device__ __forceinline__ void red_if(float *a, float v, bool p) {
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q red.global.add.f32 [%0], %1;\n}\n" ::"l"(a),
+        "f"(v), "r"((int)p)
+        : "memory");
+}
 __device__ __forceinline__ void scatter_row2(float *ia, float *ib, bool two, bool ok, int r,
                                              float2 t0, float2 t1, bool in, bool out) {
     const float nx = __shfl_up_sync(0xffffffffu, t1.x, 1);
     const float ny = __shfl_up_sync(0xffffffffu, t1.y, 1);
-    if (in) {
-        t0.x += nx;
-        t0.y += ny;
-    }
-    if (ok) {
-        atomicAdd(ia + r, t0.x);
-        if (!out) atomicAdd(ia + r + 1, t1.x);
-        if (two) {
-            atomicAdd(ib + r, t0.y);
-            if (!out) atomicAdd(ib + r + 1, t1.y);
-        }
+    t0.x = in ? t0.x + nx : t0.x;
+    t0.y = in ? t0.y + ny : t0.y;
+    float *a = ia + r, *b = ib + r;
+    red_if(a, t0.x, ok);
+    red_if(a + 1, t1.x, ok && !out);
+    if (two) {
+        red_if(b, t0.y, ok);
+        red_if(b + 1, t1.y, ok && !out);
     }
 }
 

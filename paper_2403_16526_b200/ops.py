@@ -845,6 +845,20 @@ class Model:
         return loss_trace, dice_trace, phi
 
 
+def init_model_cfg(config, seed=42):
+    """init_model(cfg, seed) (engine.hpp:143-166) for any model_config(...) by
+    libmdg on the host: the ModelParams::all_tensors list (CPU tensors),
+    bit-identical to the reference."""
+    L = _capi.lib()
+    nt = C.c_int()
+    sizes = (C.c_int64 * 128)()
+    L.mdg_config_param_count(C.byref(config), C.byref(nt), sizes)
+    out = [torch.empty(int(sizes[i]), dtype=torch.float32) for i in range(nt.value)]
+    ptrs = (C.c_void_p * nt.value)(*[t.data_ptr() for t in out])
+    _check(L.mdg_model_init_cfg(C.byref(config), seed, ptrs))
+    return out
+
+
 def init_model_native(seed=42):
     """mdg_model_init: init_model(small_preset, seed) drawn by libmdg on the
     host (no device needed); the same 75 tensors as init_model()."""
@@ -883,14 +897,20 @@ class NativeModel:
     underneath.  Same contract as Model; `tensors` are the 75 device
     parameters (updated in place by po_step)."""
 
-    def __init__(self, tensors, dims, loss: LossConfig = None, check_finite=False):
+    def __init__(self, tensors, dims, loss: LossConfig = None, check_finite=False, config=None,
+                 optimizer="adam"):
+        """config: a model_config(...) (default: the small preset);
+        optimizer: "adam" (AdamOptimizer) or "sgd" (sgd_step), engine.hpp:80."""
         self._L = _capi.lib()
         self.tensors = list(tensors)
-        if len(self.tensors) != 75:
-            raise InvalidInput("model: expects the 75 ModelParams tensors")
+        self.config = config if config is not None else model_config()
+        if optimizer not in ("adam", "sgd"):
+            raise InvalidInput("model: optimizer must be 'adam' or 'sgd'")
         nt = C.c_int()
         sizes = (C.c_int64 * 128)()
-        self._L.mdg_model_param_count(C.byref(nt), sizes)
+        self._L.mdg_config_param_count(C.byref(self.config), C.byref(nt), sizes)
+        if len(self.tensors) != nt.value:
+            raise InvalidInput(f"model: expects the {nt.value} ModelParams tensors")
         for i, t in enumerate(self.tensors):
             _ptr(t, f"model tensor {i}")
             if t.numel() != sizes[i]:
@@ -898,10 +918,12 @@ class NativeModel:
                                    f"expects {sizes[i]}")
         self.dims = tuple(int(v) for v in dims)
         lc = loss or LossConfig()
-        ptrs = (C.c_void_p * 75)(*[_ptr(t) for t in self.tensors])
+        ptrs = (C.c_void_p * len(self.tensors))(*[_ptr(t) for t in self.tensors])
         h = C.c_void_p()
-        _check(self._L.mdg_model_create(dims3(dims), ptrs, float(lc.lam), int(lc.ncc_window),
-                                        1 if check_finite else 0, C.byref(h)))
+        _check(self._L.mdg_model_create_cfg(C.byref(self.config), dims3(dims), ptrs,
+                                            float(lc.lam), int(lc.ncc_window),
+                                            1 if check_finite else 0,
+                                            0 if optimizer == "adam" else 1, C.byref(h)))
         self._h = h
         n = voxel_count(self.dims)
         dev = self.tensors[0].device
@@ -938,8 +960,8 @@ class NativeModel:
         return self._terms.clone(), self._phi.clone()
 
     def po_step(self, fixed, moving, lr=1e-4, graph=True):
-        """loss + backward + Adam; graph=True replays the iteration as one
-        CUDA graph (mdg_model_po_step).  Returns (terms, phi)."""
+        """loss + backward + the optimizer update; graph=True replays the
+        iteration as one CUDA graph (mdg_model_po_step).  Returns (terms, phi)."""
         self._check_images(fixed, moving)
         if not graph:
             terms, phi = self.loss_step(fixed, moving, backward=True)
