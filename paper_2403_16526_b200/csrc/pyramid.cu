@@ -81,8 +81,6 @@ mdg_status validate(const mdg_pyramid_config &c) {
         MDG_REQUIRE(c.channels[k] >= 1, "pyramid: feature channels must be >= 1");
         MDG_REQUIRE(dims_ok(c.dims[k]) && nvox(c.dims[k]) > 0,
                     "pyramid: invalid level dims " + dims_str(c.dims[k]));
-        MDG_REQUIRE(c.heads[k] * c.head_dim <= 64,
-                    "pyramid: S*head_dim > 64 is not supported by the B200 projection");
         if (k > 0) {
             const mdg_dims3 a = c.dims[k - 1], b = c.dims[k];
             // check_upsample_target (sampling.hpp:266-271)
