@@ -372,3 +372,41 @@ def test_po_traces_repeatable(cuda, ref, deterministic):
                 tr.append(float(t[0]))
             traces.append(tr)
         assert traces[0] == traces[1], (graph, traces)
+
+
+@pytest.mark.slow
+def test_config2_registration_forward_160x192x160(cuda, ref):
+    """BASELINE config 2: the registration forward (encoder x2 -> 5-level ModeT
+    pyramid with RegHead and warps -> loss) on the synthetic LPBA-shaped pair
+    make_synth_pair(160x192x160, seed 1), init_model(small, 42), native driver
+    vs the reference run_loss_step forward (oracle/_ref).
+
+    * the deformation elementwise within the north star's flow tolerance
+      1e-5 + 1e-4|ref| everywhere (init_model's RegHead weights are N(0, 1e-5),
+      so the forward field is ~1e-7 voxel: a relative-norm check on it would
+      measure cancellation noise, ~4e-3 at this size);
+    * the reference's own loss evaluated on OUR deformation equals its loss on
+      its deformation to 1e-5 (the field is equivalent for the objective);
+    * the warped-label Dice within 1e-3;
+    * our loss value vs the reference's within 2e-3: the reference's mean
+      (op_sum_all, tape.hpp:247-251) adds 4.9M terms sequentially in fp32, so
+      its own rounding error at this size is ~1e-3 (at 32^3 the two agree to
+      1e-6, test_full_loss_step_matches_reference); ours is a tree reduction."""
+    dims = (160, 192, 160)
+    f, m, lf, lm, _ = ref.synth_pair(dims, seed=1, max_disp=2.0)
+    packed, sizes = ref.model_params(42)
+    loss_r, _, phi_r = ref.loss_step(f, m, packed, grads=False)
+    nat = ops.NativeModel(device_tensors(packed, sizes), dims)
+    terms, phi = nat.loss_step(torch.from_numpy(f).cuda(), torch.from_numpy(m).cuda(),
+                               backward=False)
+    torch.cuda.synchronize()
+    phi_g = phi.cpu().numpy()
+    print("loss", float(terms[0]), loss_r, "phi rel", rel_norm(phi_g, phi_r), "max |d|",
+          np.abs(phi_g - phi_r).max(), "max |phi|", np.abs(phi_r).max())
+    assert np.all(np.abs(phi_g - phi_r) <= 1e-5 + 1e-4 * np.abs(phi_r))
+    terms_r_on_g = ref.total_loss(f, m, phi_g, window=9, lam=1.0, grads=False)[0]
+    assert abs(float(terms_r_on_g[0]) - loss_r) <= 1e-5 * abs(loss_r), (terms_r_on_g, loss_r)
+    dg = ref.mean_dice(lf, ref.warp_labels(lm, phi_g))
+    dr = ref.mean_dice(lf, ref.warp_labels(lm, phi_r))
+    assert abs(dg - dr) <= 1e-3, (dg, dr)
+    assert abs(float(terms[0]) - loss_r) <= 2e-3 * abs(loss_r), (float(terms[0]), loss_r)
