@@ -43,6 +43,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "mdg_common.cuh"
@@ -1302,6 +1303,328 @@ modet_bwd_fused_k(const __grid_constant__ Maps maps, const float *__restrict__ B
     }
 }
 
+// ------------------------------------------- bwd: single pass, 2 CTAs / SM
+// modet_bwd_fused2_k — the single-pass backward of modet_bwd_fused_k with
+// the source ring folded into the 8 tile warps as uniform extra work, so the
+// kernel fits two CTAs per SM (<= 128 registers, ~110 KB shared):
+//   * each step the 84 ring sources' records (Q*log2e, LSE, gSF, gSF.SF) of
+//     the entering plane go to a 3-plane shared ring buffer;
+//   * the 236 (ring source, tile key) pairs — top / bottom rows (dy = +-1,
+//     dx = -1..1) and left / right columns (dx = +-1, dy = -1..1) — are one
+//     per thread: 3 logits (the three in-flight planes), their summed key
+//     contribution into a per-pair slot;
+//   * a key adds, in a fixed order: the row above (y exchange), its own row
+//     (x shuffles), the row below, then its ring pairs.
+// Interior work runs one window column (dx) at a time: K strip, three slots,
+// then the x-shuffle of that column's key contribution (6 + 6 live floats
+// instead of 18 + 18).  Two block barriers per step; the exchange buffers are
+// double-buffered by step parity.  Deterministic (no atomics).
+constexpr int kNPair = 236, kNRing = 84;
+
+template <int D>
+struct FG2 {
+    static constexpr int D2 = (D + 1) / 2;
+    static constexpr int BUF = (2 * D + 7) * kFBox;          // K box (p) + own box (p+1)
+    static constexpr int YX = 2 * 2 * D2 * RTY * RTX;        // float2 [par][dir][pair][row][x]
+    static constexpr int RC = 2 * kNPair * D2;               // float2 [par][pair][c]
+    static constexpr int RR = 3 * kNRing * 12;               // float  [slot][ring][12]
+    static constexpr size_t SMEM = ((size_t)2 * BUF + 2 * YX + 2 * RC + RR + 32) * 4 + 16;
+};
+
+// box position (row, column) of ring source r
+__device__ __forceinline__ void ring_pos(int r, int &br, int &bc) {
+    if (r < 32) {
+        br = 0;
+        bc = r + 4;
+    } else if (r < 64) {
+        br = 9;
+        bc = r - 32 + 4;
+    } else if (r < 74) {
+        br = r - 64;
+        bc = 3;
+    } else {
+        br = r - 74;
+        bc = 36;
+    }
+}
+
+// pair t -> (ring source r, key lane kx, key row ky, dx, dy)
+__device__ __forceinline__ bool pair_of(int t, int &r, int &kx, int &ky, int &dx, int &dy) {
+    if (t < 188) {  // top (t < 94) / bottom rows, key-major, dx = -1, 0, +1
+        const bool bot = t >= 94;
+        const int u = bot ? t - 94 : t;
+        if (u < 2) {
+            kx = 0;
+            dx = u - 1;
+        } else if (u < 92) {
+            kx = 1 + (u - 2) / 3;
+            dx = (u - 2) % 3 - 1;
+        } else {
+            kx = 31;
+            dx = u - 92;
+        }
+        ky = bot ? RTY - 1 : 0;
+        dy = bot ? -1 : 1;
+        r = (bot ? 32 : 0) + kx - dx;
+        return true;
+    }
+    if (t < kNPair) {  // left (t < 212) / right columns, key-major, dy = -1, 0, +1
+        const bool right = t >= 212;
+        const int u = right ? t - 212 : t - 188;
+        ky = u / 3;
+        dy = u % 3 - 1;
+        kx = right ? 31 : 0;
+        dx = right ? -1 : 1;
+        r = (right ? 74 : 64) + (ky - dy) + 1;  // source row ky - dy, box row + 1
+        return true;
+    }
+    return false;
+}
+
+template <int D, bool ACC>
+__global__ void __launch_bounds__(256, 2)
+modet_bwd_fused2_k(const __grid_constant__ Maps maps, const float *__restrict__ B, Vol v, int zc,
+                   float *__restrict__ gQ, float *__restrict__ gK, float *__restrict__ gBpart) {
+    using G = FG2<D>;
+    constexpr int D2 = G::D2;
+    extern __shared__ __align__(128) float smem[];
+    float2 *ybuf = reinterpret_cast<float2 *>(smem + 2 * G::BUF);
+    float2 *rcon = ybuf + G::YX;
+    float *rrec = reinterpret_cast<float *>(rcon + G::RC);
+    float *sB = rrec + G::RR;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sB + 32);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int x0 = blockIdx.x * RTX, y0 = blockIdx.y * RTY;
+    const int nzc = (v.l + zc - 1) / zc;
+    const int s = blockIdx.z / nzc;
+    const int zb = (blockIdx.z - s * nzc) * zc, ze = min(zb + zc, v.l);
+    const int64_t so = (int64_t)s * v.n;
+    if (threadIdx.x < 27) sB[threadIdx.x] = B[s * 27 + threadIdx.x] * (0.5f * kLog2e);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fused_stage<D>(smem, maps, &bar[0], zb - 2, x0, y0, s);
+        fused_stage<D>(smem + G::BUF, maps, &bar[1], zb - 1, x0, y0, s);
+    }
+    const int x = x0 + lane, y = y0 + wid;
+    const bool in_xy = x < v.h && y < v.w;
+    const int pos = (wid + 1) * kBoxX + lane + 4;  // own box position of this column
+    // this thread's ring pair (t < 236) and the ring source it records (t < 84)
+    int pr = 0, pkx = 0, pky = 0, pdx = 0, pdy = 0;
+    const bool has_pair = pair_of(threadIdx.x, pr, pkx, pky, pdx, pdy);
+    int rbr = 0, rbc = 0;
+    if (threadIdx.x < kNRing) ring_pos(threadIdx.x, rbr, rbc);
+    const int rsx = x0 - 4 + rbc, rsy = y0 - 1 + rbr;
+    const bool rin = threadIdx.x < kNRing && rsx >= 0 && rsx < v.h && rsy >= 0 && rsy < v.w;
+    Src<D> S[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+#pragma unroll
+        for (int c = 0; c < D2; ++c) S[j].q[c] = S[j].dq[c] = f2(0.0f, 0.0f);
+        S[j].Lh = INFINITY;
+        S[j].gx = S[j].gy = S[j].gz = S[j].dot = S[j].mask = 0.0f;
+    }
+    float db[27];
+#pragma unroll
+    for (int o = 0; o < 27; ++o) db[o] = 0.0f;
+    float *gQh = gQ ? gQ + so * D : nullptr;
+    float *gKh = gK ? gK + so * D : nullptr;
+    for (int p = zb - 2; p <= ze; ++p) {
+        const int j = p - (zb - 2), b = j & 1, par = j & 1;
+        mbar_wait(&bar[b], (j >> 1) & 1);
+        const float *buf = smem + b * G::BUF;
+        const float *own = buf + D * kFBox;
+        const int z = p + 1;  // plane entering the window
+        const bool zok = z >= 0 && z >= zb - 1 && z <= ze && z < v.l;
+        src_load<D>(S[0], own, pos, in_xy && zok, in_xy && zok && z >= zb && z < ze);
+        // ring record slot of plane q: (q - zb + 3) mod 3
+        if (threadIdx.x < kNRing) {
+            float *rec = rrec + ((z - zb + 3) % 3) * kNRing * 12 + threadIdx.x * 12;
+            const int bp = rbr * kBoxX + rbc;
+#pragma unroll
+            for (int c = 0; c < D; ++c) rec[c] = own[c * kFBox + bp] * kLog2e;
+            const float gx = own[(D + 1) * kFBox + bp], gy = own[(D + 2) * kFBox + bp],
+                        gz = own[(D + 3) * kFBox + bp];
+            rec[D] = rin && zok ? own[D * kFBox + bp] * (0.5f * kLog2e) : INFINITY;
+            rec[D + 1] = gx;
+            rec[D + 2] = gy;
+            rec[D + 3] = gz;
+            rec[D + 4] = gx * own[(D + 4) * kFBox + bp] + gy * own[(D + 5) * kFBox + bp] +
+                         gz * own[(D + 6) * kFBox + bp];
+        }
+        const bool work = p >= zb - 1;
+        float2 ownk[D2];
+        if (work) {
+#pragma unroll
+            for (int dyi = 0; dyi < 3; ++dyi) {
+                float2 R[D2];
+#pragma unroll
+                for (int c = 0; c < D2; ++c) R[c] = f2(0.0f, 0.0f);
+                const int kpos = (wid + dyi) * kBoxX + lane + 3;
+#pragma unroll
+                for (int dxi = 0; dxi < 3; ++dxi) {
+                    float2 kr[D2], cc[D2];
+#pragma unroll
+                    for (int c = 0; c < D2; ++c)
+                        kr[c] = f2(buf[(2 * c) * kFBox + kpos + dxi],
+                                   2 * c + 1 < D ? buf[(2 * c + 1) * kFBox + kpos + dxi] : 0.0f);
+#pragma unroll
+                    for (int jj = 0; jj < 3; ++jj) {
+                        Src<D> &sr = S[jj];
+                        const int dz = jj - 1;
+                        float cf = -sr.dot;
+                        if (dz > 0) cf += sr.gz;
+                        if (dz < 0) cf -= sr.gz;
+                        if (dyi == 0) cf -= sr.gy;
+                        if (dyi == 2) cf += sr.gy;
+                        if (dxi == 0) cf -= sr.gx;
+                        if (dxi == 2) cf += sr.gx;
+                        const int o = (dz + 1) * 9 + dyi * 3 + dxi;
+                        const float dl = dl_of<D>(sr, kr, sB[o], cf);
+                        const float2 dl2 = dup2(dl);
+                        db[o] = fmaf(dl, sr.mask, db[o]);
+#pragma unroll
+                        for (int c = 0; c < D2; ++c) {
+                            sr.dq[c] = fma2(dl2, kr[c], sr.dq[c]);
+                            cc[c] = jj == 0 ? mul2(dl2, sr.q[c]) : fma2(dl2, sr.q[c], cc[c]);
+                        }
+                    }
+                    // the column's key contribution: dx = -1 goes to lane-1,
+                    // dx = +1 to lane+1 (fixed order: dx = -1, 0, +1)
+#pragma unroll
+                    for (int c = 0; c < D2; ++c) {
+                        float2 t = cc[c];
+                        if (dxi == 0) {
+                            t.x = __shfl_down_sync(0xffffffffu, t.x, 1);
+                            t.y = __shfl_down_sync(0xffffffffu, t.y, 1);
+                            if (lane == 31) t = f2(0.0f, 0.0f);
+                        } else if (dxi == 2) {
+                            t.x = __shfl_up_sync(0xffffffffu, t.x, 1);
+                            t.y = __shfl_up_sync(0xffffffffu, t.y, 1);
+                            if (lane == 0) t = f2(0.0f, 0.0f);
+                        }
+                        R[c] = add2(R[c], t);
+                    }
+                }
+                if (dyi == 1) {
+#pragma unroll
+                    for (int c = 0; c < D2; ++c) ownk[c] = R[c];
+                } else if (dyi == 0 && wid >= 1) {  // keys of row wid-1, from below
+#pragma unroll
+                    for (int c = 0; c < D2; ++c)
+                        ybuf[(((par * 2 + 1) * D2 + c) * RTY + wid - 1) * RTX + lane] = R[c];
+                } else if (dyi == 2 && wid <= RTY - 2) {  // keys of row wid+1, from above
+#pragma unroll
+                    for (int c = 0; c < D2; ++c)
+                        ybuf[(((par * 2 + 0) * D2 + c) * RTY + wid + 1) * RTX + lane] = R[c];
+                }
+            }
+        }
+        __syncthreads();  // (A) y exchange and the entering plane's ring records
+        if (work && has_pair) {
+            // the pair's three logits (the in-flight planes p+1, p, p-1)
+            const int kp = (pky + 1) * kBoxX + pkx + 4;
+            float2 k[D2];
+#pragma unroll
+            for (int c = 0; c < D2; ++c)
+                k[c] = f2(buf[(2 * c) * kFBox + kp], 2 * c + 1 < D ? buf[(2 * c + 1) * kFBox + kp] : 0.0f);
+            float2 acc[D2];
+#pragma unroll
+            for (int jj = 0; jj < 3; ++jj) {
+                const int zz = p + 1 - jj, dz = jj - 1;
+                const float *rec = rrec + ((zz - zb + 3) % 3) * kNRing * 12 + pr * 12;
+                Src<D> sr;
+#pragma unroll
+                for (int c = 0; c < D2; ++c)
+                    sr.q[c] = f2(rec[2 * c], 2 * c + 1 < D ? rec[2 * c + 1] : 0.0f);
+                sr.Lh = rec[D];
+                const float cf = -rec[D + 4] + (float)pdx * rec[D + 1] + (float)pdy * rec[D + 2] +
+                                 (float)dz * rec[D + 3];
+                const int o = (dz + 1) * 9 + (pdy + 1) * 3 + (pdx + 1);
+                const float dl = dl_of<D>(sr, k, sB[o], cf);
+                const float2 dl2 = dup2(dl);
+#pragma unroll
+                for (int c = 0; c < D2; ++c)
+                    acc[c] = jj == 0 ? mul2(dl2, sr.q[c]) : fma2(dl2, sr.q[c], acc[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < D2; ++c) rcon[(par * kNPair + threadIdx.x) * D2 + c] = acc[c];
+        }
+        __syncthreads();  // (B) ring contributions; the stage buffer is free
+        if (threadIdx.x == 0 && p + 2 <= ze) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            fused_stage<D>(smem + b * G::BUF, maps, &bar[b], p + 2, x0, y0, s);
+        }
+        if (in_xy && p >= zb && p < ze && gKh) {
+            const int64_t off = (int64_t)p * v.hw + (int64_t)y * v.h + x;
+            // ring pair ids feeding this key (key-major enumeration of pair_of)
+            const int tb = lane == 0 ? 0 : (lane == 31 ? 92 : 2 + 3 * (lane - 1));
+            const int tn = (lane == 0 || lane == 31) ? 2 : 3;
+#pragma unroll
+            for (int c = 0; c < D2; ++c) {
+                float2 t = ownk[c];
+                if (wid >= 1) t = add2(ybuf[(((par * 2 + 0) * D2 + c) * RTY + wid) * RTX + lane], t);
+                if (wid <= RTY - 2) t = add2(t, ybuf[(((par * 2 + 1) * D2 + c) * RTY + wid) * RTX + lane]);
+                if (wid == 0)
+                    for (int i = 0; i < tn; ++i) t = add2(t, rcon[(par * kNPair + tb + i) * D2 + c]);
+                if (wid == RTY - 1)
+                    for (int i = 0; i < tn; ++i) t = add2(t, rcon[(par * kNPair + 94 + tb + i) * D2 + c]);
+                if (lane == 0)
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) t = add2(t, rcon[(par * kNPair + 188 + 3 * wid + i) * D2 + c]);
+                if (lane == 31)
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) t = add2(t, rcon[(par * kNPair + 212 + 3 * wid + i) * D2 + c]);
+                t = mul2(t, dup2(kLn2));  // contributions carry Q * log2e
+                float *d0 = gKh + (int64_t)(2 * c) * v.n + off;
+                *d0 = ACC ? *d0 + t.x : t.x;
+                if (2 * c + 1 < D) {
+                    float *d1 = d0 + v.n;
+                    *d1 = ACC ? *d1 + t.y : t.y;
+                }
+            }
+        }
+        if (in_xy && p - 1 >= zb && p - 1 < ze && gQh) {
+            const int64_t off = (int64_t)(p - 1) * v.hw + (int64_t)y * v.h + x;
+#pragma unroll
+            for (int c = 0; c < D2; ++c) {
+                float *d0 = gQh + (int64_t)(2 * c) * v.n + off;
+                *d0 = ACC ? *d0 + S[2].dq[c].x : S[2].dq[c].x;
+                if (2 * c + 1 < D) {
+                    float *d1 = d0 + v.n;
+                    *d1 = ACC ? *d1 + S[2].dq[c].y : S[2].dq[c].y;
+                }
+            }
+        }
+        S[2] = S[1];
+        S[1] = S[0];
+    }
+    // dB: per-CTA partial (fixed order)
+    __syncthreads();
+    float *red = smem;
+#pragma unroll
+    for (int o = 0; o < 27; ++o) {
+        float a = db[o];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
+        if (lane == 0) red[wid * 27 + o] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x < 27) {
+        float a = 0.0f;
+#pragma unroll
+        for (int i = 0; i < RTY; ++i) a += red[i * 27 + threadIdx.x];
+        const int cta = (blockIdx.z - s * nzc) * gridDim.x * gridDim.y + blockIdx.y * gridDim.x +
+                        blockIdx.x;
+        const int ncta = nzc * gridDim.x * gridDim.y;
+        gBpart[((int64_t)s * ncta + cta) * 27 + threadIdx.x] = a;
+    }
+}
+
 // deterministic final reduction of per-CTA dB partials (fixed order tree)
 __global__ void __launch_bounds__(256)
 reduce_db_k(const float *__restrict__ part, int nparts, float *__restrict__ gB) {
@@ -1425,6 +1748,22 @@ static void col_launch(dim3 g, size_t sm, cudaStream_t st, const Maps &m, const 
     modet_bwd_col_k<D, TMA, ACC><<<g, 256, sm, st>>>(m, Q, K, B, SF, LSE, gSF, v, zc, gK, aux);
 }
 
+// which backward: MDG_MODET_BWD = "two" (row + column kernels, the default:
+// fastest measured), "fused1" (single pass, ring warps) or "fused2" (single
+// pass, ring folded into the tile warps, 2 CTAs / SM).  At 160x192x224, S=1,
+// d=6 (r02): two 0.456 ms, fused1 0.48-0.51, fused2 0.56.
+static int bwd_variant() {
+    static const int v = [] {
+        const char *e = std::getenv("MDG_MODET_BWD");
+        if (!e) return 0;
+        if (!std::strcmp(e, "two")) return 0;
+        if (!std::strcmp(e, "fused1")) return 1;
+        if (!std::strcmp(e, "fused2")) return 2;
+        return 0;
+    }();
+    return v;
+}
+
 template <int D, bool ACC>
 static void fused_launch(dim3 g, size_t sm, cudaStream_t st, const Maps &m, const float *B,
                          const Vol &v, int zc, float *gQ, float *gK, float *part) {
@@ -1440,9 +1779,7 @@ static bool bwd_fused(const float *Q, const float *K, const float *B, const floa
     if constexpr (D > 6) {
         return false;
     } else {
-        // opt-in: measured slower than the two-pass kernels at 160x192x224
-        // (0.48-0.51 vs 0.456 ms), kept for the next iteration
-        if (!std::getenv("MDG_MODET_BWD_FUSED")) return false;
+        if (bwd_variant() != 1) return false;
         Maps m{};
         if (!(make_map(&m.k, K, v, S * D, kBoxX, kFRows) &&
               make_maps_a(&m.a, Q, LSE, gSF, SF, v, S, D, kBoxX, kFRows)))
@@ -1470,6 +1807,46 @@ static bool bwd_fused(const float *Q, const float *K, const float *B, const floa
     }
 }
 
+template <int D, bool ACC>
+static void fused2_launch(dim3 g, size_t sm, cudaStream_t st, const Maps &m, const float *B,
+                          const Vol &v, int zc, float *gQ, float *gK, float *part) {
+    set_smem(modet_bwd_fused2_k<D, ACC>, sm);
+    modet_bwd_fused2_k<D, ACC><<<g, 256, sm, st>>>(m, B, v, zc, gQ, gK, part);
+}
+
+template <int D>
+static bool bwd_fused2(const float *Q, const float *K, const float *B, const float *SF,
+                       const float *LSE, const float *gSF, const Vol &v, int S, bool acc,
+                       float *gQ, float *gK, float *gB, cudaStream_t st, cudaError_t *err) {
+    if constexpr (D > 6) {
+        return false;
+    } else {
+        Maps m{};
+        if (!(make_map(&m.k, K, v, S * D, kBoxX, kFRows) &&
+              make_maps_a(&m.a, Q, LSE, gSF, SF, v, S, D, kBoxX, kFRows)))
+            return false;
+        const int gx = (v.h + RTX - 1) / RTX, gy = (v.w + RTY - 1) / RTY;
+        const int zc = pick_zc(gx * gy * S, v.l, 2, 4);
+        const int nzc = (v.l + zc - 1) / zc;
+        const int ncta = gx * gy * nzc;
+        const size_t sm = FG2<D>::SMEM;
+        float *part = nullptr;
+        keep_pool_mapped();
+        if ((*err = cudaMallocAsync(&part, (size_t)S * ncta * 27 * sizeof(float), st))) return true;
+        const dim3 g(gx, gy, S * nzc);
+        if (acc) fused2_launch<D, true>(g, sm, st, m, B, v, zc, gQ, gK, part);
+        else fused2_launch<D, false>(g, sm, st, m, B, v, zc, gQ, gK, part);
+        g_launches.fetch_add(1);
+        if (gB) {
+            reduce_db_k<<<dim3(27, S), 256, 0, st>>>(part, ncta, gB);
+            g_launches.fetch_add(1);
+        }
+        cudaFreeAsync(part, st);
+        *err = cudaPeekAtLastError();
+        return true;
+    }
+}
+
 template <int D>
 static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, const float *SF,
                               const float *LSE, const float *gSF, mdg_dims3 d, int S, bool acc,
@@ -1477,6 +1854,9 @@ static cudaError_t bwd_launch(const float *Q, const float *K, const float *B, co
     const Vol v{d.h, d.w, d.l, (int64_t)d.h * d.w * d.l, (int64_t)d.h * d.w};
     const bool tma = tma_ok(v, {Q, K, SF, LSE, gSF});
     cudaError_t e = cudaSuccess;
+    if (tma && bwd_variant() == 2 &&
+        bwd_fused2<D>(Q, K, B, SF, LSE, gSF, v, S, acc, gQ, gK, gB, st, &e))
+        return e;
     if (tma && bwd_fused<D>(Q, K, B, SF, LSE, gSF, v, S, acc, gQ, gK, gB, st, &e)) return e;
     // the row kernel always runs when dK is wanted: it writes the per-source
     // statistics {LSE*log2e, gSF.SF} the column kernel gathers

@@ -461,3 +461,40 @@ def test_two_streams_same_device_fixup_isolated(cuda, oracle):
         SF, _ = ops.modet_fwd(Q1, K1, B1, d1, cfg, layout=MDG_QK_PLANAR)
     torch.cuda.synchronize()
     assert rel_close(host(SF), SF1, FLOW_ATOL, FLOW_RTOL)
+
+
+@pytest.mark.parametrize("variant", ["fused1", "fused2"])
+@pytest.mark.parametrize("dims,S,hd", [((33, 17, 9), 1, 6), ((65, 3, 31), 2, 6), ((20, 24, 28), 4, 6),
+                                       ((10, 12, 14), 2, 3), ((32, 16, 13), 1, 5)])
+def test_single_pass_backward_variants(cuda, oracle, variant, dims, S, hd):
+    """The single-pass ModeT backward kernels (MDG_MODET_BWD=fused1 / fused2:
+    one logit evaluation per (source, window slot), the tile's source ring
+    recomputed in-CTA, no atomics) against the oracle, in subprocesses since
+    the variant is fixed at first use."""
+    import subprocess
+    import sys
+
+    code = f"""
+import sys, numpy as np, torch
+sys.path[:0] = {[os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)), os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle")]!r}
+import pyoracle
+from _util import f32, random_qk
+from test_gpu_modet import oracle_modet, run_fused, grad_ok, rel_close
+from paper_2403_16526_b200._capi import MDG_QK_PLANAR
+dims, S, hd = {dims!r}, {S}, {hd}
+n = dims[0] * dims[1] * dims[2]
+seed = sum(dims) * 5 + S + hd
+Q = random_qk(dims, S * hd, seed); K = random_qk(dims, S * hd, seed + 1)
+B = f32(pyoracle.Rng(seed + 2).normal(S * 27).reshape(S, 27))
+gSF = f32(pyoracle.Rng(seed + 3).normal(3 * S * n).reshape(3 * S, dims[2], dims[1], dims[0]))
+W0, SF0, gQ0, gK0, gB0 = oracle_modet(pyoracle.mdo(), Q, K, B, dims, S, hd, gSF)
+for acc in (False, True):
+    W, SF, LSE, gQ, gK, gB = run_fused(Q, K, B, dims, S, hd, gSF, MDG_QK_PLANAR, acc)
+    assert grad_ok(gQ, gQ0) and grad_ok(gK, gK0), acc
+    assert grad_ok(gB, gB0, 1e-4 if not acc else 1e-3), acc
+print("ok")
+"""
+    env = dict(os.environ, MDG_MODET_BWD=variant)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
