@@ -43,7 +43,9 @@ def peak():
 
 
 def short(name):
-    return re.sub(r"^void ", "", name).split("(")[0].split("<")[0].split("::")[-1]
+    name = re.sub(r"^void ", "", name).replace("(anonymous namespace)::", "")
+    name = name.replace("<unnamed>::", "")
+    return name.split("(")[0].split("<")[0].split("::")[-1]
 
 
 def launches(path):
@@ -95,18 +97,19 @@ def full_rows(d):
         r = list(csv.reader(io.StringIO(raw)))
         if len(r) < 3:
             continue
-        h, v = r[0], r[2]
+        h, u, v = r[0], r[1], r[2]
 
         def g(n):
             try:
-                return float(v[h.index(n)].replace(",", ""))
+                i = h.index(n)
+                return float(v[i].replace(",", "")) * SCALE.get(u[i], 1.0)
             except (ValueError, IndexError):
                 return float("nan")
         rows.append((short(v[h.index("Kernel Name")]), g("launch__registers_per_thread"),
                      g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                      g("sm__warps_active.avg.per_cycle_active"),
                      g("l1tex__throughput.avg.pct_of_peak_sustained_active"),
-                     g("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+                     g("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                      g("smsp__inst_executed.sum") * 32 / NVOX,
                      (g("dram__bytes_read.sum") + g("dram__bytes_write.sum")) / 1e6))
     return rows
