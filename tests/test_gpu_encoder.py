@@ -242,7 +242,45 @@ def test_po_main_cli_runs():
     out = subprocess.run([exe, "32", "32", "32", "--iters", "4", "--quiet"], check=True,
                          capture_output=True, text=True, timeout=300).stdout
     rec = json.loads(out.strip().splitlines()[-1])
-    assert rec["iters"] == 4 and rec["params"] > 0 and rec["launches"] > 0
+    assert rec["iters"] == 4 and rec["params"] > 0 and rec["launches_rank0"] > 0
+    # other configs / optimizer from C++: large preset, scaling-and-squaring, SGD
+    for flags in (["--large"], ["--diffeomorphic", "--sgd"], ["--gather", "nccl"]):
+        out = subprocess.run([exe, "16", "16", "16", "--iters", "2", "--quiet", *flags],
+                             check=True, capture_output=True, text=True, timeout=300).stdout
+        rec = json.loads(out.strip().splitlines()[-1])
+        assert all(r["loss_final"] == r["loss_final"] for r in rec["results"]), flags
+
+
+def test_po_main_pair_parallel_shards_and_gathers(tmp_path, ref):
+    """Config 5 from C++ alone: 5 synthetic pairs sharded round-robin over two
+    ranks (two processes; here they share the one GPU, so the results gather
+    through files instead of NCCL), 10 updates each; every pair reported
+    once, by the rank that owns it, with Dice rising from the initial
+    alignment; pair 2 against the reference pairwise_optimize."""
+    import json
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(__file__), "..", "examples", "po_main")
+    args = ["24", "24", "24", "--iters", "10", "--pairs", "5", "--synth", "--quiet",
+            "--world", "2", "--gather", "file", "--rendezvous", str(tmp_path)]
+    procs = [subprocess.Popen([exe, *args, "--rank", str(r)], stdout=subprocess.PIPE, text=True)
+             for r in range(2)]
+    outs = [p.communicate(timeout=600)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs)
+    rec = json.loads(outs[0].strip().splitlines()[-1])
+    assert rec["world"] == 2 and [r["pair"] for r in rec["results"]] == [0, 2, 4, 1, 3]
+    for r in rec["results"]:
+        assert r["rank"] == r["pair"] % 2
+        assert r["dice_final"] >= r["dice0"] and r["loss_final"] < r["loss0"]
+    # pair 2: make_synth_pair(24^3, seed 3), init_model(42), 10 Adam updates
+    f, m, lf, lm, _ = ref.synth_pair((24, 24, 24), seed=3, max_disp=2.0)
+    packed, _ = ref.model_params(42)
+    loss_r, dice_r, _ = ref.pairwise_optimize(f, m, lf, lm, packed, 10, lr=1e-4)
+    r2 = [r for r in rec["results"] if r["pair"] == 2][0]
+    assert abs(r2["loss0"] - loss_r[0]) <= 1e-5 * abs(loss_r[0])
+    assert abs(r2["loss_final"] - loss_r[-1]) <= 1e-3 * abs(loss_r[-1])
+    assert abs(r2["dice0"] - dice_r[0]) <= 1e-3 and abs(r2["dice_final"] - dice_r[-1]) <= 1e-3
 
 
 def _conv_ref64(x, w, b, dims):
