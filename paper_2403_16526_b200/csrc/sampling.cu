@@ -260,7 +260,13 @@ __device__ __forceinline__ void scatter_row2(float *ia, float *ib, bool two, boo
 // far_only: this launch is the gather's fallback scatter and runs only when
 // that bound exceeds the gather's reach (else every thread returns at once).
 template <int CT, bool COMPOSE = false>
-__global__ void __launch_bounds__(kSB, CT == 16 ? 4 : 5)
+#ifndef MDG_WBWD_MINB
+#define MDG_WBWD_MINB 5
+#endif
+#ifndef MDG_WBWD_MINB16
+#define MDG_WBWD_MINB16 4
+#endif
+__global__ void __launch_bounds__(kSB, CT == 16 ? MDG_WBWD_MINB16 : (CT == 3 || CT == 8) ? MDG_WBWD_MINB : 5)
 warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, const float *__restrict__ gout,
            float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe,
