@@ -135,6 +135,18 @@ mdg_status mdg_warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *
 mdg_status mdg_warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *field,
                               const float *gout, float *gin, float *gfield, int64_t pb,
                               int64_t pe, void *stream);
+/* Depth-slab warp (the per-rank call of a z-decomposed
+ * kern::warp_fwd / warp_bwd, sampling.hpp:123 / 139): the voxels of planes
+ * [z0, z1) of a volume of dims d.  in / gin hold only the planes [zi0, zi1)
+ * (the slab plus the field's reach), field / out / gout / gfield only the
+ * planes [z0, z1); results equal mdg_warp_*_range over full-size buffers.
+ * A field that samples outside [zi0, zi1) -> MDG_EINVAL (checked on the
+ * device, reported synchronously).  gin accumulates by fp32 atomics. */
+mdg_status mdg_warp_fwd_slab(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                             const float *field, float *out, int z0, int z1, void *stream);
+mdg_status mdg_warp_bwd_slab(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                             const float *field, const float *gout, float *gin, float *gfield,
+                             int z0, int z1, void *stream);
 /* sampling.hpp:225-242 kern::upsample2_fwd (target range checked as in
  * sampling.hpp:266-271 -> MDG_EINVAL) */
 mdg_status mdg_upsample2_fwd(const float *in, int C, mdg_dims3 d, mdg_dims3 td, float scale,

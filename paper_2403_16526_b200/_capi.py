@@ -112,6 +112,8 @@ SIGNATURES = {
     "mdg_conv3_bwd": (_st, [_p, _i, Dims3, _p, _i, _p, _p, _p, _p, _p]),
     "mdg_warp_fwd_range": (_st, [_p, _i, Dims3, _p, _p, C.c_int64, C.c_int64, _p]),
     "mdg_warp_bwd_range": (_st, [_p, _i, Dims3, _p, _p, _p, _p, C.c_int64, C.c_int64, _p]),
+    "mdg_warp_fwd_slab": (_st, [_p, _i, Dims3, _i, _i, _p, _p, _i, _i, _p]),
+    "mdg_warp_bwd_slab": (_st, [_p, _i, Dims3, _i, _i, _p, _p, _p, _p, _i, _i, _p]),
     "mdg_compose_fwd": (_st, [_p, _p, Dims3, _p, _p]),
     "mdg_compose_bwd": (_st, [_p, _p, Dims3, _p, _p, _p, _p]),
     "mdg_scaling_squaring_fwd": (_st, [_p, Dims3, _i, _p, _p, _p]),

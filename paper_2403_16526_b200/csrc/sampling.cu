@@ -13,6 +13,7 @@
 // bit-identical, only the summation order at a shared corner varies.  The
 // upsample backward is a pure gather over the <=5 candidate fine voxels per
 // axis (no atomics).
+#include <functional>
 #include <cstdlib>
 
 #include "mdg_common.cuh"
@@ -38,6 +39,31 @@ __device__ __forceinline__ Corners corners_at(float cx, float cy, float cz, int 
     c.o01 = c.az.i1 * sz + c.ay.i0 * sy;
     c.o11 = c.az.i1 * sz + c.ay.i1 * sy;
     return c;
+}
+
+// Buffer geometry of one warp launch.  Whole volume: channel strides n, no
+// offsets, the window [0, l).  Depth slab (mdg_warp_*_slab): `in`/`gin` hold
+// only the planes [zlo, zhi) (channel stride csi; io = zlo*h*w is subtracted
+// from every corner offset) and field/out/gout/gfield only the launch's own
+// voxels (channel stride csv; voxel p is element p - vo); a voxel whose
+// corners leave [zlo, zhi) touches nothing and raises *err.
+struct WarpWin {
+    int64_t csi, csv, vo;
+    int zlo, zhi, io;
+    unsigned *err;
+};
+inline WarpWin whole_win(int64_t n, int l) { return WarpWin{n, n, 0, 0, l, 0, nullptr}; }
+// the window test; on success the corner offsets become window-relative
+__device__ __forceinline__ bool in_window(Corners &c, const WarpWin &win) {
+    if (c.az.i0 < win.zlo || c.az.i1 >= win.zhi) {
+        if (win.err) atomicOr(win.err, 1u);
+        return false;
+    }
+    c.o00 -= win.io;
+    c.o10 -= win.io;
+    c.o01 -= win.io;
+    c.o11 -= win.io;
+    return true;
 }
 
 // sampling.hpp:53-68
@@ -145,17 +171,21 @@ __device__ __forceinline__ void grad_oct(const Oct &o, const Corners &c, float g
 // sampling.hpp:123-135.  CT > 0: channel count known at compile time, all
 // 8*CT corner loads issued before any interpolation (memory-level
 // parallelism); CT == 0: runtime channel loop.
-template <int CT>
+template <int CT, bool SLAB = false>
 __global__ void __launch_bounds__(kSB, CT > 0 ? 8 : 1)
 warp_fwd_k(const float *__restrict__ in, int C, int h, int w, int l,
-           const float *__restrict__ field, float *__restrict__ out, int64_t pb, int64_t pe) {
-    const int64_t n = (int64_t)h * w * l;
+           const float *__restrict__ field, float *__restrict__ out, int64_t pb, int64_t pe,
+           WarpWin win) {
     const int64_t p = pb + (int64_t)blockIdx.x * kSB + threadIdx.x;  // voxels [pb, pe)
     if (p >= pe) return;
     int x, y, z;
     xyz_of(p, h, w, x, y, z);
-    const Corners c = corners_at(add_((float)x, __ldg(field + p)), add_((float)y, __ldg(field + n + p)),
-                                 add_((float)z, __ldg(field + 2 * n + p)), h, w, l);
+    // in / out channel strides, voxel p's field/out element (SLAB: WarpWin)
+    const int64_t n = SLAB ? win.csi : (int64_t)h * w * l, m = SLAB ? win.csv : n;
+    const int64_t vi = SLAB ? p - win.vo : p;
+    Corners c = corners_at(add_((float)x, __ldg(field + vi)), add_((float)y, __ldg(field + m + vi)),
+                           add_((float)z, __ldg(field + 2 * m + vi)), h, w, l);
+    if (SLAB && !in_window(c, win)) return;
     if (CT > 0) {
         // 32-bit element offsets of the 4 corner rows (x0 corner; x1 = +1)
         const int r00 = c.o00 + c.ax.i0, r10 = c.o10 + c.ax.i0;
@@ -204,16 +234,16 @@ warp_fwd_k(const float *__restrict__ in, int C, int h, int w, int l,
             const float2 c0 = lerp2(lerp2(v000, v100, GX, FX), lerp2(v010, v110, GX, FX), GY, FY);
             const float2 c1 = lerp2(lerp2(v001, v101, GX, FX), lerp2(v011, v111, GX, FX), GY, FY);
             const float2 r = lerp2(c0, c1, GZ, FZ);
-            out[(int64_t)ch * n + p] = r.x;
-            out[(int64_t)(ch + 1) * n + p] = r.y;
+            out[(int64_t)ch * m + vi] = r.x;
+            out[(int64_t)(ch + 1) * m + vi] = r.y;
         }
         }
         if (CT & 1) {
             const int ch = CT - 1;
-            out[(int64_t)ch * n + p] = lerp_oct(load_oct(in + (int64_t)ch * n, c), c);
+            out[(int64_t)ch * m + vi] = lerp_oct(load_oct(in + (int64_t)ch * n, c), c);
         }
     } else {
-        for (int ch = 0; ch < C; ++ch) out[ch * n + p] = sample(in + ch * n, c);
+        for (int ch = 0; ch < C; ++ch) out[ch * m + vi] = sample(in + ch * n, c);
     }
 }
 
@@ -259,28 +289,32 @@ __device__ __forceinline__ void scatter_row2(float *ia, float *ib, bool two, boo
 // displacement bound the deterministic gin gather needs (warp_gather.cu).
 // far_only: this launch is the gather's fallback scatter and runs only when
 // that bound exceeds the gather's reach (else every thread returns at once).
-template <int CT, bool COMPOSE = false>
+template <int CT, bool COMPOSE = false, bool SLAB = false>
 #ifndef MDG_WBWD_MINB
 #define MDG_WBWD_MINB 5
 #endif
 #ifndef MDG_WBWD_MINB16
 #define MDG_WBWD_MINB16 4
 #endif
-__global__ void __launch_bounds__(kSB, CT == 16 ? MDG_WBWD_MINB16 : (CT == 3 || CT == 8) ? MDG_WBWD_MINB : 5)
+// (the slab form's extra strides and window test need more registers)
+__global__ void __launch_bounds__(kSB, SLAB ? (CT == 16 ? 3 : CT == 8 ? 4 : 5)
+                                       : CT == 16 ? MDG_WBWD_MINB16
+                                       : (CT == 3 || CT == 8) ? MDG_WBWD_MINB : 5)
 warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, const float *__restrict__ gout,
            float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe,
-           unsigned *__restrict__ rbits = nullptr, bool far_only = false) {
+           WarpWin win, unsigned *__restrict__ rbits = nullptr, bool far_only = false) {
     if (far_only && __uint_as_float(*rbits) <= (float)kGatherReach) return;
-    const int64_t n = (int64_t)h * w * l;
+    // in/gin and field/gout/gfield channel strides (SLAB: WarpWin)
+    const int64_t n = SLAB ? win.csi : (int64_t)h * w * l, m = SLAB ? win.csv : n;
     const int64_t p0 = pb + (int64_t)blockIdx.x * kSB + threadIdx.x;  // voxels [pb, pe)
     // CT > 0 keeps every lane alive for the warp-level scatter merge
-    const bool ok = p0 < pe;
+    bool ok = p0 < pe;
     if (CT == 0 && !ok && !rbits) return;
-    const int64_t p = ok ? p0 : 0;
+    const int64_t p = ok ? p0 : (SLAB ? pb : 0), vi = SLAB ? p - win.vo : p;
     int x, y, z;
     xyz_of(p, h, w, x, y, z);
-    const float phx = __ldg(field + p), phy = __ldg(field + n + p), phz = __ldg(field + 2 * n + p);
+    const float phx = __ldg(field + vi), phy = __ldg(field + m + vi), phz = __ldg(field + 2 * m + vi);
     if (rbits && !far_only) {
         float m = ok ? fmaxf(fabsf(phx), fmaxf(fabsf(phy), fabsf(phz))) : 0.0f;
         // a NaN entry (fmaxf would drop it) ranks above every bound
@@ -292,8 +326,13 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
         if ((threadIdx.x & 31) == 0) atomicMax(rbits, __float_as_uint(m));
     }
     if (CT == 0 && (!ok || (!gin && !gfield))) return;
-    const Corners c = corners_at(add_((float)x, phx), add_((float)y, phy), add_((float)z, phz), h,
-                                 w, l);
+    Corners c = corners_at(add_((float)x, phx), add_((float)y, phy), add_((float)z, phz), h, w, l);
+    if (SLAB && !in_window(c, win)) {
+        if (CT == 0) return;
+        ok = false;
+        c.o00 = c.o10 = c.o01 = c.o11 = 0;
+        c.ax.i0 = 0;
+    }
     float gx = 0.0f, gy = 0.0f, gz = 0.0f;
     if (CT > 0) {
         // channel pairs; corner rows as 32-bit element offsets (x1 = x0 + 1;
@@ -322,7 +361,7 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
         // memory latency per pair
         float gv[CT > 0 ? CT : 1];
 #pragma unroll
-        for (int ch = 0; ch < CT; ++ch) gv[ch] = __ldg(gout + (int64_t)ch * n + p);
+        for (int ch = 0; ch < CT; ++ch) gv[ch] = __ldg(gout + (int64_t)ch * m + vi);
         // phase 1, gfield: loads and arithmetic only (no atomics in between,
         // so corner loads of different channel pairs can be in flight together)
 #pragma unroll
@@ -394,7 +433,7 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
         }
     } else {
         for (int ch = 0; ch < C; ++ch) {
-            const float g = __ldg(gout + ch * n + p);
+            const float g = __ldg(gout + ch * m + vi);
             if (g == 0.0f) continue;
             if (gin) scatter(gin + ch * n, c, g);
             if (gfield) {
@@ -411,13 +450,13 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
             // op_compose = op_add(res, op_warp(prev, res)) (ops.hpp:295-298): the
             // add node replays first (gres += gout), then the warp adds its
             // coordinate gradient (tape.hpp:146-156)
-            gfield[p] = add_(add_(gfield[p], __ldg(gout + p)), gx);
-            gfield[n + p] = add_(add_(gfield[n + p], __ldg(gout + n + p)), gy);
-            gfield[2 * n + p] = add_(add_(gfield[2 * n + p], __ldg(gout + 2 * n + p)), gz);
+            gfield[vi] = add_(add_(gfield[vi], __ldg(gout + vi)), gx);
+            gfield[m + vi] = add_(add_(gfield[m + vi], __ldg(gout + m + vi)), gy);
+            gfield[2 * m + vi] = add_(add_(gfield[2 * m + vi], __ldg(gout + 2 * m + vi)), gz);
         } else {
-            gfield[p] = add_(gfield[p], gx);
-            gfield[n + p] = add_(gfield[n + p], gy);
-            gfield[2 * n + p] = add_(gfield[2 * n + p], gz);
+            gfield[vi] = add_(gfield[vi], gx);
+            gfield[m + vi] = add_(gfield[m + vi], gy);
+            gfield[2 * m + vi] = add_(gfield[2 * m + vi], gz);
         }
     }
 }
@@ -425,6 +464,16 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
 // channel counts with an unrolled instantiation (the pyramid's C = 1, 3, 8,
 // 16, ...); others use the runtime loop
 #define MDG_UNPACK(...) __VA_ARGS__
+#define MDG_WARP_DISPATCH_T(KERNEL, TA, C, CFG, ARGS)                     \
+    switch (C) {                                                           \
+        case 1: KERNEL<1, MDG_UNPACK TA><<<MDG_UNPACK CFG>>> ARGS; break;   \
+        case 2: KERNEL<2, MDG_UNPACK TA><<<MDG_UNPACK CFG>>> ARGS; break;   \
+        case 3: KERNEL<3, MDG_UNPACK TA><<<MDG_UNPACK CFG>>> ARGS; break;   \
+        case 4: KERNEL<4, MDG_UNPACK TA><<<MDG_UNPACK CFG>>> ARGS; break;   \
+        case 8: KERNEL<8, MDG_UNPACK TA><<<MDG_UNPACK CFG>>> ARGS; break;   \
+        case 16: KERNEL<16, MDG_UNPACK TA><<<MDG_UNPACK CFG>>> ARGS; break; \
+        default: KERNEL<0, MDG_UNPACK TA><<<MDG_UNPACK CFG>>> ARGS; break;  \
+    }
 #define MDG_WARP_DISPATCH(KERNEL, C, CFG, ARGS)                  \
     switch (C) {                                                 \
         case 1: KERNEL<1><<<MDG_UNPACK CFG>>> ARGS; break;       \
@@ -575,7 +624,7 @@ mdg_status warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
                           int64_t pb, int64_t pe, cudaStream_t st) {
     if (pe <= pb) return MDG_OK;
     MDG_WARP_DISPATCH(warp_fwd_k, d.h >= 2 ? C : 0, (grid1d(pe - pb, kSB), kSB, 0, st),
-                      (in, C, d.h, d.w, d.l, field, out, pb, pe));
+                      (in, C, d.h, d.w, d.l, field, out, pb, pe, whole_win(nvox(d), d.l)));
     MDG_LAUNCHED();
     return MDG_OK;
 }
@@ -594,7 +643,8 @@ mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
     // (the gather indexes with 32-bit offsets: up to 16 channel planes)
     if (!gin || warp_atomic_mode() || 16 * nvox(d) >= (int64_t(1) << 32) || d.l >= 4096) {
         MDG_WARP_DISPATCH(warp_bwd_k, CD, (grid1d(pe - pb, kSB), kSB, 0, st),
-                          (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe));
+                          (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe,
+                           whole_win(nvox(d), d.l)));
         MDG_LAUNCHED();
         return MDG_OK;
     }
@@ -605,11 +655,13 @@ mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
     unsigned *rb = ws.as<unsigned>();
     MDG_CUDA_TRY(cudaMemsetAsync(rb, 0, 2 * sizeof(unsigned), st));
     MDG_WARP_DISPATCH(warp_bwd_k, CD, (grid1d(pe - pb, kSB), kSB, 0, st),
-                      (in, C, d.h, d.w, d.l, field, gout, nullptr, gfield, pb, pe, rb, false));
+                      (in, C, d.h, d.w, d.l, field, gout, nullptr, gfield, pb, pe,
+                       whole_win(nvox(d), d.l), rb, false));
     MDG_LAUNCHED();
     if (mdg_status e = warp_gin_gather(field, gout, C, d, gin, pb, pe, rb, rb + 1, st)) return e;
     MDG_WARP_DISPATCH(warp_bwd_k, CD, (grid1d(pe - pb, kSB), kSB, 0, st),
-                      (in, C, d.h, d.w, d.l, field, gout, gin, nullptr, pb, pe, rb, true));
+                      (in, C, d.h, d.w, d.l, field, gout, gin, nullptr, pb, pe,
+                       whole_win(nvox(d), d.l), rb, true));
     MDG_LAUNCHED();
     return MDG_OK;
 }
@@ -667,6 +719,70 @@ mdg_status mdg_warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *
     return warp_bwd_range(in, C, d, field, gout, gin, gfield, pb, pe, S_(stream));
 }
 
+// Depth-slab forms: planes [z0, z1) of a volume of dims d; in / gin hold the
+// planes [zi0, zi1) only, field / out / gout / gfield planes [z0, z1) only.
+// A field that samples outside [zi0, zi1) is reported (synchronously) as
+// MDG_EINVAL and leaves the out-of-window voxels untouched.
+static mdg_status check_slab(mdg_dims3 d, int C, int zi0, int zi1, int z0, int z1) {
+    if (mdg_status e = check_field_dims(d, "warp slab")) return e;
+    MDG_REQUIRE(C >= 0, "warp slab: channels must be >= 0");
+    MDG_REQUIRE(0 <= z0 && z0 <= z1 && z1 <= d.l, "warp slab: plane range out of bounds");
+    MDG_REQUIRE(0 <= zi0 && zi0 <= z0 && z1 <= zi1 && zi1 <= d.l,
+                "warp slab: input window must cover the slab's planes");
+    return MDG_OK;
+}
+
+static mdg_status slab_run(mdg_dims3 d, int zi0, int zi1, int z0, int z1, cudaStream_t st,
+                           const std::function<void(const WarpWin &)> &launch) {
+    const int64_t hw = (int64_t)d.h * d.w;
+    Scratch ws;
+    MDG_CUDA_TRY(ws.alloc(sizeof(unsigned), st));
+    unsigned *err = ws.as<unsigned>();
+    MDG_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(unsigned), st));
+    const WarpWin win{(zi1 - zi0) * hw, (z1 - z0) * hw, z0 * hw, zi0, zi1, (int)(zi0 * hw), err};
+    launch(win);
+    MDG_LAUNCHED();
+    unsigned bad = 0;
+    MDG_CUDA_TRY(cudaMemcpyAsync(&bad, err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    MDG_CUDA_TRY(cudaStreamSynchronize(st));
+    MDG_REQUIRE(!bad, "warp slab: the field samples planes outside the input window [" +
+                          std::to_string(zi0) + ", " + std::to_string(zi1) + ")");
+    return MDG_OK;
+}
+
+mdg_status mdg_warp_fwd_slab(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                             const float *field, float *out, int z0, int z1, void *stream) {
+    if (mdg_status e = check_slab(d, C, zi0, zi1, z0, z1)) return e;
+    const int64_t hw = (int64_t)d.h * d.w;
+    if (z1 == z0 || C == 0 || hw == 0) return MDG_OK;
+    MDG_REQUIRE(in && field && out, "warp slab: null pointer");
+    const int64_t pb = z0 * hw, pe = z1 * hw;
+    cudaStream_t st = S_(stream);
+    return slab_run(d, zi0, zi1, z0, z1, st, [&](const WarpWin &win) {
+        MDG_WARP_DISPATCH_T(warp_fwd_k, (true), d.h >= 2 ? C : 0,
+                            (grid1d(pe - pb, kSB), kSB, 0, st),
+                            (in, C, d.h, d.w, d.l, field, out, pb, pe, win));
+    });
+}
+
+mdg_status mdg_warp_bwd_slab(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                             const float *field, const float *gout, float *gin, float *gfield,
+                             int z0, int z1, void *stream) {
+    if (mdg_status e = check_slab(d, C, zi0, zi1, z0, z1)) return e;
+    const int64_t hw = (int64_t)d.h * d.w;
+    if (z1 == z0 || C == 0 || hw == 0 || (!gin && !gfield)) return MDG_OK;
+    MDG_REQUIRE(in && field && gout, "warp slab: null pointer");
+    const int64_t pb = z0 * hw, pe = z1 * hw;
+    cudaStream_t st = S_(stream);
+    // gin by the float-atomic scatter (the deterministic gather works on
+    // whole-volume buffers only)
+    return slab_run(d, zi0, zi1, z0, z1, st, [&](const WarpWin &win) {
+        MDG_WARP_DISPATCH_T(warp_bwd_k, (false, true), d.h >= 2 ? C : 0,
+                            (grid1d(pe - pb, kSB), kSB, 0, st),
+                            (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe, win));
+    });
+}
+
 mdg_status mdg_compose_fwd(const float *prev, const float *res, mdg_dims3 d, float *out,
                            void *stream) {
     if (mdg_status e = check_field_dims(d, "compose")) return e;
@@ -692,7 +808,8 @@ mdg_status mdg_compose_bwd(const float *prev, const float *res, mdg_dims3 d,
         cudaStream_t st = S_(stream);
         if (!gprev || warp_atomic_mode() || 16 * n >= (int64_t(1) << 32) || d.l >= 4096) {
             warp_bwd_k<3, true><<<grid1d(n, kSB), kSB, 0, st>>>(prev, 3, d.h, d.w, d.l, res, gout,
-                                                                gprev, gres, 0, n);
+                                                                gprev, gres, 0, n,
+                                                                whole_win(n, d.l));
             MDG_LAUNCHED();
             return MDG_OK;
         }
@@ -701,11 +818,13 @@ mdg_status mdg_compose_bwd(const float *prev, const float *res, mdg_dims3 d,
         unsigned *rb = ws.as<unsigned>();
         MDG_CUDA_TRY(cudaMemsetAsync(rb, 0, 2 * sizeof(unsigned), st));
         warp_bwd_k<3, true><<<grid1d(n, kSB), kSB, 0, st>>>(prev, 3, d.h, d.w, d.l, res, gout,
-                                                            nullptr, gres, 0, n, rb, false);
+                                                            nullptr, gres, 0, n,
+                                                            whole_win(n, d.l), rb, false);
         MDG_LAUNCHED();
         if (mdg_status e = warp_gin_gather(res, gout, 3, d, gprev, 0, n, rb, rb + 1, st)) return e;
         warp_bwd_k<3, true><<<grid1d(n, kSB), kSB, 0, st>>>(prev, 3, d.h, d.w, d.l, res, gout,
-                                                            gprev, nullptr, 0, n, rb, true);
+                                                            gprev, nullptr, 0, n,
+                                                            whole_win(n, d.l), rb, true);
         MDG_LAUNCHED();
         return MDG_OK;
     }

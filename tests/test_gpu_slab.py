@@ -15,22 +15,22 @@ pytestmark = pytest.mark.gpu
 
 
 class SimExchange:
-    def __init__(self):
-        self.store = {}
+    """The neighbours' face planes, taken from the whole-volume tensors each
+    rank's exchange would deliver (tag -> the packed global tensors)."""
 
-    def put(self, name, rank, x):
-        self.store[(name, rank)] = x
+    def __init__(self, tensors):
+        self.t = tensors
 
-    def __call__(self, name, x, sl, fill):
-        self.store[(name, sl.rank)] = x
-        C = x.shape[0]
-        lo = torch.full((C, sl.w, sl.h), fill, device=x.device)
-        hi = torch.full((C, sl.w, sl.h), fill, device=x.device)
-        if sl.rank > 0:
-            lo = self.store[(name, sl.rank - 1)][:, -1].clone()
-        if sl.rank < sl.world - 1:
-            hi = self.store[(name, sl.rank + 1)][:, 0].clone()
-        return lo, hi
+    def start(self, tag, send_lo, send_hi, sl):
+        g = torch.cat(self.t[tag])  # {sum C, l, w, h}
+        lo = g[:, sl.z0 - 1].contiguous() if sl.rank > 0 else None
+        hi = g[:, sl.z1].contiguous() if sl.rank < sl.world - 1 else None
+        assert send_lo.shape == g[:, 0].shape
+
+        class P:
+            def wait(self):
+                return lo, hi
+        return P()
 
 
 @pytest.mark.parametrize("world,dims,S,hd", [(2, (20, 12, 16), 1, 6), (3, (33, 9, 10), 2, 4),
@@ -46,16 +46,11 @@ def test_slab_modet_cuda_matches_full_volume(cuda, world, dims, S, hd):
     SF, LSE = ops.modet_fwd(Q, K, B, dims, cfg, layout=ops.MDG_QK_PLANAR)
     gQ, gK, gB = ops.modet_bwd(Q, K, B, SF, LSE, gSF, dims, cfg, layout=ops.MDG_QK_PLANAR)
 
-    ex = SimExchange()
+    v = lambda t: t.reshape(t.shape[0], l, w, h)  # noqa: E731
+    ex = SimExchange({"QK": [v(Q), v(K)], "SF": [v(SF), v(LSE), v(gSF)]})
     slabs = [slabmod.Slab(h, w, l, world, rk) for rk in range(world)]
     mods = [slabmod.SlabModeT(sl, S, hd, exchange=ex, all_reduce=lambda t: None) for sl in slabs]
-    for sl in slabs:
-        ex.put("K", sl.rank, sl.local(K))
     sfs = [m.forward(sl.local(Q), sl.local(K), B) for m, sl in zip(mods, slabs)]
-    for m, sl in zip(mods, slabs):  # what each rank publishes before its backward
-        _, _, _, sf, saved, _ = m._saved
-        for name, t in (("Q", sl.local(Q)), ("SF", sf), ("saved", saved), ("gSF", sl.local(gSF))):
-            ex.put(name, sl.rank, t)
     outs = [m.backward(sl.local(gSF)) for m, sl in zip(mods, slabs)]
     torch.cuda.synchronize()
     full = lambda t: t.reshape(t.shape[0], l, w, h).cpu().numpy()  # noqa: E731
@@ -85,9 +80,10 @@ def test_slab_warp_cuda_matches_full_volume(cuda, world, dims, C, zreach):
     slabs = [slabmod.Slab(h, w, l, world, rk) for rk in range(world)]
     R = max(slabmod.warp_reach(sl.local(fld), l) for sl in slabs)
 
-    def exchange(name, x, sl, R_):
+    def exchange(name, x, sl, R_, out):
         lo, hi = max(0, sl.z0 - R_), min(l, sl.z1 + R_)
-        return vol[:, lo:hi].clone()  # what the owners would send
+        out.copy_(vol[:, lo:hi])  # what the owners would send
+        return out
 
     contribs = {}
 
@@ -114,3 +110,55 @@ def test_slab_warp_cuda_matches_full_volume(cuda, world, dims, C, zreach):
     assert R > 1 and np.array_equal(cat(outs), full(out))
     assert np.array_equal(cat([g for _, g in loc]), full(gfield))
     assert np.allclose(cat(gins), full(gin), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("C", [1, 3, 5, 8, 16])
+def test_warp_slab_abi_matches_range(cuda, C):
+    """mdg_warp_fwd_slab / _bwd_slab on window-sized buffers equal the range
+    kernels on full-size buffers (out, gfield bit for bit; gin to atomic
+    order), and a field that leaves the window is refused, not followed."""
+    h, w, l = 20, 12, 16
+    r = np.random.default_rng(31 + C)
+    vol = torch.from_numpy(f32(r.standard_normal((C, l, w, h)))).cuda()
+    fld = torch.from_numpy(f32(np.stack([r.uniform(-1.5, 1.5, (l, w, h)),
+                                         r.uniform(-1.5, 1.5, (l, w, h)),
+                                         r.uniform(-2.5, 2.5, (l, w, h))]))).cuda()
+    gout = torch.from_numpy(f32(r.standard_normal((C, l, w, h)))).cuda()
+    L, P = ops._capi.lib(), ops._ptr
+    d = ops.dims3((h, w, l))
+    hw = h * w
+    z0, z1, zi0, zi1 = 5, 11, 1, 15  # reach ceil(2.5) + 1 = 4 planes
+    out_full = torch.zeros_like(vol)
+    gin_full = torch.zeros_like(vol)
+    gf_full = torch.zeros_like(fld)
+    ops._check(L.mdg_warp_fwd_range(P(vol), C, d, P(fld), P(out_full), z0 * hw, z1 * hw,
+                                    ops._stream()))
+    ops._check(L.mdg_warp_bwd_range(P(vol), C, d, P(fld), P(gout), P(gin_full), P(gf_full),
+                                    z0 * hw, z1 * hw, ops._stream()))
+    win = vol[:, zi0:zi1].contiguous()
+    f_s, go_s = fld[:, z0:z1].contiguous(), gout[:, z0:z1].contiguous()
+    out_s = torch.zeros(C, z1 - z0, w, h, device="cuda")
+    gin_s = torch.zeros(C, zi1 - zi0, w, h, device="cuda")
+    gf_s = torch.zeros(3, z1 - z0, w, h, device="cuda")
+    ops._check(L.mdg_warp_fwd_slab(P(win), C, d, zi0, zi1, P(f_s), P(out_s), z0, z1,
+                                   ops._stream()))
+    ops._check(L.mdg_warp_bwd_slab(P(win), C, d, zi0, zi1, P(f_s), P(go_s), P(gin_s), P(gf_s),
+                                   z0, z1, ops._stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(out_s, out_full[:, z0:z1])
+    assert torch.equal(gf_s, gf_full[:, z0:z1])
+    assert not gin_full[:, :zi0].any() and not gin_full[:, zi1:].any()
+    assert torch.allclose(gin_s, gin_full[:, zi0:zi1], rtol=1e-5, atol=1e-5)
+    # a window short of the reach: refused (EINVAL; the out-of-window voxels
+    # touch nothing — compute-sanitizer clean)
+    small = vol[:, 4:12].contiguous()
+    with pytest.raises(ops.InvalidInput, match="outside the input window"):
+        ops._check(L.mdg_warp_bwd_slab(P(small), C, d, 4, 12, P(f_s), P(go_s),
+                                       P(gin_s[:, :8].contiguous()), P(gf_s), z0, z1,
+                                       ops._stream()))
+    with pytest.raises(ops.InvalidInput, match="outside the input window"):
+        ops._check(L.mdg_warp_fwd_slab(P(small), C, d, 4, 12, P(f_s), P(out_s),
+                                       z0, z1, ops._stream()))
+    with pytest.raises(ops.InvalidInput, match="must cover"):
+        ops._check(L.mdg_warp_fwd_slab(P(win), C, d, 6, 15, P(f_s), P(out_s), z0, z1,
+                                       ops._stream()))

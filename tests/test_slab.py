@@ -139,15 +139,24 @@ class OracleWarp:
 
         self.m = pyoracle.mdo()
 
-    def fwd_range(self, vol, field, out, dims, pb, pe):
-        o = self.m.warp_fwd(f32(vol.numpy()), f32(field.numpy()))
-        C = vol.shape[0]
-        out.view(C, -1)[:, pb:pe] = torch.from_numpy(o.reshape(C, -1)[:, pb:pe])
+    def _full(self, x, dims, z0):
+        h, w, l = dims
+        f = torch.zeros(x.shape[0], l, w, h, dtype=x.dtype)
+        f[:, z0:z0 + x.shape[1]] = x
+        return f
 
-    def bwd_range(self, vol, field, gout, gin, gfield, dims, pb, pe):
-        gi, gf = self.m.warp_bwd(f32(vol.numpy()), f32(field.numpy()), f32(gout.numpy()))
-        gin += torch.from_numpy(gi)
-        gfield.view(3, -1)[:, pb:pe] = torch.from_numpy(gf.reshape(3, -1)[:, pb:pe])
+    def fwd_slab(self, win, field, out, dims, zi0, zi1, z0, z1):
+        o = self.m.warp_fwd(f32(self._full(win, dims, zi0).numpy()),
+                            f32(self._full(field, dims, z0).numpy()))
+        out.copy_(torch.from_numpy(o[:, z0:z1]))
+
+    def bwd_slab(self, win, field, gout, gin_win, gfield, dims, zi0, zi1, z0, z1):
+        # gout zero outside the slab: only the slab's voxels scatter
+        gi, gf = self.m.warp_bwd(f32(self._full(win, dims, zi0).numpy()),
+                                 f32(self._full(field, dims, z0).numpy()),
+                                 f32(self._full(gout, dims, z0).numpy()))
+        gin_win += torch.from_numpy(gi[:, zi0:zi1])
+        gfield.copy_(torch.from_numpy(gf[:, z0:z1]))
 
 
 def _warp_case(dims, C, seed, zreach):

@@ -43,10 +43,21 @@ def main():
     sl = slabmod.Slab(h, w, l, world, rank)
     dz = sl.depth
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
-    Q = torch.rand(S * HD, dz, w, h, device=dev, generator=g) * 2 - 1
-    K = torch.rand(S * HD, dz, w, h, device=dev, generator=g) * 2 - 1
+    mt = slabmod.SlabModeT(sl, S, HD)
+    wp = slabmod.SlabWarp(sl)
+    # the inputs written straight into the operator's extended buffers (no
+    # staging copy; at N = 1 these are plain tensors)
+    if world > 1:
+        Q, K = mt.input_views(torch.empty(0, device=dev))
+        gSF = mt.grad_view(torch.empty(0, device=dev))
+    else:
+        Q = torch.empty(S * HD, dz, w, h, device=dev)
+        K = torch.empty_like(Q)
+        gSF = torch.empty(3 * S, dz, w, h, device=dev)
+    Q.copy_(torch.rand(S * HD, dz, w, h, device=dev, generator=g) * 2 - 1)
+    K.copy_(torch.rand(S * HD, dz, w, h, device=dev, generator=g) * 2 - 1)
     B = torch.full((S, 27), 0.1, device=dev)
-    gSF = torch.rand(3 * S, dz, w, h, device=dev, generator=g) * 2 - 1
+    gSF.copy_(torch.rand(3 * S, dz, w, h, device=dev, generator=g) * 2 - 1)
     feat = torch.randn(CH, dz, w, h, device=dev, generator=g)
     # a smooth displacement field of up to ~2 voxels (as the main bench):
     # random on a 16x coarser grid, trilinearly upsampled
@@ -55,8 +66,6 @@ def main():
     field = torch.nn.functional.interpolate(coarse, size=(dz, w, h), mode="trilinear",
                                             align_corners=True)[0].contiguous()
     gout = torch.randn(CH, dz, w, h, device=dev, generator=g)
-    mt = slabmod.SlabModeT(sl, S, HD)
-    wp = slabmod.SlabWarp(sl)
 
     def step():
         mt.forward(Q, K, B)
