@@ -1,0 +1,598 @@
+"""Depth-slab pairwise optimisation: the whole PO iteration of one pair split
+along z across ranks (BASELINE config 3: "50 iterations at
+160x192x224, 1/2/4/8 GPUs via depth-slab halo exchange").
+
+Every rank owns the planes [z0, z1) of the full-resolution grid and the
+matching planes of every coarser level (z0, z1 multiples of 16, so the five
+levels split without remainder).  The model's ops decompose as follows
+(reference files cited per op):
+
+* conv3 (encoder conv blocks, encoder.hpp:87-91; RegHead, reghead.hpp:42-47):
+  a 1-plane halo of the input, libmdg's conv over the extended slab, interior
+  planes kept.  Its adjoint returns the halo planes' input gradient to their
+  owners (the halo exchange's backward).
+* instance norm (ops.hpp:162-221): per-channel sums all-reduced (mean, then
+  the centred second moment), so every rank normalises with the global
+  statistics; the backward's sums are all-reduced by the same function.
+* leaky ReLU, 2x average pooling, the Q/K projection + layer norm
+  (attention.hpp:351-356): voxel-local.
+* the ModeT operator (attention.hpp:83-166, 282-316): 1-plane Q/K halos; the
+  fused kernels over the extended slab; the halo keys' gradient goes back to
+  their owners.
+* upsample of the running field (sampling.hpp:225-262): 1-plane halo,
+  edge-replicated at the global boundary (the reference clamps there; the
+  replicated plane interpolates to exactly the same value).
+* warps and the composition (sampling.hpp:123-167, ops.hpp:295-298): the
+  reach R = ceil(max |phi_z|) + 1 all-reduced with MAX, the planes
+  [z0-R, z1+R) gathered from their owners into a window, libmdg's slab warp
+  kernels (mdg_warp_fwd_slab / _bwd_slab); the scattered input gradient's
+  contributions to other ranks' planes are sent back and summed in rank
+  order.
+* the loss (objective.hpp:39-78): NCC box sums with 4-plane halos of the
+  fixed and warped images (and of the in-bounds counts), grad_reg with the
+  next plane; the per-rank partial sums over owned voxels add up to the
+  global means.
+* parameter gradients: one all-reduce of the flat 75-tensor gradient buffer,
+  then the same Adam update on every rank (replicated parameters).
+
+The graph is recorded by torch.autograd over these functions (PyTorch is the
+plumbing here: tape, device memory, torch.distributed); every convolution,
+projection, attention, warp and upsample runs in libmdg.  The leaky ReLU, the
+pooling, the normalisation arithmetic and the NCC / grad_reg arithmetic are
+elementwise torch ops between them.  NCCL moves device tensors directly;
+with gloo (the CPU tests, or several ranks sharing one GPU) the messages are
+staged through host memory.  Parity: tests/test_slab_po.py (the loss and all
+75 gradients against the single-volume native model)."""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+import torch.nn.functional as F
+
+from . import ops
+
+UNIT = 16  # z split granularity: 2^(levels-1)
+
+
+# --------------------------------------------------------------- plumbing
+class Comm:
+    """Rank, world and the point-to-point / all-reduce plumbing of one slab
+    group (the default process group)."""
+
+    def __init__(self):
+        if dist.is_available() and dist.is_initialized():
+            self.world, self.rank = dist.get_world_size(), dist.get_rank()
+            self.staged = self.world > 1 and dist.get_backend() == "gloo"
+        else:
+            self.world, self.rank, self.staged = 1, 0, False
+
+    def exchange(self, sends, recvs):
+        """sends [(tensor, peer)], recvs [(tensor, peer)]: the received
+        messages are written into the recv tensors (views allowed)."""
+        if not sends and not recvs:
+            return
+        ops_, keep, back = [], [], []
+        for t, q in sends:
+            m = t.contiguous()
+            if self.staged and m.is_cuda:
+                m = m.cpu()
+            keep.append(m)
+            ops_.append(dist.P2POp(dist.isend, m, q))
+        for t, q in recvs:
+            if (self.staged and t.is_cuda) or not t.is_contiguous():
+                m = torch.empty(t.shape, dtype=t.dtype, device="cpu" if self.staged else t.device)
+                back.append((t, m))
+            else:
+                m = t
+            ops_.append(dist.P2POp(dist.irecv, m, q))
+        for r in dist.batch_isend_irecv(ops_):
+            r.wait()
+        for t, m in back:
+            t.copy_(m)
+
+    def all_reduce(self, t, op=None):
+        """in place, sum (or op) over ranks"""
+        if self.world == 1:
+            return t
+        op = dist.ReduceOp.SUM if op is None else op
+        if self.staged and t.is_cuda:
+            c = t.cpu()
+            dist.all_reduce(c, op=op)
+            t.copy_(c)
+        else:
+            dist.all_reduce(t, op=op)
+        return t
+
+    def all_reduce_max_int(self, v: int) -> int:
+        if self.world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.int64)
+        if not self.staged:
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return int(t.item())
+
+
+def split_units(l: int, world: int):
+    """Balanced z ranges [(z0, z1)] in whole units of 16 planes."""
+    if l % UNIT:
+        raise ops.InvalidInput(f"slab PO: depth {l} must be a multiple of {UNIT}")
+    units = l // UNIT
+    if units < world:
+        raise ops.InvalidInput(f"slab PO: {units} units of {UNIT} planes for {world} ranks")
+    base, rem = divmod(units, world)
+    out, z = [], 0
+    for r in range(world):
+        n = (base + (1 if r < rem else 0)) * UNIT
+        out.append((z, z + n))
+        z += n
+    return out
+
+
+class Geom:
+    """Global dims (h, w, l) of the full-resolution grid and this rank's
+    z range; level e (0 = full resolution) divides everything by 2^e."""
+
+    def __init__(self, dims, comm: Comm):
+        self.dims = tuple(int(v) for v in dims)
+        self.comm = comm
+        self.ranges = split_units(self.dims[2], comm.world)
+        self.z0, self.z1 = self.ranges[comm.rank]
+
+    def level(self, e):
+        """(dims, z0, z1, all ranks' ranges) of level e; dims halve rounding
+        up (common.hpp:72-74 halved), z exactly (multiples of 16)"""
+        h, w, l = self.dims
+        for _ in range(e):
+            h, w, l = (h + 1) // 2, (w + 1) // 2, (l + 1) // 2
+        return (h, w, l), self.z0 >> e, self.z1 >> e, \
+            [(a >> e, b >> e) for a, b in self.ranges]
+
+
+# ------------------------------------------------------ autograd functions
+class _Halo(torch.autograd.Function):
+    """x {C, D, w, h} -> {C, D+2k, w, h} with the neighbours' k face planes;
+    zero (or, edge=True, the boundary plane repeated) at the global
+    boundary.  Backward: the halo planes' gradient goes back to the owners."""
+
+    @staticmethod
+    def forward(ctx, x, k, edge, comm):
+        C, D, W, H = x.shape
+        if D < k:
+            raise ops.InvalidInput(f"slab PO: {D} planes per rank < halo {k}")
+        out = x.new_zeros(C, D + 2 * k, W, H)
+        out[:, k:k + D] = x
+        r, n = comm.rank, comm.world
+        sends, recvs = [], []
+        if r > 0:
+            sends.append((x[:, :k], r - 1))
+            recvs.append((out[:, :k], r - 1))
+        if r < n - 1:
+            sends.append((x[:, D - k:], r + 1))
+            recvs.append((out[:, D + k:], r + 1))
+        comm.exchange(sends, recvs)
+        if edge:
+            if r == 0:
+                out[:, :k] = x[:, :1]
+            if r == n - 1:
+                out[:, D + k:] = x[:, D - 1:D]
+        ctx.k, ctx.edge, ctx.comm, ctx.D = k, edge, comm, D
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        k, D, comm = ctx.k, ctx.D, ctx.comm
+        r, n = comm.rank, comm.world
+        gx = g[:, k:k + D].clone()
+        sends, recvs, got = [], [], []
+        if r > 0:
+            sends.append((g[:, :k], r - 1))
+            t = torch.empty_like(gx[:, :k])
+            recvs.append((t, r - 1))
+            got.append((t, 0))
+        if r < n - 1:
+            sends.append((g[:, D + k:], r + 1))
+            t = torch.empty_like(gx[:, :k])
+            recvs.append((t, r + 1))
+            got.append((t, D - k))
+        comm.exchange(sends, recvs)
+        for t, z in got:
+            gx[:, z:z + k] += t
+        if ctx.edge:
+            if r == 0:
+                gx[:, 0] += g[:, :k].sum(1)
+            if r == n - 1:
+                gx[:, D - 1] += g[:, D + k:].sum(1)
+        return gx, None, None, None
+
+
+def halo(x, k, comm, edge=False):
+    return _Halo.apply(x, k, edge, comm)
+
+
+class _AllReduce(torch.autograd.Function):
+    """sum over ranks; the adjoint of a replicated sum is the sum of the
+    ranks' gradients"""
+
+    @staticmethod
+    def forward(ctx, t, comm):
+        ctx.comm = comm
+        return comm.all_reduce(t.clone())
+
+    @staticmethod
+    def backward(ctx, g):
+        return ctx.comm.all_reduce(g.clone()), None
+
+
+def all_reduce(t, comm):
+    return _AllReduce.apply(t, comm)
+
+
+def _dims_of(x):  # {C, l, w, h} -> (h, w, l)
+    return (x.shape[3], x.shape[2], x.shape[1])
+
+
+class _Conv3(torch.autograd.Function):
+    """libmdg's 3x3x3 conv (mdg_encoder_conv3_fwd/bwd) on {ic, l, w, h}"""
+
+    @staticmethod
+    def forward(ctx, x, w, b):
+        x = x.contiguous()
+        ic, oc = x.shape[0], w.shape[0]
+        out = x.new_empty(oc, *x.shape[1:])
+        L, P = ops._capi.lib(), ops._ptr
+        ops._check(L.mdg_encoder_conv3_fwd(P(x), ic, ops.dims3(_dims_of(x)), P(w), P(b), oc,
+                                           P(out), ops._stream()))
+        ctx.save_for_backward(x, w)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        x, w = ctx.saved_tensors
+        g = g.contiguous()
+        gin, gw = torch.zeros_like(x), torch.zeros_like(w)
+        gb = w.new_zeros(w.shape[0])
+        L, P = ops._capi.lib(), ops._ptr
+        ops._check(L.mdg_encoder_conv3_bwd(P(x), x.shape[0], ops.dims3(_dims_of(x)), P(w),
+                                           w.shape[0], P(g), P(gin), P(gw), P(gb),
+                                           ops._stream()))
+        return gin, gw, gb
+
+
+def conv3_slab(x, w, b, comm):
+    """zero-padded conv3 of a slab: 1-plane halo, interior planes kept"""
+    return _Conv3.apply(halo(x, 1, comm), w, b)[:, 1:-1]
+
+
+class _Project(torch.autograd.Function):
+    """op_project_qk (attention.hpp:351-356) -> planar Q, K {K, n}"""
+
+    @staticmethod
+    def forward(ctx, f, m, W, b, g, beta):
+        f2, m2 = f.reshape(f.shape[0], -1).contiguous(), m.reshape(m.shape[0], -1).contiguous()
+        p = ops.ProjectionParams(W, b, g, beta)
+        Q, K = ops.project_qk(f2, m2, p, layout=ops.MDG_QK_PLANAR)
+        ctx.save_for_backward(f2, m2, W, b, g, beta)
+        ctx.shape = f.shape
+        return Q, K
+
+    @staticmethod
+    def backward(ctx, gQ, gK):
+        f2, m2, W, b, g, beta = ctx.saved_tensors
+        gQ = torch.zeros_like(f2.new_empty(W.shape[0], f2.shape[1])) if gQ is None else gQ
+        gK = torch.zeros_like(gQ) if gK is None else gK
+        gf, gm, gp = ops.project_qk_bwd(f2, m2, ops.ProjectionParams(W, b, g, beta),
+                                        gQ.contiguous(), gK.contiguous(),
+                                        layout=ops.MDG_QK_PLANAR)
+        return (gf.view(ctx.shape), gm.view(ctx.shape), gp.weight, gp.bias, gp.ln_gamma,
+                gp.ln_beta)
+
+
+class _ModeT(torch.autograd.Function):
+    """the fused ModeT operator (na_fused + subfields) on extended planar
+    Q/K {S*d, D+2, w, h}; the numeric check reports global positions"""
+
+    @staticmethod
+    def forward(ctx, Qx, Kx, B, S, hd, z_shift):
+        d = _dims_of(Qx)
+        cfg = ops.AttentionConfig(S, hd, 3)
+        Q2, K2 = Qx.reshape(S * hd, -1).contiguous(), Kx.reshape(S * hd, -1).contiguous()
+        SF, LSE = ops.modet_fwd(Q2, K2, B.contiguous(), d, cfg, layout=ops.MDG_QK_PLANAR,
+                                check=False)
+        try:
+            ops.check_numeric(d)
+        except ops.NumericError as e:
+            pos = getattr(e, "position", None)
+            if pos is not None and pos[2] >= 0:
+                e.position = (pos[0], pos[1], pos[2] + z_shift, pos[3])
+            raise
+        ctx.save_for_backward(Q2, K2, B, SF, LSE)
+        ctx.cfg, ctx.d = cfg, d
+        return SF.view(3 * S, *Qx.shape[1:])
+
+    @staticmethod
+    def backward(ctx, gSF):
+        Q2, K2, B, SF, LSE = ctx.saved_tensors
+        gQ, gK, gB = ops.modet_bwd(Q2, K2, B, SF, LSE, gSF.reshape(SF.shape).contiguous(), ctx.d,
+                                   ctx.cfg, layout=ops.MDG_QK_PLANAR)
+        shp = (Q2.shape[0], *gSF.shape[1:])
+        return gQ.view(shp), gK.view(shp), gB, None, None, None
+
+
+class _Upsample(torch.autograd.Function):
+    """op_upsample_field_2x on an extended coarse slab (values x2) onto
+    (h, w) = the finer level's, z doubled"""
+
+    @staticmethod
+    def forward(ctx, x, hw):
+        d = _dims_of(x)
+        target = (hw[0], hw[1], 2 * d[2])
+        ctx.d, ctx.t = d, target
+        return ops.upsample_field_2x(x.contiguous(), target, d)
+
+    @staticmethod
+    def backward(ctx, g):
+        return ops.upsample_field_2x_bwd(g.contiguous(), ctx.d, ctx.t), None
+
+
+def upsample_slab(phi_c, comm, hw):
+    """coarse slab {3, Dc, wc, hc} -> fine slab {3, 2Dc, 2wc, 2hc}: fine plane
+    z samples coarse z/2, so the coarse slab needs its next plane (edge-
+    replicated at the global end, where the reference clamps)"""
+    Dc = phi_c.shape[1]
+    return _Upsample.apply(halo(phi_c, 1, comm, edge=True), hw)[:, 2:2 + 2 * Dc]
+
+
+def warp_reach(field_local, l):
+    fz = field_local[2]
+    if fz.numel() == 0:
+        return 1
+    if not bool(torch.isfinite(fz).all()):
+        return l
+    return min(l, int(torch.ceil(fz.abs().max()).item()) + 1)
+
+
+class _Warp(torch.autograd.Function):
+    """op_warp of a slab {C, D, w, h} by its field {3, D, w, h} (global voxel
+    units): the input planes within the all-reduced reach are gathered into a
+    window, the slab kernels index it directly."""
+
+    @staticmethod
+    def forward(ctx, vol, field, geom, e):
+        comm = geom.comm
+        (h, w, l), z0, z1, ranges = geom.level(e)
+        R = comm.all_reduce_max_int(warp_reach(field, l))
+        need = [(max(0, a - R), min(l, b + R)) for a, b in ranges]
+        lo, hi = need[comm.rank]
+        vol = vol.contiguous()
+        C = vol.shape[0]
+        win = vol.new_empty(C, hi - lo, w, h)
+        win[:, z0 - lo:z1 - lo] = vol
+        sends, recvs = [], []
+        for q, (a, b) in enumerate(ranges):
+            if q == comm.rank:
+                continue
+            s0, s1 = max(z0, need[q][0]), min(z1, need[q][1])  # mine, needed by q
+            if s0 < s1:
+                sends.append((vol[:, s0 - z0:s1 - z0], q))
+            r0, r1 = max(a, lo), min(b, hi)  # q's, needed by me
+            if r0 < r1:
+                recvs.append((win[:, r0 - lo:r1 - lo], q))
+        comm.exchange(sends, recvs)
+        field = field.contiguous()
+        out = torch.empty_like(vol)
+        L, P = ops._capi.lib(), ops._ptr
+        ops._check(L.mdg_warp_fwd_slab(P(win), C, ops.dims3((h, w, l)), lo, hi, P(field),
+                                       P(out), z0, z1, ops._stream()))
+        ctx.save_for_backward(win, field)
+        ctx.geom, ctx.e, ctx.need = geom, e, need
+        return out
+
+    @staticmethod
+    def backward(ctx, gout):
+        win, field = ctx.saved_tensors
+        geom, need = ctx.geom, ctx.need
+        comm = geom.comm
+        (h, w, l), z0, z1, ranges = geom.level(ctx.e)
+        lo, hi = need[comm.rank]
+        C = win.shape[0]
+        gin_w = torch.zeros_like(win)
+        gfield = torch.zeros_like(field)
+        L, P = ops._capi.lib(), ops._ptr
+        ops._check(L.mdg_warp_bwd_slab(P(win), C, ops.dims3((h, w, l)), lo, hi, P(field),
+                                       P(gout.contiguous()), P(gin_w), P(gfield), z0, z1,
+                                       ops._stream()))
+        # contributions to other ranks' planes go back to their owners,
+        # summed there in rank order
+        sends, recvs, got = [], [], {}
+        for q, (a, b) in enumerate(ranges):
+            if q == comm.rank:
+                continue
+            s0, s1 = max(a, lo), min(b, hi)  # my additions to q's planes
+            if s0 < s1:
+                sends.append((gin_w[:, s0 - lo:s1 - lo], q))
+            r0, r1 = max(z0, need[q][0]), min(z1, need[q][1])  # q's additions to mine
+            if r0 < r1:
+                t = win.new_empty(C, r1 - r0, w, h)
+                recvs.append((t, q))
+                got[q] = (t, r0)
+        comm.exchange(sends, recvs)
+        gin = win.new_zeros(C, z1 - z0, w, h)
+        for q in range(comm.world):
+            if q == comm.rank:
+                gin += gin_w[:, z0 - lo:z1 - lo]
+            elif q in got:
+                t, r0 = got[q]
+                gin[:, r0 - z0:r0 - z0 + t.shape[1]] += t
+        return gin, gfield, None, None
+
+
+def warp_slab(vol, field, geom, e):
+    return _Warp.apply(vol, field, geom, e)
+
+
+# ------------------------------------------------------------- the model
+def instance_norm(x, gamma, beta, n_global, comm, eps=1e-5):
+    """ops.hpp:162-221 with the per-channel sums all-reduced"""
+    mean = all_reduce(x.sum((1, 2, 3)), comm) / n_global
+    xc = x - mean[:, None, None, None]
+    var = all_reduce((xc * xc).sum((1, 2, 3)), comm) / n_global
+    inv = 1.0 / torch.sqrt(var + eps)
+    return gamma[:, None, None, None] * xc * inv[:, None, None, None] + beta[:, None, None, None]
+
+
+def leaky_relu(x, slope):
+    """ops.hpp:224-238 (the subgradient at 0 takes the slope)"""
+    return torch.where(x > 0, x, slope * x)
+
+
+def conv_block(x, p, geom, e, slope):
+    """op_conv_block (encoder.hpp:87-91); p = (w1, b1, g1, beta1, w2, b2,
+    g2, beta2)"""
+    (h, w, l), _, _, _ = geom.level(e)
+    n = h * w * l
+    comm = geom.comm
+    for wk, bk, gk, btk in (p[0:4], p[4:8]):
+        x = leaky_relu(instance_norm(conv3_slab(x, wk, bk, comm), gk, btk, n, comm), slope)
+    return x
+
+
+def encode(image, blocks, geom, slope):
+    """op_encode (encoder.hpp:102-116): features fine -> coarse"""
+    feats = []
+    x = conv_block(image, blocks[0], geom, 0, slope)
+    feats.append(x)
+    for e in range(1, len(blocks)):
+        # sampling.hpp:171-194: odd x / y extents repeat their last voxel
+        x = F.pad(x, (0, x.shape[3] % 2, 0, x.shape[2] % 2), mode="replicate")
+        x = F.avg_pool3d(x[None], 2)[0]
+        x = conv_block(x, blocks[e], geom, e, slope)
+        feats.append(x)
+    return feats
+
+
+def box_sum(x_ext, r):
+    """zero-padded box sums of half-width r of {D+2r, w, h} along z (valid:
+    the halo planes are the padding) then y and x -> {D, w, h}"""
+    k = 2 * r + 1
+    s = x_ext.unfold(0, k, 1).sum(-1)
+    s = F.pad(s, (0, 0, r, r)).unfold(1, k, 1).sum(-1)
+    return F.pad(s, (r, r)).unfold(2, k, 1).sum(-1)
+
+
+def slab_loss(fixed, warped, phi, geom, lam, window):
+    """op_total_loss (objective.hpp:39-78) minus the warp: this rank's part
+    of ncc + lam * grad_reg (the parts add up to the global loss)"""
+    comm = geom.comm
+    (h, w, l), z0, z1, _ = geom.level(0)
+    n = h * w * l
+    r = window // 2
+    fx = halo(fixed, r, comm)[0]
+    gx = halo(warped, r, comm)[0]
+    with torch.no_grad():
+        cnt = box_sum(halo(torch.ones_like(fixed), r, comm)[0], r)
+    sf, sg = box_sum(fx, r), box_sum(gx, r)
+    sff, sgg, sfg = box_sum(fx * fx, r), box_sum(gx * gx, r), box_sum(fx * gx, r)
+    cross = sfg - sf * sg / cnt
+    var_f = sff - sf * sf / cnt
+    var_g = sgg - sg * sg / cnt
+    cc = cross * cross / (var_f * var_g + 1e-5)
+    ncc = -cc.sum() / n
+    if lam == 0.0:
+        return ncc, ncc, ncc.new_zeros(())
+    ext = halo(phi, 1, comm)
+    D = phi.shape[1]
+    u = ext[:, 1:1 + D]
+    dz = ext[:, 2:2 + D] - u
+    if comm.rank == comm.world - 1:
+        dz = dz[:, :D - 1]  # the last plane has no forward difference
+    reg = 0.0
+    for diff, dim in ((u[..., 1:] - u[..., :-1], h), (u[:, :, 1:] - u[:, :, :-1], w), (dz, l)):
+        reg = reg + (diff * diff).sum() / float(n - n // dim)
+    reg = reg / 3.0
+    return ncc + lam * reg, ncc, reg
+
+
+class SlabModel:
+    """The small-preset model (or any base_channels / heads / head_dim) with
+    its PO iteration decomposed over depth slabs.  `tensors`: the 75
+    ModelParams tensors (ops.init_model order), replicated on every rank;
+    images are this rank's planes {1, z1-z0, w, h}."""
+
+    def __init__(self, tensors, dims, lam=1.0, window=9, slope=0.2, heads=(8, 4, 2, 1, 1),
+                 head_dim=6, comm: Comm | None = None):
+        self.comm = comm or Comm()
+        self.geom = Geom(dims, self.comm)
+        self.params = [t.detach().clone().contiguous().requires_grad_(True) for t in tensors]
+        if len(self.params) != 75:
+            raise ops.InvalidInput("slab PO: expects the 75 ModelParams tensors")
+        self.lam, self.window, self.slope = float(lam), int(window), float(slope)
+        self.heads, self.hd = tuple(heads), int(head_dim)
+        self.opt = ops.AdamOptimizer([p.data for p in self.params])
+        self.grads = [torch.zeros_like(p) for p in self.params]
+
+    @property
+    def z_range(self):
+        return self.geom.z0, self.geom.z1
+
+    def local(self, full):
+        """this rank's planes of a {C, l, w, h} tensor"""
+        return full[:, self.geom.z0:self.geom.z1].contiguous()
+
+    def forward(self, fixed, moving):
+        """build_pipeline (engine.hpp:179-219) on the slab: phi {3, D, w, h}"""
+        P = self.params
+        blocks = [P[8 * k:8 * k + 8] for k in range(5)]
+        geom, comm = self.geom, self.comm
+        ff = encode(fixed, blocks, geom, self.slope)
+        mf = encode(moving, blocks, geom, self.slope)
+        phi = phi_up = None
+        for k in range(5):
+            e = 4 - k
+            W, b, g, beta, B, rw, rb = P[40 + 7 * k:47 + 7 * k]
+            f, m = ff[e], mf[e]
+            m_in = m
+            if k > 0:
+                (he, we, _), _, _, _ = geom.level(e)
+                phi_up = upsample_slab(phi, comm, (he, we))
+                m_in = warp_slab(m, phi_up, geom, e)
+            S = self.heads[k]
+            Q, K = _Project.apply(f, m_in, W, b, g, beta)
+            shp = (S * self.hd, *f.shape[1:])
+            Qx, Kx = halo(Q.view(shp), 1, comm), halo(K.view(shp), 1, comm)
+            _, z0, _, _ = geom.level(e)
+            SF = _ModeT.apply(Qx, Kx, B, S, self.hd, z0 - 1)[:, 1:-1]
+            res = conv3_slab(SF, rw, rb, comm)
+            phi = res if k == 0 else res + warp_slab(phi_up, res, geom, e)
+        return phi
+
+    def loss_step(self, fixed, moving, backward=True):
+        """run_loss_step (engine.hpp:316-340): the global {total, ncc, reg}
+        (identical on every rank) and this rank's phi; with backward, the
+        all-reduced parameter gradients in self.grads."""
+        for p in self.params:
+            p.grad = None
+        with torch.set_grad_enabled(backward):
+            phi = self.forward(fixed, moving)
+            warped = warp_slab(moving, phi, self.geom, 0)
+            total, ncc, reg = slab_loss(fixed, warped, phi, self.geom, self.lam, self.window)
+            if backward:
+                total.backward()
+        terms = torch.stack([total.detach(), ncc.detach(), torch.as_tensor(reg).detach()
+                             .to(total.device, total.dtype)])
+        self.comm.all_reduce(terms)
+        if backward:
+            flat = torch.cat([(p.grad if p.grad is not None else torch.zeros_like(p)).reshape(-1)
+                              for p in self.params])
+            self.comm.all_reduce(flat)  # the one parameter-gradient all-reduce
+            o = 0
+            for g in self.grads:
+                g.copy_(flat[o:o + g.numel()].view_as(g))
+                o += g.numel()
+        return terms, phi.detach()
+
+    def po_step(self, fixed, moving, lr=1e-4):
+        """one pairwise_optimize iteration (engine.hpp:389-398)"""
+        terms, phi = self.loss_step(fixed, moving, backward=True)
+        self.opt.step(lr, self.grads)
+        return terms, phi

@@ -1,0 +1,277 @@
+"""Depth-slab PO (slab_po.py).
+
+CPU (gloo, world 1/2/3): the slab decomposition of the loss — NCC box sums
+across slab faces, grad_reg's forward differences, the global means — against
+the reference's op_total_loss (oracle/_ref via pyoracle) and its gradient;
+the halo / all-reduce functions' adjoints.
+
+GPU: the whole loss step (encoder x2 -> pyramid -> loss -> backward) on 2 and
+3 slabs (ranks sharing cuda:0, messages over gloo) against the same step on
+one slab and against the reference's run_loss_step: the loss terms, phi and
+all 75 parameter gradients, then one Adam step on the replicated
+parameters."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from _util import f32
+from paper_2403_16526_b200 import slab_po
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _init(rank, world, port):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    return dist
+
+
+def test_split_units():
+    assert slab_po.split_units(64, 2) == [(0, 32), (32, 64)]
+    assert slab_po.split_units(80, 3) == [(0, 32), (32, 64), (64, 80)]
+    with pytest.raises(ValueError):
+        slab_po.split_units(40, 2)  # not a multiple of 16
+    with pytest.raises(ValueError):
+        slab_po.split_units(32, 3)  # fewer units than ranks
+
+
+def _loss_case(dims, seed):
+    h, w, l = dims
+    r = np.random.default_rng(seed)
+    fixed = f32(r.uniform(0, 1, (1, l, w, h)))
+    moving = f32(r.uniform(0, 1, (1, l, w, h)))
+    phi = f32(r.uniform(-1.5, 1.5, (3, l, w, h)))
+    return fixed, moving, phi
+
+
+def _loss_worker(rank, world, port, dims, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import pyoracle
+
+    dist = _init(rank, world, port) if world > 1 else None
+    try:
+        comm = slab_po.Comm()
+        geom = slab_po.Geom(dims, comm)
+        fixed, moving, phi = _loss_case(dims, 5)
+        warped = pyoracle.mdo().warp_fwd(moving, phi)  # the warp is tested elsewhere
+        z0, z1 = geom.z0, geom.z1
+        f = torch.from_numpy(fixed[:, z0:z1].copy())
+        g = torch.from_numpy(warped[:, z0:z1].copy()).requires_grad_(True)
+        p = torch.from_numpy(phi[:, z0:z1].copy()).requires_grad_(True)
+        total, ncc, reg = slab_po.slab_loss(f, g, p, geom, 1.0, 9)
+        total.backward()
+        terms = torch.stack([total.detach(), ncc.detach(), reg.detach()])
+        comm.all_reduce(terms)
+        np.savez(os.path.join(out_dir, f"l{rank}.npz"), terms=terms.numpy(),
+                 gw=g.grad.numpy(), gp=p.grad.numpy())
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dims", [(1, (12, 10, 32)), (2, (12, 10, 32)),
+                                        (3, (9, 11, 48))])
+def test_slab_loss_matches_reference(oracle, ref, tmp_path, world, dims):
+    """ncc + grad_reg over slabs (4-plane NCC halos, 1-plane reg halo, partial
+    sums all-reduced) equal the reference's op_total_loss and its phi
+    gradient (through the oracle's warp adjoint) to fp32 summation order."""
+    if world == 1:
+        _loss_worker(0, 1, 0, dims, str(tmp_path))
+    else:
+        mp.start_processes(_loss_worker, args=(world, _free_port(), dims, str(tmp_path)),
+                           nprocs=world, join=True, start_method="spawn")
+    fixed, moving, phi = _loss_case(dims, 5)
+    m = oracle
+    terms_ref, warped, gphi_ref, _ = ref.total_loss(fixed, moving, phi)
+    parts = [dict(np.load(tmp_path / f"l{r}.npz")) for r in range(world)]
+    for p in parts:
+        assert np.array_equal(p["terms"], parts[0]["terms"])
+    assert np.allclose(parts[0]["terms"], terms_ref, rtol=2e-5, atol=1e-6)
+    gw = np.concatenate([p["gw"] for p in parts], axis=1)
+    gp = np.concatenate([p["gp"] for p in parts], axis=1)
+    # chain through the warp: dL/dphi = warp adjoint of dL/dwarped + reg part
+    _, gfield = m.warp_bwd(moving, phi, f32(gw), want_gin=False)
+    g = gfield + gp
+    rel = np.linalg.norm(g - gphi_ref) / np.linalg.norm(gphi_ref)
+    assert rel < 1e-4, rel
+
+
+def _adj_worker(rank, world, port, out_dir):
+    dist = _init(rank, world, port)
+    try:
+        comm = slab_po.Comm()
+        r = np.random.default_rng(3)
+        C, L, W, H = 2, 12, 3, 4
+        x = torch.from_numpy(f32(r.standard_normal((C, L, W, H))))
+        wts = torch.from_numpy(f32(r.standard_normal((C, L + 2 * world * 2, W, H))))
+        D = L // world
+        xl = x[:, rank * D:(rank + 1) * D].clone().requires_grad_(True)
+        outs = []
+        for k, edge in ((1, False), (2, False), (1, True)):
+            y = slab_po.halo(xl, k, comm, edge=edge)
+            outs.append((y * wts[:, rank * D:rank * D + D + 2 * k]).sum())
+        s = slab_po.all_reduce(xl.sum((1, 2, 3)), comm)
+        total = sum(outs) + (s * s).sum()
+        total.backward()
+        np.savez(os.path.join(out_dir, f"a{rank}.npz"), g=xl.grad.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_halo_and_all_reduce_adjoints(tmp_path):
+    """The slab halo (zero and edge-replicated) and the replicated sum are
+    differentiated exactly as the whole-volume expressions they stand for."""
+    world = 2
+    mp.start_processes(_adj_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    r = np.random.default_rng(3)
+    C, L, W, H = 2, 12, 3, 4
+    x = torch.from_numpy(f32(r.standard_normal((C, L, W, H)))).double().requires_grad_(True)
+    wts = torch.from_numpy(f32(r.standard_normal((C, L + 2 * world * 2, W, H)))).double()
+    D = L // world
+    total = 0
+    for k, edge in ((1, False), (2, False), (1, True)):
+        for rk in range(world):
+            lo, hi = rk * D - k, (rk + 1) * D + k
+            pad = torch.nn.functional.pad(x, (0, 0, 0, 0, k, k),
+                                          mode="replicate" if edge else "constant")
+            y = pad[:, lo + k:hi + k]
+            total = total + (y * wts[:, rk * D:rk * D + D + 2 * k]).sum()
+    s = x.sum((1, 2, 3))
+    total = total + world * (s * s).sum()
+    total.backward()
+    got = np.concatenate([np.load(tmp_path / f"a{rk}.npz")["g"] for rk in range(world)], axis=1)
+    assert np.allclose(got, x.grad.numpy(), rtol=1e-5, atol=1e-5)
+
+
+# ----------------------------------------------------------------- GPU
+PRE_NORM_BIAS = {8 * k + i for k in range(5) for i in (1, 5)}  # b1, b2: zero through IN
+PO_ITERS = 4
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, np.float64).ravel(), np.asarray(b, np.float64).ravel()
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / nb) if nb > 0 else float(np.linalg.norm(a))
+
+
+def _run_slab(params, fixed, moving, dims, lr=1e-4):
+    from paper_2403_16526_b200 import ops
+
+    model = slab_po.SlabModel([torch.from_numpy(p).cuda() for p in params], dims)
+    fl = model.local(torch.from_numpy(fixed).cuda())
+    ml = model.local(torch.from_numpy(moving).cuda())
+    terms, phi = model.loss_step(fl, ml)
+    out = {"terms": terms.cpu().numpy(), "phi": phi.cpu().numpy()}
+    out.update({f"g{i}": g.cpu().numpy() for i, g in enumerate(model.grads)})
+    model.opt.step(lr, model.grads)
+    out.update({f"p{i}": p.detach().cpu().numpy() for i, p in enumerate(model.params)})
+    out["terms2"] = model.loss_step(fl, ml, backward=False)[0].cpu().numpy()
+    trace = [float(model.po_step(fl, ml, lr)[0][0]) for _ in range(PO_ITERS)]
+    out["trace"] = np.array(trace)
+    del ops
+    return out
+
+
+def _model_worker(rank, world, port, dims, case, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    torch.cuda.set_device(0)
+    dist = _init(rank, world, port)
+    try:
+        c = np.load(case)
+        params = [c[f"p{i}"] for i in range(75)]
+        out = _run_slab(params, c["fixed"], c["moving"], dims)
+        np.savez(os.path.join(out_dir, f"m{rank}.npz"), **out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,dims", [(2, (32, 32, 32)), (3, (32, 24, 48))])
+def test_slab_po_matches_single_volume(cuda, ref, tmp_path, world, dims):
+    """The loss step on `world` slabs against (1) the same step on one slab —
+    the decomposition: halos, all-reduced statistics and partial sums,
+    gathered warp planes, returned scatters; (2) the single-volume native
+    model (mdg_model_loss_step): loss, phi and all 75 gradients <= 1e-4;
+    (3) the reference's run_loss_step: loss and phi <= 1e-4, gradients as
+    close as the native model's.  Then Adam steps on the replicated
+    parameters: a short PO trace against the native model's."""
+    from test_gpu_encoder import perturbed_model, shapes, split
+
+    fixed, moving, _, _, _ = ref.synth_pair(dims, seed=3)
+    packed, sizes = perturbed_model(ref, 5)
+    params = [np.ascontiguousarray(a.reshape(s)) for a, s in zip(split(packed, sizes),
+                                                                  shapes(sizes))]
+    case = tmp_path / "case.npz"
+    np.savez(case, fixed=fixed, moving=moving, **{f"p{i}": p for i, p in enumerate(params)})
+    mp.start_processes(_model_worker, args=(world, _free_port(), dims, str(case), str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    parts = [dict(np.load(tmp_path / f"m{r}.npz")) for r in range(world)]
+    one = _run_slab(params, fixed, moving, dims)  # this process alone: one slab
+    for p in parts[1:]:  # replicated: every rank holds the same terms and grads
+        assert np.array_equal(p["terms"], parts[0]["terms"])
+        for i in range(75):
+            assert np.array_equal(p[f"g{i}"], parts[0][f"g{i}"]), i
+    got = parts[0]
+    phi = np.concatenate([p["phi"] for p in parts], axis=1)
+    # 1. the decomposition
+    assert np.allclose(got["terms"], one["terms"], rtol=1e-5, atol=1e-7)
+    assert _rel(phi, one["phi"]) <= 1e-5
+    bad = []
+    for i in range(75):
+        if i in PRE_NORM_BIAS:
+            scale = max(1.0, max(float(np.abs(one[f"g{j}"]).max())
+                                 for j in range(8 * (i // 8), 8 * (i // 8) + 8)))
+            if np.abs(got[f"g{i}"] - one[f"g{i}"]).max() > 1e-4 * scale:
+                bad.append((i, "abs"))
+        elif not _rel(got[f"g{i}"], one[f"g{i}"]) <= 1e-4:
+            bad.append((i, _rel(got[f"g{i}"], one[f"g{i}"])))
+    assert not bad, bad
+    # Adam's first step is lr * sign(g) wherever |g| >> eps, so gradient
+    # entries at rounding level (e.g. the pre-norm biases, exactly 0 in exact
+    # arithmetic) may step either way: parameters agree to 2 lr, and the
+    # bulk exactly
+    for i in range(75):
+        d = np.abs(got[f"p{i}"] - one[f"p{i}"])
+        assert d.max() <= 2.1e-4, i
+        assert np.mean(d > 1e-7) <= (1.0 if i in PRE_NORM_BIAS else 0.02), (i, np.mean(d > 1e-7))
+    assert np.allclose(got["terms2"], one["terms2"], rtol=1e-4, atol=1e-6)
+    # 2. against the single-volume native model (mdg_model_loss_step): the
+    # same kernels, libmdg's own normalisation / loss arithmetic
+    from paper_2403_16526_b200 import ops
+
+    nat = ops.NativeModel([torch.from_numpy(p).cuda() for p in params], dims)
+    tn, phn = nat.loss_step(torch.from_numpy(fixed).cuda(), torch.from_numpy(moving).cuda())
+    assert np.allclose(got["terms"], tn.cpu().numpy(), rtol=1e-4, atol=1e-6)
+    assert _rel(phi, phn.cpu().numpy()) <= 1e-4
+    gn = [g.cpu().numpy() for g in nat.grads]
+    worst = max(_rel(got[f"g{i}"], gn[i]) for i in range(75) if i not in PRE_NORM_BIAS)
+    assert worst <= 1e-4, worst
+    # 3. against the reference's run_loss_step (the gradients as close as the
+    # native model's own, tests/test_gpu_encoder.py)
+    loss_r, gp_r, phi_r = ref.loss_step(fixed, moving, packed, lam=1.0, window=9)
+    assert abs(float(got["terms"][0]) - loss_r) <= 1e-4 * abs(loss_r) + 1e-6
+    assert _rel(phi, phi_r) <= 1e-4
+    theirs = split(gp_r, sizes)
+    for i in range(75):
+        if i not in PRE_NORM_BIAS:
+            assert _rel(got[f"g{i}"], theirs[i]) <= 1.05 * _rel(gn[i], theirs[i]) + 1e-5, i
+    # 4. a short PO trace (the second to fifth iterations' losses) against
+    # the native driver's
+    nat.po_step(torch.from_numpy(fixed).cuda(), torch.from_numpy(moving).cuda(), 1e-4,
+                graph=False)
+    tr = [float(nat.po_step(torch.from_numpy(fixed).cuda(), torch.from_numpy(moving).cuda(),
+                            1e-4, graph=False)[0][0]) for _ in range(PO_ITERS)]
+    assert np.allclose(got["trace"], tr, rtol=1e-4, atol=1e-6), (got["trace"], tr)
