@@ -273,6 +273,33 @@ mdg_status mdg_encoder_conv3_fwd(const float *in, int ic, mdg_dims3 d, const flo
 mdg_status mdg_encoder_conv3_bwd(const float *in, int ic, mdg_dims3 d, const float *w, int oc,
                                  const float *gout, float *gin, float *gw, float *gb,
                                  void *stream);
+/* Depth-slab instance norm + leaky ReLU: op_instance_norm (ops.hpp:162-221)
+ * and op_leaky_relu (:224-238) split at their two global reductions, so a
+ * slab-decomposed caller all-reduces the per-channel sums in between.
+ * x {C, n} (this slab's voxels).
+ *   mdg_in_slab_sums: sums[c] = sum x (mean NULL) or sum (x - mean[c])^2 (fp64)
+ *   mdg_in_lrelu_apply: z = lrelu(g (x - mean) inv + b), given the global
+ *     mean and inv = 1/sqrt(var + 1e-5)
+ *   mdg_in_lrelu_bwd_sums: sums {C, 2} = {sum gy, sum gy xh} (gy = gz lrelu', fp64)
+ *     over the slab — also the beta / gamma gradients before the all-reduce
+ *   mdg_in_lrelu_bwd_apply: gx (written) from the all-reduced sums over the
+ *     nstat voxels of the whole volume (ops.hpp:206-212) */
+mdg_status mdg_in_slab_sums(const float *x, int C, int64_t n, const float *mean, double *sums,
+                            void *stream);
+mdg_status mdg_in_lrelu_apply(const float *x, int C, int64_t n, const float *mean,
+                              const float *inv, const float *g, const float *b, float slope,
+                              float *z, void *stream);
+mdg_status mdg_in_lrelu_bwd_sums(const float *x, const float *gz, int C, int64_t n,
+                                 const float *mean, const float *inv, const float *g,
+                                 const float *b, float slope, double *sums, void *stream);
+mdg_status mdg_in_lrelu_bwd_apply(const float *x, const float *gz, int C, int64_t n,
+                                  const float *mean, const float *inv, const float *g,
+                                  const float *b, float slope, const float *sums, int64_t nstat,
+                                  float *gx, void *stream);
+/* sampling.hpp:171-219 kern::avg_pool_fwd / avg_pool_bwd (2x, odd extents
+ * repeat their last voxel; the backward accumulates gin) */
+mdg_status mdg_avgpool2_fwd(const float *in, int C, mdg_dims3 d, float *out, void *stream);
+mdg_status mdg_avgpool2_bwd(const float *gout, int C, mdg_dims3 d, float *gin, void *stream);
 typedef struct mdg_encoder mdg_encoder;
 /* dims of the full-resolution image (>= 16 per axis, encoder.hpp:95-99) */
 mdg_status mdg_encoder_create(mdg_dims3 d, int base_channels, int levels, float slope,

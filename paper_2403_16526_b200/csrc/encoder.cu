@@ -844,7 +844,8 @@ chan_sum_k(const float *__restrict__ x, int n, const float *__restrict__ mean,
     block_sum<1>(a, part + (int64_t)c * gridDim.x + blockIdx.x);
 }
 
-// stat[c] = sum(part[c]) / n  (inv: 1 / sqrt(. + eps)); fixed order
+// stat[c] = sum(part[c]) / n  (inv = 1: 1 / sqrt(. + eps); inv = 2: the raw
+// sum, for a slab whose statistics are all-reduced); fixed order
 __global__ void __launch_bounds__(256)
 chan_final_k(const float *__restrict__ part, int nparts, int n, int inv, float eps,
              float *__restrict__ stat) {
@@ -856,7 +857,7 @@ chan_final_k(const float *__restrict__ part, int nparts, int n, int inv, float e
     __syncthreads();
     if (threadIdx.x == 0) {
         const float m = r / (float)n;
-        stat[c] = inv ? 1.0f / sqrtf(m + eps) : m;
+        stat[c] = inv == 2 ? r : inv ? 1.0f / sqrtf(m + eps) : m;
     }
 }
 
@@ -993,10 +994,12 @@ __global__ void __launch_bounds__(256)
 in_bwd_apply_k(const float *__restrict__ x, const float *__restrict__ gz, PoolSrc ps, int n,
                const float *__restrict__ mean, const float *__restrict__ inv,
                const float *__restrict__ g, const float *__restrict__ b, float slope,
-               const float *__restrict__ sums, float *__restrict__ gx) {
+               const float *__restrict__ sums, int64_t nstat, float *__restrict__ gx) {
+    // nstat: the voxel count the statistics run over (n, or the whole
+    // volume's for a depth slab)
     const int c = blockIdx.y;
     const float mu = mean[c], iv = inv[c], gg = g[c], bb = b[c];
-    const float k = gg * iv, mg = sums[2 * c] / (float)n, mgx = sums[2 * c + 1] / (float)n;
+    const float k = gg * iv, mg = sums[2 * c] / (float)nstat, mgx = sums[2 * c + 1] / (float)nstat;
     const float *xs = x + (int64_t)c * n;
     float *dst = gx + (int64_t)c * n;
     auto f = [&](float xv, float gv) {
@@ -1015,6 +1018,77 @@ in_bwd_apply_k(const float *__restrict__ x, const float *__restrict__ gz, PoolSr
             dst[i] = f(xs[i], gz_at(gz, ps, c, i));
         }
     }
+}
+
+// ---- depth-slab statistics: per-channel sums accumulated in fp64 (the
+// ranks' shares are all-reduced, so their grouping must not cost accuracy).
+// part[c][blk][v]; fixed order throughout.
+template <int NV>
+__device__ __forceinline__ void block_sum64(double (&v)[NV], double *out) {
+    __shared__ double red[NV][8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+        if (lane == 0) red[k][wid] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double a = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) a += red[threadIdx.x][w];
+        out[threadIdx.x] = a;
+    }
+}
+
+// NV = 1: sum x (mean == nullptr) or sum (x - mean)^2;  NV = 2: the IN
+// backward's {sum gy, sum gy xh}
+template <int NV>
+__global__ void __launch_bounds__(256)
+slab_sum64_k(const float *__restrict__ x, const float *__restrict__ gz, int n,
+             const float *__restrict__ mean, const float *__restrict__ inv,
+             const float *__restrict__ g, const float *__restrict__ b, float slope,
+             double *__restrict__ part) {
+    const int c = blockIdx.y;
+    const float *xs = x + (int64_t)c * n;
+    double a[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) a[k] = 0.0;
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        const float xv = xs[i];
+        if (NV == 1) {
+            if (mean) {
+                const double t = (double)xv - (double)mean[c];
+                a[0] += t * t;
+            } else {
+                a[0] += (double)xv;
+            }
+        } else {
+            const float xh = (xv - mean[c]) * inv[c];
+            const float y = g[c] * xh + b[c];
+            const float gy = gz[(int64_t)c * n + i] * (y > 0.0f ? 1.0f : slope);
+            a[0] += (double)gy;
+            a[NV - 1] += (double)gy * (double)xh;
+        }
+    }
+    block_sum64<NV>(a, part + ((int64_t)c * gridDim.x + blockIdx.x) * NV);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256)
+slab_final64_k(const double *__restrict__ part, int nparts, double *__restrict__ out) {
+    const int c = blockIdx.x;
+    double a[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) a[k] = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += 256)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) a[k] += part[((int64_t)c * nparts + i) * NV + k];
+    __shared__ double r[NV];
+    block_sum64<NV>(a, r);
+    __syncthreads();
+    if (threadIdx.x < NV) out[c * NV + threadIdx.x] = r[threadIdx.x];
 }
 
 // ------------------------------------------------------------ avg pooling 2x
@@ -1380,7 +1454,53 @@ mdg_status enc_in_lrelu_bwd(const float *x, const float *gz, const float *pg, md
     in_bwd_final_k<<<C, 256, 0, st>>>(part.as<float>(), nb, sums, gg, gbeta);
     MDG_LAUNCHED();
     (vec ? in_bwd_apply_k<true> : in_bwd_apply_k<false>)<<<dim3(nb, C), 256, 0, st>>>(
-        x, gz, ps, (int)n, mean, inv, g, b, slope, sums, gx);
+        x, gz, ps, (int)n, mean, inv, g, b, slope, sums, n, gx);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+// ---- depth-slab instance norm: the same kernels with the statistics'
+// sums exposed, so a caller can all-reduce them between the passes
+// sums[c] = sum x (mean == nullptr) or sum (x - mean[c])^2 over this slab (fp64)
+mdg_status enc_in_slab_sums(const float *x, int C, int64_t n, const float *mean, double *sums,
+                            cudaStream_t st) {
+    const unsigned gx = plane_blocks(n, C);
+    Scratch part;
+    MDG_CUDA_TRY(part.alloc((size_t)C * gx * sizeof(double), st));
+    slab_sum64_k<1><<<dim3(gx, C), 256, 0, st>>>(x, nullptr, (int)n, mean, nullptr, nullptr,
+                                                nullptr, 0.0f, part.as<double>());
+    MDG_LAUNCHED();
+    slab_final64_k<1><<<C, 256, 0, st>>>(part.as<double>(), gx, sums);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+// sums[2c..2c+1] = {sum gy, sum gy xh} over this slab (gy = gz lrelu'(y); fp64)
+mdg_status enc_in_slab_bwd_sums(const float *x, const float *gz, int C, int64_t n,
+                                const float *g, const float *b, float slope, const float *mean,
+                                const float *inv, double *sums, cudaStream_t st) {
+    const unsigned nb = plane_blocks(n, C);
+    Scratch part;
+    MDG_CUDA_TRY(part.alloc((size_t)C * nb * 2 * sizeof(double), st));
+    slab_sum64_k<2><<<dim3(nb, C), 256, 0, st>>>(x, gz, (int)n, mean, inv, g, b, slope,
+                                                part.as<double>());
+    MDG_LAUNCHED();
+    slab_final64_k<2><<<C, 256, 0, st>>>(part.as<double>(), nb, sums);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+// gx (written) from the all-reduced sums over nstat voxels
+mdg_status enc_in_slab_bwd_apply(const float *x, const float *gz, int C, int64_t n,
+                                 const float *g, const float *b, float slope, const float *mean,
+                                 const float *inv, const float *sums, int64_t nstat, float *gx,
+                                 cudaStream_t st) {
+    // no pooled gradient: only d.n (gz's channel stride) is read
+    const PoolSrc ps{nullptr, D3{1, 1, 1, (int)n}, D3{1, 1, 1, 1}};
+    const bool vec = n % 4 == 0;
+    const unsigned nb = plane_blocks(vec ? n / 4 : n, C);
+    (vec ? in_bwd_apply_k<true> : in_bwd_apply_k<false>)<<<dim3(nb, C), 256, 0, st>>>(
+        x, gz, ps, (int)n, mean, inv, g, b, slope, sums, nstat, gx);
     MDG_LAUNCHED();
     return MDG_OK;
 }

@@ -90,6 +90,56 @@ mdg_status mdg_encoder_conv3_bwd(const float *in, int ic, mdg_dims3 d, const flo
     return enc_conv3_bwd(in, ic, d, w, oc, gout, gin, gw, gb, S_(stream));
 }
 
+// ---- depth-slab instance norm + leaky ReLU (ops.hpp:162-238 split at the
+// two global reductions; slab_po.py all-reduces the sums in between)
+mdg_status mdg_in_slab_sums(const float *x, int C, int64_t n, const float *mean, double *sums,
+                            void *stream) {
+    MDG_REQUIRE(C >= 1 && n >= 1 && n < (int64_t(1) << 31), "instance_norm: invalid sizes");
+    MDG_REQUIRE(x && sums, "instance_norm: null pointer");
+    return enc_in_slab_sums(x, C, n, mean, sums, S_(stream));
+}
+
+mdg_status mdg_in_lrelu_apply(const float *x, int C, int64_t n, const float *mean,
+                              const float *inv, const float *g, const float *b, float slope,
+                              float *z, void *stream) {
+    MDG_REQUIRE(C >= 1 && n >= 1 && n < (int64_t(1) << 31), "instance_norm: invalid sizes");
+    MDG_REQUIRE(x && mean && inv && g && b && z, "instance_norm: null pointer");
+    return enc_in_lrelu_apply(x, C, n, g, b, slope, z, mean, inv, S_(stream));
+}
+
+mdg_status mdg_in_lrelu_bwd_sums(const float *x, const float *gz, int C, int64_t n,
+                                 const float *mean, const float *inv, const float *g,
+                                 const float *b, float slope, double *sums, void *stream) {
+    MDG_REQUIRE(C >= 1 && n >= 1 && n < (int64_t(1) << 31), "instance_norm: invalid sizes");
+    MDG_REQUIRE(x && gz && mean && inv && g && b && sums, "instance_norm: null pointer");
+    return enc_in_slab_bwd_sums(x, gz, C, n, g, b, slope, mean, inv, sums, S_(stream));
+}
+
+mdg_status mdg_in_lrelu_bwd_apply(const float *x, const float *gz, int C, int64_t n,
+                                  const float *mean, const float *inv, const float *g,
+                                  const float *b, float slope, const float *sums, int64_t nstat,
+                                  float *gx, void *stream) {
+    MDG_REQUIRE(C >= 1 && n >= 1 && n < (int64_t(1) << 31) && nstat >= n,
+                "instance_norm: invalid sizes");
+    MDG_REQUIRE(x && gz && mean && inv && g && b && sums && gx, "instance_norm: null pointer");
+    return enc_in_slab_bwd_apply(x, gz, C, n, g, b, slope, mean, inv, sums, nstat, gx,
+                                 S_(stream));
+}
+
+mdg_status mdg_avgpool2_fwd(const float *in, int C, mdg_dims3 d, float *out, void *stream) {
+    MDG_REQUIRE(C >= 1 && dims_ok(d), "avg_pool: invalid sizes");
+    if (nvox(d) == 0) return MDG_OK;
+    MDG_REQUIRE(in && out, "avg_pool: null pointer");
+    return enc_avgpool_fwd(in, C, d, out, S_(stream));
+}
+
+mdg_status mdg_avgpool2_bwd(const float *gout, int C, mdg_dims3 d, float *gin, void *stream) {
+    MDG_REQUIRE(C >= 1 && dims_ok(d), "avg_pool: invalid sizes");
+    if (nvox(d) == 0) return MDG_OK;
+    MDG_REQUIRE(gout && gin, "avg_pool: null pointer");
+    return enc_avgpool_bwd(gout, C, d, gin, S_(stream));
+}
+
 mdg_status mdg_encoder_create(mdg_dims3 d, int base_channels, int levels, float slope,
                               mdg_encoder **out) {
     MDG_REQUIRE(out, "encoder: null pointer");

@@ -164,6 +164,15 @@ mdg_status enc_in_lrelu_bwd(const float *x, const float *gz, const float *pg, md
                             int C, int64_t n, const float *g, const float *b, float slope,
                             const float *mean, const float *inv, float *gx, float *gg,
                             float *gbeta, cudaStream_t st);
+mdg_status enc_in_slab_sums(const float *x, int C, int64_t n, const float *mean, double *sums,
+                            cudaStream_t st);
+mdg_status enc_in_slab_bwd_sums(const float *x, const float *gz, int C, int64_t n,
+                                const float *g, const float *b, float slope, const float *mean,
+                                const float *inv, double *sums, cudaStream_t st);
+mdg_status enc_in_slab_bwd_apply(const float *x, const float *gz, int C, int64_t n,
+                                 const float *g, const float *b, float slope, const float *mean,
+                                 const float *inv, const float *sums, int64_t nstat, float *gx,
+                                 cudaStream_t st);
 mdg_status enc_avgpool_fwd(const float *in, int C, mdg_dims3 d, float *out, cudaStream_t st);
 mdg_status enc_avgpool_bwd(const float *gout, int C, mdg_dims3 d, float *gin, cudaStream_t st);
 // optim.cu: AdamOptimizer::step over a whole parameter list in one launch

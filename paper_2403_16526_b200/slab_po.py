@@ -37,9 +37,9 @@ levels split without remainder).  The model's ops decompose as follows
 
 The graph is recorded by torch.autograd over these functions (PyTorch is the
 plumbing here: tape, device memory, torch.distributed); every convolution,
-projection, attention, warp and upsample runs in libmdg.  The leaky ReLU, the
-pooling, the normalisation arithmetic and the NCC / grad_reg arithmetic are
-elementwise torch ops between them.  NCCL moves device tensors directly;
+projection, attention, warp, upsample, pooling and instance norm (+ leaky
+ReLU) runs in libmdg.  The NCC / grad_reg arithmetic of the loss is torch
+elementwise and pooling ops.  NCCL moves device tensors directly;
 with gloo (the CPU tests, or several ranks sharing one GPU) the messages are
 staged through host memory.  Parity: tests/test_slab_po.py (the loss and all
 75 gradients against the single-volume native model)."""
@@ -431,21 +431,81 @@ def warp_slab(vol, field, geom, e):
     return _Warp.apply(vol, field, geom, e)
 
 
+def _dptr(t):
+    """pointer of a contiguous float64 device tensor (the fp64 sums)"""
+    if t.dtype != torch.float64 or not t.is_contiguous():
+        raise ops.InvalidInput("slab PO: fp64 sums must be contiguous float64")
+    return t.data_ptr()
+
+
+class _InLrelu(torch.autograd.Function):
+    """lrelu(instance_norm(x)) of a slab (ops.hpp:162-238) by libmdg's
+    encoder kernels, the per-channel sums all-reduced between the passes
+    (mean, then the centred second moment; backward: sum gy, sum gy xh),
+    accumulated in fp64 so the ranks' grouping costs no accuracy.
+    The gamma / beta gradients returned are this slab's share (the
+    parameter-gradient all-reduce adds the ranks')."""
+
+    @staticmethod
+    def forward(ctx, x, g, b, slope, n_global, comm):
+        x = x.contiguous()
+        C, n = x.shape[0], x[0].numel()
+        L, P, st = ops._capi.lib(), ops._ptr, ops._stream()
+        s1 = x.new_empty(C, dtype=torch.float64)
+        ops._check(L.mdg_in_slab_sums(P(x), C, n, None, _dptr(s1), st))
+        mean = (comm.all_reduce(s1) / n_global).float()
+        s2 = x.new_empty(C, dtype=torch.float64)
+        ops._check(L.mdg_in_slab_sums(P(x), C, n, P(mean), _dptr(s2), st))
+        inv = (1.0 / torch.sqrt(comm.all_reduce(s2) / n_global + 1e-5)).float()
+        z = torch.empty_like(x)
+        ops._check(L.mdg_in_lrelu_apply(P(x), C, n, P(mean), P(inv), P(g), P(b), float(slope),
+                                        P(z), st))
+        ctx.save_for_backward(x, g, b, mean, inv)
+        ctx.slope, ctx.n_global, ctx.comm = float(slope), n_global, comm
+        return z
+
+    @staticmethod
+    def backward(ctx, gz):
+        x, g, b, mean, inv = ctx.saved_tensors
+        gz = gz.contiguous()
+        C, n = x.shape[0], x[0].numel()
+        L, P, st = ops._capi.lib(), ops._ptr, ops._stream()
+        sums = x.new_empty(C, 2, dtype=torch.float64)
+        ops._check(L.mdg_in_lrelu_bwd_sums(P(x), P(gz), C, n, P(mean), P(inv), P(g), P(b),
+                                           ctx.slope, _dptr(sums), st))
+        local = sums.float()
+        sums = ctx.comm.all_reduce(sums).float()
+        gx = torch.empty_like(x)
+        ops._check(L.mdg_in_lrelu_bwd_apply(P(x), P(gz), C, n, P(mean), P(inv), P(g), P(b),
+                                            ctx.slope, P(sums), ctx.n_global, P(gx), st))
+        return gx, local[:, 1].contiguous(), local[:, 0].contiguous(), None, None, None
+
+
+class _AvgPool(torch.autograd.Function):
+    """2x average pooling (sampling.hpp:171-219) of a slab: z even per rank,
+    odd x / y extents repeat their last voxel as in the reference"""
+
+    @staticmethod
+    def forward(ctx, x):
+        x = x.contiguous()
+        C, D, W, H = x.shape
+        out = x.new_empty(C, (D + 1) // 2, (W + 1) // 2, (H + 1) // 2)
+        L, P = ops._capi.lib(), ops._ptr
+        ops._check(L.mdg_avgpool2_fwd(P(x), C, ops.dims3((H, W, D)), P(out), ops._stream()))
+        ctx.shape = x.shape
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        C, D, W, H = ctx.shape
+        gin = g.new_zeros(ctx.shape)
+        L, P = ops._capi.lib(), ops._ptr
+        ops._check(L.mdg_avgpool2_bwd(P(g.contiguous()), C, ops.dims3((H, W, D)), P(gin),
+                                      ops._stream()))
+        return gin
+
+
 # ------------------------------------------------------------- the model
-def instance_norm(x, gamma, beta, n_global, comm, eps=1e-5):
-    """ops.hpp:162-221 with the per-channel sums all-reduced"""
-    mean = all_reduce(x.sum((1, 2, 3)), comm) / n_global
-    xc = x - mean[:, None, None, None]
-    var = all_reduce((xc * xc).sum((1, 2, 3)), comm) / n_global
-    inv = 1.0 / torch.sqrt(var + eps)
-    return gamma[:, None, None, None] * xc * inv[:, None, None, None] + beta[:, None, None, None]
-
-
-def leaky_relu(x, slope):
-    """ops.hpp:224-238 (the subgradient at 0 takes the slope)"""
-    return torch.where(x > 0, x, slope * x)
-
-
 def conv_block(x, p, geom, e, slope):
     """op_conv_block (encoder.hpp:87-91); p = (w1, b1, g1, beta1, w2, b2,
     g2, beta2)"""
@@ -453,7 +513,7 @@ def conv_block(x, p, geom, e, slope):
     n = h * w * l
     comm = geom.comm
     for wk, bk, gk, btk in (p[0:4], p[4:8]):
-        x = leaky_relu(instance_norm(conv3_slab(x, wk, bk, comm), gk, btk, n, comm), slope)
+        x = _InLrelu.apply(conv3_slab(x, wk, bk, comm), gk, btk, slope, n, comm)
     return x
 
 
@@ -463,9 +523,7 @@ def encode(image, blocks, geom, slope):
     x = conv_block(image, blocks[0], geom, 0, slope)
     feats.append(x)
     for e in range(1, len(blocks)):
-        # sampling.hpp:171-194: odd x / y extents repeat their last voxel
-        x = F.pad(x, (0, x.shape[3] % 2, 0, x.shape[2] % 2), mode="replicate")
-        x = F.avg_pool3d(x[None], 2)[0]
+        x = _AvgPool.apply(x)
         x = conv_block(x, blocks[e], geom, e, slope)
         feats.append(x)
     return feats
@@ -473,7 +531,10 @@ def encode(image, blocks, geom, slope):
 
 def box_sum(x_ext, r):
     """zero-padded box sums of half-width r of {D+2r, w, h} along z (valid:
-    the halo planes are the padding) then y and x -> {D, w, h}"""
+    the halo planes are the padding) then y and x -> {D, w, h}.  Plain fp32
+    sums of the 2r+1 window terms: NCC's cross / variance terms cancel, so
+    any rescaling rounding (a mean pool times 2r+1) shows up ~1e3x in the
+    gradients."""
     k = 2 * r + 1
     s = x_ext.unfold(0, k, 1).sum(-1)
     s = F.pad(s, (0, 0, r, r)).unfold(1, k, 1).sum(-1)
