@@ -273,6 +273,18 @@ mdg_status mdg_encoder_conv3_fwd(const float *in, int ic, mdg_dims3 d, const flo
 mdg_status mdg_encoder_conv3_bwd(const float *in, int ic, mdg_dims3 d, const float *w, int oc,
                                  const float *gout, float *gin, float *gw, float *gb,
                                  void *stream);
+/* NCC of one depth slab (op_ncc_loss objective.hpp:39-69 split along z):
+ * fixed / warped {1, l, w, h} on the slab's EXTENDED grid e = its own planes
+ * plus window/2 halo planes per side (zero beyond the volume); the planes
+ * [zv0, zv1) of e lie inside the volume (the window counts).
+ *   fwd: *cc_sum (device) = sum of cc over the slab's own planes
+ *        [window/2, e.l - window/2); the caller all-reduces it, ncc = -sum/N
+ *   bwd: gwarped {e} (written) = d(gcc * sum cc)/dwarped; its halo planes hold
+ *        the contributions that belong to the neighbours */
+mdg_status mdg_ncc_slab_fwd(const float *fixed, const float *warped, mdg_dims3 e, int window,
+                            int zv0, int zv1, float *cc_sum, void *stream);
+mdg_status mdg_ncc_slab_bwd(const float *fixed, const float *warped, mdg_dims3 e, int window,
+                            int zv0, int zv1, float gcc, float *gwarped, void *stream);
 /* Depth-slab instance norm + leaky ReLU: op_instance_norm (ops.hpp:162-221)
  * and op_leaky_relu (:224-238) split at their two global reductions, so a
  * slab-decomposed caller all-reduces the per-channel sums in between.

@@ -159,10 +159,13 @@ ncc_products_k(const float *__restrict__ f, const float *__restrict__ g, int n,
     out[4 * n + p] = mul_(a, b);
 }
 
-__device__ __forceinline__ float win_count(int x, int y, int z, const LDims &d, int r) {
+// in-bounds window count; z is bounded by the planes [zv0, zv1) that lie in
+// the volume (the whole grid, or a depth slab's extended grid)
+__device__ __forceinline__ float win_count(int x, int y, int z, const LDims &d, int r, int zv0,
+                                           int zv1) {
     const int cx = min(x + r, d.h - 1) - max(x - r, 0) + 1;
     const int cy = min(y + r, d.w - 1) - max(y - r, 0) + 1;
-    const int cz = min(z + r, d.l - 1) - max(z - r, 0) + 1;
+    const int cz = min(z + r, zv1 - 1) - max(z - r, zv0) + 1;
     return (float)(cx * cy * cz);
 }
 
@@ -183,14 +186,15 @@ __device__ __forceinline__ NccTerms ncc_terms(const float *S, int p, int n, floa
     return t;
 }
 
-// per-CTA partial sums of cc; slot 1..9: grad_reg sums per (component, axis)
+// per-CTA partial sums of cc over the voxels [p0, p1)
 __global__ void __launch_bounds__(kLB)
-ncc_cc_k(const float *__restrict__ S, LDims d, int r, float *__restrict__ part) {
+ncc_cc_k(const float *__restrict__ S, LDims d, int r, int zv0, int zv1, int p0, int p1,
+         float *__restrict__ part) {
     float acc = 0.0f;
-    for (int p = blockIdx.x * kLB + threadIdx.x; p < d.n; p += gridDim.x * kLB) {
+    for (int p = p0 + blockIdx.x * kLB + threadIdx.x; p < p1; p += gridDim.x * kLB) {
         int x, y, z;
         lxyz(p, d, x, y, z);
-        const NccTerms t = ncc_terms(S, p, d.n, win_count(x, y, z, d, r));
+        const NccTerms t = ncc_terms(S, p, d.n, win_count(x, y, z, d, r, zv0, zv1));
         acc += __fdiv_rn(mul_(t.cross, t.cross), t.den);
     }
     __shared__ float red[kLB];
@@ -284,14 +288,20 @@ loss_final_k(const float *__restrict__ cc_part, int ncc_parts, const float *__re
 }
 
 // per-voxel adjoint of cc into the three statistics that depend on g:
-// G = {dL/dsg, dL/dsgg, dL/dsfg}, with dL/dcc = -seed / n
+// G = {dL/dsg, dL/dsgg, dL/dsfg}, with dL/dcc = -seed / n; zero outside the
+// voxels [p0, p1) whose cc is in the loss
 __global__ void __launch_bounds__(kLB)
-ncc_adjoint_k(const float *__restrict__ S, LDims d, int r, float gcc, float *__restrict__ G) {
+ncc_adjoint_k(const float *__restrict__ S, LDims d, int r, float gcc, int zv0, int zv1, int p0,
+              int p1, float *__restrict__ G) {
     const int p = blockIdx.x * kLB + threadIdx.x;
     if (p >= d.n) return;
+    if (p < p0 || p >= p1) {
+        G[p] = G[d.n + p] = G[2 * d.n + p] = 0.0f;
+        return;
+    }
     int x, y, z;
     lxyz(p, d, x, y, z);
-    const NccTerms t = ncc_terms(S, p, d.n, win_count(x, y, z, d, r));
+    const NccTerms t = ncc_terms(S, p, d.n, win_count(x, y, z, d, r, zv0, zv1));
     const float inv_den = 1.0f / t.den;
     const float a = t.cross;
     // cc = a^2 / den, den = vf*vg + eps
@@ -337,6 +347,20 @@ grad_reg_bwd_k(const float *__restrict__ phi, LDims d, float g, float *__restric
         }
         gphi[(int64_t)c * d.n + p] += acc;
     }
+}
+
+__global__ void __launch_bounds__(kLB)
+sum_parts_k(const float *__restrict__ part, int nparts, float *__restrict__ out) {
+    __shared__ float s[kLB];
+    float v = 0.0f;
+    for (int i = threadIdx.x; i < nparts; i += kLB) v += part[i];
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int m = kLB / 2; m > 0; m >>= 1) {
+        if (threadIdx.x < m) s[threadIdx.x] += s[threadIdx.x + m];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = s[0];
 }
 
 // three separable passes a -> b -> a -> b (both buffers owned scratch);
@@ -410,7 +434,7 @@ mdg_status mdg_total_loss_fwd(const float *fixed, const float *moving, const flo
     ncc_products_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(fixed, w, d.n, prod);
     MDG_LAUNCHED();
     if (mdg_status e = box3(prod, 5, d, r, tmp, st)) return e;  // statistics in tmp
-    ncc_cc_k<<<ncc_parts, kLB, 0, st>>>(tmp, d, r, cc_part);
+    ncc_cc_k<<<ncc_parts, kLB, 0, st>>>(tmp, d, r, 0, d.l, 0, d.n, cc_part);
     MDG_LAUNCHED();
     if (lambda != 0.0f) {
         grad_reg_k<<<reg_parts, kLB, 0, st>>>(phi, d, reg_part);
@@ -442,7 +466,7 @@ mdg_status mdg_total_loss_bwd(const float *fixed, const float *moving, const flo
     if (mdg_status e = box3(P, 5, d, r, S, st)) return e;
     // dL/dcc = seed * (-1) * (1/n)  (op_scale / op_mean_all backward)
     const float gcc = -seed * (1.0f / (float)d.n);
-    ncc_adjoint_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(S, d, r, gcc, G);
+    ncc_adjoint_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(S, d, r, gcc, 0, d.l, 0, d.n, G);
     MDG_LAUNCHED();
     if (mdg_status e = box3(G, 3, d, r, P, st)) return e;  // self-adjoint; result in P
     ncc_gwarped_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(P, fixed, w, d.n, gw);
@@ -452,6 +476,61 @@ mdg_status mdg_total_loss_bwd(const float *fixed, const float *moving, const flo
         grad_reg_bwd_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(phi, d, seed * lambda, gphi);
         MDG_LAUNCHED();
     }
+    return MDG_OK;
+}
+
+// ---- NCC of one depth slab (slab_po.py): the extended grid carries r halo
+// planes per side; the slab's own planes are [r, l - r)
+static mdg_status check_slab_ncc(mdg_dims3 e, int window, int zv0, int zv1) {
+    MDG_REQUIRE(dims_ok(e) && nvox(e) > 0, "ncc_slab: invalid dims " + dims_str(e));
+    MDG_REQUIRE(window >= 3 && window % 2 == 1 && window / 2 <= kMaxR,
+                "ncc_slab: window must be odd, >= 3 and <= 25");
+    MDG_REQUIRE(e.l > 2 * (window / 2), "ncc_slab: no own planes inside the halos");
+    MDG_REQUIRE(0 <= zv0 && zv0 <= window / 2 && e.l - window / 2 <= zv1 && zv1 <= e.l,
+                "ncc_slab: the in-volume planes must cover the slab's own planes");
+    return MDG_OK;
+}
+
+mdg_status mdg_ncc_slab_fwd(const float *fixed, const float *warped, mdg_dims3 e, int window,
+                            int zv0, int zv1, float *cc_sum, void *stream) {
+    if (mdg_status er = check_slab_ncc(e, window, zv0, zv1)) return er;
+    MDG_REQUIRE(fixed && warped && cc_sum, "ncc_slab: null pointer");
+    cudaStream_t st = S_(stream);
+    const LDims d{e.h, e.w, e.l, (int)nvox(e)};
+    const int r = window / 2, hw = e.h * e.w;
+    const int parts = (int)std::min<int64_t>(grid1d(d.n, kLB), 148 * 8);
+    Scratch sc;
+    MDG_CUDA_TRY(sc.alloc(((size_t)10 * d.n + parts) * sizeof(float), st));
+    float *prod = sc.as<float>(), *tmp = prod + (size_t)5 * d.n, *part = prod + (size_t)10 * d.n;
+    ncc_products_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(fixed, warped, d.n, prod);
+    MDG_LAUNCHED();
+    if (mdg_status er = box3(prod, 5, d, r, tmp, st)) return er;
+    ncc_cc_k<<<parts, kLB, 0, st>>>(tmp, d, r, zv0, zv1, r * hw, (e.l - r) * hw, part);
+    MDG_LAUNCHED();
+    sum_parts_k<<<1, kLB, 0, st>>>(part, parts, cc_sum);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+mdg_status mdg_ncc_slab_bwd(const float *fixed, const float *warped, mdg_dims3 e, int window,
+                            int zv0, int zv1, float gcc, float *gwarped, void *stream) {
+    if (mdg_status er = check_slab_ncc(e, window, zv0, zv1)) return er;
+    MDG_REQUIRE(fixed && warped && gwarped, "ncc_slab: null pointer");
+    cudaStream_t st = S_(stream);
+    const LDims d{e.h, e.w, e.l, (int)nvox(e)};
+    const int r = window / 2, hw = e.h * e.w;
+    Scratch sc;
+    MDG_CUDA_TRY(sc.alloc((size_t)13 * d.n * sizeof(float), st));
+    float *P = sc.as<float>(), *S = P + (size_t)5 * d.n, *G = P + (size_t)10 * d.n;
+    ncc_products_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(fixed, warped, d.n, P);
+    MDG_LAUNCHED();
+    if (mdg_status er = box3(P, 5, d, r, S, st)) return er;
+    ncc_adjoint_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(S, d, r, gcc, zv0, zv1, r * hw,
+                                                    (e.l - r) * hw, G);
+    MDG_LAUNCHED();
+    if (mdg_status er = box3(G, 3, d, r, P, st)) return er;  // self-adjoint; result in P
+    ncc_gwarped_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(P, fixed, warped, d.n, gwarped);
+    MDG_LAUNCHED();
     return MDG_OK;
 }
 

@@ -37,9 +37,9 @@ levels split without remainder).  The model's ops decompose as follows
 
 The graph is recorded by torch.autograd over these functions (PyTorch is the
 plumbing here: tape, device memory, torch.distributed); every convolution,
-projection, attention, warp, upsample, pooling and instance norm (+ leaky
-ReLU) runs in libmdg.  The NCC / grad_reg arithmetic of the loss is torch
-elementwise and pooling ops.  NCCL moves device tensors directly;
+projection, attention, warp, upsample, pooling, instance norm (+ leaky ReLU)
+and NCC box-sum statistic runs in libmdg; grad_reg's forward differences
+(3 channels, one pass) are torch elementwise ops.  NCCL moves device tensors directly;
 with gloo (the CPU tests, or several ranks sharing one GPU) the messages are
 staged through host memory.  Parity: tests/test_slab_po.py (the loss and all
 75 gradients against the single-volume native model)."""
@@ -47,7 +47,6 @@ from __future__ import annotations
 
 import torch
 import torch.distributed as dist
-import torch.nn.functional as F
 
 from . import ops
 
@@ -529,38 +528,38 @@ def encode(image, blocks, geom, slope):
     return feats
 
 
-def box_sum(x_ext, r):
-    """zero-padded box sums of half-width r of {D+2r, w, h} along z (valid:
-    the halo planes are the padding) then y and x -> {D, w, h}.  Plain fp32
-    sums of the 2r+1 window terms: NCC's cross / variance terms cancel, so
-    any rescaling rounding (a mean pool times 2r+1) shows up ~1e3x in the
-    gradients."""
-    k = 2 * r + 1
-    s = x_ext.unfold(0, k, 1).sum(-1)
-    s = F.pad(s, (0, 0, r, r)).unfold(1, k, 1).sum(-1)
-    return F.pad(s, (r, r)).unfold(2, k, 1).sum(-1)
+class _NccSlab(torch.autograd.Function):
+    """sum of NCC's per-voxel cc over the slab's own voxels (libmdg's box-sum
+    kernels on the extended grid, mdg_ncc_slab_fwd / _bwd)"""
+
+    @staticmethod
+    def forward(ctx, fx, gx, window, zv0, zv1):
+        fx, gx = fx.contiguous(), gx.contiguous()
+        e = ops.dims3(_dims_of(fx))
+        out = fx.new_empty(1)
+        L, P = ops._capi.lib(), ops._ptr
+        ops._check(L.mdg_ncc_slab_fwd(P(fx), P(gx), e, window, zv0, zv1, P(out), ops._stream()))
+        ctx.save_for_backward(fx, gx)
+        ctx.args = (e, window, zv0, zv1)
+        return out[0]
+
+    @staticmethod
+    def backward(ctx, g):
+        fx, gx = ctx.saved_tensors
+        e, window, zv0, zv1 = ctx.args
+        gw = torch.empty_like(gx)
+        L, P = ops._capi.lib(), ops._ptr
+        ops._check(L.mdg_ncc_slab_bwd(P(fx), P(gx), e, window, zv0, zv1, float(g), P(gw),
+                                      ops._stream()))
+        return None, gw, None, None, None
 
 
-def slab_loss(fixed, warped, phi, geom, lam, window):
-    """op_total_loss (objective.hpp:39-78) minus the warp: this rank's part
-    of ncc + lam * grad_reg (the parts add up to the global loss)"""
+def grad_reg_slab(phi, geom):
+    """op_grad_reg (ops.hpp:326-382): this slab's share (forward differences
+    of its planes, the z one reaching the next slab's first plane)"""
     comm = geom.comm
-    (h, w, l), z0, z1, _ = geom.level(0)
+    (h, w, l), _, _, _ = geom.level(0)
     n = h * w * l
-    r = window // 2
-    fx = halo(fixed, r, comm)[0]
-    gx = halo(warped, r, comm)[0]
-    with torch.no_grad():
-        cnt = box_sum(halo(torch.ones_like(fixed), r, comm)[0], r)
-    sf, sg = box_sum(fx, r), box_sum(gx, r)
-    sff, sgg, sfg = box_sum(fx * fx, r), box_sum(gx * gx, r), box_sum(fx * gx, r)
-    cross = sfg - sf * sg / cnt
-    var_f = sff - sf * sf / cnt
-    var_g = sgg - sg * sg / cnt
-    cc = cross * cross / (var_f * var_g + 1e-5)
-    ncc = -cc.sum() / n
-    if lam == 0.0:
-        return ncc, ncc, ncc.new_zeros(())
     ext = halo(phi, 1, comm)
     D = phi.shape[1]
     u = ext[:, 1:1 + D]
@@ -570,7 +569,24 @@ def slab_loss(fixed, warped, phi, geom, lam, window):
     reg = 0.0
     for diff, dim in ((u[..., 1:] - u[..., :-1], h), (u[:, :, 1:] - u[:, :, :-1], w), (dz, l)):
         reg = reg + (diff * diff).sum() / float(n - n // dim)
-    reg = reg / 3.0
+    return reg / 3.0
+
+
+def slab_loss(fixed, warped, phi, geom, lam, window):
+    """op_total_loss (objective.hpp:39-78) minus the warp: this rank's part
+    of ncc + lam * grad_reg (the parts add up to the global loss)"""
+    comm = geom.comm
+    (h, w, l), _, _, _ = geom.level(0)
+    r = window // 2
+    fx = halo(fixed, r, comm)
+    gx = halo(warped, r, comm)
+    D = fixed.shape[1]
+    zv0 = r if comm.rank == 0 else 0
+    zv1 = D + r if comm.rank == comm.world - 1 else D + 2 * r
+    ncc = -_NccSlab.apply(fx, gx, window, zv0, zv1) / float(h * w * l)
+    if lam == 0.0:
+        return ncc, ncc, ncc.new_zeros(())
+    reg = grad_reg_slab(phi, geom)
     return ncc + lam * reg, ncc, reg
 
 

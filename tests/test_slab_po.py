@@ -54,11 +54,46 @@ def _loss_case(dims, seed):
     return fixed, moving, phi
 
 
-def _loss_worker(rank, world, port, dims, out_dir):
+def _box_sum(x_ext, r):
+    """zero-padded box sums (plain fp32 sums of the 2r+1 taps) of
+    {D+2r, w, h}: z valid over the halo planes, then y and x"""
+    F = torch.nn.functional
+    k = 2 * r + 1
+    s = x_ext.unfold(0, k, 1).sum(-1)
+    s = F.pad(s, (0, 0, r, r)).unfold(1, k, 1).sum(-1)
+    return F.pad(s, (r, r)).unfold(2, k, 1).sum(-1)
+
+
+def _torch_slab_loss(fixed, warped, phi, geom, lam, window):
+    """The slab decomposition of op_total_loss in plain torch arithmetic
+    (test infrastructure): checks the halo / partial-sum scheme that
+    slab_po.slab_loss runs with libmdg's kernels, on CPU ranks."""
+    comm = geom.comm
+    (h, w, l), _, _, _ = geom.level(0)
+    n = h * w * l
+    r = window // 2
+    fx = slab_po.halo(fixed, r, comm)[0]
+    gx = slab_po.halo(warped, r, comm)[0]
+    with torch.no_grad():
+        cnt = _box_sum(slab_po.halo(torch.ones_like(fixed), r, comm)[0], r)
+    sf, sg = _box_sum(fx, r), _box_sum(gx, r)
+    sff, sgg, sfg = _box_sum(fx * fx, r), _box_sum(gx * gx, r), _box_sum(fx * gx, r)
+    cross = sfg - sf * sg / cnt
+    var_f = sff - sf * sf / cnt
+    var_g = sgg - sg * sg / cnt
+    cc = cross * cross / (var_f * var_g + 1e-5)
+    ncc = -cc.sum() / n
+    reg = slab_po.grad_reg_slab(phi, geom)
+    return ncc + lam * reg, ncc, reg
+
+
+def _loss_worker(rank, world, port, dims, out_dir, device="cpu"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     import pyoracle
 
+    if device == "cuda":
+        torch.cuda.set_device(0)
     dist = _init(rank, world, port) if world > 1 else None
     try:
         comm = slab_po.Comm()
@@ -66,30 +101,26 @@ def _loss_worker(rank, world, port, dims, out_dir):
         fixed, moving, phi = _loss_case(dims, 5)
         warped = pyoracle.mdo().warp_fwd(moving, phi)  # the warp is tested elsewhere
         z0, z1 = geom.z0, geom.z1
-        f = torch.from_numpy(fixed[:, z0:z1].copy())
-        g = torch.from_numpy(warped[:, z0:z1].copy()).requires_grad_(True)
-        p = torch.from_numpy(phi[:, z0:z1].copy()).requires_grad_(True)
-        total, ncc, reg = slab_po.slab_loss(f, g, p, geom, 1.0, 9)
+        f = torch.from_numpy(fixed[:, z0:z1].copy()).to(device)
+        g = torch.from_numpy(warped[:, z0:z1].copy()).to(device).requires_grad_(True)
+        p = torch.from_numpy(phi[:, z0:z1].copy()).to(device).requires_grad_(True)
+        fn = slab_po.slab_loss if device == "cuda" else _torch_slab_loss
+        total, ncc, reg = fn(f, g, p, geom, 1.0, 9)
         total.backward()
         terms = torch.stack([total.detach(), ncc.detach(), reg.detach()])
         comm.all_reduce(terms)
-        np.savez(os.path.join(out_dir, f"l{rank}.npz"), terms=terms.numpy(),
-                 gw=g.grad.numpy(), gp=p.grad.numpy())
+        np.savez(os.path.join(out_dir, f"l{rank}.npz"), terms=terms.cpu().numpy(),
+                 gw=g.grad.cpu().numpy(), gp=p.grad.cpu().numpy())
     finally:
         if dist is not None:
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dims", [(1, (12, 10, 32)), (2, (12, 10, 32)),
-                                        (3, (9, 11, 48))])
-def test_slab_loss_matches_reference(oracle, ref, tmp_path, world, dims):
-    """ncc + grad_reg over slabs (4-plane NCC halos, 1-plane reg halo, partial
-    sums all-reduced) equal the reference's op_total_loss and its phi
-    gradient (through the oracle's warp adjoint) to fp32 summation order."""
+def _check_loss_case(oracle, ref, tmp_path, world, dims, device):
     if world == 1:
-        _loss_worker(0, 1, 0, dims, str(tmp_path))
+        _loss_worker(0, 1, 0, dims, str(tmp_path), device)
     else:
-        mp.start_processes(_loss_worker, args=(world, _free_port(), dims, str(tmp_path)),
+        mp.start_processes(_loss_worker, args=(world, _free_port(), dims, str(tmp_path), device),
                            nprocs=world, join=True, start_method="spawn")
     fixed, moving, phi = _loss_case(dims, 5)
     m = oracle
@@ -105,6 +136,25 @@ def test_slab_loss_matches_reference(oracle, ref, tmp_path, world, dims):
     g = gfield + gp
     rel = np.linalg.norm(g - gphi_ref) / np.linalg.norm(gphi_ref)
     assert rel < 1e-4, rel
+
+
+@pytest.mark.parametrize("world,dims", [(1, (12, 10, 32)), (2, (12, 10, 32)),
+                                        (3, (9, 11, 48))])
+def test_slab_loss_decomposition_matches_reference(oracle, ref, tmp_path, world, dims):
+    """The slab scheme of the loss (4-plane NCC halos, in-volume window
+    counts, 1-plane reg halo, partial sums all-reduced) in torch arithmetic
+    on CPU ranks equals the reference's op_total_loss and its phi gradient
+    (through the oracle's warp adjoint) to fp32 summation order."""
+    _check_loss_case(oracle, ref, tmp_path, world, dims, "cpu")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,dims", [(1, (12, 10, 32)), (2, (12, 10, 32)),
+                                        (3, (9, 11, 48))])
+def test_slab_loss_kernels_match_reference(cuda, oracle, ref, tmp_path, world, dims):
+    """slab_po.slab_loss (mdg_ncc_slab_fwd / _bwd on the extended grid) on
+    1-3 ranks sharing the GPU: the same criteria as the CPU scheme."""
+    _check_loss_case(oracle, ref, tmp_path, world, dims, "cuda")
 
 
 def _adj_worker(rank, world, port, out_dir):
