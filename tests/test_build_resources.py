@@ -1,0 +1,63 @@
+"""Register / stack budgets of the hot kernels in the built libmdg.so
+(cuobjdump -res-usage; no GPU needed).  A spill that creeps into a hot
+kernel shows up here before it shows up as lost bandwidth.  Budgets are the
+measured values of the kept variants: zero stack for the ModeT, projection,
+encoder-conv and warp-forward kernels; warp_bwd_k keeps 16-24 B at the 48/64
+register caps that measured fastest (profiles/experiments/
+warp_bwd_launch_bounds_r02.log)."""
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                   "paper_2403_16526_b200", "libmdg.so")
+
+# (demangled-name regex, max stack bytes)
+BUDGETS = [
+    (r"mdg::tiled::modet_fwd_tiled_k<6,", 0),
+    (r"mdg::tiled::modet_bwd_row_k<6,", 0),
+    (r"mdg::tiled::modet_bwd_col_k<6,", 0),
+    (r"mdg::warp_fwd_k<", 0),
+    (r"mdg::project_fwd_k<(6|8|16|32),", 0),
+    (r"mdg::project_bwd_k<6, 8,", 0),
+    (r"mdg::enc::conv3t_k<", 0),
+    (r"mdg::enc::conv3w_k<", 0),
+    (r"mdg::warp_bwd_k<(1|2), false, false>", 0),
+    (r"mdg::warp_bwd_k<(3|4|8), (false|true), false>", 24),
+    (r"mdg::warp_bwd_k<16, false, false>", 16),
+]
+
+
+def _usage():
+    if not os.path.exists(LIB) or not shutil.which("cuobjdump") or not shutil.which("c++filt"):
+        pytest.skip("libmdg.so / cuobjdump / c++filt not available")
+    out = subprocess.run(["cuobjdump", "-res-usage", LIB], capture_output=True, text=True).stdout
+    lines = out.splitlines()
+    mangled, usage = [], []
+    for i, line in enumerate(lines):
+        m = re.match(r"\s*Function (\S+):", line)
+        if m and i + 1 < len(lines):
+            r = re.search(r"REG:(\d+) STACK:(\d+)", lines[i + 1])
+            if r:
+                mangled.append(m.group(1))
+                usage.append((int(r.group(1)), int(r.group(2))))
+    names = subprocess.run(["c++filt"], input="\n".join(mangled), capture_output=True,
+                           text=True).stdout.splitlines()
+    return {re.sub(r"\(.*", "", n): u for n, u in zip(names, usage)}
+
+
+def test_hot_kernels_within_register_and_stack_budgets():
+    use = _usage()
+    assert len(use) > 100, "expected the full kernel set in libmdg.so"
+    checked = 0
+    for pat, max_stack in BUDGETS:
+        hits = {n: u for n, u in use.items() if re.search(pat, n)}
+        assert hits, f"no kernel matches {pat}"
+        for n, (reg, stack) in hits.items():
+            assert reg <= 255, (n, reg)
+            assert stack <= max_stack, f"{n}: {stack} B stack (budget {max_stack})"
+            checked += 1
+    assert checked >= 30
