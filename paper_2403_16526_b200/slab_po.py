@@ -278,8 +278,9 @@ class _Project(torch.autograd.Function):
     @staticmethod
     def backward(ctx, gQ, gK):
         f2, m2, W, b, g, beta = ctx.saved_tensors
-        gQ = torch.zeros_like(f2.new_empty(W.shape[0], f2.shape[1])) if gQ is None else gQ
-        gK = torch.zeros_like(gQ) if gK is None else gK
+        zero = f2.new_zeros(W.shape[0], f2.shape[1])
+        gQ = zero if gQ is None else gQ
+        gK = zero if gK is None else gK
         gf, gm, gp = ops.project_qk_bwd(f2, m2, ops.ProjectionParams(W, b, g, beta),
                                         gQ.contiguous(), gK.contiguous(),
                                         layout=ops.MDG_QK_PLANAR)

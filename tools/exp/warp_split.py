@@ -34,3 +34,10 @@ print("field max", float(field.abs().max()))
 print("both   ms", t(lambda: ops.warp_bwd(vol, field, gout, gin=gin, gfield=gf)))
 print("gfield ms", t(lambda: ops.warp_bwd(vol, field, gout, gfield=gf, want_gin=False)))
 print("gin    ms", t(lambda: ops.warp_bwd(vol, field, gout, gin=gin, want_gfield=False)))
+
+for Cc in (1, 2, 4, 8, 16):
+    v = torch.randn(Cc, l, w, h, device="cuda")
+    go = torch.randn(Cc, l, w, h, device="cuda")
+    gi = torch.zeros_like(v)
+    print(f"C={Cc:2d} gin-only ms", round(t(lambda: ops.warp_bwd(v, field, go, gin=gi, want_gfield=False)), 4),
+          "gfield-only ms", round(t(lambda: ops.warp_bwd(v, field, go, gfield=gf, want_gin=False)), 4))
