@@ -267,6 +267,7 @@ def run_ours(args):
     cfg2 = None if args.no_cfg2 else run_cfg2(dev)
 
     peak, peak_kind = load_peak()
+    stress = None if args.no_stress else run_modet_stress(L, rank, dev, st, peak)
     dom = max(per_op, key=lambda k: per_op[k])
     achieved = BYTES[dom] * n / (per_op[dom] * 1e-3) / 1e9
     traffic = op_traffic(dom)
@@ -296,6 +297,7 @@ def run_ours(args):
                           "bytes_per_step": step_bytes},
         "e2e": e2e,
         "warp_random_field": warp_rf,
+        "modet_stress": stress,
         "cfg2": cfg2,
         "pyramid": pyramid,
         "po": po,
@@ -343,6 +345,55 @@ def run_warp_random_field(L, d3, feat, gout, rank, dev, st, reps=10):
     return {"field": "random_field(dims, seed 12, mag 2.0) (test_util.hpp:40-48)",
             "warp_fwd_ms": round(f, 4), "warp_bwd_ms": round(b, 4),
             "Gvoxel_per_s": round(n / ((f + b) * 1e-3) / 1e9, 3)}
+
+
+def run_modet_stress(L, rank, dev, st, peak, reps=5):
+    """SURVEY §8(d) op-at-scale stress: the ModeT operator fwd + bwd with
+    S = 8 heads of d = 8 at 160x192x224 (Q, K {64, n}: 1.76 GB each), the
+    bench.cpp distributions, device-resident; timed beside the headline."""
+    import torch
+
+    from paper_2403_16526_b200 import ops
+
+    S8, D8 = 8, 8
+    n = DIMS[0] * DIMS[1] * DIMS[2]
+    g = torch.Generator(device=dev).manual_seed(77 + rank)
+    Q = torch.rand(S8 * D8, n, device=dev, generator=g) * 2 - 1
+    K = torch.rand(S8 * D8, n, device=dev, generator=g) * 2 - 1
+    B = torch.rand(S8, 27, device=dev, generator=g) - 0.5
+    gSF = torch.rand(3 * S8, n, device=dev, generator=g) * 2 - 1
+    SF = torch.empty(3 * S8, n, device=dev)
+    LSE = torch.empty(S8, n, device=dev)
+    gQ, gK, gB = torch.empty_like(Q), torch.empty_like(K), torch.zeros_like(B)
+    d3 = ops.dims3(DIMS)
+    sp = st.cuda_stream
+    P = lambda t: t.data_ptr()  # noqa: E731
+
+    def go(ev=None):
+        if ev: ev[0].record(st)
+        rc = L.mdg_modet_fwd(P(Q), P(K), P(B), d3, S8, D8, NB, LAYOUT, P(SF), P(LSE), None, sp)
+        if ev: ev[1].record(st)
+        rc |= L.mdg_modet_bwd(P(Q), P(K), P(B), P(SF), P(LSE), P(gSF), d3, S8, D8, NB, LAYOUT,
+                              P(gQ), P(gK), P(gB), 0, sp)
+        if ev: ev[2].record(st)
+        if rc:
+            raise RuntimeError(L.mdg_last_error().decode())
+
+    for _ in range(2):
+        go()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(reps)]
+    for e in evs:
+        go(e)
+    torch.cuda.synchronize()
+    f = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
+    b = statistics.median(e[1].elapsed_time(e[2]) for e in evs)
+    fwd_bytes, bwd_bytes = 4 * (2 * S8 * D8 + 3 * S8) * n, 4 * (4 * S8 * D8 + 3 * S8) * n
+    return {"workload": "ModeT fwd+bwd, S=8, d=8, nb=3 at 160x192x224 (SURVEY 8d stress)",
+            "fwd_ms": round(f, 4), "bwd_ms": round(b, 4),
+            "Gvoxel_per_s": round(n / ((f + b) * 1e-3) / 1e9, 3),
+            "frac_fwd": round(fwd_bytes / (f * 1e-3) / 1e9 / peak, 4),
+            "frac_bwd": round(bwd_bytes / (b * 1e-3) / 1e9 / peak, 4),
+            "alg_bytes_fwd_bwd": fwd_bytes + bwd_bytes}
 
 
 def run_cfg2(dev, reps=5):
@@ -731,6 +782,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling)")
     ap.add_argument("--no-pyramid", action="store_true", help="skip the pyramid timing")
     ap.add_argument("--no-po", action="store_true", help="skip the PO-iteration timing")
+    ap.add_argument("--no-stress", action="store_true",
+                    help="skip the S=8, d=8 ModeT stress timing")
     ap.add_argument("--no-random-field", action="store_true",
                     help="skip the random_field warp timing")
     ap.add_argument("--no-cfg2", action="store_true", help="skip the config-2 forward timing")
