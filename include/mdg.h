@@ -147,6 +147,14 @@ mdg_status mdg_warp_fwd_slab(const float *in, int C, mdg_dims3 d, int zi0, int z
 mdg_status mdg_warp_bwd_slab(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
                              const float *field, const float *gout, float *gin, float *gfield,
                              int z0, int z1, void *stream);
+/* The same without the synchronous window check: a violation ORs 1 into the
+ * caller's device word *err (read it when convenient; graph-capturable). */
+mdg_status mdg_warp_fwd_slab_async(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                                   const float *field, float *out, int z0, int z1,
+                                   unsigned *err, void *stream);
+mdg_status mdg_warp_bwd_slab_async(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                                   const float *field, const float *gout, float *gin,
+                                   float *gfield, int z0, int z1, unsigned *err, void *stream);
 /* sampling.hpp:225-242 kern::upsample2_fwd (target range checked as in
  * sampling.hpp:266-271 -> MDG_EINVAL) */
 mdg_status mdg_upsample2_fwd(const float *in, int C, mdg_dims3 d, mdg_dims3 td, float scale,
@@ -285,6 +293,11 @@ mdg_status mdg_ncc_slab_fwd(const float *fixed, const float *warped, mdg_dims3 e
                             int zv0, int zv1, float *cc_sum, void *stream);
 mdg_status mdg_ncc_slab_bwd(const float *fixed, const float *warped, mdg_dims3 e, int window,
                             int zv0, int zv1, float gcc, float *gwarped, void *stream);
+/* as mdg_ncc_slab_bwd with dL/dcc = gcc * (*gscale), gscale a device scalar
+ * (the upstream gradient without a host round trip: graph-capturable) */
+mdg_status mdg_ncc_slab_bwd_dev(const float *fixed, const float *warped, mdg_dims3 e, int window,
+                                int zv0, int zv1, float gcc, const float *gscale,
+                                float *gwarped, void *stream);
 /* Depth-slab instance norm + leaky ReLU: op_instance_norm (ops.hpp:162-221)
  * and op_leaky_relu (:224-238) split at their two global reductions, so a
  * slab-decomposed caller all-reduces the per-channel sums in between.

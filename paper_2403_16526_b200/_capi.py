@@ -116,6 +116,9 @@ SIGNATURES = {
     "mdg_warp_bwd_slab": (_st, [_p, _i, Dims3, _i, _i, _p, _p, _p, _p, _i, _i, _p]),
     "mdg_ncc_slab_fwd": (_st, [_p, _p, Dims3, _i, _i, _i, _p, _p]),
     "mdg_ncc_slab_bwd": (_st, [_p, _p, Dims3, _i, _i, _i, C.c_float, _p, _p]),
+    "mdg_ncc_slab_bwd_dev": (_st, [_p, _p, Dims3, _i, _i, _i, C.c_float, _p, _p, _p]),
+    "mdg_warp_fwd_slab_async": (_st, [_p, _i, Dims3, _i, _i, _p, _p, _i, _i, _p, _p]),
+    "mdg_warp_bwd_slab_async": (_st, [_p, _i, Dims3, _i, _i, _p, _p, _p, _p, _i, _i, _p, _p]),
     "mdg_in_slab_sums": (_st, [_p, _i, C.c_int64, _p, _p, _p]),
     "mdg_in_lrelu_apply": (_st, [_p, _i, C.c_int64, _p, _p, _p, _p, C.c_float, _p, _p]),
     "mdg_in_lrelu_bwd_sums": (_st, [_p, _p, _i, C.c_int64, _p, _p, _p, _p, C.c_float, _p, _p]),

@@ -292,7 +292,10 @@ loss_final_k(const float *__restrict__ cc_part, int ncc_parts, const float *__re
 // voxels [p0, p1) whose cc is in the loss
 __global__ void __launch_bounds__(kLB)
 ncc_adjoint_k(const float *__restrict__ S, LDims d, int r, float gcc, int zv0, int zv1, int p0,
-              int p1, float *__restrict__ G) {
+              int p1, float *__restrict__ G, const float *__restrict__ gscale = nullptr) {
+    // gscale (device, nullable): dL/dcc = gcc * *gscale (the upstream gradient
+    // read on the device: no host round trip inside a captured graph)
+    if (gscale) gcc *= *gscale;
     const int p = blockIdx.x * kLB + threadIdx.x;
     if (p >= d.n) return;
     if (p < p0 || p >= p1) {
@@ -512,8 +515,9 @@ mdg_status mdg_ncc_slab_fwd(const float *fixed, const float *warped, mdg_dims3 e
     return MDG_OK;
 }
 
-mdg_status mdg_ncc_slab_bwd(const float *fixed, const float *warped, mdg_dims3 e, int window,
-                            int zv0, int zv1, float gcc, float *gwarped, void *stream) {
+static mdg_status ncc_slab_bwd_impl(const float *fixed, const float *warped, mdg_dims3 e,
+                                    int window, int zv0, int zv1, float gcc,
+                                    const float *gscale, float *gwarped, void *stream) {
     if (mdg_status er = check_slab_ncc(e, window, zv0, zv1)) return er;
     MDG_REQUIRE(fixed && warped && gwarped, "ncc_slab: null pointer");
     cudaStream_t st = S_(stream);
@@ -526,12 +530,24 @@ mdg_status mdg_ncc_slab_bwd(const float *fixed, const float *warped, mdg_dims3 e
     MDG_LAUNCHED();
     if (mdg_status er = box3(P, 5, d, r, S, st)) return er;
     ncc_adjoint_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(S, d, r, gcc, zv0, zv1, r * hw,
-                                                    (e.l - r) * hw, G);
+                                                    (e.l - r) * hw, G, gscale);
     MDG_LAUNCHED();
     if (mdg_status er = box3(G, 3, d, r, P, st)) return er;  // self-adjoint; result in P
     ncc_gwarped_k<<<grid1d(d.n, kLB), kLB, 0, st>>>(P, fixed, warped, d.n, gwarped);
     MDG_LAUNCHED();
     return MDG_OK;
+}
+
+mdg_status mdg_ncc_slab_bwd(const float *fixed, const float *warped, mdg_dims3 e, int window,
+                            int zv0, int zv1, float gcc, float *gwarped, void *stream) {
+    return ncc_slab_bwd_impl(fixed, warped, e, window, zv0, zv1, gcc, nullptr, gwarped, stream);
+}
+
+mdg_status mdg_ncc_slab_bwd_dev(const float *fixed, const float *warped, mdg_dims3 e, int window,
+                                int zv0, int zv1, float gcc, const float *gscale,
+                                float *gwarped, void *stream) {
+    MDG_REQUIRE(gscale, "ncc_slab: null gradient scale");
+    return ncc_slab_bwd_impl(fixed, warped, e, window, zv0, zv1, gcc, gscale, gwarped, stream);
 }
 
 }  // extern "C"

@@ -732,9 +732,19 @@ static mdg_status check_slab(mdg_dims3 d, int C, int zi0, int zi1, int z0, int z
     return MDG_OK;
 }
 
+// err_dev non-null: the caller's device word collects violations (no sync,
+// graph-capturable); null: a scratch word, read back synchronously
 static mdg_status slab_run(mdg_dims3 d, int zi0, int zi1, int z0, int z1, cudaStream_t st,
+                           unsigned *err_dev,
                            const std::function<void(const WarpWin &)> &launch) {
     const int64_t hw = (int64_t)d.h * d.w;
+    if (err_dev) {
+        const WarpWin win{(zi1 - zi0) * hw, (z1 - z0) * hw, z0 * hw, zi0, zi1, (int)(zi0 * hw),
+                          err_dev};
+        launch(win);
+        MDG_LAUNCHED();
+        return MDG_OK;
+    }
     Scratch ws;
     MDG_CUDA_TRY(ws.alloc(sizeof(unsigned), st));
     unsigned *err = ws.as<unsigned>();
@@ -750,24 +760,26 @@ static mdg_status slab_run(mdg_dims3 d, int zi0, int zi1, int z0, int z1, cudaSt
     return MDG_OK;
 }
 
-mdg_status mdg_warp_fwd_slab(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
-                             const float *field, float *out, int z0, int z1, void *stream) {
+static mdg_status warp_fwd_slab_impl(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                                     const float *field, float *out, int z0, int z1,
+                                     unsigned *err_dev, void *stream) {
     if (mdg_status e = check_slab(d, C, zi0, zi1, z0, z1)) return e;
     const int64_t hw = (int64_t)d.h * d.w;
     if (z1 == z0 || C == 0 || hw == 0) return MDG_OK;
     MDG_REQUIRE(in && field && out, "warp slab: null pointer");
     const int64_t pb = z0 * hw, pe = z1 * hw;
     cudaStream_t st = S_(stream);
-    return slab_run(d, zi0, zi1, z0, z1, st, [&](const WarpWin &win) {
+    return slab_run(d, zi0, zi1, z0, z1, st, err_dev, [&](const WarpWin &win) {
         MDG_WARP_DISPATCH_T(warp_fwd_k, (true), d.h >= 2 ? C : 0,
                             (grid1d(pe - pb, kSB), kSB, 0, st),
                             (in, C, d.h, d.w, d.l, field, out, pb, pe, win));
     });
 }
 
-mdg_status mdg_warp_bwd_slab(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
-                             const float *field, const float *gout, float *gin, float *gfield,
-                             int z0, int z1, void *stream) {
+static mdg_status warp_bwd_slab_impl(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                                     const float *field, const float *gout, float *gin,
+                                     float *gfield, int z0, int z1, unsigned *err_dev,
+                                     void *stream) {
     if (mdg_status e = check_slab(d, C, zi0, zi1, z0, z1)) return e;
     const int64_t hw = (int64_t)d.h * d.w;
     if (z1 == z0 || C == 0 || hw == 0 || (!gin && !gfield)) return MDG_OK;
@@ -776,11 +788,37 @@ mdg_status mdg_warp_bwd_slab(const float *in, int C, mdg_dims3 d, int zi0, int z
     cudaStream_t st = S_(stream);
     // gin by the float-atomic scatter (the deterministic gather works on
     // whole-volume buffers only)
-    return slab_run(d, zi0, zi1, z0, z1, st, [&](const WarpWin &win) {
+    return slab_run(d, zi0, zi1, z0, z1, st, err_dev, [&](const WarpWin &win) {
         MDG_WARP_DISPATCH_T(warp_bwd_k, (false, true), d.h >= 2 ? C : 0,
                             (grid1d(pe - pb, kSB), kSB, 0, st),
                             (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe, win));
     });
+}
+
+mdg_status mdg_warp_fwd_slab(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                             const float *field, float *out, int z0, int z1, void *stream) {
+    return warp_fwd_slab_impl(in, C, d, zi0, zi1, field, out, z0, z1, nullptr, stream);
+}
+
+mdg_status mdg_warp_bwd_slab(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                             const float *field, const float *gout, float *gin, float *gfield,
+                             int z0, int z1, void *stream) {
+    return warp_bwd_slab_impl(in, C, d, zi0, zi1, field, gout, gin, gfield, z0, z1, nullptr,
+                              stream);
+}
+
+mdg_status mdg_warp_fwd_slab_async(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                                   const float *field, float *out, int z0, int z1,
+                                   unsigned *err, void *stream) {
+    MDG_REQUIRE(err, "warp slab: null error word");
+    return warp_fwd_slab_impl(in, C, d, zi0, zi1, field, out, z0, z1, err, stream);
+}
+
+mdg_status mdg_warp_bwd_slab_async(const float *in, int C, mdg_dims3 d, int zi0, int zi1,
+                                   const float *field, const float *gout, float *gin,
+                                   float *gfield, int z0, int z1, unsigned *err, void *stream) {
+    MDG_REQUIRE(err, "warp slab: null error word");
+    return warp_bwd_slab_impl(in, C, d, zi0, zi1, field, gout, gin, gfield, z0, z1, err, stream);
 }
 
 mdg_status mdg_compose_fwd(const float *prev, const float *res, mdg_dims3 d, float *out,

@@ -130,13 +130,22 @@ def split_units(l: int, world: int):
 
 class Geom:
     """Global dims (h, w, l) of the full-resolution grid and this rank's
-    z range; level e (0 = full resolution) divides everything by 2^e."""
+    z range; level e (0 = full resolution) divides everything by 2^e.
 
-    def __init__(self, dims, comm: Comm):
+    reach None: every warp all-reduces its data-dependent reach (a host
+    round trip per warp).  reach R: the warps exchange R planes per side
+    without looking at the field, a field that samples further is flagged on
+    the device (err) and reported after the step — no host round trip
+    inside the step, so it can be captured as one CUDA graph."""
+
+    def __init__(self, dims, comm: Comm, reach=None):
         self.dims = tuple(int(v) for v in dims)
         self.comm = comm
         self.ranges = split_units(self.dims[2], comm.world)
         self.z0, self.z1 = self.ranges[comm.rank]
+        self.reach = None if reach is None else int(reach)
+        self.err = None  # device int32 word of the fixed-reach mode
+        self.defer_checks = self.reach is not None
 
     def level(self, e):
         """(dims, z0, z1, all ranks' ranges) of level e; dims halve rounding
@@ -293,14 +302,15 @@ class _ModeT(torch.autograd.Function):
     Q/K {S*d, D+2, w, h}; the numeric check reports global positions"""
 
     @staticmethod
-    def forward(ctx, Qx, Kx, B, S, hd, z_shift):
+    def forward(ctx, Qx, Kx, B, S, hd, z_shift, defer=False):
         d = _dims_of(Qx)
         cfg = ops.AttentionConfig(S, hd, 3)
         Q2, K2 = Qx.reshape(S * hd, -1).contiguous(), Kx.reshape(S * hd, -1).contiguous()
         SF, LSE = ops.modet_fwd(Q2, K2, B.contiguous(), d, cfg, layout=ops.MDG_QK_PLANAR,
                                 check=False)
         try:
-            ops.check_numeric(d)
+            if not defer:  # else the stream's flag is read once after the step
+                ops.check_numeric(d)
         except ops.NumericError as e:
             pos = getattr(e, "position", None)
             if pos is not None and pos[2] >= 0:
@@ -316,7 +326,7 @@ class _ModeT(torch.autograd.Function):
         gQ, gK, gB = ops.modet_bwd(Q2, K2, B, SF, LSE, gSF.reshape(SF.shape).contiguous(), ctx.d,
                                    ctx.cfg, layout=ops.MDG_QK_PLANAR)
         shp = (Q2.shape[0], *gSF.shape[1:])
-        return gQ.view(shp), gK.view(shp), gB, None, None, None
+        return gQ.view(shp), gK.view(shp), gB, None, None, None, None
 
 
 class _Upsample(torch.autograd.Function):
@@ -361,7 +371,8 @@ class _Warp(torch.autograd.Function):
     def forward(ctx, vol, field, geom, e):
         comm = geom.comm
         (h, w, l), z0, z1, ranges = geom.level(e)
-        R = comm.all_reduce_max_int(warp_reach(field, l))
+        R = geom.reach if geom.reach is not None else \
+            comm.all_reduce_max_int(warp_reach(field, l))
         need = [(max(0, a - R), min(l, b + R)) for a, b in ranges]
         lo, hi = need[comm.rank]
         vol = vol.contiguous()
@@ -382,8 +393,13 @@ class _Warp(torch.autograd.Function):
         field = field.contiguous()
         out = torch.empty_like(vol)
         L, P = ops._capi.lib(), ops._ptr
-        ops._check(L.mdg_warp_fwd_slab(P(win), C, ops.dims3((h, w, l)), lo, hi, P(field),
-                                       P(out), z0, z1, ops._stream()))
+        if geom.err is not None:
+            ops._check(L.mdg_warp_fwd_slab_async(P(win), C, ops.dims3((h, w, l)), lo, hi,
+                                                 P(field), P(out), z0, z1, geom.err.data_ptr(),
+                                                 ops._stream()))
+        else:
+            ops._check(L.mdg_warp_fwd_slab(P(win), C, ops.dims3((h, w, l)), lo, hi, P(field),
+                                           P(out), z0, z1, ops._stream()))
         ctx.save_for_backward(win, field)
         ctx.geom, ctx.e, ctx.need = geom, e, need
         return out
@@ -399,9 +415,15 @@ class _Warp(torch.autograd.Function):
         gin_w = torch.zeros_like(win)
         gfield = torch.zeros_like(field)
         L, P = ops._capi.lib(), ops._ptr
-        ops._check(L.mdg_warp_bwd_slab(P(win), C, ops.dims3((h, w, l)), lo, hi, P(field),
-                                       P(gout.contiguous()), P(gin_w), P(gfield), z0, z1,
-                                       ops._stream()))
+        if geom.err is not None:
+            ops._check(L.mdg_warp_bwd_slab_async(P(win), C, ops.dims3((h, w, l)), lo, hi,
+                                                 P(field), P(gout.contiguous()), P(gin_w),
+                                                 P(gfield), z0, z1, geom.err.data_ptr(),
+                                                 ops._stream()))
+        else:
+            ops._check(L.mdg_warp_bwd_slab(P(win), C, ops.dims3((h, w, l)), lo, hi, P(field),
+                                           P(gout.contiguous()), P(gin_w), P(gfield), z0, z1,
+                                           ops._stream()))
         # contributions to other ranks' planes go back to their owners,
         # summed there in rank order
         sends, recvs, got = [], [], {}
@@ -550,8 +572,9 @@ class _NccSlab(torch.autograd.Function):
         e, window, zv0, zv1 = ctx.args
         gw = torch.empty_like(gx)
         L, P = ops._capi.lib(), ops._ptr
-        ops._check(L.mdg_ncc_slab_bwd(P(fx), P(gx), e, window, zv0, zv1, float(g), P(gw),
-                                      ops._stream()))
+        g = g.reshape(1).contiguous()  # read on the device: no host round trip
+        ops._check(L.mdg_ncc_slab_bwd_dev(P(fx), P(gx), e, window, zv0, zv1, 1.0, P(g), P(gw),
+                                          ops._stream()))
         return None, gw, None, None, None
 
 
@@ -595,19 +618,26 @@ class SlabModel:
     """The small-preset model (or any base_channels / heads / head_dim) with
     its PO iteration decomposed over depth slabs.  `tensors`: the 75
     ModelParams tensors (ops.init_model order), replicated on every rank;
-    images are this rank's planes {1, z1-z0, w, h}."""
+    images are this rank's planes {1, z1-z0, w, h}.
+
+    reach: None (each warp all-reduces its data-dependent reach) or a fixed
+    plane count R (see Geom) — the mode po_step(..., graph=True) captures as
+    one CUDA graph per iteration."""
 
     def __init__(self, tensors, dims, lam=1.0, window=9, slope=0.2, heads=(8, 4, 2, 1, 1),
-                 head_dim=6, comm: Comm | None = None):
+                 head_dim=6, comm: Comm | None = None, reach=None):
         self.comm = comm or Comm()
-        self.geom = Geom(dims, self.comm)
+        self.geom = Geom(dims, self.comm, reach)
         self.params = [t.detach().clone().contiguous().requires_grad_(True) for t in tensors]
         if len(self.params) != 75:
             raise ops.InvalidInput("slab PO: expects the 75 ModelParams tensors")
+        if reach is not None:
+            self.geom.err = torch.zeros(1, dtype=torch.int32, device=self.params[0].device)
         self.lam, self.window, self.slope = float(lam), int(window), float(slope)
         self.heads, self.hd = tuple(heads), int(head_dim)
         self.opt = ops.AdamOptimizer([p.data for p in self.params])
         self.grads = [torch.zeros_like(p) for p in self.params]
+        self._graph = None
 
     @property
     def z_range(self):
@@ -639,17 +669,16 @@ class SlabModel:
             shp = (S * self.hd, *f.shape[1:])
             Qx, Kx = halo(Q.view(shp), 1, comm), halo(K.view(shp), 1, comm)
             _, z0, _, _ = geom.level(e)
-            SF = _ModeT.apply(Qx, Kx, B, S, self.hd, z0 - 1)[:, 1:-1]
+            SF = _ModeT.apply(Qx, Kx, B, S, self.hd, z0 - 1, geom.defer_checks)[:, 1:-1]
             res = conv3_slab(SF, rw, rb, comm)
             phi = res if k == 0 else res + warp_slab(phi_up, res, geom, e)
         return phi
 
-    def loss_step(self, fixed, moving, backward=True):
-        """run_loss_step (engine.hpp:316-340): the global {total, ncc, reg}
-        (identical on every rank) and this rank's phi; with backward, the
-        all-reduced parameter gradients in self.grads."""
-        for p in self.params:
-            p.grad = None
+    def _body(self, fixed, moving, backward):
+        """forward (+ backward and the gradient all-reduce into self.grads)
+        with no host round trip when the reach is fixed"""
+        if self.geom.err is not None:
+            self.geom.err.zero_()
         with torch.set_grad_enabled(backward):
             phi = self.forward(fixed, moving)
             warped = warp_slab(moving, phi, self.geom, 0)
@@ -669,8 +698,64 @@ class SlabModel:
                 o += g.numel()
         return terms, phi.detach()
 
-    def po_step(self, fixed, moving, lr=1e-4):
-        """one pairwise_optimize iteration (engine.hpp:389-398)"""
-        terms, phi = self.loss_step(fixed, moving, backward=True)
+    def _post_check(self):
+        """the checks a fixed-reach step defers to its end"""
+        if not self.geom.defer_checks:
+            return
+        ops.check_numeric(self.geom.dims)
+        if int(self.geom.err.item()):
+            raise ops.InvalidInput(f"slab PO: the field sampled beyond the fixed reach of "
+                                   f"{self.geom.reach} planes; construct with a larger reach")
+
+    def loss_step(self, fixed, moving, backward=True):
+        """run_loss_step (engine.hpp:316-340): the global {total, ncc, reg}
+        (identical on every rank) and this rank's phi; with backward, the
+        all-reduced parameter gradients in self.grads."""
+        for p in self.params:
+            p.grad = None
+        out = self._body(fixed, moving, backward)
+        self._post_check()
+        return out
+
+    def _replay(self, fixed, moving):
+        """the loss step as one CUDA graph (captured on first use; the images
+        are copied into the graph's static inputs)"""
+        if self._graph is None:
+            if self.geom.reach is None:
+                raise ops.InvalidInput("slab PO: graph mode needs a fixed reach")
+            if self.comm.staged:
+                raise ops.InvalidInput("slab PO: graph mode needs NCCL (or one rank)")
+            self._sf, self._sm = fixed.clone(), moving.clone()
+            for p in self.params:
+                p.grad = torch.zeros_like(p)
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for _ in range(2):  # warm-up (allocator, autograd, tensor maps)
+                    for p in self.params:
+                        p.grad.zero_()
+                    self._body(self._sf, self._sm, True)
+            torch.cuda.current_stream().wait_stream(side)
+            self._graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self._graph):
+                for p in self.params:
+                    p.grad.zero_()
+                self._gout = self._body(self._sf, self._sm, True)
+        if fixed.data_ptr() != self._sf.data_ptr():
+            self._sf.copy_(fixed)
+        if moving.data_ptr() != self._sm.data_ptr():
+            self._sm.copy_(moving)
+        self._graph.replay()
+        self._post_check()
+        return self._gout[0].clone(), self._gout[1].clone()
+
+    def po_step(self, fixed, moving, lr=1e-4, graph=False):
+        """one pairwise_optimize iteration (engine.hpp:389-398); graph=True
+        replays the loss step as a CUDA graph (fixed reach) and runs Adam
+        after it"""
+        if graph:
+            terms, phi = self._replay(fixed, moving)
+        else:
+            terms, phi = self.loss_step(fixed, moving, backward=True)
         self.opt.step(lr, self.grads)
         return terms, phi

@@ -369,3 +369,67 @@ def test_slab_instance_norm_and_pool_entry_points(cuda):
     pq = torch.nn.functional.pad(xq[None], (0, 1, 0, 1, 0, 0), mode="replicate")[0]
     torch.nn.functional.avg_pool3d(pq[None], 2)[0].backward(go.double())
     assert torch.allclose(xp.grad.double(), xq.grad, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.gpu
+def test_slab_po_fixed_reach_and_graph_replay(cuda, ref):
+    """The fixed-reach mode (no host round trip inside the step) equals the
+    data-dependent one; its CUDA-graph replay equals its eager step (to the
+    gin scatter's atomic order); a reach the field exceeds is reported."""
+    from test_gpu_encoder import perturbed_model, shapes, split
+
+    dims = (32, 32, 32)
+    fixed, moving, _, _, _ = ref.synth_pair(dims, seed=3)
+    packed, sizes = perturbed_model(ref, 5)
+    params = [torch.from_numpy(np.ascontiguousarray(a.reshape(s))).cuda()
+              for a, s in zip(split(packed, sizes), shapes(sizes))]
+    f, m = torch.from_numpy(fixed).cuda(), torch.from_numpy(moving).cuda()
+    base = slab_po.SlabModel(params, dims)
+    t0, phi0 = base.loss_step(f, m)
+    g0 = [g.clone() for g in base.grads]
+    fixedr = slab_po.SlabModel(params, dims, reach=6)
+    t1, phi1 = fixedr.loss_step(f, m)
+    assert torch.equal(t0, t1) and torch.equal(phi0, phi1)
+
+    def close(ga, gb, tol):
+        for i, (a, b) in enumerate(zip(ga, gb)):
+            a, b = a.cpu().numpy(), b.cpu().numpy()
+            if i in PRE_NORM_BIAS:  # rounding-level values (0 in exact arithmetic)
+                assert np.abs(a - b).max() <= 1e-6, i
+            else:
+                assert _rel(a, b) <= tol, (i, _rel(a, b))
+
+    # (the warps' gin scatter adds in atomic order; some gradients amplify
+    # that rounding to ~2e-4, see the model test above)
+    close(fixedr.grads, g0, 1e-3)
+    # graph: two PO iterations replayed against two eager ones
+    eager = slab_po.SlabModel(params, dims, reach=6)
+    graph = slab_po.SlabModel(params, dims, reach=6)
+    for it in range(2):
+        te, pe = eager.po_step(f, m)
+        tg, pg = graph.po_step(f, m, graph=True)
+        assert torch.allclose(te, tg, rtol=1e-5, atol=1e-7), (it, te, tg)
+        assert _rel(pg.cpu().numpy(), pe.cpu().numpy()) <= 1e-5
+        close(graph.grads, eager.grads, 1e-3)
+    # a violation flagged by the async slab warps surfaces after the step
+    graph.geom.err.fill_(1)
+    with pytest.raises(ValueError, match="fixed reach"):
+        graph._post_check()
+    # ... and the async entry points flag it on the device (no sync, no raise)
+    from paper_2403_16526_b200 import ops
+    h, w, l = 12, 10, 16
+    vol = torch.randn(2, l, w, h, device="cuda")
+    fld = torch.zeros(3, 6, w, h, device="cuda")
+    fld[2] = 3.5  # 3.5 planes down: beyond a 1-plane window
+    out = torch.empty(2, 6, w, h, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    L, P = ops._capi.lib(), ops._ptr
+    win = vol[:, 4:12].contiguous()  # planes [4, 12) for the slab [5, 11)
+    ops._check(L.mdg_warp_fwd_slab_async(P(win), 2, ops.dims3((h, w, l)), 4, 12, P(fld), P(out),
+                                         5, 11, err.data_ptr(), ops._stream()))
+    assert int(err.item()) == 1
+    err.zero_()
+    fld[2] = 0.25  # the last plane samples 10.25: corners 10 and 11, inside
+    ops._check(L.mdg_warp_fwd_slab_async(P(win), 2, ops.dims3((h, w, l)), 4, 12, P(fld), P(out),
+                                         5, 11, err.data_ptr(), ops._stream()))
+    assert int(err.item()) == 0

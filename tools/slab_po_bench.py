@@ -44,6 +44,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--reach", type=int, default=6,
+                    help="fixed warp reach (planes) of the graph-replayed mode")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -59,8 +61,15 @@ def main():
     for _ in range(args.warmup):
         model.po_step(fl, ml)
     ms = timed(lambda: model.po_step(fl, ml), args.steps, dev, world)
+    # fixed reach: no host round trip inside the step, replayed as one CUDA graph
+    gmodel = slab_po.SlabModel(params, DIMS, reach=args.reach)
+    for _ in range(args.warmup):
+        gmodel.po_step(fl, ml, graph=True)
+    gms = timed(lambda: gmodel.po_step(fl, ml, graph=True), args.steps, dev, world)
     out = {"metric": "depth-slab PO iteration, small preset, 160x192x224 (config 3)",
-           "ms_per_iter": round(ms, 3), "unit": "ms", "n_gpus": world, "scaling": "strong",
+           "ms_per_iter": round(ms, 3), "graph_ms_per_iter": round(gms, 3),
+           "graph_reach_planes": args.reach,
+           "unit": "ms", "n_gpus": world, "scaling": "strong",
            "steps": args.steps, "slab_depths": [b - a for a, b in slab_po.split_units(DIMS[2],
                                                                                        world)]}
     if world == 1:
