@@ -625,7 +625,8 @@ class SlabModel:
     one CUDA graph per iteration."""
 
     def __init__(self, tensors, dims, lam=1.0, window=9, slope=0.2, heads=(8, 4, 2, 1, 1),
-                 head_dim=6, comm: Comm | None = None, reach=None):
+                 head_dim=6, comm: Comm | None = None, reach=None, diffeomorphic=False,
+                 ss_steps=7):
         self.comm = comm or Comm()
         self.geom = Geom(dims, self.comm, reach)
         self.params = [t.detach().clone().contiguous().requires_grad_(True) for t in tensors]
@@ -635,6 +636,9 @@ class SlabModel:
             self.geom.err = torch.zeros(1, dtype=torch.int32, device=self.params[0].device)
         self.lam, self.window, self.slope = float(lam), int(window), float(slope)
         self.heads, self.hd = tuple(heads), int(head_dim)
+        self.diffeomorphic, self.ss_steps = bool(diffeomorphic), int(ss_steps)
+        if self.diffeomorphic and self.ss_steps < 1:
+            raise ops.InvalidInput("scaling_squaring: steps must be >= 1")
         self.opt = ops.AdamOptimizer([p.data for p in self.params])
         self.grads = [torch.zeros_like(p) for p in self.params]
         self._graph = None
@@ -671,6 +675,12 @@ class SlabModel:
             _, z0, _, _ = geom.level(e)
             SF = _ModeT.apply(Qx, Kx, B, S, self.hd, z0 - 1, geom.defer_checks)[:, 1:-1]
             res = conv3_slab(SF, rw, rb, comm)
+            if self.diffeomorphic:
+                # op_scaling_squaring (reghead.hpp:52-57): v / 2^T, then T
+                # self-compositions phi + warp(phi, phi)
+                res = res * (1.0 / float(1 << self.ss_steps))
+                for _ in range(self.ss_steps):
+                    res = res + warp_slab(res, res, geom, e)
             phi = res if k == 0 else res + warp_slab(phi_up, res, geom, e)
         return phi
 

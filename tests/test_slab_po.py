@@ -433,3 +433,51 @@ def test_slab_po_fixed_reach_and_graph_replay(cuda, ref):
     ops._check(L.mdg_warp_fwd_slab_async(P(win), 2, ops.dims3((h, w, l)), 4, 12, P(fld), P(out),
                                          5, 11, err.data_ptr(), ops._stream()))
     assert int(err.item()) == 0
+
+
+def _diffeo_worker(rank, world, port, dims, case, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    torch.cuda.set_device(0)
+    dist = _init(rank, world, port)
+    try:
+        c = np.load(case)
+        model = slab_po.SlabModel([torch.from_numpy(c[f"p{i}"]).cuda() for i in range(75)], dims,
+                                  diffeomorphic=True, ss_steps=3)
+        fl = model.local(torch.from_numpy(c["fixed"]).cuda())
+        ml = model.local(torch.from_numpy(c["moving"]).cuda())
+        terms, phi = model.loss_step(fl, ml)
+        np.savez(os.path.join(out_dir, f"d{rank}.npz"), terms=terms.cpu().numpy(),
+                 phi=phi.cpu().numpy(), **{f"g{i}": g.cpu().numpy() for i, g in enumerate(model.grads)})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_slab_po_diffeomorphic_matches_native(cuda, ref, tmp_path):
+    """The diffeomorphic variant (scaling and squaring of every residual, each
+    self-composition a slab warp) on 2 slabs against the native model's
+    diffeomorphic loss step (ModelConfig diffeomorphic, ss_steps 3)."""
+    from test_gpu_encoder import perturbed_model, shapes, split
+    from paper_2403_16526_b200 import ops
+
+    dims = (32, 32, 32)
+    fixed, moving, _, _, _ = ref.synth_pair(dims, seed=3)
+    packed, sizes = perturbed_model(ref, 5)
+    params = [np.ascontiguousarray(a.reshape(s)) for a, s in zip(split(packed, sizes),
+                                                                  shapes(sizes))]
+    case = tmp_path / "case.npz"
+    np.savez(case, fixed=fixed, moving=moving, **{f"p{i}": p for i, p in enumerate(params)})
+    mp.start_processes(_diffeo_worker, args=(2, _free_port(), dims, str(case), str(tmp_path)),
+                       nprocs=2, join=True, start_method="spawn")
+    parts = [dict(np.load(tmp_path / f"d{r}.npz")) for r in range(2)]
+    cfg = ops.model_config(diffeomorphic=True, ss_steps=3)
+    nat = ops.NativeModel([torch.from_numpy(p).cuda() for p in params], dims, config=cfg)
+    tn, phn = nat.loss_step(torch.from_numpy(fixed).cuda(), torch.from_numpy(moving).cuda())
+    assert np.allclose(parts[0]["terms"], tn.cpu().numpy(), rtol=1e-4, atol=1e-6)
+    phi = np.concatenate([p["phi"] for p in parts], axis=1)
+    assert _rel(phi, phn.cpu().numpy()) <= 1e-4
+    gn = [g.cpu().numpy() for g in nat.grads]
+    worst = max(_rel(parts[0][f"g{i}"], gn[i]) for i in range(75) if i not in PRE_NORM_BIAS)
+    assert worst <= 1e-3, worst
+
