@@ -56,3 +56,19 @@ print("quad gin ms", round(t(lambda: lq.quad_gin(P(field), P(gout), h, w, l, P(g
 for mb in (2, 3, 4):
     print(f"y-pair minb={mb} ms", round(t(lambda: lib.ypair_gin_b(P(field), P(gout), h, w, l, P(gin), mb,
                                                                 ctypes.c_void_p(st))), 4))
+
+# gfield-only (libmdg) and the y-pair gin (experiment) on two streams at once
+s2 = torch.cuda.Stream()
+gf = torch.zeros_like(field)
+
+
+def both_streams():
+    cur = torch.cuda.current_stream()
+    s2.wait_stream(cur)
+    ops.warp_bwd(vol, field, gout, gfield=gf, want_gin=False)
+    lib.ypair_gin_b(P(field), P(gout), h, w, l, P(gin), 4, ctypes.c_void_p(s2.cuda_stream))
+    cur.wait_stream(s2)
+
+
+print("gfield (stream 1) + y-pair gin (stream 2) ms", round(t(both_streams), 4))
+print("libmdg combined ms", round(t(lambda: ops.warp_bwd(vol, field, gout, gin=g2, gfield=gf)), 4))
