@@ -168,9 +168,13 @@ class _Halo(torch.autograd.Function):
         C, D, W, H = x.shape
         if D < k:
             raise ops.InvalidInput(f"slab PO: {D} planes per rank < halo {k}")
-        out = x.new_zeros(C, D + 2 * k, W, H)
+        out = x.new_empty(C, D + 2 * k, W, H)
         out[:, k:k + D] = x
         r, n = comm.rank, comm.world
+        if r == 0 and not edge:  # global boundary: zero padding
+            out[:, :k].zero_()
+        if r == n - 1 and not edge:
+            out[:, D + k:].zero_()
         sends, recvs = [], []
         if r > 0:
             sends.append((x[:, :k], r - 1))
