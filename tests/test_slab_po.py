@@ -216,10 +216,10 @@ def _rel(a, b):
     return float(np.linalg.norm(a - b) / nb) if nb > 0 else float(np.linalg.norm(a))
 
 
-def _run_slab(params, fixed, moving, dims, lr=1e-4):
+def _run_slab(params, fixed, moving, dims, lr=1e-4, reach=None):
     from paper_2403_16526_b200 import ops
 
-    model = slab_po.SlabModel([torch.from_numpy(p).cuda() for p in params], dims)
+    model = slab_po.SlabModel([torch.from_numpy(p).cuda() for p in params], dims, reach=reach)
     fl = model.local(torch.from_numpy(fixed).cuda())
     ml = model.local(torch.from_numpy(moving).cuda())
     terms, phi = model.loss_step(fl, ml)
@@ -234,7 +234,7 @@ def _run_slab(params, fixed, moving, dims, lr=1e-4):
     return out
 
 
-def _model_worker(rank, world, port, dims, case, out_dir):
+def _model_worker(rank, world, port, dims, case, out_dir, reach=None):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     torch.cuda.set_device(0)
@@ -242,15 +242,16 @@ def _model_worker(rank, world, port, dims, case, out_dir):
     try:
         c = np.load(case)
         params = [c[f"p{i}"] for i in range(75)]
-        out = _run_slab(params, c["fixed"], c["moving"], dims)
+        out = _run_slab(params, c["fixed"], c["moving"], dims, reach=reach)
         np.savez(os.path.join(out_dir, f"m{rank}.npz"), **out)
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,dims", [(2, (32, 32, 32)), (3, (32, 24, 48))])
-def test_slab_po_matches_single_volume(cuda, ref, tmp_path, world, dims):
+@pytest.mark.parametrize("world,dims,reach", [(2, (32, 32, 32), None), (3, (32, 24, 48), None),
+                                              (2, (32, 32, 32), 6)])
+def test_slab_po_matches_single_volume(cuda, ref, tmp_path, world, dims, reach):
     """The loss step on `world` slabs against (1) the same step on one slab —
     the decomposition: halos, all-reduced statistics and partial sums,
     gathered warp planes, returned scatters: all 75 gradients <= 1e-4;
@@ -267,7 +268,8 @@ def test_slab_po_matches_single_volume(cuda, ref, tmp_path, world, dims):
                                                                   shapes(sizes))]
     case = tmp_path / "case.npz"
     np.savez(case, fixed=fixed, moving=moving, **{f"p{i}": p for i, p in enumerate(params)})
-    mp.start_processes(_model_worker, args=(world, _free_port(), dims, str(case), str(tmp_path)),
+    mp.start_processes(_model_worker,
+                       args=(world, _free_port(), dims, str(case), str(tmp_path), reach),
                        nprocs=world, join=True, start_method="spawn")
     parts = [dict(np.load(tmp_path / f"m{r}.npz")) for r in range(world)]
     one = _run_slab(params, fixed, moving, dims)  # this process alone: one slab
