@@ -81,3 +81,34 @@ def test_host_alloc_roundtrip_api_present():
     L = _capi.lib()
     assert isinstance(L.mdg_build_info().decode(), str)
     assert L.mdg_launch_count() >= 0
+
+
+def test_slab_entry_points_validate_before_touching_the_device():
+    """The depth-slab entry points (slab warps, slab NCC, slab instance norm)
+    refuse inconsistent geometry with MDG_EINVAL and a message, no GPU."""
+    L = _capi.lib()
+    d = _capi.Dims3(8, 8, 32)
+    # the input window must cover the slab's planes
+    assert L.mdg_warp_fwd_slab(None, 2, d, 6, 20, None, None, 4, 12, None) == 1
+    assert "cover" in L.mdg_last_error().decode()
+    assert L.mdg_warp_bwd_slab(None, 2, d, 0, 40, None, None, None, None, 4, 12, None) == 1
+    assert L.mdg_warp_fwd_slab(None, 2, d, 0, 32, None, None, 12, 4, None) == 1
+    assert "plane range" in L.mdg_last_error().decode()
+    assert L.mdg_warp_fwd_slab_async(None, 2, d, 0, 32, None, None, 0, 32, None, None) == 1
+    assert "error word" in L.mdg_last_error().decode()
+    # an empty slab is a no-op
+    assert L.mdg_warp_fwd_slab(None, 2, d, 0, 32, None, None, 5, 5, None) == 0
+    # slab NCC: odd window, own planes inside the halos, in-volume range
+    e = _capi.Dims3(8, 8, 24)
+    assert L.mdg_ncc_slab_fwd(None, None, e, 8, 4, 20, None, None) == 1
+    assert "odd" in L.mdg_last_error().decode()
+    assert L.mdg_ncc_slab_fwd(None, None, _capi.Dims3(8, 8, 8), 9, 0, 8, None, None) == 1
+    assert "own planes" in L.mdg_last_error().decode()
+    assert L.mdg_ncc_slab_fwd(None, None, e, 9, 6, 24, None, None) == 1
+    assert "in-volume" in L.mdg_last_error().decode()
+    assert L.mdg_ncc_slab_bwd_dev(None, None, e, 9, 4, 20, 1.0, None, None, None) == 1
+    # slab instance norm
+    assert L.mdg_in_slab_sums(None, 0, 16, None, None, None) == 1
+    assert "invalid sizes" in L.mdg_last_error().decode()
+    assert L.mdg_in_lrelu_bwd_apply(None, None, 2, 16, None, None, None, None, 0.2, None, 8,
+                                    None, None) == 1
