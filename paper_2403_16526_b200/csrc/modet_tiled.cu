@@ -48,6 +48,10 @@
 
 #include "mdg_common.cuh"
 
+#ifndef MDG_BWD_MINB
+#define MDG_BWD_MINB 2  // resident CTAs of the row / column kernels (d <= 6)
+#endif
+
 namespace mdg {
 namespace tiled {
 
@@ -585,7 +589,7 @@ __device__ __forceinline__ void row_stage(float *buf, const Maps &m, uint64_t *b
 }
 
 template <int D, bool TMA, bool ACC>
-__global__ void __launch_bounds__(256, (D <= 6 ? 2 : 1))
+__global__ void __launch_bounds__(256, (D <= 6 ? MDG_BWD_MINB : 1))
 modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                 const float *__restrict__ K, const float *__restrict__ B,
                 const float *__restrict__ SF, const float *__restrict__ LSE,
@@ -817,7 +821,7 @@ __device__ __forceinline__ void col_stage(float *buf, const Maps &m, uint64_t *b
 }
 
 template <int D, bool TMA, bool ACC>
-__global__ void __launch_bounds__(256, (D <= 6 ? 2 : 1))
+__global__ void __launch_bounds__(256, (D <= 6 ? MDG_BWD_MINB : 1))
 modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                 const float *__restrict__ K, const float *__restrict__ B,
                 const float *__restrict__ SF, const float *__restrict__ LSE,
