@@ -268,6 +268,7 @@ def run_ours(args):
 
     peak, peak_kind = load_peak()
     stress = None if args.no_stress else run_modet_stress(L, rank, dev, st, peak)
+    slab_po_res = None if args.no_slab_po else run_slab_po(dev, world)
     dom = max(per_op, key=lambda k: per_op[k])
     achieved = BYTES[dom] * n / (per_op[dom] * 1e-3) / 1e9
     traffic = op_traffic(dom)
@@ -298,6 +299,7 @@ def run_ours(args):
         "e2e": e2e,
         "warp_random_field": warp_rf,
         "modet_stress": stress,
+        "slab_po": slab_po_res,
         "cfg2": cfg2,
         "pyramid": pyramid,
         "po": po,
@@ -510,6 +512,52 @@ def run_pyramid(dev, reps=5):
                                  "Adam with the encoder features held fixed (the full "
                                  "iteration is under 'po')",
             "arena_mib": round(pyr.device_bytes / 2 ** 20, 1)}
+
+
+def run_slab_po(dev, world, reps=3, reach=6):
+    """BASELINE config 3: the PO iteration of one 160x192x224 pair split along z
+    over the ranks (paper_2403_16526_b200/slab_po.py: halo exchange and
+    all-reduces over the job's process group, NCCL).  Device time of `reps`
+    iterations between barriers, max over ranks; at N = 1 also the fixed-reach
+    step replayed as one CUDA graph.  Strong scaling: the pair is fixed."""
+    import torch
+
+    from paper_2403_16526_b200 import ops, slab_po
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / reps], device=dev)
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return round(float(t.item()), 3)
+
+    try:
+        params = [t.to(dev) for t in ops.init_model(42)]
+        f, m, _, _, _ = ops.synth_pair(DIMS, seed=1, max_disp=2.0)
+        model = slab_po.SlabModel(params, DIMS)
+        fl, ml = model.local(f.to(dev)), model.local(m.to(dev))
+        out = {"workload": "PO iteration of one 160x192x224 pair over z-slabs (config 3)",
+               "slab_depths": [b - a for a, b in slab_po.split_units(DIMS[2], world)],
+               "scaling": "strong", "eager_ms_per_iter": timed(lambda: model.po_step(fl, ml))}
+        if world == 1:
+            g = slab_po.SlabModel(params, DIMS, reach=reach)
+            out["graph_ms_per_iter"] = timed(lambda: g.po_step(fl, ml, graph=True))
+            out["graph_reach_planes"] = reach
+        return out
+    except Exception as e:  # reported, never fatal for the headline line
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
 
 
 def run_po(dev, world, pairs=0, reps=5):
@@ -782,6 +830,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling)")
     ap.add_argument("--no-pyramid", action="store_true", help="skip the pyramid timing")
     ap.add_argument("--no-po", action="store_true", help="skip the PO-iteration timing")
+    ap.add_argument("--no-slab-po", action="store_true",
+                    help="skip the depth-slab PO (config 3) timing")
     ap.add_argument("--no-stress", action="store_true",
                     help="skip the S=8, d=8 ModeT stress timing")
     ap.add_argument("--no-random-field", action="store_true",

@@ -12,7 +12,7 @@ TAG=${1:-r02}
 O=gpurun_out/ncu_$TAG
 mkdir -p $O
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
-CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-pyramid --no-po --no-cfg2 --no-random-field --no-stress"
+CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-pyramid --no-po --no-cfg2 --no-random-field --no-stress --no-slab-po"
 $CMD > $O/plain.log 2>&1 || { echo "plain bench failed"; exit 1; }
 ncu --metrics $M --clock-control none --csv --log-file $O/step_launches.csv $CMD > $O/step.log 2>&1
 # full captures are large: keep the raw-metric CSV of each (what the summary
