@@ -546,15 +546,17 @@ def run_slab_po(dev, world, reps=3, reach=6):
     try:
         params = [t.to(dev) for t in ops.init_model(42)]
         f, m, _, _, _ = ops.synth_pair(DIMS, seed=1, max_disp=2.0)
-        model = slab_po.SlabModel(params, DIMS)
+        model = slab_po.SlabModel(params, DIMS, reach=reach)
         fl, ml = model.local(f.to(dev)), model.local(m.to(dev))
+        # eager with a fixed reach (no host round trip inside the step; the
+        # host-side floor of an eager step is ~15.6 ms, tools/exp/slab_cpu_floor.py)
         out = {"workload": "PO iteration of one 160x192x224 pair over z-slabs (config 3)",
                "slab_depths": [b - a for a, b in slab_po.split_units(DIMS[2], world)],
-               "scaling": "strong", "eager_ms_per_iter": timed(lambda: model.po_step(fl, ml))}
-        if world == 1:
+               "scaling": "strong", "reach_planes": reach,
+               "eager_ms_per_iter": timed(lambda: model.po_step(fl, ml))}
+        if world == 1:  # (multi-rank capture of the NCCL exchange is not exercised here)
             g = slab_po.SlabModel(params, DIMS, reach=reach)
             out["graph_ms_per_iter"] = timed(lambda: g.po_step(fl, ml, graph=True))
-            out["graph_reach_planes"] = reach
         return out
     except Exception as e:  # reported, never fatal for the headline line
         return {"error": f"{type(e).__name__}: {e}"[:300]}

@@ -61,13 +61,19 @@ def main():
     for _ in range(args.warmup):
         model.po_step(fl, ml)
     ms = timed(lambda: model.po_step(fl, ml), args.steps, dev, world)
+    # fixed reach, eager: no host round trip inside the step (the host runs ahead)
+    fmodel = slab_po.SlabModel(params, DIMS, reach=args.reach)
+    for _ in range(args.warmup):
+        fmodel.po_step(fl, ml)
+    fms = timed(lambda: fmodel.po_step(fl, ml), args.steps, dev, world)
     # fixed reach: no host round trip inside the step, replayed as one CUDA graph
     gmodel = slab_po.SlabModel(params, DIMS, reach=args.reach)
     for _ in range(args.warmup):
         gmodel.po_step(fl, ml, graph=True)
     gms = timed(lambda: gmodel.po_step(fl, ml, graph=True), args.steps, dev, world)
     out = {"metric": "depth-slab PO iteration, small preset, 160x192x224 (config 3)",
-           "ms_per_iter": round(ms, 3), "graph_ms_per_iter": round(gms, 3),
+           "ms_per_iter": round(ms, 3), "fixed_reach_eager_ms_per_iter": round(fms, 3),
+           "graph_ms_per_iter": round(gms, 3),
            "graph_reach_planes": args.reach,
            "unit": "ms", "n_gpus": world, "scaling": "strong",
            "steps": args.steps, "slab_depths": [b - a for a, b in slab_po.split_units(DIMS[2],
