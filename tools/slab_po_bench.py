@@ -8,7 +8,9 @@ scaling: the pair is fixed, each rank owns a slab.
 
 Prints one JSON line from rank 0: ms per PO iteration (device time of K
 iterations between barriers, max over ranks) and the single-volume native
-driver's time for comparison at N = 1."""
+driver's time for comparison at N = 1.  Modes: eager (data-dependent reach),
+eager with a fixed reach, graph-replayed.  The graph mode at N > 1 captures
+the NCCL exchange; it has only been run at N = 1 here (one GPU per call)."""
 import argparse
 import json
 import os
