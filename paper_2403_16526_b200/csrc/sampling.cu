@@ -549,28 +549,32 @@ upsample2_fwd_k(const float *__restrict__ in, int C, int h, int w, int l, int th
     int x, y, z;
     xyz_of(p, th, tw, x, y, z);
     const Corners c = corners_at((float)x / 2.0f, (float)y / 2.0f, (float)z / 2.0f, h, w, l);
+    if (C == 3) {  // the displacement field: the three channels' loads in flight together
+        const Oct o0 = load_oct(in, c), o1 = load_oct(in + ni, c), o2 = load_oct(in + 2 * ni, c);
+        out[p] = mul_(scale, lerp_oct(o0, c));
+        out[no + p] = mul_(scale, lerp_oct(o1, c));
+        out[2 * no + p] = mul_(scale, lerp_oct(o2, c));
+        return;
+    }
     for (int ch = 0; ch < C; ++ch) out[ch * no + p] = mul_(scale, sample(in + ch * ni, c));
 }
 
-// fine positions t on one axis whose resolved corners include coarse index i,
-// with the corner weight the reference scatter uses (1-f for i0, f for i1)
-__device__ __forceinline__ int axis_sources(int i, int dim, int tdim, int *ts, float *ws) {
-    int m = 0;
-    const int t0 = max(0, 2 * i - 2), t1 = min(tdim - 1, 2 * i + 2);
-    for (int t = t0; t <= t1; ++t) {
+// The fine positions t = 2i-2 .. 2i+2 on one axis and the corner weight of
+// coarse index i in each (the reference scatter's 1-f for i0, f for i1; 0
+// when t does not reach i or lies outside the grid).  Fixed-size, fully
+// unrolled: no local-memory arrays.
+constexpr int kUpTaps = 5;
+__device__ __forceinline__ float axis_tap(int i, int k, int dim, int tdim, int &t) {
+    t = 2 * i - 2 + k;
+    float wgt = 0.0f;
+    if (t >= 0 && t < tdim) {
         const Ax a = resolve_axis((float)t / 2.0f, dim);
-        if (a.i0 == i) {
-            ts[m] = t;
-            ws[m] = sub_(1.0f, a.f);
-            ++m;
-        }
-        if (a.i1 == i) {
-            ts[m] = t;
-            ws[m] = a.f;
-            ++m;
-        }
+        // (a collapsed axis has i0 == i1 with f = 0: the reference adds the
+        // i1 term g*0 after the i0 term, which changes nothing)
+        if (a.i0 == i) wgt = sub_(1.0f, a.f);
+        else if (a.i1 == i) wgt = a.f;
     }
-    return m;
+    return wgt;
 }
 
 // sampling.hpp:245-262 as a gather onto each coarse voxel
@@ -582,23 +586,44 @@ upsample2_bwd_k(int C, int h, int w, int l, int th, int tw, int tl, float scale,
     if (p >= ni) return;
     int x, y, z;
     xyz_of(p, h, w, x, y, z);
-    int tx[10], ty[10], tz[10];
-    float wx[10], wy[10], wz[10];
-    const int mx = axis_sources(x, h, th, tx, wx);
-    const int my = axis_sources(y, w, tw, ty, wy);
-    const int mz = axis_sources(z, l, tl, tz, wz);
-    for (int ch = 0; ch < C; ++ch) {
-        const float *go = gout + ch * no;
-        float acc = gin[ch * ni + p];
-        for (int a = 0; a < mz; ++a)
-            for (int b = 0; b < my; ++b) {
-                const int64_t row = ((int64_t)tz[a] * tw + ty[b]) * th;
-                for (int e = 0; e < mx; ++e) {
-                    const float g = mul_(scale, __ldg(go + row + tx[e]));
-                    acc = add_(acc, mul_(mul_(mul_(g, wx[e]), wy[b]), wz[a]));
+    int tx[kUpTaps];
+    float wx[kUpTaps];
+#pragma unroll
+    for (int e = 0; e < kUpTaps; ++e) wx[e] = axis_tap(x, e, h, th, tx[e]);
+    // the reference's terms ((scale*g*wx)*wy)*wz in fine-voxel order (z, y,
+    // x ascending); zero-weight taps are skipped, as a gather adds nothing.
+    // Channels inside, so each fine row's taps are computed once.
+    float acc[4];
+    for (int c0 = 0; c0 < C; c0 += 4) {
+        const int cn = min(4, C - c0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = k < cn ? gin[(c0 + k) * ni + p] : 0.0f;
+#pragma unroll 1
+        for (int a = 0; a < kUpTaps; ++a) {
+            int tz;
+            const float wz = axis_tap(z, a, l, tl, tz);
+            if (wz == 0.0f) continue;
+#pragma unroll 1
+            for (int b = 0; b < kUpTaps; ++b) {
+                int ty;
+                const float wy = axis_tap(y, b, w, tw, ty);
+                if (wy == 0.0f) continue;
+                const int64_t row = ((int64_t)tz * tw + ty) * th;
+#pragma unroll
+                for (int e = 0; e < kUpTaps; ++e) {
+                    if (wx[e] == 0.0f) continue;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (k >= cn) break;
+                        const float g = mul_(scale, __ldg(gout + (c0 + k) * no + row + tx[e]));
+                        acc[k] = add_(acc[k], mul_(mul_(mul_(g, wx[e]), wy), wz));
+                    }
                 }
             }
-        gin[ch * ni + p] = acc;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < cn) gin[(c0 + k) * ni + p] = acc[k];
     }
 }
 
