@@ -199,8 +199,11 @@ struct BwdShape {
     static constexpr int NSLOT = KMAX * CT + NE;
 };
 
+#ifndef MDG_PROJ_BWD_MINB
+#define MDG_PROJ_BWD_MINB 4  // measured: 697 vs 750 (2) vs 786 us (3) at L1 (tools/exp/proj_minb.sh)
+#endif
 template <int KMAX, int CT, bool EXACT>
-__global__ void __launch_bounds__(kPB, KMAX <= 6 ? 2 : 1)
+__global__ void __launch_bounds__(kPB, KMAX <= 6 ? MDG_PROJ_BWD_MINB : 1)
 project_bwd_k(ProjArgs a, const float *__restrict__ W, const float *__restrict__ b,
               const float *__restrict__ g, int ntiles, float *__restrict__ part) {
     extern __shared__ __align__(16) float sm[];
@@ -539,7 +542,7 @@ mdg_status project_bwd_launch(const ProjArgs &a0, const float *W, const float *b
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t blocks_needed = (a.n + kPB - 1) / kPB;
-    const int per_sm = KMAX <= 6 ? 2 : 1;
+    const int per_sm = KMAX <= 6 ? MDG_PROJ_BWD_MINB : 1;
     // one channel tile: gW accumulates in registers next to everything else;
     // several: two-phase (graw to scratch, then the chunked reduction)
     const bool two_phase = gW && a.C > CT;
