@@ -33,8 +33,19 @@ class SimExchange:
         return P()
 
 
+def _random_modet_cases(seed, count):
+    r = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        world = int(r.integers(2, 5))
+        out.append((world, (int(r.integers(2, 40)), int(r.integers(1, 20)),
+                            int(r.integers(world, 4 * world + 4))),
+                    int(r.choice([1, 2, 3])), int(r.choice([1, 2, 3, 4, 5, 6, 8]))))
+    return out
+
+
 @pytest.mark.parametrize("world,dims,S,hd", [(2, (20, 12, 16), 1, 6), (3, (33, 9, 10), 2, 4),
-                                              (4, (16, 16, 8), 1, 6)])
+                                              (4, (16, 16, 8), 1, 6)] + _random_modet_cases(43, 8))
 def test_slab_modet_cuda_matches_full_volume(cuda, world, dims, S, hd):
     h, w, l = dims
     r = np.random.default_rng(5)
@@ -62,7 +73,19 @@ def test_slab_modet_cuda_matches_full_volume(cuda, world, dims, S, hd):
     assert np.allclose(gB_sum.cpu().numpy(), gB.cpu().numpy(), rtol=1e-5, atol=1e-5)
 
 
-@pytest.mark.parametrize("world,dims,C,zreach", [(2, (20, 12, 16), 8, 2.5), (4, (16, 9, 12), 3, 4.2)])
+def _random_slab_cases(seed, count):
+    r = np.random.default_rng(seed)
+    cases = []
+    for _ in range(count):
+        world = int(r.integers(2, 5))
+        l = int(r.integers(world, 3 * world + 6))
+        cases.append((world, (int(r.integers(2, 23)), int(r.integers(1, 13)), l),
+                      int(r.choice([1, 2, 3, 4, 5, 8, 16])), float(r.uniform(0.2, 5.0))))
+    return cases
+
+
+@pytest.mark.parametrize("world,dims,C,zreach", [(2, (20, 12, 16), 8, 2.5), (4, (16, 9, 12), 3, 4.2)]
+                         + _random_slab_cases(41, 10))
 def test_slab_warp_cuda_matches_full_volume(cuda, world, dims, C, zreach):
     """SlabWarp with the libmdg range kernels, ranks run in turn with a
     simulated plane exchange / reduction: out and gfield equal the
