@@ -148,9 +148,19 @@ def test_slab_loss_decomposition_matches_reference(oracle, ref, tmp_path, world,
     _check_loss_case(oracle, ref, tmp_path, world, dims, "cpu")
 
 
+def _random_loss_cases(seed, count):
+    r = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        world = int(r.integers(1, 4))
+        units = int(r.integers(world, world + 3))
+        out.append((world, (int(r.integers(2, 15)), int(r.integers(2, 15)), 16 * units)))
+    return out
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,dims", [(1, (12, 10, 32)), (2, (12, 10, 32)),
-                                        (3, (9, 11, 48))])
+                                        (3, (9, 11, 48))] + _random_loss_cases(47, 4))
 def test_slab_loss_kernels_match_reference(cuda, oracle, ref, tmp_path, world, dims):
     """slab_po.slab_loss (mdg_ncc_slab_fwd / _bwd on the extended grid) on
     1-3 ranks sharing the GPU: the same criteria as the CPU scheme."""
