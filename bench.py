@@ -20,7 +20,6 @@ Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every key.
 from __future__ import annotations
 
 import argparse
-import ctypes as C
 import json
 import os
 import statistics
