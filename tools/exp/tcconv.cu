@@ -1,0 +1,209 @@
+// Experiment: the encoder's 3x3x3 convolution (zero padded, ops.hpp:58-74) as
+// an implicit GEMM on the 5th-generation tensor cores: D[voxel][oc] =
+// sum_k A[voxel][k] B[oc][k], k = tap * ic + c, with fp32 accuracy from
+// 3xTF32 (hi*hi + hi*lo + lo*hi).  One CTA = 128 consecutive output voxels
+// (M = 128); per K chunk of 32 the 128 threads gather their voxel's 32
+// values (im2col on the fly), split them into tf32 hi / lo and store them
+// 128-byte swizzled K-major in shared memory; one thread issues the 12
+// tcgen05.mma (4 K-steps x 3 products) into a TMEM accumulator of N = oc
+// columns; the epilogue reads TMEM back (tcgen05.ld), adds the bias and
+// writes the planar output.  dev experiment: compared with
+// mdg_encoder_conv3_fwd in tcconv_bench.py.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace {
+
+__device__ __forceinline__ uint32_t su32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+// element (r, k) of an R x 32 fp32 tile, 128B swizzle (8-row atoms of 1 KB)
+__device__ __forceinline__ int swz(int r, int k) {
+    return ((r >> 3) * 1024 + (r & 7) * 128 + (((k >> 2) ^ (r & 7)) << 4)) / 4 + (k & 3);
+}
+__device__ __forceinline__ uint64_t desc_swz(uint32_t addr) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) |
+           ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ uint32_t idesc_tf32(int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ float tf32r(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned phase) {
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done) : "r"(su32(b)), "r"(phase) : "memory");
+    } while (!done);
+}
+
+// weights w {oc, ic, 3, 3, 3} -> B hi / lo {oc, Kp} (k = tap * ic + c, zero padded)
+__global__ void prep_b(const float *w, int oc, int ic, int Kp, float *bhi, float *blo) {
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= oc * Kp) return;
+    const int o = i / Kp, k = i % Kp;
+    float v = 0.0f;
+    if (k < 27 * ic) {
+        const int tap = k / ic, c = k % ic;
+        v = w[((int64_t)o * ic + c) * 27 + tap];
+    }
+    const float h = tf32r(v);
+    bhi[i] = h;
+    blo[i] = tf32r(v - h);
+}
+
+template <int N>
+__global__ void __launch_bounds__(128)
+tcconv_k(const float *__restrict__ in, int ic, int h, int w, int l, const float *__restrict__ bhi,
+         const float *__restrict__ blo, int Kp, const float *__restrict__ bias,
+         float *__restrict__ out) {
+    extern __shared__ __align__(1024) float sm_raw[];
+    // the swizzle atoms must start on 1 KB boundaries of the shared window
+    float *sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u) / 4;
+    constexpr int STAGE = 2 * 128 * 32 + 2 * N * 32;  // floats per pipeline stage
+    __shared__ uint64_t bar[2];
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int64_t n = (int64_t)h * w * l;
+    const int64_t p = (int64_t)blockIdx.x * 128 + tid;
+    const bool live = p < n;
+    int x = 0, y = 0, z = 0;
+    if (live) {
+        const int t = (int)(p / h);
+        x = (int)(p - (int64_t)t * h);
+        z = t / w;
+        y = t - z * w;
+    }
+    constexpr int NCOL = N < 32 ? 32 : N;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         su32(&tmem_base)), "r"(NCOL));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[1])));
+    }
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base, id = idesc_tf32(N);
+    const int nchunk = Kp / 32, K27 = 27 * ic;
+    for (int j = 0; j < nchunk; ++j) {
+        const int sidx = j & 1;
+        float *aH = sm + sidx * STAGE, *aL = aH + 128 * 32, *bH = aL + 128 * 32, *bL = bH + N * 32;
+        // the MMAs of chunk j-2 read this stage: wait for them
+        if (j >= 2) mbar_wait(&bar[sidx], ((j - 2) >> 1) & 1);
+        // A: this thread's voxel, K = 32j .. 32j+31: runs of one tap
+        int k = 32 * j;
+        const int kend = k + 32;
+        int i = 0;
+        while (k < kend) {
+            const int tap = k < K27 ? k / ic : 27;
+            const int c0 = k - tap * ic;
+            const int run = tap < 27 ? min(ic - c0, kend - k) : kend - k;
+            bool ok = false;
+            int64_t off = 0;
+            if (tap < 27 && live) {
+                const int xx = x + tap % 3 - 1, yy = y + (tap / 3) % 3 - 1, zz = z + tap / 9 - 1;
+                ok = xx >= 0 && xx < h && yy >= 0 && yy < w && zz >= 0 && zz < l;
+                off = (int64_t)c0 * n + ((int64_t)zz * w + yy) * h + xx;
+            }
+            // runs are multiples of 4 (ic % 4 == 0): one 16-byte swizzle chunk
+            // per 4 values, stored as float4
+            for (int q = 0; q < run; q += 4, i += 4) {
+                float4 v4;
+                v4.x = ok ? __ldg(in + off + (int64_t)(q + 0) * n) : 0.0f;
+                v4.y = ok ? __ldg(in + off + (int64_t)(q + 1) * n) : 0.0f;
+                v4.z = ok ? __ldg(in + off + (int64_t)(q + 2) * n) : 0.0f;
+                v4.w = ok ? __ldg(in + off + (int64_t)(q + 3) * n) : 0.0f;
+                const float4 h4 = make_float4(tf32r(v4.x), tf32r(v4.y), tf32r(v4.z), tf32r(v4.w));
+                const float4 l4 = make_float4(tf32r(v4.x - h4.x), tf32r(v4.y - h4.y),
+                                              tf32r(v4.z - h4.z), tf32r(v4.w - h4.w));
+                *reinterpret_cast<float4 *>(aH + swz(tid, i)) = h4;
+                *reinterpret_cast<float4 *>(aL + swz(tid, i)) = l4;
+            }
+            k += run;
+        }
+        // B: N rows x 32
+        for (int e = tid; e < N * 32; e += 128) {
+            const int r = e >> 5, kk = e & 31;
+            bH[swz(r, kk)] = __ldg(bhi + (int64_t)r * Kp + 32 * j + kk);
+            bL[swz(r, kk)] = __ldg(blo + (int64_t)r * Kp + 32 * j + kk);
+        }
+        asm volatile("fence.proxy.async.shared::cta;");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const uint64_t ah = desc_swz(su32(aH) + 32 * s), al = desc_swz(su32(aL) + 32 * s);
+                const uint64_t bh = desc_swz(su32(bH) + 32 * s), bl = desc_swz(su32(bL) + 32 * s);
+                mma(tmem, ah, bh, id, (j | s) ? 1u : 0u);
+                mma(tmem, ah, bl, id, 1u);
+                mma(tmem, al, bh, id, 1u);
+            }
+            asm volatile(
+                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    su32(&bar[sidx])));
+        }
+    }
+    // the last chunk's commit covers every MMA before it
+    mbar_wait(&bar[(nchunk - 1) & 1], ((nchunk - 1) >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // epilogue: lane = voxel, columns = output channels
+#pragma unroll
+    for (int c = 0; c < N; c += 8) {
+        uint32_t v[8];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                       "=r"(v[6]), "=r"(v[7]) : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (live)
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                out[(int64_t)(c + q) * n + p] = __uint_as_float(v[q]) + (bias ? bias[c + q] : 0.0f);
+    }
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(NCOL));
+}
+
+}  // namespace
+
+extern "C" int tcconv_fwd(const float *in, int ic, int h, int w, int l, const float *wt,
+                          const float *bias, int oc, float *out, float *scratch, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int Kp = (27 * ic + 31) / 32 * 32;
+    float *bhi = scratch, *blo = scratch + (size_t)oc * Kp;
+    prep_b<<<(oc * Kp + 255) / 256, 256, 0, st>>>(wt, oc, ic, Kp, bhi, blo);
+    const int64_t n = (int64_t)h * w * l;
+    const unsigned g = (unsigned)((n + 127) / 128);
+    const size_t smem = (size_t)2 * (2 * 128 * 32 + 2 * oc * 32) * 4 + 1024;
+#define TC(NV)                                                                                  \
+    case NV:                                                                                    \
+        cudaFuncSetAttribute(tcconv_k<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                             (int)smem);                                                        \
+        tcconv_k<NV><<<g, 128, smem, st>>>(in, ic, h, w, l, bhi, blo, Kp, bias, out);           \
+        break;
+    switch (oc) {
+        TC(8) TC(16) TC(32) TC(64) TC(128)
+        default: return -1;
+    }
+#undef TC
+    return (int)cudaPeekAtLastError();
+}
