@@ -65,8 +65,44 @@ __global__ void prep_b(const float *w, int oc, int ic, int Kp, float *bhi, float
     blo[i] = tf32r(v - h);
 }
 
+// A and B values of one K chunk for this thread, in registers (ic % 16 == 0)
 template <int N>
-__global__ void __launch_bounds__(128)
+struct ChunkRegs {
+    static constexpr int BPT = (N * 32 + 255) / 256;
+    float a[16], bh[BPT], bl[BPT];
+};
+
+template <int N>
+__device__ __forceinline__ void load_chunk(ChunkRegs<N> &R, int j, int half, int tid, bool live,
+                                           int x, int y, int z, int h, int w, int l, int64_t n,
+                                           int ic, int K27, int Kp, const float *__restrict__ in,
+                                           const float *__restrict__ bhi,
+                                           const float *__restrict__ blo) {
+#pragma unroll
+    for (int u = 0; u < ChunkRegs<N>::BPT; ++u) {
+        const int e = tid + 256 * u;
+        if (e < N * 32) {
+            const int r = e >> 5, kk = e & 31;
+            R.bh[u] = __ldg(bhi + (int64_t)r * Kp + 32 * j + kk);
+            R.bl[u] = __ldg(blo + (int64_t)r * Kp + 32 * j + kk);
+        }
+    }
+    const int k = 32 * j + 16 * half;
+    const int tap = k < K27 ? k / ic : 27;
+    const int c0 = k - tap * ic;
+    bool ok = false;
+    int64_t off = 0;
+    if (tap < 27 && live) {
+        const int xx = x + tap % 3 - 1, yy = y + (tap / 3) % 3 - 1, zz = z + tap / 9 - 1;
+        ok = xx >= 0 && xx < h && yy >= 0 && yy < w && zz >= 0 && zz < l;
+        off = (int64_t)c0 * n + ((int64_t)zz * w + yy) * h + xx;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) R.a[q] = ok ? __ldg(in + off + (int64_t)q * n) : 0.0f;
+}
+
+template <int N>
+__global__ void __launch_bounds__(256)
 tcconv_k(const float *__restrict__ in, int ic, int h, int w, int l, const float *__restrict__ bhi,
          const float *__restrict__ blo, int Kp, const float *__restrict__ bias,
          float *__restrict__ out) {
@@ -77,8 +113,9 @@ tcconv_k(const float *__restrict__ in, int ic, int h, int w, int l, const float 
     __shared__ uint64_t bar[2];
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5;
+    const int row = tid & 127, half = tid >> 7;  // voxel row, K half of each chunk
     const int64_t n = (int64_t)h * w * l;
-    const int64_t p = (int64_t)blockIdx.x * 128 + tid;
+    const int64_t p = (int64_t)blockIdx.x * 128 + row;
     const bool live = p < n;
     int x = 0, y = 0, z = 0;
     if (live) {
@@ -101,48 +138,37 @@ tcconv_k(const float *__restrict__ in, int ic, int h, int w, int l, const float 
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base, id = idesc_tf32(N);
     const int nchunk = Kp / 32, K27 = 27 * ic;
+    // software pipeline: chunk j+1's global loads are in flight while chunk
+    // j is split, stored and handed to the tensor core
+    ChunkRegs<N> R;
+    load_chunk<N>(R, 0, half, tid, live, x, y, z, h, w, l, n, ic, K27, Kp, in, bhi, blo);
     for (int j = 0; j < nchunk; ++j) {
         const int sidx = j & 1;
         float *aH = sm + sidx * STAGE, *aL = aH + 128 * 32, *bH = aL + 128 * 32, *bL = bH + N * 32;
         // the MMAs of chunk j-2 read this stage: wait for them
         if (j >= 2) mbar_wait(&bar[sidx], ((j - 2) >> 1) & 1);
-        // A: this thread's voxel, K = 32j .. 32j+31: runs of one tap
-        int k = 32 * j;
-        const int kend = k + 32;
-        int i = 0;
-        while (k < kend) {
-            const int tap = k < K27 ? k / ic : 27;
-            const int c0 = k - tap * ic;
-            const int run = tap < 27 ? min(ic - c0, kend - k) : kend - k;
-            bool ok = false;
-            int64_t off = 0;
-            if (tap < 27 && live) {
-                const int xx = x + tap % 3 - 1, yy = y + (tap / 3) % 3 - 1, zz = z + tap / 9 - 1;
-                ok = xx >= 0 && xx < h && yy >= 0 && yy < w && zz >= 0 && zz < l;
-                off = (int64_t)c0 * n + ((int64_t)zz * w + yy) * h + xx;
-            }
-            // runs are multiples of 4 (ic % 4 == 0): one 16-byte swizzle chunk
-            // per 4 values, stored as float4
-            for (int q = 0; q < run; q += 4, i += 4) {
-                float4 v4;
-                v4.x = ok ? __ldg(in + off + (int64_t)(q + 0) * n) : 0.0f;
-                v4.y = ok ? __ldg(in + off + (int64_t)(q + 1) * n) : 0.0f;
-                v4.z = ok ? __ldg(in + off + (int64_t)(q + 2) * n) : 0.0f;
-                v4.w = ok ? __ldg(in + off + (int64_t)(q + 3) * n) : 0.0f;
-                const float4 h4 = make_float4(tf32r(v4.x), tf32r(v4.y), tf32r(v4.z), tf32r(v4.w));
-                const float4 l4 = make_float4(tf32r(v4.x - h4.x), tf32r(v4.y - h4.y),
-                                              tf32r(v4.z - h4.z), tf32r(v4.w - h4.w));
-                *reinterpret_cast<float4 *>(aH + swz(tid, i)) = h4;
-                *reinterpret_cast<float4 *>(aL + swz(tid, i)) = l4;
-            }
-            k += run;
+        const int i = 16 * half;
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) {
+            const float4 h4 = make_float4(tf32r(R.a[q]), tf32r(R.a[q + 1]), tf32r(R.a[q + 2]),
+                                          tf32r(R.a[q + 3]));
+            const float4 l4 = make_float4(tf32r(R.a[q] - h4.x), tf32r(R.a[q + 1] - h4.y),
+                                          tf32r(R.a[q + 2] - h4.z), tf32r(R.a[q + 3] - h4.w));
+            *reinterpret_cast<float4 *>(aH + swz(row, i + q)) = h4;
+            *reinterpret_cast<float4 *>(aL + swz(row, i + q)) = l4;
         }
-        // B: N rows x 32
-        for (int e = tid; e < N * 32; e += 128) {
-            const int r = e >> 5, kk = e & 31;
-            bH[swz(r, kk)] = __ldg(bhi + (int64_t)r * Kp + 32 * j + kk);
-            bL[swz(r, kk)] = __ldg(blo + (int64_t)r * Kp + 32 * j + kk);
+#pragma unroll
+        for (int u = 0; u < ChunkRegs<N>::BPT; ++u) {
+            const int e = tid + 256 * u;
+            if (e < N * 32) {
+                const int r = e >> 5, kk = e & 31;
+                bH[swz(r, kk)] = R.bh[u];
+                bL[swz(r, kk)] = R.bl[u];
+            }
         }
+        if (j + 1 < nchunk)
+            load_chunk<N>(R, j + 1, half, tid, live, x, y, z, h, w, l, n, ic, K27, Kp, in, bhi,
+                          blo);
         asm volatile("fence.proxy.async.shared::cta;");
         __syncthreads();
         if (tid == 0) {
@@ -163,19 +189,23 @@ tcconv_k(const float *__restrict__ in, int ic, int h, int w, int l, const float 
     // the last chunk's commit covers every MMA before it
     mbar_wait(&bar[(nchunk - 1) & 1], ((nchunk - 1) >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    // epilogue: lane = voxel, columns = output channels
+    // epilogue: lane = voxel, columns = output channels (warps 0-3 own TMEM
+    // lanes 0-127)
+    if (warp < 4) {
 #pragma unroll
-    for (int c = 0; c < N; c += 8) {
-        uint32_t v[8];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c;
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                       "=r"(v[6]), "=r"(v[7]) : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-        if (live)
+        for (int c = 0; c < N; c += 8) {
+            uint32_t v[8];
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c;
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                           "=r"(v[6]), "=r"(v[7]) : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            if (live)
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                out[(int64_t)(c + q) * n + p] = __uint_as_float(v[q]) + (bias ? bias[c + q] : 0.0f);
+                for (int q = 0; q < 8; ++q)
+                    out[(int64_t)(c + q) * n + p] =
+                        __uint_as_float(v[q]) + (bias ? bias[c + q] : 0.0f);
+        }
     }
     __syncthreads();
     if (warp == 0)
@@ -198,8 +228,9 @@ extern "C" int tcconv_fwd(const float *in, int ic, int h, int w, int l, const fl
     case NV:                                                                                    \
         cudaFuncSetAttribute(tcconv_k<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                              (int)smem);                                                        \
-        tcconv_k<NV><<<g, 128, smem, st>>>(in, ic, h, w, l, bhi, blo, Kp, bias, out);           \
+        tcconv_k<NV><<<g, 256, smem, st>>>(in, ic, h, w, l, bhi, blo, Kp, bias, out);           \
         break;
+    if (ic % 16) return -1;  // the chunk loader assumes one tap per 16 channels
     switch (oc) {
         TC(8) TC(16) TC(32) TC(64) TC(128)
         default: return -1;
