@@ -124,7 +124,7 @@ tcconv_k(const float *__restrict__ in, int ic, int h, int w, int l, const float 
         z = t / w;
         y = t - z * w;
     }
-    constexpr int NCOL = N < 32 ? 32 : N;
+    constexpr int NCOL = 2 * N < 32 ? 32 : 2 * N;  // two accumulators (ping-pong)
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          su32(&tmem_base)), "r"(NCOL));
@@ -142,11 +142,38 @@ tcconv_k(const float *__restrict__ in, int ic, int h, int w, int l, const float 
     // j is split, stored and handed to the tensor core
     ChunkRegs<N> R;
     load_chunk<N>(R, 0, half, tid, live, x, y, z, h, w, l, n, ic, K27, Kp, in, bhi, blo);
+    // each chunk's 12 MMAs accumulate into a fresh TMEM accumulator (alternating
+    // between two); the chunk sums are added in fp32 registers, RN, in chunk
+    // order — the tensor core never accumulates across chunks.  Warps w and
+    // w+4 read TMEM lanes 32(w%4).. for the column halves [0, N/2), [N/2, N).
+    constexpr int NH = N / 2;
+    float acc[NH];
+#pragma unroll
+    for (int q = 0; q < NH; ++q) acc[q] = 0.0f;
+    auto drain = [&](int jc) {  // add chunk jc's accumulator
+        const uint32_t col = (uint32_t)((jc & 1) * N + half * NH);
+#pragma unroll
+        for (int c = 0; c < NH; c += 8) {
+            uint32_t v[8];
+            const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + col + (uint32_t)c;
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]),
+                           "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[c + q] += __uint_as_float(v[q]);
+        }
+    };
     for (int j = 0; j < nchunk; ++j) {
         const int sidx = j & 1;
         float *aH = sm + sidx * STAGE, *aL = aH + 128 * 32, *bH = aL + 128 * 32, *bL = bH + N * 32;
-        // the MMAs of chunk j-2 read this stage: wait for them
-        if (j >= 2) mbar_wait(&bar[sidx], ((j - 2) >> 1) & 1);
+        // the MMAs of chunk j-2 read this stage and wrote accumulator j & 1:
+        // wait for them, then fold that accumulator into the registers
+        if (j >= 2) {
+            mbar_wait(&bar[sidx], ((j - 2) >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            drain(j - 2);
+        }
         const int i = 16 * half;
 #pragma unroll
         for (int q = 0; q < 16; q += 4) {
@@ -170,43 +197,37 @@ tcconv_k(const float *__restrict__ in, int ic, int h, int w, int l, const float 
             load_chunk<N>(R, j + 1, half, tid, live, x, y, z, h, w, l, n, ic, K27, Kp, in, bhi,
                           blo);
         asm volatile("fence.proxy.async.shared::cta;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
         __syncthreads();
         if (tid == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t tacc = tmem + (uint32_t)(sidx * N);
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
                 const uint64_t ah = desc_swz(su32(aH) + 32 * s), al = desc_swz(su32(aL) + 32 * s);
                 const uint64_t bh = desc_swz(su32(bH) + 32 * s), bl = desc_swz(su32(bL) + 32 * s);
-                mma(tmem, ah, bh, id, (j | s) ? 1u : 0u);
-                mma(tmem, ah, bl, id, 1u);
-                mma(tmem, al, bh, id, 1u);
+                mma(tacc, ah, bh, id, s ? 1u : 0u);
+                mma(tacc, ah, bl, id, 1u);
+                mma(tacc, al, bh, id, 1u);
             }
             asm volatile(
                 "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                     su32(&bar[sidx])));
         }
     }
-    // the last chunk's commit covers every MMA before it
-    mbar_wait(&bar[(nchunk - 1) & 1], ((nchunk - 1) >> 1) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    // epilogue: lane = voxel, columns = output channels (warps 0-3 own TMEM
-    // lanes 0-127)
-    if (warp < 4) {
-#pragma unroll
-        for (int c = 0; c < N; c += 8) {
-            uint32_t v[8];
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c;
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                           "=r"(v[6]), "=r"(v[7]) : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;");
-            if (live)
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    out[(int64_t)(c + q) * n + p] =
-                        __uint_as_float(v[q]) + (bias ? bias[c + q] : 0.0f);
-        }
+    // the last two chunks' accumulators
+    for (int jc = (nchunk >= 2 ? nchunk - 2 : 0); jc < nchunk; ++jc) {
+        mbar_wait(&bar[jc & 1], (jc >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        drain(jc);
     }
+    // epilogue: warps w and w+4 hold the two column halves of voxel row
+    if (live)
+#pragma unroll
+        for (int q = 0; q < NH; ++q) {
+            const int c = half * NH + q;
+            out[(int64_t)c * n + p] = acc[q] + (bias ? bias[c] : 0.0f);
+        }
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
