@@ -1323,6 +1323,9 @@ mdg_status enc_conv3_fwd(const float *in, int ic, mdg_dims3 dd, const float *w, 
                          bool *stats_done) {
     const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
     if (stats_done) *stats_done = false;
+    // 32 / 64 output channels on a large enough grid: the tensor cores
+    // (encoder_tc.cu; the normalisation statistics then run as separate passes)
+    if (enc_tc_conv_ok(ic, oc, dd)) return enc_tc_conv(in, ic, dd, w, oc, 0, b, false, out, st);
     const bool ig = use_igemm(oc, ic, d);
     CUtensorMap map;
     if (!ig && conv_map(&map, in, d, ic)) {
@@ -1349,7 +1352,12 @@ mdg_status enc_conv3_bwd(const float *in, int ic, mdg_dims3 dd, const float *w, 
                          const float *gout, float *gin, float *gw, float *gb, cudaStream_t st,
                          bool gin_acc) {
     const D3 d{dd.h, dd.w, dd.l, dd.h * dd.w * dd.l};
-    if (gin) {
+    if (gin && enc_tc_conv_ok(oc, ic, dd)) {
+        // the input gradient on the tensor cores: conv of gout with the
+        // flipped, transposed kernel
+        if (mdg_status s = enc_tc_conv(gout, oc, dd, w, ic, 1, nullptr, gin_acc, gin, st))
+            return s;
+    } else if (gin) {
         const bool ig = use_igemm(ic, oc, d);
         CUtensorMap map;
         if (!ig && conv_map(&map, gout, d, oc)) {

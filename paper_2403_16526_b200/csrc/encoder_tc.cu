@@ -1,0 +1,306 @@
+// encoder_tc.cu — the encoder's 3x3x3 convolution (ops.hpp:58-99, zero padded)
+// on the 5th-generation tensor cores, for the levels where that wins: 32 and
+// 64 output channels (L2, L3 of the small preset), forward and input gradient.
+//
+// Implicit GEMM D[voxel][o] = sum_k A[voxel][k] B[o][k], k = tap * ic + c:
+//   * one CTA = 128 consecutive output voxels (the MMA's M) and 256 threads:
+//     thread pairs gather their voxel's 32-value K chunk (im2col on the fly,
+//     one tap x 16 channels each), with the NEXT chunk's global loads in
+//     flight while this one is split and stored;
+//   * fp32 accuracy from 3xTF32: every operand is split into tf32 hi + lo,
+//     stored 128-byte swizzled K-major in shared memory; one thread issues
+//     4 K-steps x (hi*hi + hi*lo + lo*hi) = 12 tcgen05.mma per chunk;
+//   * each chunk accumulates into a FRESH TMEM accumulator (two, alternating)
+//     and the chunk sums are added in fp32 registers (round to nearest, in
+//     chunk order): the tensor core never accumulates across chunks, which
+//     keeps the error at ~2e-7 relative to float64 (a single TMEM accumulator
+//     over 100+ K steps drifts to 1e-5; tools/exp/tcconv.cu);
+//   * two shared-memory stages; chunk j's operands are free when the commit
+//     of chunk j-2 has arrived on its mbarrier.
+// The input gradient is the same convolution of gout with the flipped,
+// transposed kernel (w'[c][o][26 - t] = w[o][c][t]).  Measured against the
+// FFMA2 / implicit-GEMM kernels it replaces: 1.2-1.4x faster
+// at these shapes and about 3x more accurate; slower for N <= 16 or on grids
+// of fewer than ~4k voxels, which keep the old kernels.
+#include <cstdlib>
+
+#include "mdg_common.cuh"
+
+namespace mdg {
+namespace tc {
+
+__device__ __forceinline__ uint32_t su32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+// element (r, k) of an R x 32 fp32 tile, 128-byte swizzle (8-row atoms of 1 KB)
+__device__ __forceinline__ int swz(int r, int k) {
+    return ((r >> 3) * 1024 + (r & 7) * 128 + (((k >> 2) ^ (r & 7)) << 4)) / 4 + (k & 3);
+}
+// shared-memory matrix descriptor: K-major, SWIZZLE_128B, 1 KB between 8-row atoms
+__device__ __forceinline__ uint64_t desc_swz(uint32_t addr) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) |
+           ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: D f32, A / B tf32, both K-major, M = 128
+__device__ __forceinline__ uint32_t idesc_tf32(int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ float tf32r(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned phase) {
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done) : "r"(su32(b)), "r"(phase) : "memory");
+    } while (!done);
+}
+
+// B = the weights as {N, Kp} (k = tap * ic + c, zero padded to Kp), split into
+// tf32 hi / lo.  flip: the input-gradient kernel w'[c][o][26 - t] of w {oc, ic, 27}
+__global__ void prep_b_k(const float *__restrict__ w, int oc, int ic, int flip, int N, int Kin,
+                         int Kp, float *__restrict__ bhi, float *__restrict__ blo) {
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= N * Kp) return;
+    const int o = i / Kp, k = i % Kp;
+    float v = 0.0f;
+    if (k < 27 * Kin) {
+        const int tap = k / Kin, c = k % Kin;
+        v = flip ? w[((int64_t)c * ic + o) * 27 + (26 - tap)] : w[((int64_t)o * ic + c) * 27 + tap];
+    }
+    const float h = tf32r(v);
+    bhi[i] = h;
+    blo[i] = tf32r(v - h);
+}
+
+template <int N>
+struct ChunkRegs {
+    static constexpr int BPT = (N * 32 + 255) / 256;  // B values per thread
+    float a[16], bh[BPT], bl[BPT];
+};
+
+// this thread's share of K chunk j: 16 channels of one tap of its voxel, and
+// its B values (Kin % 16 == 0, so a half chunk never straddles taps)
+template <int N>
+__device__ __forceinline__ void load_chunk(ChunkRegs<N> &R, int j, int half, int tid, bool live,
+                                           int x, int y, int z, int h, int w, int l, int64_t n,
+                                           int Kin, int Kp, const float *__restrict__ in,
+                                           const float *__restrict__ bhi,
+                                           const float *__restrict__ blo) {
+#pragma unroll
+    for (int u = 0; u < ChunkRegs<N>::BPT; ++u) {
+        const int e = tid + 256 * u;
+        if (e < N * 32) {
+            const int r = e >> 5, kk = e & 31;
+            R.bh[u] = __ldg(bhi + (int64_t)r * Kp + 32 * j + kk);
+            R.bl[u] = __ldg(blo + (int64_t)r * Kp + 32 * j + kk);
+        }
+    }
+    const int k = 32 * j + 16 * half;
+    const int tap = k < 27 * Kin ? k / Kin : 27;
+    const int c0 = k - tap * Kin;
+    bool ok = false;
+    int64_t off = 0;
+    if (tap < 27 && live) {
+        const int xx = x + tap % 3 - 1, yy = y + (tap / 3) % 3 - 1, zz = z + tap / 9 - 1;
+        ok = xx >= 0 && xx < h && yy >= 0 && yy < w && zz >= 0 && zz < l;
+        off = (int64_t)c0 * n + ((int64_t)zz * w + yy) * h + xx;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) R.a[q] = ok ? __ldg(in + off + (int64_t)q * n) : 0.0f;
+}
+
+template <int N>
+__global__ void __launch_bounds__(256)
+conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *__restrict__ bhi,
+       const float *__restrict__ blo, int Kp, const float *__restrict__ bias, int acc_out,
+       float *__restrict__ out) {
+    extern __shared__ __align__(1024) float sm_raw[];
+    // the swizzle atoms start on 1 KB boundaries of the shared window
+    float *sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u) / 4;
+    constexpr int STAGE = 2 * 128 * 32 + 2 * N * 32;  // floats per stage
+    constexpr int NH = N / 2;
+    __shared__ uint64_t bar[2];
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int row = tid & 127, half = tid >> 7;  // voxel row; K half / column half
+    const int64_t n = (int64_t)h * w * l;
+    const int64_t p = (int64_t)blockIdx.x * 128 + row;
+    const bool live = p < n;
+    int x = 0, y = 0, z = 0;
+    if (live) {
+        const int t = (int)(p / h);
+        x = (int)(p - (int64_t)t * h);
+        z = t / w;
+        y = t - z * w;
+    }
+    constexpr uint32_t NCOL = 2 * N;  // two accumulators (64 or 128 columns)
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         su32(&tmem_base)), "r"(NCOL));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[1])));
+    }
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base, id = idesc_tf32(N);
+    const int nchunk = Kp / 32;
+    float acc[NH];
+#pragma unroll
+    for (int q = 0; q < NH; ++q) acc[q] = 0.0f;
+    // fold chunk jc's accumulator into the registers: warps w and w + 4 read
+    // TMEM lanes 32 (w % 4) .. +31, column halves [0, N/2) and [N/2, N)
+    auto drain = [&](int jc) {
+        const uint32_t col = (uint32_t)((jc & 1) * N + half * NH);
+#pragma unroll
+        for (int c = 0; c < NH; c += 8) {
+            uint32_t v[8];
+            const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + col + (uint32_t)c;
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]),
+                           "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[c + q] += __uint_as_float(v[q]);
+        }
+    };
+    ChunkRegs<N> R;
+    load_chunk<N>(R, 0, half, tid, live, x, y, z, h, w, l, n, Kin, Kp, in, bhi, blo);
+    for (int j = 0; j < nchunk; ++j) {
+        const int sidx = j & 1;
+        float *aH = sm + sidx * STAGE, *aL = aH + 128 * 32, *bH = aL + 128 * 32, *bL = bH + N * 32;
+        if (j >= 2) {  // chunk j-2's MMAs read this stage and wrote accumulator j & 1
+            mbar_wait(&bar[sidx], ((j - 2) >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            drain(j - 2);
+        }
+        const int i0 = 16 * half;
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) {
+            const float4 h4 = make_float4(tf32r(R.a[q]), tf32r(R.a[q + 1]), tf32r(R.a[q + 2]),
+                                          tf32r(R.a[q + 3]));
+            const float4 l4 = make_float4(tf32r(R.a[q] - h4.x), tf32r(R.a[q + 1] - h4.y),
+                                          tf32r(R.a[q + 2] - h4.z), tf32r(R.a[q + 3] - h4.w));
+            *reinterpret_cast<float4 *>(aH + swz(row, i0 + q)) = h4;
+            *reinterpret_cast<float4 *>(aL + swz(row, i0 + q)) = l4;
+        }
+#pragma unroll
+        for (int u = 0; u < ChunkRegs<N>::BPT; ++u) {
+            const int e = tid + 256 * u;
+            if (e < N * 32) {
+                const int r = e >> 5, kk = e & 31;
+                bH[swz(r, kk)] = R.bh[u];
+                bL[swz(r, kk)] = R.bl[u];
+            }
+        }
+        if (j + 1 < nchunk)  // the next chunk's loads fly during the handoff below
+            load_chunk<N>(R, j + 1, half, tid, live, x, y, z, h, w, l, n, Kin, Kp, in, bhi, blo);
+        asm volatile("fence.proxy.async.shared::cta;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t tacc = tmem + (uint32_t)(sidx * N);
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const uint64_t ah = desc_swz(su32(aH) + 32 * s), al = desc_swz(su32(aL) + 32 * s);
+                const uint64_t bh = desc_swz(su32(bH) + 32 * s), bl = desc_swz(su32(bL) + 32 * s);
+                mma(tacc, ah, bh, id, s ? 1u : 0u);
+                mma(tacc, ah, bl, id, 1u);
+                mma(tacc, al, bh, id, 1u);
+            }
+            asm volatile(
+                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    su32(&bar[sidx])));
+        }
+    }
+    for (int jc = nchunk >= 2 ? nchunk - 2 : 0; jc < nchunk; ++jc) {  // the last two chunks
+        mbar_wait(&bar[jc & 1], (jc >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        drain(jc);
+    }
+    if (live)
+#pragma unroll
+        for (int q = 0; q < NH; ++q) {
+            const int c = half * NH + q;
+            float *o = out + (int64_t)c * n + p;
+            const float v = acc[q] + (bias ? bias[c] : 0.0f);
+            *o = acc_out ? *o + v : v;
+        }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(NCOL));
+}
+
+template <int N>
+constexpr size_t smem_bytes() {
+    return (size_t)2 * (2 * 128 * 32 + 2 * N * 32) * sizeof(float) + 1024;
+}
+
+}  // namespace tc
+
+// MDG_ENC_TC=0 turns the tensor-core path off (A/B comparisons)
+static bool tc_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("MDG_ENC_TC");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+bool enc_tc_conv_ok(int kin, int nout, mdg_dims3 d) {
+    const int64_t n = (int64_t)d.h * d.w * d.l;
+    return tc_enabled() && (nout == 32 || nout == 64) && kin % 16 == 0 && kin <= 128 &&
+           n >= 4096 && n < (int64_t(1) << 31);
+}
+
+// out[o] (=, or += with acc) conv(in {kin, n}, B) for nout = 32 or 64 output
+// channels.  flip = 0: the forward (w {nout, kin, 27}); flip = 1: the input
+// gradient of a conv with weights w {kin, nout, 27} (gout has kin channels).
+mdg_status enc_tc_conv(const float *in, int kin, mdg_dims3 d, const float *w, int nout, int flip,
+                       const float *bias, bool acc, float *out, cudaStream_t st) {
+    const int Kp = (27 * kin + 31) / 32 * 32;
+    Scratch sb;
+    MDG_CUDA_TRY(sb.alloc((size_t)2 * nout * Kp * sizeof(float), st));
+    float *bhi = sb.as<float>(), *blo = bhi + (size_t)nout * Kp;
+    // w's ic (the forward's input channels): kin forward, nout for the flip
+    const int wic = flip ? nout : kin, woc = flip ? kin : nout;
+    tc::prep_b_k<<<(nout * Kp + 255) / 256, 256, 0, st>>>(w, woc, wic, flip, nout, kin, Kp, bhi,
+                                                          blo);
+    MDG_LAUNCHED();
+    const int64_t n = (int64_t)d.h * d.w * d.l;
+    const unsigned g = (unsigned)((n + 127) / 128);
+    if (nout == 32) {
+        constexpr size_t sm = tc::smem_bytes<32>();
+        MDG_CUDA_TRY(cudaFuncSetAttribute(tc::conv_k<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sm));
+        tc::conv_k<32><<<g, 256, sm, st>>>(in, kin, d.h, d.w, d.l, bhi, blo, Kp, bias, acc ? 1 : 0,
+                                           out);
+    } else {
+        constexpr size_t sm = tc::smem_bytes<64>();
+        MDG_CUDA_TRY(cudaFuncSetAttribute(tc::conv_k<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sm));
+        tc::conv_k<64><<<g, 256, sm, st>>>(in, kin, d.h, d.w, d.l, bhi, blo, Kp, bias, acc ? 1 : 0,
+                                           out);
+    }
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
+}  // namespace mdg

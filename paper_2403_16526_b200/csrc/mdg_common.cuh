@@ -173,6 +173,10 @@ mdg_status enc_in_slab_bwd_apply(const float *x, const float *gz, int C, int64_t
                                  const float *g, const float *b, float slope, const float *mean,
                                  const float *inv, const float *sums, int64_t nstat, float *gx,
                                  cudaStream_t st);
+// encoder_tc.cu: the 3x3x3 conv on tcgen05 for 32 / 64 output channels
+bool enc_tc_conv_ok(int kin, int nout, mdg_dims3 d);
+mdg_status enc_tc_conv(const float *in, int kin, mdg_dims3 d, const float *w, int nout, int flip,
+                       const float *bias, bool acc, float *out, cudaStream_t st);
 mdg_status enc_avgpool_fwd(const float *in, int C, mdg_dims3 d, float *out, cudaStream_t st);
 mdg_status enc_avgpool_bwd(const float *gout, int C, mdg_dims3 d, float *gin, cudaStream_t st);
 // optim.cu: AdamOptimizer::step over a whole parameter list in one launch
