@@ -22,6 +22,7 @@
 // FFMA2 / implicit-GEMM kernels it replaces: 1.2-1.4x faster
 // at these shapes and about 3x more accurate; slower for N <= 16 or on grids
 // of fewer than ~4k voxels, which keep the old kernels.
+#include <algorithm>
 #include <cstdlib>
 
 #include "mdg_common.cuh"
@@ -121,11 +122,16 @@ __device__ __forceinline__ void load_chunk(ChunkRegs<N> &R, int j, int half, int
     for (int q = 0; q < 16; ++q) R.a[q] = ok ? __ldg(in + off + (int64_t)q * n) : 0.0f;
 }
 
+// blockIdx.x: 128-voxel tile; blockIdx.y: K split (chunks [y*jsplit, ..));
+// blockIdx.z: the output-channel slice [z*N, z*N+N) of nout.  With part
+// non-null the split's partial sums go to part[y][c][p] (the reduce kernel
+// adds them in split order); otherwise out (=, or += with acc_out) + bias.
 template <int N>
 __global__ void __launch_bounds__(256)
 conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *__restrict__ bhi,
-       const float *__restrict__ blo, int Kp, const float *__restrict__ bias, int acc_out,
-       float *__restrict__ out) {
+       const float *__restrict__ blo, int Kp, int jsplit, int nout,
+       const float *__restrict__ bias, int acc_out, float *__restrict__ out,
+       float *__restrict__ part) {
     extern __shared__ __align__(1024) float sm_raw[];
     // the swizzle atoms start on 1 KB boundaries of the shared window
     float *sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u) / 4;
@@ -158,14 +164,17 @@ conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base, id = idesc_tf32(N);
-    const int nchunk = Kp / 32;
+    const int jb = blockIdx.y * jsplit, je = min(jb + jsplit, Kp / 32), nl = je - jb;
+    const int cz = blockIdx.z * N;  // first output channel of this CTA
+    bhi += (int64_t)cz * Kp;
+    blo += (int64_t)cz * Kp;
     float acc[NH];
 #pragma unroll
     for (int q = 0; q < NH; ++q) acc[q] = 0.0f;
     // fold chunk jc's accumulator into the registers: warps w and w + 4 read
     // TMEM lanes 32 (w % 4) .. +31, column halves [0, N/2) and [N/2, N)
-    auto drain = [&](int jc) {
-        const uint32_t col = (uint32_t)((jc & 1) * N + half * NH);
+    auto drain = [&](int tc) {  // local chunk index: accumulator tc & 1
+        const uint32_t col = (uint32_t)((tc & 1) * N + half * NH);
 #pragma unroll
         for (int c = 0; c < NH; c += 8) {
             uint32_t v[8];
@@ -179,14 +188,14 @@ conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *
         }
     };
     ChunkRegs<N> R;
-    load_chunk<N>(R, 0, half, tid, live, x, y, z, h, w, l, n, Kin, Kp, in, bhi, blo);
-    for (int j = 0; j < nchunk; ++j) {
-        const int sidx = j & 1;
+    load_chunk<N>(R, jb, half, tid, live, x, y, z, h, w, l, n, Kin, Kp, in, bhi, blo);
+    for (int t = 0; t < nl; ++t) {  // local chunk t = global chunk jb + t
+        const int j = jb + t, sidx = t & 1;
         float *aH = sm + sidx * STAGE, *aL = aH + 128 * 32, *bH = aL + 128 * 32, *bL = bH + N * 32;
-        if (j >= 2) {  // chunk j-2's MMAs read this stage and wrote accumulator j & 1
-            mbar_wait(&bar[sidx], ((j - 2) >> 1) & 1);
+        if (t >= 2) {  // chunk t-2's MMAs read this stage and wrote accumulator t & 1
+            mbar_wait(&bar[sidx], ((t - 2) >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            drain(j - 2);
+            drain(t - 2);
         }
         const int i0 = 16 * half;
 #pragma unroll
@@ -207,7 +216,7 @@ conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *
                 bL[swz(r, kk)] = R.bl[u];
             }
         }
-        if (j + 1 < nchunk)  // the next chunk's loads fly during the handoff below
+        if (t + 1 < nl)  // the next chunk's loads fly during the handoff below
             load_chunk<N>(R, j + 1, half, tid, live, x, y, z, h, w, l, n, Kin, Kp, in, bhi, blo);
         asm volatile("fence.proxy.async.shared::cta;");
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -228,24 +237,44 @@ conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *
                     su32(&bar[sidx])));
         }
     }
-    for (int jc = nchunk >= 2 ? nchunk - 2 : 0; jc < nchunk; ++jc) {  // the last two chunks
-        mbar_wait(&bar[jc & 1], (jc >> 1) & 1);
+    for (int tc = nl >= 2 ? nl - 2 : 0; tc < nl; ++tc) {  // the last two chunks
+        mbar_wait(&bar[tc & 1], (tc >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        drain(jc);
+        drain(tc);
     }
-    if (live)
+    if (live) {
+        if (part) {
 #pragma unroll
-        for (int q = 0; q < NH; ++q) {
-            const int c = half * NH + q;
-            float *o = out + (int64_t)c * n + p;
-            const float v = acc[q] + (bias ? bias[c] : 0.0f);
-            *o = acc_out ? *o + v : v;
+            for (int q = 0; q < NH; ++q)
+                part[((int64_t)blockIdx.y * nout + cz + half * NH + q) * n + p] = acc[q];
+        } else {
+#pragma unroll
+            for (int q = 0; q < NH; ++q) {
+                const int c = cz + half * NH + q;
+                float *o = out + (int64_t)c * n + p;
+                const float v = acc[q] + (bias ? bias[c] : 0.0f);
+                *o = acc_out ? *o + v : v;
+            }
         }
+    }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                      "r"(NCOL));
+}
+
+// out[c][p] (=, or +=) sum over splits s in order of part[s][c][p], + bias
+__global__ void split_reduce_k(const float *__restrict__ part, int S, int nout, int64_t n,
+                               const float *__restrict__ bias, int acc_out,
+                               float *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (i >= (int64_t)nout * n) return;
+    const int c = (int)(i / n);
+    float v = 0.0f;
+    for (int s = 0; s < S; ++s) v += part[(int64_t)s * nout * n + i];
+    v += bias ? bias[c] : 0.0f;
+    out[i] = acc_out ? out[i] + v : v;
 }
 
 template <int N>
@@ -266,40 +295,57 @@ static bool tc_enabled() {
 
 bool enc_tc_conv_ok(int kin, int nout, mdg_dims3 d) {
     const int64_t n = (int64_t)d.h * d.w * d.l;
-    return tc_enabled() && (nout == 32 || nout == 64) && kin % 16 == 0 && kin <= 128 &&
-           n >= 4096 && n < (int64_t(1) << 31);
+    return tc_enabled() && (nout == 32 || nout == 64 || nout == 128) && kin % 16 == 0 &&
+           kin <= 128 && n >= 128 && n < (int64_t(1) << 31);
 }
 
-// out[o] (=, or += with acc) conv(in {kin, n}, B) for nout = 32 or 64 output
-// channels.  flip = 0: the forward (w {nout, kin, 27}); flip = 1: the input
-// gradient of a conv with weights w {kin, nout, 27} (gout has kin channels).
+// out[o] (=, or += with acc) conv(in {kin, n}, B) for nout = 32, 64 or 128
+// output channels.  flip = 0: the forward (w {nout, kin, 27}); flip = 1: the
+// input gradient of a conv with weights w {kin, nout, 27} (gout has kin
+// channels).  Small grids split K across CTAs (fixed-order reduction) and
+// 128 outputs run as two 64-channel slices.
 mdg_status enc_tc_conv(const float *in, int kin, mdg_dims3 d, const float *w, int nout, int flip,
                        const float *bias, bool acc, float *out, cudaStream_t st) {
-    const int Kp = (27 * kin + 31) / 32 * 32;
+    const int Kp = (27 * kin + 31) / 32 * 32, nchunk = Kp / 32;
+    const int N = nout == 32 ? 32 : 64, nz = nout / N;
+    const int64_t n = (int64_t)d.h * d.w * d.l;
+    const int tiles = (int)((n + 127) / 128);
+    // enough CTAs for 2 per SM, each split >= 4 chunks
+    int S = std::max(1, (2 * 148 + tiles * nz - 1) / (tiles * nz));
+    S = std::min(S, std::max(1, nchunk / 4));
+    const int jsplit = (nchunk + S - 1) / S;
+    S = (nchunk + jsplit - 1) / jsplit;
     Scratch sb;
-    MDG_CUDA_TRY(sb.alloc((size_t)2 * nout * Kp * sizeof(float), st));
+    MDG_CUDA_TRY(sb.alloc(((size_t)2 * nout * Kp + (S > 1 ? (size_t)S * nout * n : 0)) *
+                              sizeof(float), st));
     float *bhi = sb.as<float>(), *blo = bhi + (size_t)nout * Kp;
+    float *part = S > 1 ? blo + (size_t)nout * Kp : nullptr;
     // w's ic (the forward's input channels): kin forward, nout for the flip
     const int wic = flip ? nout : kin, woc = flip ? kin : nout;
     tc::prep_b_k<<<(nout * Kp + 255) / 256, 256, 0, st>>>(w, woc, wic, flip, nout, kin, Kp, bhi,
                                                           blo);
     MDG_LAUNCHED();
-    const int64_t n = (int64_t)d.h * d.w * d.l;
-    const unsigned g = (unsigned)((n + 127) / 128);
-    if (nout == 32) {
+    const dim3 g((unsigned)tiles, (unsigned)S, (unsigned)nz);
+    const int accf = acc ? 1 : 0;
+    if (N == 32) {
         constexpr size_t sm = tc::smem_bytes<32>();
         MDG_CUDA_TRY(cudaFuncSetAttribute(tc::conv_k<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)sm));
-        tc::conv_k<32><<<g, 256, sm, st>>>(in, kin, d.h, d.w, d.l, bhi, blo, Kp, bias, acc ? 1 : 0,
-                                           out);
+        tc::conv_k<32><<<g, 256, sm, st>>>(in, kin, d.h, d.w, d.l, bhi, blo, Kp, jsplit, nout,
+                                           bias, accf, out, part);
     } else {
         constexpr size_t sm = tc::smem_bytes<64>();
         MDG_CUDA_TRY(cudaFuncSetAttribute(tc::conv_k<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)sm));
-        tc::conv_k<64><<<g, 256, sm, st>>>(in, kin, d.h, d.w, d.l, bhi, blo, Kp, bias, acc ? 1 : 0,
-                                           out);
+        tc::conv_k<64><<<g, 256, sm, st>>>(in, kin, d.h, d.w, d.l, bhi, blo, Kp, jsplit, nout,
+                                           bias, accf, out, part);
     }
     MDG_LAUNCHED();
+    if (S > 1) {
+        tc::split_reduce_k<<<(unsigned)(((int64_t)nout * n + 255) / 256), 256, 0, st>>>(
+            part, S, nout, n, bias, accf, out);
+        MDG_LAUNCHED();
+    }
     return MDG_OK;
 }
 
