@@ -84,10 +84,12 @@ int64_t mdg_launch_count(void);
 /* Deterministic mode (process-wide; initial value from the environment
  * variable MDG_DETERMINISTIC).  Off: the warp / compose input gradients are
  * scattered with float atomics (fastest; the summation order at a shared
- * corner varies between runs).  On: they are gathered per target in a fixed
- * order, so every result — and a whole pairwise optimisation — is
- * bit-identical from run to run, as the reference guarantees
- * (test_engine.cpp:194-213); the warp backward then costs ~3x.  Every other
+ * corner varies between runs).  On: whole-volume calls scatter into a 64-bit
+ * fixed-point accumulator (integer adds: order independent; ~1.7x the warp
+ * backward's time and 8 bytes of pool scratch per gin element), voxel-range
+ * calls gather per target in a fixed order (~3x), so every result — and a
+ * whole pairwise optimisation — is bit-identical from run to run, as the
+ * reference guarantees (test_engine.cpp:194-213).  Every other
  * kernel is deterministic in both modes.  Returns the previous setting. */
 int mdg_set_deterministic(int on);
 int mdg_get_deterministic(void);

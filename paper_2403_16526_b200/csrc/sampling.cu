@@ -283,27 +283,98 @@ __device__ __forceinline__ void scatter_row2(float *ia, float *ib, bool two, boo
     }
 }
 
+// Deterministic gin (mdg_set_deterministic): a 64-bit fixed-point scatter.
+// Channel c's terms are rounded to integers at the scale 2^k_c, k_c chosen from
+// max |gout_c| so that a sum of up to 8n terms stays below 2^62 (2^-36 of the
+// channel maximum or finer at 7 M voxels), and added with integer REDs: an
+// integer sum does not depend on the order the adds arrive in, so gin is
+// bit-identical from run to run.  fix_convert_k adds acc * 2^-k_c into gin
+// (one rounding of the exact sum).  A channel whose gradient holds Inf/NaN
+// has no scale and is scattered in fp32 (NaN propagation as the reference).
+struct FixAcc {
+    long long *acc;      // C planes of n, zeroed
+    const unsigned *mx;  // per channel max |gout| as float bits (fix_maxabs_k)
+};
+__device__ __forceinline__ bool fix_finite(unsigned mbits) { return mbits < 0x7f800000u; }
+__device__ __forceinline__ int fix_exp(unsigned mbits, int64_t n) {
+    int e;
+    frexpf(__uint_as_float(mbits), &e);  // max |g| < 2^e
+    const int hb = 64 - __clzll((unsigned long long)(8 * n));
+    return 62 - e - hb;
+}
+// 2^k as two float factors (k spans about [-100, 211])
+__device__ __forceinline__ float2 fix_scale(unsigned mbits, int64_t n) {
+    const int k = fix_exp(mbits, n);
+    return make_float2(exp2f((float)(k / 2)), exp2f((float)(k - k / 2)));
+}
+// round(t * 2^k): the power-of-two products are exact
+__device__ __forceinline__ long long fix_q(float t, float2 s) {
+    return __float2ll_rn(mul_(mul_(t, s.x), s.y));
+}
+__device__ __forceinline__ void red_fix_if(long long *a, long long v, bool p) {
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q red.global.add.u64 [%0], %1;\n}\n" ::"l"(a),
+        "l"(v), "r"((int)p)
+        : "memory");
+}
+__device__ __forceinline__ void scatter_row2_fix(long long *ia, long long *ib, bool two, bool ok,
+                                                 int r, float2 t0, float2 t1, bool in, bool out,
+                                                 float2 sa, float2 sb) {
+    long long q0a = fix_q(t0.x, sa), q1a = fix_q(t1.x, sa);
+    long long q0b = fix_q(t0.y, sb), q1b = fix_q(t1.y, sb);
+    const long long na = __shfl_up_sync(0xffffffffu, q1a, 1);
+    const long long nb = __shfl_up_sync(0xffffffffu, q1b, 1);
+    q0a = in ? q0a + na : q0a;
+    q0b = in ? q0b + nb : q0b;
+    long long *a = ia + r, *b = ib + r;
+    red_fix_if(a, q0a, ok);
+    red_fix_if(a + 1, q1a, ok && !out);
+    if (two) {
+        red_fix_if(b, q0b, ok);
+        red_fix_if(b + 1, q1b, ok && !out);
+    }
+}
+__device__ __forceinline__ void scatter_fix(long long *__restrict__ gp, const Corners &c, float g,
+                                            float2 s) {
+    const int x0 = c.ax.i0, dx = c.ax.i1 - c.ax.i0;
+    const float wx0 = sub_(1.0f, c.ax.f), wx1 = c.ax.f;
+    const float wy0 = sub_(1.0f, c.ay.f), wy1 = c.ay.f;
+    const float wz0 = sub_(1.0f, c.az.f), wz1 = c.az.f;
+    long long *r00 = gp + (c.o00 + x0), *r10 = gp + (c.o10 + x0);
+    long long *r01 = gp + (c.o01 + x0), *r11 = gp + (c.o11 + x0);
+    red_fix_if(r00, fix_q(mul_(mul_(mul_(g, wx0), wy0), wz0), s), true);
+    red_fix_if(r00 + dx, fix_q(mul_(mul_(mul_(g, wx1), wy0), wz0), s), true);
+    red_fix_if(r10, fix_q(mul_(mul_(mul_(g, wx0), wy1), wz0), s), true);
+    red_fix_if(r10 + dx, fix_q(mul_(mul_(mul_(g, wx1), wy1), wz0), s), true);
+    red_fix_if(r01, fix_q(mul_(mul_(mul_(g, wx0), wy0), wz1), s), true);
+    red_fix_if(r01 + dx, fix_q(mul_(mul_(mul_(g, wx1), wy0), wz1), s), true);
+    red_fix_if(r11, fix_q(mul_(mul_(mul_(g, wx0), wy1), wz1), s), true);
+    red_fix_if(r11 + dx, fix_q(mul_(mul_(mul_(g, wx1), wy1), wz1), s), true);
+}
+
 // --------------------------------------------------------------- warp bwd
 // sampling.hpp:139-167 (gfield: same per-channel order => bit-exact)
 // rbits (nullable): atomicMax of max |phi| over the voxels (float bits), the
 // displacement bound the deterministic gin gather needs (warp_gather.cu).
 // far_only: this launch is the gather's fallback scatter and runs only when
 // that bound exceeds the gather's reach (else every thread returns at once).
-template <int CT, bool COMPOSE = false, bool SLAB = false>
+template <int CT, bool COMPOSE = false, bool SLAB = false, bool FIX = false>
 #ifndef MDG_WBWD_MINB
 #define MDG_WBWD_MINB 5
 #endif
 #ifndef MDG_WBWD_MINB16
 #define MDG_WBWD_MINB16 4
 #endif
-// (the slab form's extra strides and window test need more registers)
-__global__ void __launch_bounds__(kSB, SLAB ? (CT == 16 ? 3 : CT == 8 ? 4 : 5)
+// (the slab form's extra strides and window test, and the fixed-point
+// scatter's 64-bit terms, need more registers)
+__global__ void __launch_bounds__(kSB, (SLAB || FIX) ? (CT == 16 ? 3 : CT == 8 ? 4 : 5)
                                        : CT == 16 ? MDG_WBWD_MINB16
                                        : (CT == 3 || CT == 8) ? MDG_WBWD_MINB : 5)
 warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
            const float *__restrict__ field, const float *__restrict__ gout,
            float *__restrict__ gin, float *__restrict__ gfield, int64_t pb, int64_t pe,
-           WarpWin win, unsigned *__restrict__ rbits = nullptr, bool far_only = false) {
+           WarpWin win, unsigned *__restrict__ rbits = nullptr, bool far_only = false,
+           FixAcc fxa = FixAcc{nullptr, nullptr}) {
     if (far_only && __uint_as_float(*rbits) <= (float)kGatherReach) return;
     // in/gin and field/gout/gfield channel strides (SLAB: WarpWin)
     const int64_t n = SLAB ? win.csi : (int64_t)h * w * l, m = SLAB ? win.csv : n;
@@ -340,7 +411,7 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
         const int r00 = c.o00 + c.ax.i0, r10 = c.o10 + c.ax.i0;
         const int r01 = c.o01 + c.ax.i0, r11 = c.o11 + c.ax.i0;
         XMerge mg;
-        if (gin) {
+        if (gin || FIX) {
             xmerge_row(r00, ok, mg.in[0], mg.out[0]);
             xmerge_row(r10, ok, mg.in[1], mg.out[1]);
             xmerge_row(r01, ok, mg.in[2], mg.out[2]);
@@ -413,7 +484,14 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
             const float ga = gv[ch];
             const float gb = two ? gv[ch + 1] : 0.0f;
             const float2 g2 = make_float2(ga, gb);
-            if (gin) {
+            // FIX: the pair's fixed-point scales (uniform branch: a non-finite
+            // channel sends the pair to the fp32 scatter)
+            const unsigned mba = FIX ? __ldg(fxa.mx + ch) : 0u;
+            const unsigned mbb = FIX && two ? __ldg(fxa.mx + ch + 1) : 0u;
+            // (a lone last channel counts as its own pair partner)
+            const bool fa = FIX && fix_finite(mba), fb = two ? FIX && fix_finite(mbb) : fa;
+            const bool fixp = fa && fb;
+            if (gin || FIX) {
                 // terms ((g*wx)*wy)*wz exactly as sampling.hpp:110-117, with the
                 // shared prefixes computed once
                 const float2 gx0 = m2(g2, GX), gx1 = m2(g2, FX);
@@ -424,18 +502,45 @@ warp_bwd_k(const float *__restrict__ in, int C, int h, int w, int l,
                              t011 = m2(g01, FZ), t111 = m2(g11, FZ);
                 // (a zero gradient gives exact zero terms: the reference's skip
                 // of g == 0 channels, sampling.hpp:152, changes nothing)
-                float *ia = gin + (int64_t)ch * n, *ib = ia + n;
-                scatter_row2(ia, ib, two, ok, r00, t000, t100, mg.in[0], mg.out[0]);
-                scatter_row2(ia, ib, two, ok, r10, t010, t110, mg.in[1], mg.out[1]);
-                scatter_row2(ia, ib, two, ok, r01, t001, t101, mg.in[2], mg.out[2]);
-                scatter_row2(ia, ib, two, ok, r11, t011, t111, mg.in[3], mg.out[3]);
+                if (fixp) {
+                    const float2 sa = fix_scale(mba, n), sb = two ? fix_scale(mbb, n) : sa;
+                    long long *ia = fxa.acc + (int64_t)ch * n, *ib = ia + n;
+                    scatter_row2_fix(ia, ib, two, ok, r00, t000, t100, mg.in[0], mg.out[0], sa, sb);
+                    scatter_row2_fix(ia, ib, two, ok, r10, t010, t110, mg.in[1], mg.out[1], sa, sb);
+                    scatter_row2_fix(ia, ib, two, ok, r01, t001, t101, mg.in[2], mg.out[2], sa, sb);
+                    scatter_row2_fix(ia, ib, two, ok, r11, t011, t111, mg.in[3], mg.out[3], sa, sb);
+                } else if (FIX && fa != fb) {
+                    // one channel of the pair finite, the other not: each alone
+                    auto sw = [](float2 v) { return make_float2(v.y, v.x); };
+                    const int rr[4] = {r00, r10, r01, r11};
+                    const float2 t0s[4] = {t000, t010, t001, t011}, t1s[4] = {t100, t110, t101, t111};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float2 u0 = fa ? t0s[q] : sw(t0s[q]), u1 = fa ? t1s[q] : sw(t1s[q]);
+                        const float2 v0 = sw(u0), v1 = sw(u1);
+                        const int cf = fa ? ch : ch + 1, cn = fa ? ch + 1 : ch;
+                        const float2 sf = fix_scale(fa ? mba : mbb, n);
+                        scatter_row2_fix(fxa.acc + (int64_t)cf * n, nullptr, false, ok, rr[q], u0, u1,
+                                         mg.in[q], mg.out[q], sf, sf);
+                        scatter_row2(gin + (int64_t)cn * n, nullptr, false, ok, rr[q], v0, v1,
+                                     mg.in[q], mg.out[q]);
+                    }
+                } else {
+                    float *ia = gin + (int64_t)ch * n, *ib = ia + n;
+                    scatter_row2(ia, ib, two, ok, r00, t000, t100, mg.in[0], mg.out[0]);
+                    scatter_row2(ia, ib, two, ok, r10, t010, t110, mg.in[1], mg.out[1]);
+                    scatter_row2(ia, ib, two, ok, r01, t001, t101, mg.in[2], mg.out[2]);
+                    scatter_row2(ia, ib, two, ok, r11, t011, t111, mg.in[3], mg.out[3]);
+                }
             }
         }
     } else {
         for (int ch = 0; ch < C; ++ch) {
             const float g = __ldg(gout + ch * m + vi);
             if (g == 0.0f) continue;
-            if (gin) scatter(gin + ch * n, c, g);
+            const unsigned mb = FIX ? __ldg(fxa.mx + ch) : 0u;
+            if (FIX && fix_finite(mb)) scatter_fix(fxa.acc + ch * n, c, g, fix_scale(mb, n));
+            else if (gin) scatter(gin + ch * n, c, g);
             if (gfield) {
                 float cg[3];
                 sample_grad(in + ch * n, c, cg);
@@ -643,6 +748,81 @@ __global__ void add2_k(const float *__restrict__ a, const float *__restrict__ b,
     if (i < m) out[i] = add_(a[i], b[i]);
 }
 
+// per channel max |g| as float bits (unsigned order = magnitude order; NaN
+// ranks above Inf): the fixed-point scale of the deterministic scatter
+__global__ void __launch_bounds__(kSB)
+fix_maxabs_k(const float *__restrict__ g, int64_t n, unsigned *__restrict__ mx) {
+    const float *gc = g + (int64_t)blockIdx.y * n;
+    unsigned m = 0u;
+    const int64_t stride = (int64_t)gridDim.x * kSB;
+    if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+        const float4 *g4 = reinterpret_cast<const float4 *>(gc);
+        for (int64_t i = (int64_t)blockIdx.x * kSB + threadIdx.x; i < n / 4; i += stride) {
+            const float4 v = __ldg(g4 + i);
+            m = max(max(m, __float_as_uint(fabsf(v.x))), __float_as_uint(fabsf(v.y)));
+            m = max(max(m, __float_as_uint(fabsf(v.z))), __float_as_uint(fabsf(v.w)));
+        }
+    } else {
+        for (int64_t i = (int64_t)blockIdx.x * kSB + threadIdx.x; i < n; i += stride)
+            m = max(m, __float_as_uint(fabsf(__ldg(gc + i))));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(mx + blockIdx.y, m);
+}
+
+// gin += acc * 2^-k (acc zero: gin untouched, a -0 stays -0)
+__device__ __forceinline__ float fix_add(float gin, long long a, float2 inv) {
+    return a == 0 ? gin : add_(gin, mul_(mul_(__ll2float_rn(a), inv.x), inv.y));
+}
+__global__ void __launch_bounds__(kSB)
+fix_convert_k(const long long *__restrict__ acc, int64_t n, const unsigned *__restrict__ mx,
+              float *__restrict__ gin) {
+    const unsigned mb = __ldg(mx + blockIdx.y);
+    if (!fix_finite(mb)) return;  // scattered in fp32
+    const int k = fix_exp(mb, n);
+    const float2 inv = make_float2(exp2f((float)(-(k / 2))), exp2f((float)(-(k - k / 2))));
+    const long long *ac = acc + (int64_t)blockIdx.y * n;
+    float *gc = gin + (int64_t)blockIdx.y * n;
+    const int64_t stride = (int64_t)gridDim.x * kSB;
+    if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(gin) & 15) == 0) {
+        for (int64_t i = (int64_t)blockIdx.x * kSB + threadIdx.x; i < n / 4; i += stride) {
+            const longlong2 a = __ldg(reinterpret_cast<const longlong2 *>(ac) + 2 * i);
+            const longlong2 b = __ldg(reinterpret_cast<const longlong2 *>(ac) + 2 * i + 1);
+            float4 v = reinterpret_cast<float4 *>(gc)[i];
+            v.x = fix_add(v.x, a.x, inv);
+            v.y = fix_add(v.y, a.y, inv);
+            v.z = fix_add(v.z, b.x, inv);
+            v.w = fix_add(v.w, b.y, inv);
+            reinterpret_cast<float4 *>(gc)[i] = v;
+        }
+    } else {
+        for (int64_t i = (int64_t)blockIdx.x * kSB + threadIdx.x; i < n; i += stride)
+            gc[i] = fix_add(gc[i], __ldg(ac + i), inv);
+    }
+}
+
+// The deterministic whole-volume gin: max |gout| per channel, the fixed-point
+// scatter (`launch` runs warp_bwd_k<..., FIX = true> with the FixAcc), the
+// conversion into gin.  Scratch: 8 bytes per gin element.
+static mdg_status fix_gin(const float *gout, int C, int64_t n, float *gin, cudaStream_t st,
+                          const std::function<void(const FixAcc &)> &launch) {
+    Scratch ws;
+    const size_t accb = (size_t)C * n * sizeof(long long);
+    MDG_CUDA_TRY(ws.alloc(accb + C * sizeof(unsigned), st));
+    long long *acc = ws.as<long long>();
+    unsigned *mx = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(acc) + accb);
+    MDG_CUDA_TRY(cudaMemsetAsync(ws.p, 0, accb + C * sizeof(unsigned), st));
+    const unsigned gx = (unsigned)std::min<int64_t>((n / 4 + kSB - 1) / kSB + 1, 148 * 8);
+    fix_maxabs_k<<<dim3(gx, C), kSB, 0, st>>>(gout, n, mx);
+    MDG_LAUNCHED();
+    launch(FixAcc{acc, mx});
+    MDG_LAUNCHED();
+    fix_convert_k<<<dim3(gx, C), kSB, 0, st>>>(acc, n, mx, gin);
+    MDG_LAUNCHED();
+    return MDG_OK;
+}
+
 // voxel-range launchers (the host-call pipeline computes z-chunks of a volume
 // whose inputs are fully resident)
 mdg_status warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *field, float *out,
@@ -656,8 +836,10 @@ mdg_status warp_fwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
 
 // gin by the float-atomic scatter (fast; the summation order at a shared
 // corner varies from run to run) unless deterministic mode is on
-// (mdg_set_deterministic / MDG_DETERMINISTIC=1): then by the per-target
-// gather of warp_gather.cu, bit-identical from run to run, ~3x the cost
+// (mdg_set_deterministic / MDG_DETERMINISTIC=1): then, for the whole volume,
+// by the 64-bit fixed-point scatter (fix_gin; ~1.5x the cost), and for a voxel
+// range by the per-target gather of warp_gather.cu (~3x: a range's targets
+// are not bounded, the gather's are); both bit-identical from run to run
 static bool warp_atomic_mode() { return !deterministic_mode(); }
 
 mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *field,
@@ -665,6 +847,13 @@ mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
                           cudaStream_t st) {
     if (pe <= pb) return MDG_OK;
     const int CD = d.h >= 2 ? C : 0;
+    if (gin && !warp_atomic_mode() && pb == 0 && pe == nvox(d))
+        return fix_gin(gout, C, nvox(d), gin, st, [&](const FixAcc &fx) {
+            MDG_WARP_DISPATCH_T(warp_bwd_k, (false, false, true), CD,
+                                (grid1d(pe - pb, kSB), kSB, 0, st),
+                                (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe,
+                                 whole_win(nvox(d), d.l), nullptr, false, fx));
+        });
     // (the gather indexes with 32-bit offsets: up to 16 channel planes)
     if (!gin || warp_atomic_mode() || 16 * nvox(d) >= (int64_t(1) << 32) || d.l >= 4096) {
         MDG_WARP_DISPATCH(warp_bwd_k, CD, (grid1d(pe - pb, kSB), kSB, 0, st),
@@ -867,8 +1056,15 @@ mdg_status mdg_compose_bwd(const float *prev, const float *res, mdg_dims3 d,
     MDG_REQUIRE(!(gprev && gprev == gres), "compose: gprev and gres must not alias");
     if (d.h >= 2 && gres) {
         // the warp backward with C = 3 plus the add node: gres by the gather
-        // kernel, gprev (the scatter) by the deterministic gather
+        // kernel, gprev (the scatter) by the fp32 scatter, or in deterministic
+        // mode by the fixed-point scatter
         cudaStream_t st = S_(stream);
+        if (gprev && !warp_atomic_mode())
+            return fix_gin(gout, 3, n, gprev, st, [&](const FixAcc &fx) {
+                warp_bwd_k<3, true, false, true><<<grid1d(n, kSB), kSB, 0, st>>>(
+                    prev, 3, d.h, d.w, d.l, res, gout, gprev, gres, 0, n, whole_win(n, d.l),
+                    nullptr, false, fx);
+            });
         if (!gprev || warp_atomic_mode() || 16 * n >= (int64_t(1) << 32) || d.l >= 4096) {
             warp_bwd_k<3, true><<<grid1d(n, kSB), kSB, 0, st>>>(prev, 3, d.h, d.w, d.l, res, gout,
                                                                 gprev, gres, 0, n,

@@ -25,4 +25,9 @@ for K in modet_fwd_tiled_k modet_bwd_row_k modet_bwd_col_k warp_fwd_k warp_bwd_k
 done
 ncu --profile-from-start off --metrics $M --clock-control none --csv \
     --log-file $O/po_launches.csv python tools/po_iter_once.py > $O/po.log 2>&1
+# 5. --set full of one tcgen05 encoder convolution launch of the PO iteration
+#    (SASS: UTCHMMA/UTCBAR; tensor-pipe utilisation)
+ncu --profile-from-start off --set full --clock-control none --import-source on \
+    -k regex:"conv_k" -c 1 -o $O/full_tc_conv_k python tools/po_iter_once.py > $O/full_tc_conv_k.log 2>&1
+ncu -i $O/full_tc_conv_k.ncu-rep --page raw --csv > $O/full_tc_conv_k.raw.csv 2>/dev/null
 echo "ncu rc=$?"

@@ -28,9 +28,11 @@ BUDGETS = [
     (r"mdg::project_bwd_k<6, 8,", 192),
     (r"mdg::enc::conv3t_k<", 0),
     (r"mdg::enc::conv3w_k<", 0),
-    (r"mdg::warp_bwd_k<(1|2), false, false>", 0),
-    (r"mdg::warp_bwd_k<(3|4|8), (false|true), false>", 24),
-    (r"mdg::warp_bwd_k<16, false, false>", 16),
+    # (template: channels, compose, slab, fixed-point deterministic scatter)
+    (r"mdg::warp_bwd_k<(1|2), false, false, (false|true)>", 0),
+    (r"mdg::warp_bwd_k<(3|4|8), (false|true), false, (false|true)>", 24),
+    (r"mdg::warp_bwd_k<16, false, false, false>", 16),
+    (r"mdg::warp_bwd_k<16, false, false, true>", 24),
 ]
 
 

@@ -2,11 +2,11 @@
 
 Forward results and every gather-form gradient are BIT-IDENTICAL to the CPU
 reference (same fp32 evaluation order, no FMA contraction); the image-side
-scatter gradients (warp gin, compose gprev) are gathered per target
-(warp_gather.cu): every term is the reference's, the sum order is fixed but
-cell-major instead of the reference's source-major, so they are checked to
-|d| <= 1e-5 + 1e-4|ref| and bit-identical from run to run (and bit-identical
-to the reference on the exact path crowded cells take).  The integer corner logic (resolve_axis) is checked
+scatter gradients (warp gin, compose gprev) are fp32 atomic scatters by
+default, checked to |d| <= 1e-5 + 1e-4|ref|; in deterministic mode they are a
+64-bit fixed-point scatter (whole volume) or gathered per target
+(warp_gather.cu, voxel ranges), bit-identical from run to run (the gather
+also bit-identical to the reference on the exact path crowded cells take).  The integer corner logic (resolve_axis) is checked
 bit-for-bit on the device.
 """
 import numpy as np
@@ -269,6 +269,65 @@ def test_warp_gin_gather_deterministic_and_correct(cuda, oracle, ref, determinis
     assert rel_close(a, want), np.abs(a - want).max()
     if kind != "far":
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("C", [1, 3, 5, 8, 16])
+@pytest.mark.parametrize("kind", ["smooth", "far"])
+def test_warp_gin_fixed_point_whole_volume(cuda, oracle, deterministic, C, kind):
+    """Deterministic mode, whole volume: gin by the 64-bit fixed-point scatter
+    (integer REDs, order independent): within tolerance of the reference and
+    bit-identical from run to run, also for a field beyond the range
+    gather's reach (|phi| = 9) and for channel counts without an unrolled
+    kernel (5: the runtime loop)."""
+    dims = (37, 21, 19)
+    h, w, l = dims
+    vol = random_feature_map(C, dims, 15)
+    if kind == "smooth":
+        fld = random_field(dims, 16, 1.5)
+    else:
+        fld = f32(np.full((3, l, w, h), 9.0))
+        fld[1] *= -1.0
+    gout = random_feature_map(C, dims, 17)
+    want, want_gf = oracle.warp_bwd(vol, fld, gout)
+    a, b = _gin_twice(dev(vol), dev(fld), dev(gout))
+    assert rel_close(a, want), np.abs(a - want).max()
+    assert np.array_equal(a, b)
+    _, gf = ops.warp_bwd(dev(vol), dev(fld), dev(gout))
+    assert np.array_equal(host(gf), want_gf)  # gfield stays bit-exact
+
+
+def test_warp_gin_fixed_point_nonfinite_channel(cuda, oracle, deterministic):
+    """A channel whose upstream gradient holds NaN / Inf has no fixed-point
+    scale: it is scattered in fp32 (NaN and Inf land where the reference puts
+    them), the finite channels stay fixed point and repeatable."""
+    dims = (24, 10, 9)
+    vol = random_feature_map(3, dims, 18)
+    fld = random_field(dims, 19, 1.2)
+    gout = random_feature_map(3, dims, 20)
+    gout[1, 4, 5, 6] = np.nan
+    gout[2, 2, 3, 4] = np.inf
+    want, _ = oracle.warp_bwd(vol, fld, gout)
+    a, b = _gin_twice(dev(vol), dev(fld), dev(gout))
+    assert np.array_equal(np.isnan(a), np.isnan(want))
+    assert np.array_equal(np.isinf(a), np.isinf(want))
+    fin = np.isfinite(want)
+    assert rel_close(a[fin], want[fin])
+    assert np.array_equal(a[0], b[0])
+
+
+def test_compose_gprev_fixed_point_repeatable(cuda, oracle, deterministic):
+    """Compose backward in deterministic mode: gprev (the scatter) by the
+    fixed-point path, repeatable and within tolerance; gres bit-exact."""
+    dims = (29, 17, 13)
+    prev = random_field(dims, 21, 1.5)
+    res = random_field(dims, 22, 2.5)
+    gout = random_field(dims, 23, 1.0)
+    wp, wr = oracle.compose_bwd(prev, res, gout)
+    gp1, gr1 = ops.compose_bwd(dev(prev), dev(res), dev(gout))
+    gp2, _ = ops.compose_bwd(dev(prev), dev(res), dev(gout))
+    assert rel_close(host(gp1), wp)
+    assert np.array_equal(host(gp1), host(gp2))
+    assert np.array_equal(host(gr1), wr)
 
 
 def test_warp_gin_gather_range_matches_whole(cuda, oracle, deterministic):
