@@ -8,9 +8,9 @@ levels split without remainder).  The model's ops decompose as follows
 (reference files cited per op):
 
 * conv3 (encoder conv blocks, encoder.hpp:87-91; RegHead, reghead.hpp:42-47):
-  a 1-plane halo of the input, libmdg's conv over the extended slab, interior
-  planes kept.  Its adjoint returns the halo planes' input gradient to their
-  owners (the halo exchange's backward).
+  libmdg's conv over the slab, plus the neighbours' face planes' taps added
+  to the two boundary output planes; the adjoint returns the face planes'
+  input gradient to their owners.
 * instance norm (ops.hpp:162-221): per-channel sums all-reduced (mean, then
   the centred second moment), so every rank normalises with the global
   statistics; the backward's sums are all-reduced by the same function.
@@ -244,36 +244,100 @@ def _dims_of(x):  # {C, l, w, h} -> (h, w, l)
     return (x.shape[3], x.shape[2], x.shape[1])
 
 
-class _Conv3(torch.autograd.Function):
-    """libmdg's 3x3x3 conv (mdg_encoder_conv3_fwd/bwd) on {ic, l, w, h}"""
+def _conv3(x, w, b, out):
+    """libmdg's 3x3x3 conv (mdg_encoder_conv3_fwd) of {ic, D, w, h}, zero
+    padded at its own faces; b nullable"""
+    ic, D, W, H = x.shape
+    ops._check(ops._capi.lib().mdg_encoder_conv3_fwd(ops._ptr(x), ic, ops.dims3((H, W, D)),
+                                                     ops._ptr(w), ops._ptr(b), w.shape[0],
+                                                     ops._ptr(out), ops._stream()))
+    return out
+
+
+def _conv3_bwd(x, w, g, gin, gw, gb):
+    """mdg_encoder_conv3_bwd: accumulates gin, gw, gb (each nullable)"""
+    ic, D, W, H = x.shape
+    ops._check(ops._capi.lib().mdg_encoder_conv3_bwd(ops._ptr(x), ic, ops.dims3((H, W, D)),
+                                                     ops._ptr(w), w.shape[0], ops._ptr(g),
+                                                     ops._ptr(gin), ops._ptr(gw), ops._ptr(gb),
+                                                     ops._stream()))
+
+
+class _Conv3Slab(torch.autograd.Function):
+    """conv3 of a slab {ic, D, w, h}, zero padded at the global z faces.
+    libmdg's conv runs over the slab itself (zero padded at the slab's own
+    faces, output contiguous: no extended copy, no interior slice); the
+    neighbours' face planes then add their dz = -1 / +1 taps to the two
+    boundary output planes (a conv over the 2-plane volume [face, 0] or
+    [0, face], no bias).  Backward: the slab's conv backward, plus each face
+    plane's share of the kernel gradient and its input gradient, which goes
+    back to the owner.  One rank: libmdg's conv alone."""
 
     @staticmethod
-    def forward(ctx, x, w, b):
+    def forward(ctx, x, w, b, comm):
         x = x.contiguous()
-        ic, oc = x.shape[0], w.shape[0]
-        out = x.new_empty(oc, *x.shape[1:])
-        L, P = ops._capi.lib(), ops._ptr
-        ops._check(L.mdg_encoder_conv3_fwd(P(x), ic, ops.dims3(_dims_of(x)), P(w), P(b), oc,
-                                           P(out), ops._stream()))
-        ctx.save_for_backward(x, w)
+        ic, D, W, H = x.shape
+        oc = w.shape[0]
+        out = _conv3(x, w, b, x.new_empty(oc, D, W, H))
+        r, n = comm.rank, comm.world
+        lo = hi = None
+        if n > 1:
+            sends, recvs = [], []
+            if r > 0:  # [rank r-1's last plane, 0]
+                lo = x.new_zeros(ic, 2, W, H)
+                sends.append((x[:, :1], r - 1))
+                recvs.append((lo[:, :1], r - 1))
+            if r < n - 1:  # [0, rank r+1's first plane]
+                hi = x.new_zeros(ic, 2, W, H)
+                sends.append((x[:, D - 1:], r + 1))
+                recvs.append((hi[:, 1:], r + 1))
+            comm.exchange(sends, recvs)
+            if lo is not None:
+                out[:, 0] += _conv3(lo, w, None, x.new_empty(oc, 2, W, H))[:, 1]
+            if hi is not None:
+                out[:, D - 1] += _conv3(hi, w, None, x.new_empty(oc, 2, W, H))[:, 0]
+        ctx.save_for_backward(x, w, lo, hi)
+        ctx.comm = comm
         return out
 
     @staticmethod
     def backward(ctx, g):
-        x, w = ctx.saved_tensors
+        x, w, lo, hi = ctx.saved_tensors
+        comm = ctx.comm
+        r = comm.rank
         g = g.contiguous()
-        gin, gw = torch.zeros_like(x), torch.zeros_like(w)
-        gb = w.new_zeros(w.shape[0])
-        L, P = ops._capi.lib(), ops._ptr
-        ops._check(L.mdg_encoder_conv3_bwd(P(x), x.shape[0], ops.dims3(_dims_of(x)), P(w),
-                                           w.shape[0], P(g), P(gin), P(gw), P(gb),
-                                           ops._stream()))
-        return gin, gw, gb
+        ic, D, W, H = x.shape
+        oc = w.shape[0]
+        gin, gw, gb = torch.zeros_like(x), torch.zeros_like(w), w.new_zeros(oc)
+        _conv3_bwd(x, w, g, gin, gw, gb)
+        sends, recvs, got = [], [], []
+        if lo is not None:
+            gm = g.new_zeros(oc, 2, W, H)
+            gm[:, 1] = g[:, 0]
+            gl = torch.zeros_like(lo)
+            _conv3_bwd(lo, w, gm, gl, gw, None)
+            sends.append((gl[:, :1], r - 1))
+            t = x.new_empty(ic, 1, W, H)
+            recvs.append((t, r - 1))
+            got.append((t, 0))
+        if hi is not None:
+            gm = g.new_zeros(oc, 2, W, H)
+            gm[:, 0] = g[:, D - 1]
+            gh = torch.zeros_like(hi)
+            _conv3_bwd(hi, w, gm, gh, gw, None)
+            sends.append((gh[:, 1:], r + 1))
+            t = x.new_empty(ic, 1, W, H)
+            recvs.append((t, r + 1))
+            got.append((t, D - 1))
+        comm.exchange(sends, recvs)
+        for t, z in got:
+            gin[:, z:z + 1] += t
+        return gin, gw, gb, None
 
 
 def conv3_slab(x, w, b, comm):
-    """zero-padded conv3 of a slab: 1-plane halo, interior planes kept"""
-    return _Conv3.apply(halo(x, 1, comm), w, b)[:, 1:-1]
+    """zero-padded conv3 of a slab (encoder.hpp:87-91, reghead.hpp:42-47)"""
+    return _Conv3Slab.apply(x, w, b, comm)
 
 
 class _Project(torch.autograd.Function):
@@ -352,8 +416,11 @@ class _Upsample(torch.autograd.Function):
 def upsample_slab(phi_c, comm, hw):
     """coarse slab {3, Dc, wc, hc} -> fine slab {3, 2Dc, 2wc, 2hc}: fine plane
     z samples coarse z/2, so the coarse slab needs its next plane (edge-
-    replicated at the global end, where the reference clamps)"""
+    replicated at the global end, where the reference clamps).  One rank:
+    the whole volume, upsampled directly."""
     Dc = phi_c.shape[1]
+    if comm.world == 1:
+        return _Upsample.apply(phi_c, hw)
     return _Upsample.apply(halo(phi_c, 1, comm, edge=True), hw)[:, 2:2 + 2 * Dc]
 
 
@@ -675,9 +742,13 @@ class SlabModel:
             S = self.heads[k]
             Q, K = _Project.apply(f, m_in, W, b, g, beta)
             shp = (S * self.hd, *f.shape[1:])
-            Qx, Kx = halo(Q.view(shp), 1, comm), halo(K.view(shp), 1, comm)
             _, z0, _, _ = geom.level(e)
-            SF = _ModeT.apply(Qx, Kx, B, S, self.hd, z0 - 1, geom.defer_checks)[:, 1:-1]
+            if comm.world == 1:  # the whole volume: no halo planes
+                SF = _ModeT.apply(Q.view(shp), K.view(shp), B, S, self.hd, z0,
+                                  geom.defer_checks)
+            else:
+                Qx, Kx = halo(Q.view(shp), 1, comm), halo(K.view(shp), 1, comm)
+                SF = _ModeT.apply(Qx, Kx, B, S, self.hd, z0 - 1, geom.defer_checks)[:, 1:-1]
             res = conv3_slab(SF, rw, rb, comm)
             if self.diffeomorphic:
                 # op_scaling_squaring (reghead.hpp:52-57): v / 2^T, then T
