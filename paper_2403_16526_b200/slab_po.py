@@ -448,8 +448,11 @@ class _Warp(torch.autograd.Function):
         lo, hi = need[comm.rank]
         vol = vol.contiguous()
         C = vol.shape[0]
-        win = vol.new_empty(C, hi - lo, w, h)
-        win[:, z0 - lo:z1 - lo] = vol
+        if (lo, hi) == (z0, z1):  # the window is the slab itself (one rank)
+            win = vol
+        else:
+            win = vol.new_empty(C, hi - lo, w, h)
+            win[:, z0 - lo:z1 - lo] = vol
         sends, recvs = [], []
         for q, (a, b) in enumerate(ranges):
             if q == comm.rank:
@@ -510,6 +513,8 @@ class _Warp(torch.autograd.Function):
                 recvs.append((t, q))
                 got[q] = (t, r0)
         comm.exchange(sends, recvs)
+        if (lo, hi) == (z0, z1) and not got:  # nothing to or from other ranks
+            return gin_w, gfield, None, None
         gin = win.new_zeros(C, z1 - z0, w, h)
         for q in range(comm.world):
             if q == comm.rank:
@@ -655,12 +660,16 @@ def grad_reg_slab(phi, geom):
     comm = geom.comm
     (h, w, l), _, _, _ = geom.level(0)
     n = h * w * l
-    ext = halo(phi, 1, comm)
     D = phi.shape[1]
-    u = ext[:, 1:1 + D]
-    dz = ext[:, 2:2 + D] - u
-    if comm.rank == comm.world - 1:
-        dz = dz[:, :D - 1]  # the last plane has no forward difference
+    if comm.world == 1:
+        u = phi
+        dz = phi[:, 1:] - phi[:, :-1]
+    else:
+        ext = halo(phi, 1, comm)
+        u = ext[:, 1:1 + D]
+        dz = ext[:, 2:2 + D] - u
+        if comm.rank == comm.world - 1:
+            dz = dz[:, :D - 1]  # the last plane has no forward difference
     reg = 0.0
     for diff, dim in ((u[..., 1:] - u[..., :-1], h), (u[:, :, 1:] - u[:, :, :-1], w), (dz, l)):
         reg = reg + (diff * diff).sum() / float(n - n // dim)
