@@ -68,49 +68,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned phase) {
     } while (!done);
 }
 
-// B = the weights as {N, Kp} (k = tap * ic + c, zero padded to Kp), split into
-// tf32 hi / lo.  flip: the input-gradient kernel w'[c][o][26 - t] of w {oc, ic, 27}
-__global__ void prep_b_k(const float *__restrict__ w, int oc, int ic, int flip, int N, int Kin,
-                         int Kp, float *__restrict__ bhi, float *__restrict__ blo) {
+// B = the weights as {nout, Kp} (k = tap * ic + c, zero padded to Kp), split
+// into tf32 hi / lo and stored as the shared-memory image of each (N-slice z,
+// chunk j): tile ((z * nchunk + j) * 2 + {0: hi, 1: lo}) of N x 32 floats in
+// the 128-byte-swizzled order, so one bulk copy stages a chunk's B.
+// flip: the input-gradient kernel w'[c][o][26 - t] of w {oc, ic, 27}
+__global__ void prep_b_k(const float *__restrict__ w, int oc, int ic, int flip, int nout, int N,
+                         int Kin, int Kp, float *__restrict__ bsw) {
     const int i = blockIdx.x * 256 + threadIdx.x;
-    if (i >= N * Kp) return;
+    if (i >= nout * Kp) return;
     const int o = i / Kp, k = i % Kp;
     float v = 0.0f;
     if (k < 27 * Kin) {
         const int tap = k / Kin, c = k % Kin;
         v = flip ? w[((int64_t)c * ic + o) * 27 + (26 - tap)] : w[((int64_t)o * ic + c) * 27 + tap];
     }
+    const int nchunk = Kp / 32, z = o / N, r = o % N, j = k / 32, kk = k % 32;
+    float *tile = bsw + (int64_t)((z * nchunk + j) * 2) * (N * 32);
     const float h = tf32r(v);
-    bhi[i] = h;
-    blo[i] = tf32r(v - h);
+    tile[swz(r, kk)] = h;
+    tile[N * 32 + swz(r, kk)] = tf32r(v - h);
 }
 
-template <int N>
 struct ChunkRegs {
-    static constexpr int BPT = (N * 32 + 255) / 256;  // B values per thread
-    float a[16], bh[BPT], bl[BPT];
+    float a[16];
 };
 
-// this thread's share of K chunk j: 16 channels of one tap of its voxel, and
-// its B values (Kin % 16 == 0, so a half chunk never straddles taps)
-template <int N>
-__device__ __forceinline__ void load_chunk(ChunkRegs<N> &R, int j, int half, int tid, bool live,
-                                           int x, int y, int z, int h, int w, int l, int64_t n,
-                                           int Kin, int Kp, const float *__restrict__ in,
-                                           const float *__restrict__ bhi,
-                                           const float *__restrict__ blo) {
-#pragma unroll
-    for (int u = 0; u < ChunkRegs<N>::BPT; ++u) {
-        const int e = tid + 256 * u;
-        if (e < N * 32) {
-            const int r = e >> 5, kk = e & 31;
-            R.bh[u] = __ldg(bhi + (int64_t)r * Kp + 32 * j + kk);
-            R.bl[u] = __ldg(blo + (int64_t)r * Kp + 32 * j + kk);
-        }
-    }
-    const int k = 32 * j + 16 * half;
-    const int tap = k < 27 * Kin ? k / Kin : 27;
-    const int c0 = k - tap * Kin;
+// this thread's share of the next K chunk: 16 channels (c0 ..) of one tap of
+// its voxel (Kin % 16 == 0, so a half chunk never straddles taps); tap / c0
+// advance by 32 values per chunk
+__device__ __forceinline__ void load_chunk(ChunkRegs &R, int &tap, int &c0, bool live, int x, int y,
+                                           int z, int h, int w, int l, int64_t n, int Kin,
+                                           const float *__restrict__ in) {
     bool ok = false;
     int64_t off = 0;
     if (tap < 27 && live) {
@@ -118,8 +107,26 @@ __device__ __forceinline__ void load_chunk(ChunkRegs<N> &R, int j, int half, int
         ok = xx >= 0 && xx < h && yy >= 0 && yy < w && zz >= 0 && zz < l;
         off = (int64_t)c0 * n + ((int64_t)zz * w + yy) * h + xx;
     }
+    const float *src = in + off;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) R.a[q] = ok ? __ldg(in + off + (int64_t)q * n) : 0.0f;
+    for (int q = 0; q < 16; ++q) R.a[q] = ok ? __ldg(src + (int64_t)q * n) : 0.0f;
+    c0 += 32;
+    while (c0 >= Kin) {
+        c0 -= Kin;
+        ++tap;
+    }
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(su32(bar))
+        : "memory");
 }
 
 // blockIdx.x: 128-voxel tile; blockIdx.y: K split (chunks [y*jsplit, ..));
@@ -128,8 +135,8 @@ __device__ __forceinline__ void load_chunk(ChunkRegs<N> &R, int j, int half, int
 // adds them in split order); otherwise out (=, or += with acc_out) + bias.
 template <int N>
 __global__ void __launch_bounds__(256)
-conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *__restrict__ bhi,
-       const float *__restrict__ blo, int Kp, int jsplit, int nout,
+conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *__restrict__ bsw,
+       int Kp, int jsplit, int nout,
        const float *__restrict__ bias, int acc_out, float *__restrict__ out,
        float *__restrict__ part) {
     extern __shared__ __align__(1024) float sm_raw[];
@@ -137,7 +144,7 @@ conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *
     float *sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u) / 4;
     constexpr int STAGE = 2 * 128 * 32 + 2 * N * 32;  // floats per stage
     constexpr int NH = N / 2;
-    __shared__ uint64_t bar[2];
+    __shared__ uint64_t bar[2], bbar[2];  // MMA commits; B bulk copies
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5;
     const int row = tid & 127, half = tid >> 7;  // voxel row; K half / column half
@@ -160,14 +167,17 @@ conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[1])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bbar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bbar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;");
     }
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base, id = idesc_tf32(N);
     const int jb = blockIdx.y * jsplit, je = min(jb + jsplit, Kp / 32), nl = je - jb;
     const int cz = blockIdx.z * N;  // first output channel of this CTA
-    bhi += (int64_t)cz * Kp;
-    blo += (int64_t)cz * Kp;
+    const int nchunk = Kp / 32;
+    const float *btile = bsw + (int64_t)blockIdx.z * nchunk * 2 * (N * 32);
     float acc[NH];
 #pragma unroll
     for (int q = 0; q < NH; ++q) acc[q] = 0.0f;
@@ -175,20 +185,27 @@ conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *
     // TMEM lanes 32 (w % 4) .. +31, column halves [0, N/2) and [N/2, N)
     auto drain = [&](int tc) {  // local chunk index: accumulator tc & 1
         const uint32_t col = (uint32_t)((tc & 1) * N + half * NH);
+        uint32_t v[NH];
 #pragma unroll
-        for (int c = 0; c < NH; c += 8) {
-            uint32_t v[8];
+        for (int c = 0; c < NH; c += 8) {  // all loads in flight, one wait
             const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + col + (uint32_t)c;
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]),
-                           "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc[c + q] += __uint_as_float(v[q]);
+                         : "=r"(v[c]), "=r"(v[c + 1]), "=r"(v[c + 2]), "=r"(v[c + 3]),
+                           "=r"(v[c + 4]), "=r"(v[c + 5]), "=r"(v[c + 6]), "=r"(v[c + 7])
+                         : "r"(taddr));
         }
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int q = 0; q < NH; ++q) acc[q] += __uint_as_float(v[q]);
     };
-    ChunkRegs<N> R;
-    load_chunk<N>(R, jb, half, tid, live, x, y, z, h, w, l, n, Kin, Kp, in, bhi, blo);
+    ChunkRegs R;
+    int tap, c0;
+    {
+        const int k0 = 32 * jb + 16 * half;
+        tap = k0 < 27 * Kin ? k0 / Kin : 27;
+        c0 = k0 - tap * Kin;
+    }
+    load_chunk(R, tap, c0, live, x, y, z, h, w, l, n, Kin, in);
     for (int t = 0; t < nl; ++t) {  // local chunk t = global chunk jb + t
         const int j = jb + t, sidx = t & 1;
         float *aH = sm + sidx * STAGE, *aL = aH + 128 * 32, *bH = aL + 128 * 32, *bL = bH + N * 32;
@@ -197,6 +214,8 @@ conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *
             asm volatile("tcgen05.fence::after_thread_sync;");
             drain(t - 2);
         }
+        if (tid == 0)  // this chunk's B (hi and lo tiles, contiguous) by one bulk copy
+            bulk_g2s(su32(bH), btile + (int64_t)j * 2 * (N * 32), 2 * N * 32 * 4, &bbar[sidx]);
         const int i0 = 16 * half;
 #pragma unroll
         for (int q = 0; q < 16; q += 4) {
@@ -207,21 +226,13 @@ conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *
             *reinterpret_cast<float4 *>(aH + swz(row, i0 + q)) = h4;
             *reinterpret_cast<float4 *>(aL + swz(row, i0 + q)) = l4;
         }
-#pragma unroll
-        for (int u = 0; u < ChunkRegs<N>::BPT; ++u) {
-            const int e = tid + 256 * u;
-            if (e < N * 32) {
-                const int r = e >> 5, kk = e & 31;
-                bH[swz(r, kk)] = R.bh[u];
-                bL[swz(r, kk)] = R.bl[u];
-            }
-        }
         if (t + 1 < nl)  // the next chunk's loads fly during the handoff below
-            load_chunk<N>(R, j + 1, half, tid, live, x, y, z, h, w, l, n, Kin, Kp, in, bhi, blo);
+            load_chunk(R, tap, c0, live, x, y, z, h, w, l, n, Kin, in);
         asm volatile("fence.proxy.async.shared::cta;");
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncthreads();
         if (tid == 0) {
+            mbar_wait(&bbar[sidx], (t >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t tacc = tmem + (uint32_t)(sidx * N);
 #pragma unroll
@@ -318,12 +329,12 @@ mdg_status enc_tc_conv(const float *in, int kin, mdg_dims3 d, const float *w, in
     Scratch sb;
     MDG_CUDA_TRY(sb.alloc(((size_t)2 * nout * Kp + (S > 1 ? (size_t)S * nout * n : 0)) *
                               sizeof(float), st));
-    float *bhi = sb.as<float>(), *blo = bhi + (size_t)nout * Kp;
-    float *part = S > 1 ? blo + (size_t)nout * Kp : nullptr;
+    float *bsw = sb.as<float>();
+    float *part = S > 1 ? bsw + (size_t)2 * nout * Kp : nullptr;
     // w's ic (the forward's input channels): kin forward, nout for the flip
     const int wic = flip ? nout : kin, woc = flip ? kin : nout;
-    tc::prep_b_k<<<(nout * Kp + 255) / 256, 256, 0, st>>>(w, woc, wic, flip, nout, kin, Kp, bhi,
-                                                          blo);
+    tc::prep_b_k<<<(nout * Kp + 255) / 256, 256, 0, st>>>(w, woc, wic, flip, nout, N, kin, Kp,
+                                                          bsw);
     MDG_LAUNCHED();
     const dim3 g((unsigned)tiles, (unsigned)S, (unsigned)nz);
     const int accf = acc ? 1 : 0;
@@ -331,14 +342,14 @@ mdg_status enc_tc_conv(const float *in, int kin, mdg_dims3 d, const float *w, in
         constexpr size_t sm = tc::smem_bytes<32>();
         MDG_CUDA_TRY(cudaFuncSetAttribute(tc::conv_k<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)sm));
-        tc::conv_k<32><<<g, 256, sm, st>>>(in, kin, d.h, d.w, d.l, bhi, blo, Kp, jsplit, nout,
-                                           bias, accf, out, part);
+        tc::conv_k<32><<<g, 256, sm, st>>>(in, kin, d.h, d.w, d.l, bsw, Kp, jsplit, nout, bias,
+                                           accf, out, part);
     } else {
         constexpr size_t sm = tc::smem_bytes<64>();
         MDG_CUDA_TRY(cudaFuncSetAttribute(tc::conv_k<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)sm));
-        tc::conv_k<64><<<g, 256, sm, st>>>(in, kin, d.h, d.w, d.l, bhi, blo, Kp, jsplit, nout,
-                                           bias, accf, out, part);
+        tc::conv_k<64><<<g, 256, sm, st>>>(in, kin, d.h, d.w, d.l, bsw, Kp, jsplit, nout, bias,
+                                           accf, out, part);
     }
     MDG_LAUNCHED();
     if (S > 1) {
