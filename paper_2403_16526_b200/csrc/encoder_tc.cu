@@ -1,12 +1,14 @@
 // encoder_tc.cu — the encoder's 3x3x3 convolution (ops.hpp:58-99, zero padded)
-// on the 5th-generation tensor cores, for the levels where that wins: 32 and
-// 64 output channels (L2, L3 of the small preset), forward and input gradient.
+// on the 5th-generation tensor cores, for the levels where that wins: 32, 64
+// and 128 output channels (L2-L4 of the small preset), forward and input
+// gradient.
 //
 // Implicit GEMM D[voxel][o] = sum_k A[voxel][k] B[o][k], k = tap * ic + c:
 //   * one CTA = 128 consecutive output voxels (the MMA's M) and 256 threads:
 //     thread pairs gather their voxel's 32-value K chunk (im2col on the fly,
 //     one tap x 16 channels each), with the NEXT chunk's global loads in
-//     flight while this one is split and stored;
+//     flight while this one is split and stored; the chunk's weight tiles
+//     (pre-split, pre-swizzled) arrive by one bulk copy;
 //   * fp32 accuracy from 3xTF32: every operand is split into tf32 hi + lo,
 //     stored 128-byte swizzled K-major in shared memory; one thread issues
 //     4 K-steps x (hi*hi + hi*lo + lo*hi) = 12 tcgen05.mma per chunk;
@@ -19,9 +21,9 @@
 //     of chunk j-2 has arrived on its mbarrier.
 // The input gradient is the same convolution of gout with the flipped,
 // transposed kernel (w'[c][o][26 - t] = w[o][c][t]).  Measured against the
-// FFMA2 / implicit-GEMM kernels it replaces: 1.2-1.4x faster
-// at these shapes and about 3x more accurate; slower for N <= 16 or on grids
-// of fewer than ~4k voxels, which keep the old kernels.
+// FFMA2 / implicit-GEMM kernels it replaces: 1.2-1.8x faster
+// at these shapes and about 3x more accurate; slower for N <= 16, which keeps
+// the old kernels.  Grids too small to fill the GPU split K across CTAs.
 #include <algorithm>
 #include <cstdlib>
 

@@ -301,14 +301,15 @@ def _conv_ref64(x, w, b, dims):
     (32, 64, (10, 12, 14)), (64, 64, (10, 12, 14)), (64, 128, (5, 6, 7)), (128, 128, (10, 12, 14)),
     (48, 40, (9, 7, 5)), (1, 8, (40, 17, 9)), (8, 8, (64, 20, 10)), (8, 16, (36, 9, 13)),
     (16, 16, (44, 16, 8)), (5, 8, (12, 9, 6)),
-    # the tcgen05 path (32 / 64 outputs, >= 4096 voxels; encoder_tc.cu), odd extents
+    # the tcgen05 path (32 / 64 / 128 outputs, >= 128 voxels; encoder_tc.cu), odd extents
     (16, 32, (40, 48, 20)), (32, 64, (20, 24, 28)), (64, 64, (20, 24, 28)),
     (64, 32, (17, 19, 23)), (128, 64, (21, 17, 13)),
 ])
 def test_encoder_conv3_fwd_bwd(cuda, ic, oc, dims):
     """mdg_encoder_conv3_fwd/bwd (tiled slab kernel for narrow outputs, tcgen05
-    3xTF32 implicit GEMM for 32 / 64 outputs on >= 4096 voxels, FFMA implicit
-    GEMM otherwise, split-K on small grids) against float64 conv3d: output,
+    3xTF32 implicit GEMM for 32 / 64 / 128 outputs on >= 128 voxels (split-K
+    and 64-output slices on small grids), FFMA implicit GEMM otherwise)
+    against float64 conv3d: output,
     input gradient (accumulated), kernel and bias gradients."""
     from paper_2403_16526_b200 import _capi
 
