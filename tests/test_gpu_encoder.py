@@ -304,6 +304,8 @@ def _conv_ref64(x, w, b, dims):
     # the tcgen05 path (32 / 64 / 128 outputs, >= 128 voxels; encoder_tc.cu), odd extents
     (16, 32, (40, 48, 20)), (32, 64, (20, 24, 28)), (64, 64, (20, 24, 28)),
     (64, 32, (17, 19, 23)), (128, 64, (21, 17, 13)),
+    # the halo-tile form (32 outputs, h % 4 == 0): partial 8x4x4 tiles, split groups
+    (16, 32, (12, 8, 4)), (64, 32, (8, 6, 5)), (32, 32, (4, 9, 7)),
 ])
 def test_encoder_conv3_fwd_bwd(cuda, ic, oc, dims):
     """mdg_encoder_conv3_fwd/bwd (tiled slab kernel for narrow outputs, tcgen05
