@@ -296,6 +296,23 @@ def test_warp_gin_fixed_point_whole_volume(cuda, oracle, deterministic, C, kind)
     assert np.array_equal(host(gf), want_gf)  # gfield stays bit-exact
 
 
+@pytest.mark.parametrize("scale", [1e30, 1e-30, 1e-41])
+def test_warp_gin_fixed_point_extreme_magnitudes(cuda, oracle, deterministic, scale):
+    """The fixed-point scale follows each channel's max |gout| over any float
+    exponent (huge, tiny, subnormal gradients): relative parity with the
+    reference scatter and run-to-run identity."""
+    dims = (20, 12, 10)
+    vol = random_feature_map(3, dims, 24)
+    fld = random_field(dims, 25, 1.5)
+    gout = f32(random_feature_map(3, dims, 26) * np.float32(scale))
+    gout[1] *= np.float32(1e-3)  # channels of different magnitude
+    want, _ = oracle.warp_bwd(vol, fld, gout)
+    a, b = _gin_twice(dev(vol), dev(fld), dev(gout))
+    assert np.array_equal(a, b)
+    m = np.abs(want).max()
+    assert rel_close(a / m, want / m, atol=1e-6), np.abs(a - want).max() / m
+
+
 def test_warp_gin_fixed_point_nonfinite_channel(cuda, oracle, deterministic):
     """A channel whose upstream gradient holds NaN / Inf has no fixed-point
     scale: it is scattered in fp32 (NaN and Inf land where the reference puts
