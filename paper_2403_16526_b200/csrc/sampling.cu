@@ -804,15 +804,12 @@ fix_convert_k(const long long *__restrict__ acc, int64_t n, const unsigned *__re
 
 // The deterministic whole-volume gin: max |gout| per channel, the fixed-point
 // scatter (`launch` runs warp_bwd_k<..., FIX = true> with the FixAcc), the
-// conversion into gin.  Scratch: 8 bytes per gin element.
-static mdg_status fix_gin(const float *gout, int C, int64_t n, float *gin, cudaStream_t st,
-                          const std::function<void(const FixAcc &)> &launch) {
-    Scratch ws;
-    const size_t accb = (size_t)C * n * sizeof(long long);
-    MDG_CUDA_TRY(ws.alloc(accb + C * sizeof(unsigned), st));
-    long long *acc = ws.as<long long>();
-    unsigned *mx = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(acc) + accb);
-    MDG_CUDA_TRY(cudaMemsetAsync(ws.p, 0, accb + C * sizeof(unsigned), st));
+// conversion into gin.  Scratch: 8 bytes per gin element; if the pool cannot
+// provide it the caller falls back to the per-target gather.
+static mdg_status fix_gin_run(long long *acc, unsigned *mx, size_t bytes, const float *gout, int C,
+                              int64_t n, float *gin, cudaStream_t st,
+                              const std::function<void(const FixAcc &)> &launch) {
+    MDG_CUDA_TRY(cudaMemsetAsync(acc, 0, bytes, st));
     const unsigned gx = (unsigned)std::min<int64_t>((n / 4 + kSB - 1) / kSB + 1, 148 * 8);
     fix_maxabs_k<<<dim3(gx, C), kSB, 0, st>>>(gout, n, mx);
     MDG_LAUNCHED();
@@ -821,6 +818,25 @@ static mdg_status fix_gin(const float *gout, int C, int64_t n, float *gin, cudaS
     fix_convert_k<<<dim3(gx, C), kSB, 0, st>>>(acc, n, mx, gin);
     MDG_LAUNCHED();
     return MDG_OK;
+}
+// false: no memory for the accumulator (the caller gathers per target instead)
+static bool fix_gin(const float *gout, int C, int64_t n, float *gin, cudaStream_t st,
+                    mdg_status *rc, const std::function<void(const FixAcc &)> &launch) {
+    Scratch ws;
+    const size_t accb = (size_t)C * n * sizeof(long long), bytes = accb + C * sizeof(unsigned);
+    const cudaError_t e = ws.alloc(bytes, st);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();  // clear it: the gather path needs no accumulator
+        return false;
+    }
+    if (e != cudaSuccess) {
+        *rc = status_from_cuda(e, "fix_gin");
+        return true;
+    }
+    long long *acc = ws.as<long long>();
+    unsigned *mx = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(acc) + accb);
+    *rc = fix_gin_run(acc, mx, bytes, gout, C, n, gin, st, launch);
+    return true;
 }
 
 // voxel-range launchers (the host-call pipeline computes z-chunks of a volume
@@ -847,13 +863,15 @@ mdg_status warp_bwd_range(const float *in, int C, mdg_dims3 d, const float *fiel
                           cudaStream_t st) {
     if (pe <= pb) return MDG_OK;
     const int CD = d.h >= 2 ? C : 0;
-    if (gin && !warp_atomic_mode() && pb == 0 && pe == nvox(d))
-        return fix_gin(gout, C, nvox(d), gin, st, [&](const FixAcc &fx) {
+    mdg_status frc = MDG_OK;
+    if (gin && !warp_atomic_mode() && pb == 0 && pe == nvox(d) &&
+        fix_gin(gout, C, nvox(d), gin, st, &frc, [&](const FixAcc &fx) {
             MDG_WARP_DISPATCH_T(warp_bwd_k, (false, false, true), CD,
                                 (grid1d(pe - pb, kSB), kSB, 0, st),
                                 (in, C, d.h, d.w, d.l, field, gout, gin, gfield, pb, pe,
                                  whole_win(nvox(d), d.l), nullptr, false, fx));
-        });
+        }))
+        return frc;
     // (the gather indexes with 32-bit offsets: up to 16 channel planes)
     if (!gin || warp_atomic_mode() || 16 * nvox(d) >= (int64_t(1) << 32) || d.l >= 4096) {
         MDG_WARP_DISPATCH(warp_bwd_k, CD, (grid1d(pe - pb, kSB), kSB, 0, st),
@@ -1059,12 +1077,14 @@ mdg_status mdg_compose_bwd(const float *prev, const float *res, mdg_dims3 d,
         // kernel, gprev (the scatter) by the fp32 scatter, or in deterministic
         // mode by the fixed-point scatter
         cudaStream_t st = S_(stream);
-        if (gprev && !warp_atomic_mode())
-            return fix_gin(gout, 3, n, gprev, st, [&](const FixAcc &fx) {
+        mdg_status frc = MDG_OK;
+        if (gprev && !warp_atomic_mode() &&
+            fix_gin(gout, 3, n, gprev, st, &frc, [&](const FixAcc &fx) {
                 warp_bwd_k<3, true, false, true><<<grid1d(n, kSB), kSB, 0, st>>>(
                     prev, 3, d.h, d.w, d.l, res, gout, gprev, gres, 0, n, whole_win(n, d.l),
                     nullptr, false, fx);
-            });
+            }))
+            return frc;
         if (!gprev || warp_atomic_mode() || 16 * n >= (int64_t(1) << 32) || d.l >= 4096) {
             warp_bwd_k<3, true><<<grid1d(n, kSB), kSB, 0, st>>>(prev, 3, d.h, d.w, d.l, res, gout,
                                                                 gprev, gres, 0, n,
