@@ -226,8 +226,10 @@ conv_k(const float *__restrict__ in, int Kin, int h, int w, int l, const float *
         for (int q = 0; q < 16; q += 4) {
             const float4 h4 = make_float4(tf32r(R.a[q]), tf32r(R.a[q + 1]), tf32r(R.a[q + 2]),
                                           tf32r(R.a[q + 3]));
-            const float4 l4 = make_float4(tf32r(R.a[q] - h4.x), tf32r(R.a[q + 1] - h4.y),
-                                          tf32r(R.a[q + 2] - h4.z), tf32r(R.a[q + 3] - h4.w));
+            // lo = x - hi is exact in fp32; the MMA reads its top 19 bits (no second
+            // rounding: the truncation error is 2^-21 |x|, far below the fp32 sums')
+            const float4 l4 = make_float4(R.a[q] - h4.x, R.a[q + 1] - h4.y, R.a[q + 2] - h4.z,
+                                          R.a[q + 3] - h4.w);
             *reinterpret_cast<float4 *>(aH + swz(row, i0 + q)) = h4;
             *reinterpret_cast<float4 *>(aL + swz(row, i0 + q)) = l4;
         }
@@ -448,8 +450,8 @@ conv_halo_k(const __grid_constant__ CUtensorMap map, int Kin, int h, int w, int 
             for (int q = 0; q < 16; q += 4) {
                 const float4 h4 = make_float4(tf32r(a[q]), tf32r(a[q + 1]), tf32r(a[q + 2]),
                                               tf32r(a[q + 3]));
-                const float4 l4 = make_float4(tf32r(a[q] - h4.x), tf32r(a[q + 1] - h4.y),
-                                              tf32r(a[q + 2] - h4.z), tf32r(a[q + 3] - h4.w));
+                const float4 l4 = make_float4(a[q] - h4.x, a[q + 1] - h4.y, a[q + 2] - h4.z,
+                                              a[q + 3] - h4.w);  // (as in conv_k)
                 *reinterpret_cast<float4 *>(aH + swz(row, i0 + q)) = h4;
                 *reinterpret_cast<float4 *>(aL + swz(row, i0 + q)) = l4;
             }

@@ -217,6 +217,14 @@ def test_halo_and_all_reduce_adjoints(tmp_path):
 
 # ----------------------------------------------------------------- GPU
 PRE_NORM_BIAS = {8 * k + i for k in range(5) for i in (1, 5)}  # b1, b2: zero through IN
+# the Q/K projection + layer-norm parameters of each pyramid level (W, b, gamma,
+# beta): sums over every voxel of the level with heavy cancellation, so two
+# fp32 evaluations that differ only in the convolutions' rounding (the slab's
+# face-plane corrections, a different conv kernel for a different slab shape)
+# move them by up to ~1e-4 relative with the tensor-core convolutions and
+# ~5e-4 with the FFMA ones (MDG_ENC_TC=0) — the 1e-3 bound the native model is
+# held to against the reference (test_gpu_encoder.py)
+PROJ_PARAMS = {40 + 7 * k + i for k in range(5) for i in range(4)}
 PO_ITERS = 4
 
 
@@ -264,7 +272,8 @@ def _model_worker(rank, world, port, dims, case, out_dir, reach=None):
 def test_slab_po_matches_single_volume(cuda, ref, tmp_path, world, dims, reach):
     """The loss step on `world` slabs against (1) the same step on one slab —
     the decomposition: halos, all-reduced statistics and partial sums,
-    gathered warp planes, returned scatters: all 75 gradients <= 1e-4;
+    gathered warp planes, returned scatters: the 75 gradients <= 1e-4 (the
+    projection / layer-norm parameters, sums with cancellation, <= 1e-3);
     (2) the single-volume native model (mdg_model_loss_step): loss and phi
     <= 1e-4, gradients <= 1e-3; (3) the reference's run_loss_step: loss and
     phi <= 1e-4, gradients as close as the native model's.  Then Adam steps
@@ -299,7 +308,7 @@ def test_slab_po_matches_single_volume(cuda, ref, tmp_path, world, dims, reach):
                                  for j in range(8 * (i // 8), 8 * (i // 8) + 8)))
             if np.abs(got[f"g{i}"] - one[f"g{i}"]).max() > 1e-4 * scale:
                 bad.append((i, "abs"))
-        elif not _rel(got[f"g{i}"], one[f"g{i}"]) <= 1e-4:
+        elif not _rel(got[f"g{i}"], one[f"g{i}"]) <= (1e-3 if i in PROJ_PARAMS else 1e-4):
             bad.append((i, _rel(got[f"g{i}"], one[f"g{i}"])))
     assert not bad, bad
     # Adam's first step is lr * sign(g) wherever |g| >> eps, so gradient
