@@ -403,9 +403,9 @@ def test_po_recovers_known_translation(cuda, ref):
 def test_po_traces_repeatable(cuda, ref, deterministic):
     """test_engine.cpp:194-213: fixed seeds give bitwise-identical PO traces.
     In deterministic mode every kernel of the iteration is deterministic (the
-    warp / compose input gradients are gathered per target, warp_gather.cu;
-    reductions run in a fixed order), so two runs agree bit for bit — eagerly
-    and as CUDA graphs."""
+    warp / compose input gradients are 64-bit fixed-point scatters, whose
+    integer sums do not depend on the order of the adds; reductions run in a
+    fixed order), so two runs agree bit for bit — eagerly and as CUDA graphs."""
     dims = (16, 16, 16)
     f, m, _, _, _ = ref.synth_pair(dims, seed=14, max_disp=1.0)
     fd, md = torch.from_numpy(f).cuda(), torch.from_numpy(m).cuda()
