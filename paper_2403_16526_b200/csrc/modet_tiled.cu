@@ -51,6 +51,12 @@
 #ifndef MDG_BWD_MINB
 #define MDG_BWD_MINB 2  // resident CTAs of the row / column kernels (d <= 6)
 #endif
+#ifndef MDG_BWD_ROW_MINB
+#define MDG_BWD_ROW_MINB MDG_BWD_MINB
+#endif
+#ifndef MDG_BWD_COL_MINB  // the column kernel fits 3 (79 registers, no spill):
+#define MDG_BWD_COL_MINB 3  // 0.4505 vs 0.4554 ms (profiles/experiments/modet_bwd_split_minb_r02.log)
+#endif
 #ifndef MDG_BWD_MINB8
 #define MDG_BWD_MINB8 1  // the same for d = 8..16
 #endif
@@ -592,7 +598,7 @@ __device__ __forceinline__ void row_stage(float *buf, const Maps &m, uint64_t *b
 }
 
 template <int D, bool TMA, bool ACC>
-__global__ void __launch_bounds__(256, (D <= 6 ? MDG_BWD_MINB : MDG_BWD_MINB8))
+__global__ void __launch_bounds__(256, (D <= 6 ? MDG_BWD_ROW_MINB : MDG_BWD_MINB8))
 modet_bwd_row_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                 const float *__restrict__ K, const float *__restrict__ B,
                 const float *__restrict__ SF, const float *__restrict__ LSE,
@@ -824,7 +830,7 @@ __device__ __forceinline__ void col_stage(float *buf, const Maps &m, uint64_t *b
 }
 
 template <int D, bool TMA, bool ACC>
-__global__ void __launch_bounds__(256, (D <= 6 ? MDG_BWD_MINB : MDG_BWD_MINB8))
+__global__ void __launch_bounds__(256, (D <= 6 ? MDG_BWD_COL_MINB : MDG_BWD_MINB8))
 modet_bwd_col_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                 const float *__restrict__ K, const float *__restrict__ B,
                 const float *__restrict__ SF, const float *__restrict__ LSE,
