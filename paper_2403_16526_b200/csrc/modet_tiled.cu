@@ -438,7 +438,10 @@ __device__ __forceinline__ void fwd_stage(float *buf, const Maps &m, uint64_t *b
 }
 
 template <int D, bool TMA>
-__global__ void __launch_bounds__(256, (D <= 6 ? 3 : 2))
+#ifndef MDG_FWD_MINB
+#define MDG_FWD_MINB 3
+#endif
+__global__ void __launch_bounds__(256, (D <= 6 ? MDG_FWD_MINB : 2))
 modet_fwd_tiled_k(const __grid_constant__ Maps maps, const float *__restrict__ Q,
                   const float *__restrict__ K, const float *__restrict__ B, Vol v, int zc,
                   float *__restrict__ SF, float *__restrict__ LSE,
