@@ -40,7 +40,10 @@ __device__ __forceinline__ void lxyz(int p, const LDims &d, int &x, int &y, int 
 // order, so the sums are bit-identical to the reference); lanes run along x,
 // so every tap load is coalesced.  For the x axis the strip runs along y
 // instead (x stays the lane axis).
-constexpr int kStrip = 4;
+#ifndef MDG_BOX_STRIP
+#define MDG_BOX_STRIP 8  // 4: +30 % box-pass time, 16: register pressure (profiles/experiments/box_strip_r02.log)
+#endif
+constexpr int kStrip = MDG_BOX_STRIP;
 constexpr int kMaxR = 12;
 
 // x pass, one warp per row: the row (zero-padded by R each side) is staged in
